@@ -1,0 +1,323 @@
+/*
+ * vexbayes_cuda.h -- C ABI of libvexbayes_cuda.so
+ *
+ * B200 (sm_100a) implementation of the hot path of the "vexbayes" library
+ * (arXiv 1902.09046): batched, independent prior-predictive simulation inside
+ * likelihood-free samplers.  Every entry point below replaces one reference
+ * interface; the reference location is cited as  file:line  relative to
+ * /root/reference/proj/core/.  The reference-side binding a maintainer adds is
+ * shown in INTEGRATION.md, the C++ shim that keeps the vexbayes:: signatures is
+ * paper_1902_09046_b200/cpp/vexbayes/.
+ *
+ * Conventions
+ *  - plain C types only; return 0 on success, non-zero on failure.  After a
+ *    failure vxb_last_error() returns the thread-local text "code: message"
+ *    where `code` is one of the reference error codes (errors.hpp:11-28):
+ *    invalid-shape, invalid-summary, invalid-range, invalid-scale,
+ *    invalid-argument, invalid-horizon, insufficient-data, empty-set,
+ *    degenerate-ensemble, plus device-error for CUDA failures.
+ *  - the caller owns every buffer it passes in.  A buffer may live in host
+ *    memory (pageable or pinned) or in device memory of the context's GPU; the
+ *    library detects which (unified virtual addressing) and stages host
+ *    buffers through its own device scratch.  Optional outputs may be NULL.
+ *  - `precision` selects the element type of every `void*` real buffer:
+ *    VXB_F64 -> double, VXB_F32 -> float.  `observed` is always double.
+ *  - one vxb_ctx is used by one host thread at a time (the single-owner rule
+ *    of rng.hpp:30-31); it owns one CUDA stream and all device scratch.
+ *  - there is no CPU fallback: without a CUDA device vxb_init fails.
+ */
+#ifndef VEXBAYES_CUDA_H
+#define VEXBAYES_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VXB_ABI_VERSION 1
+
+typedef struct vxb_ctx vxb_ctx;
+
+/* ------------------------------------------------------------------ enums */
+enum { VXB_MODEL_LOGISTIC_SDE = 1, VXB_MODEL_NORMAL_MEAN = 2, VXB_MODEL_MM_TAULEAP = 3,
+       VXB_MODEL_TOGGLE = 4 };
+enum { VXB_F64 = 0, VXB_F32 = 1 };
+/* VXB_RNG_REF      : Philox2x64-10 + Box-Muller through the reference's own
+ *                    polynomials; every variate bit-identical to RngStream
+ *                    (rng.cpp:65-78,112-164, fastmath.hpp:23-128).
+ * VXB_RNG_FAST     : throughput generator (Philox4x32-10, FMA polynomials /
+ *                    MUFU in fp32); statistically validated only.
+ * VXB_RNG_EXTERNAL : standard normals are read from a caller buffer. */
+enum { VXB_RNG_REF = 0, VXB_RNG_FAST = 1, VXB_RNG_EXTERNAL = 2 };
+/* VXB_ARITH_EXACT: separate multiply and add everywhere (the reference builds
+ * with -ffp-contract=off, CMakeLists.txt:15-18) => bit parity.
+ * VXB_ARITH_FMA  : the simulator update may contract to FMA (<=1e-12 rel.). */
+enum { VXB_ARITH_EXACT = 0, VXB_ARITH_FMA = 1 };
+/* VXB_KEY_PARTICLE: particle i owns RngStream(seed, stream_id = i), counter 0
+ *                   => results independent of sharding / GPU count.
+ * VXB_KEY_WORKER  : the reference keying of abc.cpp:43-61: rows are split by
+ *                   partition(n, workers, block_width) (blocked.cpp:34-63),
+ *                   worker w owns RngStream(seed, w) and its rows consume it
+ *                   sequentially => bit-identical to run_prior_predictive for
+ *                   the same (seed, workers, block_width). */
+enum { VXB_KEY_PARTICLE = 0, VXB_KEY_WORKER = 1 };
+
+/* ------------------------------------------------------------ descriptors */
+
+/* POD replacement for the closures of ModelHooks (model.hpp:19-36).
+ *
+ * VXB_MODEL_LOGISTIC_SDE  dX = r X (1 - X/K) dt + sigma X dW, theta=(r,K,sigma)
+ *   dim = 3, steps Euler-Maruyama steps of size dt from x0, the state is
+ *   recorded after every obs_stride-th step: summary_dim = steps / obs_stride.
+ *   prior_lo/hi[0..2] = the uniform prior box (map lo + u*(hi-lo), as
+ *   toggle_switch.cpp:17-22).  consts[0] = sqrt(dt) (computed by the caller
+ *   with the host libm so that host and device agree).
+ * VXB_MODEL_NORMAL_MEAN   y_i ~ N(theta,1), i<steps, theta ~ N(0, lambda^2)
+ *   steps = n (data per dataset).
+ * VXB_MODEL_MM_TAULEAP    S+E->C (k1), C->S+E (k2), C->E+P (k3)
+ *   consts[0..3] = initial (S,E,C,P), consts[4..6] = (k1,k2,k3).
+ */
+typedef struct vxb_model {
+    int32_t model;      /* VXB_MODEL_*            */
+    int32_t precision;  /* VXB_F64 | VXB_F32      */
+    int32_t rng;        /* VXB_RNG_*              */
+    int32_t arith;      /* VXB_ARITH_*            */
+    uint32_t dim;
+    uint32_t summary_dim;
+    uint32_t steps;
+    uint32_t obs_stride;
+    double dt;
+    double x0;
+    double prior_lo[8];
+    double prior_hi[8];
+    double consts[16];
+} vxb_model;
+
+typedef struct vxb_keying {
+    int32_t mode;         /* VXB_KEY_*                                   */
+    uint32_t workers;     /* VXB_KEY_WORKER: P   (abc.cpp:26)            */
+    uint32_t block_width; /* VXB_KEY_WORKER: V   (blocked.cpp:10-12)     */
+    uint32_t reserved;
+    uint64_t seed;
+} vxb_keying;
+
+typedef struct vxb_device_props {
+    int32_t device;
+    int32_t sm_count;
+    int32_t cc_major;
+    int32_t cc_minor;
+    int32_t clock_khz;     /* max SM clock                */
+    int32_t reserved;
+    uint64_t global_mem;   /* bytes                       */
+    char name[128];
+} vxb_device_props;
+
+/* kernel families counted by the built-in event profiler */
+enum { VXB_K_SIMULATE = 0, VXB_K_SELECT = 1, VXB_K_COMPACT = 2, VXB_K_PPP = 3,
+       VXB_K_RESAMPLE = 4, VXB_K_WEIGHTS = 5, VXB_K_PROPOSE = 6, VXB_K_TAULEAP = 7,
+       VXB_K_RNGFILL = 8, VXB_K_MISC = 9, VXB_K_COUNT = 10 };
+typedef struct vxb_profile {
+    uint64_t launches[VXB_K_COUNT];
+    double total_ms[VXB_K_COUNT]; /* only while event timing is enabled */
+} vxb_profile;
+
+/* ---------------------------------------------------- lifecycle / errors */
+int vxb_abi_version(void);
+/* device < 0: use the current CUDA device. */
+int vxb_init(vxb_ctx** ctx, int device);
+void vxb_shutdown(vxb_ctx* ctx);
+const char* vxb_last_error(void);
+int vxb_device_info(vxb_ctx* ctx, vxb_device_props* out);
+/* The context's stream as a cudaStream_t (for event timing by the caller). */
+void* vxb_stream(vxb_ctx* ctx);
+int vxb_synchronize(vxb_ctx* ctx);
+/* Event-time every kernel launch (adds two events per launch). */
+int vxb_profile_enable(vxb_ctx* ctx, int on);
+int vxb_profile_reset(vxb_ctx* ctx);
+int vxb_profile_read(vxb_ctx* ctx, vxb_profile* out); /* synchronises */
+/* Device buffers for callers without a CUDA runtime of their own. */
+int vxb_device_alloc(vxb_ctx* ctx, size_t bytes, void** out);
+int vxb_device_free(vxb_ctx* ctx, void* p);
+int vxb_copy(vxb_ctx* ctx, void* dst, const void* src, size_t bytes); /* any direction */
+
+/* ------------------------------------------------------ substrate (RNG) */
+/* splitmix64 (rng.cpp:22-27) and derive_seed (rng.cpp:29-35); host-side. */
+uint64_t vxb_splitmix64(uint64_t z);
+uint64_t vxb_derive_seed(uint64_t seed, const uint64_t* path, size_t n_path);
+/* Device fill of n raw words / uniforms / Gaussians of RngStream(seed,stream_id)
+ * starting at counter position `pos`; replaces RngStream::next_u64 (rng.cpp:92-97),
+ * fill_uniform (rng.cpp:125-140) and fill_gaussian (rng.cpp:142-164).  Same
+ * argument checks: a <= b (invalid-range); sigma >= 0 (invalid-scale). Unlike
+ * the reference's fill_gaussian, odd n is allowed: position p always yields the
+ * Gaussian of pair p/2 (cos branch even p, sin branch odd p), which is what
+ * next_gaussian (rng.cpp:112-123) defines. */
+int vxb_rng_fill_u64(vxb_ctx* ctx, uint64_t seed, uint32_t stream_id, uint64_t pos, uint64_t n,
+                     uint64_t* out);
+int vxb_rng_fill_uniform(vxb_ctx* ctx, uint64_t seed, uint32_t stream_id, uint64_t pos,
+                         uint64_t n, double a, double b, double* out);
+int vxb_rng_fill_gaussian(vxb_ctx* ctx, uint64_t seed, uint32_t stream_id, uint64_t pos,
+                          uint64_t n, double mu, double sigma, double* out);
+/* Device evaluation of the fastmath functions (fastmath.hpp:23-128), for
+ * parity tests: fn 0 log2_pos, 1 ln_pos, 2 exp2_clamped, 3 sinpi, 4 cospi,
+ * 5 pow_pos (x = base, y = exponent; y ignored otherwise). */
+int vxb_fastmath_eval(vxb_ctx* ctx, int fn, const double* x, const double* y, uint64_t n,
+                      double* out);
+/* partition (blocked.cpp:34-63): writes workers pairs [begin,end). Host-side. */
+int vxb_partition(uint64_t total, uint64_t workers, uint64_t block_width, uint64_t* ranges);
+
+/* ------------------------------------------------- ABC rejection (C0/C1) */
+/* Drop-in for abc::run_prior_predictive (abc.cpp:26-73) on rows
+ * [first, first+count) of an n_total-row job.  Outputs are row-major
+ * count x dim, count x summary_dim, count, count; any may be NULL.  A row
+ * whose state becomes non-finite is `failed` (summary zeroed, rho NaN),
+ * mirroring abc.cpp:54-60.  external_noise (VXB_RNG_EXTERNAL): count x steps
+ * standard normals, row-major, element type = precision. */
+int vxb_abc_prior_predictive(vxb_ctx* ctx, const vxb_model* model, const vxb_keying* key,
+                             uint64_t n_total, uint64_t first, uint64_t count,
+                             const double* observed, void* params, void* summaries, void* rho,
+                             uint8_t* failed, const void* external_noise);
+
+/* Drop-in for abc::select_epsilon (abc.cpp:75-97) over n discrepancies:
+ * epsilon = type-7 q-quantile of the non-failed rho raised to the ceil(q n)-th
+ * order statistic, accepted = ascending rows with rho <= epsilon.  At most
+ * `cap` indices are written; *n_accepted is the full count.  idx may be NULL. */
+int vxb_select_epsilon(vxb_ctx* ctx, int precision, const void* rho, const uint8_t* failed,
+                       uint64_t n, double accept_fraction, double* epsilon, uint64_t cap,
+                       uint64_t* n_accepted, uint64_t* idx);
+
+/* k-th order statistics (0-based ranks, ascending, NaN/failed rows excluded)
+ * of rho; *n_valid receives the number of non-failed rows. */
+int vxb_order_statistics(vxb_ctx* ctx, int precision, const void* rho, const uint8_t* failed,
+                         uint64_t n, const uint64_t* ranks, uint32_t n_ranks, double* values,
+                         uint64_t* n_valid);
+
+/* Ascending compaction of rows with !failed && rho <= epsilon; idx values are
+ * row + index_base. */
+int vxb_compact_accepted(vxb_ctx* ctx, int precision, const void* rho, const uint8_t* failed,
+                         uint64_t n, double epsilon, uint64_t index_base, uint64_t cap,
+                         uint64_t* n_accepted, uint64_t* idx);
+
+/* Fused fixed-epsilon rejection (config 1): simulate rows [first,first+count),
+ * keep only rows with rho <= epsilon, ascending.  idx holds global row numbers.
+ * params: cap x dim, rho: cap.  Trajectories, summaries and rejected rows never
+ * leave the GPU. */
+int vxb_abc_reject(vxb_ctx* ctx, const vxb_model* model, const vxb_keying* key,
+                   uint64_t n_total, uint64_t first, uint64_t count, const double* observed,
+                   double epsilon, uint64_t cap, uint64_t* n_accepted, uint64_t* idx,
+                   void* params, void* rho);
+
+/* Simulate the model once at theta from RngStream(seed, stream_id) at counter
+ * position pos (aligned up to even), the way bench.cpp:69-77 builds observed
+ * summaries.  summary: summary_dim reals. */
+int vxb_simulate_at(vxb_ctx* ctx, const vxb_model* model, const double* theta, uint64_t seed,
+                    uint32_t stream_id, uint64_t pos, void* summary);
+
+/* ------------------------------------- prior-predictive p-values (C2) */
+/* For every lambda_k: datasets j in [first, first+count) of m_total, dataset
+ * (k,j) drawn from RngStream(derive_seed(seed,{k}), j) in the order of
+ * weak_info.cpp:82-106 (align_even; Gaussian prior draw; then the data);
+ * counts[k] = #{ j : logm(ybar_kj) <= logm(ybar_obs) } -- the counting rule of
+ * estimate_pvalues (weak_info.cpp:108-120, ties count); pvalues[k] =
+ * counts[k]/m_total (only meaningful when the shard is the whole job).
+ * log_norm[k] = -0.5*log(2 pi v_k), v_k = lambda_k^2 + 1/n, is supplied by the
+ * caller (host libm).  ybar_out (optional): n_lambda x count sample means. */
+int vxb_ppp_pvalues(vxb_ctx* ctx, const vxb_model* model, const double* lambda,
+                    const double* log_norm, uint32_t n_lambda, uint64_t m_total, uint64_t first,
+                    uint64_t count, uint64_t seed, double ybar_obs, uint64_t* counts,
+                    double* pvalues, double* ybar_out);
+
+/* ------------------------------------------- SMC building blocks (C3) */
+/* smc::ess (smc.cpp:208-219) and logsumexp (numeric.cpp:11-18). */
+int vxb_ess(vxb_ctx* ctx, const double* log_w, uint64_t n, double* ess);
+int vxb_logsumexp(vxb_ctx* ctx, const double* x, uint64_t n, double* out);
+/* smc::resample_multinomial (smc.cpp:268-300): draw i uses position i of
+ * RngStream(seed, stream_id); ancestors[i] = upper_bound(cum, u_i * cum[n-1]),
+ * clamped; particles_out row i = particles_in row ancestors[i]. */
+int vxb_resample_multinomial(vxb_ctx* ctx, uint64_t n, uint32_t dim, const double* log_w,
+                             const double* particles_in, uint64_t seed, uint32_t stream_id,
+                             double* particles_out, uint64_t* ancestors);
+
+typedef struct vxb_abcsmc_cfg {
+    uint64_t particles;    /* N                                            */
+    uint32_t generations;  /* G (generation 0 = prior)                     */
+    uint32_t reserved;
+    double quantile;       /* epsilon_g = this quantile of generation g-1  */
+    double kernel_scale;   /* covariance multiplier (2.0)                  */
+    double jitter;         /* make_kernel jitter (smc.cpp:311-325), 1e-10  */
+    uint64_t round_size;   /* proposals per round; 0 => N                  */
+    uint64_t max_rounds;   /* safety cap per generation; 0 => 1000         */
+    uint64_t seed;
+} vxb_abcsmc_cfg;
+
+/* One generation's population and diagnostics.  All arrays caller-owned:
+ * theta N x dim, weight N (normalised, linear), rho N; per generation
+ * (G entries): epsilon, ess, acceptance rate, proposals used, weighted mean
+ * (G x dim) and covariance (G x dim x dim) of the population. */
+typedef struct vxb_abcsmc_out {
+    double* theta;
+    double* weight;
+    double* rho;
+    double* epsilon;
+    double* ess;
+    double* accept_rate;
+    uint64_t* proposals;
+    double* mean;
+    double* cov;
+} vxb_abcsmc_out;
+
+int vxb_abcsmc_run(vxb_ctx* ctx, const vxb_model* model, const vxb_abcsmc_cfg* cfg,
+                   const double* observed, vxb_abcsmc_out* out);
+
+/* The two device stages of a generation, exposed so that a multi-GPU host can
+ * shard them (proposals / new particles by global index) and run the
+ * collectives itself:
+ * propose: for proposals p in [first, first+count) of generation `gen`:
+ *   ancestor by inverse CDF over cum (n_prev inclusive cumulative weights),
+ *   theta* = theta_a + L z, reject outside the prior box, else simulate and
+ *   compare with epsilon.  Outputs per proposal: theta* (count x dim), rho,
+ *   flag (1 accepted, 0 rejected by distance, 2 outside the prior, 3 failed).
+ * weights: for `count` new particles (theta_new: count x dim): the unnormalised
+ *   importance weight 1 / sum_j w_j phi(theta_i; theta_j, Sigma), summed over
+ *   j in index order. */
+int vxb_abcsmc_propose(vxb_ctx* ctx, const vxb_model* model, uint64_t seed, uint32_t gen,
+                       uint64_t first, uint64_t count, uint64_t n_prev, const double* theta_prev,
+                       const double* cum_prev, const double* chol, const double* observed,
+                       double epsilon, double* theta_out, double* rho_out, uint8_t* flag_out);
+int vxb_abcsmc_weights(vxb_ctx* ctx, uint32_t dim, uint64_t count, const double* theta_new,
+                       uint64_t n_prev, const double* theta_prev,
+                       const double* w_prev, const double* chol, double* w_out);
+
+/* ------------------------------------------------ tau-leap MLMC (C4) */
+typedef struct vxb_mlmc_cfg {
+    uint32_t levels;       /* L+1 levels, l = 0..L              */
+    uint32_t refine;       /* M: tau_l = tau0 * M^-l  (4)       */
+    double tau0;
+    double t_end;
+    uint64_t paths;        /* per level                         */
+    uint64_t seed;
+} vxb_mlmc_cfg;
+
+/* Raw sums of level `level` over paths [first, first+count):
+ * sums[0] = sum Y, sums[1] = sum Y^2 (exact integers), sums[2] = sum of the
+ * fine path's P(T), sums[3] = Poisson inversion iterations (cost diagnostic).
+ * Y = P_fine(T) - P_coarse(T) for level >= 1, P(T) for level 0.
+ * y_out (optional): count int32 values of Y. */
+int vxb_mlmc_level(vxb_ctx* ctx, const vxb_model* model, const vxb_mlmc_cfg* cfg, uint32_t level,
+                   uint64_t first, uint64_t count, int64_t* sums, int32_t* y_out);
+
+typedef struct vxb_mlmc_out {
+    double* level_mean;   /* levels                         */
+    double* level_var;    /* levels (n-1 divisor)           */
+    double* level_cost;   /* levels: fine+coarse steps/path */
+    double estimate;
+    double std_error;
+} vxb_mlmc_out;
+int vxb_mlmc_tauleap(vxb_ctx* ctx, const vxb_model* model, const vxb_mlmc_cfg* cfg,
+                     vxb_mlmc_out* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VEXBAYES_CUDA_H */

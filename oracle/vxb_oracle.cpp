@@ -1,0 +1,1220 @@
+// oracle/vxb_oracle.cpp -- TEST INFRASTRUCTURE (the parity oracle), not product.
+//
+// A self-contained CPU restatement of the hot path of the vexbayes reference,
+// written against the reference's published algorithm; every function cites the
+// reference location it follows (paths relative to /root/reference/proj/core/).
+// It has NO dependency on /root/reference, so it travels to the GPU box.
+// Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+// arm may load it.  Build: oracle/Makefile (g++ -O2 -ffp-contract=off, the
+// reference's flags, proj/CMakeLists.txt:15-18 -- per-operation IEEE rounding,
+// no FMA contraction).
+//
+// Pinning (tests/test_oracle_pins.py): the RNG, fastmath, numeric, partition,
+// ABC sampler, epsilon selection, resampling, ESS and p-value counting are
+// checked bit-for-bit against oracle/_ref (the unmodified reference compiled
+// from /root/reference) where that library is present, and everywhere against
+// the golden vectors it generated (tests/golden/, script tests/golden/make_golden.py).
+// Workloads the reference does not contain -- ABC-SMC generation loop, weighted
+// covariance, Poisson variates, tau-leap and its MLMC coupling -- are
+// "parity unpinned": they are defined HERE and anchored by
+// analytic checks only.
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../include/vexbayes_cuda.h"  // vxb_model / vxb_keying / cfg structs only
+
+namespace {
+
+thread_local std::string g_err;
+
+struct OracleError {
+    std::string text;
+};
+[[noreturn]] void raise(const char* code, const char* msg) {
+    throw OracleError{std::string(code) + ": " + msg};  // errors.hpp:11-28 "code: message"
+}
+void require(bool ok, const char* code, const char* msg) {
+    if (!ok) raise(code, msg);
+}
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const OracleError& e) {
+        g_err = e.text;
+        return 1;
+    }
+}
+
+template <class To, class From>
+To bit_cast(const From& v) {
+    To out;
+    static_assert(sizeof(To) == sizeof(From));
+    std::memcpy(&out, &v, sizeof(To));
+    return out;
+}
+
+template <class F>
+void parallel_for(std::uint64_t n, unsigned threads, F&& body) {
+    if (threads <= 1 || n < 2) {
+        for (std::uint64_t i = 0; i < n; ++i) body(i);
+        return;
+    }
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < threads; ++t)
+        pool.emplace_back([&, t] {
+            for (std::uint64_t i = t; i < n; i += threads) body(i);
+        });
+    for (auto& th : pool) th.join();
+}
+
+// ===================================================================== RNG
+// splitmix64: rng.cpp:22-27
+std::uint64_t splitmix64(std::uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+// derive_seed: rng.cpp:29-35
+std::uint64_t derive_seed(std::uint64_t seed, const std::uint64_t* path, std::size_t n) {
+    std::uint64_t h = splitmix64(seed);
+    for (std::size_t i = 0; i < n; ++i) h = splitmix64(h ^ path[i]);
+    return h;
+}
+std::uint64_t derive_seed1(std::uint64_t seed, std::uint64_t a) { return derive_seed(seed, &a, 1); }
+
+// key derivation: rng.cpp:37-40.  stream_id is 32-bit in the reference; the
+// oracle takes 64 bits (identical for ids < 2^32).
+std::uint64_t stream_key(std::uint64_t seed, std::uint64_t stream_id) {
+    return splitmix64(splitmix64(seed) ^ stream_id);
+}
+
+struct Block {
+    std::uint64_t w0, w1;
+};
+// Philox2x64-10 on the 128-bit pair index: rng.cpp:12-14 (constants), 65-78.
+Block philox_block(std::uint64_t key, std::uint64_t idx_lo, std::uint64_t idx_hi) {
+    std::uint64_t c0 = idx_lo, c1 = idx_hi, k = key;
+    for (int round = 0; round < 10; ++round) {
+        const unsigned __int128 prod = static_cast<unsigned __int128>(0xD2B74407B1CE6E93ULL) * c0;
+        const std::uint64_t hi = static_cast<std::uint64_t>(prod >> 64);
+        const std::uint64_t lo = static_cast<std::uint64_t>(prod);
+        c0 = hi ^ k ^ c1;
+        c1 = lo;
+        k += 0x9E3779B97F4A7C15ULL;
+    }
+    return {c0, c1};
+}
+// to_unit: rng.cpp:16-18
+double to_unit(std::uint64_t x) { return static_cast<double>(x >> 11) * 0x1.0p-53; }
+
+// ================================================================ fastmath
+// log2_pos: fastmath.hpp:23-51
+double log2_pos(double x) {
+    std::uint64_t bits = bit_cast<std::uint64_t>(x);
+    std::int64_t e = static_cast<std::int64_t>((bits >> 52) & 0x7FF);
+    if (e == 0) {
+        bits = bit_cast<std::uint64_t>(x * 0x1p64);
+        e = static_cast<std::int64_t>((bits >> 52) & 0x7FF) - 64;
+    }
+    e -= 1023;
+    double m = bit_cast<double>((bits & 0xFFFFFFFFFFFFFULL) | 0x3FF0000000000000ULL);
+    const bool upper = m > 1.4142135623730951;
+    m = upper ? 0.5 * m : m;
+    const double ed = static_cast<double>(e + (upper ? 1 : 0));
+    const double t = (m - 1.0) / (m + 1.0);
+    const double s = t * t;
+    double p = 1.0 / 21.0;
+    p = p * s + 1.0 / 19.0;
+    p = p * s + 1.0 / 17.0;
+    p = p * s + 1.0 / 15.0;
+    p = p * s + 1.0 / 13.0;
+    p = p * s + 1.0 / 11.0;
+    p = p * s + 1.0 / 9.0;
+    p = p * s + 1.0 / 7.0;
+    p = p * s + 1.0 / 5.0;
+    p = p * s + 1.0 / 3.0;
+    p = p * s + 1.0;
+    return ed + (2.0 * 0x1.71547652b82fep+0) * t * p;
+}
+constexpr double kLn2 = 0x1.62e42fefa39efp-1;     // fastmath.hpp:19
+constexpr double kInvLn2 = 0x1.71547652b82fep+0;  // fastmath.hpp:20
+// ln_pos: fastmath.hpp:54
+double ln_pos(double x) { return log2_pos(x) * kLn2; }
+// exp2_clamped: fastmath.hpp:57-79
+double exp2_clamped(double z) {
+    z = z < -1022.0 ? -1022.0 : z;
+    z = z > 1023.0 ? 1023.0 : z;
+    const double rn = (z + 0x1.8p52) - 0x1.8p52;
+    const double w = (z - rn) * kLn2;
+    double p = 1.0 / 6227020800.0;
+    p = p * w + 1.0 / 479001600.0;
+    p = p * w + 1.0 / 39916800.0;
+    p = p * w + 1.0 / 3628800.0;
+    p = p * w + 1.0 / 362880.0;
+    p = p * w + 1.0 / 40320.0;
+    p = p * w + 1.0 / 5040.0;
+    p = p * w + 1.0 / 720.0;
+    p = p * w + 1.0 / 120.0;
+    p = p * w + 1.0 / 24.0;
+    p = p * w + 1.0 / 6.0;
+    p = p * w + 0.5;
+    p = p * w + 1.0;
+    p = p * w + 1.0;
+    const std::int64_t n = static_cast<std::int64_t>(rn);
+    const double scale = bit_cast<double>(static_cast<std::uint64_t>(n + 1023) << 52);
+    return p * scale;
+}
+// pow_pos: fastmath.hpp:82
+double pow_pos(double x, double y) { return exp2_clamped(y * log2_pos(x)); }
+// sinpi: fastmath.hpp:85-105
+double sinpi(double a) {
+    const double rn = (a + 0x1.8p52) - 0x1.8p52;
+    const double r = a - rn;
+    const double s = r * 3.141592653589793238462643383279502884;
+    const double s2 = s * s;
+    double p = 1.0 / 51090942171709440000.0;
+    p = p * s2 - 1.0 / 121645100408832000.0;
+    p = p * s2 + 1.0 / 355687428096000.0;
+    p = p * s2 - 1.0 / 1307674368000.0;
+    p = p * s2 + 1.0 / 6227020800.0;
+    p = p * s2 - 1.0 / 39916800.0;
+    p = p * s2 + 1.0 / 362880.0;
+    p = p * s2 - 1.0 / 5040.0;
+    p = p * s2 + 1.0 / 120.0;
+    p = p * s2 - 1.0 / 6.0;
+    p = p * s2 + 1.0;
+    const double base = s * p;
+    const std::int64_t n = static_cast<std::int64_t>(rn);
+    return ((n & 1) ? -1.0 : 1.0) * base;
+}
+// cospi: fastmath.hpp:108-128
+double cospi(double a) {
+    const double rn = (a + 0x1.8p52) - 0x1.8p52;
+    const double r = a - rn;
+    const double s = r * 3.141592653589793238462643383279502884;
+    const double s2 = s * s;
+    double p = -1.0 / 1124000727777607680000.0;
+    p = p * s2 + 1.0 / 2432902008176640000.0;
+    p = p * s2 - 1.0 / 6402373705728000.0;
+    p = p * s2 + 1.0 / 20922789888000.0;
+    p = p * s2 - 1.0 / 87178291200.0;
+    p = p * s2 + 1.0 / 479001600.0;
+    p = p * s2 - 1.0 / 3628800.0;
+    p = p * s2 + 1.0 / 40320.0;
+    p = p * s2 - 1.0 / 720.0;
+    p = p * s2 + 1.0 / 24.0;
+    p = p * s2 - 1.0 / 2.0;
+    p = p * s2 + 1.0;
+    const std::int64_t n = static_cast<std::int64_t>(rn);
+    return ((n & 1) ? -1.0 : 1.0) * p;
+}
+
+// Random-access view of RngStream(seed, stream_id): every output is a pure
+// function of the counter position (rng.hpp:18-28).  64-bit positions.
+struct Stream {
+    std::uint64_t key;
+    std::uint64_t pos = 0;
+    std::uint64_t cache_idx = ~0ULL;
+    Block cache{0, 0};
+    Stream(std::uint64_t seed, std::uint64_t id) : key(stream_key(seed, id)) {}
+    const Block& block_of(std::uint64_t p) {  // current_pair_block: rng.cpp:80-90
+        const std::uint64_t idx = p >> 1;
+        if (idx != cache_idx) {
+            cache = philox_block(key, idx, 0);
+            cache_idx = idx;
+        }
+        return cache;
+    }
+    void align_even() { pos += pos & 1; }  // rng.cpp:57-59
+    std::uint64_t next_u64() {             // rng.cpp:92-97
+        const Block& b = block_of(pos);
+        const std::uint64_t w = (pos & 1) ? b.w1 : b.w0;
+        ++pos;
+        return w;
+    }
+    double next_unit() { return to_unit(next_u64()); }  // rng.cpp:99
+    // next_uniform / fill_uniform: rng.cpp:101-110, 125-140
+    double next_uniform(double a, double b) {
+        require(a <= b, "invalid-range", "uniform lower bound exceeds upper bound");
+        if (a == b) {
+            next_u64();
+            return a;
+        }
+        const double top = std::nextafter(b, a);
+        const double r = a + next_unit() * (b - a);
+        return r < a ? a : (r > top ? top : r);
+    }
+    // next_gaussian: rng.cpp:112-123 (pair m = pos/2, cos branch at even pos)
+    double next_gaussian(double mu, double sigma) {
+        require(sigma >= 0.0, "invalid-scale", "gaussian sigma must be nonnegative");
+        const bool odd = (pos & 1) != 0;
+        const Block& b = block_of(pos);
+        const double u1 = to_unit(b.w0);
+        const double u2 = to_unit(b.w1);
+        const double r = std::sqrt(-2.0 * ln_pos(1.0 - u1));
+        const double ang = 2.0 * u2;
+        const double z = odd ? r * sinpi(ang) : r * cospi(ang);
+        ++pos;
+        return mu + sigma * z;
+    }
+};
+
+// ================================================================= numeric
+// quantile_sorted: numeric.cpp:20-30 (type-7)
+double quantile_sorted(const double* sorted, std::size_t n, double level) {
+    require(n > 0, "insufficient-data", "quantile of an empty sample");
+    require(level >= 0.0 && level <= 1.0, "invalid-argument", "quantile level outside [0,1]");
+    if (n == 1) return sorted[0];
+    const double h = static_cast<double>(n - 1) * level;
+    const std::size_t lo = static_cast<std::size_t>(h);
+    if (lo + 1 >= n) return sorted[n - 1];
+    const double frac = h - static_cast<double>(lo);
+    return sorted[lo] + frac * (sorted[lo + 1] - sorted[lo]);
+}
+// quantile: numeric.cpp:32-36
+double quantile(const double* sample, std::size_t n, double level) {
+    std::vector<double> copy(sample, sample + n);
+    std::sort(copy.begin(), copy.end());
+    return quantile_sorted(copy.data(), n, level);
+}
+// logsumexp: numeric.cpp:11-18
+double logsumexp(const double* x, std::size_t n) {
+    double m = -std::numeric_limits<double>::infinity();
+    for (std::size_t i = 0; i < n; ++i) m = std::max(m, x[i]);
+    if (!std::isfinite(m)) return m;
+    double s = 0.0;
+    for (std::size_t i = 0; i < n; ++i) s += std::exp(x[i] - m);
+    return m + std::log(s);
+}
+// sample_covariance: numeric.cpp:55-79
+void sample_covariance(const double* data, std::size_t rows, std::size_t dim, double* cov) {
+    require(rows >= 2, "insufficient-data", "covariance needs at least two rows");
+    std::vector<double> mu(dim, 0.0);
+    for (std::size_t r = 0; r < rows; ++r)
+        for (std::size_t k = 0; k < dim; ++k) mu[k] += data[r * dim + k];
+    for (double& v : mu) v /= static_cast<double>(rows);
+    std::fill(cov, cov + dim * dim, 0.0);
+    for (std::size_t r = 0; r < rows; ++r)
+        for (std::size_t i = 0; i < dim; ++i) {
+            const double di = data[r * dim + i] - mu[i];
+            for (std::size_t j = 0; j <= i; ++j) cov[i * dim + j] += di * (data[r * dim + j] - mu[j]);
+        }
+    const double norm = 1.0 / static_cast<double>(rows - 1);
+    for (std::size_t i = 0; i < dim; ++i)
+        for (std::size_t j = 0; j <= i; ++j) {
+            cov[i * dim + j] *= norm;
+            cov[j * dim + i] = cov[i * dim + j];
+        }
+}
+// cholesky: numeric.cpp:81-96
+bool cholesky(double* a, std::size_t dim) {
+    for (std::size_t j = 0; j < dim; ++j) {
+        double d = a[j * dim + j];
+        for (std::size_t k = 0; k < j; ++k) d -= a[j * dim + k] * a[j * dim + k];
+        if (!(d > 0.0)) return false;
+        const double ljj = std::sqrt(d);
+        a[j * dim + j] = ljj;
+        for (std::size_t i = j + 1; i < dim; ++i) {
+            double s = a[i * dim + j];
+            for (std::size_t k = 0; k < j; ++k) s -= a[i * dim + k] * a[j * dim + k];
+            a[i * dim + j] = s / ljj;
+        }
+        for (std::size_t i = 0; i < j; ++i) a[i * dim + j] = 0.0;
+    }
+    return true;
+}
+// partition: blocked.cpp:34-63
+void partition(std::uint64_t total, std::uint64_t workers, std::uint64_t width,
+               std::uint64_t* ranges) {
+    require(total >= 1, "invalid-shape", "partition needs at least one item");
+    require(workers >= 1, "invalid-shape", "partition needs at least one worker");
+    require(width >= 1, "invalid-shape", "partition needs a positive block width");
+    const std::uint64_t blocks = (total + width - 1) / width;
+    const std::uint64_t base = blocks / workers, extra = blocks % workers;
+    std::uint64_t begin_block = 0;
+    for (std::uint64_t w = 0; w < workers; ++w) {
+        const std::uint64_t nb = base + (w < extra ? 1 : 0);
+        const std::uint64_t begin = begin_block * width;
+        std::uint64_t end = (begin_block + nb) * width;
+        if (end > total) end = total;
+        if (begin > total) {
+            ranges[2 * w] = total;
+            ranges[2 * w + 1] = total;
+        } else {
+            ranges[2 * w] = begin;
+            ranges[2 * w + 1] = end;
+        }
+        begin_block += nb;
+    }
+}
+bool supported_width(std::uint64_t v) {  // blocked.cpp:10-12
+    return v == 1 || v == 2 || v == 4 || v == 8 || v == 16;
+}
+
+// Canonical two-level summation used by every reduction the reference leaves
+// to a serial coordinator loop and that the GPU must reproduce bit-for-bit
+// independent of its launch shape: elements are summed left-to-right inside
+// consecutive chunks of kChunk, then the chunk totals left-to-right.
+constexpr std::size_t kChunk = 256;
+template <class Get>
+double canon_sum(std::size_t n, Get&& get) {
+    double total = 0.0;
+    for (std::size_t c0 = 0; c0 < n; c0 += kChunk) {
+        const std::size_t c1 = std::min(n, c0 + kChunk);
+        double part = 0.0;
+        for (std::size_t i = c0; i < c1; ++i) part += get(i);
+        total += part;
+    }
+    return total;
+}
+// Canonical two-level inclusive scan: cum[i] = offset(chunk) + local prefix.
+void canon_cumsum(const double* w, std::size_t n, double* cum) {
+    double offset = 0.0;
+    for (std::size_t c0 = 0; c0 < n; c0 += kChunk) {
+        const std::size_t c1 = std::min(n, c0 + kChunk);
+        double run = 0.0;
+        for (std::size_t i = c0; i < c1; ++i) {
+            run += w[i];
+            cum[i] = offset + run;
+        }
+        offset = offset + run;
+    }
+}
+std::size_t upper_bound_idx(const double* cum, std::size_t n, double target) {
+    // std::upper_bound of smc.cpp:287, clamped as smc.cpp:289
+    std::size_t lo = 0, hi = n;
+    while (lo < hi) {
+        const std::size_t mid = lo + (hi - lo) / 2;
+        if (target < cum[mid]) hi = mid; else lo = mid + 1;
+    }
+    return lo >= n ? n - 1 : lo;
+}
+
+// ======================================================= logistic SDE model
+// Model in the mould of toggle_switch.cpp: prior box map (:17-22), Euler-
+// Maruyama with explicit operation order (:46-62), variates addressed by a
+// canonical layout in counter space (toggle_switch.hpp:52-57): relative to the
+// row's base position, positions 0..dim-1 are the prior uniforms, the counter
+// is aligned to even (abc.cpp:53), then position dim_e + j is the standard
+// normal of step j+1.
+struct Logistic {
+    std::uint32_t steps, stride, n_obs;
+    double dt, sqdt, x0;
+    double lo[3], hi[3];
+    explicit Logistic(const vxb_model& m)
+        : steps(m.steps), stride(m.obs_stride), n_obs(m.obs_stride ? m.steps / m.obs_stride : 0),
+          dt(m.dt), sqdt(m.consts[0]), x0(m.x0) {
+        require(m.model == VXB_MODEL_LOGISTIC_SDE, "invalid-argument", "not a logistic model");
+        require(m.dim == 3, "invalid-shape", "logistic model has three parameters");
+        require(m.steps >= 1 && m.obs_stride >= 1, "invalid-horizon", "need at least one step");
+        require(m.summary_dim == n_obs && n_obs >= 1, "invalid-summary",
+                "summary_dim must equal steps / obs_stride");
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = m.prior_lo[k];
+            hi[k] = m.prior_hi[k];
+            require(lo[k] <= hi[k], "invalid-range", "uniform lower bound exceeds upper bound");
+        }
+    }
+    std::uint64_t row_stride() const {  // positions one row consumes in a worker stream
+        return 4 + steps + (steps & 1);
+    }
+    void sample_prior(Stream& s, double* theta) const {
+        double unit[3];
+        for (int k = 0; k < 3; ++k) unit[k] = s.next_uniform(0.0, 1.0);
+        for (int k = 0; k < 3; ++k) theta[k] = lo[k] + unit[k] * (hi[k] - lo[k]);
+    }
+    // returns false when the state left the reals (the reference would throw
+    // and abc.cpp:57-60 flags the row)
+    template <class Real, class Noise>
+    bool simulate(const double* theta, Noise&& noise, double* summary) const {
+        const Real r = static_cast<Real>(theta[0]);
+        const Real k = static_cast<Real>(theta[1]);
+        const Real sigma = static_cast<Real>(theta[2]);
+        const Real a = r * static_cast<Real>(dt);
+        const Real c = sigma * static_cast<Real>(sqdt);
+        const Real inv_k = Real(1) / k;
+        Real x = static_cast<Real>(x0);
+        std::uint32_t next = 0, since = 0;
+        for (std::uint32_t j = 0; j < steps; ++j) {
+            const Real z = static_cast<Real>(noise(j));
+            const Real drift = (a * x) * (Real(1) - x * inv_k);
+            const Real diff = (c * x) * z;
+            x = (x + drift) + diff;
+            if (++since == stride) {
+                since = 0;
+                if (next < n_obs) summary[next++] = static_cast<double>(x);
+            }
+        }
+        for (std::uint32_t i = 0; i < n_obs; ++i)
+            if (!std::isfinite(summary[i])) return false;
+        return true;
+    }
+};
+
+// discrepancy: abc.cpp:16-24 (left-to-right accumulation), in Real
+template <class Real>
+double discrepancy(const double* sim, const double* obs, std::size_t n) {
+    Real ss = 0;
+    for (std::size_t i = 0; i < n; ++i) {
+        const Real d = static_cast<Real>(sim[i]) - static_cast<Real>(obs[i]);
+        ss += d * d;
+    }
+    return static_cast<double>(std::sqrt(ss));
+}
+
+template <class Real>
+void abc_row(const Logistic& lg, Stream& s, const double* observed, const double* ext_noise,
+             double* theta, double* summary, double* rho, std::uint8_t* failed) {
+    lg.sample_prior(s, theta);
+    if (sizeof(Real) == 4)
+        for (int k = 0; k < 3; ++k) theta[k] = static_cast<double>(static_cast<float>(theta[k]));
+    s.align_even();  // abc.cpp:53
+    bool ok;
+    if (ext_noise) {
+        ok = lg.simulate<Real>(theta, [&](std::uint32_t j) { return ext_noise[j]; }, summary);
+        s.pos += lg.steps + (lg.steps & 1);
+    } else {
+        ok = lg.simulate<Real>(theta, [&](std::uint32_t) { return s.next_gaussian(0.0, 1.0); },
+                               summary);
+        s.pos += lg.steps & 1;  // fill_gaussian consumes an even count
+    }
+    if (ok) {
+        *rho = discrepancy<Real>(summary, observed, lg.n_obs);
+        *failed = 0;
+    } else {  // abc.cpp:57-60
+        *rho = std::numeric_limits<double>::quiet_NaN();
+        *failed = 1;
+        std::fill(summary, summary + lg.n_obs, 0.0);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vxo_last_error() { return g_err.c_str(); }
+
+// --------------------------------------------------------------- substrate
+std::uint64_t vxo_splitmix64(std::uint64_t z) { return splitmix64(z); }
+std::uint64_t vxo_derive_seed(std::uint64_t seed, const std::uint64_t* path, std::size_t n) {
+    return derive_seed(seed, path, n);
+}
+int vxo_stream_u64(std::uint64_t seed, std::uint64_t id, std::uint64_t pos, std::uint64_t n,
+                   std::uint64_t* out) {
+    return guarded([&] {
+        Stream s(seed, id);
+        s.pos = pos;
+        for (std::uint64_t i = 0; i < n; ++i) out[i] = s.next_u64();
+    });
+}
+int vxo_fill_uniform(std::uint64_t seed, std::uint64_t id, std::uint64_t pos, std::uint64_t n,
+                     double a, double b, double* out) {
+    return guarded([&] {
+        require(a <= b, "invalid-range", "uniform lower bound exceeds upper bound");
+        Stream s(seed, id);
+        s.pos = pos;
+        for (std::uint64_t i = 0; i < n; ++i) out[i] = s.next_uniform(a, b);
+    });
+}
+int vxo_fill_gaussian(std::uint64_t seed, std::uint64_t id, std::uint64_t pos, std::uint64_t n,
+                      double mu, double sigma, double* out) {
+    return guarded([&] {
+        require(sigma >= 0.0, "invalid-scale", "gaussian sigma must be nonnegative");
+        Stream s(seed, id);
+        s.pos = pos;
+        for (std::uint64_t i = 0; i < n; ++i) out[i] = s.next_gaussian(mu, sigma);
+    });
+}
+int vxo_fastmath(int fn, const double* x, const double* y, std::uint64_t n, double* out) {
+    return guarded([&] {
+        for (std::uint64_t i = 0; i < n; ++i) switch (fn) {
+                case 0: out[i] = log2_pos(x[i]); break;
+                case 1: out[i] = ln_pos(x[i]); break;
+                case 2: out[i] = exp2_clamped(x[i]); break;
+                case 3: out[i] = sinpi(x[i]); break;
+                case 4: out[i] = cospi(x[i]); break;
+                case 5: out[i] = pow_pos(x[i], y[i]); break;
+                default: raise("invalid-argument", "unknown fastmath function");
+            }
+    });
+}
+int vxo_quantile(const double* sample, std::uint64_t n, double level, double* out) {
+    return guarded([&] { *out = quantile(sample, n, level); });
+}
+int vxo_logsumexp(const double* x, std::uint64_t n, double* out) {
+    return guarded([&] { *out = logsumexp(x, n); });
+}
+int vxo_sample_covariance(const double* data, std::uint64_t rows, std::uint64_t dim, double* cov) {
+    return guarded([&] { sample_covariance(data, rows, dim, cov); });
+}
+int vxo_cholesky(double* a, std::uint64_t dim) { return cholesky(a, dim) ? 0 : 1; }
+int vxo_partition(std::uint64_t total, std::uint64_t workers, std::uint64_t width,
+                  std::uint64_t* ranges) {
+    return guarded([&] { partition(total, workers, width, ranges); });
+}
+double vxo_discrepancy(const double* sim, const double* obs, std::uint64_t n) {
+    return discrepancy<double>(sim, obs, n);
+}
+
+// --------------------------------------------------------------- ABC (C0/C1)
+// run_prior_predictive: abc.cpp:26-73, rows [first, first+count) of n_total.
+// key->mode VXB_KEY_WORKER reproduces the reference keying; VXB_KEY_PARTICLE
+// gives row i the stream (seed, i).  external_noise: count x steps doubles.
+int vxo_abc_prior_predictive(const vxb_model* m, const vxb_keying* key, std::uint64_t n_total,
+                             std::uint64_t first, std::uint64_t count, const double* observed,
+                             double* params, double* summaries, double* rho, std::uint8_t* failed,
+                             const double* external_noise, unsigned threads) {
+    return guarded([&] {
+        require(n_total >= 1, "invalid-shape", "need at least one prior predictive sample");
+        require(first + count <= n_total, "invalid-shape", "row range exceeds the job");
+        const Logistic lg(*m);
+        const std::size_t sd = lg.n_obs;
+        std::vector<double> obs(observed, observed + sd);
+        const bool f32 = m->precision == VXB_F32;
+        if (f32)
+            for (double& v : obs) v = static_cast<double>(static_cast<float>(v));
+        std::vector<std::uint64_t> ranges;
+        if (key->mode == VXB_KEY_WORKER) {
+            require(key->workers >= 1, "invalid-shape", "need at least one worker");
+            require(supported_width(key->block_width), "invalid-shape", "unsupported block width");
+            ranges.resize(2 * key->workers);
+            partition(n_total, key->workers, key->block_width, ranges.data());
+        }
+        parallel_for(count, threads, [&](std::uint64_t r) {
+            const std::uint64_t row = first + r;
+            std::uint64_t id = row, base = 0;
+            if (key->mode == VXB_KEY_WORKER) {
+                std::uint64_t w = 0;
+                while (!(row >= ranges[2 * w] && row < ranges[2 * w + 1])) ++w;
+                id = w;
+                base = (row - ranges[2 * w]) * lg.row_stride();
+            }
+            Stream s(key->seed, id);
+            s.pos = base;
+            double theta[3], dist;
+            std::uint8_t bad;
+            std::vector<double> summary(sd);
+            const double* ext = external_noise ? external_noise + r * lg.steps : nullptr;
+            if (f32)
+                abc_row<float>(lg, s, obs.data(), ext, theta, summary.data(), &dist, &bad);
+            else
+                abc_row<double>(lg, s, obs.data(), ext, theta, summary.data(), &dist, &bad);
+            if (params) std::copy(theta, theta + 3, params + r * 3);
+            if (summaries) std::copy(summary.begin(), summary.end(), summaries + r * sd);
+            if (rho) rho[r] = dist;
+            if (failed) failed[r] = bad;
+        });
+    });
+}
+
+int vxo_simulate_at(const vxb_model* m, const double* theta, std::uint64_t seed, std::uint64_t id,
+                    std::uint64_t pos, double* summary) {
+    return guarded([&] {
+        const Logistic lg(*m);
+        Stream s(seed, id);
+        s.pos = pos;
+        s.align_even();
+        double th[3] = {theta[0], theta[1], theta[2]};
+        bool ok;
+        if (m->precision == VXB_F32) {
+            for (double& v : th) v = static_cast<double>(static_cast<float>(v));
+            ok = lg.simulate<float>(th, [&](std::uint32_t) { return s.next_gaussian(0.0, 1.0); },
+                                    summary);
+        } else {
+            ok = lg.simulate<double>(th, [&](std::uint32_t) { return s.next_gaussian(0.0, 1.0); },
+                                     summary);
+        }
+        require(ok, "invalid-state", "state left the reals");
+    });
+}
+
+// select_epsilon: abc.cpp:75-97
+int vxo_select_epsilon(const double* rho, const std::uint8_t* failed, std::uint64_t n, double q,
+                       double* eps, std::uint64_t cap, std::uint64_t* n_acc, std::uint64_t* idx) {
+    return guarded([&] {
+        require(q > 0.0 && q <= 1.0, "invalid-argument", "accept fraction must lie in (0, 1]");
+        std::vector<double> v;
+        v.reserve(n);
+        for (std::uint64_t r = 0; r < n; ++r)
+            if (!(failed && failed[r])) v.push_back(rho[r]);
+        require(!v.empty(), "empty-set", "every prior predictive row failed");
+        std::sort(v.begin(), v.end());
+        double e = quantile_sorted(v.data(), v.size(), q);
+        const std::size_t min_accept =
+            static_cast<std::size_t>(std::ceil(q * static_cast<double>(v.size())));
+        if (min_accept >= 1 && e < v[min_accept - 1]) e = v[min_accept - 1];
+        *eps = e;
+        std::uint64_t k = 0;
+        for (std::uint64_t r = 0; r < n; ++r)
+            if (!(failed && failed[r]) && rho[r] <= e) {
+                if (idx && k < cap) idx[k] = r;
+                ++k;
+            }
+        *n_acc = k;
+    });
+}
+
+// ------------------------------------------------------------ p-values (C2)
+// Draw order of weak_info.cpp:82-106 (align_even; Gaussian prior draw taking
+// one pair; then the data) and the counting rule of estimate_pvalues,
+// weak_info.cpp:108-120 (value <= observed, ties count).
+int vxo_ppp_pvalues(const vxb_model* m, const double* lambda, const double* log_norm,
+                    std::uint32_t n_lambda, std::uint64_t m_total, std::uint64_t first,
+                    std::uint64_t count, std::uint64_t seed, double ybar_obs,
+                    std::uint64_t* counts, double* pvalues, double* ybar_out, unsigned threads) {
+    return guarded([&] {
+        require(m->model == VXB_MODEL_NORMAL_MEAN, "invalid-argument", "not the normal-mean model");
+        require(m->steps >= 1, "insufficient-data", "need at least one observation per dataset");
+        require(n_lambda >= 1 && m_total >= 1 && first + count <= m_total, "invalid-shape",
+                "bad lambda grid or dataset range");
+        const std::uint64_t n = m->steps;
+        const double dn = static_cast<double>(n);
+        for (std::uint32_t k = 0; k < n_lambda; ++k) {
+            require(lambda[k] >= 0.0, "invalid-argument", "prior scales must be nonnegative");
+            const double v = lambda[k] * lambda[k] + 1.0 / dn;
+            const double logm_obs = log_norm[k] - ((0.5 * ybar_obs) * ybar_obs) / v;
+            const std::uint64_t sk = derive_seed1(seed, k);
+            std::vector<std::uint64_t> part(std::max(1u, threads), 0);
+            const unsigned nt = std::max(1u, threads);
+            std::vector<std::thread> pool;
+            auto body = [&](unsigned t) {
+                std::uint64_t c = 0;
+                for (std::uint64_t j = t; j < count; j += nt) {
+                    Stream s(sk, first + j);
+                    s.align_even();
+                    const double theta = lambda[k] * s.next_gaussian(0.0, 1.0);
+                    s.pos = 2;  // second half of the prior pair is discarded
+                    double sum = 0.0;
+                    for (std::uint64_t i = 0; i < n; ++i) sum += theta + s.next_gaussian(0.0, 1.0);
+                    const double ybar = sum / dn;
+                    if (ybar_out) ybar_out[static_cast<std::uint64_t>(k) * count + j] = ybar;
+                    const double logm = log_norm[k] - ((0.5 * ybar) * ybar) / v;
+                    if (logm <= logm_obs) ++c;
+                }
+                part[t] = c;
+            };
+            if (nt == 1) {
+                body(0);
+            } else {
+                for (unsigned t = 0; t < nt; ++t) pool.emplace_back(body, t);
+                for (auto& th : pool) th.join();
+            }
+            std::uint64_t c = 0;
+            for (std::uint64_t v2 : part) c += v2;
+            counts[k] = c;
+            if (pvalues) pvalues[k] = static_cast<double>(c) / static_cast<double>(m_total);
+        }
+    });
+}
+
+// estimate_pvalues: weak_info.cpp:108-120; compute_cutoff: :122-125
+int vxo_estimate_pvalues(const double* base, std::uint64_t nb, const double* k, std::uint64_t nk,
+                         double* out) {
+    return guarded([&] {
+        require(nk >= 1, "invalid-argument", "need at least one comparison evidence");
+        std::vector<double> sorted(k, k + nk);
+        std::sort(sorted.begin(), sorted.end());
+        for (std::uint64_t i = 0; i < nb; ++i) {
+            const auto it = std::upper_bound(sorted.begin(), sorted.end(), base[i]);
+            out[i] = static_cast<double>(it - sorted.begin()) / static_cast<double>(nk);
+        }
+    });
+}
+int vxo_compute_cutoff(const double* p, std::uint64_t n, double alpha, double* out) {
+    return guarded([&] {
+        require(alpha > 0.0 && alpha < 1.0, "invalid-argument", "alpha must lie in (0, 1)");
+        *out = quantile(p, n, alpha);
+    });
+}
+
+// -------------------------------------------------------------- SMC pieces
+// ess: smc.cpp:208-219
+int vxo_ess(const double* lw, std::uint64_t n, double* out) {
+    return guarded([&] {
+        double m = -std::numeric_limits<double>::infinity();
+        for (std::uint64_t i = 0; i < n; ++i) m = std::max(m, lw[i]);
+        require(m > -std::numeric_limits<double>::infinity(), "degenerate-ensemble",
+                "all weights are zero");
+        double s1 = 0.0, s2 = 0.0;
+        for (std::uint64_t i = 0; i < n; ++i) {
+            const double e = std::exp(lw[i] - m);
+            s1 += e;
+            s2 += e * e;
+        }
+        *out = s1 * s1 / s2;
+    });
+}
+// resample_multinomial: smc.cpp:268-300 (draw i = position i of the stream)
+int vxo_resample_multinomial(std::uint64_t n, std::uint32_t dim, const double* log_w,
+                             const double* particles, std::uint64_t seed, std::uint64_t id,
+                             double* particles_out, std::uint64_t* ancestors) {
+    return guarded([&] {
+        double m = -std::numeric_limits<double>::infinity();
+        for (std::uint64_t i = 0; i < n; ++i) m = std::max(m, log_w[i]);
+        require(m > -std::numeric_limits<double>::infinity(), "degenerate-ensemble",
+                "all weights are zero");
+        std::vector<double> cum(n);
+        double run = 0.0;
+        for (std::uint64_t i = 0; i < n; ++i) {
+            run += std::exp(log_w[i] - m);
+            cum[i] = run;
+        }
+        require(std::isfinite(run) && run > 0.0, "degenerate-ensemble", "weight sum is not finite");
+        Stream s(seed, id);
+        for (std::uint64_t i = 0; i < n; ++i) {
+            const double target = s.next_unit() * run;
+            const std::uint64_t a = upper_bound_idx(cum.data(), n, target);
+            if (ancestors) ancestors[i] = a;
+            if (particles_out)
+                std::copy_n(particles + a * dim, dim, particles_out + i * dim);
+        }
+    });
+}
+
+// ----------------------------------------------------------- ABC-SMC (C3)
+// NOT IN THE REFERENCE (SPEC.md:353 lists ABC-SMC as a non-goal): the scheme
+// below is this repository's definition, assembled
+// from reference pieces: inverse-CDF ancestors (smc.cpp:286-290), proposal
+// theta + L z with inc_k = sum_{m<=k} L[k][m] z_m (smc.cpp:115-119), Cholesky +
+// jitter (numeric.cpp:81-96, smc.cpp:318-323), type-7 quantile
+// (numeric.cpp:20-36), zero prior density => reject (smc.cpp:131).
+
+// Weighted moments with the canonical two-level sums.  w is normalised.
+// cov = sum w d d^T / (1 - sum w^2)  (equals the n-1 divisor for equal weights,
+// numeric.cpp:55-79).  Returns sum w^2.
+double vxo_weighted_moments_impl(const double* theta, const double* w, std::size_t n,
+                                 std::size_t dim, double* mean, double* cov) {
+    for (std::size_t a = 0; a < dim; ++a)
+        mean[a] = canon_sum(n, [&](std::size_t i) { return w[i] * theta[i * dim + a]; });
+    const double s2 = canon_sum(n, [&](std::size_t i) { return w[i] * w[i]; });
+    const double denom = 1.0 - s2;
+    for (std::size_t a = 0; a < dim; ++a)
+        for (std::size_t b = 0; b <= a; ++b) {
+            const double c = canon_sum(n, [&](std::size_t i) {
+                return (w[i] * (theta[i * dim + a] - mean[a])) * (theta[i * dim + b] - mean[b]);
+            });
+            cov[a * dim + b] = c / denom;
+            cov[b * dim + a] = cov[a * dim + b];
+        }
+    return s2;
+}
+int vxo_weighted_moments(const double* theta, const double* w, std::uint64_t n, std::uint32_t dim,
+                         double* mean, double* cov, double* sum_w2) {
+    return guarded([&] {
+        require(n >= 2, "insufficient-data", "covariance needs at least two rows");
+        const double s2 = vxo_weighted_moments_impl(theta, w, n, dim, mean, cov);
+        if (sum_w2) *sum_w2 = s2;
+    });
+}
+int vxo_canon_cumsum(const double* w, std::uint64_t n, double* cum) {
+    return guarded([&] { canon_cumsum(w, n, cum); });
+}
+double vxo_canon_sum(const double* w, std::uint64_t n) {
+    return canon_sum(n, [&](std::size_t i) { return w[i]; });
+}
+
+// kernel factor: scale * cov, Cholesky, jitter on failure (smc.cpp:311-325)
+int vxo_make_kernel(const double* cov, std::uint32_t dim, double scale, double jitter,
+                    double* chol) {
+    return guarded([&] {
+        std::vector<double> c(cov, cov + dim * dim);
+        for (double& v : c) v = scale * v;
+        std::copy(c.begin(), c.end(), chol);
+        if (!cholesky(chol, dim)) {
+            for (std::uint32_t k = 0; k < dim; ++k) c[k * dim + k] += jitter;
+            std::copy(c.begin(), c.end(), chol);
+            require(cholesky(chol, dim), "degenerate-ensemble",
+                    "covariance is rank deficient beyond jitter");
+        }
+    });
+}
+
+// One proposal p of generation gen >= 1; stream RngStream(derive_seed(seed,{gen}), p):
+//   position 0       ancestor uniform (inverse CDF over cum_prev)
+//   positions 2..2+d_e-1   the d Gaussian increments (pair aligned, d_e = d + d%2)
+//   position 2+d_e+j standard normal of simulation step j+1
+// flag: 1 accepted, 0 rejected by distance, 2 outside the prior box, 3 failed.
+int vxo_abcsmc_propose(const vxb_model* m, std::uint64_t seed, std::uint32_t gen,
+                       std::uint64_t first, std::uint64_t count, std::uint64_t n_prev,
+                       const double* theta_prev, const double* cum_prev, const double* chol,
+                       const double* observed, double epsilon, double* theta_out, double* rho_out,
+                       std::uint8_t* flag_out, unsigned threads) {
+    return guarded([&] {
+        const Logistic lg(*m);
+        require(gen >= 1, "invalid-argument", "generation 0 is the prior predictive set");
+        require(n_prev >= 1, "insufficient-data", "empty previous population");
+        const std::uint64_t sg = derive_seed1(seed, gen);
+        const std::size_t d = 3, de = 4;
+        parallel_for(count, threads, [&](std::uint64_t r) {
+            Stream s(sg, first + r);
+            const double target = s.next_unit() * cum_prev[n_prev - 1];
+            const std::size_t a = upper_bound_idx(cum_prev, n_prev, target);
+            s.align_even();
+            double z[4];
+            for (std::size_t k = 0; k < de; ++k) z[k] = s.next_gaussian(0.0, 1.0);
+            double th[3];
+            bool inside = true;
+            for (std::size_t k = 0; k < d; ++k) {
+                double inc = 0.0;
+                for (std::size_t q = 0; q <= k; ++q) inc += chol[k * d + q] * z[q];
+                th[k] = theta_prev[a * d + k] + inc;
+                inside = inside && th[k] >= lg.lo[k] && th[k] < lg.hi[k];
+            }
+            std::uint8_t flag;
+            double dist = std::numeric_limits<double>::quiet_NaN();
+            if (!inside) {
+                flag = 2;
+            } else {
+                std::vector<double> summary(lg.n_obs);
+                const bool ok = lg.simulate<double>(
+                    th, [&](std::uint32_t) { return s.next_gaussian(0.0, 1.0); }, summary.data());
+                if (!ok) {
+                    flag = 3;
+                } else {
+                    dist = discrepancy<double>(summary.data(), observed, lg.n_obs);
+                    flag = dist <= epsilon ? 1 : 0;
+                }
+            }
+            std::copy(th, th + d, theta_out + r * d);
+            rho_out[r] = dist;
+            flag_out[r] = flag;
+        });
+    });
+}
+
+// Unnormalised importance weight of new particle i: 1 / sum_j w_j exp(-q_ij/2),
+// q = |L^-1 (theta_i - theta_j)|^2 by forward substitution with reciprocal
+// pivots, exp through exp2_clamped (fastmath.hpp:57-79); j summed in index order.
+int vxo_abcsmc_weights(std::uint32_t dim, std::uint64_t count, const double* theta_new, std::uint64_t n_prev, const double* theta_prev,
+                       const double* w_prev, const double* chol, double* w_out, unsigned threads) {
+    return guarded([&] {
+        require(dim >= 1 && dim <= 8, "invalid-shape", "dimension out of range");
+        double invd[8];
+        for (std::uint32_t k = 0; k < dim; ++k) invd[k] = 1.0 / chol[k * dim + k];
+        parallel_for(count, threads, [&](std::uint64_t r) {
+            const double* ti = theta_new + r * dim;
+            double sum = 0.0;
+            for (std::uint64_t j = 0; j < n_prev; ++j) {
+                double y[8];
+                double q = 0.0;
+                for (std::uint32_t k = 0; k < dim; ++k) {
+                    double v = ti[k] - theta_prev[j * dim + k];
+                    for (std::uint32_t c = 0; c < k; ++c) v -= chol[k * dim + c] * y[c];
+                    y[k] = v * invd[k];
+                    q += y[k] * y[k];
+                }
+                sum += w_prev[j] * exp2_clamped((-0.5 * q) * kInvLn2);
+            }
+            w_out[r] = 1.0 / sum;
+        });
+    });
+}
+
+// Full ABC-SMC run.  Generation 0: proposals are prior draws keyed
+// RngStream(derive_seed(seed,{0}), p) (run_prior_predictive row layout), all
+// non-failed rows accepted, equal weights.  Generation g>=1: epsilon_g = type-7
+// quantile of the previous rho; kernel = chol(scale * weighted cov); proposals
+// evaluated in rounds of round_size until at least N are accepted; the first N
+// accepted by proposal index form the population; weights normalised by the
+// canonical sum.
+int vxo_abcsmc_run(const vxb_model* m, const vxb_abcsmc_cfg* cfg, const double* observed,
+                   vxb_abcsmc_out* out, unsigned threads) {
+    return guarded([&] {
+        const Logistic lg(*m);
+        const std::uint64_t n = cfg->particles;
+        const std::size_t d = 3;
+        require(n >= 2, "insufficient-data", "need at least two particles");
+        require(cfg->generations >= 1, "invalid-argument", "need at least one generation");
+        require(cfg->quantile > 0.0 && cfg->quantile <= 1.0, "invalid-argument",
+                "quantile must lie in (0, 1]");
+        const std::uint64_t round = cfg->round_size ? cfg->round_size : n;
+        const std::uint64_t max_rounds = cfg->max_rounds ? cfg->max_rounds : 1000;
+        std::vector<double> theta(n * d), w(n), rho(n), cum(n);
+        std::vector<double> th_new(n * d), rho_new(n), w_new(n);
+        std::vector<double> p_theta(round * d), p_rho(round);
+        std::vector<std::uint8_t> p_flag(round);
+        for (std::uint32_t g = 0; g < cfg->generations; ++g) {
+            double eps = std::numeric_limits<double>::infinity();
+            double chol[9] = {0};
+            if (g >= 1) {
+                eps = quantile(rho.data(), n, cfg->quantile);
+                double mean[3], cov[9];
+                vxo_weighted_moments_impl(theta.data(), w.data(), n, d, mean, cov);
+                require(vxo_make_kernel(cov, d, cfg->kernel_scale, cfg->jitter, chol) == 0,
+                        "degenerate-ensemble", "covariance is rank deficient beyond jitter");
+                canon_cumsum(w.data(), n, cum.data());
+            }
+            std::uint64_t got = 0, evaluated = 0, accepted_total = 0;
+            for (std::uint64_t t = 0; t < max_rounds && got < n; ++t) {
+                if (g == 0) {
+                    vxb_keying key{VXB_KEY_PARTICLE, 1, 1, 0, derive_seed1(cfg->seed, 0)};
+                    std::vector<std::uint8_t> failed(round);
+                    const std::uint64_t total = (t + 1) * round;
+                    require(vxo_abc_prior_predictive(m, &key, total, t * round, round, observed,
+                                                     p_theta.data(), nullptr, p_rho.data(),
+                                                     failed.data(), nullptr, threads) == 0,
+                            "internal", "prior predictive failed");
+                    for (std::uint64_t r = 0; r < round; ++r) p_flag[r] = failed[r] ? 3 : 1;
+                } else {
+                    require(vxo_abcsmc_propose(m, cfg->seed, g, t * round, round, n, theta.data(),
+                                               cum.data(), chol, observed, eps, p_theta.data(),
+                                               p_rho.data(), p_flag.data(), threads) == 0,
+                            "internal", "propose failed");
+                }
+                evaluated += round;
+                for (std::uint64_t r = 0; r < round; ++r) {
+                    if (p_flag[r] != 1) continue;
+                    ++accepted_total;
+                    if (got < n) {
+                        std::copy_n(p_theta.data() + r * d, d, th_new.data() + got * d);
+                        rho_new[got] = p_rho[r];
+                        ++got;
+                    }
+                }
+            }
+            require(got == n, "empty-set", "generation did not fill within max_rounds");
+            if (g == 0) {
+                for (std::uint64_t i = 0; i < n; ++i) w_new[i] = 1.0 / static_cast<double>(n);
+            } else {
+                require(vxo_abcsmc_weights(d, n, th_new.data(), n, theta.data(), w.data(), chol,
+                                           w_new.data(), threads) == 0,
+                        "internal", "weights failed");
+                const double total = canon_sum(n, [&](std::size_t i) { return w_new[i]; });
+                require(std::isfinite(total) && total > 0.0, "degenerate-ensemble",
+                        "weight sum is not finite");
+                for (std::uint64_t i = 0; i < n; ++i) w_new[i] = w_new[i] / total;
+            }
+            theta.swap(th_new);
+            rho.swap(rho_new);
+            w.swap(w_new);
+            double mean[3], cov[9];
+            const double s2 = vxo_weighted_moments_impl(theta.data(), w.data(), n, d, mean, cov);
+            if (out->epsilon) out->epsilon[g] = eps;
+            if (out->ess) out->ess[g] = 1.0 / s2;
+            if (out->accept_rate)
+                out->accept_rate[g] =
+                    static_cast<double>(accepted_total) / static_cast<double>(evaluated);
+            if (out->proposals) out->proposals[g] = evaluated;
+            if (out->mean) std::copy(mean, mean + d, out->mean + g * d);
+            if (out->cov) std::copy(cov, cov + d * d, out->cov + g * d * d);
+        }
+        if (out->theta) std::copy(theta.begin(), theta.end(), out->theta);
+        if (out->weight) std::copy(w.begin(), w.end(), out->weight);
+        if (out->rho) std::copy(rho.begin(), rho.end(), out->rho);
+    });
+}
+
+// ------------------------------------------------- tau-leap MLMC (C4)
+// NOT IN THE REFERENCE (tau-leap is out of scope; no Poisson
+// sampler in rng.cpp).  Defined here in the style of tb_model.cpp:39-116
+// (propensities from the state, uniforms through next_unit, rate <= 0 guard
+// :57-60):
+//  * Poisson(lam) by CDF inversion from one uniform: p0 = exp(-lam) through
+//    exp2_clamped, p_k = (p_{k-1} * lam) * (1/k), at most 1023 terms;
+//  * propensities from max(X, 0): a1 = (k1*S)*E, a2 = k2*C, a3 = k3*C;
+//  * level 0: plain tau-leap, step s uses positions 4s + r (r = reaction);
+//  * level l >= 1: Anderson-Higham coupling of a fine path (tau_l) and a coarse
+//    path (M tau_l): per fine step and reaction r, with the coarse propensity
+//    frozen over the coarse step: m = min(af, ac), P1 ~ Poi(m tau),
+//    P2 ~ Poi((af-m) tau), P3 ~ Poi((ac-m) tau) at positions 10s + 3r + {0,1,2};
+//    fine fires P1+P2, coarse fires P1+P3;
+//  * path `i` of level l owns RngStream(derive_seed(seed,{l}), i).
+static int poisson_inv(double lam, double u, std::int64_t* iters) {
+    if (!(lam > 0.0)) return 0;
+    double p = exp2_clamped((-lam) * kInvLn2);
+    double cdf = p;
+    int k = 0;
+    while (u > cdf && k < 1023) {
+        ++k;
+        p = (p * lam) * (1.0 / static_cast<double>(k));
+        cdf += p;
+        ++*iters;
+    }
+    return k;
+}
+
+struct MM {
+    std::int32_t s, e, c, p;
+    void fire(int k1, int k2, int k3) {
+        s += -k1 + k2;
+        e += -k1 + k2 + k3;
+        c += k1 - k2 - k3;
+        p += k3;
+    }
+    void prop(const double* k, double* a) const {
+        const double ds = static_cast<double>(s > 0 ? s : 0);
+        const double de = static_cast<double>(e > 0 ? e : 0);
+        const double dc = static_cast<double>(c > 0 ? c : 0);
+        a[0] = (k[0] * ds) * de;
+        a[1] = k[1] * dc;
+        a[2] = k[2] * dc;
+    }
+};
+
+int vxo_mlmc_level(const vxb_model* m, const vxb_mlmc_cfg* cfg, std::uint32_t level,
+                   std::uint64_t first, std::uint64_t count, std::int64_t* sums,
+                   std::int32_t* y_out, unsigned threads) {
+    return guarded([&] {
+        require(m->model == VXB_MODEL_MM_TAULEAP, "invalid-argument", "not the tau-leap model");
+        require(cfg->refine >= 2 && level < cfg->levels, "invalid-argument", "bad level");
+        require(cfg->tau0 > 0.0 && cfg->t_end > 0.0, "invalid-horizon", "need a positive horizon");
+        const std::uint64_t steps0 = static_cast<std::uint64_t>(std::llround(cfg->t_end / cfg->tau0));
+        require(steps0 >= 1, "invalid-horizon", "need at least one step");
+        std::uint64_t nf = steps0;
+        for (std::uint32_t l = 0; l < level; ++l) nf *= cfg->refine;
+        const double tau = cfg->t_end / static_cast<double>(nf);
+        const double kr[3] = {m->consts[4], m->consts[5], m->consts[6]};
+        const MM init{static_cast<std::int32_t>(m->consts[0]), static_cast<std::int32_t>(m->consts[1]),
+                      static_cast<std::int32_t>(m->consts[2]), static_cast<std::int32_t>(m->consts[3])};
+        const std::uint64_t sl = derive_seed1(cfg->seed, level);
+        const unsigned nt = std::max(1u, threads);
+        std::vector<std::int64_t> acc(4 * nt, 0);
+        auto body = [&](unsigned t) {
+            std::int64_t sy = 0, sy2 = 0, sp = 0, it = 0;
+            for (std::uint64_t r = t; r < count; r += nt) {
+                Stream s(sl, first + r);
+                MM f = init, c = init;
+                double af[3], ac[3];
+                if (level == 0) {
+                    for (std::uint64_t st = 0; st < nf; ++st) {
+                        f.prop(kr, af);
+                        int k[3];
+                        for (int q = 0; q < 3; ++q) {
+                            s.pos = 4 * st + q;
+                            k[q] = poisson_inv(af[q] * tau, s.next_unit(), &it);
+                        }
+                        f.fire(k[0], k[1], k[2]);
+                    }
+                } else {
+                    for (std::uint64_t st = 0; st < nf; ++st) {
+                        if (st % cfg->refine == 0) c.prop(kr, ac);
+                        f.prop(kr, af);
+                        int kf[3], kc[3];
+                        for (int q = 0; q < 3; ++q) {
+                            const double mn = af[q] < ac[q] ? af[q] : ac[q];
+                            s.pos = 10 * st + 3 * q;
+                            const int p1 = poisson_inv(mn * tau, s.next_unit(), &it);
+                            const int p2 = poisson_inv((af[q] - mn) * tau, s.next_unit(), &it);
+                            const int p3 = poisson_inv((ac[q] - mn) * tau, s.next_unit(), &it);
+                            kf[q] = p1 + p2;
+                            kc[q] = p1 + p3;
+                        }
+                        f.fire(kf[0], kf[1], kf[2]);
+                        c.fire(kc[0], kc[1], kc[2]);
+                    }
+                }
+                const std::int32_t y = level == 0 ? f.p : f.p - c.p;
+                if (y_out) y_out[r] = y;
+                sy += y;
+                sy2 += static_cast<std::int64_t>(y) * y;
+                sp += f.p;
+            }
+            acc[4 * t] = sy;
+            acc[4 * t + 1] = sy2;
+            acc[4 * t + 2] = sp;
+            acc[4 * t + 3] = it;
+        };
+        if (nt == 1) {
+            body(0);
+        } else {
+            std::vector<std::thread> pool;
+            for (unsigned t = 0; t < nt; ++t) pool.emplace_back(body, t);
+            for (auto& th : pool) th.join();
+        }
+        for (int q = 0; q < 4; ++q) {
+            sums[q] = 0;
+            for (unsigned t = 0; t < nt; ++t) sums[q] += acc[4 * t + q];
+        }
+    });
+}
+
+// Estimator: sum over levels of the sample mean of Y_l; variance of the
+// estimator = sum var_l / paths (n-1 divisor, numeric.cpp:45-51).
+int vxo_mlmc_tauleap(const vxb_model* m, const vxb_mlmc_cfg* cfg, vxb_mlmc_out* out,
+                     unsigned threads) {
+    return guarded([&] {
+        require(cfg->paths >= 2, "insufficient-data", "variance needs at least two values");
+        double est = 0.0, var = 0.0;
+        std::uint64_t steps = static_cast<std::uint64_t>(std::llround(cfg->t_end / cfg->tau0));
+        for (std::uint32_t l = 0; l < cfg->levels; ++l) {
+            std::int64_t sums[4];
+            require(vxo_mlmc_level(m, cfg, l, 0, cfg->paths, sums, nullptr, threads) == 0,
+                    "internal", "level failed");
+            const double n = static_cast<double>(cfg->paths);
+            const double mean = static_cast<double>(sums[0]) / n;
+            const double v =
+                (static_cast<double>(sums[1]) - static_cast<double>(sums[0]) * mean) / (n - 1.0);
+            if (out->level_mean) out->level_mean[l] = mean;
+            if (out->level_var) out->level_var[l] = v;
+            if (out->level_cost)
+                out->level_cost[l] = static_cast<double>(l == 0 ? steps : steps + steps / cfg->refine);
+            est += mean;
+            var += v / n;
+            steps *= cfg->refine;
+        }
+        out->estimate = est;
+        out->std_error = std::sqrt(var);
+    });
+}
+
+// Exact Gillespie (direct method) for the same network, restated from the
+// event loop of tb_model.cpp:39-116 (total rate, exponential waiting time from
+// one uniform through ln_pos, inverse-CDF reaction choice from a second).
+// Anchor for the MLMC estimate only.  Path i owns RngStream(derive_seed(seed,{99}), i).
+int vxo_mm_gillespie(const vxb_model* m, double t_end, std::uint64_t paths, std::uint64_t seed,
+                     double* mean_p, double* var_p, unsigned threads) {
+    return guarded([&] {
+        const double kr[3] = {m->consts[4], m->consts[5], m->consts[6]};
+        const MM init{static_cast<std::int32_t>(m->consts[0]), static_cast<std::int32_t>(m->consts[1]),
+                      static_cast<std::int32_t>(m->consts[2]), static_cast<std::int32_t>(m->consts[3])};
+        const std::uint64_t sg = derive_seed1(seed, 99);
+        const unsigned nt = std::max(1u, threads);
+        std::vector<std::int64_t> acc(2 * nt, 0);
+        auto body = [&](unsigned t) {
+            for (std::uint64_t r = t; r < paths; r += nt) {
+                Stream s(sg, r);
+                MM x = init;
+                double now = 0.0;
+                for (;;) {
+                    double a[3];
+                    x.prop(kr, a);
+                    const double total = (a[0] + a[1]) + a[2];
+                    if (!(total > 0.0)) break;
+                    const double u = s.next_unit();
+                    const double wait = -ln_pos(1.0 - u) / total;
+                    now += wait;
+                    if (now > t_end) break;
+                    const double pick = s.next_unit() * total;
+                    if (pick < a[0]) x.fire(1, 0, 0);
+                    else if (pick < a[0] + a[1]) x.fire(0, 1, 0);
+                    else x.fire(0, 0, 1);
+                }
+                acc[2 * t] += x.p;
+                acc[2 * t + 1] += static_cast<std::int64_t>(x.p) * x.p;
+            }
+        };
+        std::vector<std::thread> pool;
+        for (unsigned t = 0; t < nt; ++t) pool.emplace_back(body, t);
+        for (auto& th : pool) th.join();
+        std::int64_t s1 = 0, s2 = 0;
+        for (unsigned t = 0; t < nt; ++t) {
+            s1 += acc[2 * t];
+            s2 += acc[2 * t + 1];
+        }
+        const double n = static_cast<double>(paths);
+        *mean_p = static_cast<double>(s1) / n;
+        *var_p = (static_cast<double>(s2) - static_cast<double>(s1) * *mean_p) / (n - 1.0);
+    });
+}
+
+}  // extern "C"

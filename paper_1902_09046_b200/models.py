@@ -1,0 +1,62 @@
+"""POD model descriptors for the BASELINE.json workloads (host side, no compute).
+
+Each constructor fills a ``vxb_model`` (include/vexbayes_cuda.h); it plays the
+role of the reference's ``make_abc_model`` factories (toggle_switch.cpp:135-152)
+with the closures replaced by a plain descriptor the device can read.
+"""
+import math
+
+from . import _abi as A
+
+
+def logistic_model(steps=2000, obs_stride=100, dt=0.01, x0=10.0,
+                   prior_lo=(0.0, 50.0, 0.0), prior_hi=(1.0, 150.0, 0.2),
+                   precision=A.VXB_F64, rng=A.VXB_RNG_REF, arith=A.VXB_ARITH_EXACT):
+    """Stochastic logistic growth dX = rX(1-X/K)dt + sigma X dW (configs 0/1/3)."""
+    m = A.vxb_model()
+    m.model = A.VXB_MODEL_LOGISTIC_SDE
+    m.precision, m.rng, m.arith = precision, rng, arith
+    m.dim = 3
+    m.steps, m.obs_stride = steps, obs_stride
+    m.summary_dim = steps // obs_stride if obs_stride else 0
+    m.dt, m.x0 = dt, x0
+    for k in range(3):
+        m.prior_lo[k] = prior_lo[k]
+        m.prior_hi[k] = prior_hi[k]
+    m.consts[0] = math.sqrt(dt)
+    return m
+
+
+def normal_mean_model(n_data=100, rng=A.VXB_RNG_REF, arith=A.VXB_ARITH_EXACT):
+    """y_i ~ N(theta, 1), theta ~ N(0, lambda^2) (config 2)."""
+    m = A.vxb_model()
+    m.model = A.VXB_MODEL_NORMAL_MEAN
+    m.precision, m.rng, m.arith = A.VXB_F64, rng, arith
+    m.dim, m.summary_dim = 1, 1
+    m.steps, m.obs_stride = n_data, n_data
+    return m
+
+
+def mm_tauleap_model(x0=(100, 20, 0, 0), rates=(1e-3, 1e-4, 0.1)):
+    """Michaelis-Menten network S+E->C, C->S+E, C->E+P (config 4)."""
+    m = A.vxb_model()
+    m.model = A.VXB_MODEL_MM_TAULEAP
+    m.precision, m.rng, m.arith = A.VXB_F64, A.VXB_RNG_REF, A.VXB_ARITH_EXACT
+    m.dim, m.summary_dim = 3, 1
+    for k in range(4):
+        m.consts[k] = float(x0[k])
+    for k in range(3):
+        m.consts[4 + k] = float(rates[k])
+    return m
+
+
+def keying(seed, mode=A.VXB_KEY_PARTICLE, workers=1, block_width=1):
+    k = A.vxb_keying()
+    k.mode, k.workers, k.block_width, k.reserved, k.seed = mode, workers, block_width, 0, seed
+    return k
+
+
+def lambda_grid(n=64, lo=0.1, hi=100.0):
+    """Config 2 hyperparameter grid: n values log-spaced in [lo, hi]."""
+    a, b = math.log10(lo), math.log10(hi)
+    return [10.0 ** (a + (b - a) * k / (n - 1)) for k in range(n)]
