@@ -1,0 +1,186 @@
+// vxb_common.cuh -- host-side plumbing shared by the C-ABI translation units:
+// the context, the error convention (errors.hpp:11-28 "code: message" carried
+// across the ABI as a thread-local string), host/device buffer staging and the
+// per-launch event profiler.
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/vexbayes_cuda.h"
+
+namespace vxb {
+
+struct Error {
+    std::string code, message;
+};
+[[noreturn]] inline void raise(const char* code, const std::string& message) {
+    throw Error{code, message};
+}
+inline void require(bool ok, const char* code, const char* message) {
+    if (!ok) raise(code, message);
+}
+void set_last_error(const std::string& text);
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        raise("device-error", std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define VXB_CUDA(call) ::vxb::cuda_check((call), #call)
+
+// Runs `f`, maps vxb::Error to the ABI convention (0 ok / 1 library error).
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const Error& e) {
+        set_last_error(e.code + ": " + e.message);
+        return 1;
+    } catch (const std::exception& e) {
+        set_last_error(std::string("internal: ") + e.what());
+        return 2;
+    }
+}
+
+}  // namespace vxb
+
+struct vxb_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaDeviceProp prop{};
+    bool profiling = false;
+    vxb_profile profile{};
+    std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> pending;
+    std::vector<cudaEvent_t> event_pool;
+};
+
+namespace vxb {
+
+inline void use(vxb_ctx* ctx) {
+    require(ctx != nullptr, "invalid-argument", "null context");
+    VXB_CUDA(cudaSetDevice(ctx->device));
+}
+
+inline bool is_device_pointer(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+// A device view of a caller buffer.  Device pointers pass through; host
+// pointers are staged through stream-ordered scratch (input: copied in on
+// construction; output: copied back by finish()).
+class Staged {
+public:
+    Staged() = default;
+    Staged(vxb_ctx* ctx, const void* user, size_t bytes, bool is_input, bool is_output)
+        : ctx_(ctx), user_(const_cast<void*>(user)), bytes_(bytes), out_(is_output) {
+        if (!user || bytes == 0) return;
+        if (is_device_pointer(user)) {
+            dev_ = user_;
+            return;
+        }
+        owned_ = true;
+        VXB_CUDA(cudaMallocAsync(&dev_, bytes, ctx->stream));
+        if (is_input)
+            VXB_CUDA(cudaMemcpyAsync(dev_, user, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    Staged(const Staged&) = delete;
+    Staged& operator=(const Staged&) = delete;
+    ~Staged() {
+        if (owned_ && dev_) cudaFreeAsync(dev_, ctx_->stream);
+    }
+    // queue the device->host copy of an output (no-op for device buffers)
+    void finish(size_t bytes = ~size_t(0)) {
+        if (owned_ && out_ && dev_) {
+            const size_t n = bytes < bytes_ ? bytes : bytes_;
+            if (n) VXB_CUDA(cudaMemcpyAsync(user_, dev_, n, cudaMemcpyDeviceToHost, ctx_->stream));
+        }
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(dev_);
+    }
+    void* ptr() const { return dev_; }
+    bool staged() const { return owned_; }
+
+private:
+    vxb_ctx* ctx_ = nullptr;
+    void* user_ = nullptr;
+    void* dev_ = nullptr;
+    size_t bytes_ = 0;
+    bool owned_ = false, out_ = false;
+};
+
+// Stream-ordered scratch with RAII.
+class Scratch {
+public:
+    Scratch(vxb_ctx* ctx, size_t bytes) : ctx_(ctx) {
+        if (bytes) VXB_CUDA(cudaMallocAsync(&p_, bytes, ctx->stream));
+    }
+    Scratch(const Scratch&) = delete;
+    Scratch& operator=(const Scratch&) = delete;
+    ~Scratch() {
+        if (p_) cudaFreeAsync(p_, ctx_->stream);
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p_);
+    }
+
+private:
+    vxb_ctx* ctx_;
+    void* p_ = nullptr;
+};
+
+// Counts a launch of family `kind`; with profiling on, brackets it by events.
+class LaunchScope {
+public:
+    LaunchScope(vxb_ctx* ctx, int kind) : ctx_(ctx), kind_(kind) {
+        ctx->profile.launches[kind]++;
+        if (ctx->profiling) {
+            a_ = take();
+            b_ = take();
+            cudaEventRecord(a_, ctx->stream);
+        }
+    }
+    ~LaunchScope() {
+        if (ctx_->profiling) {
+            cudaEventRecord(b_, ctx_->stream);
+            ctx_->pending.emplace_back(kind_, a_, b_);
+        }
+    }
+
+private:
+    cudaEvent_t take() {
+        if (!ctx_->event_pool.empty()) {
+            cudaEvent_t e = ctx_->event_pool.back();
+            ctx_->event_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+    vxb_ctx* ctx_;
+    int kind_;
+    cudaEvent_t a_ = nullptr, b_ = nullptr;
+};
+
+inline void check_launch(const char* what) { cuda_check(cudaGetLastError(), what); }
+
+inline unsigned grid_for(uint64_t n, unsigned block) {
+    return static_cast<unsigned>((n + block - 1) / block);
+}
+
+}  // namespace vxb

@@ -1,0 +1,344 @@
+// vxb_logistic.cu -- ABC rejection on the logistic SDE (configs 0/1): the fused
+// simulate -> summary -> distance kernel and the C-ABI entry points built on it
+// (drop-ins for abc::run_prior_predictive, abc.cpp:26-73).
+//
+// Launch shape: one particle per thread, state in registers, 256-thread CTAs.
+// The kernel is FP64-pipe bound (fp32: FP32/MUFU bound); HBM traffic is the
+// per-row outputs only (<= 8 B/row on the fused fixed-epsilon path).
+
+#include <cmath>
+#include <limits>
+
+#include "vxb_common.cuh"
+#include "vxb_logistic.cuh"
+
+namespace vxb {
+
+struct AbcParams {
+    uint64_t first, count;
+    Keying key;
+    LogisticModel model;
+    double observed[VXB_MAX_SUMMARY];
+    const double* theta_in;  // kKeyFixed: simulate at this theta, no prior draw
+    void* params;
+    void* summaries;
+    void* rho;
+    uint8_t* failed;
+    const void* noise;
+};
+
+constexpr int kBlock = 256;
+
+template <class Real, int kRng, bool kFma>
+__global__ void __launch_bounds__(kBlock)
+logistic_abc_kernel(const __grid_constant__ AbcParams p) {
+    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
+    if (r >= p.count) return;
+    const uint64_t row = p.first + r;
+    uint64_t key, base;
+    locate_row(p.key, row, key, base);
+
+    double theta[3];
+    uint64_t noise_pos;
+    if (p.theta_in) {
+        theta[0] = p.theta_in[0];
+        theta[1] = p.theta_in[1];
+        theta[2] = p.theta_in[2];
+        noise_pos = base + (base & 1);
+    } else {
+        if (kRng == VXB_RNG_FAST)
+            draw_prior_fast(p.model, key, theta);
+        else
+            draw_prior_ref(p.model, key, base, theta);
+        noise_pos = base + 4;  // three uniforms, aligned to the pair boundary
+    }
+    if (sizeof(Real) == 4) {
+        theta[0] = static_cast<double>(static_cast<float>(theta[0]));
+        theta[1] = static_cast<double>(static_cast<float>(theta[1]));
+        theta[2] = static_cast<double>(static_cast<float>(theta[2]));
+    }
+    if (p.params) {
+        Real* out = static_cast<Real*>(p.params) + r * 3;
+        out[0] = static_cast<Real>(theta[0]);
+        out[1] = static_cast<Real>(theta[1]);
+        out[2] = static_cast<Real>(theta[2]);
+    }
+
+    Real* summary = p.summaries ? static_cast<Real*>(p.summaries) + r * p.model.n_obs : nullptr;
+    auto emit = [summary](uint32_t k, Real v) {
+        if (summary) summary[k] = v;
+    };
+    using A = typename std::conditional<kFma, Fused, Exact>::type;
+    bool bad;
+    Real rho;
+    if (kRng == VXB_RNG_REF) {
+        RefNoise<Real> noise{key, noise_pos >> 1};
+        rho = logistic_path<Real, A>(p.model, theta, p.observed, noise, emit, bad);
+    } else if (kRng == VXB_RNG_FAST) {
+        typename std::conditional<sizeof(Real) == 4, FastNoise32, FastNoise64>::type noise{key, 0};
+        rho = logistic_path<Real, A>(p.model, theta, p.observed, noise, emit, bad);
+    } else {
+        ExternalNoise<Real> noise{static_cast<const Real*>(p.noise) + r * p.model.steps, 0,
+                                  p.model.steps};
+        rho = logistic_path<Real, A>(p.model, theta, p.observed, noise, emit, bad);
+    }
+    if (bad) {  // abc.cpp:57-60: flag the row, zero its summary, rho stays NaN
+        rho = static_cast<Real>(__longlong_as_double(0x7FF8000000000000LL));
+        if (summary)
+            for (uint32_t k = 0; k < p.model.n_obs; ++k) summary[k] = Real(0);
+    }
+    if (p.rho) static_cast<Real*>(p.rho)[r] = rho;
+    if (p.failed) p.failed[r] = bad ? 1 : 0;
+}
+
+// Re-derives the prior draw of accepted rows and gathers their rho (fused
+// fixed-epsilon path: rejected rows never leave the device).
+template <class Real, int kRng>
+__global__ void gather_accepted_kernel(Keying key, LogisticModel model, uint64_t first,
+                                       const uint64_t* __restrict__ idx, uint64_t n_acc,
+                                       const Real* __restrict__ rho_all, Real* params_out,
+                                       Real* rho_out) {
+    const uint64_t a = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (a >= n_acc) return;
+    const uint64_t row = idx[a];
+    uint64_t k, base;
+    locate_row(key, row, k, base);
+    double theta[3];
+    if (kRng == VXB_RNG_FAST)
+        draw_prior_fast(model, k, theta);
+    else
+        draw_prior_ref(model, k, base, theta);
+    if (params_out) {
+        params_out[a * 3 + 0] = static_cast<Real>(theta[0]);
+        params_out[a * 3 + 1] = static_cast<Real>(theta[1]);
+        params_out[a * 3 + 2] = static_cast<Real>(theta[2]);
+    }
+    if (rho_out) rho_out[a] = rho_all[row - first];
+}
+
+LogisticModel make_logistic(const vxb_model& m) {
+    require(m.model == VXB_MODEL_LOGISTIC_SDE, "invalid-argument", "not a logistic model");
+    require(m.dim == 3, "invalid-shape", "logistic model has three parameters");
+    require(m.steps >= 1 && m.obs_stride >= 1, "invalid-horizon", "need at least one step");
+    require(m.summary_dim >= 1 && m.summary_dim == m.steps / m.obs_stride, "invalid-summary",
+            "summary_dim must equal steps / obs_stride");
+    require(m.summary_dim <= VXB_MAX_SUMMARY, "invalid-summary", "summary dimension too large");
+    require(m.precision == VXB_F64 || m.precision == VXB_F32, "invalid-argument", "bad precision");
+    require(m.rng >= VXB_RNG_REF && m.rng <= VXB_RNG_EXTERNAL, "invalid-argument", "bad rng mode");
+    LogisticModel d;
+    d.steps = m.steps;
+    d.obs_stride = m.obs_stride;
+    d.n_obs = m.summary_dim;
+    d.dt = m.dt;
+    d.sqdt = m.consts[0];
+    d.x0 = m.x0;
+    for (int k = 0; k < 3; ++k) {
+        require(m.prior_lo[k] <= m.prior_hi[k], "invalid-range",
+                "uniform lower bound exceeds upper bound");
+        d.lo[k] = m.prior_lo[k];
+        d.hi[k] = m.prior_hi[k];
+    }
+    return d;
+}
+
+Keying make_keying(const vxb_keying& k, const vxb_model& m, uint64_t n_total) {
+    Keying d{};
+    d.seed_hash = splitmix64(k.seed);
+    if (k.mode == VXB_KEY_PARTICLE) {
+        d.mode = kKeyParticle;
+    } else if (k.mode == VXB_KEY_WORKER) {
+        require(k.workers >= 1, "invalid-shape", "need at least one worker");
+        const uint32_t v = k.block_width;
+        require(v == 1 || v == 2 || v == 4 || v == 8 || v == 16, "invalid-shape",
+                "block width must be one of 1, 2, 4, 8, 16");  // blocked.cpp:10-12
+        require(m.rng != VXB_RNG_FAST, "invalid-argument",
+                "worker keying is defined for the reference generator only");
+        d.mode = kKeyWorker;
+        const uint64_t blocks = (n_total + v - 1) / v;
+        d.base_blocks = blocks / k.workers;
+        d.extra_blocks = blocks % k.workers;
+        d.width = v;
+        d.row_stride = 4 + m.steps + (m.steps & 1);
+    } else {
+        raise("invalid-argument", "unknown keying mode");
+    }
+    return d;
+}
+
+template <class Real, int kRng>
+void launch_abc2(vxb_ctx* ctx, const AbcParams& p, bool fma) {
+    const unsigned grid = grid_for(p.count, kBlock);
+    LaunchScope scope(ctx, VXB_K_SIMULATE);
+    if (fma)
+        logistic_abc_kernel<Real, kRng, true><<<grid, kBlock, 0, ctx->stream>>>(p);
+    else
+        logistic_abc_kernel<Real, kRng, false><<<grid, kBlock, 0, ctx->stream>>>(p);
+    check_launch("logistic_abc_kernel");
+}
+template <class Real>
+void launch_abc1(vxb_ctx* ctx, const AbcParams& p, int rng, bool fma) {
+    if (rng == VXB_RNG_REF)
+        launch_abc2<Real, VXB_RNG_REF>(ctx, p, fma);
+    else if (rng == VXB_RNG_FAST)
+        launch_abc2<Real, VXB_RNG_FAST>(ctx, p, fma);
+    else
+        launch_abc2<Real, VXB_RNG_EXTERNAL>(ctx, p, fma);
+}
+void launch_abc(vxb_ctx* ctx, const vxb_model& m, const AbcParams& p) {
+    if (p.count == 0) return;
+    const bool fma = m.arith == VXB_ARITH_FMA || m.rng == VXB_RNG_FAST;
+    if (m.precision == VXB_F32)
+        launch_abc1<float>(ctx, p, m.rng, fma);
+    else
+        launch_abc1<double>(ctx, p, m.rng, fma);
+}
+
+// implemented in vxb_select.cu
+void compact_accepted_device(vxb_ctx* ctx, int precision, const void* rho_dev,
+                             const uint8_t* failed_dev, uint64_t n, double epsilon,
+                             uint64_t index_base, uint64_t cap, uint64_t* n_accepted_host,
+                             uint64_t* idx_dev);
+
+}  // namespace vxb
+
+using namespace vxb;
+
+extern "C" int vxb_abc_prior_predictive(vxb_ctx* ctx, const vxb_model* model,
+                                        const vxb_keying* key, uint64_t n_total, uint64_t first,
+                                        uint64_t count, const double* observed, void* params,
+                                        void* summaries, void* rho, uint8_t* failed,
+                                        const void* external_noise) {
+    return guarded([&] {
+        use(ctx);
+        require(model && key && observed, "invalid-argument", "null argument");
+        require(n_total >= 1, "invalid-shape", "need at least one prior predictive sample");
+        require(first + count <= n_total, "invalid-shape", "row range exceeds the job");
+        AbcParams p{};
+        p.model = make_logistic(*model);
+        p.key = make_keying(*key, *model, n_total);
+        p.first = first;
+        p.count = count;
+        for (uint32_t k = 0; k < p.model.n_obs; ++k)
+            p.observed[k] = model->precision == VXB_F32
+                                ? static_cast<double>(static_cast<float>(observed[k]))
+                                : observed[k];
+        require(model->rng != VXB_RNG_EXTERNAL || external_noise, "invalid-argument",
+                "external rng mode needs a noise buffer");
+        const size_t real = model->precision == VXB_F32 ? 4 : 8;
+        Staged d_params(ctx, params, count * 3 * real, false, true);
+        Staged d_summ(ctx, summaries, count * p.model.n_obs * real, false, true);
+        Staged d_rho(ctx, rho, count * real, false, true);
+        Staged d_failed(ctx, failed, count, false, true);
+        Staged d_noise(ctx, model->rng == VXB_RNG_EXTERNAL ? external_noise : nullptr,
+                       count * p.model.steps * real, true, false);
+        p.params = d_params.ptr();
+        p.summaries = d_summ.ptr();
+        p.rho = d_rho.ptr();
+        p.failed = d_failed.as<uint8_t>();
+        p.noise = d_noise.ptr();
+        launch_abc(ctx, *model, p);
+        d_params.finish();
+        d_summ.finish();
+        d_rho.finish();
+        d_failed.finish();
+        if (d_params.staged() || d_summ.staged() || d_rho.staged() || d_failed.staged())
+            VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+extern "C" int vxb_simulate_at(vxb_ctx* ctx, const vxb_model* model, const double* theta,
+                               uint64_t seed, uint32_t stream_id, uint64_t pos, void* summary) {
+    return guarded([&] {
+        use(ctx);
+        require(model && theta && summary, "invalid-argument", "null argument");
+        require(model->rng == VXB_RNG_REF, "invalid-argument",
+                "simulate_at is defined for the reference generator");
+        AbcParams p{};
+        p.model = make_logistic(*model);
+        p.key.mode = kKeyFixed;
+        p.key.fixed_key = stream_key(splitmix64(seed), stream_id);
+        p.key.fixed_pos = pos;
+        p.first = 0;
+        p.count = 1;
+        const size_t real = model->precision == VXB_F32 ? 4 : 8;
+        Staged d_theta(ctx, theta, 3 * sizeof(double), true, false);
+        Staged d_summ(ctx, summary, p.model.n_obs * real, false, true);
+        Scratch d_failed(ctx, 1);
+        p.theta_in = d_theta.as<double>();
+        p.summaries = d_summ.ptr();
+        p.failed = d_failed.as<uint8_t>();
+        launch_abc(ctx, *model, p);
+        uint8_t bad = 0;
+        VXB_CUDA(cudaMemcpyAsync(&bad, p.failed, 1, cudaMemcpyDeviceToHost, ctx->stream));
+        d_summ.finish();
+        VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+        require(!bad, "invalid-state", "state left the reals");
+    });
+}
+
+extern "C" int vxb_abc_reject(vxb_ctx* ctx, const vxb_model* model, const vxb_keying* key,
+                              uint64_t n_total, uint64_t first, uint64_t count,
+                              const double* observed, double epsilon, uint64_t cap,
+                              uint64_t* n_accepted, uint64_t* idx, void* params, void* rho) {
+    return guarded([&] {
+        use(ctx);
+        require(model && key && observed && n_accepted, "invalid-argument", "null argument");
+        require(n_total >= 1, "invalid-shape", "need at least one prior predictive sample");
+        require(first + count <= n_total, "invalid-shape", "row range exceeds the job");
+        require(model->rng != VXB_RNG_EXTERNAL, "invalid-argument",
+                "the fused path generates its own noise");
+        AbcParams p{};
+        p.model = make_logistic(*model);
+        p.key = make_keying(*key, *model, n_total);
+        p.first = first;
+        p.count = count;
+        const bool f32 = model->precision == VXB_F32;
+        for (uint32_t k = 0; k < p.model.n_obs; ++k)
+            p.observed[k] = f32 ? static_cast<double>(static_cast<float>(observed[k])) : observed[k];
+        const size_t real = f32 ? 4 : 8;
+        Scratch d_rho_all(ctx, count * real);
+        Scratch d_failed(ctx, count);
+        p.rho = d_rho_all.as<void>();
+        p.failed = d_failed.as<uint8_t>();
+        launch_abc(ctx, *model, p);
+
+        Staged d_idx(ctx, idx, cap * sizeof(uint64_t), false, true);
+        Scratch d_idx_tmp(ctx, d_idx.ptr() ? 0 : cap * sizeof(uint64_t));
+        uint64_t* idx_dev = d_idx.ptr() ? d_idx.as<uint64_t>() : d_idx_tmp.as<uint64_t>();
+        uint64_t n_acc = 0;
+        compact_accepted_device(ctx, model->precision, p.rho, p.failed, count, epsilon, first, cap,
+                                &n_acc, idx_dev);
+        *n_accepted = n_acc;
+        const uint64_t kept = n_acc < cap ? n_acc : cap;
+        Staged d_params(ctx, params, cap * 3 * real, false, true);
+        Staged d_rho(ctx, rho, cap * real, false, true);
+        if (kept && (params || rho)) {
+            LaunchScope scope(ctx, VXB_K_COMPACT);
+            const unsigned grid = grid_for(kept, 128);
+            if (f32) {
+                if (model->rng == VXB_RNG_FAST)
+                    gather_accepted_kernel<float, VXB_RNG_FAST><<<grid, 128, 0, ctx->stream>>>(
+                        p.key, p.model, first, idx_dev, kept, static_cast<const float*>(p.rho),
+                        d_params.as<float>(), d_rho.as<float>());
+                else
+                    gather_accepted_kernel<float, VXB_RNG_REF><<<grid, 128, 0, ctx->stream>>>(
+                        p.key, p.model, first, idx_dev, kept, static_cast<const float*>(p.rho),
+                        d_params.as<float>(), d_rho.as<float>());
+            } else {
+                if (model->rng == VXB_RNG_FAST)
+                    gather_accepted_kernel<double, VXB_RNG_FAST><<<grid, 128, 0, ctx->stream>>>(
+                        p.key, p.model, first, idx_dev, kept, static_cast<const double*>(p.rho),
+                        d_params.as<double>(), d_rho.as<double>());
+                else
+                    gather_accepted_kernel<double, VXB_RNG_REF><<<grid, 128, 0, ctx->stream>>>(
+                        p.key, p.model, first, idx_dev, kept, static_cast<const double*>(p.rho),
+                        d_params.as<double>(), d_rho.as<double>());
+            }
+            check_launch("gather_accepted_kernel");
+        }
+        d_idx.finish(kept * sizeof(uint64_t));
+        d_params.finish(kept * 3 * real);
+        d_rho.finish(kept * real);
+        VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}

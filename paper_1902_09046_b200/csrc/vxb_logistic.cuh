@@ -1,0 +1,182 @@
+// vxb_logistic.cuh -- device side of the logistic-growth SDE simulator
+// (kernels 2+3 of the hot path): keying, prior draw, Euler-Maruyama path with
+// the summary/distance evaluation fused into the step loop.
+//
+// The model follows the pattern of toggle_switch.cpp: prior box map (:17-22),
+// explicit operation order in the update (:46-62), variates addressed by a
+// canonical layout in counter space (toggle_switch.hpp:52-57).  Relative to a
+// row's base position: positions 0..2 are the prior uniforms, the counter is
+// aligned to even (abc.cpp:53), and position 4+j is the normal of step j+1.
+#pragma once
+
+#include "vxb_rng.cuh"
+
+#define VXB_MAX_SUMMARY 128
+
+namespace vxb {
+
+enum { kKeyParticle = 0, kKeyWorker = 1, kKeyFixed = 2 };
+
+struct Keying {
+    int mode;
+    uint64_t seed_hash;    // splitmix64(seed)
+    uint64_t fixed_key;    // kKeyFixed
+    uint64_t fixed_pos;    // kKeyFixed
+    uint64_t base_blocks;  // worker mode: blocks per worker (blocked.cpp:46-47)
+    uint64_t extra_blocks;
+    uint64_t width;       // V
+    uint64_t row_stride;  // stream positions one row consumes
+};
+
+struct LogisticModel {
+    uint32_t steps, obs_stride, n_obs;
+    double dt, sqdt, x0;
+    double lo[3], hi[3];
+};
+
+// Stream key and base counter position of global row `row`.
+__device__ __forceinline__ void locate_row(const Keying& k, uint64_t row, uint64_t& key,
+                                           uint64_t& base) {
+    if (k.mode == kKeyParticle) {
+        key = stream_key(k.seed_hash, row);
+        base = 0;
+    } else if (k.mode == kKeyWorker) {
+        // inverse of partition(n, P, V) (blocked.cpp:34-63): the first `extra`
+        // workers own base+1 blocks of V rows, the rest own base blocks.
+        const uint64_t b = row / k.width;
+        const uint64_t big = k.extra_blocks * (k.base_blocks + 1);
+        uint64_t w, first_block;
+        if (b < big) {
+            w = b / (k.base_blocks + 1);
+            first_block = w * (k.base_blocks + 1);
+        } else {
+            w = k.extra_blocks + (b - big) / k.base_blocks;
+            first_block = big + (w - k.extra_blocks) * k.base_blocks;
+        }
+        key = stream_key(k.seed_hash, w);
+        base = (row - first_block * k.width) * k.row_stride;
+    } else {
+        key = k.fixed_key;
+        base = k.fixed_pos;
+    }
+}
+
+// Prior draw (reference RNG): three uniforms at positions base..base+2 mapped
+// onto the box as lo + u*(hi-lo).  base is even.
+__device__ __forceinline__ void draw_prior_ref(const LogisticModel& m, uint64_t key, uint64_t base,
+                                               double* theta) {
+    const Words a = philox2x64(key, base >> 1);
+    const Words b = philox2x64(key, (base >> 1) + 1);
+    const double u0 = to_unit(a.w0), u1 = to_unit(a.w1), u2 = to_unit(b.w0);
+    theta[0] = __dadd_rn(m.lo[0], __dmul_rn(u0, __dsub_rn(m.hi[0], m.lo[0])));
+    theta[1] = __dadd_rn(m.lo[1], __dmul_rn(u1, __dsub_rn(m.hi[1], m.lo[1])));
+    theta[2] = __dadd_rn(m.lo[2], __dmul_rn(u2, __dsub_rn(m.hi[2], m.lo[2])));
+}
+// Prior draw of the throughput generator: Philox4x32 block (0, domain 1).
+__device__ __forceinline__ void draw_prior_fast(const LogisticModel& m, uint64_t key,
+                                                double* theta) {
+    const Words a = philox4x32(key, 0, 1u);
+    const Words b = philox4x32(key, 1, 1u);
+    const double u0 = to_unit(a.w0), u1 = to_unit(a.w1), u2 = to_unit(b.w0);
+    theta[0] = m.lo[0] + u0 * (m.hi[0] - m.lo[0]);
+    theta[1] = m.lo[1] + u1 * (m.hi[1] - m.lo[1]);
+    theta[2] = m.lo[2] + u2 * (m.hi[2] - m.lo[2]);
+}
+
+// ------------------------------------------------------------ noise sources
+// next(z) yields the next kBatch standard normals of the row.
+template <class Real>
+struct RefNoise {  // bit-identical to RngStream::fill_gaussian (rng.cpp:142-164)
+    static constexpr int kBatch = 2;
+    uint64_t key, pair;
+    __device__ __forceinline__ void next(Real* z) {
+        double ze, zo;
+        box_muller<Exact>(philox2x64(key, pair++), ze, zo);
+        z[0] = static_cast<Real>(ze);
+        z[1] = static_cast<Real>(zo);
+    }
+};
+struct FastNoise64 {
+    static constexpr int kBatch = 2;
+    uint64_t key, pair;
+    __device__ __forceinline__ void next(double* z) {
+        box_muller<Fused>(philox4x32(key, pair++, 0u), z[0], z[1]);
+    }
+};
+struct FastNoise32 {
+    static constexpr int kBatch = 4;
+    uint64_t key, pair;
+    __device__ __forceinline__ void next(float* z) {
+        const Words w = philox4x32(key, pair++, 0u);
+        box_muller_f32(static_cast<uint32_t>(w.w0), static_cast<uint32_t>(w.w0 >> 32), z[0], z[1]);
+        box_muller_f32(static_cast<uint32_t>(w.w1), static_cast<uint32_t>(w.w1 >> 32), z[2], z[3]);
+    }
+};
+template <class Real>
+struct ExternalNoise {
+    static constexpr int kBatch = 2;
+    const Real* row;
+    uint32_t j, steps;
+    __device__ __forceinline__ void next(Real* z) {
+        z[0] = j < steps ? row[j] : Real(0);
+        z[1] = j + 1 < steps ? row[j + 1] : Real(0);
+        j += 2;
+    }
+};
+
+// One Euler-Maruyama step:  x + (a x)(1 - x/K) + (c x) z  with a = r dt,
+// c = sigma sqrt(dt), 1/K hoisted; evaluated ((x + drift) + diffusion).
+template <class Real, class A>
+__device__ __forceinline__ Real logistic_step(Real x, Real a, Real c, Real inv_k, Real z) {
+    if (A::kExact) {
+        const Real drift = A::mul(A::mul(a, x), A::sub(Real(1), A::mul(x, inv_k)));
+        const Real diff = A::mul(A::mul(c, x), z);
+        return A::add(A::add(x, drift), diff);
+    } else {
+        const Real sat = A::mad(-x, inv_k, Real(1));
+        return A::mad(A::mul(c, x), z, A::mad(A::mul(a, x), sat, x));
+    }
+}
+
+// Runs one path; returns rho (NaN if the state left the reals).  Summaries are
+// written through `emit(k, value)` as they are produced, so the trajectory never
+// leaves registers; the squared distance accumulates left to right in
+// observation order (abc.cpp:16-24).
+template <class Real, class A, class Noise, class Emit>
+__device__ __forceinline__ Real logistic_path(const LogisticModel& m, const double* theta,
+                                              const double* __restrict__ observed, Noise& noise,
+                                              Emit&& emit, bool& bad) {
+    const Real r = static_cast<Real>(theta[0]);
+    const Real k = static_cast<Real>(theta[1]);
+    const Real sigma = static_cast<Real>(theta[2]);
+    const Real a = Exact::mul(r, static_cast<Real>(m.dt));
+    const Real c = Exact::mul(sigma, static_cast<Real>(m.sqdt));
+    const Real inv_k = Exact::div(Real(1), k);
+    Real x = static_cast<Real>(m.x0);
+    Real ss = 0;
+    uint32_t next = 0, since = 0;
+    bad = false;
+    for (uint32_t j = 0; j < m.steps; j += Noise::kBatch) {
+        Real z[Noise::kBatch];
+        noise.next(z);
+#pragma unroll
+        for (int q = 0; q < Noise::kBatch; ++q) {
+            if (j + q < m.steps) {
+                x = logistic_step<Real, A>(x, a, c, inv_k, z[q]);
+                if (++since == m.obs_stride) {
+                    since = 0;
+                    if (next < m.n_obs) {
+                        const Real d = A::sub(x, static_cast<Real>(observed[next]));
+                        ss = A::mad(d, d, ss);
+                        bad = bad || !isfinite(x);
+                        emit(next, x);
+                        ++next;
+                    }
+                }
+            }
+        }
+    }
+    return Exact::sqrt(ss);
+}
+
+}  // namespace vxb

@@ -1,0 +1,482 @@
+// vxb_select.cu -- epsilon selection and accepted-row compaction (kernel 4).
+//
+// Replaces the single-threaded tail of the reference ABC sampler,
+// abc::select_epsilon (abc.cpp:75-97): std::sort of all discrepancies, type-7
+// quantile (numeric.cpp:20-30), ceil(q n) guard, ascending scan for rho <= eps.
+// On the device no sort is needed:
+//   * the two or three order statistics the quantile rule reads are found by a
+//     most-significant-digit radix select (11-bit digits, shared-memory
+//     histograms, digit choice on the device so the passes queue without host
+//     round trips) -- exact, so epsilon is bit-identical to the sorted answer;
+//   * accepted rows are compacted by warp ballot + block prefix sums with the
+//     block offsets taken from a scan (not from atomics), which yields the
+//     ascending row order of abc.cpp:93-95 deterministically.
+// Both are HBM-bound streaming passes over rho (8 B/row per pass).
+
+#include <cmath>
+#include <limits>
+
+#include "vxb_common.cuh"
+
+namespace vxb {
+
+constexpr int kDigitBits = 11;
+constexpr int kBins = 1 << kDigitBits;
+constexpr int kMaxRanks = 4;
+constexpr int kSelBlock = 256;
+constexpr int kSelItems = 16;  // rows per thread per block tile
+
+// Monotone map of a real to an unsigned key (total order of the reals).
+__device__ __forceinline__ uint64_t order_key(double v) {
+    const uint64_t b = static_cast<uint64_t>(__double_as_longlong(v));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ uint64_t order_key(float v) {
+    const uint32_t b = __float_as_uint(v);
+    const uint32_t k = (b >> 31) ? ~b : (b | 0x80000000u);
+    return static_cast<uint64_t>(k) << 32;  // high half so the digit schedule is shared
+}
+__host__ inline double key_to_double(uint64_t k) {
+    const uint64_t b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFULL) : ~k;
+    double v;
+    memcpy(&v, &b, 8);
+    return v;
+}
+__host__ inline float key_to_float(uint64_t k64) {
+    const uint32_t k = static_cast<uint32_t>(k64 >> 32);
+    const uint32_t b = (k >> 31) ? (k & 0x7FFFFFFFu) : ~k;
+    float v;
+    memcpy(&v, &b, 4);
+    return v;
+}
+
+template <class Real>
+__device__ __forceinline__ bool row_valid(const Real* rho, const uint8_t* failed, uint64_t i) {
+    return !(failed && failed[i]) && !isnan(rho[i]);
+}
+
+struct SelectState {
+    uint64_t prefix[kMaxRanks];     // digits fixed so far (high bits)
+    uint64_t remaining[kMaxRanks];  // rank inside the current bucket
+    uint64_t n_valid;
+};
+
+template <class Real>
+__global__ void count_valid_kernel(const Real* __restrict__ rho,
+                                   const uint8_t* __restrict__ failed, uint64_t n,
+                                   unsigned long long* out) {
+    uint64_t c = 0;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        c += row_valid(rho, failed, i) ? 1 : 0;
+    for (int o = 16; o; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, static_cast<unsigned long long>(c));
+}
+
+// One digit pass: histogram of the digit at `shift` over the rows whose higher
+// digits equal the rank's prefix.
+template <class Real>
+__global__ void __launch_bounds__(kSelBlock)
+radix_hist_kernel(const Real* __restrict__ rho, const uint8_t* __restrict__ failed, uint64_t n,
+                  int shift, int bits, int n_ranks, const SelectState* __restrict__ state,
+                  unsigned int* __restrict__ hist /* n_ranks x kBins */) {
+    __shared__ unsigned int sh[kMaxRanks * kBins];
+    for (int i = threadIdx.x; i < n_ranks * kBins; i += kSelBlock) sh[i] = 0;
+    __syncthreads();
+    uint64_t prefix[kMaxRanks];
+    for (int q = 0; q < n_ranks; ++q) prefix[q] = state->prefix[q];
+    const int hi_shift = shift + bits;  // bits above the current digit
+    const uint64_t mask = (1ull << bits) - 1;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kSelBlock + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * kSelBlock) {
+        if (!row_valid(rho, failed, i)) continue;
+        const uint64_t key = order_key(rho[i]);
+        const uint64_t high = hi_shift >= 64 ? 0 : (key >> hi_shift);
+        const unsigned digit = static_cast<unsigned>((key >> shift) & mask);
+        for (int q = 0; q < n_ranks; ++q) {
+            const uint64_t want = hi_shift >= 64 ? 0 : (prefix[q] >> hi_shift);
+            if (high == want) atomicAdd(&sh[q * kBins + digit], 1u);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_ranks * kBins; i += kSelBlock)
+        if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+// Picks, for every rank, the bucket holding it; clears the histogram.
+__global__ void radix_pick_kernel(int shift, int bits, int n_ranks, SelectState* state,
+                                  unsigned int* hist) {
+    const int q = blockIdx.x;
+    if (q >= n_ranks) return;
+    __shared__ unsigned int bins[kBins];
+    const int nb = 1 << bits;
+    for (int i = threadIdx.x; i < kBins; i += blockDim.x) {
+        bins[i] = i < nb ? hist[q * kBins + i] : 0;
+        hist[q * kBins + i] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t k = state->remaining[q], run = 0;
+        int chosen = nb - 1;
+        for (int b = 0; b < nb; ++b) {
+            if (k < run + bins[b]) {
+                chosen = b;
+                break;
+            }
+            run += bins[b];
+        }
+        state->remaining[q] = k - run;
+        state->prefix[q] |= static_cast<uint64_t>(chosen) << shift;
+    }
+}
+
+// ---- compaction: tile = kSelBlock*kSelItems consecutive rows per block ----
+template <class Real>
+__device__ __forceinline__ bool row_accepted(const Real* rho, const uint8_t* failed, uint64_t i,
+                                             uint64_t n, double eps) {
+    // compared in double so that an fp32 rho is tested against the unrounded
+    // epsilon, as the host rule does; NaN compares false
+    return i < n && !(failed && failed[i]) && static_cast<double>(rho[i]) <= eps;
+}
+
+template <class Real>
+__global__ void __launch_bounds__(kSelBlock)
+accept_count_kernel(const Real* __restrict__ rho, const uint8_t* __restrict__ failed, uint64_t n,
+                    double eps, unsigned int* __restrict__ block_counts) {
+    const uint64_t tile0 = static_cast<uint64_t>(blockIdx.x) * kSelBlock * kSelItems;
+    unsigned c = 0;
+#pragma unroll 4
+    for (int s = 0; s < kSelItems; ++s)
+        c += row_accepted(rho, failed, tile0 + static_cast<uint64_t>(s) * kSelBlock + threadIdx.x,
+                          n, eps)
+                 ? 1u
+                 : 0u;
+    for (int o = 16; o; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+    __shared__ unsigned int warp_sum[kSelBlock / 32];
+    if ((threadIdx.x & 31) == 0) warp_sum[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned t = 0;
+        for (int w = 0; w < kSelBlock / 32; ++w) t += warp_sum[w];
+        block_counts[blockIdx.x] = t;
+    }
+}
+
+// Exclusive scan of the block counts (one CTA, serial over chunks of 1024).
+__global__ void __launch_bounds__(1024)
+scan_blocks_kernel(const unsigned int* __restrict__ counts, uint64_t n_blocks,
+                   unsigned long long* __restrict__ offsets, unsigned long long* total) {
+    __shared__ unsigned long long warp_tot[32];
+    __shared__ unsigned long long carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (uint64_t c0 = 0; c0 < n_blocks; c0 += 1024) {
+        const uint64_t i = c0 + threadIdx.x;
+        const unsigned long long v = i < n_blocks ? counts[i] : 0;
+        unsigned long long incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+            if ((threadIdx.x & 31) >= o) incl += t;
+        }
+        if ((threadIdx.x & 31) == 31) warp_tot[threadIdx.x >> 5] = incl;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            unsigned long long w = warp_tot[threadIdx.x];
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long t = __shfl_up_sync(0xffffffffu, w, o);
+                if (threadIdx.x >= o) w += t;
+            }
+            warp_tot[threadIdx.x] = w;  // inclusive over warps
+        }
+        __syncthreads();
+        const unsigned long long warp_off = (threadIdx.x >> 5) ? warp_tot[(threadIdx.x >> 5) - 1] : 0;
+        const unsigned long long base = carry;
+        if (i < n_blocks) offsets[i] = base + warp_off + incl - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = base + warp_off + incl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total = carry;
+}
+
+template <class Real>
+__global__ void __launch_bounds__(kSelBlock)
+accept_write_kernel(const Real* __restrict__ rho, const uint8_t* __restrict__ failed, uint64_t n,
+                    double eps, const unsigned long long* __restrict__ offsets, uint64_t index_base,
+                    uint64_t cap, uint64_t* __restrict__ idx) {
+    __shared__ unsigned int warp_cnt[kSelBlock / 32];
+    __shared__ unsigned long long run;
+    const uint64_t tile0 = static_cast<uint64_t>(blockIdx.x) * kSelBlock * kSelItems;
+    if (threadIdx.x == 0) run = offsets[blockIdx.x];
+    __syncthreads();
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int s = 0; s < kSelItems; ++s) {
+        const uint64_t i = tile0 + static_cast<uint64_t>(s) * kSelBlock + threadIdx.x;
+        const bool acc = row_accepted(rho, failed, i, n, eps);
+        const unsigned ballot = __ballot_sync(0xffffffffu, acc);
+        if (lane == 0) warp_cnt[warp] = __popc(ballot);
+        __syncthreads();
+        unsigned before = 0, total = 0;
+        for (int w = 0; w < kSelBlock / 32; ++w) {
+            const unsigned c = warp_cnt[w];
+            before += w < static_cast<int>(warp) ? c : 0;
+            total += c;
+        }
+        if (acc) {
+            const unsigned long long dst = run + before + __popc(ballot & ((1u << lane) - 1));
+            if (dst < cap) idx[dst] = i + index_base;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) run += total;
+        __syncthreads();
+    }
+}
+
+template <class Real>
+void order_statistics_device(vxb_ctx* ctx, const Real* rho, const uint8_t* failed, uint64_t n,
+                             const uint64_t* ranks, int n_ranks, double* values) {
+    require(n_ranks >= 1 && n_ranks <= kMaxRanks, "invalid-argument", "too many ranks");
+    Scratch d_state(ctx, sizeof(SelectState));
+    Scratch d_hist(ctx, sizeof(unsigned int) * kMaxRanks * kBins);
+    SelectState init{};
+    for (int q = 0; q < n_ranks; ++q) init.remaining[q] = ranks[q];
+    VXB_CUDA(cudaMemcpyAsync(d_state.as<void>(), &init, sizeof(init), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    VXB_CUDA(cudaMemsetAsync(d_hist.as<void>(), 0, sizeof(unsigned int) * kMaxRanks * kBins,
+                             ctx->stream));
+    const int key_bits = sizeof(Real) == 8 ? 64 : 32;
+    const int low = 64 - key_bits;  // float keys live in the high half
+    const unsigned grid = static_cast<unsigned>(
+        std::min<uint64_t>((n + kSelBlock - 1) / kSelBlock,
+                           static_cast<uint64_t>(ctx->prop.multiProcessorCount) * 8));
+    int top = 64;
+    while (top > low) {
+        const int bits = std::min(kDigitBits, top - low);
+        const int shift = top - bits;
+        {
+            LaunchScope scope(ctx, VXB_K_SELECT);
+            radix_hist_kernel<Real><<<grid, kSelBlock, 0, ctx->stream>>>(
+                rho, failed, n, shift, bits, n_ranks, d_state.as<SelectState>(),
+                d_hist.as<unsigned int>());
+            check_launch("radix_hist_kernel");
+        }
+        {
+            LaunchScope scope(ctx, VXB_K_SELECT);
+            radix_pick_kernel<<<n_ranks, 256, 0, ctx->stream>>>(shift, bits, n_ranks,
+                                                                d_state.as<SelectState>(),
+                                                                d_hist.as<unsigned int>());
+            check_launch("radix_pick_kernel");
+        }
+        top = shift;
+    }
+    SelectState fin{};
+    VXB_CUDA(cudaMemcpyAsync(&fin, d_state.as<void>(), sizeof(fin), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int q = 0; q < n_ranks; ++q)
+        values[q] = sizeof(Real) == 8 ? key_to_double(fin.prefix[q])
+                                      : static_cast<double>(key_to_float(fin.prefix[q]));
+}
+
+template <class Real>
+uint64_t count_valid_device(vxb_ctx* ctx, const Real* rho, const uint8_t* failed, uint64_t n) {
+    Scratch d_cnt(ctx, sizeof(unsigned long long));
+    VXB_CUDA(cudaMemsetAsync(d_cnt.as<void>(), 0, sizeof(unsigned long long), ctx->stream));
+    const unsigned grid = static_cast<unsigned>(
+        std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(ctx->prop.multiProcessorCount) * 8));
+    {
+        LaunchScope scope(ctx, VXB_K_SELECT);
+        count_valid_kernel<Real><<<grid, 256, 0, ctx->stream>>>(rho, failed, n,
+                                                               d_cnt.as<unsigned long long>());
+        check_launch("count_valid_kernel");
+    }
+    unsigned long long c = 0;
+    VXB_CUDA(cudaMemcpyAsync(&c, d_cnt.as<void>(), sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
+    VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    return c;
+}
+
+template <class Real>
+void compact_device_t(vxb_ctx* ctx, const Real* rho, const uint8_t* failed, uint64_t n, double eps,
+                      uint64_t index_base, uint64_t cap, uint64_t* n_accepted_host,
+                      uint64_t* idx_dev) {
+    const uint64_t tile = static_cast<uint64_t>(kSelBlock) * kSelItems;
+    const uint64_t n_blocks = (n + tile - 1) / tile;
+    if (n_blocks == 0) {
+        *n_accepted_host = 0;
+        return;
+    }
+    Scratch d_counts(ctx, n_blocks * sizeof(unsigned int));
+    Scratch d_offsets(ctx, n_blocks * sizeof(unsigned long long));
+    Scratch d_total(ctx, sizeof(unsigned long long));
+    {
+        LaunchScope scope(ctx, VXB_K_COMPACT);
+        accept_count_kernel<Real><<<static_cast<unsigned>(n_blocks), kSelBlock, 0, ctx->stream>>>(
+            rho, failed, n, eps, d_counts.as<unsigned int>());
+        check_launch("accept_count_kernel");
+    }
+    {
+        LaunchScope scope(ctx, VXB_K_COMPACT);
+        scan_blocks_kernel<<<1, 1024, 0, ctx->stream>>>(d_counts.as<unsigned int>(), n_blocks,
+                                                        d_offsets.as<unsigned long long>(),
+                                                        d_total.as<unsigned long long>());
+        check_launch("scan_blocks_kernel");
+    }
+    if (idx_dev && cap) {
+        LaunchScope scope(ctx, VXB_K_COMPACT);
+        accept_write_kernel<Real><<<static_cast<unsigned>(n_blocks), kSelBlock, 0, ctx->stream>>>(
+            rho, failed, n, eps, d_offsets.as<unsigned long long>(), index_base, cap, idx_dev);
+        check_launch("accept_write_kernel");
+    }
+    unsigned long long total = 0;
+    VXB_CUDA(cudaMemcpyAsync(&total, d_total.as<void>(), sizeof(total), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    *n_accepted_host = total;
+}
+
+void compact_accepted_device(vxb_ctx* ctx, int precision, const void* rho_dev,
+                             const uint8_t* failed_dev, uint64_t n, double epsilon,
+                             uint64_t index_base, uint64_t cap, uint64_t* n_accepted_host,
+                             uint64_t* idx_dev) {
+    if (precision == VXB_F32)
+        compact_device_t<float>(ctx, static_cast<const float*>(rho_dev), failed_dev, n, epsilon,
+                                index_base, cap, n_accepted_host, idx_dev);
+    else
+        compact_device_t<double>(ctx, static_cast<const double*>(rho_dev), failed_dev, n, epsilon,
+                                 index_base, cap, n_accepted_host, idx_dev);
+}
+
+void order_statistics_any(vxb_ctx* ctx, int precision, const void* rho_dev,
+                          const uint8_t* failed_dev, uint64_t n, const uint64_t* ranks,
+                          int n_ranks, double* values) {
+    if (precision == VXB_F32)
+        order_statistics_device<float>(ctx, static_cast<const float*>(rho_dev), failed_dev, n,
+                                       ranks, n_ranks, values);
+    else
+        order_statistics_device<double>(ctx, static_cast<const double*>(rho_dev), failed_dev, n,
+                                        ranks, n_ranks, values);
+}
+
+uint64_t count_valid_any(vxb_ctx* ctx, int precision, const void* rho_dev,
+                         const uint8_t* failed_dev, uint64_t n) {
+    return precision == VXB_F32
+               ? count_valid_device<float>(ctx, static_cast<const float*>(rho_dev), failed_dev, n)
+               : count_valid_device<double>(ctx, static_cast<const double*>(rho_dev), failed_dev, n);
+}
+
+// The quantile rule of select_epsilon (abc.cpp:85-89 with numeric.cpp:20-30)
+// evaluated on exact order statistics: same operations in the same order as
+// the reference performs on its sorted array.
+double epsilon_from_order_statistics(vxb_ctx* ctx, int precision, const void* rho_dev,
+                                     const uint8_t* failed_dev, uint64_t n, double q) {
+    require(q > 0.0 && q <= 1.0, "invalid-argument", "accept fraction must lie in (0, 1]");
+    const uint64_t nv = count_valid_any(ctx, precision, rho_dev, failed_dev, n);
+    require(nv >= 1, "empty-set", "every prior predictive row failed");
+    uint64_t ranks[3];
+    int nr = 0;
+    double eps;
+    const uint64_t min_accept = static_cast<uint64_t>(std::ceil(q * static_cast<double>(nv)));
+    // quantile_sorted
+    uint64_t lo = 0;
+    double frac = 0.0;
+    int mode;  // 0: single element, 1: last element, 2: interpolate
+    if (nv == 1) {
+        mode = 0;
+        ranks[nr++] = 0;
+    } else {
+        const double h = static_cast<double>(nv - 1) * q;
+        lo = static_cast<uint64_t>(h);
+        if (lo + 1 >= nv) {
+            mode = 1;
+            ranks[nr++] = nv - 1;
+        } else {
+            mode = 2;
+            frac = h - static_cast<double>(lo);
+            ranks[nr++] = lo;
+            ranks[nr++] = lo + 1;
+        }
+    }
+    const int guard_slot = nr;
+    if (min_accept >= 1) ranks[nr++] = min_accept - 1;
+    double v[3];
+    order_statistics_any(ctx, precision, rho_dev, failed_dev, n, ranks, nr, v);
+    if (mode == 2)
+        eps = v[0] + frac * (v[1] - v[0]);
+    else
+        eps = v[0];
+    if (min_accept >= 1 && eps < v[guard_slot]) eps = v[guard_slot];
+    return eps;
+}
+
+}  // namespace vxb
+
+using namespace vxb;
+
+extern "C" int vxb_order_statistics(vxb_ctx* ctx, int precision, const void* rho,
+                                    const uint8_t* failed, uint64_t n, const uint64_t* ranks,
+                                    uint32_t n_ranks, double* values, uint64_t* n_valid) {
+    return guarded([&] {
+        use(ctx);
+        require(rho && ranks && values, "invalid-argument", "null argument");
+        require(n >= 1, "insufficient-data", "order statistic of an empty sample");
+        const size_t real = precision == VXB_F32 ? 4 : 8;
+        Staged d_rho(ctx, rho, n * real, true, false);
+        Staged d_failed(ctx, failed, n, true, false);
+        const uint64_t nv = count_valid_any(ctx, precision, d_rho.ptr(), d_failed.as<uint8_t>(), n);
+        if (n_valid) *n_valid = nv;
+        for (uint32_t q = 0; q < n_ranks; ++q)
+            require(ranks[q] < nv, "invalid-argument", "rank exceeds the number of valid rows");
+        for (uint32_t q0 = 0; q0 < n_ranks; q0 += kMaxRanks) {
+            const int nr = static_cast<int>(std::min<uint32_t>(kMaxRanks, n_ranks - q0));
+            order_statistics_any(ctx, precision, d_rho.ptr(), d_failed.as<uint8_t>(), n, ranks + q0,
+                                 nr, values + q0);
+        }
+    });
+}
+
+extern "C" int vxb_compact_accepted(vxb_ctx* ctx, int precision, const void* rho,
+                                    const uint8_t* failed, uint64_t n, double epsilon,
+                                    uint64_t index_base, uint64_t cap, uint64_t* n_accepted,
+                                    uint64_t* idx) {
+    return guarded([&] {
+        use(ctx);
+        require(rho && n_accepted, "invalid-argument", "null argument");
+        const size_t real = precision == VXB_F32 ? 4 : 8;
+        Staged d_rho(ctx, rho, n * real, true, false);
+        Staged d_failed(ctx, failed, n, true, false);
+        Staged d_idx(ctx, idx, cap * sizeof(uint64_t), false, true);
+        uint64_t total = 0;
+        compact_accepted_device(ctx, precision, d_rho.ptr(), d_failed.as<uint8_t>(), n, epsilon,
+                                index_base, cap, &total, d_idx.as<uint64_t>());
+        *n_accepted = total;
+        d_idx.finish(std::min(total, cap) * sizeof(uint64_t));
+        VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+extern "C" int vxb_select_epsilon(vxb_ctx* ctx, int precision, const void* rho,
+                                  const uint8_t* failed, uint64_t n, double accept_fraction,
+                                  double* epsilon, uint64_t cap, uint64_t* n_accepted,
+                                  uint64_t* idx) {
+    return guarded([&] {
+        use(ctx);
+        require(rho && epsilon && n_accepted, "invalid-argument", "null argument");
+        require(accept_fraction > 0.0 && accept_fraction <= 1.0, "invalid-argument",
+                "accept fraction must lie in (0, 1]");
+        require(n >= 1, "empty-set", "every prior predictive row failed");
+        const size_t real = precision == VXB_F32 ? 4 : 8;
+        Staged d_rho(ctx, rho, n * real, true, false);
+        Staged d_failed(ctx, failed, n, true, false);
+        const double eps = epsilon_from_order_statistics(ctx, precision, d_rho.ptr(),
+                                                         d_failed.as<uint8_t>(), n, accept_fraction);
+        *epsilon = eps;
+        Staged d_idx(ctx, idx, cap * sizeof(uint64_t), false, true);
+        uint64_t total = 0;
+        compact_accepted_device(ctx, precision, d_rho.ptr(), d_failed.as<uint8_t>(), n, eps, 0, cap,
+                                &total, d_idx.as<uint64_t>());
+        *n_accepted = total;
+        d_idx.finish(std::min(total, cap) * sizeof(uint64_t));
+        VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}

@@ -1,0 +1,353 @@
+"""ctypes binding of libvexbayes_cuda.so -- the Python face of the C ABI.
+
+Thin by design: every method forwards to one ``vxb_*`` entry point of
+include/vexbayes_cuda.h, passing numpy arrays (host buffers), torch CUDA
+tensors or raw device pointers straight through.  There is no CPU fallback: if
+the shared object or a CUDA device is missing, loading / ``Context()`` raises.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import _abi as A
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libvexbayes_cuda.so")
+
+u64, u32, f64, i32 = C.c_uint64, C.c_uint32, C.c_double, C.c_int32
+P = C.c_void_p
+_lib = None
+
+
+class VxbError(RuntimeError):
+    """Mirror of vexbayes::Error (errors.hpp:11-28): ``code`` + message."""
+
+    def __init__(self, text):
+        super().__init__(text)
+        self.code = text.split(":", 1)[0]
+
+
+def load():
+    """Load the CUDA library (built in-tree by paper_1902_09046_b200.build)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise FileNotFoundError(
+                f"{LIB_PATH} is missing: run `python -m paper_1902_09046_b200.build` "
+                "(there is no CPU fallback)")
+        _lib = C.CDLL(LIB_PATH)
+        _lib.vxb_last_error.restype = C.c_char_p
+        _lib.vxb_stream.restype = P
+        _lib.vxb_stream.argtypes = [P]
+        _lib.vxb_splitmix64.restype = u64
+        _lib.vxb_splitmix64.argtypes = [u64]
+        _lib.vxb_derive_seed.restype = u64
+        _lib.vxb_derive_seed.argtypes = [u64, P, C.c_size_t]
+    return _lib
+
+
+def _ptr(a):
+    """numpy array / torch tensor / int address / None -> c_void_p."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.flags["C_CONTIGUOUS"], "buffers must be contiguous"
+        return C.c_void_p(a.ctypes.data)
+    if hasattr(a, "data_ptr"):  # torch tensor (host or device)
+        assert a.is_contiguous()
+        return C.c_void_p(a.data_ptr())
+    return C.c_void_p(int(a))
+
+
+def splitmix64(z):
+    return int(load().vxb_splitmix64(z))
+
+
+def derive_seed(seed, path):
+    a = np.asarray(path, dtype=np.uint64)
+    return int(load().vxb_derive_seed(seed, _ptr(a), len(a)))
+
+
+def partition(total, workers, block_width):
+    r = np.zeros((workers, 2), dtype=np.uint64)
+    rc = load().vxb_partition(u64(total), u64(workers), u64(block_width), _ptr(r))
+    if rc:
+        raise VxbError(load().vxb_last_error().decode())
+    return r
+
+
+class Context:
+    """One GPU, one stream (vxb_ctx)."""
+
+    def __init__(self, device=-1):
+        self.lib = load()
+        self.handle = P()
+        self._check(self.lib.vxb_init(C.byref(self.handle), i32(device)))
+
+    def _check(self, rc):
+        if rc != 0:
+            raise VxbError(self.lib.vxb_last_error().decode())
+
+    def close(self):
+        if self.handle:
+            self.lib.vxb_shutdown(self.handle)
+            self.handle = P()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- plumbing
+    def device_info(self):
+        out = A.vxb_device_props()
+        self._check(self.lib.vxb_device_info(self.handle, C.byref(out)))
+        return dict(device=out.device, sm_count=out.sm_count, cc=(out.cc_major, out.cc_minor),
+                    clock_khz=out.clock_khz, global_mem=out.global_mem, name=out.name.decode())
+
+    def stream(self):
+        return self.lib.vxb_stream(self.handle)
+
+    def synchronize(self):
+        self._check(self.lib.vxb_synchronize(self.handle))
+
+    def profile_enable(self, on=True):
+        self._check(self.lib.vxb_profile_enable(self.handle, i32(1 if on else 0)))
+
+    def profile_reset(self):
+        self._check(self.lib.vxb_profile_reset(self.handle))
+
+    def profile_read(self):
+        out = A.vxb_profile()
+        self._check(self.lib.vxb_profile_read(self.handle, C.byref(out)))
+        return {name: dict(launches=int(out.launches[i]), total_ms=float(out.total_ms[i]))
+                for i, name in enumerate(A.VXB_K_NAMES)}
+
+    def device_alloc(self, nbytes):
+        out = P()
+        self._check(self.lib.vxb_device_alloc(self.handle, C.c_size_t(nbytes), C.byref(out)))
+        return out.value
+
+    def device_free(self, p):
+        self._check(self.lib.vxb_device_free(self.handle, P(p)))
+
+    def copy(self, dst, src, nbytes):
+        self._check(self.lib.vxb_copy(self.handle, _ptr(dst), _ptr(src), C.c_size_t(nbytes)))
+
+    # ---- substrate
+    def rng_fill_u64(self, seed, stream_id, pos, n):
+        out = np.zeros(n, dtype=np.uint64)
+        self._check(self.lib.vxb_rng_fill_u64(self.handle, u64(seed), u32(stream_id), u64(pos),
+                                              u64(n), _ptr(out)))
+        return out
+
+    def rng_fill_uniform(self, seed, stream_id, pos, n, a=0.0, b=1.0):
+        out = np.zeros(n)
+        self._check(self.lib.vxb_rng_fill_uniform(self.handle, u64(seed), u32(stream_id), u64(pos),
+                                                  u64(n), f64(a), f64(b), _ptr(out)))
+        return out
+
+    def rng_fill_gaussian(self, seed, stream_id, pos, n, mu=0.0, sigma=1.0):
+        out = np.zeros(n)
+        self._check(self.lib.vxb_rng_fill_gaussian(self.handle, u64(seed), u32(stream_id),
+                                                   u64(pos), u64(n), f64(mu), f64(sigma),
+                                                   _ptr(out)))
+        return out
+
+    def fastmath(self, fn, x, y=None):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.float64) if y is not None else None
+        out = np.zeros_like(x)
+        self._check(self.lib.vxb_fastmath_eval(self.handle, i32(fn), _ptr(x), _ptr(y), u64(x.size),
+                                               _ptr(out)))
+        return out
+
+    # ---- ABC
+    def abc_prior_predictive(self, model, key, n_total, first, count, observed, params=None,
+                             summaries=None, rho=None, failed=None, noise=None):
+        """Raw form: every buffer is caller-supplied (numpy / torch / address)."""
+        obs = np.ascontiguousarray(observed, dtype=np.float64)
+        self._check(self.lib.vxb_abc_prior_predictive(
+            self.handle, C.byref(model), C.byref(key), u64(n_total), u64(first), u64(count),
+            _ptr(obs), _ptr(params), _ptr(summaries), _ptr(rho), _ptr(failed), _ptr(noise)))
+
+    def abc_prior_predictive_host(self, model, key, n_total, first, count, observed, noise=None,
+                                  want_summaries=True):
+        """Convenience form returning numpy arrays (params, summaries, rho, failed)."""
+        dt = np.float32 if model.precision == A.VXB_F32 else np.float64
+        params = np.zeros((count, model.dim), dtype=dt)
+        summ = np.zeros((count, model.summary_dim), dtype=dt) if want_summaries else None
+        rho = np.zeros(count, dtype=dt)
+        failed = np.zeros(count, dtype=np.uint8)
+        if noise is not None:
+            noise = np.ascontiguousarray(noise, dtype=dt)
+        self.abc_prior_predictive(model, key, n_total, first, count, observed, params, summ, rho,
+                                  failed, noise)
+        return params, summ, rho, failed
+
+    def simulate_at(self, model, theta, seed, stream_id, pos):
+        dt = np.float32 if model.precision == A.VXB_F32 else np.float64
+        th = np.ascontiguousarray(theta, dtype=np.float64)
+        out = np.zeros(model.summary_dim, dtype=dt)
+        self._check(self.lib.vxb_simulate_at(self.handle, C.byref(model), _ptr(th), u64(seed),
+                                             u32(stream_id), u64(pos), _ptr(out)))
+        return out
+
+    def select_epsilon(self, rho, failed, q, cap=None, precision=None, n=None, idx=None):
+        if isinstance(rho, np.ndarray):
+            n = rho.size
+            precision = A.VXB_F32 if rho.dtype == np.float32 else A.VXB_F64
+        cap = n if cap is None else cap
+        if idx is None:
+            idx = np.zeros(cap, dtype=np.uint64)
+        eps, nacc = f64(), u64()
+        self._check(self.lib.vxb_select_epsilon(self.handle, i32(precision), _ptr(rho),
+                                                _ptr(failed), u64(n), f64(q), C.byref(eps),
+                                                u64(cap), C.byref(nacc), _ptr(idx)))
+        k = min(nacc.value, cap)
+        return eps.value, (idx[:k] if isinstance(idx, np.ndarray) else idx), nacc.value
+
+    def order_statistics(self, rho, failed, ranks, precision=None, n=None):
+        if isinstance(rho, np.ndarray):
+            n = rho.size
+            precision = A.VXB_F32 if rho.dtype == np.float32 else A.VXB_F64
+        ranks = np.ascontiguousarray(ranks, dtype=np.uint64)
+        vals = np.zeros(ranks.size)
+        nv = u64()
+        self._check(self.lib.vxb_order_statistics(self.handle, i32(precision), _ptr(rho),
+                                                  _ptr(failed), u64(n), _ptr(ranks),
+                                                  u32(ranks.size), _ptr(vals), C.byref(nv)))
+        return vals, nv.value
+
+    def compact_accepted(self, rho, failed, eps, index_base=0, cap=None, precision=None, n=None,
+                         idx=None):
+        if isinstance(rho, np.ndarray):
+            n = rho.size
+            precision = A.VXB_F32 if rho.dtype == np.float32 else A.VXB_F64
+        cap = n if cap is None else cap
+        if idx is None:
+            idx = np.zeros(cap, dtype=np.uint64)
+        nacc = u64()
+        self._check(self.lib.vxb_compact_accepted(self.handle, i32(precision), _ptr(rho),
+                                                  _ptr(failed), u64(n), f64(eps), u64(index_base),
+                                                  u64(cap), C.byref(nacc), _ptr(idx)))
+        k = min(nacc.value, cap)
+        return (idx[:k] if isinstance(idx, np.ndarray) else idx), nacc.value
+
+    def abc_reject(self, model, key, n_total, first, count, observed, eps, cap, idx=None,
+                   params=None, rho=None):
+        """Fused fixed-epsilon rejection; host numpy outputs unless buffers are given."""
+        obs = np.ascontiguousarray(observed, dtype=np.float64)
+        dt = np.float32 if model.precision == A.VXB_F32 else np.float64
+        own = idx is None
+        if own:
+            idx = np.zeros(cap, dtype=np.uint64)
+            params = np.zeros((cap, model.dim), dtype=dt)
+            rho = np.zeros(cap, dtype=dt)
+        nacc = u64()
+        self._check(self.lib.vxb_abc_reject(self.handle, C.byref(model), C.byref(key),
+                                            u64(n_total), u64(first), u64(count), _ptr(obs),
+                                            f64(eps), u64(cap), C.byref(nacc), _ptr(idx),
+                                            _ptr(params), _ptr(rho)))
+        k = min(nacc.value, cap)
+        if own:
+            return nacc.value, idx[:k], params[:k], rho[:k]
+        return nacc.value, idx, params, rho
+
+    # ---- p-values
+    def ppp_pvalues(self, model, lam, log_norm, m_total, first, count, seed, ybar_obs,
+                    want_ybar=False):
+        lam = np.ascontiguousarray(lam, dtype=np.float64)
+        ln = np.ascontiguousarray(log_norm, dtype=np.float64)
+        counts = np.zeros(lam.size, dtype=np.uint64)
+        pv = np.zeros(lam.size)
+        yb = np.zeros((lam.size, count)) if want_ybar else None
+        self._check(self.lib.vxb_ppp_pvalues(self.handle, C.byref(model), _ptr(lam), _ptr(ln),
+                                             u32(lam.size), u64(m_total), u64(first), u64(count),
+                                             u64(seed), f64(ybar_obs), _ptr(counts), _ptr(pv),
+                                             _ptr(yb)))
+        return counts, pv, yb
+
+    # ---- SMC pieces
+    def ess(self, log_w):
+        lw = np.ascontiguousarray(log_w, dtype=np.float64)
+        out = f64()
+        self._check(self.lib.vxb_ess(self.handle, _ptr(lw), u64(lw.size), C.byref(out)))
+        return out.value
+
+    def logsumexp(self, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        out = f64()
+        self._check(self.lib.vxb_logsumexp(self.handle, _ptr(x), u64(x.size), C.byref(out)))
+        return out.value
+
+    def resample_multinomial(self, log_w, particles, seed, stream_id):
+        lw = np.ascontiguousarray(log_w, dtype=np.float64)
+        p = np.ascontiguousarray(particles, dtype=np.float64)
+        n, d = p.shape
+        out = np.zeros_like(p)
+        anc = np.zeros(n, dtype=np.uint64)
+        self._check(self.lib.vxb_resample_multinomial(self.handle, u64(n), u32(d), _ptr(lw),
+                                                      _ptr(p), u64(seed), u32(stream_id),
+                                                      _ptr(out), _ptr(anc)))
+        return out, anc
+
+    def abcsmc_propose(self, model, seed, gen, first, count, theta_prev, cum_prev, chol, observed,
+                       eps):
+        tp = np.ascontiguousarray(theta_prev, dtype=np.float64)
+        cp = np.ascontiguousarray(cum_prev, dtype=np.float64)
+        ch = np.ascontiguousarray(chol, dtype=np.float64)
+        obs = np.ascontiguousarray(observed, dtype=np.float64)
+        th = np.zeros((count, model.dim))
+        rho = np.zeros(count)
+        flag = np.zeros(count, dtype=np.uint8)
+        self._check(self.lib.vxb_abcsmc_propose(self.handle, C.byref(model), u64(seed), u32(gen),
+                                                u64(first), u64(count), u64(tp.shape[0]), _ptr(tp),
+                                                _ptr(cp), _ptr(ch), _ptr(obs), f64(eps), _ptr(th),
+                                                _ptr(rho), _ptr(flag)))
+        return th, rho, flag
+
+    def abcsmc_weights(self, theta_new, theta_prev, w_prev, chol):
+        tn = np.ascontiguousarray(theta_new, dtype=np.float64)
+        tp = np.ascontiguousarray(theta_prev, dtype=np.float64)
+        wp = np.ascontiguousarray(w_prev, dtype=np.float64)
+        ch = np.ascontiguousarray(chol, dtype=np.float64)
+        out = np.zeros(tn.shape[0])
+        self._check(self.lib.vxb_abcsmc_weights(self.handle, u32(tn.shape[1]), u64(tn.shape[0]),
+                                                _ptr(tn), u64(tp.shape[0]), _ptr(tp), _ptr(wp),
+                                                _ptr(ch), _ptr(out)))
+        return out
+
+    def abcsmc_run(self, model, cfg, observed):
+        n, g, d = cfg.particles, cfg.generations, model.dim
+        obs = np.ascontiguousarray(observed, dtype=np.float64)
+        res = dict(theta=np.zeros((n, d)), weight=np.zeros(n), rho=np.zeros(n),
+                   epsilon=np.zeros(g), ess=np.zeros(g), accept_rate=np.zeros(g),
+                   proposals=np.zeros(g, dtype=np.uint64), mean=np.zeros((g, d)),
+                   cov=np.zeros((g, d, d)))
+        out = A.vxb_abcsmc_out(*[res[k].ctypes.data for k in
+                                 ("theta", "weight", "rho", "epsilon", "ess", "accept_rate",
+                                  "proposals", "mean", "cov")])
+        self._check(self.lib.vxb_abcsmc_run(self.handle, C.byref(model), C.byref(cfg), _ptr(obs),
+                                            C.byref(out)))
+        return res
+
+    # ---- tau-leap
+    def mlmc_level(self, model, cfg, level, first, count, want_y=False):
+        sums = np.zeros(4, dtype=np.int64)
+        y = np.zeros(count, dtype=np.int32) if want_y else None
+        self._check(self.lib.vxb_mlmc_level(self.handle, C.byref(model), C.byref(cfg), u32(level),
+                                            u64(first), u64(count), _ptr(sums), _ptr(y)))
+        return sums, y
+
+    def mlmc_tauleap(self, model, cfg):
+        L = cfg.levels
+        res = dict(level_mean=np.zeros(L), level_var=np.zeros(L), level_cost=np.zeros(L))
+        out = A.vxb_mlmc_out(res["level_mean"].ctypes.data, res["level_var"].ctypes.data,
+                             res["level_cost"].ctypes.data, 0.0, 0.0)
+        self._check(self.lib.vxb_mlmc_tauleap(self.handle, C.byref(model), C.byref(cfg),
+                                              C.byref(out)))
+        res["estimate"], res["std_error"] = out.estimate, out.std_error
+        return res

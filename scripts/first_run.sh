@@ -1,0 +1,5 @@
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv
+nproc
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -5
+python -m pytest tests -m gpu -x -q 2>&1 | tail -30

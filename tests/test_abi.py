@@ -1,0 +1,76 @@
+"""CPU tests of the drop-in boundary: the C-ABI library loads and exports every
+symbol include/vexbayes_cuda.h declares; the ctypes mirror matches the header;
+host-only entry points (no GPU needed) behave like the reference."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1902_09046_b200 import _abi as A, build, lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "vexbayes_cuda.h")
+
+
+@pytest.fixture(scope="module")
+def so():
+    build.build_library()  # nvcc cross-compiles sm_100a without a GPU
+    return lib.load()
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(vxb_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_and_python_mirror_agree():
+    assert declared_functions() == sorted(A.EXPORTED_SYMBOLS)
+    text = open(HEADER).read()
+    assert f"#define VXB_ABI_VERSION {A.VXB_ABI_VERSION}" in text
+    # struct sizes follow from the header's field lists
+    assert ctypes.sizeof(A.vxb_model) == 4 * 4 + 4 * 4 + 2 * 8 + 8 * 8 + 8 * 8 + 16 * 8
+    assert ctypes.sizeof(A.vxb_keying) == 24
+    assert ctypes.sizeof(A.vxb_abcsmc_cfg) == 64
+    assert ctypes.sizeof(A.vxb_mlmc_cfg) == 40
+    assert ctypes.sizeof(A.vxb_profile) == 16 * A.VXB_K_COUNT
+
+
+def test_library_exports_every_declared_symbol(so):
+    for name in declared_functions():
+        assert hasattr(so, name), f"libvexbayes_cuda.so does not export {name}"
+    assert so.vxb_abi_version() == A.VXB_ABI_VERSION
+
+
+def test_host_side_entry_points(so, oracle, golden):
+    assert lib.splitmix64(0) == 0xE220A8397B1DCDAF
+    assert lib.derive_seed(42, [1, 2, 3]) == 0x3FB96077DA5807FD
+    assert lib.derive_seed(1, [90]) == oracle.derive_seed(1, [90])
+    assert np.array_equal(lib.partition(8064, 16, 4), golden["partition_8064_16_4"])
+    assert np.array_equal(lib.partition(1003, 7, 8), golden["partition_1003_7_8"])
+    for total, workers, width in [(5, 9, 1), (100, 3, 16), (17, 4, 4), (1, 1, 1)]:
+        assert np.array_equal(lib.partition(total, workers, width), oracle.partition(total, workers, width))
+    with pytest.raises(lib.VxbError) as e:
+        lib.partition(0, 1, 1)
+    assert e.value.code == "invalid-shape"
+
+
+def test_no_cpu_fallback_without_gpu(so):
+    """vxb_init must fail loudly (device-error) when no CUDA device exists."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(lib.VxbError) as e:
+        lib.Context(0)
+    assert e.value.code == "device-error"
+
+
+def test_product_package_never_imports_the_oracle():
+    pkg = os.path.join(ROOT, "paper_1902_09046_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".hpp", ".cpp", ".h")):
+                text = open(os.path.join(dirpath, f), errors="ignore").read()
+                assert "pyoracle" not in text and "vxb_oracle" not in text and "libvxb_ref" not in text, f

@@ -1,0 +1,277 @@
+"""GPU parity tests (through the C ABI): RNG substrate, fused logistic ABC
+kernel, epsilon selection and compaction, against the oracle and the golden
+vectors of the unmodified reference.  Bar: bit-exact in the exact modes."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_1902_09046_b200 import _abi as A, lib, models as M
+
+pytestmark = pytest.mark.gpu
+
+
+def eq(a, b):
+    return np.array_equal(np.asarray(a), np.asarray(b), equal_nan=True)
+
+
+# ---------------------------------------------------------------- kernel 1
+def test_rng_known_answers_on_device(ctx, golden):
+    w = ctx.rng_fill_u64(1337, 0, 0, 64)
+    assert [hex(x) for x in w[:4]] == ["0xfe78345bef749875", "0x77013bd4b5221611",
+                                       "0xa5f809b9395f05e5", "0x66b9e7b9a087a139"]
+    assert eq(w, golden["words_1337_0"])
+    assert eq(ctx.rng_fill_u64(7, 3, 1001, 33), golden["words_7_3_pos1001"])
+    g = ctx.rng_fill_gaussian(1337, 0, 0, 64)
+    assert [repr(float(x)) for x in g[:4]] == ["-3.1222123110592097", "0.7007283101377776",
+                                               "-1.1763603487266563", "0.8403694724866424"]
+    assert eq(g, golden["gauss_1337_0"])
+    assert eq(ctx.rng_fill_gaussian(555, 9, 13, 41, 1.5, 2.0), golden["gauss_555_9_pos13"])
+    assert eq(ctx.rng_fill_uniform(4242, 1, 0, 64, 250.0, 400.0), golden["unif_4242_1"])
+    assert eq(ctx.rng_fill_uniform(4242, 1, 5, 64, 1e16, 1e16 + 4.0), golden["unif_big"])
+
+
+def test_rng_bulk_matches_oracle(ctx, oracle):
+    for seed, sid, pos, n in [(1, 0, 0, 100001), (20240518, 1, 12345678901, 4097), (99, 4000000000, 3, 31)]:
+        assert eq(ctx.rng_fill_u64(seed, sid, pos, n), oracle.stream_u64(seed, sid, pos, n))
+        assert eq(ctx.rng_fill_gaussian(seed, sid, pos, n, -1.0, 0.5), oracle.fill_gaussian(seed, sid, pos, n, -1.0, 0.5))
+        assert eq(ctx.rng_fill_uniform(seed, sid, pos, n, -3.0, 7.5), oracle.fill_uniform(seed, sid, pos, n, -3.0, 7.5))
+
+
+def test_rng_properties_on_device(ctx):
+    # purity in the counter (test_rng.cpp:120-156)
+    whole = ctx.rng_fill_gaussian(777, 5, 0, 40)
+    assert eq(np.concatenate([ctx.rng_fill_gaussian(777, 5, 0, 16), ctx.rng_fill_gaussian(777, 5, 16, 24)]), whole)
+    assert ctx.rng_fill_gaussian(777, 5, 21, 1)[0] == whole[21]
+    assert ctx.rng_fill_gaussian(777, 5, 20, 1)[0] == whole[20]
+    # degenerate range / zero sigma exact (:51-56, :85-89), half-open (:68-77)
+    assert (ctx.rng_fill_uniform(7, 3, 0, 100, 3.0, 3.0) == 3.0).all()
+    assert (ctx.rng_fill_gaussian(8, 0, 0, 100, 5.0, 0.0) == 5.0).all()
+    u = ctx.rng_fill_uniform(4242, 1, 0, 4096, 1e16, 1e16 + 4.0)
+    assert u.min() >= 1e16 and u.max() < 1e16 + 4.0
+    # error codes (:79-83, :112-118)
+    with pytest.raises(lib.VxbError) as e:
+        ctx.rng_fill_uniform(1, 1, 0, 4, 2.0, 1.0)
+    assert e.value.code == "invalid-range"
+    with pytest.raises(lib.VxbError) as e:
+        ctx.rng_fill_gaussian(0, 0, 0, 4, 0.0, -1.0)
+    assert e.value.code == "invalid-scale"
+    # moments (:58-66, :91-101)
+    assert abs(ctx.rng_fill_uniform(99, 0, 0, 100000).mean() - 0.5) < 0.005
+    assert abs(ctx.rng_fill_gaussian(31337, 2, 0, 100000).var(ddof=1) - 1.0) < 0.03
+
+
+def test_fastmath_on_device(ctx, oracle, golden):
+    assert eq(ctx.fastmath(0, golden["fm_x_log"]), golden["fm_log2"])
+    assert eq(ctx.fastmath(1, golden["fm_x_log"]), golden["fm_ln"])
+    assert eq(ctx.fastmath(2, golden["fm_x_exp"]), golden["fm_exp2"])
+    assert eq(ctx.fastmath(3, golden["fm_x_ang"]), golden["fm_sinpi"])
+    assert eq(ctx.fastmath(4, golden["fm_x_ang"]), golden["fm_cospi"])
+    assert eq(ctx.fastmath(5, golden["fm_pow_b"], golden["fm_pow_e"]), golden["fm_pow"])
+    rs = np.random.RandomState(11)
+    x = np.exp(rs.uniform(-700, 700, 200000))
+    assert eq(ctx.fastmath(1, x), oracle.fastmath(1, x))
+    z = rs.uniform(-1100, 1100, 200000)
+    assert eq(ctx.fastmath(2, z), oracle.fastmath(2, z))
+    a = rs.uniform(-4, 4, 200000)
+    assert eq(ctx.fastmath(3, a), oracle.fastmath(3, a))
+    assert eq(ctx.fastmath(4, a), oracle.fastmath(4, a))
+    b, e = rs.uniform(1, 2000, 200000), rs.uniform(-8, 8, 200000)
+    assert eq(ctx.fastmath(5, b, e), oracle.fastmath(5, b, e))
+
+
+# ------------------------------------------------------------ kernels 2 + 3
+def test_logistic_abc_golden_on_device(ctx, golden):
+    m = M.logistic_model()
+    obs = ctx.simulate_at(m, [0.5, 100.0, 0.05], lib.derive_seed(1, [90]), 0, 0)
+    assert eq(obs, golden["logistic_observed"])
+    # reference keying: bit-identical to abc::run_prior_predictive(seed, P=3, V=4)
+    p, s, rho, f = ctx.abc_prior_predictive_host(m, M.keying(1337, A.VXB_KEY_WORKER, 3, 4), 96, 0, 96, obs)
+    assert eq(p, golden["abc_w_params"]) and eq(s, golden["abc_w_summ"])
+    assert eq(rho, golden["abc_w_rho"]) and eq(f, golden["abc_w_failed"])
+    p, s, rho, f = ctx.abc_prior_predictive_host(m, M.keying(1337), 5000, 1000, 32, obs)
+    assert eq(p, golden["abc_p_params"]) and eq(s, golden["abc_p_summ"]) and eq(rho, golden["abc_p_rho"])
+    m32 = M.logistic_model(precision=A.VXB_F32)
+    p, s, rho, f = ctx.abc_prior_predictive_host(m32, M.keying(1337), 5000, 1000, 32, obs)
+    assert p.dtype == np.float32
+    assert eq(p, golden["abc32_p_params"]) and eq(s, golden["abc32_p_summ"]) and eq(rho, golden["abc32_p_rho"])
+    p, s, rho, f = ctx.abc_prior_predictive_host(m32, M.keying(7, A.VXB_KEY_WORKER, 2, 1), 48, 0, 48, obs)
+    assert eq(p, golden["abc32_w_params"]) and eq(s, golden["abc32_w_summ"]) and eq(rho, golden["abc32_w_rho"])
+
+
+def test_logistic_edge_cases_on_device(ctx, golden):
+    mo = M.logistic_model(steps=37, obs_stride=5)  # odd horizon, ragged observation grid
+    oo = ctx.simulate_at(mo, [0.5, 100.0, 0.05], 99, 4, 3)
+    assert eq(oo, golden["odd_observed"])
+    p, s, rho, f = ctx.abc_prior_predictive_host(mo, M.keying(11, A.VXB_KEY_WORKER, 4, 2), 50, 0, 50, oo)
+    assert eq(p, golden["odd_w_params"]) and eq(s, golden["odd_w_summ"]) and eq(rho, golden["odd_w_rho"])
+    mb = M.logistic_model(steps=400, obs_stride=100, prior_hi=(4000.0, 150.0, 0.2))  # failing rows
+    p, s, rho, f = ctx.abc_prior_predictive_host(mb, M.keying(21), 64, 0, 64, golden["bad_observed"])
+    assert eq(f, golden["bad_failed"]) and f.any()
+    assert eq(p, golden["bad_params"]) and eq(s, golden["bad_summ"]) and eq(rho, golden["bad_rho"])
+    # argument errors mirror abc.cpp:29-32
+    m = M.logistic_model()
+    with pytest.raises(lib.VxbError) as e:
+        ctx.abc_prior_predictive_host(m, M.keying(1), 0, 0, 0, np.zeros(20))
+    assert e.value.code == "invalid-shape"
+    with pytest.raises(lib.VxbError) as e:
+        ctx.abc_prior_predictive_host(m, M.keying(1, A.VXB_KEY_WORKER, 0, 1), 8, 0, 8, np.zeros(20))
+    assert e.value.code == "invalid-shape"
+    with pytest.raises(lib.VxbError) as e:
+        ctx.abc_prior_predictive_host(m, M.keying(1, A.VXB_KEY_WORKER, 2, 3), 8, 0, 8, np.zeros(20))
+    assert e.value.code == "invalid-shape"
+    bad = M.logistic_model()
+    bad.summary_dim = 19
+    with pytest.raises(lib.VxbError) as e:
+        ctx.abc_prior_predictive_host(bad, M.keying(1), 8, 0, 8, np.zeros(19))
+    assert e.value.code == "invalid-summary"
+    # empty shard is a no-op
+    p, s, rho, f = ctx.abc_prior_predictive_host(m, M.keying(1), 8, 8, 0, np.zeros(20))
+    assert p.shape == (0, 3)
+
+
+@pytest.mark.parametrize("precision", [A.VXB_F64, A.VXB_F32])
+def test_logistic_abc_matches_oracle(ctx, oracle, golden, precision):
+    """20 000 particles, reference-exact RNG on the device, both keyings."""
+    m = M.logistic_model(precision=precision)
+    obs = golden["logistic_observed"]
+    n = 20000
+    got = ctx.abc_prior_predictive_host(m, M.keying(1337), n, 0, n, obs)
+    want = oracle.abc_prior_predictive(m, M.keying(1337), n, 0, n, obs)
+    for g, w in zip(got, want):
+        assert eq(g, w)
+    key = M.keying(42, A.VXB_KEY_WORKER, 7, 8)
+    got = ctx.abc_prior_predictive_host(m, key, 3001, 0, 3001, obs)
+    want = oracle.abc_prior_predictive(m, key, 3001, 0, 3001, obs)
+    for g, w in zip(got, want):
+        assert eq(g, w)
+    # shards of the same job reproduce the whole (any GPU count gives one answer)
+    a = ctx.abc_prior_predictive_host(m, M.keying(1337), n, 0, 777, obs)
+    b = ctx.abc_prior_predictive_host(m, M.keying(1337), n, 777, 1223, obs)
+    whole = ctx.abc_prior_predictive_host(m, M.keying(1337), n, 0, 2000, obs)
+    for w, x, y in zip(whole, a, b):
+        assert eq(w, np.concatenate([x, y]))
+
+
+@pytest.mark.parametrize("precision", [A.VXB_F64, A.VXB_F32])
+def test_external_noise_mode(ctx, oracle, golden, precision):
+    """Mode A of north_star: identical pre-generated noise arrays."""
+    rs = np.random.RandomState(5)
+    n, steps = 4096, 2000
+    dt = np.float32 if precision == A.VXB_F32 else np.float64
+    noise = rs.standard_normal((n, steps)).astype(dt)
+    obs = golden["logistic_observed"]
+    m = M.logistic_model(precision=precision, rng=A.VXB_RNG_EXTERNAL)
+    got = ctx.abc_prior_predictive_host(m, M.keying(9), n, 0, n, obs, noise=noise)
+    want = oracle.abc_prior_predictive(m, M.keying(9), n, 0, n, obs, noise=noise.astype(np.float64))
+    for g, w in zip(got, want):
+        assert eq(g, w)  # exact arithmetic: bit-identical states, distances, flags
+    # FMA-contracted update: states within 1e-12 relative (fp32: 1e-5)
+    mf = M.logistic_model(precision=precision, rng=A.VXB_RNG_EXTERNAL, arith=A.VXB_ARITH_FMA)
+    p, s, rho, f = ctx.abc_prior_predictive_host(mf, M.keying(9), n, 0, n, obs, noise=noise)
+    tol = 1e-5 if precision == A.VXB_F32 else 1e-12
+    assert eq(p, want[0])
+    assert np.max(np.abs(s - want[1]) / np.abs(want[1])) < tol
+    assert np.max(np.abs(rho - want[2]) / np.abs(want[2])) < tol
+
+
+# ---------------------------------------------------------------- kernel 4
+def test_select_epsilon_golden_on_device(ctx, golden):
+    rho = golden["sel_rho"]
+    for q in (0.001, 0.01, 0.5, 1.0):
+        eps, idx, nacc = ctx.select_epsilon(rho, None, q)
+        assert eps == golden[f"sel_eps_{q}"][0] and eq(idx, golden[f"sel_idx_{q}"])
+        assert nacc == len(idx) >= math.ceil(q * len(rho))
+    eps, idx, nacc = ctx.select_epsilon(golden["bad_rho"], golden["bad_failed"], 0.25)
+    assert eps == golden["sel_bad_eps"][0] and eq(idx, golden["sel_bad_idx"])
+    eps, idx, nacc = ctx.select_epsilon(golden["toggle_rho"], None, 0.01)  # SURVEY.md 8c KAT
+    assert eps == 208.44209220565364 and idx.tolist() == [120, 208, 239]
+    eps, idx, _ = ctx.select_epsilon(np.array([1.0, 2.0, 3.0, 4.0]), None, 0.5)
+    assert idx.tolist() == [0, 1]
+    with pytest.raises(lib.VxbError) as e:
+        ctx.select_epsilon(np.array([np.nan, np.nan]), np.array([1, 1], dtype=np.uint8), 0.5)
+    assert e.value.code == "empty-set"
+    with pytest.raises(lib.VxbError) as e:
+        ctx.select_epsilon(np.array([1.0]), None, 0.0)
+    assert e.value.code == "invalid-argument"
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 4097, 1000003])
+def test_select_epsilon_matches_oracle(ctx, oracle, n):
+    rs = np.random.RandomState(n)
+    rho = np.abs(rs.standard_normal(n)) * 50.0
+    rho[rs.randint(0, n, size=n // 10)] = rho[0]  # ties
+    if n > 10:
+        rho[rs.randint(0, n, size=3)] *= -1.0  # negative values order correctly too
+    failed = (rs.uniform(size=n) < 0.01).astype(np.uint8)
+    failed[0] = 0
+    rho[failed == 1] = np.nan
+    for q in (1e-3, 0.05, 0.5, 0.999, 1.0):
+        eps_o, idx_o = oracle.select_epsilon(rho, failed, q)
+        eps, idx, nacc = ctx.select_epsilon(rho, failed, q)
+        assert eps == eps_o and nacc == len(idx_o) and eq(idx, idx_o)
+    # sortedness / idempotence properties at this size
+    eps, idx, _ = ctx.select_epsilon(rho, failed, 0.3)
+    assert (np.diff(idx.astype(np.int64)) > 0).all()
+    idx2, n2 = ctx.compact_accepted(rho, failed, eps, index_base=10)
+    assert eq(idx2, idx + 10)
+    # capped output keeps the smallest indices and still reports the full count
+    idx3, n3 = ctx.compact_accepted(rho, failed, eps, cap=min(5, len(idx)))
+    assert n3 == len(idx) and eq(idx3, idx[: min(5, len(idx))])
+
+
+def test_order_statistics_f32_and_f64(ctx):
+    rs = np.random.RandomState(3)
+    for dt in (np.float64, np.float32):
+        x = (rs.standard_normal(50001) * 100).astype(dt)
+        ranks = [0, 1, 25000, 50000]
+        vals, nv = ctx.order_statistics(x, None, ranks)
+        assert nv == x.size and eq(vals, np.sort(x)[ranks].astype(np.float64))
+
+
+@pytest.mark.parametrize("precision", [A.VXB_F64, A.VXB_F32])
+def test_fused_reject_path(ctx, oracle, golden, precision):
+    """Config 1 shape: fixed epsilon, only accepted rows leave the device."""
+    m = M.logistic_model(precision=precision)
+    obs = golden["logistic_observed"]
+    n = 30000
+    p, s, rho, f = oracle.abc_prior_predictive(m, M.keying(1337), n, 0, n, obs, want_summaries=False)
+    eps, idx_o = oracle.select_epsilon(rho, f, 0.01)
+    nacc, idx, params, rho_acc = ctx.abc_reject(m, M.keying(1337), n, 0, n, obs, eps, cap=n)
+    assert nacc == len(idx_o) and eq(idx, idx_o)
+    assert eq(params, p[idx_o]) and eq(rho_acc, rho[idx_o])
+    # two shards concatenate to the same ascending set
+    n1, i1, p1, r1 = ctx.abc_reject(m, M.keying(1337), n, 0, 11111, obs, eps, cap=n)
+    n2, i2, p2, r2 = ctx.abc_reject(m, M.keying(1337), n, 11111, n - 11111, obs, eps, cap=n)
+    assert eq(np.concatenate([i1, i2]), idx_o) and eq(np.concatenate([p1, p2]), p[idx_o])
+
+
+def test_fast_generator_statistics(ctx, oracle, golden):
+    """Mode B of north_star: the throughput generator is validated end to end --
+    acceptance rate and posterior moments within Monte-Carlo error and a
+    two-sample KS test at the 1% level against the oracle's accepted set."""
+    obs = golden["logistic_observed"]
+    n = 200000
+    m_ref = M.logistic_model()
+    p, s, rho, f = ctx.abc_prior_predictive_host(m_ref, M.keying(1337), n, 0, n, obs, want_summaries=False)
+    eps, idx, nacc = ctx.select_epsilon(rho, f, 0.01)
+    for precision in (A.VXB_F64, A.VXB_F32):
+        mf = M.logistic_model(precision=precision, rng=A.VXB_RNG_FAST)
+        pf, _, rf, ff = ctx.abc_prior_predictive_host(mf, M.keying(2024), n, 0, n, obs, want_summaries=False)
+        acc = (rf <= eps) & (ff == 0)
+        rate, rate_ref = acc.mean(), nacc / n
+        assert abs(rate - rate_ref) < 5 * math.sqrt(rate_ref / n) + 1e-4
+        a, b = pf[acc].astype(np.float64), p[idx]
+        for k in range(3):
+            se = math.sqrt(a[:, k].var() / len(a) + b[:, k].var() / len(b))
+            assert abs(a[:, k].mean() - b[:, k].mean()) < 4.5 * se
+            # two-sample Kolmogorov-Smirnov, alpha = 0.01 -> c = 1.628
+            xs = np.sort(np.concatenate([a[:, k], b[:, k]]))
+            d = np.abs(np.searchsorted(np.sort(a[:, k]), xs, side="right") / len(a)
+                       - np.searchsorted(np.sort(b[:, k]), xs, side="right") / len(b)).max()
+            assert d < 1.628 * math.sqrt((len(a) + len(b)) / (len(a) * len(b)))
+        # the normals themselves: rho distribution over all particles
+        xs = np.sort(np.concatenate([rf[ff == 0].astype(np.float64), rho]))
+        d = np.abs(np.searchsorted(np.sort(rf.astype(np.float64)), xs, side="right") / n
+                   - np.searchsorted(np.sort(rho), xs, side="right") / n).max()
+        assert d < 1.628 * math.sqrt(2.0 / n)
