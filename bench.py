@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""bench.py -- headline benchmark of the hot path (BASELINE.json config 1).
+
+Workload: ABC rejection on the stochastic logistic-growth SDE, N = 1e8 prior
+samples per step (2000 Euler-Maruyama steps each), acceptance threshold fixed at
+the 0.1% quantile taken from config 0 (N = 1e6, seed 1337), particles sharded
+evenly over the GPUs (strong scaling, as config 1 states), accepted samples
+gathered over NCCL.  One "step" = one full pass over the N particles.
+
+    python bench.py --gpus 1 --steps 5 --warmup 3
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+    python bench.py --impl reference ...      # the reference's CPU path, host cores
+
+Prints ONE JSON line (rank 0).  Inputs are synthetic (seeded); see DESIGN.md.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FLOPS_PER_STEP = 55                     # 47 per N(0,1) + 8 for the update
+STEPS_PER_SIM = 2000
+FLOPS_PER_SIM = STEPS_PER_SIM * FLOPS_PER_STEP + 3 * 3 + 20 * 3 + 1   # prior + distance
+NOMINAL_PEAK = {"f64": 148 * 64 * 2 * 1.965e9 / 1e12, "f32": 148 * 128 * 2 * 1.965e9 / 1e12}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--particles", type=float, default=1e8)
+    ap.add_argument("--variant", default="f64_fast",
+                    choices=["f64_fast", "f64_ref", "f32_fast", "f32_ref"])
+    ap.add_argument("--no-extras", action="store_true", help="skip variants and cpu baseline")
+    ap.add_argument("--cpu-sample", type=float, default=4e5)
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """SM clock, power and throttle reasons DURING the timed region, read through
+    NVML in a background thread (polling the nvidia-smi CLI instead stalls the
+    launching thread by ~10% on this driver)."""
+    REASONS = {"hw_slowdown": 0x8, "sw_power_cap": 0x4, "hw_thermal_slowdown": 0x40,
+               "sw_thermal_slowdown": 0x20}
+
+    def __init__(self, device, period=0.25):
+        self.device, self.period = device, period
+        self.sm, self.pw, self.mask, self.max_sm = [], [], 0, None
+        self.stop = threading.Event()
+        self.thread = None
+
+    def _handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            import torch
+            uuid = str(torch.cuda.get_device_properties(self.device).uuid)
+            if not uuid.startswith("GPU-"):
+                uuid = "GPU-" + uuid
+            return pynvml, pynvml.nvmlDeviceGetHandleByUUID(uuid)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.device)
+
+    def _run(self):
+        try:
+            nv, h = self._handle()
+            self.max_sm = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            while not self.stop.is_set():
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                self.pw.append(nv.nvmlDeviceGetPowerUsage(h) / 1000.0)
+                self.mask |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+                self.stop.wait(self.period)
+        except Exception as e:  # NVML missing: report no samples rather than fail the bench
+            self.error = repr(e)
+
+    def __enter__(self):
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
+        return self
+
+    def __exit__(self, *exc):
+        self.stop.set()
+        self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_sm, "reasons": [], "samples": 0,
+                    "error": getattr(self, "error", None)}
+        reasons = sorted(n for n, bit in self.REASONS.items() if self.mask & bit)
+        return {"sm_mhz": float(np.median(self.sm)), "sm_min_mhz": min(self.sm),
+                "sm_max_mhz": self.max_sm, "power_w_max": max(self.pw), "reasons": reasons,
+                "samples": len(self.sm)}
+
+
+def logistic_variant(name):
+    from paper_1902_09046_b200 import _abi as A, models as M
+    prec = A.VXB_F32 if name.startswith("f32") else A.VXB_F64
+    rng = A.VXB_RNG_FAST if name.endswith("fast") else A.VXB_RNG_REF
+    return M.logistic_model(precision=prec, rng=rng)
+
+
+def run_reference(args, rank, world):
+    """The reference's own CPU implementation of the path on the host cores:
+    abc::run_prior_predictive (unmodified reference, oracle/_ref) on the logistic
+    hooks + the fixed-epsilon accept scan; bounded sample per step."""
+    if rank != 0:
+        return
+    from oracle.pyoracle import Oracle, Ref
+    from paper_1902_09046_b200 import _abi as A, models as M
+    cores = os.cpu_count() or 1
+    m = M.logistic_model()
+    sample = int(args.cpu_sample)
+    use_ref = Ref.available()
+    o = Ref() if use_ref else Oracle(threads=cores)
+    theta = [0.5, 100.0, 0.05]
+    seed_obs = o.derive_seed(1, [90])
+    obs = o.logistic_simulate(m, theta, seed_obs, 0, 0) if use_ref else o.simulate_at(m, theta, seed_obs, 0, 0)
+    eps = 5.0
+
+    def step(s):
+        if use_ref:
+            p, summ, rho, f = o.logistic_abc(m, sample, cores, 1, 1337 + s, obs)
+        else:
+            p, summ, rho, f = o.abc_prior_predictive(m, M.keying(1337 + s), sample, 0, sample, obs)
+        return int(((rho <= eps) & (f == 0)).sum())
+
+    for s in range(args.warmup):
+        step(s)
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        step(args.warmup + s)
+    dt = time.perf_counter() - t0
+    sims = args.steps * sample / dt
+    line = {
+        "impl": "reference", "metric": "prior-predictive sims/sec (logistic SDE ABC rejection)",
+        "value": sims, "unit": "sims/s", "sde_steps_per_s": sims * STEPS_PER_SIM,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config1: logistic-SDE ABC rejection, fixed epsilon, fp64",
+                   "particles_per_step": sample, "sde_steps_per_particle": STEPS_PER_SIM},
+        "cpu_baseline": {"value": sims, "unit": "sims/s", "cores": cores,
+                         "kind": "reference" if use_ref else "port",
+                         "sample": f"{sample} particles per step (of the 1e8-particle job), "
+                                   f"{cores} std::thread workers, reference keying"},
+        "e2e": {"value": sims, "unit": "sims/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_1902_09046_b200 import _abi as A, dist as D, lib, models as M
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = lib.Context(local)
+    info = ctx.device_info()
+    ext = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
+    n_total = int(args.particles)
+
+    # ---- synthetic data: config 0 observation and its 0.1% epsilon
+    m_ref = M.logistic_model()
+    obs = ctx.simulate_at(m_ref, [0.5, 100.0, 0.05], lib.derive_seed(1, [90]), 0, 0)
+    n0 = 1_000_000
+    rho0 = torch.empty(n0, dtype=torch.float64, device=f"cuda:{local}")
+    ctx.abc_prior_predictive(m_ref, M.keying(1337), n0, 0, n0, obs, rho=rho0)
+    eps, _, nacc0 = ctx.select_epsilon(rho0, None, 1e-3, cap=0, precision=A.VXB_F64, n=n0,
+                                       idx=np.zeros(1, dtype=np.uint64))
+    del rho0
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn, warmup, steps):
+        """W untimed + exactly K timed steps, events on the launching stream, max over ranks."""
+        with torch.cuda.stream(ext):
+            for s in range(warmup):
+                fn(s)
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(ext)
+            out = None
+            for s in range(steps):
+                out = fn(warmup + s)
+            e1.record(ext)
+            barrier()
+        ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=f"cuda:{local}")
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return float(ms.item()), out
+
+    def device_step(model):
+        def fn(s):
+            return D.sharded_reject(ctx, model, M.keying(1337 + s), n_total, obs, eps)
+        return fn
+
+    def host_step(model):
+        begin, end = D.shard_range(n_total, world, rank)
+        cap = max(1024, int((end - begin) * 0.01))
+
+        def fn(s):  # public host-buffer call: H2D of the observation, D2H of the accepted rows
+            return ctx.abc_reject(model, M.keying(1337 + s), n_total, begin, end - begin, obs, eps, cap)
+        return fn
+
+    # ---- headline: device-resident
+    model = logistic_variant(args.variant)
+    ctx.profile_enable(True)
+    ctx.profile_reset()
+    with ClockSampler(local) as clocks:
+        ms, out = timed(device_step(model), args.warmup, args.steps)
+    prof = ctx.profile_read()
+    ctx.profile_enable(False)
+    total_launches = sum(v["launches"] for v in prof.values())
+    timed_fraction = args.steps / (args.warmup + args.steps)
+    sims_per_s = args.steps * n_total / (ms * 1e-3)
+    n_acc = sum(out[3])
+    sim = prof["simulate"]
+    kernel_ms = sim["total_ms"] / max(sim["launches"], 1)   # per launch, this rank's shard
+    begin, end = D.shard_range(n_total, world, rank)
+    kernel_flops = (end - begin) * FLOPS_PER_SIM
+    dt_name = "f32" if args.variant.startswith("f32") else "f64"
+    peak_meas, _ = ctx.fma_peak(A.VXB_F32 if dt_name == "f32" else A.VXB_F64)
+    achieved = kernel_flops / (kernel_ms * 1e-3) / 1e12
+
+    # ---- e2e: host buffers through the public call
+    ms_e2e, out_h = timed(host_step(model), args.warmup, args.steps)
+    e2e_sims = args.steps * n_total / (ms_e2e * 1e-3)
+    real = 4 if dt_name == "f32" else 8
+    k_local = len(out_h[1])
+    d2h = k_local * (8 + 3 * real + real) + 8
+    h2d = obs.nbytes + 256
+
+    line = {
+        "metric": "prior-predictive sims/sec (logistic SDE ABC rejection)",
+        "value": sims_per_s, "unit": "sims/s", "sde_steps_per_s": sims_per_s * STEPS_PER_SIM,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": dt_name, "data": "synthetic",
+        "config": {"workload": f"config1: logistic-SDE ABC rejection, N={n_total:.0e} particles/step, "
+                               f"fixed epsilon from config0, {args.variant}",
+                   "particles_per_step": n_total, "sde_steps_per_particle": STEPS_PER_SIM,
+                   "epsilon": eps, "accepted_per_step": n_acc, "variant": args.variant,
+                   "sharding": f"particles/{world}",
+                   "l2": "no reusable input (compute-bound); per-step rho scratch "
+                         f"{(end - begin) * real / 1e6:.0f} MB exceeds L2"},
+        "e2e": {"value": e2e_sims, "unit": "sims/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e / args.steps},
+        "gpu_launches": int(round(total_launches * timed_fraction)),
+        "roofline": {"bound": f"{dt_name}-pipe", "achieved": achieved, "peak": peak_meas,
+                     "unit": "TFLOP/s", "frac": achieved / peak_meas,
+                     "peak_nominal": NOMINAL_PEAK[dt_name],
+                     "frac_of_nominal": achieved / NOMINAL_PEAK[dt_name],
+                     "peak_source": "measured FMA-chain probe (vxb_fma_peak) on this GPU; "
+                                    "MEASURED_PEAKS.json has no fp64/fp32 entry",
+                     "kernel": "logistic_abc_kernel", "kernel_ms": kernel_ms,
+                     "flops_per_sim": FLOPS_PER_SIM, "traffic": None},
+        "clocks": clocks.summary(),
+        "device": info["name"],
+    }
+
+    if not args.no_extras:
+        variants = {}
+        for name in ("f64_fast", "f64_ref", "f32_fast"):
+            if name == args.variant:
+                variants[name] = {"sims_per_s": sims_per_s, "ms_per_step": ms / args.steps}
+                continue
+            w, k = min(args.warmup, 2), min(args.steps, 3)
+            ms_v, _ = timed(device_step(logistic_variant(name)), w, k)
+            pk = NOMINAL_PEAK["f32" if name.startswith("f32") else "f64"]
+            sv = k * n_total / (ms_v * 1e-3)
+            variants[name] = {"sims_per_s": sv, "ms_per_step": ms_v / k, "steps": k, "warmup": w,
+                              "frac_of_nominal_peak": sv * FLOPS_PER_SIM / 1e12 / pk}
+        line["variants"] = variants
+        if rank == 0 and world == 1:
+            line["cpu_baseline"] = cpu_baseline(args, obs, eps)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(args, obs, eps):
+    """The reference CPU path on this box's host cores, bounded sample (rank 0, N=1)."""
+    from oracle.pyoracle import Oracle, Ref
+    from paper_1902_09046_b200 import models as M
+    cores = os.cpu_count() or 1
+    m = M.logistic_model()
+    sample = int(args.cpu_sample)
+    use_ref = Ref.available()
+    o = Ref() if use_ref else Oracle(threads=cores)
+
+    def step(s):
+        if use_ref:
+            return o.logistic_abc(m, sample, cores, 1, 1337 + s, obs)
+        return o.abc_prior_predictive(m, M.keying(1337 + s), sample, 0, sample, obs)
+
+    step(0)  # one discarded warm-up, then 3 replicates (bench.cpp:140-172 protocol)
+    t0 = time.perf_counter()
+    for s in range(3):
+        p, summ, rho, f = step(1 + s)
+        int(((rho <= eps) & (f == 0)).sum())
+    dt = (time.perf_counter() - t0) / 3
+    return {"value": sample / dt, "unit": "sims/s", "cores": cores,
+            "kind": "reference" if use_ref else "port",
+            "sample": f"{sample} particles (of the 1e8-particle job; scales linearly), "
+                      f"{cores} std::thread workers"}
+
+
+if __name__ == "__main__":
+    main()

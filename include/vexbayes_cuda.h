@@ -142,6 +142,11 @@ int vxb_device_alloc(vxb_ctx* ctx, size_t bytes, void** out);
 int vxb_device_free(vxb_ctx* ctx, void* p);
 int vxb_copy(vxb_ctx* ctx, void* dst, const void* src, size_t bytes); /* any direction */
 
+/* Roofline denominator: measured throughput (TFLOP/s, FMA = 2 flops) of a
+ * dependency-free FMA chain kernel in the given precision on this GPU, timed
+ * with events over `iters` iterations per thread.  Diagnostics only. */
+int vxb_fma_peak(vxb_ctx* ctx, int precision, uint32_t iters, double* tflops, double* ms);
+
 /* ------------------------------------------------------ substrate (RNG) */
 /* splitmix64 (rng.cpp:22-27) and derive_seed (rng.cpp:29-35); host-side. */
 uint64_t vxb_splitmix64(uint64_t z);

@@ -70,7 +70,7 @@ class vxb_mlmc_out(C.Structure):
 EXPORTED_SYMBOLS = (
     "vxb_abi_version", "vxb_init", "vxb_shutdown", "vxb_last_error", "vxb_device_info",
     "vxb_stream", "vxb_synchronize", "vxb_profile_enable", "vxb_profile_reset",
-    "vxb_profile_read", "vxb_device_alloc", "vxb_device_free", "vxb_copy",
+    "vxb_profile_read", "vxb_fma_peak", "vxb_device_alloc", "vxb_device_free", "vxb_copy",
     "vxb_splitmix64", "vxb_derive_seed", "vxb_rng_fill_u64", "vxb_rng_fill_uniform",
     "vxb_rng_fill_gaussian", "vxb_fastmath_eval", "vxb_partition",
     "vxb_abc_prior_predictive", "vxb_select_epsilon", "vxb_order_statistics",

@@ -1,0 +1,75 @@
+"""Host-side mirror of the reference ABC sampler interface (abc.hpp:16-58).
+
+Same names, argument meaning and error behaviour as ``vexbayes::abc``; every
+call runs on the GPU through the C ABI (``lib.Context``).  The C++ form of the
+same shim lives in ``cpp/vexbayes/abc.hpp``.
+"""
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi as A, models as M
+from .lib import VxbError
+
+
+@dataclass
+class PriorPredictiveSet:
+    """abc.hpp:16-31 -- rows x dim params, rows x summary_dim summaries, rho, failed."""
+    rows: int
+    dim: int
+    summary_dim: int
+    params: np.ndarray
+    summaries: np.ndarray
+    discrepancies: np.ndarray
+    failed: np.ndarray
+
+    def param_row(self, r):
+        return self.params[r]
+
+    def summary_row(self, r):
+        return self.summaries[r]
+
+
+@dataclass
+class EpsilonSelection:
+    """abc.hpp:45-48"""
+    epsilon: float
+    accepted: np.ndarray  # ascending row indices with rho <= epsilon
+
+
+def discrepancy(sim, obs):
+    """abc::discrepancy (abc.cpp:16-24): Euclidean, left-to-right accumulation."""
+    sim, obs = np.asarray(sim, dtype=np.float64), np.asarray(obs, dtype=np.float64)
+    if sim.shape != obs.shape:
+        raise VxbError("invalid-summary: summary vector lengths differ")
+    ss = 0.0
+    for s, o in zip(sim.tolist(), obs.tolist()):
+        d = s - o
+        ss += d * d
+    return float(np.sqrt(ss))
+
+
+def run_prior_predictive(ctx, model, n, workers, block_width, seed, observed):
+    """abc::run_prior_predictive (abc.cpp:26-73) on the GPU.
+
+    ``model`` is a ``vxb_model`` descriptor (models.logistic_model).  Results
+    are bit-identical to the reference for the same (seed, workers,
+    block_width): the device reproduces the reference's per-worker stream
+    consumption (VXB_KEY_WORKER)."""
+    if n < 1:
+        raise VxbError("invalid-shape: need at least one prior predictive sample")
+    if workers < 1:
+        raise VxbError("invalid-shape: need at least one worker")
+    observed = np.asarray(observed, dtype=np.float64)
+    if observed.size != model.summary_dim:
+        raise VxbError("invalid-summary: observed summary length differs from the model "
+                       "summary dimension")
+    key = M.keying(seed, A.VXB_KEY_WORKER, workers, block_width)
+    p, s, rho, f = ctx.abc_prior_predictive_host(model, key, n, 0, n, observed)
+    return PriorPredictiveSet(n, model.dim, model.summary_dim, p, s, rho, f)
+
+
+def select_epsilon(ctx, pps, accept_fraction):
+    """abc::select_epsilon (abc.cpp:75-97) on the GPU."""
+    eps, idx, _ = ctx.select_epsilon(pps.discrepancies, pps.failed, accept_fraction)
+    return EpsilonSelection(eps, idx)

@@ -14,6 +14,29 @@ namespace vxb {
 static thread_local std::string g_last_error;
 void set_last_error(const std::string& text) { g_last_error = text; }
 
+// Table of the fast fp64 logarithm (see fast_radius in vxb_rng.cuh).
+void build_fast_log_table(double* table) {
+    auto from_hi = [](uint32_t hi) {
+        const uint64_t bits = static_cast<uint64_t>(hi) << 32;
+        double v;
+        std::memcpy(&v, &bits, 8);
+        return v;
+    };
+    const uint32_t one_entry = (0x3FF00000u - 0x3FE6A09Eu) >> 13;
+    for (uint32_t i = 0; i < kLogTableSize; ++i) {
+        const double lo = from_hi(0x3FE6A09Eu + (i << 13));
+        const double hi = from_hi(0x3FE6A09Eu + ((i + 1) << 13));
+        double c = 1.0 / (0.5 * (lo + hi));
+        double t = 2.0 * std::log(c);
+        if (i == one_entry) {  // exact around u = 1
+            c = 1.0;
+            t = 0.0;
+        }
+        table[2 * i] = c;
+        table[2 * i + 1] = t;
+    }
+}
+
 // ------------------------------------------------------------ fill kernels
 // Thread t produces the pair block t of the requested range and writes the
 // one or two positions of it that fall inside [pos, pos+n): one Philox call
@@ -120,6 +143,10 @@ extern "C" int vxb_init(vxb_ctx** out, int device) {
             uint64_t threshold = ~0ull;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
         }
+        double table[2 * kLogTableSize];
+        build_fast_log_table(table);
+        VXB_CUDA(cudaMalloc(&ctx->log_table, sizeof(table)));
+        VXB_CUDA(cudaMemcpy(ctx->log_table, table, sizeof(table), cudaMemcpyHostToDevice));
         *out = ctx;
     });
 }
@@ -134,6 +161,7 @@ extern "C" void vxb_shutdown(vxb_ctx* ctx) {
     }
     for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
     cudaStreamDestroy(ctx->stream);
+    cudaFree(ctx->log_table);
     delete ctx;
 }
 
@@ -332,5 +360,56 @@ extern "C" int vxb_partition(uint64_t total, uint64_t workers, uint64_t block_wi
             ranges[2 * w + 1] = begin > total ? total : end;
             begin_block += nb;
         }
+    });
+}
+
+// ------------------------------------------------------------ FMA peak probe
+namespace vxb {
+template <class Real>
+__global__ void __launch_bounds__(256) fma_peak_kernel(uint32_t iters, Real seed, Real* sink) {
+    Real a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = seed + Real(k + threadIdx.x) * Real(1e-3);
+    const Real m = Real(0.999), c = Real(1e-3);
+    for (uint32_t i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] = a[k] * m + c;  // contracted to one FMA
+    }
+    Real s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += a[k];
+    if (s == Real(-1)) sink[0] = s;  // never true: keeps the chains alive
+}
+}  // namespace vxb
+
+extern "C" int vxb_fma_peak(vxb_ctx* ctx, int precision, uint32_t iters, double* tflops,
+                            double* ms_out) {
+    return guarded([&] {
+        use(ctx);
+        require(tflops != nullptr && iters >= 1, "invalid-argument", "bad probe arguments");
+        Scratch sink(ctx, 16);
+        const unsigned blocks = static_cast<unsigned>(ctx->prop.multiProcessorCount) * 8;
+        cudaEvent_t a, b;
+        VXB_CUDA(cudaEventCreate(&a));
+        VXB_CUDA(cudaEventCreate(&b));
+        float best = 1e30f;
+        for (int rep = 0; rep < 4; ++rep) {  // first repetition is the warm-up
+            VXB_CUDA(cudaEventRecord(a, ctx->stream));
+            if (precision == VXB_F32)
+                fma_peak_kernel<float><<<blocks, 256, 0, ctx->stream>>>(iters, 1.0f, sink.as<float>());
+            else
+                fma_peak_kernel<double><<<blocks, 256, 0, ctx->stream>>>(iters, 1.0, sink.as<double>());
+            VXB_CUDA(cudaEventRecord(b, ctx->stream));
+            VXB_CUDA(cudaEventSynchronize(b));
+            float ms = 0.f;
+            VXB_CUDA(cudaEventElapsedTime(&ms, a, b));
+            if (rep > 0 && ms < best) best = ms;
+        }
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        check_launch("fma_peak_kernel");
+        const double flops = 2.0 * 8.0 * static_cast<double>(iters) * 256.0 * blocks;
+        *tflops = flops / (best * 1e-3) / 1e12;
+        if (ms_out) *ms_out = best;
     });
 }

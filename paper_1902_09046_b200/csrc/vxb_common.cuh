@@ -54,6 +54,7 @@ struct vxb_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaDeviceProp prop{};
+    double2* log_table = nullptr;  // fast fp64 generator table (vxb_rng.cuh)
     bool profiling = false;
     vxb_profile profile{};
     std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> pending;

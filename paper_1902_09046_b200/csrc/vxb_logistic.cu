@@ -20,6 +20,7 @@ struct AbcParams {
     LogisticModel model;
     double observed[VXB_MAX_SUMMARY];
     const double* theta_in;  // kKeyFixed: simulate at this theta, no prior draw
+    const double2* log_table;  // fast fp64 generator: (c_i, 2 ln c_i), kLogTableSize entries
     void* params;
     void* summaries;
     void* rho;
@@ -32,6 +33,12 @@ constexpr int kBlock = 256;
 template <class Real, int kRng, bool kFma>
 __global__ void __launch_bounds__(kBlock)
 logistic_abc_kernel(const __grid_constant__ AbcParams p) {
+    // fast fp64 generator: stage the 2 KB log table in shared memory
+    __shared__ double2 s_log[(kRng == VXB_RNG_FAST && sizeof(Real) == 8) ? kLogTableSize : 1];
+    if (kRng == VXB_RNG_FAST && sizeof(Real) == 8) {
+        if (threadIdx.x < kLogTableSize) s_log[threadIdx.x] = p.log_table[threadIdx.x];
+        __syncthreads();
+    }
     const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
     if (r >= p.count) return;
     const uint64_t row = p.first + r;
@@ -47,7 +54,7 @@ logistic_abc_kernel(const __grid_constant__ AbcParams p) {
         noise_pos = base + (base & 1);
     } else {
         if (kRng == VXB_RNG_FAST)
-            draw_prior_fast(p.model, key, theta);
+            draw_prior_fast(p.model, p.key.fast, row, theta);
         else
             draw_prior_ref(p.model, key, base, theta);
         noise_pos = base + 4;  // three uniforms, aligned to the pair boundary
@@ -75,8 +82,14 @@ logistic_abc_kernel(const __grid_constant__ AbcParams p) {
         RefNoise<Real> noise{key, noise_pos >> 1};
         rho = logistic_path<Real, A>(p.model, theta, p.observed, noise, emit, bad);
     } else if (kRng == VXB_RNG_FAST) {
-        typename std::conditional<sizeof(Real) == 4, FastNoise32, FastNoise64>::type noise{key, 0};
-        rho = logistic_path<Real, A>(p.model, theta, p.observed, noise, emit, bad);
+        const uint32_t rl = static_cast<uint32_t>(row), rh = static_cast<uint32_t>(row >> 32);
+        if constexpr (sizeof(Real) == 4) {
+            FastNoise32 noise{p.key.fast, rl, rh, 0u};
+            rho = logistic_path<Real, A>(p.model, theta, p.observed, noise, emit, bad);
+        } else {
+            FastNoise64 noise{p.key.fast, s_log, rl, rh, 0u};
+            rho = logistic_path<Real, A>(p.model, theta, p.observed, noise, emit, bad);
+        }
     } else {
         ExternalNoise<Real> noise{static_cast<const Real*>(p.noise) + r * p.model.steps, 0,
                                   p.model.steps};
@@ -105,7 +118,7 @@ __global__ void gather_accepted_kernel(Keying key, LogisticModel model, uint64_t
     locate_row(key, row, k, base);
     double theta[3];
     if (kRng == VXB_RNG_FAST)
-        draw_prior_fast(model, k, theta);
+        draw_prior_fast(model, key.fast, row, theta);
     else
         draw_prior_ref(model, k, base, theta);
     if (params_out) {
@@ -144,6 +157,7 @@ LogisticModel make_logistic(const vxb_model& m) {
 Keying make_keying(const vxb_keying& k, const vxb_model& m, uint64_t n_total) {
     Keying d{};
     d.seed_hash = splitmix64(k.seed);
+    d.fast = make_fast_keys(d.seed_hash);
     if (k.mode == VXB_KEY_PARTICLE) {
         d.mode = kKeyParticle;
     } else if (k.mode == VXB_KEY_WORKER) {
@@ -184,8 +198,9 @@ void launch_abc1(vxb_ctx* ctx, const AbcParams& p, int rng, bool fma) {
     else
         launch_abc2<Real, VXB_RNG_EXTERNAL>(ctx, p, fma);
 }
-void launch_abc(vxb_ctx* ctx, const vxb_model& m, const AbcParams& p) {
+void launch_abc(vxb_ctx* ctx, const vxb_model& m, AbcParams p) {
     if (p.count == 0) return;
+    p.log_table = ctx->log_table;
     const bool fma = m.arith == VXB_ARITH_FMA || m.rng == VXB_RNG_FAST;
     if (m.precision == VXB_F32)
         launch_abc1<float>(ctx, p, m.rng, fma);

@@ -26,6 +26,7 @@ struct Keying {
     uint64_t extra_blocks;
     uint64_t width;       // V
     uint64_t row_stride;  // stream positions one row consumes
+    FastKeys fast;        // VXB_RNG_FAST: Philox4x32 round keys of the seed
 };
 
 struct LogisticModel {
@@ -72,12 +73,13 @@ __device__ __forceinline__ void draw_prior_ref(const LogisticModel& m, uint64_t 
     theta[1] = __dadd_rn(m.lo[1], __dmul_rn(u1, __dsub_rn(m.hi[1], m.lo[1])));
     theta[2] = __dadd_rn(m.lo[2], __dmul_rn(u2, __dsub_rn(m.hi[2], m.lo[2])));
 }
-// Prior draw of the throughput generator: Philox4x32 block (0, domain 1).
-__device__ __forceinline__ void draw_prior_fast(const LogisticModel& m, uint64_t key,
-                                                double* theta) {
-    const Words a = philox4x32(key, 0, 1u);
-    const Words b = philox4x32(key, 1, 1u);
-    const double u0 = to_unit(a.w0), u1 = to_unit(a.w1), u2 = to_unit(b.w0);
+// Prior draw of the throughput generator: counter (0..1, kDomPrior, row).
+__device__ __forceinline__ void draw_prior_fast(const LogisticModel& m, const FastKeys& fk,
+                                                uint64_t row, double* theta) {
+    const uint32_t rl = static_cast<uint32_t>(row), rh = static_cast<uint32_t>(row >> 32);
+    const Words32 a = philox4x32(fk, 0u, kDomPrior, rl, rh);
+    const Words32 b = philox4x32(fk, 1u, kDomPrior, rl, rh);
+    const double u0 = fast_unit(a.a, a.b), u1 = fast_unit(a.c, a.d), u2 = fast_unit(b.a, b.b);
     theta[0] = m.lo[0] + u0 * (m.hi[0] - m.lo[0]);
     theta[1] = m.lo[1] + u1 * (m.hi[1] - m.lo[1]);
     theta[2] = m.lo[2] + u2 * (m.hi[2] - m.lo[2]);
@@ -98,18 +100,21 @@ struct RefNoise {  // bit-identical to RngStream::fill_gaussian (rng.cpp:142-164
 };
 struct FastNoise64 {
     static constexpr int kBatch = 2;
-    uint64_t key, pair;
+    const FastKeys& fk;
+    const double2* tbl;
+    uint32_t row_lo, row_hi, block;
     __device__ __forceinline__ void next(double* z) {
-        box_muller<Fused>(philox4x32(key, pair++, 0u), z[0], z[1]);
+        fast_box_muller(philox4x32(fk, block++, kDomNoise, row_lo, row_hi), tbl, z[0], z[1]);
     }
 };
 struct FastNoise32 {
     static constexpr int kBatch = 4;
-    uint64_t key, pair;
+    const FastKeys& fk;
+    uint32_t row_lo, row_hi, block;
     __device__ __forceinline__ void next(float* z) {
-        const Words w = philox4x32(key, pair++, 0u);
-        box_muller_f32(static_cast<uint32_t>(w.w0), static_cast<uint32_t>(w.w0 >> 32), z[0], z[1]);
-        box_muller_f32(static_cast<uint32_t>(w.w1), static_cast<uint32_t>(w.w1 >> 32), z[2], z[3]);
+        const Words32 w = philox4x32(fk, block++, kDomNoise, row_lo, row_hi);
+        box_muller_f32(w.a, w.b, z[0], z[1]);
+        box_muller_f32(w.c, w.d, z[2], z[3]);
     }
 };
 template <class Real>
@@ -133,15 +138,17 @@ __device__ __forceinline__ Real logistic_step(Real x, Real a, Real c, Real inv_k
         const Real diff = A::mul(A::mul(c, x), z);
         return A::add(A::add(x, drift), diff);
     } else {
+        // x (1 + a (1 - x/K) + c z): same polynomial, four FMAs
         const Real sat = A::mad(-x, inv_k, Real(1));
-        return A::mad(A::mul(c, x), z, A::mad(A::mul(a, x), sat, x));
+        const Real g = A::mad(c, z, A::mul(a, sat));
+        return A::mad(x, g, x);
     }
 }
 
-// Runs one path; returns rho (NaN if the state left the reals).  Summaries are
-// written through `emit(k, value)` as they are produced, so the trajectory never
-// leaves registers; the squared distance accumulates left to right in
-// observation order (abc.cpp:16-24).
+// Runs one path; returns rho.  Summaries are handed to `emit(k, value)` as they
+// are produced, so the trajectory never leaves registers; the squared distance
+// accumulates left to right in observation order (abc.cpp:16-24).  `bad` is set
+// when an observed state is not finite.
 template <class Real, class A, class Noise, class Emit>
 __device__ __forceinline__ Real logistic_path(const LogisticModel& m, const double* theta,
                                               const double* __restrict__ observed, Noise& noise,
@@ -156,24 +163,40 @@ __device__ __forceinline__ Real logistic_path(const LogisticModel& m, const doub
     Real ss = 0;
     uint32_t next = 0, since = 0;
     bad = false;
-    for (uint32_t j = 0; j < m.steps; j += Noise::kBatch) {
-        Real z[Noise::kBatch];
+    constexpr uint32_t kB = Noise::kBatch;
+    const uint32_t steps = m.steps, stride = m.obs_stride;
+    auto observe = [&] {
+        since = 0;
+        if (next < m.n_obs) {
+            const Real d = A::sub(x, static_cast<Real>(observed[next]));
+            ss = A::mad(d, d, ss);
+            bad = bad || !isfinite(x);
+            emit(next, x);
+            ++next;
+        }
+    };
+    uint32_t j = 0;
+    for (; j + kB <= steps; j += kB) {
+        Real z[kB];
         noise.next(z);
+        if (since + kB < stride) {  // no observation inside this batch (warp-uniform)
 #pragma unroll
-        for (int q = 0; q < Noise::kBatch; ++q) {
-            if (j + q < m.steps) {
+            for (uint32_t q = 0; q < kB; ++q) x = logistic_step<Real, A>(x, a, c, inv_k, z[q]);
+            since += kB;
+        } else {
+#pragma unroll
+            for (uint32_t q = 0; q < kB; ++q) {
                 x = logistic_step<Real, A>(x, a, c, inv_k, z[q]);
-                if (++since == m.obs_stride) {
-                    since = 0;
-                    if (next < m.n_obs) {
-                        const Real d = A::sub(x, static_cast<Real>(observed[next]));
-                        ss = A::mad(d, d, ss);
-                        bad = bad || !isfinite(x);
-                        emit(next, x);
-                        ++next;
-                    }
-                }
+                if (++since == stride) observe();
             }
+        }
+    }
+    if (j < steps) {  // ragged tail: fewer than kBatch steps left
+        Real z[kB];
+        noise.next(z);
+        for (uint32_t q = 0; j + q < steps; ++q) {
+            x = logistic_step<Real, A>(x, a, c, inv_k, z[q]);
+            if (++since == stride) observe();
         }
     }
     return Exact::sqrt(ss);

@@ -115,15 +115,33 @@ __global__ void radix_pick_kernel(int shift, int bits, int n_ranks, SelectState*
         hist[q * kBins + i] = 0;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        uint64_t k = state->remaining[q], run = 0;
-        int chosen = nb - 1;
-        for (int b = 0; b < nb; ++b) {
-            if (k < run + bins[b]) {
-                chosen = b;
+    // block-wide exclusive scan: 256 threads x 8 consecutive bins
+    constexpr int kPer = kBins / 256;
+    __shared__ unsigned long long warp_tot[8];
+    unsigned long long local = 0;
+    for (int j = 0; j < kPer; ++j) local += bins[threadIdx.x * kPer + j];
+    unsigned long long incl = local;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((threadIdx.x & 31) >= o) incl += t;
+    }
+    if ((threadIdx.x & 31) == 31) warp_tot[threadIdx.x >> 5] = incl;
+    __syncthreads();
+    unsigned long long before = incl - local;
+    for (int w = 0; w < static_cast<int>(threadIdx.x >> 5); ++w) before += warp_tot[w];
+    // exactly one thread owns the bucket that holds rank k (k < total by contract)
+    const unsigned long long k = state->remaining[q];
+    __syncthreads();
+    if (k >= before && k < before + local) {
+        unsigned long long run = before;
+        int chosen = threadIdx.x * kPer;
+        for (int j = 0; j < kPer; ++j) {
+            const unsigned c = bins[threadIdx.x * kPer + j];
+            if (k < run + c) {
+                chosen = threadIdx.x * kPer + j;
                 break;
             }
-            run += bins[b];
+            run += c;
         }
         state->remaining[q] = k - run;
         state->prefix[q] |= static_cast<uint64_t>(chosen) << shift;

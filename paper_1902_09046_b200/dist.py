@@ -1,0 +1,86 @@
+"""Multi-GPU host layer: one process per GPU, torch.distributed for the exchange.
+
+The hot path shards by construction: rows are keyed by
+their global index, so rank r simulating rows [begin_r, end_r) of the job
+produces exactly the rows a single GPU would.  The data path needs no
+collective; only results are exchanged:
+
+* accepted sets (config 0/1): all_gather of the per-rank counts, then a padded
+  all_gather of (index, theta, rho); concatenation in rank order is ascending
+  in the global row index because the shards are contiguous and ordered.
+* counters (config 2) / level sums (config 4): one all_reduce(SUM).
+
+On CUDA ranks the exchange runs over NCCL (NVLink); the same code runs over
+gloo with CPU tensors for the world_size-2 tests.
+"""
+import numpy as np
+
+
+def shard_range(total, world, rank, block=1):
+    """The reference's static partition (blocked.cpp:34-63) as the shard rule."""
+    blocks = (total + block - 1) // block
+    base, extra = divmod(blocks, world)
+    begin_block = rank * base + min(rank, extra)
+    nblocks = base + (1 if rank < extra else 0)
+    begin = min(total, begin_block * block)
+    end = min(total, (begin_block + nblocks) * block)
+    return begin, end
+
+
+def gather_accepted(idx, params, rho, group=None):
+    """All-gather variable-length accepted sets; returns the concatenation in
+    rank order (ascending global row index).  Inputs are torch tensors on the
+    rank's device (CUDA -> NCCL, CPU -> gloo), trimmed to the local count."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    n_local = torch.tensor([idx.shape[0]], dtype=torch.int64, device=idx.device)
+    counts = [torch.zeros_like(n_local) for _ in range(world)]
+    dist.all_gather(counts, n_local, group=group)
+    counts = [int(c.item()) for c in counts]
+    cap = max(max(counts), 1)
+
+    def padded(t):
+        out = torch.zeros((cap,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        out[: t.shape[0]] = t
+        return out
+
+    outs = []
+    for t in (idx, params, rho):
+        buf = [torch.empty((cap,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+               for _ in range(world)]
+        dist.all_gather(buf, padded(t), group=group)
+        outs.append(torch.cat([b[:c] for b, c in zip(buf, counts)], dim=0))
+    return outs[0], outs[1], outs[2], counts
+
+
+def allreduce_sum(t, group=None):
+    import torch.distributed as dist
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
+def sharded_reject(ctx, model, key, n_total, observed, eps, cap_fraction=0.01, group=None):
+    """Config 1 on this rank's shard + the gather of accepted samples.
+
+    Device-resident: outputs are torch CUDA tensors filled by the fused kernel
+    path; only the accepted rows travel."""
+    import torch
+    import torch.distributed as dist
+    from . import _abi as A
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    begin, end = shard_range(n_total, world, rank)
+    count = end - begin
+    cap = max(1024, int(count * cap_fraction))
+    dev = torch.device("cuda", ctx.device_info()["device"])
+    real = torch.float32 if model.precision == A.VXB_F32 else torch.float64
+    idx = torch.empty(cap, dtype=torch.int64, device=dev)
+    params = torch.empty((cap, model.dim), dtype=real, device=dev)
+    rho = torch.empty(cap, dtype=real, device=dev)
+    nacc, _, _, _ = ctx.abc_reject(model, key, n_total, begin, count, observed, eps, cap,
+                                   idx=idx, params=params, rho=rho)
+    k = min(nacc, cap)
+    if world == 1:
+        return idx[:k], params[:k], rho[:k], [nacc]
+    return gather_accepted(idx[:k], params[:k], rho[:k], group)

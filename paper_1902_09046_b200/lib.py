@@ -125,6 +125,13 @@ class Context:
         return {name: dict(launches=int(out.launches[i]), total_ms=float(out.total_ms[i]))
                 for i, name in enumerate(A.VXB_K_NAMES)}
 
+    def fma_peak(self, precision=A.VXB_F64, iters=200000):
+        """Measured FMA-chain throughput (TFLOP/s) -- the roofline denominator."""
+        tf, ms = f64(), f64()
+        self._check(self.lib.vxb_fma_peak(self.handle, i32(precision), u32(iters), C.byref(tf),
+                                          C.byref(ms)))
+        return tf.value, ms.value
+
     def device_alloc(self, nbytes):
         out = P()
         self._check(self.lib.vxb_device_alloc(self.handle, C.c_size_t(nbytes), C.byref(out)))

@@ -1,0 +1,74 @@
+"""CPU tests of the multi-GPU host logic (gloo, world_size 2).
+
+The data path has no collective: ranks simulate contiguous row ranges keyed by
+global row index.  What needs testing without GPUs is the host side: the shard
+rule (the reference's partition), the variable-length gather of accepted sets in
+ascending global order, and the counter all-reduce.  The per-rank compute is
+played by the oracle here (tests may use it); on the GPU box the same gather
+code moves CUDA tensors over NCCL.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1902_09046_b200 import dist as D, models as M
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, n_total, eps, obs, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.pyoracle import Oracle
+    o = Oracle(threads=2)
+    m = M.logistic_model(steps=200, obs_stride=10)
+    begin, end = D.shard_range(n_total, world, rank)
+    p, s, rho, f = o.abc_prior_predictive(m, M.keying(1337), n_total, begin, end - begin, obs,
+                                          want_summaries=False)
+    keep = (rho <= eps) & (f == 0)
+    idx = torch.from_numpy((np.nonzero(keep)[0] + begin).astype(np.int64))
+    g_idx, g_p, g_rho, counts = D.gather_accepted(idx, torch.from_numpy(p[keep]),
+                                                  torch.from_numpy(rho[keep]))
+    total = D.allreduce_sum(torch.tensor([int(keep.sum())], dtype=torch.int64))
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), idx=g_idx.numpy(), p=g_p.numpy(),
+             rho=g_rho.numpy(), counts=np.array(counts), total=total.numpy())
+    dist.destroy_process_group()
+
+
+def test_shard_rule_is_the_reference_partition(oracle):
+    for total, world in [(100_000_000, 8), (1_000_003, 4), (7, 8), (1, 2), (1000, 3)]:
+        want = oracle.partition(total, world, 1)
+        got = np.array([D.shard_range(total, world, r) for r in range(world)], dtype=np.uint64)
+        assert np.array_equal(got, want)
+    want = oracle.partition(1003, 7, 8)
+    got = np.array([D.shard_range(1003, 7, r, 8) for r in range(7)], dtype=np.uint64)
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_gather_equals_single_rank(tmp_path, oracle):
+    n_total, world = 3001, 2
+    m = M.logistic_model(steps=200, obs_stride=10)
+    obs = oracle.simulate_at(m, [0.5, 100.0, 0.05], 5, 0, 0)
+    p, s, rho, f = oracle.abc_prior_predictive(m, M.keying(1337), n_total, 0, n_total, obs,
+                                               want_summaries=False)
+    eps, idx = oracle.select_epsilon(rho, f, 0.05)
+    mp.spawn(_worker, args=(world, free_port(), n_total, eps, obs, str(tmp_path)), nprocs=world,
+             join=True)
+    for r in range(world):
+        z = np.load(tmp_path / f"rank{r}.npz")
+        assert np.array_equal(z["idx"], idx.astype(np.int64))      # ascending global order
+        assert np.array_equal(z["p"], p[idx]) and np.array_equal(z["rho"], rho[idx])
+        assert z["counts"].sum() == len(idx) == z["total"][0]
