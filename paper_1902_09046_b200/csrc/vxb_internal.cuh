@@ -1,0 +1,25 @@
+// vxb_internal.cuh -- functions shared between the C-ABI translation units.
+#pragma once
+
+#include "vxb_common.cuh"
+#include "vxb_logistic.cuh"
+
+namespace vxb {
+
+// vxb_logistic.cu
+LogisticModel make_logistic(const vxb_model& m);
+
+// vxb_select.cu
+void compact_accepted_device(vxb_ctx* ctx, int precision, const void* rho_dev,
+                             const uint8_t* failed_dev, uint64_t n, double epsilon,
+                             uint64_t index_base, uint64_t cap, uint64_t* n_accepted_host,
+                             uint64_t* idx_dev);
+void order_statistics_any(vxb_ctx* ctx, int precision, const void* rho_dev,
+                          const uint8_t* failed_dev, uint64_t n, const uint64_t* ranks,
+                          int n_ranks, double* values);
+uint64_t count_valid_any(vxb_ctx* ctx, int precision, const void* rho_dev,
+                         const uint8_t* failed_dev, uint64_t n);
+// type-7 quantile (numeric.cpp:20-36) of n device-resident values (all valid)
+double quantile_device(vxb_ctx* ctx, const double* values_dev, uint64_t n, double level);
+
+}  // namespace vxb

@@ -28,10 +28,16 @@ struct AbcParams {
     const void* noise;
 };
 
-constexpr int kBlock = 256;
+#ifndef VXB_SIM_BLOCK
+#define VXB_SIM_BLOCK 256
+#endif
+#ifndef VXB_SIM_MIN_BLOCKS
+#define VXB_SIM_MIN_BLOCKS 1
+#endif
+constexpr int kBlock = VXB_SIM_BLOCK;
 
 template <class Real, int kRng, bool kFma>
-__global__ void __launch_bounds__(kBlock)
+__global__ void __launch_bounds__(kBlock, VXB_SIM_MIN_BLOCKS)
 logistic_abc_kernel(const __grid_constant__ AbcParams p) {
     // fast fp64 generator: stage the 2 KB log table in shared memory
     __shared__ double2 s_log[(kRng == VXB_RNG_FAST && sizeof(Real) == 8) ? kLogTableSize : 1];

@@ -6,7 +6,6 @@ using namespace vxb;
     extern "C" int name(__VA_ARGS__) {                                             \
         return guarded([&] { raise("not-implemented", #name " is not built yet"); }); \
     }
-VXB_STUB(vxb_ppp_pvalues, vxb_ctx*, const vxb_model*, const double*, const double*, uint32_t, uint64_t, uint64_t, uint64_t, uint64_t, double, uint64_t*, double*, double*)
 VXB_STUB(vxb_ess, vxb_ctx*, const double*, uint64_t, double*)
 VXB_STUB(vxb_logsumexp, vxb_ctx*, const double*, uint64_t, double*)
 VXB_STUB(vxb_resample_multinomial, vxb_ctx*, uint64_t, uint32_t, const double*, const double*, uint64_t, uint32_t, double*, uint64_t*)
