@@ -427,6 +427,30 @@ double epsilon_from_order_statistics(vxb_ctx* ctx, int precision, const void* rh
     return eps;
 }
 
+// quantile (numeric.cpp:20-36) of n device-resident finite values.
+double quantile_device(vxb_ctx* ctx, const double* values_dev, uint64_t n, double level) {
+    require(n >= 1, "insufficient-data", "quantile of an empty sample");
+    require(level >= 0.0 && level <= 1.0, "invalid-argument", "quantile level outside [0,1]");
+    uint64_t ranks[2] = {0, 0};
+    double v[2];
+    if (n == 1) {
+        order_statistics_any(ctx, VXB_F64, values_dev, nullptr, n, ranks, 1, v);
+        return v[0];
+    }
+    const double h = static_cast<double>(n - 1) * level;
+    const uint64_t lo = static_cast<uint64_t>(h);
+    if (lo + 1 >= n) {
+        ranks[0] = n - 1;
+        order_statistics_any(ctx, VXB_F64, values_dev, nullptr, n, ranks, 1, v);
+        return v[0];
+    }
+    const double frac = h - static_cast<double>(lo);
+    ranks[0] = lo;
+    ranks[1] = lo + 1;
+    order_statistics_any(ctx, VXB_F64, values_dev, nullptr, n, ranks, 2, v);
+    return v[0] + frac * (v[1] - v[0]);
+}
+
 }  // namespace vxb
 
 using namespace vxb;

@@ -1,0 +1,710 @@
+// vxb_smc.cu -- SMC building blocks and the ABC-SMC driver (kernel 5, config 3).
+//
+// Reference pieces replaced here (all single-threaded on the coordinator in the
+// reference):
+//   smc::ess                    smc.cpp:208-219
+//   logsumexp                   numeric.cpp:11-18
+//   smc::resample_multinomial   smc.cpp:268-300  (inverse-CDF, draw i = stream position i)
+//   make_kernel / cholesky      smc.cpp:311-325, numeric.cpp:81-96
+//   proposal theta + L z        smc.cpp:115-119
+// The ABC-SMC generation loop itself is not in the reference; it is
+// defined by oracle/vxb_oracle.cpp (vxo_abcsmc_run) and reproduced here
+// bit-for-bit: every reduction uses the canonical two-level order (chunks of
+// 256 summed left to right, then the chunk totals left to right), which one
+// thread per chunk reproduces exactly on the device, independent of launch
+// shape and GPU count.
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <vector>
+
+#include "vxb_internal.cuh"
+
+namespace vxb {
+
+constexpr int kChunk = 256;  // canonical reduction chunk (oracle: kChunk)
+
+// ------------------------------------------------------------- reductions
+// Deterministic max / (sum e, sum e^2) with a fixed grid: per-thread strided
+// partials, block tree in shared memory, per-block results finished by one
+// thread in block order.
+constexpr int kRedBlock = 256;
+constexpr int kRedGrid = 296;
+
+__global__ void __launch_bounds__(kRedBlock) max_partial_kernel(const double* __restrict__ x, uint64_t n,
+                                                             double* __restrict__ part) {
+    __shared__ double sh[kRedBlock];
+    double m = -INFINITY;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kRedBlock + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(kRedGrid) * kRedBlock)
+        m = fmax(m, x[i]);  // NaN-ignoring like std::max(m, v) with m first
+    sh[threadIdx.x] = m;
+    __syncthreads();
+    for (int s = kRedBlock / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+__global__ void max_final_kernel(const double* part, double* out) {
+    double m = -INFINITY;
+    for (int b = 0; b < kRedGrid; ++b) m = fmax(m, part[b]);
+    *out = m;
+}
+__global__ void __launch_bounds__(kRedBlock)
+expsum_partial_kernel(const double* __restrict__ x, uint64_t n, const double* __restrict__ mx,
+                      double* __restrict__ part /* 2 x kRedGrid */) {
+    __shared__ double s1[kRedBlock], s2[kRedBlock];
+    const double m = *mx;
+    double a = 0.0, b = 0.0;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kRedBlock + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(kRedGrid) * kRedBlock) {
+        const double e = exp(x[i] - m);
+        a += e;
+        b += e * e;
+    }
+    s1[threadIdx.x] = a;
+    s2[threadIdx.x] = b;
+    __syncthreads();
+    for (int s = kRedBlock / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            s1[threadIdx.x] += s1[threadIdx.x + s];
+            s2[threadIdx.x] += s2[threadIdx.x + s];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = s1[0];
+        part[kRedGrid + blockIdx.x] = s2[0];
+    }
+}
+__global__ void expsum_final_kernel(const double* part, double* out /* 2 */) {
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < kRedGrid; ++i) {
+        a += part[i];
+        b += part[kRedGrid + i];
+    }
+    out[0] = a;
+    out[1] = b;
+}
+
+// max, sum exp(x-max), sum exp(x-max)^2 of a device array -> host
+void max_and_expsums(vxb_ctx* ctx, const double* x_dev, uint64_t n, double* mx, double* s1,
+                     double* s2) {
+    Scratch part(ctx, sizeof(double) * 2 * kRedGrid);
+    Scratch res(ctx, sizeof(double) * 3);
+    {
+        LaunchScope scope(ctx, VXB_K_RESAMPLE);
+        max_partial_kernel<<<kRedGrid, kRedBlock, 0, ctx->stream>>>(x_dev, n, part.as<double>());
+        max_final_kernel<<<1, 1, 0, ctx->stream>>>(part.as<double>(), res.as<double>());
+        check_launch("max kernels");
+    }
+    double h[3] = {0, 0, 0};
+    VXB_CUDA(cudaMemcpyAsync(h, res.as<double>(), 8, cudaMemcpyDeviceToHost, ctx->stream));
+    VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    *mx = h[0];
+    if (!(h[0] > -INFINITY) || !std::isfinite(h[0])) {
+        *s1 = *s2 = 0.0;
+        return;
+    }
+    {
+        LaunchScope scope(ctx, VXB_K_RESAMPLE);
+        expsum_partial_kernel<<<kRedGrid, kRedBlock, 0, ctx->stream>>>(x_dev, n, res.as<double>(),
+                                                                     part.as<double>());
+        expsum_final_kernel<<<1, 1, 0, ctx->stream>>>(part.as<double>(), res.as<double>() + 1);
+        check_launch("expsum kernels");
+    }
+    VXB_CUDA(cudaMemcpyAsync(h, res.as<double>(), 24, cudaMemcpyDeviceToHost, ctx->stream));
+    VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    *s1 = h[1];
+    *s2 = h[2];
+}
+
+// --------------------------------------------- resample_multinomial pieces
+__global__ void expw_kernel(const double* __restrict__ lw, const double* __restrict__ mx, uint64_t n,
+                            double* __restrict__ e) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) e[i] = exp(lw[i] - *mx);
+}
+// Strictly sequential running sum (the order of smc.cpp:276-280): one warp
+// stages 1024-element tiles through shared memory, lane 0 accumulates.
+__global__ void __launch_bounds__(32) sequential_cumsum_kernel(double* __restrict__ e, uint64_t n) {
+    __shared__ double tile[1024];
+    double run = 0.0;
+    for (uint64_t t0 = 0; t0 < n; t0 += 1024) {
+        const uint64_t len = min(static_cast<uint64_t>(1024), n - t0);
+        for (uint64_t k = threadIdx.x; k < len; k += 32) tile[k] = e[t0 + k];
+        __syncwarp();
+        if (threadIdx.x == 0)
+            for (uint64_t k = 0; k < len; ++k) {
+                run = __dadd_rn(run, tile[k]);
+                tile[k] = run;
+            }
+        __syncwarp();
+        for (uint64_t k = threadIdx.x; k < len; k += 32) e[t0 + k] = tile[k];
+        __syncwarp();
+    }
+}
+__device__ __forceinline__ uint64_t upper_bound_dev(const double* __restrict__ cum, uint64_t n,
+                                                    double target) {
+    uint64_t lo = 0, hi = n;  // std::upper_bound (smc.cpp:287), clamped (smc.cpp:289)
+    while (lo < hi) {
+        const uint64_t mid = lo + ((hi - lo) >> 1);
+        if (target < cum[mid]) hi = mid; else lo = mid + 1;
+    }
+    return lo >= n ? n - 1 : lo;
+}
+__global__ void resample_draw_kernel(const double* __restrict__ cum, uint64_t n, uint32_t dim,
+                                     uint64_t key, const double* __restrict__ in,
+                                     double* __restrict__ out, uint64_t* __restrict__ anc) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const Words w = philox2x64(key, i >> 1);  // draw i = stream position i (smc.cpp:285)
+    const double u = to_unit((i & 1) ? w.w1 : w.w0);
+    const double target = __dmul_rn(u, cum[n - 1]);
+    const uint64_t a = upper_bound_dev(cum, n, target);
+    if (anc) anc[i] = a;
+    if (out)
+        for (uint32_t k = 0; k < dim; ++k) out[i * dim + k] = in[a * dim + k];
+}
+
+// ---------------------------------------------------- canonical reductions
+// One thread per chunk of kChunk consecutive rows; `cols` running sums each.
+// mode 0: w*theta_a (a<dim) and w*w  -> cols = dim+1
+// mode 1: (w*(theta_a-mean_a))*(theta_b-mean_b), b<=a, row-major lower triangle
+// mode 2: plain sum of v (cols = 1)
+__global__ void canon_partial_kernel(int mode, const double* __restrict__ theta,
+                                     const double* __restrict__ w, const double* __restrict__ mean,
+                                     uint64_t n, uint32_t dim, uint32_t cols,
+                                     double* __restrict__ part /* nchunks x cols */) {
+    const uint64_t c = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t i0 = c * kChunk;
+    if (i0 >= n) return;
+    const uint64_t i1 = min(n, i0 + kChunk);
+    double acc[37];  // dim <= 8: 8*9/2 = 36, or dim+1
+    for (uint32_t q = 0; q < cols; ++q) acc[q] = 0.0;
+    for (uint64_t i = i0; i < i1; ++i) {
+        const double wi = w[i];
+        if (mode == 0) {
+            for (uint32_t a = 0; a < dim; ++a) acc[a] = __dadd_rn(acc[a], __dmul_rn(wi, theta[i * dim + a]));
+            acc[dim] = __dadd_rn(acc[dim], __dmul_rn(wi, wi));
+        } else if (mode == 1) {
+            uint32_t q = 0;
+            for (uint32_t a = 0; a < dim; ++a) {
+                const double wa = __dmul_rn(wi, __dsub_rn(theta[i * dim + a], mean[a]));
+                for (uint32_t b = 0; b <= a; ++b, ++q)
+                    acc[q] = __dadd_rn(acc[q], __dmul_rn(wa, __dsub_rn(theta[i * dim + b], mean[b])));
+            }
+        } else {
+            acc[0] = __dadd_rn(acc[0], wi);
+        }
+    }
+    for (uint32_t q = 0; q < cols; ++q) part[c * cols + q] = acc[q];
+}
+__global__ void canon_final_kernel(const double* __restrict__ part, uint64_t nchunks, uint32_t cols,
+                                   double* __restrict__ out) {
+    const uint32_t q = threadIdx.x;
+    if (q >= cols) return;
+    double total = 0.0;
+    for (uint64_t c = 0; c < nchunks; ++c) total = __dadd_rn(total, part[c * cols + q]);
+    out[q] = total;
+}
+// canonical inclusive scan: cum[i] = offset(chunk) + local prefix
+__global__ void cumsum_local_kernel(const double* __restrict__ w, uint64_t n, double* __restrict__ cum,
+                                    double* __restrict__ totals) {
+    const uint64_t c = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t i0 = c * kChunk;
+    if (i0 >= n) return;
+    const uint64_t i1 = min(n, i0 + kChunk);
+    double run = 0.0;
+    for (uint64_t i = i0; i < i1; ++i) {
+        run = __dadd_rn(run, w[i]);
+        cum[i] = run;
+    }
+    totals[c] = run;
+}
+__global__ void cumsum_offsets_kernel(double* totals, uint64_t nchunks) {
+    double offset = 0.0;  // totals[c] <- exclusive offset of chunk c
+    for (uint64_t c = 0; c < nchunks; ++c) {
+        const double t = totals[c];
+        totals[c] = offset;
+        offset = __dadd_rn(offset, t);
+    }
+}
+__global__ void cumsum_apply_kernel(double* __restrict__ cum, const double* __restrict__ offsets,
+                                    uint64_t n) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) cum[i] = __dadd_rn(offsets[i / kChunk], cum[i]);
+}
+__global__ void scale_kernel(double* __restrict__ v, uint64_t n, const double* __restrict__ total) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = __ddiv_rn(v[i], *total);
+}
+__global__ void fill_kernel(double* __restrict__ v, uint64_t n, double value) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = value;
+}
+
+static uint64_t n_chunks(uint64_t n) { return (n + kChunk - 1) / kChunk; }
+
+void canon_reduce(vxb_ctx* ctx, int mode, const double* theta, const double* w, const double* mean,
+                  uint64_t n, uint32_t dim, uint32_t cols, double* out_dev) {
+    const uint64_t nc = n_chunks(n);
+    Scratch part(ctx, nc * cols * sizeof(double));
+    LaunchScope scope(ctx, VXB_K_RESAMPLE);
+    canon_partial_kernel<<<grid_for(nc, 128), 128, 0, ctx->stream>>>(mode, theta, w, mean, n, dim,
+                                                                   cols, part.as<double>());
+    canon_final_kernel<<<1, 64, 0, ctx->stream>>>(part.as<double>(), nc, cols, out_dev);
+    check_launch("canon_reduce");
+}
+
+// Weighted mean / covariance with the oracle's operation order
+// (vxo_weighted_moments_impl).  Results on the host; returns sum w^2.
+double weighted_moments_device(vxb_ctx* ctx, const double* theta, const double* w, uint64_t n,
+                               uint32_t dim, double* mean, double* cov) {
+    require(dim >= 1 && dim <= 8, "invalid-shape", "dimension out of range");
+    Scratch d_first(ctx, (dim + 1) * sizeof(double));
+    canon_reduce(ctx, 0, theta, w, nullptr, n, dim, dim + 1, d_first.as<double>());
+    const uint32_t tri = dim * (dim + 1) / 2;
+    Scratch d_second(ctx, tri * sizeof(double));
+    canon_reduce(ctx, 1, theta, w, d_first.as<double>(), n, dim, tri, d_second.as<double>());
+    double h1[9], h2[36];
+    VXB_CUDA(cudaMemcpyAsync(h1, d_first.as<double>(), (dim + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    VXB_CUDA(cudaMemcpyAsync(h2, d_second.as<double>(), tri * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (uint32_t a = 0; a < dim; ++a) mean[a] = h1[a];
+    const double s2 = h1[dim];
+    const double denom = 1.0 - s2;
+    uint32_t q = 0;
+    for (uint32_t a = 0; a < dim; ++a)
+        for (uint32_t b = 0; b <= a; ++b, ++q) {
+            cov[a * dim + b] = h2[q] / denom;
+            cov[b * dim + a] = cov[a * dim + b];
+        }
+    return s2;
+}
+
+void canon_cumsum_device(vxb_ctx* ctx, const double* w, uint64_t n, double* cum) {
+    const uint64_t nc = n_chunks(n);
+    Scratch totals(ctx, nc * sizeof(double));
+    LaunchScope scope(ctx, VXB_K_RESAMPLE);
+    cumsum_local_kernel<<<grid_for(nc, 128), 128, 0, ctx->stream>>>(w, n, cum, totals.as<double>());
+    cumsum_offsets_kernel<<<1, 1, 0, ctx->stream>>>(totals.as<double>(), nc);
+    cumsum_apply_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(cum, totals.as<double>(), n);
+    check_launch("canon_cumsum");
+}
+
+// cholesky (numeric.cpp:81-96) and the jitter rule of make_kernel (smc.cpp:311-325)
+static bool cholesky_host(double* a, uint32_t dim) {
+    for (uint32_t j = 0; j < dim; ++j) {
+        double d = a[j * dim + j];
+        for (uint32_t k = 0; k < j; ++k) d -= a[j * dim + k] * a[j * dim + k];
+        if (!(d > 0.0)) return false;
+        const double ljj = std::sqrt(d);
+        a[j * dim + j] = ljj;
+        for (uint32_t i = j + 1; i < dim; ++i) {
+            double s = a[i * dim + j];
+            for (uint32_t k = 0; k < j; ++k) s -= a[i * dim + k] * a[j * dim + k];
+            a[i * dim + j] = s / ljj;
+        }
+        for (uint32_t i = 0; i < j; ++i) a[i * dim + j] = 0.0;
+    }
+    return true;
+}
+static void make_kernel_host(const double* cov, uint32_t dim, double scale, double jitter,
+                             double* chol) {
+    double c[64];
+    for (uint32_t i = 0; i < dim * dim; ++i) c[i] = scale * cov[i];
+    std::copy(c, c + dim * dim, chol);
+    if (!cholesky_host(chol, dim)) {
+        for (uint32_t k = 0; k < dim; ++k) c[k * dim + k] += jitter;
+        std::copy(c, c + dim * dim, chol);
+        require(cholesky_host(chol, dim), "degenerate-ensemble",
+                "covariance is rank deficient beyond jitter");
+    }
+}
+
+// ------------------------------------------------------- ABC-SMC propagation
+struct ProposeParams {
+    uint64_t first, count, n_prev;
+    uint64_t seed_hash;  // splitmix64(derive_seed(seed,{gen}))
+    LogisticModel model;
+    double observed[VXB_MAX_SUMMARY];
+    double chol[9];
+    double epsilon;
+    const double* theta_prev;
+    const double* cum_prev;
+    double* theta_out;
+    double* rho_out;
+    uint8_t* flag_out;
+};
+
+// One proposal per thread (layout: vxo_abcsmc_propose): position 0 ancestor
+// uniform, positions 2..4 the Gaussian increments, position 6+j the normal of
+// simulation step j+1.
+__global__ void __launch_bounds__(256) abcsmc_propose_kernel(const __grid_constant__ ProposeParams p) {
+    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * 256 + threadIdx.x;
+    if (r >= p.count) return;
+    const uint64_t key = stream_key(p.seed_hash, p.first + r);
+    const Words w0 = philox2x64(key, 0);
+    const double target = __dmul_rn(to_unit(w0.w0), p.cum_prev[p.n_prev - 1]);
+    const uint64_t a = upper_bound_dev(p.cum_prev, p.n_prev, target);
+    double z[4];
+    box_muller<Exact>(philox2x64(key, 1), z[0], z[1]);
+    box_muller<Exact>(philox2x64(key, 2), z[2], z[3]);
+    double th[3];
+    bool inside = true;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        double inc = 0.0;
+#pragma unroll
+        for (int q = 0; q <= k; ++q) inc = __dadd_rn(inc, __dmul_rn(p.chol[k * 3 + q], z[q]));
+        th[k] = __dadd_rn(p.theta_prev[a * 3 + k], inc);
+        inside = inside && th[k] >= p.model.lo[k] && th[k] < p.model.hi[k];
+    }
+    double rho = __longlong_as_double(0x7FF8000000000000LL);
+    uint8_t flag = 2;
+    if (inside) {
+        RefNoise<double> noise{key, 3};
+        bool bad;
+        auto emit = [](uint32_t, double) {};
+        rho = logistic_path<double, Exact>(p.model, th, p.observed, noise, emit, bad);
+        if (bad) {
+            rho = __longlong_as_double(0x7FF8000000000000LL);
+            flag = 3;
+        } else {
+            flag = rho <= p.epsilon ? 1 : 0;
+        }
+    }
+    p.theta_out[r * 3 + 0] = th[0];
+    p.theta_out[r * 3 + 1] = th[1];
+    p.theta_out[r * 3 + 2] = th[2];
+    p.rho_out[r] = rho;
+    p.flag_out[r] = flag;
+}
+
+// Importance-weight denominator: one new particle per thread, previous
+// population streamed through shared memory in index order, so the sum over j
+// is the oracle's sequential sum (vxo_abcsmc_weights).
+template <int D>
+__global__ void __launch_bounds__(128)
+abcsmc_weights_kernel(uint64_t count, const double* __restrict__ theta_new, uint64_t n_prev,
+                      const double* __restrict__ theta_prev, const double* __restrict__ w_prev,
+                      const double* __restrict__ chol, double* __restrict__ w_out) {
+    constexpr int kTile = 128;
+    __shared__ double s_theta[kTile * D];
+    __shared__ double s_w[kTile];
+    __shared__ double s_chol[D * D], s_invd[D];
+    if (threadIdx.x < D * D) s_chol[threadIdx.x] = chol[threadIdx.x];
+    if (threadIdx.x < D) s_invd[threadIdx.x] = __ddiv_rn(1.0, chol[threadIdx.x * D + threadIdx.x]);
+    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * 128 + threadIdx.x;
+    double ti[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) ti[k] = r < count ? theta_new[r * D + k] : 0.0;
+    double sum = 0.0;
+    for (uint64_t j0 = 0; j0 < n_prev; j0 += kTile) {
+        const uint64_t len = min(static_cast<uint64_t>(kTile), n_prev - j0);
+        __syncthreads();
+        for (uint64_t t = threadIdx.x; t < len * D; t += 128) s_theta[t] = theta_prev[j0 * D + t];
+        if (threadIdx.x < len) s_w[threadIdx.x] = w_prev[j0 + threadIdx.x];
+        __syncthreads();
+        for (uint64_t j = 0; j < len; ++j) {
+            double y[D];
+            double q = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                double v = __dsub_rn(ti[k], s_theta[j * D + k]);
+#pragma unroll
+                for (int c = 0; c < k; ++c) v = __dsub_rn(v, __dmul_rn(s_chol[k * D + c], y[c]));
+                y[k] = __dmul_rn(v, s_invd[k]);
+                q = __dadd_rn(q, __dmul_rn(y[k], y[k]));
+            }
+            const double e = exp2_clamped<Exact>(__dmul_rn(__dmul_rn(-0.5, q), kInvLn2));
+            sum = __dadd_rn(sum, __dmul_rn(s_w[j], e));
+        }
+    }
+    if (r < count) w_out[r] = __ddiv_rn(1.0, sum);
+}
+
+__global__ void gather_rows_kernel(const uint64_t* __restrict__ idx, uint64_t n_take, uint32_t dim,
+                                   const double* __restrict__ src_theta,
+                                   const double* __restrict__ src_rho, double* __restrict__ dst_theta,
+                                   double* __restrict__ dst_rho) {
+    const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= n_take) return;
+    const uint64_t s = idx[t];
+    for (uint32_t k = 0; k < dim; ++k) dst_theta[t * dim + k] = src_theta[s * dim + k];
+    dst_rho[t] = src_rho[s];
+}
+
+void propose_device(vxb_ctx* ctx, const vxb_model& model, uint64_t seed, uint32_t gen,
+                    uint64_t first, uint64_t count, uint64_t n_prev, const double* theta_prev,
+                    const double* cum_prev, const double* chol_host, const double* observed_host,
+                    double epsilon, double* theta_out, double* rho_out, uint8_t* flag_out) {
+    require(gen >= 1, "invalid-argument", "generation 0 is the prior predictive set");
+    require(n_prev >= 1, "insufficient-data", "empty previous population");
+    require(model.precision == VXB_F64 && model.rng == VXB_RNG_REF, "invalid-argument",
+            "ABC-SMC propagation runs in fp64 with the reference generator");
+    ProposeParams p{};
+    p.model = make_logistic(model);
+    p.first = first;
+    p.count = count;
+    p.n_prev = n_prev;
+    const uint64_t g = gen;
+    p.seed_hash = splitmix64(vxb_derive_seed(seed, &g, 1));
+    for (uint32_t k = 0; k < p.model.n_obs; ++k) p.observed[k] = observed_host[k];
+    for (int k = 0; k < 9; ++k) p.chol[k] = chol_host[k];
+    p.epsilon = epsilon;
+    p.theta_prev = theta_prev;
+    p.cum_prev = cum_prev;
+    p.theta_out = theta_out;
+    p.rho_out = rho_out;
+    p.flag_out = flag_out;
+    if (count == 0) return;
+    LaunchScope scope(ctx, VXB_K_PROPOSE);
+    abcsmc_propose_kernel<<<grid_for(count, 256), 256, 0, ctx->stream>>>(p);
+    check_launch("abcsmc_propose_kernel");
+}
+
+void weights_device(vxb_ctx* ctx, uint32_t dim, uint64_t count, const double* theta_new,
+                    uint64_t n_prev, const double* theta_prev, const double* w_prev,
+                    const double* chol_dev, double* w_out) {
+    if (count == 0) return;
+    LaunchScope scope(ctx, VXB_K_WEIGHTS);
+    const unsigned grid = grid_for(count, 128);
+    switch (dim) {
+        case 1: abcsmc_weights_kernel<1><<<grid, 128, 0, ctx->stream>>>(count, theta_new, n_prev, theta_prev, w_prev, chol_dev, w_out); break;
+        case 2: abcsmc_weights_kernel<2><<<grid, 128, 0, ctx->stream>>>(count, theta_new, n_prev, theta_prev, w_prev, chol_dev, w_out); break;
+        case 3: abcsmc_weights_kernel<3><<<grid, 128, 0, ctx->stream>>>(count, theta_new, n_prev, theta_prev, w_prev, chol_dev, w_out); break;
+        case 4: abcsmc_weights_kernel<4><<<grid, 128, 0, ctx->stream>>>(count, theta_new, n_prev, theta_prev, w_prev, chol_dev, w_out); break;
+        default: raise("invalid-shape", "dimension out of range (1..4)");
+    }
+    check_launch("abcsmc_weights_kernel");
+}
+
+}  // namespace vxb
+
+using namespace vxb;
+
+extern "C" int vxb_ess(vxb_ctx* ctx, const double* log_w, uint64_t n, double* ess) {
+    return guarded([&] {
+        use(ctx);
+        require(log_w && ess && n >= 1, "invalid-argument", "null or empty argument");
+        Staged d(ctx, log_w, n * 8, true, false);
+        double mx, s1, s2;
+        max_and_expsums(ctx, d.as<double>(), n, &mx, &s1, &s2);
+        require(mx > -INFINITY, "degenerate-ensemble", "all weights are zero");
+        *ess = s1 * s1 / s2;
+    });
+}
+
+extern "C" int vxb_logsumexp(vxb_ctx* ctx, const double* x, uint64_t n, double* out) {
+    return guarded([&] {
+        use(ctx);
+        require(out != nullptr, "invalid-argument", "null output");
+        if (n == 0) {
+            *out = -INFINITY;
+            return;
+        }
+        Staged d(ctx, x, n * 8, true, false);
+        double mx, s1, s2;
+        max_and_expsums(ctx, d.as<double>(), n, &mx, &s1, &s2);
+        *out = std::isfinite(mx) ? mx + std::log(s1) : mx;
+    });
+}
+
+extern "C" int vxb_resample_multinomial(vxb_ctx* ctx, uint64_t n, uint32_t dim, const double* log_w,
+                                        const double* particles_in, uint64_t seed,
+                                        uint32_t stream_id, double* particles_out,
+                                        uint64_t* ancestors) {
+    return guarded([&] {
+        use(ctx);
+        require(log_w && n >= 1, "invalid-argument", "null or empty argument");
+        require(!particles_out || particles_in, "invalid-argument", "missing input particles");
+        Staged d_lw(ctx, log_w, n * 8, true, false);
+        Staged d_in(ctx, particles_in, n * dim * 8, true, false);
+        Staged d_out(ctx, particles_out, n * dim * 8, false, true);
+        Staged d_anc(ctx, ancestors, n * 8, false, true);
+        double mx, s1, s2;
+        max_and_expsums(ctx, d_lw.as<double>(), n, &mx, &s1, &s2);
+        require(mx > -INFINITY, "degenerate-ensemble", "all weights are zero");
+        require(std::isfinite(s1) && s1 > 0.0, "degenerate-ensemble", "weight sum is not finite");
+        Scratch d_cum(ctx, n * 8);
+        Scratch d_mx(ctx, 8);
+        VXB_CUDA(cudaMemcpyAsync(d_mx.as<void>(), &mx, 8, cudaMemcpyHostToDevice, ctx->stream));
+        {
+            LaunchScope scope(ctx, VXB_K_RESAMPLE);
+            expw_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(d_lw.as<double>(), d_mx.as<double>(),
+                                                                 n, d_cum.as<double>());
+            sequential_cumsum_kernel<<<1, 32, 0, ctx->stream>>>(d_cum.as<double>(), n);
+            resample_draw_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
+                d_cum.as<double>(), n, dim, stream_key(splitmix64(seed), stream_id), d_in.as<double>(),
+                d_out.as<double>(), d_anc.as<uint64_t>());
+            check_launch("resample kernels");
+        }
+        d_out.finish();
+        d_anc.finish();
+        VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+extern "C" int vxb_abcsmc_propose(vxb_ctx* ctx, const vxb_model* model, uint64_t seed, uint32_t gen,
+                                  uint64_t first, uint64_t count, uint64_t n_prev,
+                                  const double* theta_prev, const double* cum_prev,
+                                  const double* chol, const double* observed, double epsilon,
+                                  double* theta_out, double* rho_out, uint8_t* flag_out) {
+    return guarded([&] {
+        use(ctx);
+        require(model && theta_prev && cum_prev && chol && observed && theta_out && rho_out &&
+                    flag_out,
+                "invalid-argument", "null argument");
+        require(!is_device_pointer(chol) && !is_device_pointer(observed), "invalid-argument",
+                "chol and observed are host arrays");
+        Staged d_tp(ctx, theta_prev, n_prev * 3 * 8, true, false);
+        Staged d_cp(ctx, cum_prev, n_prev * 8, true, false);
+        Staged d_th(ctx, theta_out, count * 3 * 8, false, true);
+        Staged d_rho(ctx, rho_out, count * 8, false, true);
+        Staged d_flag(ctx, flag_out, count, false, true);
+        propose_device(ctx, *model, seed, gen, first, count, n_prev, d_tp.as<double>(),
+                       d_cp.as<double>(), chol, observed, epsilon, d_th.as<double>(),
+                       d_rho.as<double>(), d_flag.as<uint8_t>());
+        d_th.finish();
+        d_rho.finish();
+        d_flag.finish();
+        VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+extern "C" int vxb_abcsmc_weights(vxb_ctx* ctx, uint32_t dim, uint64_t count,
+                                  const double* theta_new, uint64_t n_prev,
+                                  const double* theta_prev, const double* w_prev,
+                                  const double* chol, double* w_out) {
+    return guarded([&] {
+        use(ctx);
+        require(theta_new && theta_prev && w_prev && chol && w_out, "invalid-argument",
+                "null argument");
+        require(dim >= 1 && dim <= 4, "invalid-shape", "dimension out of range (1..4)");
+        Staged d_tn(ctx, theta_new, count * dim * 8, true, false);
+        Staged d_tp(ctx, theta_prev, n_prev * dim * 8, true, false);
+        Staged d_wp(ctx, w_prev, n_prev * 8, true, false);
+        Staged d_ch(ctx, chol, dim * dim * 8, true, false);
+        Staged d_out(ctx, w_out, count * 8, false, true);
+        weights_device(ctx, dim, count, d_tn.as<double>(), n_prev, d_tp.as<double>(),
+                       d_wp.as<double>(), d_ch.as<double>(), d_out.as<double>());
+        d_out.finish();
+        VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+// Full run, device resident; follows vxo_abcsmc_run step for step.
+extern "C" int vxb_abcsmc_run(vxb_ctx* ctx, const vxb_model* model, const vxb_abcsmc_cfg* cfg,
+                              const double* observed, vxb_abcsmc_out* out) {
+    return guarded([&] {
+        use(ctx);
+        require(model && cfg && observed && out, "invalid-argument", "null argument");
+        const LogisticModel lm = make_logistic(*model);
+        (void)lm;
+        require(model->precision == VXB_F64 && model->rng == VXB_RNG_REF, "invalid-argument",
+                "ABC-SMC runs in fp64 with the reference generator");
+        const uint64_t n = cfg->particles;
+        const uint32_t d = 3;
+        require(n >= 2, "insufficient-data", "need at least two particles");
+        require(cfg->generations >= 1, "invalid-argument", "need at least one generation");
+        require(cfg->quantile > 0.0 && cfg->quantile <= 1.0, "invalid-argument",
+                "quantile must lie in (0, 1]");
+        const uint64_t round = cfg->round_size ? cfg->round_size : n;
+        const uint64_t max_rounds = cfg->max_rounds ? cfg->max_rounds : 1000;
+        const uint64_t zero = 0;
+
+        Scratch theta(ctx, n * d * 8), w(ctx, n * 8), rho(ctx, n * 8), cum(ctx, n * 8);
+        Scratch th_new(ctx, n * d * 8), rho_new(ctx, n * 8), w_new(ctx, n * 8);
+        Scratch p_theta(ctx, round * d * 8), p_rho(ctx, round * 8), p_flag(ctx, round);
+        Scratch p_idx(ctx, round * 8), d_chol(ctx, 9 * 8), d_total(ctx, 8);
+        double* cur_theta = theta.as<double>();
+        double* cur_w = w.as<double>();
+        double* cur_rho = rho.as<double>();
+        double* nxt_theta = th_new.as<double>();
+        double* nxt_w = w_new.as<double>();
+        double* nxt_rho = rho_new.as<double>();
+
+        for (uint32_t g = 0; g < cfg->generations; ++g) {
+            double eps = std::numeric_limits<double>::infinity();
+            double chol[9] = {0};
+            if (g >= 1) {
+                eps = quantile_device(ctx, cur_rho, n, cfg->quantile);
+                double mean[3], cov[9];
+                weighted_moments_device(ctx, cur_theta, cur_w, n, d, mean, cov);
+                make_kernel_host(cov, d, cfg->kernel_scale, cfg->jitter, chol);
+                canon_cumsum_device(ctx, cur_w, n, cum.as<double>());
+                VXB_CUDA(cudaMemcpyAsync(d_chol.as<void>(), chol, sizeof(chol), cudaMemcpyHostToDevice,
+                                         ctx->stream));
+            }
+            uint64_t got = 0, evaluated = 0, accepted_total = 0;
+            for (uint64_t t = 0; t < max_rounds && got < n; ++t) {
+                if (g == 0) {
+                    vxb_keying key{VXB_KEY_PARTICLE, 1, 1, 0, vxb_derive_seed(cfg->seed, &zero, 1)};
+                    const int rc = vxb_abc_prior_predictive(
+                        ctx, model, &key, (t + 1) * round, t * round, round, observed,
+                        p_theta.as<double>(), nullptr, p_rho.as<double>(), p_flag.as<uint8_t>(),
+                        nullptr);
+                    require(rc == 0, "internal", vxb_last_error());
+                } else {
+                    propose_device(ctx, *model, cfg->seed, g, t * round, round, n, cur_theta,
+                                   cum.as<double>(), chol, observed, eps, p_theta.as<double>(),
+                                   p_rho.as<double>(), p_flag.as<uint8_t>());
+                }
+                evaluated += round;
+                // accepted <=> finite rho <= eps (rejected / outside / failed rows carry
+                // rho > eps or NaN); generation 0: failed flag excludes the row
+                uint64_t acc = 0;
+                compact_accepted_device(ctx, VXB_F64, p_rho.as<double>(),
+                                        g == 0 ? p_flag.as<uint8_t>() : nullptr, round, eps, 0, round,
+                                        &acc, p_idx.as<uint64_t>());
+                accepted_total += acc;
+                const uint64_t take = std::min(acc, n - got);
+                if (take) {
+                    LaunchScope scope(ctx, VXB_K_COMPACT);
+                    gather_rows_kernel<<<grid_for(take, 256), 256, 0, ctx->stream>>>(
+                        p_idx.as<uint64_t>(), take, d, p_theta.as<double>(), p_rho.as<double>(),
+                        nxt_theta + got * d, nxt_rho + got);
+                    check_launch("gather_rows_kernel");
+                }
+                got += take;
+            }
+            require(got == n, "empty-set", "generation did not fill within max_rounds");
+            if (g == 0) {
+                LaunchScope scope(ctx, VXB_K_MISC);
+                fill_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(nxt_w, n, 1.0 / static_cast<double>(n));
+                check_launch("fill_kernel");
+            } else {
+                weights_device(ctx, d, n, nxt_theta, n, cur_theta, cur_w, d_chol.as<double>(), nxt_w);
+                canon_reduce(ctx, 2, nullptr, nxt_w, nullptr, n, d, 1, d_total.as<double>());
+                double total = 0.0;
+                VXB_CUDA(cudaMemcpyAsync(&total, d_total.as<void>(), 8, cudaMemcpyDeviceToHost, ctx->stream));
+                VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+                require(std::isfinite(total) && total > 0.0, "degenerate-ensemble",
+                        "weight sum is not finite");
+                LaunchScope scope(ctx, VXB_K_MISC);
+                scale_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(nxt_w, n, d_total.as<double>());
+                check_launch("scale_kernel");
+            }
+            std::swap(cur_theta, nxt_theta);
+            std::swap(cur_w, nxt_w);
+            std::swap(cur_rho, nxt_rho);
+            double mean[3], cov[9];
+            const double s2 = weighted_moments_device(ctx, cur_theta, cur_w, n, d, mean, cov);
+            if (out->epsilon) out->epsilon[g] = eps;
+            if (out->ess) out->ess[g] = 1.0 / s2;
+            if (out->accept_rate)
+                out->accept_rate[g] = static_cast<double>(accepted_total) / static_cast<double>(evaluated);
+            if (out->proposals) out->proposals[g] = evaluated;
+            if (out->mean) std::copy(mean, mean + d, out->mean + g * d);
+            if (out->cov) std::copy(cov, cov + d * d, out->cov + g * d * d);
+        }
+        if (out->theta) VXB_CUDA(cudaMemcpyAsync(out->theta, cur_theta, n * d * 8, cudaMemcpyDefault, ctx->stream));
+        if (out->weight) VXB_CUDA(cudaMemcpyAsync(out->weight, cur_w, n * 8, cudaMemcpyDefault, ctx->stream));
+        if (out->rho) VXB_CUDA(cudaMemcpyAsync(out->rho, cur_rho, n * 8, cudaMemcpyDefault, ctx->stream));
+        VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}

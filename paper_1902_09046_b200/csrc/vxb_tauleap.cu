@@ -1,0 +1,246 @@
+// vxb_tauleap.cu -- multilevel Monte Carlo with coupled Poisson tau-leaping on
+// the Michaelis-Menten network (config 4): S+E->C (k1), C->S+E (k2), C->E+P (k3).
+//
+// Not in the reference (tau-leap is out of scope there; rng.cpp
+// has no Poisson sampler).  The scheme is defined by oracle/vxb_oracle.cpp
+// (vxo_mlmc_level) in the style of tb_model.cpp:39-116 and reproduced here
+// bit-for-bit:
+//  * Poisson(lam) by CDF inversion from ONE uniform: p0 = exp(-lam) through the
+//    reference's exp2_clamped (fastmath.hpp:57-79), p_k = (p_{k-1} lam)(1/k),
+//    at most 1023 terms; the reciprocals 1/k come from a shared-memory table;
+//  * propensities from max(X,0): a1 = (k1 S) E, a2 = k2 C, a3 = k3 C;
+//  * level 0: plain tau-leap; step s reads stream positions 4s + r;
+//  * level l>=1: Anderson-Higham coupling of a fine path (tau_l) with a coarse
+//    path (M tau_l) whose propensities are frozen over the coarse step; per fine
+//    step and reaction r: m = min(af, ac), P1~Poi(m tau), P2~Poi((af-m) tau),
+//    P3~Poi((ac-m) tau) at positions 10s + 3r + {0,1,2}; fine fires P1+P2,
+//    coarse fires P1+P3;
+//  * path i of level l owns RngStream(derive_seed(seed,{l}), i).
+// One path per thread, integer state in registers; only four 64-bit sums (and
+// optionally Y per path) leave the device, so the level sums are exact integers
+// and identical for any sharding.
+
+#include <cmath>
+#include <vector>
+
+#include "vxb_common.cuh"
+#include "vxb_rng.cuh"
+
+namespace vxb {
+
+constexpr int kTlBlock = 128;
+constexpr int kMaxPoisson = 1023;
+
+struct TauParams {
+    uint64_t first, count;
+    uint64_t seed_hash;  // splitmix64(derive_seed(seed,{level}))
+    uint64_t n_fine;     // fine steps
+    uint32_t level, refine;
+    double tau;
+    double rate[3];
+    int32_t init[4];
+    long long* sums;  // 4
+    int32_t* y_out;
+};
+
+struct MM {
+    int32_t s, e, c, p;
+    __device__ __forceinline__ void fire(int k1, int k2, int k3) {
+        s += -k1 + k2;
+        e += -k1 + k2 + k3;
+        c += k1 - k2 - k3;
+        p += k3;
+    }
+    __device__ __forceinline__ void prop(const double* k, double* a) const {
+        const double ds = static_cast<double>(s > 0 ? s : 0);
+        const double de = static_cast<double>(e > 0 ? e : 0);
+        const double dc = static_cast<double>(c > 0 ? c : 0);
+        a[0] = __dmul_rn(__dmul_rn(k[0], ds), de);
+        a[1] = __dmul_rn(k[1], dc);
+        a[2] = __dmul_rn(k[2], dc);
+    }
+};
+
+__device__ __forceinline__ int poisson_inv(double lam, double u, const double* __restrict__ inv,
+                                           long long& iters) {
+    if (!(lam > 0.0)) return 0;
+    double p = exp2_clamped<Exact>(__dmul_rn(-lam, kInvLn2));
+    double cdf = p;
+    int k = 0;
+    while (u > cdf && k < kMaxPoisson) {
+        ++k;
+        p = __dmul_rn(__dmul_rn(p, lam), inv[k]);
+        cdf = __dadd_rn(cdf, p);
+        ++iters;
+    }
+    return k;
+}
+
+__global__ void __launch_bounds__(kTlBlock) tauleap_kernel(const __grid_constant__ TauParams p) {
+    __shared__ double s_inv[kMaxPoisson + 1];
+    __shared__ long long s_sum[4];
+    for (int k = threadIdx.x; k <= kMaxPoisson; k += kTlBlock)
+        s_inv[k] = k ? __ddiv_rn(1.0, static_cast<double>(k)) : 0.0;
+    if (threadIdx.x < 4) s_sum[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kTlBlock + threadIdx.x;
+    long long sy = 0, sy2 = 0, sp = 0, it = 0;
+    if (r < p.count) {
+        const uint64_t key = stream_key(p.seed_hash, p.first + r);
+        MM f{p.init[0], p.init[1], p.init[2], p.init[3]};
+        MM c = f;
+        double af[3], ac[3];
+        if (p.level == 0) {
+            for (uint64_t st = 0; st < p.n_fine; ++st) {
+                f.prop(p.rate, af);
+                const Words wa = philox2x64(key, 2 * st);      // positions 4s, 4s+1
+                const Words wb = philox2x64(key, 2 * st + 1);  // position 4s+2
+                const int k0 = poisson_inv(__dmul_rn(af[0], p.tau), to_unit(wa.w0), s_inv, it);
+                const int k1 = poisson_inv(__dmul_rn(af[1], p.tau), to_unit(wa.w1), s_inv, it);
+                const int k2 = poisson_inv(__dmul_rn(af[2], p.tau), to_unit(wb.w0), s_inv, it);
+                f.fire(k0, k1, k2);
+            }
+        } else {
+            uint32_t phase = 0;
+            for (uint64_t st = 0; st < p.n_fine; ++st) {
+                if (phase == 0) c.prop(p.rate, ac);
+                if (++phase == p.refine) phase = 0;
+                f.prop(p.rate, af);
+                // positions 10s .. 10s+8 = pair blocks 5s .. 5s+4
+                uint64_t u[10];
+#pragma unroll
+                for (int b = 0; b < 5; ++b) {
+                    const Words w = philox2x64(key, 5 * st + b);
+                    u[2 * b] = w.w0;
+                    u[2 * b + 1] = w.w1;
+                }
+                int kf[3], kc[3];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const double mn = af[q] < ac[q] ? af[q] : ac[q];
+                    const int p1 = poisson_inv(__dmul_rn(mn, p.tau), to_unit(u[3 * q]), s_inv, it);
+                    const int p2 = poisson_inv(__dmul_rn(__dsub_rn(af[q], mn), p.tau),
+                                               to_unit(u[3 * q + 1]), s_inv, it);
+                    const int p3 = poisson_inv(__dmul_rn(__dsub_rn(ac[q], mn), p.tau),
+                                               to_unit(u[3 * q + 2]), s_inv, it);
+                    kf[q] = p1 + p2;
+                    kc[q] = p1 + p3;
+                }
+                f.fire(kf[0], kf[1], kf[2]);
+                c.fire(kc[0], kc[1], kc[2]);
+            }
+        }
+        const int32_t y = p.level == 0 ? f.p : f.p - c.p;
+        if (p.y_out) p.y_out[r] = y;
+        sy = y;
+        sy2 = static_cast<long long>(y) * y;
+        sp = f.p;
+    }
+    for (int o = 16; o; o >>= 1) {
+        sy += __shfl_down_sync(0xffffffffu, sy, o);
+        sy2 += __shfl_down_sync(0xffffffffu, sy2, o);
+        sp += __shfl_down_sync(0xffffffffu, sp, o);
+        it += __shfl_down_sync(0xffffffffu, it, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s_sum[0]), static_cast<unsigned long long>(sy));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s_sum[1]), static_cast<unsigned long long>(sy2));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s_sum[2]), static_cast<unsigned long long>(sp));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s_sum[3]), static_cast<unsigned long long>(it));
+    }
+    __syncthreads();
+    if (threadIdx.x < 4)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&p.sums[threadIdx.x]),
+                  static_cast<unsigned long long>(s_sum[threadIdx.x]));
+}
+
+static uint64_t level_steps(const vxb_mlmc_cfg& cfg, uint32_t level) {
+    require(cfg.tau0 > 0.0 && cfg.t_end > 0.0, "invalid-horizon", "need a positive horizon");
+    uint64_t nf = static_cast<uint64_t>(std::llround(cfg.t_end / cfg.tau0));
+    require(nf >= 1, "invalid-horizon", "need at least one step");
+    for (uint32_t l = 0; l < level; ++l) nf *= cfg.refine;
+    return nf;
+}
+
+void mlmc_level_device(vxb_ctx* ctx, const vxb_model& model, const vxb_mlmc_cfg& cfg,
+                       uint32_t level, uint64_t first, uint64_t count, int64_t* sums_host,
+                       int32_t* y_dev) {
+    require(model.model == VXB_MODEL_MM_TAULEAP, "invalid-argument", "not the tau-leap model");
+    require(cfg.refine >= 2 && level < cfg.levels, "invalid-argument", "bad level");
+    TauParams p{};
+    p.first = first;
+    p.count = count;
+    const uint64_t lv = level;
+    p.seed_hash = splitmix64(vxb_derive_seed(cfg.seed, &lv, 1));
+    p.n_fine = level_steps(cfg, level);
+    p.level = level;
+    p.refine = cfg.refine;
+    p.tau = cfg.t_end / static_cast<double>(p.n_fine);
+    for (int k = 0; k < 3; ++k) p.rate[k] = model.consts[4 + k];
+    for (int k = 0; k < 4; ++k) p.init[k] = static_cast<int32_t>(model.consts[k]);
+    Scratch d_sums(ctx, 4 * sizeof(long long));
+    VXB_CUDA(cudaMemsetAsync(d_sums.as<void>(), 0, 4 * sizeof(long long), ctx->stream));
+    p.sums = d_sums.as<long long>();
+    p.y_out = y_dev;
+    if (count) {
+        LaunchScope scope(ctx, VXB_K_TAULEAP);
+        tauleap_kernel<<<grid_for(count, kTlBlock), kTlBlock, 0, ctx->stream>>>(p);
+        check_launch("tauleap_kernel");
+    }
+    long long h[4];
+    VXB_CUDA(cudaMemcpyAsync(h, p.sums, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int k = 0; k < 4; ++k) sums_host[k] = h[k];
+}
+
+}  // namespace vxb
+
+using namespace vxb;
+
+extern "C" int vxb_mlmc_level(vxb_ctx* ctx, const vxb_model* model, const vxb_mlmc_cfg* cfg,
+                              uint32_t level, uint64_t first, uint64_t count, int64_t* sums,
+                              int32_t* y_out) {
+    return guarded([&] {
+        use(ctx);
+        require(model && cfg && sums, "invalid-argument", "null argument");
+        Staged d_y(ctx, y_out, count * sizeof(int32_t), false, true);
+        int64_t h[4];
+        mlmc_level_device(ctx, *model, *cfg, level, first, count, h, d_y.as<int32_t>());
+        if (is_device_pointer(sums))
+            VXB_CUDA(cudaMemcpy(sums, h, sizeof(h), cudaMemcpyHostToDevice));
+        else
+            for (int k = 0; k < 4; ++k) sums[k] = h[k];
+        d_y.finish();
+        VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+// Estimator (vxo_mlmc_tauleap): sum of the level means; variance = sum var_l / paths.
+extern "C" int vxb_mlmc_tauleap(vxb_ctx* ctx, const vxb_model* model, const vxb_mlmc_cfg* cfg,
+                                vxb_mlmc_out* out) {
+    return guarded([&] {
+        use(ctx);
+        require(model && cfg && out, "invalid-argument", "null argument");
+        require(cfg->paths >= 2, "insufficient-data", "variance needs at least two values");
+        double est = 0.0, var = 0.0;
+        uint64_t steps = level_steps(*cfg, 0);
+        for (uint32_t l = 0; l < cfg->levels; ++l) {
+            int64_t sums[4];
+            mlmc_level_device(ctx, *model, *cfg, l, 0, cfg->paths, sums, nullptr);
+            const double n = static_cast<double>(cfg->paths);
+            const double mean = static_cast<double>(sums[0]) / n;
+            const double v =
+                (static_cast<double>(sums[1]) - static_cast<double>(sums[0]) * mean) / (n - 1.0);
+            if (out->level_mean) out->level_mean[l] = mean;
+            if (out->level_var) out->level_var[l] = v;
+            if (out->level_cost)
+                out->level_cost[l] =
+                    static_cast<double>(l == 0 ? steps : steps + steps / cfg->refine);
+            est += mean;
+            var += v / n;
+            steps *= cfg->refine;
+        }
+        out->estimate = est;
+        out->std_error = std::sqrt(var);
+    });
+}

@@ -1,0 +1,183 @@
+"""GPU parity tests for configs 2-4 and the SMC building blocks, through the C
+ABI, against the oracle (bit-exact for counts, indices and the canonical-order
+fp64 reductions; stated tolerances where the reference calls libm)."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_1902_09046_b200 import _abi as A, lib, models as M
+
+pytestmark = pytest.mark.gpu
+
+
+def eq(a, b):
+    return np.array_equal(np.asarray(a), np.asarray(b), equal_nan=True)
+
+
+def mm_cfg(levels=3, paths=20000, seed=1337):
+    c = A.vxb_mlmc_cfg()
+    c.levels, c.refine, c.tau0, c.t_end, c.paths, c.seed = levels, 4, 1.0, 30.0, paths, seed
+    return c
+
+
+def smc_cfg(n=1500, gens=4, seed=1337, round_size=0):
+    c = A.vxb_abcsmc_cfg()
+    c.particles, c.generations, c.quantile, c.kernel_scale = n, gens, 0.5, 2.0
+    c.jitter, c.round_size, c.max_rounds, c.seed = 1e-10, round_size, 0, seed
+    return c
+
+
+# ----------------------------------------------------------------- config 2
+def test_ppp_pvalues_parity(ctx, oracle, golden):
+    n, m_total = 100, 20000
+    mdl = M.normal_mean_model(n)
+    lam = np.array(M.lambda_grid(64))
+    ln = np.array([-0.5 * math.log(2.0 * math.pi * (l * l + 1.0 / n)) for l in lam])
+    y_obs = 3.0 + oracle.fill_gaussian(oracle.derive_seed(2, [90]), 0, 0, n)
+    ybar_obs = float(y_obs.mean())
+    want_c, want_p, want_y = oracle.ppp_pvalues(mdl, lam, ln, m_total, 0, m_total, 1337, ybar_obs, want_ybar=True)
+    got_c, got_p, got_y = ctx.ppp_pvalues(mdl, lam, ln, m_total, 0, m_total, 1337, ybar_obs, want_ybar=True)
+    assert eq(got_y, want_y)                       # every dataset mean bit-identical
+    assert eq(got_c, want_c) and eq(got_p, want_p)
+    # golden: reference-drawn datasets (weak_info.cpp draw order)
+    lam6, ln6 = np.full(6, 0.7), np.full(6, golden["nm_lognorm"][0])
+    _, _, yb = ctx.ppp_pvalues(mdl, lam6, ln6, 1000, 10, 40, 1337, 0.3, want_ybar=True)
+    assert eq(yb[5], golden["nm_ybar"])
+    # shards add up; odd n; error codes
+    c1, _, _ = ctx.ppp_pvalues(mdl, lam, ln, m_total, 0, 7001, 1337, ybar_obs)
+    c2, _, _ = ctx.ppp_pvalues(mdl, lam, ln, m_total, 7001, m_total - 7001, 1337, ybar_obs)
+    assert eq(c1 + c2, want_c)
+    m7 = M.normal_mean_model(7)
+    a = oracle.ppp_pvalues(m7, lam[:5], ln[:5], 500, 0, 500, 3, 0.2, want_ybar=True)
+    b = ctx.ppp_pvalues(m7, lam[:5], ln[:5], 500, 0, 500, 3, 0.2, want_ybar=True)
+    assert eq(a[0], b[0]) and eq(a[2], b[2])
+    with pytest.raises(lib.VxbError) as e:
+        ctx.ppp_pvalues(mdl, -lam, ln, 10, 0, 10, 1, 0.0)
+    assert e.value.code == "invalid-argument"
+
+
+def test_ppp_fast_generator_matches_closed_form(ctx):
+    n, m_total = 100, 400000
+    mdl = M.normal_mean_model(n, rng=A.VXB_RNG_FAST)
+    lam = np.array(M.lambda_grid(16))
+    ln = np.array([-0.5 * math.log(2.0 * math.pi * (l * l + 1.0 / n)) for l in lam])
+    ybar_obs = 2.95
+    counts, pv, _ = ctx.ppp_pvalues(mdl, lam, ln, m_total, 0, m_total, 99, ybar_obs)
+    for k, l in enumerate(lam):
+        exact = math.erfc(abs(ybar_obs) / math.sqrt(2.0 * (l * l + 1.0 / n)))
+        se = math.sqrt(max(exact * (1 - exact), 1e-12) / m_total)
+        assert abs(pv[k] - exact) < 5 * se + 2.0 / m_total
+
+
+# ------------------------------------------------------------- SMC pieces
+def test_ess_logsumexp_resample(ctx, oracle, golden):
+    lw = golden["smc_lw"]
+    assert abs(ctx.ess(lw) / golden["smc_ess"][0] - 1.0) < 1e-12      # libm exp on both sides
+    assert abs(ctx.ess(np.log([1.0, 1.0, 2.0])) - 16.0 / 6.0) < 1e-12
+    assert abs(ctx.logsumexp(lw) - oracle.logsumexp(lw)) < 1e-12
+    assert ctx.logsumexp(np.array([-np.inf, -np.inf])) == -np.inf
+    with pytest.raises(lib.VxbError) as e:
+        ctx.ess(np.array([-np.inf, -np.inf]))
+    assert e.value.code == "degenerate-ensemble"
+    out, anc = ctx.resample_multinomial(lw, golden["smc_particles"], 2718, 3 | (5 << 16))
+    assert eq(anc, golden["smc_ancestors"]) and eq(out, golden["smc_resampled"])
+    rs = np.random.RandomState(9)
+    lw = rs.normal(size=100000) * 3
+    parts = rs.normal(size=(100000, 3))
+    o_out, o_anc = oracle.resample_multinomial(lw, parts, 77, 9)
+    g_out, g_anc = ctx.resample_multinomial(lw, parts, 77, 9)
+    # indices agree except where device exp and libm exp differ in the last ulp at a CDF boundary
+    assert (g_anc != o_anc).mean() < 1e-4
+    same = g_anc == o_anc
+    assert eq(g_out[same], o_out[same])
+    # point mass: every draw picks it
+    lw0 = np.full(1000, -np.inf)
+    lw0[123] = 0.0
+    _, anc0 = ctx.resample_multinomial(lw0, parts[:1000], 1, 0)
+    assert (anc0 == 123).all()
+    # unbiasedness: ancestor frequencies follow the weights
+    w = np.exp(lw - lw.max())
+    w /= w.sum()
+    top = np.argsort(w)[-5:]
+    cnt = np.bincount(g_anc.astype(np.int64), minlength=lw.size)
+    for i in top:
+        assert abs(cnt[i] - lw.size * w[i]) < 6 * math.sqrt(lw.size * w[i]) + 3
+
+
+# ----------------------------------------------------------------- config 3
+def test_abcsmc_stages_parity(ctx, oracle, golden):
+    m = M.logistic_model()
+    obs = golden["logistic_observed"]
+    n = 3000
+    key = M.keying(oracle.derive_seed(5, [0]))
+    theta, _, rho, f = oracle.abc_prior_predictive(m, key, n, 0, n, obs, want_summaries=False)
+    rs = np.random.RandomState(1)
+    w = rs.uniform(0.5, 1.5, size=n)
+    w /= oracle.canon_sum(w)
+    mean, cov, s2 = oracle.weighted_moments(theta, w)
+    chol = oracle.make_kernel(cov, 2.0)
+    cum = oracle.canon_cumsum(w)
+    eps = oracle.quantile(rho, 0.5)
+    want = oracle.abcsmc_propose(m, 5, 1, 100, 4000, theta, cum, chol, obs, eps)
+    got = ctx.abcsmc_propose(m, 5, 1, 100, 4000, theta, cum, chol, obs, eps)
+    assert eq(got[2], want[2]) and eq(got[0], want[0]) and eq(got[1], want[1])
+    assert set(np.unique(want[2])) >= {0, 1, 2}      # accepted, rejected and outside-prior rows
+    new = want[0][want[2] == 1][:500]
+    w_o = oracle.abcsmc_weights(new, theta, w, chol)
+    w_g = ctx.abcsmc_weights(new, theta, w, chol)
+    assert eq(w_g, w_o)                               # sequential-order sum reproduced exactly
+
+
+@pytest.mark.timeout(900)
+def test_abcsmc_run_parity(ctx, oracle, golden):
+    m = M.logistic_model()
+    obs = golden["logistic_observed"]
+    for cfg in (smc_cfg(n=2000, gens=5), smc_cfg(n=777, gens=3, seed=9, round_size=300)):
+        want = oracle.abcsmc_run(m, cfg, obs)
+        got = ctx.abcsmc_run(m, cfg, obs)
+        for k in ("epsilon", "proposals", "accept_rate", "theta", "rho", "weight", "ess", "mean", "cov"):
+            assert eq(got[k], want[k]), k
+        assert abs(got["weight"].sum() - 1.0) < 1e-12
+
+
+# ----------------------------------------------------------------- config 4
+def test_tauleap_parity(ctx, oracle):
+    m = M.mm_tauleap_model()
+    cfg = mm_cfg(levels=5, paths=4000)
+    for level in range(5):
+        s_o, y_o = oracle.mlmc_level(m, cfg, level, 0, 4000, want_y=True)
+        s_g, y_g = ctx.mlmc_level(m, cfg, level, 0, 4000, want_y=True)
+        assert eq(y_g, y_o) and eq(s_g, s_o)          # every coupled path identical, exact sums
+        a, _ = ctx.mlmc_level(m, cfg, level, 0, 1234)
+        b, _ = ctx.mlmc_level(m, cfg, level, 1234, 4000 - 1234)
+        assert eq(a + b, s_o)
+    res_o = oracle.mlmc_tauleap(m, cfg)
+    res_g = ctx.mlmc_tauleap(m, cfg)
+    for k in ("level_mean", "level_var", "level_cost"):
+        assert eq(res_g[k], res_o[k])
+    assert res_g["estimate"] == res_o["estimate"] and res_g["std_error"] == res_o["std_error"]
+    # other networks / rates through the same kernel
+    m2 = M.mm_tauleap_model(x0=(40, 7, 3, 1), rates=(5e-3, 2e-2, 0.3))
+    cfg2 = mm_cfg(levels=3, paths=1000, seed=5)
+    cfg2.refine, cfg2.tau0, cfg2.t_end = 3, 0.5, 6.0
+    for level in range(3):
+        s_o, y_o = oracle.mlmc_level(m2, cfg2, level, 0, 1000, want_y=True)
+        s_g, y_g = ctx.mlmc_level(m2, cfg2, level, 0, 1000, want_y=True)
+        assert eq(y_g, y_o) and eq(s_g, s_o)
+    with pytest.raises(lib.VxbError) as e:
+        ctx.mlmc_level(m, cfg, 7, 0, 10)
+    assert e.value.code == "invalid-argument"
+
+
+def test_tauleap_full_level_properties(ctx):
+    """BASELINE size for one level (1e6 paths): integer sums are shard-additive
+    and the level mean sits where the small-sample oracle runs put it."""
+    m = M.mm_tauleap_model()
+    cfg = mm_cfg(levels=6, paths=1_000_000)
+    whole, _ = ctx.mlmc_level(m, cfg, 2, 0, 1_000_000)
+    parts = [ctx.mlmc_level(m, cfg, 2, b, 250_000)[0] for b in range(0, 1_000_000, 250_000)]
+    assert eq(sum(parts), whole)
+    mean = whole[0] / 1e6
+    var = (whole[1] - whole[0] * mean) / (1e6 - 1)
+    assert abs(mean) < 1.0 and 0.0 < var < 10.0
