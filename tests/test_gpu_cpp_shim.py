@@ -1,0 +1,64 @@
+"""GPU test of the C++ shim (paper_1902_09046_b200/cpp/vexbayes): a program
+written against the reference's own API names is compiled with g++, linked to
+libvexbayes_cuda.so and its output compared with the oracle / reference."""
+import math
+import os
+import struct
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_1902_09046_b200 import _abi as A, lib, models as M
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def parse(out):
+    res = {}
+    for line in out.strip().splitlines():
+        name, *rest = line.split()
+        res[name] = rest
+    return res
+
+
+def hexd(tokens):
+    return np.array([struct.unpack("<d", bytes.fromhex(t)[::-1])[0] for t in tokens[1:]])
+
+
+def test_cpp_shim_matches_oracle(tmp_path, oracle, golden):
+    exe = tmp_path / "test_shim"
+    pkg = os.path.join(ROOT, "paper_1902_09046_b200")
+    cmd = ["g++", "-std=c++20", "-O1", "-I", os.path.join(pkg, "cpp"),
+           os.path.join(ROOT, "tests", "cpp", "test_shim.cpp"), "-o", str(exe),
+           "-L", pkg, "-lvexbayes_cuda", f"-Wl,-rpath,{pkg}"]
+    subprocess.run(cmd, check=True)
+    run = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert run.returncode == 0, run.stdout + run.stderr
+    r = parse(run.stdout)
+    m = M.logistic_model()
+    obs = hexd(r["observed"])
+    assert np.array_equal(obs, golden["logistic_observed"])
+    key = M.keying(1337, A.VXB_KEY_WORKER, 3, 4)
+    p, s, rho, f = oracle.abc_prior_predictive(m, key, 500, 0, 500, obs)
+    assert np.array_equal(hexd(r["params"]), p.ravel())
+    assert np.array_equal(hexd(r["summaries"]), s.ravel())
+    assert np.array_equal(hexd(r["rho"]), rho)
+    eps, idx = oracle.select_epsilon(rho, f, 0.05)
+    assert hexd(r["epsilon"])[0] == eps
+    assert [int(t) for t in r["accepted"][1:]] == idx.tolist()
+    assert float(r["discrepancy"][0]) == 5.0
+    p2, _, rho2, f2 = oracle.abc_prior_predictive(m, M.keying(1337), 20000, 0, 20000, obs, want_summaries=False)
+    want = np.nonzero((rho2 <= eps) & (f2 == 0))[0]
+    assert int(r["reject"][0]) == len(want) and [int(t) for t in r["reject"][1:]] == want.tolist()
+    assert r["errors"] == ["6"]
+    g = oracle.fill_gaussian(7, 1, 0, 768)
+    assert abs(float(r["ess"][0]) / oracle.ess(g[512:]) - 1.0) < 1e-12
+    out, anc = oracle.resample_multinomial(g[512:], g[:512].reshape(256, 2), 2718, 3)
+    assert np.array_equal(hexd(r["resampled"]), out.ravel())
+    lam = np.array([0.1, 1.0, 10.0, 100.0])
+    ln = np.array([-0.5 * math.log(2.0 * math.pi * (l * l + 1.0 / 100)) for l in lam])
+    counts, _, _ = oracle.ppp_pvalues(M.normal_mean_model(100), lam, ln, 20000, 0, 20000, 1337, 2.9)
+    assert [int(t) for t in r["counts"]] == counts.tolist()
+    assert [float(t) for t in r["pvalues"]] == [0.25, 0.75]
