@@ -35,6 +35,12 @@ void build_fast_log_table(double* table) {
         table[2 * i] = c;
         table[2 * i + 1] = t;
     }
+    const double two_pi = 6.283185307179586476925286766559;
+    for (uint32_t i = 0; i < kTrigTableSize; ++i) {
+        const double a = two_pi * (static_cast<double>(i) + 0.5) / kTrigTableSize;
+        table[2 * (kLogTableSize + i)] = std::cos(a);
+        table[2 * (kLogTableSize + i) + 1] = std::sin(a);
+    }
 }
 
 // ------------------------------------------------------------ fill kernels
@@ -143,7 +149,7 @@ extern "C" int vxb_init(vxb_ctx** out, int device) {
             uint64_t threshold = ~0ull;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
         }
-        double table[2 * kLogTableSize];
+        double table[2 * kFastTableSize];
         build_fast_log_table(table);
         VXB_CUDA(cudaMalloc(&ctx->log_table, sizeof(table)));
         VXB_CUDA(cudaMemcpy(ctx->log_table, table, sizeof(table), cudaMemcpyHostToDevice));

@@ -20,7 +20,7 @@ struct AbcParams {
     LogisticModel model;
     double observed[VXB_MAX_SUMMARY];
     const double* theta_in;  // kKeyFixed: simulate at this theta, no prior draw
-    const double2* log_table;  // fast fp64 generator: (c_i, 2 ln c_i), kLogTableSize entries
+    const double2* log_table;  // fast fp64 generator: log + trig tables, kFastTableSize entries
     void* params;
     void* summaries;
     void* rho;
@@ -40,9 +40,9 @@ template <class Real, int kRng, bool kFma>
 __global__ void __launch_bounds__(kBlock, VXB_SIM_MIN_BLOCKS)
 logistic_abc_kernel(const __grid_constant__ AbcParams p) {
     // fast fp64 generator: stage the 2 KB log table in shared memory
-    __shared__ double2 s_log[(kRng == VXB_RNG_FAST && sizeof(Real) == 8) ? kLogTableSize : 1];
+    __shared__ double2 s_log[(kRng == VXB_RNG_FAST && sizeof(Real) == 8) ? kFastTableSize : 1];
     if (kRng == VXB_RNG_FAST && sizeof(Real) == 8) {
-        if (threadIdx.x < kLogTableSize) s_log[threadIdx.x] = p.log_table[threadIdx.x];
+        for (int i = threadIdx.x; i < kFastTableSize; i += kBlock) s_log[i] = p.log_table[i];
         __syncthreads();
     }
     const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;

@@ -39,9 +39,10 @@ struct PppParams {
 
 template <int kRng>
 __global__ void __launch_bounds__(kPppBlock) ppp_kernel(const __grid_constant__ PppParams p) {
-    __shared__ double2 s_log[kRng == VXB_RNG_FAST ? kLogTableSize : 1];
+    __shared__ double2 s_log[kRng == VXB_RNG_FAST ? kFastTableSize : 1];
     __shared__ unsigned int s_count;
-    if (kRng == VXB_RNG_FAST && threadIdx.x < kLogTableSize) s_log[threadIdx.x] = p.log_table[threadIdx.x];
+    if (kRng == VXB_RNG_FAST)
+        for (int i = threadIdx.x; i < kFastTableSize; i += kPppBlock) s_log[i] = p.log_table[i];
     if (threadIdx.x == 0) s_count = 0;
     __syncthreads();
     const uint32_t k = blockIdx.y;
