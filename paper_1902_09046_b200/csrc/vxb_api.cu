@@ -30,7 +30,7 @@ void build_fast_log_table(double* table) {
         double t = 2.0 * std::log(c);
         if (i == one_entry) {  // exact around u = 1
             c = 1.0;
-            t = 0.0;
+            t = 1e-300;  // keeps -2 ln u > 0 when u == 1 exactly (no NaN from rsqrt(0))
         }
         table[2 * i] = c;
         table[2 * i + 1] = t;

@@ -175,6 +175,21 @@ __device__ __forceinline__ Real logistic_path(const LogisticModel& m, const doub
             ++next;
         }
     };
+    if (stride % kB == 0 && steps == stride * m.n_obs) {
+        // regular grid (the BASELINE configs): whole batches between observations,
+        // no per-step bookkeeping
+        const uint32_t per = stride / kB;
+        for (uint32_t k = 0; k < m.n_obs; ++k) {
+            for (uint32_t i = 0; i < per; ++i) {
+                Real z[kB];
+                noise.next(z);
+#pragma unroll
+                for (uint32_t q = 0; q < kB; ++q) x = logistic_step<Real, A>(x, a, c, inv_k, z[q]);
+            }
+            observe();
+        }
+        return Exact::sqrt(ss);
+    }
     uint32_t j = 0;
     for (; j + kB <= steps; j += kB) {
         Real z[kB];
