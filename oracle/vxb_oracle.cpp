@@ -498,6 +498,120 @@ void abc_row(const Logistic& lg, Stream& s, const double* observed, const double
     }
 }
 
+// ===================================================== toggle-switch model
+// The reference's own SDE (toggle_switch.cpp), restated: prior box map
+// (:17-22), per-cell canonical variate layout cell_stride = 2T
+// (toggle_switch.hpp:52-57): relative to the aligned call position, cell c owns
+// positions [c*2T, (c+1)*2T); positions 2(j-1), 2(j-1)+1 are step j's (u, v)
+// increments, position 2(T-1) the observation normal, the last one padding.
+// Euler-Maruyama update with previous-step powers and floor at 1 (:46-62),
+// noisy observation (:64-69), 19 type-7 quantiles of the sorted observations
+// (:123-133).
+struct Toggle {
+    std::uint32_t steps, cells;
+    double lo[7], hi[7];
+    explicit Toggle(const vxb_model& m) : steps(m.steps), cells(static_cast<std::uint32_t>(m.consts[1])) {
+        require(m.model == VXB_MODEL_TOGGLE, "invalid-argument", "not the toggle-switch model");
+        require(m.dim == 7 && m.summary_dim == 19, "invalid-shape",
+                "toggle model has 7 parameters and 19 summaries");
+        require(cells >= 1, "invalid-shape", "toggle simulation needs at least one cell");
+        for (int k = 0; k < 7; ++k) {
+            lo[k] = m.prior_lo[k];
+            hi[k] = m.prior_hi[k];
+            require(lo[k] <= hi[k], "invalid-range", "uniform lower bound exceeds upper bound");
+        }
+    }
+    std::uint64_t padded(std::uint64_t v) const { return (cells + v - 1) / v * v; }
+    // stream positions one row consumes: 7 uniforms, align, padded cells x 2T
+    std::uint64_t row_stride(std::uint64_t v) const { return 8 + padded(v) * 2 * steps; }
+    void sample_prior(Stream& s, double* theta) const {
+        double unit[7];
+        for (int k = 0; k < 7; ++k) unit[k] = s.next_uniform(0.0, 1.0);
+        for (int k = 0; k < 7; ++k) theta[k] = lo[k] + unit[k] * (hi[k] - lo[k]);
+    }
+    // y[cells] for one parameter vector; s.pos must be the aligned call position
+    void simulate(const double* th, Stream& s, std::uint64_t v, double* y) const {
+        const double mu = th[0], sigma = th[1], gamma = th[2];
+        const double alpha_u = th[3], alpha_v = th[4], beta_u = th[5], beta_v = th[6];
+        const std::uint64_t b0 = s.pos;
+        for (std::uint64_t c = 0; c < cells; ++c) {
+            s.pos = b0 + c * 2 * steps;
+            double u = 10.0, w = 10.0;
+            for (std::uint32_t j = 1; j < steps; ++j) {
+                const double zu = s.next_gaussian(0.0, 1.0);
+                const double zv = s.next_gaussian(0.0, 1.0);
+                const double p_u = pow_pos(w, beta_u);
+                const double p_v = pow_pos(u, beta_v);
+                double ut = u * 0.97;
+                ut += alpha_u / (1.0 + p_u) - 1.0;
+                double vt = w * 0.97;
+                vt += alpha_v / (1.0 + p_v) - 1.0;
+                ut += 0.5 * zu;
+                vt += 0.5 * zv;
+                u = ut >= 1.0 ? ut : 1.0;
+                w = vt >= 1.0 ? vt : 1.0;
+            }
+            const double eta = s.next_gaussian(0.0, 1.0);
+            const double obs = u + mu + sigma * mu * eta / pow_pos(u, gamma);
+            y[c] = obs >= 1.0 ? obs : 1.0;
+        }
+        s.pos = b0 + padded(v) * 2 * steps;
+    }
+    // returns false for the rows the reference would flag (Error inside simulate)
+    bool summaries(const double* th, Stream& s, std::uint64_t v, double* q) const {
+        if (steps < 2 || cells < 19) return false;  // invalid-horizon / insufficient-data
+        std::vector<double> y(cells);
+        simulate(th, s, v, y.data());
+        std::sort(y.begin(), y.end());
+        for (int k = 0; k < 19; ++k) q[k] = quantile_sorted(y.data(), cells, 0.05 * static_cast<double>(k + 1));
+        return true;
+    }
+};
+
+void toggle_prior_predictive(const vxb_model* m, const vxb_keying* key, std::uint64_t n_total,
+                             std::uint64_t first, std::uint64_t count, const double* observed,
+                             double* params, double* summaries, double* rho, std::uint8_t* failed,
+                             unsigned threads) {
+    const Toggle tg(*m);
+    require(m->precision == VXB_F64, "invalid-argument", "the toggle model is fp64");
+    std::vector<std::uint64_t> ranges;
+    std::uint64_t v = 1;
+    if (key->mode == VXB_KEY_WORKER) {
+        require(key->workers >= 1, "invalid-shape", "need at least one worker");
+        require(supported_width(key->block_width), "invalid-shape", "unsupported block width");
+        v = key->block_width;
+        ranges.resize(2 * key->workers);
+        partition(n_total, key->workers, v, ranges.data());
+    }
+    parallel_for(count, threads, [&](std::uint64_t r) {
+        const std::uint64_t row = first + r;
+        std::uint64_t id = row, base = 0;
+        if (key->mode == VXB_KEY_WORKER) {
+            std::uint64_t w = 0;
+            while (!(row >= ranges[2 * w] && row < ranges[2 * w + 1])) ++w;
+            id = w;
+            base = (row - ranges[2 * w]) * tg.row_stride(v);
+        }
+        Stream s(key->seed, id);
+        s.pos = base;
+        double theta[7], q[19];
+        tg.sample_prior(s, theta);
+        s.align_even();
+        double dist = std::numeric_limits<double>::quiet_NaN();
+        std::uint8_t bad = 0;
+        if (tg.summaries(theta, s, v, q)) {
+            dist = discrepancy<double>(q, observed, 19);
+        } else {
+            bad = 1;
+            std::fill(q, q + 19, 0.0);
+        }
+        if (params) std::copy(theta, theta + 7, params + r * 7);
+        if (summaries) std::copy(q, q + 19, summaries + r * 19);
+        if (rho) rho[r] = dist;
+        if (failed) failed[r] = bad;
+    });
+}
+
 }  // namespace
 
 extern "C" {
@@ -577,6 +691,11 @@ int vxo_abc_prior_predictive(const vxb_model* m, const vxb_keying* key, std::uin
     return guarded([&] {
         require(n_total >= 1, "invalid-shape", "need at least one prior predictive sample");
         require(first + count <= n_total, "invalid-shape", "row range exceeds the job");
+        if (m->model == VXB_MODEL_TOGGLE) {
+            toggle_prior_predictive(m, key, n_total, first, count, observed, params, summaries, rho,
+                                    failed, threads);
+            return;
+        }
         const Logistic lg(*m);
         const std::size_t sd = lg.n_obs;
         std::vector<double> obs(observed, observed + sd);
@@ -620,6 +739,16 @@ int vxo_abc_prior_predictive(const vxb_model* m, const vxb_keying* key, std::uin
 int vxo_simulate_at(const vxb_model* m, const double* theta, std::uint64_t seed, std::uint64_t id,
                     std::uint64_t pos, double* summary) {
     return guarded([&] {
+        if (m->model == VXB_MODEL_TOGGLE) {  // bench.cpp:69-77 (block width 1: no padding)
+            const Toggle tg(*m);
+            require(tg.steps >= 2, "invalid-horizon", "toggle simulation needs at least two time points");
+            require(tg.cells >= 19, "insufficient-data", "need at least 19 observations for the quantile summary");
+            Stream st(seed, id);
+            st.pos = pos;
+            st.align_even();
+            tg.summaries(theta, st, 1, summary);
+            return;
+        }
         const Logistic lg(*m);
         Stream s(seed, id);
         s.pos = pos;

@@ -9,6 +9,12 @@ namespace vxb {
 // vxb_logistic.cu
 LogisticModel make_logistic(const vxb_model& m);
 
+// vxb_toggle.cu
+void toggle_launch(vxb_ctx* ctx, const vxb_model& m, const Keying& key, uint64_t first,
+                   uint64_t count, uint64_t block_width, const double* observed_host,
+                   const double* theta_dev, double* params, double* summaries, double* rho,
+                   uint8_t* failed);
+
 // vxb_select.cu
 void compact_accepted_device(vxb_ctx* ctx, int precision, const void* rho_dev,
                              const uint8_t* failed_dev, uint64_t n, double epsilon,

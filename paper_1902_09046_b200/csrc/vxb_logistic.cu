@@ -9,8 +9,7 @@
 #include <cmath>
 #include <limits>
 
-#include "vxb_common.cuh"
-#include "vxb_logistic.cuh"
+#include "vxb_internal.cuh"
 
 namespace vxb {
 
@@ -214,12 +213,6 @@ void launch_abc(vxb_ctx* ctx, const vxb_model& m, AbcParams p) {
         launch_abc1<double>(ctx, p, m.rng, fma);
 }
 
-// implemented in vxb_select.cu
-void compact_accepted_device(vxb_ctx* ctx, int precision, const void* rho_dev,
-                             const uint8_t* failed_dev, uint64_t n, double epsilon,
-                             uint64_t index_base, uint64_t cap, uint64_t* n_accepted_host,
-                             uint64_t* idx_dev);
-
 }  // namespace vxb
 
 using namespace vxb;
@@ -234,6 +227,24 @@ extern "C" int vxb_abc_prior_predictive(vxb_ctx* ctx, const vxb_model* model,
         require(model && key && observed, "invalid-argument", "null argument");
         require(n_total >= 1, "invalid-shape", "need at least one prior predictive sample");
         require(first + count <= n_total, "invalid-shape", "row range exceeds the job");
+        if (model->model == VXB_MODEL_TOGGLE) {  // the reference's own SDE: vxb_toggle.cu
+            const Keying tk = make_keying(*key, *model, n_total);
+            Staged t_params(ctx, params, count * 7 * 8, false, true);
+            Staged t_summ(ctx, summaries, count * 19 * 8, false, true);
+            Staged t_rho(ctx, rho, count * 8, false, true);
+            Staged t_failed(ctx, failed, count, false, true);
+            toggle_launch(ctx, *model, tk, first, count,
+                          key->mode == VXB_KEY_WORKER ? key->block_width : 1, observed, nullptr,
+                          t_params.as<double>(), t_summ.as<double>(), t_rho.as<double>(),
+                          t_failed.as<uint8_t>());
+            t_params.finish();
+            t_summ.finish();
+            t_rho.finish();
+            t_failed.finish();
+            if (t_params.staged() || t_summ.staged() || t_rho.staged() || t_failed.staged())
+                VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+            return;
+        }
         AbcParams p{};
         p.model = make_logistic(*model);
         p.key = make_keying(*key, *model, n_total);
@@ -274,6 +285,23 @@ extern "C" int vxb_simulate_at(vxb_ctx* ctx, const vxb_model* model, const doubl
         require(model && theta && summary, "invalid-argument", "null argument");
         require(model->rng == VXB_RNG_REF, "invalid-argument",
                 "simulate_at is defined for the reference generator");
+        if (model->model == VXB_MODEL_TOGGLE) {
+            require(model->steps >= 2, "invalid-horizon",
+                    "toggle simulation needs at least two time points");
+            require(model->consts[1] >= 19.0, "insufficient-data",
+                    "need at least 19 observations for the quantile summary");
+            Keying tk{};
+            tk.mode = kKeyFixed;
+            tk.fixed_key = stream_key(splitmix64(seed), stream_id);
+            tk.fixed_pos = pos;
+            Staged t_theta(ctx, theta, 7 * sizeof(double), true, false);
+            Staged t_summ(ctx, summary, 19 * sizeof(double), false, true);
+            toggle_launch(ctx, *model, tk, 0, 1, 1, nullptr, t_theta.as<double>(), nullptr,
+                          t_summ.as<double>(), nullptr, nullptr);
+            t_summ.finish();
+            VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+            return;
+        }
         AbcParams p{};
         p.model = make_logistic(*model);
         p.key.mode = kKeyFixed;

@@ -27,6 +27,28 @@ def logistic_model(steps=2000, obs_stride=100, dt=0.01, x0=10.0,
     return m
 
 
+TOGGLE_PRIOR_LO = (250.0, 0.05, 0.05, 0.0, 0.0, 0.0, 0.0)
+TOGGLE_PRIOR_HI = (400.0, 0.5, 0.35, 50.0, 50.0, 7.0, 7.0)
+TOGGLE_MIDPOINT = (325.0, 0.275, 0.2, 25.0, 25.0, 3.5, 3.5)  # bench.cpp:72 "true" parameters
+
+
+def toggle_model(steps=600, cells=8000, rng=A.VXB_RNG_REF):
+    """The reference's toggle-switch SDE (toggle_switch.hpp:16-82): theta =
+    (mu, sigma, gamma, alpha_u, alpha_v, beta_u, beta_v), C cells, T time points,
+    summaries = 19 quantiles of the noisy terminal observations."""
+    m = A.vxb_model()
+    m.model = A.VXB_MODEL_TOGGLE
+    m.precision, m.rng, m.arith = A.VXB_F64, rng, A.VXB_ARITH_EXACT
+    m.dim, m.summary_dim = 7, 19
+    m.steps, m.obs_stride = steps, steps
+    m.x0 = 10.0
+    for k in range(7):
+        m.prior_lo[k] = TOGGLE_PRIOR_LO[k]
+        m.prior_hi[k] = TOGGLE_PRIOR_HI[k]
+    m.consts[1] = float(cells)
+    return m
+
+
 def normal_mean_model(n_data=100, rng=A.VXB_RNG_REF, arith=A.VXB_ARITH_EXACT):
     """y_i ~ N(theta, 1), theta ~ N(0, lambda^2) (config 2)."""
     m = A.vxb_model()

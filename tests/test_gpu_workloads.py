@@ -181,3 +181,34 @@ def test_tauleap_full_level_properties(ctx):
     mean = whole[0] / 1e6
     var = (whole[1] - whole[0] * mean) / (1e6 - 1)
     assert abs(mean) < 1.0 and 0.0 < var < 10.0
+
+
+# ------------------------------------------- toggle switch
+def test_toggle_switch_parity(ctx, oracle, golden):
+    """The reference's own SDE, through the reference's own sampler keying:
+    bit-identical summaries, distances and selection (KAT of SURVEY.md 8c)."""
+    m = M.toggle_model(100, 256)
+    obs = ctx.simulate_at(m, M.TOGGLE_MIDPOINT, lib.derive_seed(1337, [90]), 0, 0)
+    assert eq(obs, golden["toggle_observed"])
+    key = M.keying(1337, A.VXB_KEY_WORKER, 1, 4)
+    p, s, rho, f = ctx.abc_prior_predictive_host(m, key, 256, 0, 256, obs)
+    assert rho[0] == 445.69940013687017
+    assert eq(rho, golden["toggle_rho"]) and eq(s[0], golden["toggle_summ0"])
+    eps, idx, nacc = ctx.select_epsilon(rho, f, 0.01)
+    assert eps == 208.44209220565364 and idx.tolist() == [120, 208, 239]
+    # other (workers, block width) layouts and particle keying against the oracle
+    m2 = M.toggle_model(37, 250)     # cells not a multiple of V: padded stream positions
+    obs2 = oracle.simulate_at(m2, M.TOGGLE_MIDPOINT, 5, 2, 7)
+    assert eq(ctx.simulate_at(m2, M.TOGGLE_MIDPOINT, 5, 2, 7), obs2)
+    for key in (M.keying(3, A.VXB_KEY_WORKER, 3, 16), M.keying(3, A.VXB_KEY_WORKER, 5, 1), M.keying(3)):
+        want = oracle.abc_prior_predictive(m2, key, 97, 10, 80, obs2)
+        got = ctx.abc_prior_predictive_host(m2, key, 97, 10, 80, obs2)
+        for g, w in zip(got, want):
+            assert eq(g, w)
+    # rows the reference flags: too few cells for 19 quantiles / a single time point
+    for bad in (M.toggle_model(50, 10), M.toggle_model(1, 64)):
+        want = oracle.abc_prior_predictive(bad, M.keying(1), 8, 0, 8, np.zeros(19))
+        got = ctx.abc_prior_predictive_host(bad, M.keying(1), 8, 0, 8, np.zeros(19))
+        assert (got[3] == 1).all() and np.isnan(got[2]).all() and (got[1] == 0).all()
+        for g, w in zip(got, want):
+            assert eq(g, w)
