@@ -207,7 +207,10 @@ int vxb_compact_accepted(vxb_ctx* ctx, int precision, const void* rho, const uin
 /* Fused fixed-epsilon rejection (config 1): simulate rows [first,first+count),
  * keep only rows with rho <= epsilon, ascending.  idx holds global row numbers.
  * params: cap x dim, rho: cap.  Trajectories, summaries and rejected rows never
- * leave the GPU. */
+ * leave the GPU.  If n_accepted points to DEVICE memory the call is fully
+ * asynchronous: the count is written there, idx/params/rho must be device
+ * buffers (or NULL), nothing is copied to the host and the stream is not
+ * synchronised -- steps can be queued back to back. */
 int vxb_abc_reject(vxb_ctx* ctx, const vxb_model* model, const vxb_keying* key,
                    uint64_t n_total, uint64_t first, uint64_t count, const double* observed,
                    double epsilon, uint64_t cap, uint64_t* n_accepted, uint64_t* idx,

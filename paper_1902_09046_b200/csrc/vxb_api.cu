@@ -168,6 +168,7 @@ extern "C" void vxb_shutdown(vxb_ctx* ctx) {
     for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
     cudaStreamDestroy(ctx->stream);
     cudaFree(ctx->log_table);
+    for (void* a : ctx->arena) cudaFree(a);
     delete ctx;
 }
 

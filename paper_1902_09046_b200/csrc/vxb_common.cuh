@@ -59,6 +59,10 @@ struct vxb_ctx {
     vxb_profile profile{};
     std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> pending;
     std::vector<cudaEvent_t> event_pool;
+    // grow-only device arenas for the large per-call temporaries (kept across
+    // calls so that the steady state performs no allocation at all)
+    void* arena[4] = {nullptr, nullptr, nullptr, nullptr};
+    size_t arena_bytes[4] = {0, 0, 0, 0};
 };
 
 namespace vxb {
@@ -122,6 +126,20 @@ private:
     size_t bytes_ = 0;
     bool owned_ = false, out_ = false;
 };
+
+// Persistent scratch slot `slot` of at least `bytes` (grow-only; the contents do
+// not survive a growth).  Stream-ordered use only.
+inline void* arena_get(vxb_ctx* ctx, int slot, size_t bytes) {
+    if (ctx->arena_bytes[slot] < bytes) {
+        VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (ctx->arena[slot]) VXB_CUDA(cudaFree(ctx->arena[slot]));
+        ctx->arena[slot] = nullptr;
+        ctx->arena_bytes[slot] = 0;
+        VXB_CUDA(cudaMalloc(&ctx->arena[slot], bytes));
+        ctx->arena_bytes[slot] = bytes;
+    }
+    return ctx->arena[slot];
+}
 
 // Stream-ordered scratch with RAII.
 class Scratch {

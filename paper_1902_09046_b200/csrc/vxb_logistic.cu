@@ -115,9 +115,12 @@ template <class Real, int kRng>
 __global__ void gather_accepted_kernel(Keying key, LogisticModel model, uint64_t first,
                                        const uint64_t* __restrict__ idx, uint64_t n_acc,
                                        const Real* __restrict__ rho_all, Real* params_out,
-                                       Real* rho_out) {
+                                       Real* rho_out,
+                                       const unsigned long long* __restrict__ n_acc_dev) {
     const uint64_t a = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (a >= n_acc) return;
+    // asynchronous form: the accepted count lives on the device, n_acc is the cap
+    const uint64_t lim = n_acc_dev ? min(n_acc, static_cast<uint64_t>(*n_acc_dev)) : n_acc;
+    if (a >= lim) return;
     const uint64_t row = idx[a];
     uint64_t k, base;
     locate_row(key, row, k, base);
@@ -345,20 +348,26 @@ extern "C" int vxb_abc_reject(vxb_ctx* ctx, const vxb_model* model, const vxb_ke
         for (uint32_t k = 0; k < p.model.n_obs; ++k)
             p.observed[k] = f32 ? static_cast<double>(static_cast<float>(observed[k])) : observed[k];
         const size_t real = f32 ? 4 : 8;
-        Scratch d_rho_all(ctx, count * real);
-        Scratch d_failed(ctx, count);
-        p.rho = d_rho_all.as<void>();
-        p.failed = d_failed.as<uint8_t>();
+        p.rho = arena_get(ctx, 0, count * real);
+        p.failed = static_cast<uint8_t*>(arena_get(ctx, 1, count));
         launch_abc(ctx, *model, p);
 
         Staged d_idx(ctx, idx, cap * sizeof(uint64_t), false, true);
         Scratch d_idx_tmp(ctx, d_idx.ptr() ? 0 : cap * sizeof(uint64_t));
         uint64_t* idx_dev = d_idx.ptr() ? d_idx.as<uint64_t>() : d_idx_tmp.as<uint64_t>();
+        // n_accepted in device memory => fully asynchronous call: the count stays on
+        // the device, nothing is copied to the host and the stream is not synchronised
+        const bool async = is_device_pointer(n_accepted);
+        require(!async || ((!idx || is_device_pointer(idx)) && (!params || is_device_pointer(params)) &&
+                           (!rho || is_device_pointer(rho))),
+                "invalid-argument", "a device-resident count needs device-resident outputs");
         uint64_t n_acc = 0;
         compact_accepted_device(ctx, model->precision, p.rho, p.failed, count, epsilon, first, cap,
-                                &n_acc, idx_dev);
-        *n_accepted = n_acc;
-        const uint64_t kept = n_acc < cap ? n_acc : cap;
+                                async ? n_accepted : &n_acc, idx_dev);
+        const unsigned long long* n_acc_dev =
+            async ? reinterpret_cast<const unsigned long long*>(n_accepted) : nullptr;
+        if (!async) *n_accepted = n_acc;
+        const uint64_t kept = async ? cap : (n_acc < cap ? n_acc : cap);
         Staged d_params(ctx, params, cap * 3 * real, false, true);
         Staged d_rho(ctx, rho, cap * real, false, true);
         if (kept && (params || rho)) {
@@ -368,23 +377,24 @@ extern "C" int vxb_abc_reject(vxb_ctx* ctx, const vxb_model* model, const vxb_ke
                 if (model->rng == VXB_RNG_FAST)
                     gather_accepted_kernel<float, VXB_RNG_FAST><<<grid, 128, 0, ctx->stream>>>(
                         p.key, p.model, first, idx_dev, kept, static_cast<const float*>(p.rho),
-                        d_params.as<float>(), d_rho.as<float>());
+                        d_params.as<float>(), d_rho.as<float>(), n_acc_dev);
                 else
                     gather_accepted_kernel<float, VXB_RNG_REF><<<grid, 128, 0, ctx->stream>>>(
                         p.key, p.model, first, idx_dev, kept, static_cast<const float*>(p.rho),
-                        d_params.as<float>(), d_rho.as<float>());
+                        d_params.as<float>(), d_rho.as<float>(), n_acc_dev);
             } else {
                 if (model->rng == VXB_RNG_FAST)
                     gather_accepted_kernel<double, VXB_RNG_FAST><<<grid, 128, 0, ctx->stream>>>(
                         p.key, p.model, first, idx_dev, kept, static_cast<const double*>(p.rho),
-                        d_params.as<double>(), d_rho.as<double>());
+                        d_params.as<double>(), d_rho.as<double>(), n_acc_dev);
                 else
                     gather_accepted_kernel<double, VXB_RNG_REF><<<grid, 128, 0, ctx->stream>>>(
                         p.key, p.model, first, idx_dev, kept, static_cast<const double*>(p.rho),
-                        d_params.as<double>(), d_rho.as<double>());
+                        d_params.as<double>(), d_rho.as<double>(), n_acc_dev);
             }
             check_launch("gather_accepted_kernel");
         }
+        if (async) return;
         d_idx.finish(kept * sizeof(uint64_t));
         d_params.finish(kept * 3 * real);
         d_rho.finish(kept * real);

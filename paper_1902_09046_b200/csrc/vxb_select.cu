@@ -321,7 +321,10 @@ void compact_device_t(vxb_ctx* ctx, const Real* rho, const uint8_t* failed, uint
     const uint64_t tile = static_cast<uint64_t>(kSelBlock) * kSelItems;
     const uint64_t n_blocks = (n + tile - 1) / tile;
     if (n_blocks == 0) {
-        *n_accepted_host = 0;
+        if (is_device_pointer(n_accepted_host))
+            VXB_CUDA(cudaMemsetAsync(n_accepted_host, 0, sizeof(uint64_t), ctx->stream));
+        else
+            *n_accepted_host = 0;
         return;
     }
     Scratch d_counts(ctx, n_blocks * sizeof(unsigned int));
@@ -345,6 +348,12 @@ void compact_device_t(vxb_ctx* ctx, const Real* rho, const uint8_t* failed, uint
         accept_write_kernel<Real><<<static_cast<unsigned>(n_blocks), kSelBlock, 0, ctx->stream>>>(
             rho, failed, n, eps, d_offsets.as<unsigned long long>(), index_base, cap, idx_dev);
         check_launch("accept_write_kernel");
+    }
+    if (is_device_pointer(n_accepted_host)) {
+        // device-resident count: the call stays asynchronous (no host round trip)
+        VXB_CUDA(cudaMemcpyAsync(n_accepted_host, d_total.as<void>(), sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
+        return;
     }
     unsigned long long total = 0;
     VXB_CUDA(cudaMemcpyAsync(&total, d_total.as<void>(), sizeof(total), cudaMemcpyDeviceToHost,

@@ -75,12 +75,20 @@ def sharded_reject(ctx, model, key, n_total, observed, eps, cap_fraction=0.01, g
     cap = max(1024, int(count * cap_fraction))
     dev = torch.device("cuda", ctx.device_info()["device"])
     real = torch.float32 if model.precision == A.VXB_F32 else torch.float64
-    idx = torch.empty(cap, dtype=torch.int64, device=dev)
-    params = torch.empty((cap, model.dim), dtype=real, device=dev)
-    rho = torch.empty(cap, dtype=real, device=dev)
+    # allocate on the library's stream so that the caching allocator's reuse of
+    # these buffers is ordered with the kernels that fill them
+    with torch.cuda.stream(torch.cuda.ExternalStream(ctx.stream(), device=dev)):
+        idx = torch.empty(cap, dtype=torch.int64, device=dev)
+        params = torch.empty((cap, model.dim), dtype=real, device=dev)
+        rho = torch.empty(cap, dtype=real, device=dev)
+        n_dev = torch.empty(1, dtype=torch.int64, device=dev)
+    if world == 1:
+        # single GPU: fully asynchronous -- the accepted count stays on the device,
+        # the host only enqueues (rows [0, count) of the returned buffers are valid)
+        ctx.abc_reject(model, key, n_total, begin, count, observed, eps, cap, idx=idx,
+                       params=params, rho=rho, n_accepted=n_dev)
+        return idx, params, rho, n_dev
     nacc, _, _, _ = ctx.abc_reject(model, key, n_total, begin, count, observed, eps, cap,
                                    idx=idx, params=params, rho=rho)
     k = min(nacc, cap)
-    if world == 1:
-        return idx[:k], params[:k], rho[:k], [nacc]
     return gather_accepted(idx[:k], params[:k], rho[:k], group)

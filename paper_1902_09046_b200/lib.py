@@ -244,8 +244,10 @@ class Context:
         return (idx[:k] if isinstance(idx, np.ndarray) else idx), nacc.value
 
     def abc_reject(self, model, key, n_total, first, count, observed, eps, cap, idx=None,
-                   params=None, rho=None):
-        """Fused fixed-epsilon rejection; host numpy outputs unless buffers are given."""
+                   params=None, rho=None, n_accepted=None):
+        """Fused fixed-epsilon rejection; host numpy outputs unless buffers are given.
+        With ``n_accepted`` a device int64 tensor (and device outputs) the call is
+        fully asynchronous: nothing returns to the host."""
         obs = np.ascontiguousarray(observed, dtype=np.float64)
         dt = np.float32 if model.precision == A.VXB_F32 else np.float64
         own = idx is None
@@ -253,6 +255,13 @@ class Context:
             idx = np.zeros(cap, dtype=np.uint64)
             params = np.zeros((cap, model.dim), dtype=dt)
             rho = np.zeros(cap, dtype=dt)
+        if n_accepted is not None:
+            # asynchronous form: the count is written to device memory, no host sync
+            self._check(self.lib.vxb_abc_reject(self.handle, C.byref(model), C.byref(key),
+                                                u64(n_total), u64(first), u64(count), _ptr(obs),
+                                                f64(eps), u64(cap), _ptr(n_accepted), _ptr(idx),
+                                                _ptr(params), _ptr(rho)))
+            return n_accepted, idx, params, rho
         nacc = u64()
         self._check(self.lib.vxb_abc_reject(self.handle, C.byref(model), C.byref(key),
                                             u64(n_total), u64(first), u64(count), _ptr(obs),

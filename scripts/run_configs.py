@@ -94,6 +94,17 @@ def main():
                       "std_error": out["std_error"], "level_mean": out["level_mean"].tolist(),
                       "level_var": out["level_var"].tolist(), "path_steps_per_s": steps / wall,
                       "kernels": prof}
+    # ---- the paper's toggle-switch workload: N = 8064, C = 8000, T = 600
+    n_t, c_t, t_t = (512 if quick else 8064), 8000, 600
+    tm = M.toggle_model(t_t, c_t)
+    tobs = ctx.simulate_at(tm, M.TOGGLE_MIDPOINT, lib.derive_seed(1337, [90]), 0, 0)
+    trho = torch.empty(n_t, dtype=torch.float64, device="cuda")
+    tkey = M.keying(1337, A.VXB_KEY_WORKER, 16, 4)   # the layout of the published 16-thread run
+    _, wall, prof = timed(ctx, lambda: ctx.abc_prior_predictive(tm, tkey, n_t, 0, n_t, tobs, rho=trho))
+    cell_steps = n_t * c_t * (t_t - 1)
+    res["toggle_paper"] = {"samples": n_t, "cells": c_t, "steps": t_t, "wall_ms": wall * 1e3,
+                           "cell_steps_per_s": cell_steps / wall, "sims_per_s": n_t / wall,
+                           "published_best_s": 69.0, "kernels": prof}
     print(json.dumps(res))
 
 
