@@ -1155,7 +1155,9 @@ int vxo_abcsmc_run(const vxb_model* m, const vxb_abcsmc_cfg* cfg, const double* 
 //  * level l >= 1: Anderson-Higham coupling of a fine path (tau_l) and a coarse
 //    path (M tau_l): per fine step and reaction r, with the coarse propensity
 //    frozen over the coarse step: m = min(af, ac), P1 ~ Poi(m tau),
-//    P2 ~ Poi((af-m) tau), P3 ~ Poi((ac-m) tau) at positions 10s + 3r + {0,1,2};
+//    P2 ~ Poi((af-m) tau), P3 ~ Poi((ac-m) tau); reaction r of fine step s owns
+//    the Philox block 3s + r: position 6s + 2r drives P1, position 6s + 2r + 1 the
+//    residual (at most one of P2, P3 has a positive rate, so they share it);
 //    fine fires P1+P2, coarse fires P1+P3;
 //  * path `i` of level l owns RngStream(derive_seed(seed,{l}), i).
 static int poisson_inv(double lam, double u, std::int64_t* iters) {
@@ -1231,10 +1233,12 @@ int vxo_mlmc_level(const vxb_model* m, const vxb_mlmc_cfg* cfg, std::uint32_t le
                         int kf[3], kc[3];
                         for (int q = 0; q < 3; ++q) {
                             const double mn = af[q] < ac[q] ? af[q] : ac[q];
-                            s.pos = 10 * st + 3 * q;
-                            const int p1 = poisson_inv(mn * tau, s.next_unit(), &it);
-                            const int p2 = poisson_inv((af[q] - mn) * tau, s.next_unit(), &it);
-                            const int p3 = poisson_inv((ac[q] - mn) * tau, s.next_unit(), &it);
+                            s.pos = 6 * st + 2 * q;
+                            const double u1 = s.next_unit(), u2 = s.next_unit();
+                            const int p1 = poisson_inv(mn * tau, u1, &it);
+                            // at most one residual rate is positive: they share u2
+                            const int p2 = poisson_inv((af[q] - mn) * tau, u2, &it);
+                            const int p3 = poisson_inv((ac[q] - mn) * tau, u2, &it);
                             kf[q] = p1 + p2;
                             kc[q] = p1 + p3;
                         }

@@ -13,8 +13,9 @@
 //  * level l>=1: Anderson-Higham coupling of a fine path (tau_l) with a coarse
 //    path (M tau_l) whose propensities are frozen over the coarse step; per fine
 //    step and reaction r: m = min(af, ac), P1~Poi(m tau), P2~Poi((af-m) tau),
-//    P3~Poi((ac-m) tau) at positions 10s + 3r + {0,1,2}; fine fires P1+P2,
-//    coarse fires P1+P3;
+//    P3~Poi((ac-m) tau); reaction r of fine step s owns Philox block 3s + r
+//    (position 6s+2r drives P1, position 6s+2r+1 the residual -- at most one of
+//    P2, P3 has a positive rate, so they share it); fine fires P1+P2, coarse P1+P3;
 //  * path i of level l owns RngStream(derive_seed(seed,{l}), i).
 // One path per thread, integer state in registers; only four 64-bit sums (and
 // optionally Y per path) leave the device, so the level sums are exact integers
@@ -106,25 +107,20 @@ __global__ void __launch_bounds__(kTlBlock) tauleap_kernel(const __grid_constant
                 if (phase == 0) c.prop(p.rate, ac);
                 if (++phase == p.refine) phase = 0;
                 f.prop(p.rate, af);
-                // positions 10s .. 10s+8 = pair blocks 5s .. 5s+4
-                uint64_t u[10];
-#pragma unroll
-                for (int b = 0; b < 5; ++b) {
-                    const Words w = philox2x64(key, 5 * st + b);
-                    u[2 * b] = w.w0;
-                    u[2 * b + 1] = w.w1;
-                }
                 int kf[3], kc[3];
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
+                    // reaction q of fine step st owns Philox block 3 st + q: word 0 drives
+                    // the common Poisson, word 1 the residual one
+                    const Words w = philox2x64(key, 3 * st + q);
+                    const bool fine_larger = af[q] > ac[q];
                     const double mn = af[q] < ac[q] ? af[q] : ac[q];
-                    const int p1 = poisson_inv(__dmul_rn(mn, p.tau), to_unit(u[3 * q]), s_inv, it);
-                    const int p2 = poisson_inv(__dmul_rn(__dsub_rn(af[q], mn), p.tau),
-                                               to_unit(u[3 * q + 1]), s_inv, it);
-                    const int p3 = poisson_inv(__dmul_rn(__dsub_rn(ac[q], mn), p.tau),
-                                               to_unit(u[3 * q + 2]), s_inv, it);
-                    kf[q] = p1 + p2;
-                    kc[q] = p1 + p3;
+                    const double mx = fine_larger ? af[q] : ac[q];
+                    const int p1 = poisson_inv(__dmul_rn(mn, p.tau), to_unit(w.w0), s_inv, it);
+                    // at most one of (af - m), (ac - m) is positive: one inversion serves both
+                    const int pr = poisson_inv(__dmul_rn(__dsub_rn(mx, mn), p.tau), to_unit(w.w1), s_inv, it);
+                    kf[q] = p1 + (fine_larger ? pr : 0);
+                    kc[q] = p1 + (fine_larger ? 0 : pr);
                 }
                 f.fire(kf[0], kf[1], kf[2]);
                 c.fire(kc[0], kc[1], kc[2]);
