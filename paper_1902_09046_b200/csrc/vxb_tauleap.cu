@@ -35,6 +35,7 @@ constexpr int kMaxPoisson = 1023;
 struct TauParams {
     uint64_t first, count;
     uint64_t seed_hash;  // splitmix64(derive_seed(seed,{level}))
+    FastKeys fast;       // VXB_RNG_FAST: Philox4x32 round keys of the seed
     uint64_t n_fine;     // fine steps
     uint32_t level, refine;
     double tau;
@@ -62,22 +63,44 @@ struct MM {
     }
 };
 
+template <class A>
 __device__ __forceinline__ int poisson_inv(double lam, double u, const double* __restrict__ inv,
                                            long long& iters) {
     if (!(lam > 0.0)) return 0;
-    double p = exp2_clamped<Exact>(__dmul_rn(-lam, kInvLn2));
+    double p = exp2_clamped<A>(A::mul(-lam, kInvLn2));
     double cdf = p;
     int k = 0;
     while (u > cdf && k < kMaxPoisson) {
         ++k;
-        p = __dmul_rn(__dmul_rn(p, lam), inv[k]);
-        cdf = __dadd_rn(cdf, p);
+        p = A::mul(A::mul(p, lam), inv[k]);
+        cdf = A::add(cdf, p);
         ++iters;
     }
     return k;
 }
 
+// Two uniforms of random block `block` of this path: the reference stream's pair
+// block (positions 2*block, 2*block+1) or, for the throughput generator, the
+// Philox4x32 block (block, level domain, path).
+template <int kRng>
+__device__ __forceinline__ void draw_pair(const TauParams& p, uint64_t key, uint64_t path,
+                                          uint64_t block, double& u0, double& u1) {
+    if (kRng == VXB_RNG_REF) {
+        const Words w = philox2x64(key, block);
+        u0 = to_unit(w.w0);
+        u1 = to_unit(w.w1);
+    } else {
+        const Words32 w = philox4x32(p.fast, static_cast<uint32_t>(block),
+                                     kDomNoise | (p.level << 8) | (static_cast<uint32_t>(block >> 32) << 16),
+                                     static_cast<uint32_t>(path), static_cast<uint32_t>(path >> 32));
+        u0 = fast_unit(w.a, w.b);
+        u1 = fast_unit(w.c, w.d);
+    }
+}
+
+template <int kRng>
 __global__ void __launch_bounds__(kTlBlock) tauleap_kernel(const __grid_constant__ TauParams p) {
+    using PA = typename std::conditional<kRng == VXB_RNG_REF, Exact, Fused>::type;
     __shared__ double s_inv[kMaxPoisson + 1];
     __shared__ long long s_sum[4];
     for (int k = threadIdx.x; k <= kMaxPoisson; k += kTlBlock)
@@ -87,18 +110,20 @@ __global__ void __launch_bounds__(kTlBlock) tauleap_kernel(const __grid_constant
     const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kTlBlock + threadIdx.x;
     long long sy = 0, sy2 = 0, sp = 0, it = 0;
     if (r < p.count) {
-        const uint64_t key = stream_key(p.seed_hash, p.first + r);
+        const uint64_t path = p.first + r;
+        const uint64_t key = stream_key(p.seed_hash, path);
         MM f{p.init[0], p.init[1], p.init[2], p.init[3]};
         MM c = f;
         double af[3], ac[3];
         if (p.level == 0) {
             for (uint64_t st = 0; st < p.n_fine; ++st) {
                 f.prop(p.rate, af);
-                const Words wa = philox2x64(key, 2 * st);      // positions 4s, 4s+1
-                const Words wb = philox2x64(key, 2 * st + 1);  // position 4s+2
-                const int k0 = poisson_inv(__dmul_rn(af[0], p.tau), to_unit(wa.w0), s_inv, it);
-                const int k1 = poisson_inv(__dmul_rn(af[1], p.tau), to_unit(wa.w1), s_inv, it);
-                const int k2 = poisson_inv(__dmul_rn(af[2], p.tau), to_unit(wb.w0), s_inv, it);
+                double ua, ub, uc, ud;
+                draw_pair<kRng>(p, key, path, 2 * st, ua, ub);      // positions 4s, 4s+1
+                draw_pair<kRng>(p, key, path, 2 * st + 1, uc, ud);  // position 4s+2
+                const int k0 = poisson_inv<PA>(__dmul_rn(af[0], p.tau), ua, s_inv, it);
+                const int k1 = poisson_inv<PA>(__dmul_rn(af[1], p.tau), ub, s_inv, it);
+                const int k2 = poisson_inv<PA>(__dmul_rn(af[2], p.tau), uc, s_inv, it);
                 f.fire(k0, k1, k2);
             }
         } else {
@@ -112,13 +137,14 @@ __global__ void __launch_bounds__(kTlBlock) tauleap_kernel(const __grid_constant
                 for (int q = 0; q < 3; ++q) {
                     // reaction q of fine step st owns Philox block 3 st + q: word 0 drives
                     // the common Poisson, word 1 the residual one
-                    const Words w = philox2x64(key, 3 * st + q);
+                    double u0, u1;
+                    draw_pair<kRng>(p, key, path, 3 * st + q, u0, u1);
                     const bool fine_larger = af[q] > ac[q];
                     const double mn = af[q] < ac[q] ? af[q] : ac[q];
                     const double mx = fine_larger ? af[q] : ac[q];
-                    const int p1 = poisson_inv(__dmul_rn(mn, p.tau), to_unit(w.w0), s_inv, it);
+                    const int p1 = poisson_inv<PA>(__dmul_rn(mn, p.tau), u0, s_inv, it);
                     // at most one of (af - m), (ac - m) is positive: one inversion serves both
-                    const int pr = poisson_inv(__dmul_rn(__dsub_rn(mx, mn), p.tau), to_unit(w.w1), s_inv, it);
+                    const int pr = poisson_inv<PA>(__dmul_rn(__dsub_rn(mx, mn), p.tau), u1, s_inv, it);
                     kf[q] = p1 + (fine_larger ? pr : 0);
                     kc[q] = p1 + (fine_larger ? 0 : pr);
                 }
@@ -168,6 +194,8 @@ void mlmc_level_device(vxb_ctx* ctx, const vxb_model& model, const vxb_mlmc_cfg&
     p.count = count;
     const uint64_t lv = level;
     p.seed_hash = splitmix64(vxb_derive_seed(cfg.seed, &lv, 1));
+    p.fast = make_fast_keys(splitmix64(cfg.seed));
+    require(model.rng == VXB_RNG_REF || model.rng == VXB_RNG_FAST, "invalid-argument", "bad rng mode");
     p.n_fine = level_steps(cfg, level);
     p.level = level;
     p.refine = cfg.refine;
@@ -180,7 +208,10 @@ void mlmc_level_device(vxb_ctx* ctx, const vxb_model& model, const vxb_mlmc_cfg&
     p.y_out = y_dev;
     if (count) {
         LaunchScope scope(ctx, VXB_K_TAULEAP);
-        tauleap_kernel<<<grid_for(count, kTlBlock), kTlBlock, 0, ctx->stream>>>(p);
+        if (model.rng == VXB_RNG_FAST)
+            tauleap_kernel<VXB_RNG_FAST><<<grid_for(count, kTlBlock), kTlBlock, 0, ctx->stream>>>(p);
+        else
+            tauleap_kernel<VXB_RNG_REF><<<grid_for(count, kTlBlock), kTlBlock, 0, ctx->stream>>>(p);
         check_launch("tauleap_kernel");
     }
     long long h[4];

@@ -183,6 +183,24 @@ def test_tauleap_full_level_properties(ctx):
     assert abs(mean) < 1.0 and 0.0 < var < 10.0
 
 
+def test_tauleap_fast_generator_statistics(ctx):
+    """The throughput generator (Philox4x32, FMA exp) agrees with the exact-RNG
+    run level by level within Monte-Carlo error, and is shard independent."""
+    cfg = mm_cfg(levels=5, paths=400000)
+    ref = ctx.mlmc_tauleap(M.mm_tauleap_model(), cfg)
+    fast_model = M.mm_tauleap_model(rng=A.VXB_RNG_FAST)
+    fast = ctx.mlmc_tauleap(fast_model, cfg)
+    n = cfg.paths
+    for l in range(5):
+        se = math.sqrt((ref["level_var"][l] + fast["level_var"][l]) / n)
+        assert abs(ref["level_mean"][l] - fast["level_mean"][l]) < 4.5 * se
+        assert abs(fast["level_var"][l] / ref["level_var"][l] - 1.0) < 0.05
+    a, _ = ctx.mlmc_level(fast_model, cfg, 3, 0, 1000)
+    b, _ = ctx.mlmc_level(fast_model, cfg, 3, 1000, 3000)
+    c, _ = ctx.mlmc_level(fast_model, cfg, 3, 0, 4000)
+    assert eq(a + b, c)
+
+
 # ------------------------------------------- toggle switch (SURVEY.md 8f-1)
 def test_toggle_switch_parity(ctx, oracle, golden):
     """The reference's own SDE, through the reference's own sampler keying:
