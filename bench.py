@@ -103,6 +103,19 @@ class ClockSampler:
                 "samples": len(self.sm)}
 
 
+def ncu_traffic(variant):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture
+    (profiles/r1_traffic.json); the capture was taken at 2e6 rows per launch."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json")))
+        k = t["kernels"][variant]
+        return {"traffic": k["dram_bytes"],
+                "traffic_note": f"ncu dram bytes per launch at {t['rows_per_profiled_launch']} rows "
+                                f"(algorithmic: {k['algorithmic_bytes']} B of rho, L2 resident)"}
+    except (OSError, KeyError, ValueError):
+        return {"traffic": None}
+
+
 def logistic_variant(name):
     from paper_1902_09046_b200 import _abi as A, models as M
     prec = A.VXB_F32 if name.startswith("f32") else A.VXB_F64
@@ -278,7 +291,7 @@ def main():
                      "peak_source": "measured FMA-chain probe (vxb_fma_peak) on this GPU; "
                                     "MEASURED_PEAKS.json has no fp64/fp32 entry",
                      "kernel": "logistic_abc_kernel", "kernel_ms": kernel_ms,
-                     "flops_per_sim": FLOPS_PER_SIM, "traffic": None},
+                     "flops_per_sim": FLOPS_PER_SIM, **ncu_traffic(args.variant)},
         "clocks": clocks.summary(),
         "device": info["name"],
     }
