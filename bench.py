@@ -139,7 +139,10 @@ def run_reference(args, rank, world):
     theta = [0.5, 100.0, 0.05]
     seed_obs = o.derive_seed(1, [90])
     obs = o.logistic_simulate(m, theta, seed_obs, 0, 0) if use_ref else o.simulate_at(m, theta, seed_obs, 0, 0)
-    eps = 5.0
+    # config 1 fixes epsilon at config 0's 0.1% quantile (seed 1337, reference-exact
+    # RNG, particle keying); its value is a pure function of the seeds, so the arm
+    # uses the constant the GPU arm recomputes every run (profiles/r1_bench_1gpu.json)
+    eps = 19.712058377057488
 
     def step(s):
         if use_ref:

@@ -47,6 +47,49 @@ def _worker(rank, world, port, n_total, eps, obs, out_dir):
     dist.destroy_process_group()
 
 
+def _counter_worker(rank, world, port, out_dir):
+    """Configs 2 and 4: ranks own disjoint dataset / path ranges; one
+    all-reduce(SUM) of integer counters gives the job's result."""
+    import math
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.pyoracle import Oracle
+    from paper_1902_09046_b200 import _abi as A
+    o = Oracle(threads=2)
+    n_data, m_total = 20, 1001
+    lam = np.array(M.lambda_grid(4))
+    ln = np.array([-0.5 * math.log(2.0 * math.pi * (l * l + 1.0 / n_data)) for l in lam])
+    b, e = D.shard_range(m_total, world, rank)
+    counts, _, _ = o.ppp_pvalues(M.normal_mean_model(n_data), lam, ln, m_total, b, e - b, 7, 0.4)
+    t = D.allreduce_sum(torch.from_numpy(counts.astype(np.int64)))
+    cfg = A.vxb_mlmc_cfg()
+    cfg.levels, cfg.refine, cfg.tau0, cfg.t_end, cfg.paths, cfg.seed = 3, 4, 1.0, 10.0, 501, 3
+    b, e = D.shard_range(cfg.paths, world, rank)
+    sums, _ = o.mlmc_level(M.mm_tauleap_model(), cfg, 2, b, e - b)
+    s = D.allreduce_sum(torch.from_numpy(sums.copy()))
+    np.savez(os.path.join(out_dir, f"c{rank}.npz"), counts=t.numpy(), sums=s.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_counter_allreduce(tmp_path, oracle):
+    import math
+    from paper_1902_09046_b200 import _abi as A
+    mp.spawn(_counter_worker, args=(2, free_port(), str(tmp_path)), nprocs=2, join=True)
+    n_data, m_total = 20, 1001
+    lam = np.array(M.lambda_grid(4))
+    ln = np.array([-0.5 * math.log(2.0 * math.pi * (l * l + 1.0 / n_data)) for l in lam])
+    counts, _, _ = oracle.ppp_pvalues(M.normal_mean_model(n_data), lam, ln, m_total, 0, m_total, 7, 0.4)
+    cfg = A.vxb_mlmc_cfg()
+    cfg.levels, cfg.refine, cfg.tau0, cfg.t_end, cfg.paths, cfg.seed = 3, 4, 1.0, 10.0, 501, 3
+    sums, _ = oracle.mlmc_level(M.mm_tauleap_model(), cfg, 2, 0, 501)
+    for r in range(2):
+        z = np.load(tmp_path / f"c{r}.npz")
+        assert np.array_equal(z["counts"], counts.astype(np.int64))
+        assert np.array_equal(z["sums"], sums)
+
+
 def test_shard_rule_is_the_reference_partition(oracle):
     for total, world in [(100_000_000, 8), (1_000_003, 4), (7, 8), (1, 2), (1000, 3)]:
         want = oracle.partition(total, world, 1)

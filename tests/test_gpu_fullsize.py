@@ -1,0 +1,80 @@
+"""GPU tests at BASELINE.json's full sizes, through size-independent properties
+(the oracle cannot run these sizes): ascending accepted indices, rho <= epsilon,
+binomial acceptance counts, shard concatenation == whole job, selection
+idempotence."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_1902_09046_b200 import _abi as A, dist as D, lib, models as M
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def config0(ctx, golden):
+    """Config 0: N = 1e6, exact RNG, epsilon = 0.1% quantile."""
+    import torch
+    m = M.logistic_model()
+    obs = golden["logistic_observed"]
+    n = 1_000_000
+    rho = torch.empty(n, dtype=torch.float64, device="cuda")
+    failed = torch.empty(n, dtype=torch.uint8, device="cuda")
+    ctx.abc_prior_predictive(m, M.keying(1337), n, 0, n, obs, rho=rho, failed=failed)
+    idx = torch.empty(n, dtype=torch.int64, device="cuda")
+    eps, _, nacc = ctx.select_epsilon(rho, failed, 1e-3, cap=n, precision=A.VXB_F64, n=n, idx=idx)
+    return dict(obs=obs, rho=rho, failed=failed, eps=eps, nacc=nacc, idx=idx[:nacc].cpu().numpy())
+
+
+def test_config0_full_size(ctx, config0):
+    c = config0
+    rho = c["rho"].cpu().numpy()
+    assert c["nacc"] >= 1000 and c["nacc"] == (rho <= c["eps"]).sum()      # >= ceil(q N)
+    assert (np.diff(c["idx"]) > 0).all()
+    assert np.array_equal(c["idx"], np.nonzero(rho <= c["eps"])[0])
+    s = np.sort(rho)                                                       # numeric.cpp:20-30 on the host
+    h = (len(s) - 1) * 1e-3
+    lo = int(h)
+    want = s[lo] + (h - lo) * (s[lo + 1] - s[lo])
+    want = max(want, s[math.ceil(1e-3 * len(s)) - 1])
+    assert c["eps"] == want
+    assert c["eps"] == 19.712058377057488                                   # the constant bench.py quotes
+    # idempotence: selecting among the accepted rows with q = 1 keeps them all
+    eps2, idx2, n2 = ctx.select_epsilon(rho[c["idx"]], None, 1.0)
+    assert n2 == c["nacc"] and eps2 == rho[c["idx"]].max()
+
+
+@pytest.mark.parametrize("variant", [(A.VXB_F64, A.VXB_RNG_FAST), (A.VXB_F64, A.VXB_RNG_REF),
+                                     (A.VXB_F32, A.VXB_RNG_FAST)])
+def test_config1_full_size_properties(ctx, config0, variant):
+    """N = 1e8 particles, fixed epsilon from config 0."""
+    precision, rng = variant
+    m = M.logistic_model(precision=precision, rng=rng)
+    n, eps, obs = 100_000_000, config0["eps"], config0["obs"]
+    idx, params, rho, n_dev = D.sharded_reject(ctx, m, M.keying(1337), n, obs, eps)
+    ctx.synchronize()
+    k = int(n_dev.item())
+    p_acc = config0["nacc"] / 1e6
+    # binomial count; p_acc itself is an in-sample estimate from 1000 of 1e6 rows (3.2% s.d.)
+    assert abs(k - n * p_acc) < 6 * math.sqrt(n * p_acc) + 0.16 * n * p_acc
+    i = idx[:k].cpu().numpy()
+    r = rho[:k].cpu().numpy().astype(np.float64)
+    th = params[:k].cpu().numpy().astype(np.float64)
+    assert (np.diff(i) > 0).all() and i.min() >= 0 and i.max() < n
+    assert (r <= eps).all() and (r >= 0).all()
+    lo, hi = np.array([0.0, 50.0, 0.0]), np.array([1.0, 150.0, 0.2])
+    assert ((th >= lo) & (th <= hi)).all()
+    assert abs(th[:, 1].mean() - 100.0) < 3.0              # posterior concentrates at K = 100
+    if rng == A.VXB_RNG_REF and precision == A.VXB_F64:
+        # the first 1e6 rows are config 0 itself: identical accepted prefix
+        pre = i[i < 1_000_000]
+        assert np.array_equal(pre, config0["idx"])
+    # two shards of the job concatenate to the whole (any GPU count gives one answer)
+    cut = 37_654_321
+    cap = 1_200_000
+    n1, i1, p1, r1 = ctx.abc_reject(m, M.keying(1337), n, 0, cut, obs, eps, cap)
+    n2, i2, p2, r2 = ctx.abc_reject(m, M.keying(1337), n, cut, n - cut, obs, eps, cap)
+    assert n1 + n2 == k
+    assert np.array_equal(np.concatenate([i1, i2]).astype(np.int64), i)
+    assert np.array_equal(np.concatenate([r1, r2]).astype(np.float64), r)
