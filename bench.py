@@ -254,7 +254,7 @@ def main():
     total_launches = sum(v["launches"] for v in prof.values())
     timed_fraction = args.steps / (args.warmup + args.steps)
     sims_per_s = args.steps * n_total / (ms * 1e-3)
-    n_acc = int(out[3].item()) if world == 1 else sum(out[3])  # device-resident count at N=1
+    n_acc = int(out[3].sum().item())  # device-resident count(s), read once after the timed region
     sim = prof["simulate"]
     kernel_ms = sim["total_ms"] / max(sim["launches"], 1)   # per launch, this rank's shard
     begin, end = D.shard_range(n_total, world, rank)

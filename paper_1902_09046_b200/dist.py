@@ -54,6 +54,35 @@ def gather_accepted(idx, params, rho, group=None):
     return outs[0], outs[1], outs[2], counts
 
 
+def gather_accepted_padded(idx, params, rho, n_dev, group=None):
+    """Asynchronous form: fixed-capacity buffers (rows [0, n_dev) valid) and the
+    device-resident count are all-gathered as they are -- no host round trip, so
+    steps queue back to back on every rank.  Returns tensors shaped
+    [world, cap, ...] plus the [world] count tensor; ``compact_gathered`` turns
+    them into the ascending concatenation once the host needs it."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    outs = []
+    for t in (idx, params, rho, n_dev):
+        buf = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        # per-rank views of one buffer: works on gloo (tests) and NCCL alike
+        dist.all_gather([buf[r] for r in range(world)], t.contiguous(), group=group)
+        outs.append(buf)
+    return outs[0], outs[1], outs[2], outs[3].reshape(world)
+
+
+def compact_gathered(idx, params, rho, counts):
+    """Concatenate the valid rows of a padded gather in rank order (synchronises)."""
+    import torch
+    c = [int(v) for v in counts.tolist()]
+    cap = idx.shape[1]
+    keep = [min(k, cap) for k in c]
+    return (torch.cat([idx[r, :k] for r, k in enumerate(keep)]),
+            torch.cat([params[r, :k] for r, k in enumerate(keep)]),
+            torch.cat([rho[r, :k] for r, k in enumerate(keep)]), c)
+
+
 def allreduce_sum(t, group=None):
     import torch.distributed as dist
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
@@ -82,13 +111,13 @@ def sharded_reject(ctx, model, key, n_total, observed, eps, cap_fraction=0.01, g
         params = torch.empty((cap, model.dim), dtype=real, device=dev)
         rho = torch.empty(cap, dtype=real, device=dev)
         n_dev = torch.empty(1, dtype=torch.int64, device=dev)
+    # fully asynchronous: the accepted count stays on the device, the host only
+    # enqueues (rows [0, count) of the buffers are valid once the stream drains)
+    ctx.abc_reject(model, key, n_total, begin, count, observed, eps, cap, idx=idx,
+                   params=params, rho=rho, n_accepted=n_dev)
     if world == 1:
-        # single GPU: fully asynchronous -- the accepted count stays on the device,
-        # the host only enqueues (rows [0, count) of the returned buffers are valid)
-        ctx.abc_reject(model, key, n_total, begin, count, observed, eps, cap, idx=idx,
-                       params=params, rho=rho, n_accepted=n_dev)
         return idx, params, rho, n_dev
-    nacc, _, _, _ = ctx.abc_reject(model, key, n_total, begin, count, observed, eps, cap,
-                                   idx=idx, params=params, rho=rho)
-    k = min(nacc, cap)
-    return gather_accepted(idx[:k], params[:k], rho[:k], group)
+    # the gather of accepted samples over NVLink, on the library's stream, padded to
+    # the fixed capacity so that no rank has to read a count back first
+    with torch.cuda.stream(torch.cuda.ExternalStream(ctx.stream(), device=dev)):
+        return gather_accepted_padded(idx, params, rho, n_dev, group)

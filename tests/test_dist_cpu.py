@@ -42,6 +42,15 @@ def _worker(rank, world, port, n_total, eps, obs, out_dir):
     g_idx, g_p, g_rho, counts = D.gather_accepted(idx, torch.from_numpy(p[keep]),
                                                   torch.from_numpy(rho[keep]))
     total = D.allreduce_sum(torch.tensor([int(keep.sum())], dtype=torch.int64))
+    # asynchronous form: fixed-capacity buffers + device-resident count
+    cap, k = 400, int(keep.sum())
+    b_idx = torch.full((cap,), -1, dtype=torch.int64)
+    b_p = torch.zeros((cap, 3), dtype=torch.float64)
+    b_rho = torch.zeros(cap, dtype=torch.float64)
+    b_idx[:k], b_p[:k], b_rho[:k] = idx, torch.from_numpy(p[keep]), torch.from_numpy(rho[keep])
+    pi, pp, pr, pc = D.gather_accepted_padded(b_idx, b_p, b_rho, torch.tensor([k], dtype=torch.int64))
+    ci, cp, cr, cc = D.compact_gathered(pi, pp, pr, pc)
+    assert torch.equal(ci, g_idx) and torch.equal(cp, g_p) and torch.equal(cr, g_rho) and cc == counts
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), idx=g_idx.numpy(), p=g_p.numpy(),
              rho=g_rho.numpy(), counts=np.array(counts), total=total.numpy())
     dist.destroy_process_group()
