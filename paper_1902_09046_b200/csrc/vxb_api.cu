@@ -41,6 +41,8 @@ void build_fast_log_table(double* table) {
         table[2 * (kLogTableSize + i)] = std::cos(a);
         table[2 * (kLogTableSize + i) + 1] = std::sin(a);
     }
+    for (uint32_t j = 0; j < kExpTableSize; ++j)  // 2^(j/64) for fast_exp2_neg
+        table[2 * (kLogTableSize + kTrigTableSize) + j] = std::exp2(static_cast<double>(j) / 64.0);
 }
 
 // ------------------------------------------------------------ fill kernels

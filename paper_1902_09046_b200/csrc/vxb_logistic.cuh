@@ -103,8 +103,9 @@ struct FastNoise64 {
     const FastKeys& fk;
     const double2* tbl;
     uint32_t row_lo, row_hi, block;
+    uint32_t domain = kDomNoise;
     __device__ __forceinline__ void next(double* z) {
-        fast_box_muller(philox4x32(fk, block++, kDomNoise, row_lo, row_hi), tbl, z[0], z[1]);
+        fast_box_muller(philox4x32(fk, block++, domain, row_lo, row_hi), tbl, z[0], z[1]);
     }
 };
 struct FastNoise32 {

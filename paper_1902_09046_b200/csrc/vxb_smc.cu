@@ -438,14 +438,133 @@ __global__ void gather_rows_kernel(const uint64_t* __restrict__ idx, uint64_t n_
     dst_rho[t] = src_rho[s];
 }
 
+// ------------------------------------------- throughput mode (VXB_RNG_FAST)
+// Same generation scheme with the throughput generator (Philox4x32, table-based
+// normals, FMA arithmetic).  Statistically validated against the exact mode.
+struct ProposeFastParams {
+    ProposeParams base;
+    FastKeys fast;
+    uint32_t gen;
+    const double2* fast_table;
+};
+
+__global__ void __launch_bounds__(256)
+abcsmc_propose_fast_kernel(const __grid_constant__ ProposeFastParams pp) {
+    __shared__ double2 s_tab[kFastTableSize];
+    for (int i = threadIdx.x; i < kFastTableSize; i += 256) s_tab[i] = pp.fast_table[i];
+    __syncthreads();
+    const ProposeParams& p = pp.base;
+    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * 256 + threadIdx.x;
+    if (r >= p.count) return;
+    const uint64_t row = p.first + r;
+    const uint32_t rl = static_cast<uint32_t>(row), rh = static_cast<uint32_t>(row >> 32);
+    const uint32_t dom = kDomProposal | (pp.gen << 8);
+    const Words32 w0 = philox4x32(pp.fast, 0u, dom, rl, rh);
+    const double target = fast_unit(w0.a, w0.b) * p.cum_prev[p.n_prev - 1];
+    const uint64_t a = upper_bound_dev(p.cum_prev, p.n_prev, target);
+    double z[4];
+    fast_box_muller(philox4x32(pp.fast, 1u, dom, rl, rh), s_tab, z[0], z[1]);
+    fast_box_muller(philox4x32(pp.fast, 2u, dom, rl, rh), s_tab, z[2], z[3]);
+    double th[3];
+    bool inside = true;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        double inc = 0.0;
+#pragma unroll
+        for (int q = 0; q <= k; ++q) inc = fma(p.chol[k * 3 + q], z[q], inc);
+        th[k] = p.theta_prev[a * 3 + k] + inc;
+        inside = inside && th[k] >= p.model.lo[k] && th[k] < p.model.hi[k];
+    }
+    double rho = __longlong_as_double(0x7FF8000000000000LL);
+    uint8_t flag = 2;
+    if (inside) {
+        FastNoise64 noise{pp.fast, s_tab, rl, rh, 0u};
+        // noise domain of this generation: block counter offset keeps it apart from
+        // the proposal draws (domain kDomProposal) of the same row
+        noise.domain = kDomNoise | (pp.gen << 8);
+        bool bad;
+        auto emit = [](uint32_t, double) {};
+        rho = logistic_path<double, Fused>(p.model, th, p.observed, noise, emit, bad);
+        if (bad) {
+            rho = __longlong_as_double(0x7FF8000000000000LL);
+            flag = 3;
+        } else {
+            flag = rho <= p.epsilon ? 1 : 0;
+        }
+    }
+    p.theta_out[r * 3 + 0] = th[0];
+    p.theta_out[r * 3 + 1] = th[1];
+    p.theta_out[r * 3 + 2] = th[2];
+    p.rho_out[r] = rho;
+    p.flag_out[r] = flag;
+}
+
+// Whitening pre-pass for the throughput weights kernel: y = s L^-1 theta with
+// s^2 = log2(e)/2, so that  w_j exp(-q_ij/2) = w_j 2^(2 y_i.y_j - |y_i|^2 - |y_j|^2).
+// mode 0 (previous population): out = (2 y, -|y|^2); mode 1 (new): out = (y, -|y|^2).
+template <int D>
+__global__ void whiten_kernel(int mode, uint64_t n, const double* __restrict__ theta,
+                              const double* __restrict__ chol, double* __restrict__ out) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double s = 0.84932180028801907;  // sqrt(log2(e) / 2)
+    double y[D], a = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        double v = theta[i * D + k];
+#pragma unroll
+        for (int c = 0; c < k; ++c) v = fma(-chol[k * D + c], y[c], v);
+        y[k] = v / chol[k * D + k];
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        y[k] *= s;
+        a = fma(y[k], y[k], a);
+        out[i * (D + 1) + k] = mode == 0 ? 2.0 * y[k] : y[k];
+    }
+    out[i * (D + 1) + D] = -a;
+}
+
+template <int D>
+__global__ void __launch_bounds__(128)
+abcsmc_weights_fast_kernel(uint64_t count, const double* __restrict__ y_new, uint64_t n_prev,
+                           const double* __restrict__ y_prev, const double* __restrict__ w_prev,
+                           const double2* __restrict__ fast_table, double* __restrict__ w_out) {
+    constexpr int kTile = 128;
+    __shared__ double s_y[kTile * (D + 1)];
+    __shared__ double s_w[kTile];
+    __shared__ double2 s_tab[kFastTableSize];
+    for (int i = threadIdx.x; i < kFastTableSize; i += 128) s_tab[i] = fast_table[i];
+    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * 128 + threadIdx.x;
+    double yi[D + 1];
+#pragma unroll
+    for (int k = 0; k <= D; ++k) yi[k] = r < count ? y_new[r * (D + 1) + k] : 0.0;
+    double sum = 0.0;
+    for (uint64_t j0 = 0; j0 < n_prev; j0 += kTile) {
+        const uint64_t len = min(static_cast<uint64_t>(kTile), n_prev - j0);
+        __syncthreads();
+        for (uint64_t t = threadIdx.x; t < len * (D + 1); t += 128) s_y[t] = y_prev[j0 * (D + 1) + t];
+        if (threadIdx.x < len) s_w[threadIdx.x] = w_prev[j0 + threadIdx.x];
+        __syncthreads();
+        for (uint64_t j = 0; j < len; ++j) {
+            double z = s_y[j * (D + 1) + D];
+#pragma unroll
+            for (int k = 0; k < D; ++k) z = fma(yi[k], s_y[j * (D + 1) + k], z);
+            z += yi[D];  // -|y_i - y_j|^2 (<= 0 up to rounding)
+            sum = fma(s_w[j], fast_exp2_neg(fmin(z, 0.0), s_tab), sum);
+        }
+    }
+    if (r < count) w_out[r] = 1.0 / sum;
+}
+
 void propose_device(vxb_ctx* ctx, const vxb_model& model, uint64_t seed, uint32_t gen,
                     uint64_t first, uint64_t count, uint64_t n_prev, const double* theta_prev,
                     const double* cum_prev, const double* chol_host, const double* observed_host,
                     double epsilon, double* theta_out, double* rho_out, uint8_t* flag_out) {
     require(gen >= 1, "invalid-argument", "generation 0 is the prior predictive set");
     require(n_prev >= 1, "insufficient-data", "empty previous population");
-    require(model.precision == VXB_F64 && model.rng == VXB_RNG_REF, "invalid-argument",
-            "ABC-SMC propagation runs in fp64 with the reference generator");
+    require(model.precision == VXB_F64 && (model.rng == VXB_RNG_REF || model.rng == VXB_RNG_FAST),
+            "invalid-argument", "ABC-SMC propagation runs in fp64 (reference or throughput generator)");
     ProposeParams p{};
     p.model = make_logistic(model);
     p.first = first;
@@ -463,8 +582,35 @@ void propose_device(vxb_ctx* ctx, const vxb_model& model, uint64_t seed, uint32_
     p.flag_out = flag_out;
     if (count == 0) return;
     LaunchScope scope(ctx, VXB_K_PROPOSE);
-    abcsmc_propose_kernel<<<grid_for(count, 256), 256, 0, ctx->stream>>>(p);
+    if (model.rng == VXB_RNG_FAST) {
+        ProposeFastParams pf{};
+        pf.base = p;
+        pf.fast = make_fast_keys(splitmix64(seed));
+        pf.gen = gen;
+        pf.fast_table = ctx->log_table;
+        abcsmc_propose_fast_kernel<<<grid_for(count, 256), 256, 0, ctx->stream>>>(pf);
+    } else {
+        abcsmc_propose_kernel<<<grid_for(count, 256), 256, 0, ctx->stream>>>(p);
+    }
     check_launch("abcsmc_propose_kernel");
+}
+
+// Throughput form of the importance weights: whiten both populations once, then
+// one fused multiply-add per coordinate and a table-based exp2 per pair.
+void weights_fast_device(vxb_ctx* ctx, uint32_t dim, uint64_t count, const double* theta_new,
+                         uint64_t n_prev, const double* theta_prev, const double* w_prev,
+                         const double* chol_dev, double* w_out) {
+    require(dim == 3, "invalid-shape", "the throughput weights kernel is built for dim = 3");
+    if (count == 0) return;
+    Scratch y_prev(ctx, n_prev * 4 * sizeof(double)), y_new(ctx, count * 4 * sizeof(double));
+    LaunchScope scope(ctx, VXB_K_WEIGHTS);
+    whiten_kernel<3><<<grid_for(n_prev, 256), 256, 0, ctx->stream>>>(0, n_prev, theta_prev, chol_dev,
+                                                                    y_prev.as<double>());
+    whiten_kernel<3><<<grid_for(count, 256), 256, 0, ctx->stream>>>(1, count, theta_new, chol_dev,
+                                                                   y_new.as<double>());
+    abcsmc_weights_fast_kernel<3><<<grid_for(count, 128), 128, 0, ctx->stream>>>(
+        count, y_new.as<double>(), n_prev, y_prev.as<double>(), w_prev, ctx->log_table, w_out);
+    check_launch("abcsmc_weights_fast_kernel");
 }
 
 void weights_device(vxb_ctx* ctx, uint32_t dim, uint64_t count, const double* theta_new,
@@ -605,8 +751,10 @@ extern "C" int vxb_abcsmc_run(vxb_ctx* ctx, const vxb_model* model, const vxb_ab
         require(model && cfg && observed && out, "invalid-argument", "null argument");
         const LogisticModel lm = make_logistic(*model);
         (void)lm;
-        require(model->precision == VXB_F64 && model->rng == VXB_RNG_REF, "invalid-argument",
-                "ABC-SMC runs in fp64 with the reference generator");
+        require(model->precision == VXB_F64 &&
+                    (model->rng == VXB_RNG_REF || model->rng == VXB_RNG_FAST),
+                "invalid-argument", "ABC-SMC runs in fp64 (reference or throughput generator)");
+        const bool fast = model->rng == VXB_RNG_FAST;
         const uint64_t n = cfg->particles;
         const uint32_t d = 3;
         require(n >= 2, "insufficient-data", "need at least two particles");
@@ -678,7 +826,10 @@ extern "C" int vxb_abcsmc_run(vxb_ctx* ctx, const vxb_model* model, const vxb_ab
                 fill_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(nxt_w, n, 1.0 / static_cast<double>(n));
                 check_launch("fill_kernel");
             } else {
-                weights_device(ctx, d, n, nxt_theta, n, cur_theta, cur_w, d_chol.as<double>(), nxt_w);
+                if (fast)
+                    weights_fast_device(ctx, d, n, nxt_theta, n, cur_theta, cur_w, d_chol.as<double>(), nxt_w);
+                else
+                    weights_device(ctx, d, n, nxt_theta, n, cur_theta, cur_w, d_chol.as<double>(), nxt_w);
                 canon_reduce(ctx, 2, nullptr, nxt_w, nullptr, n, d, 1, d_total.as<double>());
                 double total = 0.0;
                 VXB_CUDA(cudaMemcpyAsync(&total, d_total.as<void>(), 8, cudaMemcpyDeviceToHost, ctx->stream));

@@ -84,6 +84,14 @@ def main():
                       "proposals": out["proposals"].tolist(),
                       "posterior_mean": out["mean"][-1].tolist(), "kernels": prof}
 
+    mfast = M.logistic_model(rng=A.VXB_RNG_FAST)
+    outf, wall, prof = timed(ctx, lambda: ctx.abcsmc_run(mfast, cfg, obs))
+    res["config3_fast"] = {"particles": cfg.particles, "generations": 10, "wall_ms": wall * 1e3,
+                           "epsilon": outf["epsilon"].tolist(), "ess": outf["ess"].tolist(),
+                           "accept_rate": outf["accept_rate"].tolist(),
+                           "proposals": outf["proposals"].tolist(),
+                           "posterior_mean": outf["mean"][-1].tolist(), "kernels": prof}
+
     # ---- config 4: MLMC tau-leap, 6 levels x 1e6 paths
     mm = M.mm_tauleap_model()
     mc = A.vxb_mlmc_cfg()
