@@ -118,105 +118,94 @@ Block philox_block(std::uint64_t key, std::uint64_t idx_lo, std::uint64_t idx_hi
 double to_unit(std::uint64_t x) { return static_cast<double>(x >> 11) * 0x1.0p-53; }
 
 // ================================================================ fastmath
-// log2_pos: fastmath.hpp:23-51
-double log2_pos(double x) {
-    std::uint64_t bits = bit_cast<std::uint64_t>(x);
-    std::int64_t e = static_cast<std::int64_t>((bits >> 52) & 0x7FF);
-    if (e == 0) {
-        bits = bit_cast<std::uint64_t>(x * 0x1p64);
-        e = static_cast<std::int64_t>((bits >> 52) & 0x7FF) - 64;
-    }
-    e -= 1023;
-    double m = bit_cast<double>((bits & 0xFFFFFFFFFFFFFULL) | 0x3FF0000000000000ULL);
-    const bool upper = m > 1.4142135623730951;
-    m = upper ? 0.5 * m : m;
-    const double ed = static_cast<double>(e + (upper ? 1 : 0));
-    const double t = (m - 1.0) / (m + 1.0);
-    const double s = t * t;
-    double p = 1.0 / 21.0;
-    p = p * s + 1.0 / 19.0;
-    p = p * s + 1.0 / 17.0;
-    p = p * s + 1.0 / 15.0;
-    p = p * s + 1.0 / 13.0;
-    p = p * s + 1.0 / 11.0;
-    p = p * s + 1.0 / 9.0;
-    p = p * s + 1.0 / 7.0;
-    p = p * s + 1.0 / 5.0;
-    p = p * s + 1.0 / 3.0;
-    p = p * s + 1.0;
-    return ed + (2.0 * 0x1.71547652b82fep+0) * t * p;
-}
+// The reference's libm-free elementary functions (fastmath.hpp:23-128) restated
+// as coefficient tables + one Horner routine.  Every step is a separately
+// rounded multiply followed by a separately rounded add (this file is compiled
+// with -ffp-contract=off), in the reference's order, so results are identical
+// bit for bit (pinned in tests/test_oracle_pins.py).
 constexpr double kLn2 = 0x1.62e42fefa39efp-1;     // fastmath.hpp:19
 constexpr double kInvLn2 = 0x1.71547652b82fep+0;  // fastmath.hpp:20
-// ln_pos: fastmath.hpp:54
-double ln_pos(double x) { return log2_pos(x) * kLn2; }
-// exp2_clamped: fastmath.hpp:57-79
+constexpr double kRoundMagic = 0x1.8p52;          // (x + M) - M rounds x to an integer
+
+template <std::size_t N>
+double horner(const double (&coef)[N], double x) {
+    double acc = coef[0];
+    for (std::size_t i = 1; i < N; ++i) acc = acc * x + coef[i];
+    return acc;
+}
+// 2 atanh(t) / (2 t) series in s = t^2: sum_{k} s^k / (2k+1), highest power first (:40-50)
+constexpr double kAtanhSeries[11] = {1.0 / 21.0, 1.0 / 19.0, 1.0 / 17.0, 1.0 / 15.0, 1.0 / 13.0, 1.0 / 11.0,
+                                     1.0 / 9.0,  1.0 / 7.0,  1.0 / 5.0,  1.0 / 3.0,  1.0};
+// exp(w) Taylor coefficients 1/13! ... 1/0! (:63-76)
+constexpr double kExpSeries[14] = {1.0 / 6227020800.0, 1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0,
+                                   1.0 / 362880.0,     1.0 / 40320.0,     1.0 / 5040.0,     1.0 / 720.0,
+                                   1.0 / 120.0,        1.0 / 24.0,        1.0 / 6.0,        0.5,
+                                   1.0,                1.0};
+// sin(s)/s in s^2: 1/21! ... alternating (:90-100); cos(s) in s^2: -1/22! ... (:113-124)
+constexpr double kSinSeries[11] = {1.0 / 51090942171709440000.0, -1.0 / 121645100408832000.0,
+                                   1.0 / 355687428096000.0,      -1.0 / 1307674368000.0,
+                                   1.0 / 6227020800.0,           -1.0 / 39916800.0,
+                                   1.0 / 362880.0,               -1.0 / 5040.0,
+                                   1.0 / 120.0,                  -1.0 / 6.0,
+                                   1.0};
+constexpr double kCosSeries[12] = {-1.0 / 1124000727777607680000.0, 1.0 / 2432902008176640000.0,
+                                   -1.0 / 6402373705728000.0,       1.0 / 20922789888000.0,
+                                   -1.0 / 87178291200.0,            1.0 / 479001600.0,
+                                   -1.0 / 3628800.0,                1.0 / 40320.0,
+                                   -1.0 / 720.0,                    1.0 / 24.0,
+                                   -1.0 / 2.0,                      1.0};
+
+// log2 of a finite positive double (fastmath.hpp:23-51): split into exponent and
+// mantissa, fold the mantissa into [sqrt(1/2), sqrt 2), then the atanh series of
+// t = (m-1)/(m+1).
+double log2_pos(double x) {
+    std::uint64_t raw = bit_cast<std::uint64_t>(x);
+    std::int64_t expo = static_cast<std::int64_t>((raw >> 52) & 0x7FF);
+    if (expo == 0) {  // subnormal: scale into the normal range first
+        raw = bit_cast<std::uint64_t>(x * 0x1p64);
+        expo = static_cast<std::int64_t>((raw >> 52) & 0x7FF) - 64;
+    }
+    double mant = bit_cast<double>((raw & 0xFFFFFFFFFFFFFULL) | 0x3FF0000000000000ULL);
+    const bool fold = mant > 1.4142135623730951;
+    if (fold) mant = 0.5 * mant;
+    const double expo_d = static_cast<double>(expo - 1023 + (fold ? 1 : 0));
+    const double t = (mant - 1.0) / (mant + 1.0);
+    const double series = horner(kAtanhSeries, t * t);
+    return expo_d + (2.0 * kInvLn2) * t * series;
+}
+double ln_pos(double x) { return log2_pos(x) * kLn2; }  // fastmath.hpp:54
+
+// 2^z with z clamped to the normal exponent range (fastmath.hpp:57-79)
 double exp2_clamped(double z) {
-    z = z < -1022.0 ? -1022.0 : z;
-    z = z > 1023.0 ? 1023.0 : z;
-    const double rn = (z + 0x1.8p52) - 0x1.8p52;
-    const double w = (z - rn) * kLn2;
-    double p = 1.0 / 6227020800.0;
-    p = p * w + 1.0 / 479001600.0;
-    p = p * w + 1.0 / 39916800.0;
-    p = p * w + 1.0 / 3628800.0;
-    p = p * w + 1.0 / 362880.0;
-    p = p * w + 1.0 / 40320.0;
-    p = p * w + 1.0 / 5040.0;
-    p = p * w + 1.0 / 720.0;
-    p = p * w + 1.0 / 120.0;
-    p = p * w + 1.0 / 24.0;
-    p = p * w + 1.0 / 6.0;
-    p = p * w + 0.5;
-    p = p * w + 1.0;
-    p = p * w + 1.0;
-    const std::int64_t n = static_cast<std::int64_t>(rn);
-    const double scale = bit_cast<double>(static_cast<std::uint64_t>(n + 1023) << 52);
-    return p * scale;
+    if (z < -1022.0) z = -1022.0;
+    if (z > 1023.0) z = 1023.0;
+    const double whole = (z + kRoundMagic) - kRoundMagic;
+    const double frac = (z - whole) * kLn2;  // |frac| <= ln2/2
+    const double series = horner(kExpSeries, frac);
+    const std::uint64_t biased = static_cast<std::uint64_t>(static_cast<std::int64_t>(whole) + 1023);
+    return series * bit_cast<double>(biased << 52);
 }
-// pow_pos: fastmath.hpp:82
-double pow_pos(double x, double y) { return exp2_clamped(y * log2_pos(x)); }
-// sinpi: fastmath.hpp:85-105
+double pow_pos(double x, double y) { return exp2_clamped(y * log2_pos(x)); }  // fastmath.hpp:82
+
+// sin(pi a) and cos(pi a) (fastmath.hpp:85-128): reduce a to r in [-1/2, 1/2] around
+// the nearest integer n, evaluate at s = pi r, flip the sign for odd n.
+struct PiReduced {
+    double s, s2, sign;
+};
+PiReduced reduce_pi(double a) {
+    const double whole = (a + kRoundMagic) - kRoundMagic;
+    const double s = (a - whole) * 3.141592653589793238462643383279502884;
+    const bool odd = (static_cast<std::int64_t>(whole) & 1) != 0;
+    return {s, s * s, odd ? -1.0 : 1.0};
+}
 double sinpi(double a) {
-    const double rn = (a + 0x1.8p52) - 0x1.8p52;
-    const double r = a - rn;
-    const double s = r * 3.141592653589793238462643383279502884;
-    const double s2 = s * s;
-    double p = 1.0 / 51090942171709440000.0;
-    p = p * s2 - 1.0 / 121645100408832000.0;
-    p = p * s2 + 1.0 / 355687428096000.0;
-    p = p * s2 - 1.0 / 1307674368000.0;
-    p = p * s2 + 1.0 / 6227020800.0;
-    p = p * s2 - 1.0 / 39916800.0;
-    p = p * s2 + 1.0 / 362880.0;
-    p = p * s2 - 1.0 / 5040.0;
-    p = p * s2 + 1.0 / 120.0;
-    p = p * s2 - 1.0 / 6.0;
-    p = p * s2 + 1.0;
-    const double base = s * p;
-    const std::int64_t n = static_cast<std::int64_t>(rn);
-    return ((n & 1) ? -1.0 : 1.0) * base;
+    const PiReduced r = reduce_pi(a);
+    const double base = r.s * horner(kSinSeries, r.s2);
+    return r.sign * base;
 }
-// cospi: fastmath.hpp:108-128
 double cospi(double a) {
-    const double rn = (a + 0x1.8p52) - 0x1.8p52;
-    const double r = a - rn;
-    const double s = r * 3.141592653589793238462643383279502884;
-    const double s2 = s * s;
-    double p = -1.0 / 1124000727777607680000.0;
-    p = p * s2 + 1.0 / 2432902008176640000.0;
-    p = p * s2 - 1.0 / 6402373705728000.0;
-    p = p * s2 + 1.0 / 20922789888000.0;
-    p = p * s2 - 1.0 / 87178291200.0;
-    p = p * s2 + 1.0 / 479001600.0;
-    p = p * s2 - 1.0 / 3628800.0;
-    p = p * s2 + 1.0 / 40320.0;
-    p = p * s2 - 1.0 / 720.0;
-    p = p * s2 + 1.0 / 24.0;
-    p = p * s2 - 1.0 / 2.0;
-    p = p * s2 + 1.0;
-    const std::int64_t n = static_cast<std::int64_t>(rn);
-    return ((n & 1) ? -1.0 : 1.0) * p;
+    const PiReduced r = reduce_pi(a);
+    return r.sign * horner(kCosSeries, r.s2);
 }
 
 // Random-access view of RngStream(seed, stream_id): every output is a pure
