@@ -297,6 +297,29 @@ int vxb_abcsmc_weights(vxb_ctx* ctx, uint32_t dim, uint64_t count, const double*
                        uint64_t n_prev, const double* theta_prev,
                        const double* w_prev, const double* chol, double* w_out);
 
+/* Population statistics of a generation in the canonical two-level summation
+ * order (chunks of 256 rows left to right, then chunk totals left to right) --
+ * the order that makes single- and multi-GPU runs bit-identical.  Exposed for
+ * the multi-GPU host (every rank holds the replicated previous population).
+ * weighted_moments: mean[dim], cov[dim x dim] = sum w d d^T / (1 - sum w^2)
+ *   (sample_covariance's n-1 divisor for equal weights, numeric.cpp:55-79);
+ *   *sum_w2 = sum w^2 (ESS = 1/sum_w2, smc.cpp:208-219).  Host outputs.
+ * canon_cumsum: inclusive cumulative weights (resample_multinomial's `cum`,
+ *   smc.cpp:276-283).  canon_chunk_sums: the ceil(n/256) chunk totals of v, so
+ *   that ranks owning chunk-aligned shards can all-reduce them exactly.
+ * divide: in-place normalisation of the weights by their canonical sum.
+ * quantile: numeric.cpp:20-36 (type 7) of n device- or host-resident values.
+ * make_kernel (host only): chol(scale * cov) with the jitter rule of
+ *   smc.cpp:311-325. */
+int vxb_weighted_moments(vxb_ctx* ctx, const double* theta, const double* w, uint64_t n,
+                         uint32_t dim, double* mean, double* cov, double* sum_w2);
+int vxb_canon_cumsum(vxb_ctx* ctx, const double* w, uint64_t n, double* cum);
+int vxb_canon_chunk_sums(vxb_ctx* ctx, const double* v, uint64_t n, double* chunk_sums);
+int vxb_quantile(vxb_ctx* ctx, const double* values, uint64_t n, double level, double* out);
+/* v[i] <- v[i] / divisor with IEEE division (the weight normalisation). */
+int vxb_divide(vxb_ctx* ctx, double* v, uint64_t n, double divisor);
+int vxb_make_kernel(const double* cov, uint32_t dim, double scale, double jitter, double* chol);
+
 /* ------------------------------------------------ tau-leap MLMC (C4) */
 typedef struct vxb_mlmc_cfg {
     uint32_t levels;       /* L+1 levels, l = 0..L              */

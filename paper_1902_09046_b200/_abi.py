@@ -76,5 +76,6 @@ EXPORTED_SYMBOLS = (
     "vxb_abc_prior_predictive", "vxb_select_epsilon", "vxb_order_statistics",
     "vxb_compact_accepted", "vxb_abc_reject", "vxb_simulate_at", "vxb_ppp_pvalues",
     "vxb_ess", "vxb_logsumexp", "vxb_resample_multinomial", "vxb_abcsmc_run",
-    "vxb_abcsmc_propose", "vxb_abcsmc_weights", "vxb_mlmc_level", "vxb_mlmc_tauleap",
+    "vxb_abcsmc_propose", "vxb_abcsmc_weights", "vxb_weighted_moments", "vxb_canon_cumsum",
+    "vxb_canon_chunk_sums", "vxb_quantile", "vxb_divide", "vxb_make_kernel", "vxb_mlmc_level", "vxb_mlmc_tauleap",
 )

@@ -743,6 +743,92 @@ extern "C" int vxb_abcsmc_weights(vxb_ctx* ctx, uint32_t dim, uint64_t count,
     });
 }
 
+// ---- population statistics in the canonical order, for the multi-GPU host
+extern "C" int vxb_weighted_moments(vxb_ctx* ctx, const double* theta, const double* w, uint64_t n,
+                                    uint32_t dim, double* mean, double* cov, double* sum_w2) {
+    return guarded([&] {
+        use(ctx);
+        require(theta && w && mean && cov, "invalid-argument", "null argument");
+        require(n >= 2, "insufficient-data", "covariance needs at least two rows");
+        require(!is_device_pointer(mean) && !is_device_pointer(cov), "invalid-argument",
+                "mean and cov are host arrays");
+        Staged d_th(ctx, theta, n * dim * 8, true, false);
+        Staged d_w(ctx, w, n * 8, true, false);
+        const double s2 = weighted_moments_device(ctx, d_th.as<double>(), d_w.as<double>(), n, dim,
+                                                  mean, cov);
+        if (sum_w2) *sum_w2 = s2;
+    });
+}
+
+extern "C" int vxb_canon_cumsum(vxb_ctx* ctx, const double* w, uint64_t n, double* cum) {
+    return guarded([&] {
+        use(ctx);
+        require(w && cum && n >= 1, "invalid-argument", "null argument");
+        Staged d_w(ctx, w, n * 8, true, false);
+        Staged d_c(ctx, cum, n * 8, false, true);
+        canon_cumsum_device(ctx, d_w.as<double>(), n, d_c.as<double>());
+        d_c.finish();
+        if (d_c.staged()) VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+extern "C" int vxb_canon_chunk_sums(vxb_ctx* ctx, const double* v, uint64_t n, double* chunk_sums) {
+    return guarded([&] {
+        use(ctx);
+        require(v && chunk_sums && n >= 1, "invalid-argument", "null argument");
+        const uint64_t nc = n_chunks(n);
+        Staged d_v(ctx, v, n * 8, true, false);
+        Staged d_s(ctx, chunk_sums, nc * 8, false, true);
+        {
+            LaunchScope scope(ctx, VXB_K_RESAMPLE);
+            canon_partial_kernel<<<grid_for(nc, 128), 128, 0, ctx->stream>>>(
+                2, nullptr, d_v.as<double>(), nullptr, n, 1, 1, d_s.as<double>());
+            check_launch("canon_partial_kernel");
+        }
+        d_s.finish();
+        if (d_s.staged()) VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+extern "C" int vxb_quantile(vxb_ctx* ctx, const double* values, uint64_t n, double level,
+                            double* out) {
+    return guarded([&] {
+        use(ctx);
+        require(values && out, "invalid-argument", "null argument");
+        require(n >= 1, "insufficient-data", "quantile of an empty sample");
+        Staged d_v(ctx, values, n * 8, true, false);
+        *out = quantile_device(ctx, d_v.as<double>(), n, level);
+    });
+}
+
+extern "C" int vxb_divide(vxb_ctx* ctx, double* v, uint64_t n, double divisor) {
+    return guarded([&] {
+        use(ctx);
+        require(v && n >= 1, "invalid-argument", "null argument");
+        Staged d_v(ctx, v, n * 8, true, true);
+        Scratch d_div(ctx, 8);
+        VXB_CUDA(cudaMemcpyAsync(d_div.as<void>(), &divisor, 8, cudaMemcpyHostToDevice, ctx->stream));
+        {
+            LaunchScope scope(ctx, VXB_K_MISC);
+            scale_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(d_v.as<double>(), n,
+                                                                  d_div.as<double>());
+            check_launch("scale_kernel");
+        }
+        d_v.finish();
+        // `divisor` is a stack variable of the caller: the copy must have left it
+        VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+extern "C" int vxb_make_kernel(const double* cov, uint32_t dim, double scale, double jitter,
+                               double* chol) {
+    return guarded([&] {
+        require(cov && chol, "invalid-argument", "null argument");
+        require(dim >= 1 && dim <= 8, "invalid-shape", "dimension out of range");
+        make_kernel_host(cov, dim, scale, jitter, chol);
+    });
+}
+
 // Full run, device resident; follows vxo_abcsmc_run step for step.
 extern "C" int vxb_abcsmc_run(vxb_ctx* ctx, const vxb_model* model, const vxb_abcsmc_cfg* cfg,
                               const double* observed, vxb_abcsmc_out* out) {

@@ -121,3 +121,277 @@ def sharded_reject(ctx, model, key, n_total, observed, eps, cap_fraction=0.01, g
     # the fixed capacity so that no rank has to read a count back first
     with torch.cuda.stream(torch.cuda.ExternalStream(ctx.stream(), device=dev)):
         return gather_accepted_padded(idx, params, rho, n_dev, group)
+
+
+# --------------------------------------------------------------------------
+# ABC-SMC (config 3) over several GPUs
+# --------------------------------------------------------------------------
+CHUNK = 256  # the canonical reduction chunk (csrc/vxb_smc.cu: kChunk)
+
+
+def _world(group):
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(group), dist.get_world_size(group)
+    return 0, 1
+
+
+def allgather_rows(tensors, group=None):
+    """All-gather row blocks of different length: one all_gather of the counts,
+    then one padded all_gather per tensor; returns the rank-order concatenations
+    and the per-rank counts.  With one rank it is the identity."""
+    import torch
+    import torch.distributed as dist
+    rank, world = _world(group)
+    k = int(tensors[0].shape[0])
+    if world == 1:
+        return list(tensors), [k]
+    n_local = torch.tensor([k], dtype=torch.int64, device=tensors[0].device)
+    counts = torch.empty(world, dtype=torch.int64, device=n_local.device)
+    dist.all_gather([counts[r:r + 1] for r in range(world)], n_local, group=group)
+    counts = [int(c) for c in counts.tolist()]
+    cap = max(max(counts), 1)
+    outs = []
+    for t in tensors:
+        pad = torch.zeros((cap,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        pad[:k] = t
+        buf = torch.empty((world,) + tuple(pad.shape), dtype=t.dtype, device=t.device)
+        dist.all_gather([buf[r] for r in range(world)], pad, group=group)
+        outs.append(torch.cat([buf[r, :c] for r, c in enumerate(counts)], dim=0))
+    return outs, counts
+
+
+class DeviceStages:
+    """The per-rank stage operations of an ABC-SMC generation on this rank's GPU,
+    each one call into the C ABI (include/vexbayes_cuda.h).  Tensors are torch
+    CUDA tensors that live on the library's stream; torch only allocates, slices
+    and carries them into the collectives."""
+
+    def __init__(self, ctx):
+        import torch
+        self.ctx = ctx
+        self.device = torch.device("cuda", ctx.device_info()["device"])
+        self._stream = torch.cuda.ExternalStream(ctx.stream(), device=self.device)
+
+    def scope(self):
+        import torch
+        return torch.cuda.stream(self._stream)
+
+    def _rows(self, count, dim):
+        import torch
+        return (torch.empty((count, dim), dtype=torch.float64, device=self.device),
+                torch.empty(count, dtype=torch.float64, device=self.device))
+
+    def _compacted(self, theta, rho, failed, eps):
+        """Ascending rows with !failed and rho <= eps (ballot/scan compaction kernel)."""
+        import torch
+        from . import _abi as A
+        count = int(rho.shape[0])
+        idx = torch.empty(max(count, 1), dtype=torch.int64, device=self.device)
+        _, k = self.ctx.compact_accepted(rho, failed, eps, 0, count, A.VXB_F64, count, idx)
+        keep = idx[:k]
+        return theta.index_select(0, keep), rho.index_select(0, keep)
+
+    def prior_rows(self, model, seed0, n_total, first, count, observed):
+        import torch
+        from . import models as M
+        theta, rho = self._rows(count, model.dim)
+        failed = torch.empty(count, dtype=torch.uint8, device=self.device)
+        self.ctx.abc_prior_predictive(model, M.keying(seed0), n_total, first, count, observed,
+                                      params=theta, rho=rho, failed=failed)
+        return self._compacted(theta, rho, failed, float("inf"))
+
+    def propose(self, model, seed, gen, first, count, theta_prev, cum_prev, chol, observed, eps):
+        import ctypes as C
+        import torch
+        from .lib import _ptr, u32, u64, f64
+        theta, rho = self._rows(count, model.dim)
+        flag = torch.empty(count, dtype=torch.uint8, device=self.device)
+        ch = np.ascontiguousarray(chol, dtype=np.float64)
+        obs = np.ascontiguousarray(observed, dtype=np.float64)
+        c = self.ctx
+        c._check(c.lib.vxb_abcsmc_propose(c.handle, C.byref(model), u64(seed), u32(gen), u64(first),
+                                          u64(count), u64(int(theta_prev.shape[0])),
+                                          _ptr(theta_prev), _ptr(cum_prev), _ptr(ch), _ptr(obs),
+                                          f64(eps), _ptr(theta), _ptr(rho), _ptr(flag)))
+        return self._compacted(theta, rho, None, eps)
+
+    def weights(self, theta_new, theta_prev, w_prev, chol):
+        import torch
+        from .lib import _ptr, u32, u64
+        out = torch.empty(int(theta_new.shape[0]), dtype=torch.float64, device=self.device)
+        ch = np.ascontiguousarray(chol, dtype=np.float64)
+        c = self.ctx
+        c._check(c.lib.vxb_abcsmc_weights(c.handle, u32(int(theta_new.shape[1])),
+                                          u64(int(theta_new.shape[0])), _ptr(theta_new),
+                                          u64(int(theta_prev.shape[0])), _ptr(theta_prev),
+                                          _ptr(w_prev), _ptr(ch), _ptr(out)))
+        return out
+
+    def quantile(self, values, level):
+        return self.ctx.quantile(values, level)
+
+    def moments(self, theta, w):
+        return self.ctx.weighted_moments(theta, w)
+
+    def cumsum(self, w):
+        import torch
+        return self.ctx.canon_cumsum(w, torch.empty_like(w))
+
+    def chunk_sums(self, v):
+        import torch
+        n = int(v.shape[0])
+        return self.ctx.canon_chunk_sums(
+            v, torch.empty((n + CHUNK - 1) // CHUNK, dtype=torch.float64, device=self.device))
+
+    def normalise(self, w_raw, total):
+        # not `w_raw / total`: torch multiplies by the reciprocal of a host scalar
+        return self.ctx.divide(w_raw.contiguous(), total)
+
+    def make_kernel(self, cov, scale, jitter):
+        from . import lib
+        return lib.make_kernel(cov, scale, jitter)
+
+
+def sharded_abcsmc(stages, model, cfg, observed, group=None):
+    """ABC-SMC (BASELINE config 3; scheme of DESIGN.md section 3.3) with the
+    proposals of every round and the new particles of every generation sharded
+    over the ranks by global index.  Exchanges per generation:
+
+    * all-gather of each round's accepted proposals (theta*, rho), rank order =
+      ascending proposal index, so "the first N accepted by proposal index" is
+      the same set on every rank and for every world size;
+    * all-gather of the unnormalised importance weights (shards are aligned to
+      the 256-row canonical chunks);
+    * all-reduce(SUM) of the vector of chunk totals -- every entry has exactly
+      one non-zero contributor, so the reduction is exact and the weight sum
+      (chunk totals added left to right) is bit-identical to the one-GPU run.
+
+    The previous population (theta, w, rho) is replicated; its statistics
+    (epsilon, weighted covariance, cumulative weights) are recomputed on every
+    rank.  `stages` supplies the per-rank compute (DeviceStages on a GPU).
+    Returns the dictionary of Context.abcsmc_run."""
+    import torch
+    from .lib import derive_seed
+    rank, world = _world(group)
+    n, gens, d = int(cfg.particles), int(cfg.generations), int(model.dim)
+    round_size = int(cfg.round_size) or n
+    max_rounds = int(cfg.max_rounds) or 1000
+    if n < 2:
+        raise ValueError("insufficient-data: need at least two particles")
+    res = dict(epsilon=np.zeros(gens), ess=np.zeros(gens), accept_rate=np.zeros(gens),
+               proposals=np.zeros(gens, dtype=np.uint64), mean=np.zeros((gens, d)),
+               cov=np.zeros((gens, d, d)))
+    n_chunks = (n + CHUNK - 1) // CHUNK
+    c_begin, c_end = shard_range(n_chunks, world, rank)
+    w_begin, w_end = min(n, c_begin * CHUNK), min(n, c_end * CHUNK)
+    seed0 = derive_seed(cfg.seed, [0])
+    theta = w = rho = None
+    with stages.scope():
+        for g in range(gens):
+            eps, chol, cum = float("inf"), None, None
+            if g >= 1:
+                eps = stages.quantile(rho, cfg.quantile)
+                _, cov, _ = stages.moments(theta, w)
+                chol = stages.make_kernel(cov, cfg.kernel_scale, cfg.jitter)
+                cum = stages.cumsum(w)
+            got = evaluated = accepted_total = 0
+            kept_theta, kept_rho = [], []
+            for t in range(max_rounds):
+                if got >= n:
+                    break
+                b, e = shard_range(round_size, world, rank)
+                first, count = t * round_size + b, e - b
+                if g == 0:
+                    th, r = stages.prior_rows(model, seed0, (t + 1) * round_size, first, count,
+                                              observed)
+                else:
+                    th, r = stages.propose(model, cfg.seed, g, first, count, theta, cum, chol,
+                                           observed, eps)
+                (th, r), counts = allgather_rows([th, r], group)
+                accepted = sum(counts)
+                take = min(accepted, n - got)
+                kept_theta.append(th[:take])
+                kept_rho.append(r[:take])
+                got += take
+                accepted_total += accepted
+                evaluated += round_size
+            if got != n:
+                raise RuntimeError("empty-set: generation did not fill within max_rounds")
+            theta_new = torch.cat(kept_theta).contiguous()
+            rho_new = torch.cat(kept_rho).contiguous()
+            if g == 0:
+                w_new = torch.full((n,), 1.0 / n, dtype=torch.float64, device=theta_new.device)
+            else:
+                w_local = stages.weights(theta_new[w_begin:w_end], theta, w, chol)
+                (w_raw,), _ = allgather_rows([w_local], group)
+                totals = torch.zeros(n_chunks, dtype=torch.float64, device=w_raw.device)
+                if w_end > w_begin:
+                    totals[c_begin:c_end] = stages.chunk_sums(w_local)
+                if world > 1:
+                    allreduce_sum(totals, group)
+                total = 0.0
+                for v in totals.tolist():  # chunk totals, left to right
+                    total += v
+                if not (np.isfinite(total) and total > 0.0):
+                    raise RuntimeError("degenerate-ensemble: weight sum is not finite")
+                w_new = stages.normalise(w_raw, total)
+            theta, w, rho = theta_new, w_new.contiguous(), rho_new
+            mean, cov, s2 = stages.moments(theta, w)
+            res["epsilon"][g], res["ess"][g] = eps, 1.0 / s2
+            res["accept_rate"][g] = accepted_total / evaluated
+            res["proposals"][g] = evaluated
+            res["mean"][g], res["cov"][g] = mean, cov
+        res["theta"] = theta.cpu().numpy()
+        res["weight"] = w.cpu().numpy()
+        res["rho"] = rho.cpu().numpy()
+    return res
+
+
+# --------------------------------------------------------------------------
+# configs 0, 2 and 4 over several GPUs
+# --------------------------------------------------------------------------
+def sharded_select(ctx, model, key, n_total, observed, accept_fraction, group=None):
+    """Config 0: every rank simulates its rows, the discrepancies (8 B/row, 8 MB
+    at N = 1e6) are all-gathered, and every rank runs the same select_epsilon
+    (abc.cpp:75-97) over the full vector -- epsilon and the ascending accepted
+    indices are identical on every rank and for every world size.  Returns
+    (epsilon, idx tensor, theta tensor of the accepted rows, rho tensor)."""
+    import torch
+    import torch.distributed as dist
+    from . import _abi as A
+    rank, world = _world(group)
+    begin, end = shard_range(n_total, world, rank)
+    count = end - begin
+    dev = torch.device("cuda", ctx.device_info()["device"])
+    real = torch.float32 if model.precision == A.VXB_F32 else torch.float64
+    with torch.cuda.stream(torch.cuda.ExternalStream(ctx.stream(), device=dev)):
+        theta = torch.empty((count, model.dim), dtype=real, device=dev)
+        rho = torch.empty(count, dtype=real, device=dev)
+        failed = torch.empty(count, dtype=torch.uint8, device=dev)
+        ctx.abc_prior_predictive(model, key, n_total, begin, count, observed, params=theta,
+                                 rho=rho, failed=failed)
+        if world > 1:
+            (rho_all, failed_all), counts = allgather_rows([rho, failed], group)
+        else:
+            rho_all, failed_all = rho, failed
+        cap = max(1024, int(4 * accept_fraction * n_total) + 64)
+        idx = torch.empty(cap, dtype=torch.int64, device=dev)
+        eps, _, n_acc = ctx.select_epsilon(rho_all.contiguous(), failed_all.contiguous(),
+                                           accept_fraction, cap, model.precision, n_total, idx)
+        idx = idx[:min(n_acc, cap)]
+        # accepted theta live on the rank that simulated them: gather in rank order
+        mine = idx[(idx >= begin) & (idx < end)] - begin
+        th_acc = theta.index_select(0, mine)
+        if world > 1:
+            (th_acc,), _ = allgather_rows([th_acc], group)
+        return eps, idx, th_acc, rho_all.index_select(0, idx)
+
+
+def sharded_counts(local_counts, group=None):
+    """Configs 2 and 4: integer counters of disjoint dataset / path ranges add up
+    with one all-reduce(SUM); integer sums are exact in any order."""
+    rank, world = _world(group)
+    if world > 1:
+        allreduce_sum(local_counts, group)
+    return local_counts

@@ -69,6 +69,16 @@ def derive_seed(seed, path):
     return int(load().vxb_derive_seed(seed, _ptr(a), len(a)))
 
 
+def make_kernel(cov, scale, jitter=1e-10):
+    """chol(scale * cov) with the jitter rule of smc.cpp:311-325 (host side)."""
+    cov = np.ascontiguousarray(cov, dtype=np.float64)
+    chol = np.zeros_like(cov)
+    rc = load().vxb_make_kernel(_ptr(cov), u32(cov.shape[0]), f64(scale), f64(jitter), _ptr(chol))
+    if rc:
+        raise VxbError(load().vxb_last_error().decode())
+    return chol
+
+
 def partition(total, workers, block_width):
     r = np.zeros((workers, 2), dtype=np.uint64)
     rc = load().vxb_partition(u64(total), u64(workers), u64(block_width), _ptr(r))
@@ -349,6 +359,41 @@ class Context:
         self._check(self.lib.vxb_abcsmc_run(self.handle, C.byref(model), C.byref(cfg), _ptr(obs),
                                             C.byref(out)))
         return res
+
+    # ---- population statistics (canonical order) for the multi-GPU host
+    def weighted_moments(self, theta, w, n=None, dim=None):
+        """theta (n x dim), w (n): numpy arrays or device tensors."""
+        if n is None:
+            n, dim = int(theta.shape[0]), int(theta.shape[1])
+        mean, cov, s2 = np.zeros(dim), np.zeros((dim, dim)), f64()
+        self._check(self.lib.vxb_weighted_moments(self.handle, _ptr(theta), _ptr(w), u64(n),
+                                                  u32(dim), _ptr(mean), _ptr(cov), C.byref(s2)))
+        return mean, cov, s2.value
+
+    def canon_cumsum(self, w, out=None):
+        n = int(w.shape[0])
+        if out is None:
+            out = np.zeros(n)
+        self._check(self.lib.vxb_canon_cumsum(self.handle, _ptr(w), u64(n), _ptr(out)))
+        return out
+
+    def canon_chunk_sums(self, v, out=None):
+        n = int(v.shape[0])
+        if out is None:
+            out = np.zeros((n + 255) // 256)
+        self._check(self.lib.vxb_canon_chunk_sums(self.handle, _ptr(v), u64(n), _ptr(out)))
+        return out
+
+    def divide(self, v, divisor):
+        """In place: v[i] <- v[i] / divisor (IEEE division on the device)."""
+        self._check(self.lib.vxb_divide(self.handle, _ptr(v), u64(int(v.shape[0])), f64(divisor)))
+        return v
+
+    def quantile(self, values, level):
+        out = f64()
+        self._check(self.lib.vxb_quantile(self.handle, _ptr(values), u64(int(values.shape[0])),
+                                          f64(level), C.byref(out)))
+        return out.value
 
     # ---- tau-leap
     def mlmc_level(self, model, cfg, level, first, count, want_y=False):

@@ -124,3 +124,96 @@ def test_two_rank_gather_equals_single_rank(tmp_path, oracle):
         assert np.array_equal(z["idx"], idx.astype(np.int64))      # ascending global order
         assert np.array_equal(z["p"], p[idx]) and np.array_equal(z["rho"], rho[idx])
         assert z["counts"].sum() == len(idx) == z["total"][0]
+
+
+# ---------------------------------------------------------------- ABC-SMC
+class OracleStages:
+    """Test stand-in for dist.DeviceStages: the same stage interface, computed by
+    the CPU oracle on torch CPU tensors (so the gloo run exercises exactly the
+    host logic that moves CUDA tensors over NCCL on the GPU box)."""
+
+    def __init__(self, oracle):
+        self.o = oracle
+
+    def scope(self):
+        import contextlib
+        return contextlib.nullcontext()
+
+    @staticmethod
+    def _keep(theta, rho, mask):
+        return (torch.from_numpy(np.ascontiguousarray(theta[mask])),
+                torch.from_numpy(np.ascontiguousarray(rho[mask])))
+
+    def prior_rows(self, model, seed0, n_total, first, count, observed):
+        p, _, rho, f = self.o.abc_prior_predictive(model, M.keying(seed0), n_total, first, count,
+                                                   observed, want_summaries=False)
+        return self._keep(p, rho, f == 0)
+
+    def propose(self, model, seed, gen, first, count, theta_prev, cum_prev, chol, observed, eps):
+        th, rho, flag = self.o.abcsmc_propose(model, seed, gen, first, count, theta_prev.numpy(),
+                                              cum_prev.numpy(), chol, observed, eps)
+        return self._keep(th, rho, flag == 1)
+
+    def weights(self, theta_new, theta_prev, w_prev, chol):
+        return torch.from_numpy(self.o.abcsmc_weights(theta_new.numpy(), theta_prev.numpy(),
+                                                      w_prev.numpy(), chol))
+
+    def quantile(self, values, level):
+        return self.o.quantile(values.numpy(), level)
+
+    def moments(self, theta, w):
+        return self.o.weighted_moments(theta.numpy(), w.numpy())
+
+    def cumsum(self, w):
+        return torch.from_numpy(self.o.canon_cumsum(w.numpy()))
+
+    def chunk_sums(self, v):
+        v = v.numpy()
+        return torch.tensor([self.o.canon_sum(v[i:i + D.CHUNK]) for i in range(0, v.size, D.CHUNK)],
+                            dtype=torch.float64)
+
+    def normalise(self, w_raw, total):
+        return torch.from_numpy(w_raw.numpy() / total)
+
+    def make_kernel(self, cov, scale, jitter):
+        return self.o.make_kernel(cov, scale, jitter)
+
+
+def smc_case():
+    from paper_1902_09046_b200 import _abi as A
+    m = M.logistic_model(steps=100, obs_stride=10)
+    cfg = A.vxb_abcsmc_cfg()
+    cfg.particles, cfg.generations, cfg.quantile = 700, 3, 0.5
+    cfg.kernel_scale, cfg.jitter, cfg.round_size, cfg.max_rounds, cfg.seed = 2.0, 1e-10, 900, 200, 11
+    return m, cfg
+
+
+def _smc_worker(rank, world, port, obs, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.pyoracle import Oracle
+    m, cfg = smc_case()
+    res = D.sharded_abcsmc(OracleStages(Oracle(threads=2)), m, cfg, obs)
+    np.savez(os.path.join(out_dir, f"smc{rank}.npz"), **res)
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_abcsmc_equals_single_run(tmp_path, oracle, world):
+    """Proposals and new particles sharded over ranks; accepted rows all-gathered,
+    chunk totals of the weights all-reduced: bit-identical to the one-process run
+    (oracle.abcsmc_run) for every world size."""
+    m, cfg = smc_case()
+    obs = oracle.simulate_at(m, [0.5, 100.0, 0.05], 5, 0, 0)
+    want = oracle.abcsmc_run(m, cfg, obs)
+    mp.spawn(_smc_worker, args=(world, free_port(), obs, str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        z = np.load(tmp_path / f"smc{r}.npz")
+        for k, v in want.items():
+            assert np.array_equal(z[k], v), (k, r)
+    # one rank, no process group: same driver, same result
+    got = D.sharded_abcsmc(OracleStages(oracle), m, cfg, obs)
+    for k, v in want.items():
+        assert np.array_equal(got[k], v), k

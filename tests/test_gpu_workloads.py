@@ -142,6 +142,52 @@ def test_abcsmc_run_parity(ctx, oracle, golden):
 
 
 @pytest.mark.timeout(900)
+def test_sharded_abcsmc_driver_on_device(ctx, oracle, golden):
+    """The multi-GPU ABC-SMC host driver (dist.sharded_abcsmc) with the device
+    stages, run as one rank: bit-identical to the native one-GPU driver
+    (vxb_abcsmc_run) and to the oracle; also the stage entry points it uses."""
+    import torch
+    from paper_1902_09046_b200 import dist as D
+    m = M.logistic_model()
+    obs = golden["logistic_observed"]
+    for cfg in (smc_cfg(n=2000, gens=4), smc_cfg(n=777, gens=3, seed=9, round_size=300)):
+        native = ctx.abcsmc_run(m, cfg, obs)
+        got = D.sharded_abcsmc(D.DeviceStages(ctx), m, cfg, obs)
+        for k in ("epsilon", "proposals", "accept_rate", "theta", "rho", "weight", "ess", "mean", "cov"):
+            assert eq(got[k], native[k]), k
+    want = oracle.abcsmc_run(m, cfg, obs)
+    assert eq(got["theta"], want["theta"]) and eq(got["weight"], want["weight"])
+    # stage entry points against the oracle (host and device buffers)
+    rs = np.random.RandomState(3)
+    theta = rs.normal(size=(1000, 3))
+    w = rs.uniform(0.1, 1.0, size=1000)
+    w /= oracle.canon_sum(w)
+    mean, cov, s2 = ctx.weighted_moments(theta, w)
+    mo, co, so = oracle.weighted_moments(theta, w)
+    assert eq(mean, mo) and eq(cov, co) and s2 == so
+    assert eq(ctx.canon_cumsum(w), oracle.canon_cumsum(w))
+    cs = ctx.canon_chunk_sums(w)
+    assert eq(cs, [oracle.canon_sum(w[i:i + 256]) for i in range(0, 1000, 256)])
+    assert ctx.quantile(w, 0.37) == oracle.quantile(w, 0.37)
+    assert eq(lib.make_kernel(cov, 2.0), oracle.make_kernel(cov, 2.0))
+    w_dev = torch.from_numpy(w).cuda()
+    assert eq(ctx.canon_cumsum(w_dev, torch.empty_like(w_dev)).cpu().numpy(), oracle.canon_cumsum(w))
+
+
+def test_sharded_select_on_device(ctx, oracle, golden):
+    """dist.sharded_select as one rank equals select_epsilon over the whole job."""
+    from paper_1902_09046_b200 import dist as D
+    m = M.logistic_model(steps=200, obs_stride=10)
+    obs = oracle.simulate_at(m, [0.5, 100.0, 0.05], 5, 0, 0)
+    n = 20000
+    p, _, rho, f = oracle.abc_prior_predictive(m, M.keying(1337), n, 0, n, obs, want_summaries=False)
+    eps_o, idx_o = oracle.select_epsilon(rho, f, 0.01)
+    eps, idx, th, r = D.sharded_select(ctx, m, M.keying(1337), n, obs, 0.01)
+    assert eps == eps_o and eq(idx.cpu().numpy(), idx_o)
+    assert eq(th.cpu().numpy(), p[idx_o]) and eq(r.cpu().numpy(), rho[idx_o])
+
+
+@pytest.mark.timeout(900)
 def test_abcsmc_fast_generator_statistics(ctx, golden):
     """Throughput mode (Philox4x32, FMA, whitened weights with table-based exp2)
     against the exact mode: same epsilon schedule, ESS and posterior moments
