@@ -383,6 +383,26 @@ class Ref(_Base):
                    u64(seed), _ptr(obs), _ptr(params), _ptr(summ), _ptr(rho), _ptr(failed))
         return params, summ, rho, failed
 
+    def logistic_abc_csv(self, model, n, workers, block_width, seed, observed, path):
+        """abc::write_csv of the reference's own run_prior_predictive result."""
+        obs = _f64(observed)
+        self._call("logistic_abc_csv", C.byref(model), u64(n), u64(workers), u64(block_width),
+                   u64(seed), _ptr(obs), C.c_char_p(os.fsencode(path)))
+
+    def bench_csv(self, records, path):
+        """bench::write_csv of (experiment, mode, threads, width, replicate, runtime, failed)."""
+        cols = list(zip(*records))
+        e, m = np.array(cols[0], dtype=np.int32), np.array(cols[1], dtype=np.int32)
+        t, w, r = (np.array(cols[k], dtype=np.uint64) for k in (2, 3, 4))
+        rt, f = np.array(cols[5], dtype=np.float64), np.array(cols[6], dtype=np.uint8)
+        self._call("bench_csv", u64(len(records)), _ptr(e), _ptr(m), _ptr(t), _ptr(w), _ptr(r),
+                   _ptr(rt), _ptr(f), C.c_char_p(os.fsencode(path)))
+
+    def amdahl_bound(self, serial, parallel, units):
+        out = f64()
+        self._call("amdahl_bound", f64(serial), f64(parallel), f64(units), C.byref(out))
+        return out.value
+
     def logistic_abc_particle(self, model, first, count, seed, observed, threads=None,
                               want_summaries=True):
         d, sd = model.dim, model.summary_dim

@@ -33,6 +33,7 @@
 #include <vector>
 
 #include "vexbayes/abc.hpp"
+#include "vexbayes/bench.hpp"
 #include "vexbayes/blocked.hpp"
 #include "vexbayes/errors.hpp"
 #include "vexbayes/fastmath.hpp"
@@ -467,6 +468,42 @@ int ref_resample_multinomial(std::uint64_t n, std::uint32_t dim, const double* l
                 ancestors[i] = static_cast<std::uint64_t>(tag.particles[i]);
         }
     });
+}
+
+// ------------------------------------------------ reference-format outputs
+// abc::write_csv (abc.cpp:99-124) of the set the reference's own
+// run_prior_predictive produces for the logistic hooks.
+int ref_logistic_abc_csv(const vxb_model* m, std::uint64_t n, std::uint64_t workers,
+                         std::uint64_t block_width, std::uint64_t seed, const double* observed,
+                         const char* path) {
+    return guarded([&] {
+        const ModelHooks hooks = logistic_for(*m);
+        std::vector<double> obs(observed, observed + hooks.summary_dim);
+        const abc::PriorPredictiveSet set = abc::run_prior_predictive(
+            hooks, n, workers, block_width, seed, std::span<const double>(obs));
+        abc::write_csv(set, std::string(path));
+    });
+}
+
+// bench::write_csv (bench.cpp:215-230: records section + summary section) of
+// caller-supplied records; experiment 0..3 = toggle-abc, weakinfo, bege, tb;
+// mode 0 scalar, 1 blocked.
+int ref_bench_csv(std::uint64_t n, const std::int32_t* experiment, const std::int32_t* mode,
+                  const std::uint64_t* threads, const std::uint64_t* width,
+                  const std::uint64_t* replicate, const double* runtime,
+                  const std::uint8_t* failed, const char* path) {
+    return guarded([&] {
+        std::vector<bench::BenchmarkRecord> records;
+        for (std::uint64_t i = 0; i < n; ++i)
+            records.push_back({static_cast<bench::Experiment>(experiment[i]),
+                               static_cast<bench::Mode>(mode[i]), threads[i], width[i],
+                               replicate[i], runtime[i], failed[i] != 0});
+        bench::write_csv(records, std::string(path));
+    });
+}
+
+int ref_amdahl_bound(double serial, double parallel, double units, double* out) {
+    return guarded([&] { *out = bench::amdahl_bound(serial, parallel, units); });
 }
 
 }  // extern "C"

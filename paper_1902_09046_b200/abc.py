@@ -73,3 +73,42 @@ def select_epsilon(ctx, pps, accept_fraction):
     """abc::select_epsilon (abc.cpp:75-97) on the GPU."""
     eps, idx, _ = ctx.select_epsilon(pps.discrepancies, pps.failed, accept_fraction)
     return EpsilonSelection(eps, idx)
+
+
+def write_csv(pps, out):
+    """abc::write_csv (abc.cpp:99-124): header ``row,theta_*,s_*,rho,failed``,
+    every real with ``%.17g``.  `out` is a path or a text file object."""
+    from .bench_harness import _c_g
+    head = ["row"] + [f"theta_{k + 1}" for k in range(pps.dim)] + \
+           [f"s_{k + 1}" for k in range(pps.summary_dim)] + ["rho", "failed"]
+    lines = [",".join(head)]
+    params = np.asarray(pps.params, dtype=np.float64).reshape(pps.rows, pps.dim)
+    summ = np.asarray(pps.summaries, dtype=np.float64).reshape(pps.rows, pps.summary_dim)
+    rho = np.asarray(pps.discrepancies, dtype=np.float64)
+    for r in range(pps.rows):
+        cells = [str(r)] + [_c_g(v, 17) for v in params[r].tolist()] + \
+                [_c_g(v, 17) for v in summ[r].tolist()] + [_c_g(float(rho[r]), 17),
+                                                          str(int(pps.failed[r]))]
+        lines.append(",".join(cells))
+    text = "\n".join(lines) + "\n"
+    if hasattr(out, "write"):
+        out.write(text)
+        return
+    try:
+        with open(out, "w", newline="") as fh:
+            fh.write(text)
+    except OSError:
+        raise VxbError(f"io-error: cannot open {out} for writing")
+
+
+def read_csv(text):
+    """Inverse of write_csv (``%.17g`` round-trips every double)."""
+    lines = [ln for ln in text.split("\n") if ln]
+    head = lines[0].split(",")
+    dim = sum(h.startswith("theta_") for h in head)
+    sd = sum(h.startswith("s_") for h in head)
+    body = np.array([[float(c) for c in ln.split(",")] for ln in lines[1:]], dtype=np.float64)
+    body = body.reshape(len(lines) - 1, len(head))
+    return PriorPredictiveSet(body.shape[0], dim, sd, body[:, 1:1 + dim].copy(),
+                              body[:, 1 + dim:1 + dim + sd].copy(), body[:, 1 + dim + sd].copy(),
+                              body[:, -1].astype(np.uint8))

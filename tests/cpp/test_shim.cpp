@@ -3,9 +3,12 @@
 // hex doubles for tests/test_gpu_cpp_shim.py to compare with the oracle.
 #include <cstdio>
 #include <cstring>
+#include <fstream>
+#include <sstream>
 #include <vector>
 
 #include "vexbayes/abc.hpp"
+#include "vexbayes/bench.hpp"
 #include "vexbayes/logistic.hpp"
 #include "vexbayes/rng.hpp"
 #include "vexbayes/smc.hpp"
@@ -23,8 +26,52 @@ static void dump(const char* name, const std::vector<double>& v) {
     std::printf("\n");
 }
 
-int main() {
+// Reference-format outputs (argv: golden bench csv, observed hex file, out dir):
+// the set of the fixture's (n, P, V, seed) case written by abc::write_csv, the
+// golden bench file parsed and written again, and a short run_benchmark sweep.
+static int csv_mode(const char* bench_golden, const char* out_dir) {
+    const std::string dir(out_dir);
+    std::ifstream in(bench_golden);
+    const auto records = bench::parse_csv(in);
+    bench::write_csv(records, dir + "/bench_rewritten.csv");
+
+    auto dm = std::make_shared<DeviceModel>(*logistic::make_abc_model().device);
+    dm->steps = 400;
+    dm->obs_stride = 100;
+    dm->summary_dim = 4;
+    dm->prior_hi[0] = 4000.0;
+    ModelHooks bad;
+    bad.dim = 3;
+    bad.summary_dim = 4;
+    bad.device = dm;
+    auto good = std::make_shared<DeviceModel>(*dm);
+    good->prior_hi[0] = 1.0;
+    ModelHooks ok = bad;
+    ok.device = good;
+    const auto observed = logistic::simulate_at(ok, std::vector<double>{0.5, 100.0, 0.05}, 5, 0, 0);
+    abc::write_csv(abc::run_prior_predictive(bad, 24, 3, 2, 21, observed), dir + "/set.csv");
+
+    bench::BenchConfig cfg;
+    cfg.threads = {1, 3};
+    cfg.block_widths = {1, 4};
+    cfg.replicates = 2;
+    cfg.sizes.samples = 32;
+    const auto sweep = bench::run_benchmark(cfg);
+    bench::write_csv(sweep, dir + "/sweep.csv");
+    int failures = 0;
+    for (const auto& r : sweep) failures += r.failed ? 1 : 0;
+    std::printf("sweep %zu %d\n", sweep.size(), failures);
+    int codes = 0;
+    try { bench::run_experiment_once(bench::Experiment::bege, cfg.sizes, 1, 1, 1); } catch (const Error& e) { codes += e.code() == "unsupported-model"; }
+    try { bench::amdahl_bound(0.0, 0.0, 2.0); } catch (const Error& e) { codes += e.code() == "invalid-input"; }
+    try { bench::experiment_from_string("toggle"); } catch (const Error& e) { codes += e.code() == "invalid-input"; }
+    std::printf("bench_errors %d amdahl %.17g\n", codes, bench::amdahl_bound(1.0, 9.0, 4.0));
+    return 0;
+}
+
+int main(int argc, char** argv) {
     try {
+        if (argc == 4 && std::string(argv[1]) == "csv") return csv_mode(argv[2], argv[3]);
         const ModelHooks model = logistic::make_abc_model();
         const std::vector<double> theta{0.5, 100.0, 0.05};
         const auto observed = logistic::simulate_at(model, theta, derive_seed(1, {90}), 0, 0);

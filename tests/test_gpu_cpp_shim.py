@@ -1,6 +1,7 @@
 """GPU test of the C++ shim (paper_1902_09046_b200/cpp/vexbayes): a program
 written against the reference's own API names is compiled with g++, linked to
 libvexbayes_cuda.so and its output compared with the oracle / reference."""
+import io
 import math
 import os
 import struct
@@ -62,3 +63,32 @@ def test_cpp_shim_matches_oracle(tmp_path, oracle, golden):
     counts, _, _ = oracle.ppp_pvalues(M.normal_mean_model(100), lam, ln, 20000, 0, 20000, 1337, 2.9)
     assert [int(t) for t in r["counts"]] == counts.tolist()
     assert [float(t) for t in r["pvalues"]] == [0.25, 0.75]
+
+
+def test_cpp_shim_reference_format_outputs(tmp_path, golden):
+    """abc::write_csv and the bench harness of the C++ shim: the set file equals
+    the file the reference wrote; the bench file survives parse -> write."""
+    from paper_1902_09046_b200 import bench_harness as B
+    exe = tmp_path / "test_shim"
+    pkg = os.path.join(ROOT, "paper_1902_09046_b200")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(pkg, "cpp"),
+                    os.path.join(ROOT, "tests", "cpp", "test_shim.cpp"), "-o", str(exe),
+                    "-L", pkg, "-lvexbayes_cuda", f"-Wl,-rpath,{pkg}"], check=True)
+    gold = os.path.join(ROOT, "tests", "golden")
+    run = subprocess.run([str(exe), "csv", os.path.join(gold, "bench_records.csv"), str(tmp_path)],
+                         capture_output=True, text=True, timeout=300)
+    assert run.returncode == 0, run.stdout + run.stderr
+    r = parse(run.stdout)
+    assert r["sweep"] == ["8", "0"]
+    assert r["bench_errors"][0] == "3" and float(r["bench_errors"][2]) == B.amdahl_bound(1.0, 9.0, 4.0)
+    read = lambda p: open(p, newline="").read()
+    assert read(tmp_path / "set.csv") == read(os.path.join(gold, "logistic_set.csv"))
+    text = read(os.path.join(gold, "bench_records.csv"))
+    want = io.StringIO()
+    B.write_csv(B.parse_csv(text), want)
+    assert read(tmp_path / "bench_rewritten.csv") == want.getvalue()
+    cut = text.index(B.SUMMARY_HEADER)
+    assert read(tmp_path / "bench_rewritten.csv")[:cut] == text[:cut]   # records section: reference bytes
+    sweep = B.parse_csv(read(tmp_path / "sweep.csv"))
+    assert [(x.block_width, x.threads, x.replicate) for x in sweep] == \
+        [(v, p, k) for v in (1, 4) for p in (1, 3) for k in (0, 1)]
