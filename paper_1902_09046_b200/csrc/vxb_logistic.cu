@@ -84,15 +84,15 @@ logistic_abc_kernel(const __grid_constant__ AbcParams p) {
     bool bad;
     Real rho;
     if (kRng == VXB_RNG_REF) {
-        RefNoise<Real> noise{key, noise_pos >> 1};
+        RefNoise<Real> noise(key, noise_pos >> 1);
         rho = logistic_path<Real, A>(p.model, theta, p.observed, noise, emit, bad);
     } else if (kRng == VXB_RNG_FAST) {
         const uint32_t rl = static_cast<uint32_t>(row), rh = static_cast<uint32_t>(row >> 32);
         if constexpr (sizeof(Real) == 4) {
-            FastNoise32 noise{p.key.fast, rl, rh, 0u};
+            FastNoise32 noise(p.key.fast, rl, rh, 0u);
             rho = logistic_path<Real, A>(p.model, theta, p.observed, noise, emit, bad);
         } else {
-            FastNoise64 noise{p.key.fast, s_log, rl, rh, 0u};
+            FastNoise64 noise(p.key.fast, s_log, rl, rh, 0u);
             rho = logistic_path<Real, A>(p.model, theta, p.observed, noise, emit, bad);
         }
     } else {

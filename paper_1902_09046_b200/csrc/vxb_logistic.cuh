@@ -87,33 +87,70 @@ __device__ __forceinline__ void draw_prior_fast(const LogisticModel& m, const Fa
 
 // ------------------------------------------------------------ noise sources
 // next(z) yields the next kBatch standard normals of the row.
+//
+// The counter-based generators run ONE BATCH AHEAD: next() turns the random bits
+// drawn during the previous call into normals and draws the bits of the
+// following batch.  The two halves are independent, so the integer Philox
+// rounds (FMA-heavy/ALU pipes) and the FP64 Box-Muller + SDE steps of a warp
+// sit in the same basic block and are interleaved by the instruction
+// scheduler.  Without this every warp alternates between an all-integer and an
+// all-FP64 phase, the warps of an SM sub-partition fall into step, and the
+// pipes are used one after the other instead of side by side (measured: the
+// step time was the SUM of the integer and FP64 pipe times).
 template <class Real>
 struct RefNoise {  // bit-identical to RngStream::fill_gaussian (rng.cpp:142-164)
     static constexpr int kBatch = 2;
     uint64_t key, pair;
+    Words ahead;
+    __device__ __forceinline__ RefNoise(uint64_t key_, uint64_t first_pair)
+        : key(key_), pair(first_pair + 1), ahead(philox2x64(key_, first_pair)) {}
     __device__ __forceinline__ void next(Real* z) {
+        const Words w = ahead;
+        ahead = philox2x64(key, pair++);
         double ze, zo;
-        box_muller<Exact>(philox2x64(key, pair++), ze, zo);
+        box_muller<Exact>(w, ze, zo);
         z[0] = static_cast<Real>(ze);
         z[1] = static_cast<Real>(zo);
     }
 };
 struct FastNoise64 {
-    static constexpr int kBatch = 2;
+    // eight normals from three Philox blocks (fast_box_muller_x4); batch q of the
+    // row uses blocks 3q, 3q+1, 3q+2 of its (domain, row) counter space
+    static constexpr int kBatch = 8;
     const FastKeys& fk;
     const double2* tbl;
-    uint32_t row_lo, row_hi, block;
-    uint32_t domain = kDomNoise;
+    uint32_t row_lo, row_hi, block, domain;
+    Words32 ahead0, ahead1, ahead2;
+    __device__ __forceinline__ FastNoise64(const FastKeys& fk_, const double2* tbl_, uint32_t rl,
+                                           uint32_t rh, uint32_t first_block,
+                                           uint32_t domain_ = kDomNoise)
+        : fk(fk_), tbl(tbl_), row_lo(rl), row_hi(rh), block(first_block), domain(domain_) {
+        draw();
+    }
+    __device__ __forceinline__ void draw() {
+        ahead0 = philox4x32(fk, block, domain, row_lo, row_hi);
+        ahead1 = philox4x32(fk, block + 1, domain, row_lo, row_hi);
+        ahead2 = philox4x32(fk, block + 2, domain, row_lo, row_hi);
+        block += 3;
+    }
     __device__ __forceinline__ void next(double* z) {
-        fast_box_muller(philox4x32(fk, block++, domain, row_lo, row_hi), tbl, z[0], z[1]);
+        const Words32 u = ahead0, v = ahead1, w = ahead2;
+        draw();
+        fast_box_muller_x4(u, v, w, tbl, z);
     }
 };
 struct FastNoise32 {
     static constexpr int kBatch = 4;
     const FastKeys& fk;
     uint32_t row_lo, row_hi, block;
+    Words32 ahead;
+    __device__ __forceinline__ FastNoise32(const FastKeys& fk_, uint32_t rl, uint32_t rh,
+                                           uint32_t first_block)
+        : fk(fk_), row_lo(rl), row_hi(rh), block(first_block + 1),
+          ahead(philox4x32(fk_, first_block, kDomNoise, rl, rh)) {}
     __device__ __forceinline__ void next(float* z) {
-        const Words32 w = philox4x32(fk, block++, kDomNoise, row_lo, row_hi);
+        const Words32 w = ahead;
+        ahead = philox4x32(fk, block++, kDomNoise, row_lo, row_hi);
         box_muller_f32(w.a, w.b, z[0], z[1]);
         box_muller_f32(w.c, w.d, z[2], z[3]);
     }

@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(256) abcsmc_propose_kernel(const __grid_consta
     double rho = __longlong_as_double(0x7FF8000000000000LL);
     uint8_t flag = 2;
     if (inside) {
-        RefNoise<double> noise{key, 3};
+        RefNoise<double> noise(key, 3);
         bool bad;
         auto emit = [](uint32_t, double) {};
         rho = logistic_path<double, Exact>(p.model, th, p.observed, noise, emit, bad);
@@ -478,10 +478,9 @@ abcsmc_propose_fast_kernel(const __grid_constant__ ProposeFastParams pp) {
     double rho = __longlong_as_double(0x7FF8000000000000LL);
     uint8_t flag = 2;
     if (inside) {
-        FastNoise64 noise{pp.fast, s_tab, rl, rh, 0u};
-        // noise domain of this generation: block counter offset keeps it apart from
-        // the proposal draws (domain kDomProposal) of the same row
-        noise.domain = kDomNoise | (pp.gen << 8);
+        // noise domain of this generation: keeps it apart from the proposal draws
+        // (domain kDomProposal) of the same row
+        FastNoise64 noise(pp.fast, s_tab, rl, rh, 0u, kDomNoise | (pp.gen << 8));
         bool bad;
         auto emit = [](uint32_t, double) {};
         rho = logistic_path<double, Fused>(p.model, th, p.observed, noise, emit, bad);

@@ -16,12 +16,12 @@ OUT = os.path.join(ROOT, "build_variants")
 
 VARIANTS = {
     "base": [],
-    "rounds7": ["-DVXB_FAST_ROUNDS=7"],
-    "block128": ["-DVXB_SIM_BLOCK=128"],
-    "block512": ["-DVXB_SIM_BLOCK=512"],
-    "minblk6": ["-DVXB_SIM_MIN_BLOCKS=6"],
-    "minblk8": ["-DVXB_SIM_MIN_BLOCKS=8"],
-    "block128_min12": ["-DVXB_SIM_BLOCK=128", "-DVXB_SIM_MIN_BLOCKS=12"],
+    "minblk4": ["-DVXB_SIM_MIN_BLOCKS=4"],
+    "minblk5": ["-DVXB_SIM_MIN_BLOCKS=5"],
+    "block128_min8": ["-DVXB_SIM_BLOCK=128", "-DVXB_SIM_MIN_BLOCKS=8"],
+    "block128_min10": ["-DVXB_SIM_BLOCK=128", "-DVXB_SIM_MIN_BLOCKS=10"],
+    "block512_min2": ["-DVXB_SIM_BLOCK=512", "-DVXB_SIM_MIN_BLOCKS=2"],
+    "block64_min16": ["-DVXB_SIM_BLOCK=64", "-DVXB_SIM_MIN_BLOCKS=16"],
 }
 
 
