@@ -164,6 +164,11 @@ int vxb_rng_fill_uniform(vxb_ctx* ctx, uint64_t seed, uint32_t stream_id, uint64
                          uint64_t n, double a, double b, double* out);
 int vxb_rng_fill_gaussian(vxb_ctx* ctx, uint64_t seed, uint32_t stream_id, uint64_t pos,
                           uint64_t n, double mu, double sigma, double* out);
+/* The standard normals of the throughput generator (VXB_RNG_FAST) exactly as the
+ * simulation kernels consume them: row r of [first_row, first_row+rows), step j
+ * -> out[r*per_row + j]; element type by precision.  For statistical validation. */
+int vxb_rng_fill_gaussian_fast(vxb_ctx* ctx, int precision, uint64_t seed, uint64_t first_row,
+                               uint64_t rows, uint32_t per_row, void* out);
 /* Device evaluation of the fastmath functions (fastmath.hpp:23-128), for
  * parity tests: fn 0 log2_pos, 1 ln_pos, 2 exp2_clamped, 3 sinpi, 4 cospi,
  * 5 pow_pos (x = base, y = exponent; y ignored otherwise). */

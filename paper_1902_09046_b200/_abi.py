@@ -72,7 +72,7 @@ EXPORTED_SYMBOLS = (
     "vxb_stream", "vxb_synchronize", "vxb_profile_enable", "vxb_profile_reset",
     "vxb_profile_read", "vxb_fma_peak", "vxb_device_alloc", "vxb_device_free", "vxb_copy",
     "vxb_splitmix64", "vxb_derive_seed", "vxb_rng_fill_u64", "vxb_rng_fill_uniform",
-    "vxb_rng_fill_gaussian", "vxb_fastmath_eval", "vxb_partition",
+    "vxb_rng_fill_gaussian", "vxb_rng_fill_gaussian_fast", "vxb_fastmath_eval", "vxb_partition",
     "vxb_abc_prior_predictive", "vxb_select_epsilon", "vxb_order_statistics",
     "vxb_compact_accepted", "vxb_abc_reject", "vxb_simulate_at", "vxb_ppp_pvalues",
     "vxb_ess", "vxb_logsumexp", "vxb_resample_multinomial", "vxb_abcsmc_run",

@@ -109,6 +109,40 @@ logistic_abc_kernel(const __grid_constant__ AbcParams p) {
     if (p.failed) p.failed[r] = bad ? 1 : 0;
 }
 
+// The standard normals the step loop of the throughput generator consumes for
+// rows [first, first+rows): row r, step j -> out[r * per_row + j].  Validation
+// aid (vxb_rng_fill_gaussian_fast); same noise sources as the kernels above.
+template <class Real>
+__global__ void __launch_bounds__(128) fast_normals_kernel(FastKeys fk, const double2* table,
+                                                           uint64_t first, uint64_t rows,
+                                                           uint32_t per_row, Real* out) {
+    __shared__ double2 s_tab[sizeof(Real) == 8 ? kFastTableSize : 1];
+    if (sizeof(Real) == 8) {
+        for (int i = threadIdx.x; i < kFastTableSize; i += 128) s_tab[i] = table[i];
+        __syncthreads();
+    }
+    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * 128 + threadIdx.x;
+    if (r >= rows) return;
+    const uint64_t row = first + r;
+    const uint32_t rl = static_cast<uint32_t>(row), rh = static_cast<uint32_t>(row >> 32);
+    Real* dst = out + r * per_row;
+    auto run = [&](auto& noise) {
+        constexpr uint32_t kB = std::remove_reference<decltype(noise)>::type::kBatch;
+        for (uint32_t j = 0; j < per_row; j += kB) {
+            Real z[kB];
+            noise.next(z);
+            for (uint32_t q = 0; q < kB && j + q < per_row; ++q) dst[j + q] = z[q];
+        }
+    };
+    if constexpr (sizeof(Real) == 8) {
+        FastNoise64 noise(fk, s_tab, rl, rh, 0u);
+        run(noise);
+    } else {
+        FastNoise32 noise(fk, rl, rh, 0u);
+        run(noise);
+    }
+}
+
 // Re-derives the prior draw of accepted rows and gathers their rho (fused
 // fixed-epsilon path: rejected rows never leave the device).
 template <class Real, int kRng>
@@ -399,5 +433,32 @@ extern "C" int vxb_abc_reject(vxb_ctx* ctx, const vxb_model* model, const vxb_ke
         d_params.finish(kept * 3 * real);
         d_rho.finish(kept * real);
         VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+extern "C" int vxb_rng_fill_gaussian_fast(vxb_ctx* ctx, int precision, uint64_t seed,
+                                          uint64_t first_row, uint64_t rows, uint32_t per_row,
+                                          void* out) {
+    return guarded([&] {
+        use(ctx);
+        require(precision == VXB_F64 || precision == VXB_F32, "invalid-argument",
+                "unknown precision");
+        if (rows == 0 || per_row == 0) return;
+        require(out != nullptr, "invalid-argument", "null output");
+        const size_t elem = precision == VXB_F32 ? 4 : 8;
+        Staged d_out(ctx, out, rows * per_row * elem, false, true);
+        const FastKeys fk = make_fast_keys(splitmix64(seed));
+        {
+            LaunchScope scope(ctx, VXB_K_RNGFILL);
+            if (precision == VXB_F32)
+                fast_normals_kernel<float><<<grid_for(rows, 128), 128, 0, ctx->stream>>>(
+                    fk, ctx->log_table, first_row, rows, per_row, d_out.as<float>());
+            else
+                fast_normals_kernel<double><<<grid_for(rows, 128), 128, 0, ctx->stream>>>(
+                    fk, ctx->log_table, first_row, rows, per_row, d_out.as<double>());
+            check_launch("fast_normals_kernel");
+        }
+        d_out.finish();
+        if (d_out.staged()) VXB_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }

@@ -140,19 +140,26 @@ struct FastNoise64 {
     }
 };
 struct FastNoise32 {
-    static constexpr int kBatch = 4;
+    // sixteen normals from three Philox blocks (box_muller_f32_x8)
+    static constexpr int kBatch = 16;
     const FastKeys& fk;
     uint32_t row_lo, row_hi, block;
-    Words32 ahead;
+    Words32 ahead0, ahead1, ahead2;
     __device__ __forceinline__ FastNoise32(const FastKeys& fk_, uint32_t rl, uint32_t rh,
                                            uint32_t first_block)
-        : fk(fk_), row_lo(rl), row_hi(rh), block(first_block + 1),
-          ahead(philox4x32(fk_, first_block, kDomNoise, rl, rh)) {}
+        : fk(fk_), row_lo(rl), row_hi(rh), block(first_block) {
+        draw();
+    }
+    __device__ __forceinline__ void draw() {
+        ahead0 = philox4x32(fk, block, kDomNoise, row_lo, row_hi);
+        ahead1 = philox4x32(fk, block + 1, kDomNoise, row_lo, row_hi);
+        ahead2 = philox4x32(fk, block + 2, kDomNoise, row_lo, row_hi);
+        block += 3;
+    }
     __device__ __forceinline__ void next(float* z) {
-        const Words32 w = ahead;
-        ahead = philox4x32(fk, block++, kDomNoise, row_lo, row_hi);
-        box_muller_f32(w.a, w.b, z[0], z[1]);
-        box_muller_f32(w.c, w.d, z[2], z[3]);
+        const Words32 u = ahead0, v = ahead1, w = ahead2;
+        draw();
+        box_muller_f32_x8(u, v, w, z);
     }
 };
 template <class Real>

@@ -173,6 +173,14 @@ class Context:
                                                    _ptr(out)))
         return out
 
+    def rng_fill_gaussian_fast(self, precision, seed, first_row, rows, per_row):
+        """Normals of the throughput generator as the step loop consumes them."""
+        out = np.zeros((rows, per_row), dtype=np.float32 if precision == A.VXB_F32 else np.float64)
+        self._check(self.lib.vxb_rng_fill_gaussian_fast(self.handle, i32(precision), u64(seed),
+                                                        u64(first_row), u64(rows), u32(per_row),
+                                                        _ptr(out)))
+        return out
+
     def fastmath(self, fn, x, y=None):
         x = np.ascontiguousarray(x, dtype=np.float64)
         y = np.ascontiguousarray(y, dtype=np.float64) if y is not None else None

@@ -275,3 +275,48 @@ def test_fast_generator_statistics(ctx, oracle, golden):
         d = np.abs(np.searchsorted(np.sort(rf.astype(np.float64)), xs, side="right") / n
                    - np.searchsorted(np.sort(rho), xs, side="right") / n).max()
         assert d < 1.628 * math.sqrt(2.0 / n)
+
+
+@pytest.mark.parametrize("precision", [A.VXB_F64, A.VXB_F32])
+def test_fast_generator_normals(ctx, precision):
+    """The throughput generator's normals, exactly as the step loop consumes them
+    (three Philox4x32 blocks per batch, bit fields shared between variates):
+    moments, Kolmogorov-Smirnov against N(0,1), tail mass, serial and
+    within-batch correlations, shard independence."""
+    from math import erf, sqrt
+    rows, per = 4096, 2000
+    z = ctx.rng_fill_gaussian_fast(precision, 99, 0, rows, per).astype(np.float64)
+    n = z.size
+    assert np.isfinite(z).all()
+    assert abs(z.mean()) < 5 / sqrt(n)
+    assert abs(z.var() - 1.0) < 5 * sqrt(2.0 / n)
+    assert abs((z ** 3).mean()) < 5 * sqrt(15.0 / n)
+    assert abs((z ** 4).mean() - 3.0) < 5 * sqrt(96.0 / n)
+    # KS against the normal CDF on a 400k subsample, alpha = 0.001 -> c = 1.95
+    sub = np.sort(z.ravel()[::20])
+    cdf = 0.5 * (1.0 + np.vectorize(erf)(sub / sqrt(2.0)))
+    k = np.arange(1, sub.size + 1) / sub.size
+    d = max(np.abs(cdf - k).max(), np.abs(cdf - (k - 1.0 / sub.size)).max())
+    assert d < 1.95 / sqrt(sub.size)
+    # tails: P(|z| > 3) = 2.6998e-3, P(|z| > 4) = 6.334e-5
+    for t, p in ((3.0, 2.6998e-3), (4.0, 6.334e-5)):
+        cnt = (np.abs(z) > t).sum()
+        assert abs(cnt - n * p) < 5 * sqrt(n * p)
+    # correlations: neighbouring steps, the two halves of a pair, variates that share
+    # Philox words inside a batch (lags up to one batch), squares (radius sharing)
+    batch = 16 if precision == A.VXB_F32 else 8
+    zc = z - z.mean()
+    for lag in list(range(1, batch + 1)) + [2 * batch]:
+        r = (zc[:, :-lag] * zc[:, lag:]).mean()
+        assert abs(r) < 5 / sqrt(rows * (per - lag)), (lag, r)
+        r2 = ((z[:, :-lag] ** 2 - 1) * (z[:, lag:] ** 2 - 1)).mean() / 2.0
+        if lag != 1:   # the two halves of a Box-Muller pair share the radius exactly as they should: z0^2 + z1^2 = r^2
+            assert abs(r2) < 5 / sqrt(rows * (per - lag)), (lag, r2)
+    # rows are independent streams; a shard sees the same numbers
+    r = (zc[:-1] * zc[1:]).mean()
+    assert abs(r) < 5 / sqrt(n)
+    part = ctx.rng_fill_gaussian_fast(precision, 99, 1000, 16, per)
+    assert np.array_equal(part, ctx.rng_fill_gaussian_fast(precision, 99, 0, rows, per)[1000:1016])
+    # ragged request lengths give prefixes of the same stream
+    short = ctx.rng_fill_gaussian_fast(precision, 99, 0, 8, 37)
+    assert np.array_equal(short.astype(np.float64), z[:8, :37])
