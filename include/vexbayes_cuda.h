@@ -325,6 +325,61 @@ int vxb_quantile(vxb_ctx* ctx, const double* values, uint64_t n, double level, d
 int vxb_divide(vxb_ctx* ctx, double* v, uint64_t n, double divisor);
 int vxb_make_kernel(const double* cov, uint32_t dim, double scale, double jitter, double* chol);
 
+/* ------------------ likelihood-annealed SMC / weak-informativity test */
+/* The bioassay model (weak_info.cpp:18-160): M dose groups, group sizes n_g,
+ * deaths y_g, p_g = 1/(1 + exp(b0 + b1 x_g)), prior (b0, b1) ~ N(0, diag(l1, l2)^2).
+ *
+ * vxb_bioassay_log_likelihood: bioassay_block_log_likelihood (weak_info.cpp:72-80)
+ *   over `lanes` (b0, b1) pairs, row-major.
+ * vxb_bioassay_sample: n independent sample_prior_predictive draws
+ *   (weak_info.cpp:82-106), draw j from RngStream(seeds[j], 0) under the prior
+ *   lambda[2j..2j+1]; theta (optional) n x 2, deaths n x groups.
+ * vxb_smc_bioassay: n_runs independent evidence estimates, run r = smc::run_smc
+ *   (smc.cpp:352-488; workers = 1, fixed proposal scale, SmcConfig defaults) on
+ *   make_bioassay_model(deaths[r], lambda[r]) with seed seeds[r] -- the
+ *   evidence_of closure of weak_info.cpp:200-215.  One CTA per run.  status[r]:
+ *   0 ok, 1 invalid-model, 2 degenerate-ensemble, 3 non-convergence (the errors
+ *   the reference turns into a skipped evidence); log_evidence is NaN then.
+ *   trace (optional): n_runs x trace_rows x 4 doubles per iteration: temperature,
+ *   ESS after reweighting, move steps R_n, pilot acceptance (smc.hpp:125).
+ *   deaths, lambda, seeds: host arrays.  particles <= 2048. */
+int vxb_bioassay_log_likelihood(vxb_ctx* ctx, const double* beta, uint64_t lanes, uint32_t groups,
+                                const double* dose, const uint32_t* group_size,
+                                const uint32_t* deaths, double* out);
+int vxb_bioassay_sample(vxb_ctx* ctx, uint64_t n, uint32_t groups, const double* dose,
+                        const uint32_t* group_size, const double* lambda, const uint64_t* seeds,
+                        double* theta, uint32_t* deaths);
+int vxb_smc_bioassay(vxb_ctx* ctx, uint64_t n_runs, uint32_t groups, const double* dose,
+                     const uint32_t* group_size, const uint32_t* deaths, const double* lambda,
+                     const uint64_t* seeds, uint64_t particles, uint64_t block_width, double c,
+                     double scale, double* log_evidence, uint32_t* iterations, uint8_t* status,
+                     double* trace, uint32_t trace_rows);
+
+/* WeakInfoConfig (weak_info.hpp:62-75) as a POD; `workers` has no device meaning
+ * (all 2 (K+1) N sampler runs are one launch). */
+typedef struct vxb_weakinfo_cfg {
+    uint64_t hyper_count;  /* K                                   */
+    uint64_t datasets;     /* N per prior                         */
+    uint64_t particles;    /* N_p                                 */
+    uint64_t block_width;  /* validated (blocked.cpp:10-12) only  */
+    uint64_t seed;
+    double alpha;
+    double c;
+    double scale;          /* h; <= 0 selects 2.38/sqrt(2)        */
+    double base[2];        /* base prior (10, 2.5)                */
+    int32_t redraw_base;
+    uint32_t groups;
+    uint32_t group_size[16];
+    double dose[16];
+} vxb_weakinfo_cfg;
+
+/* run_weak_info_test (weak_info.cpp:163-277): outputs per row k = 0..K (row 0 is
+ * the base prior): lambda (K+1) x 2, gamma, weakly_informative, completed.
+ * evidence (optional): (K+1) x N x 2 log evidences, [k][i][0] base data,
+ * [k][i][1] data drawn under prior k (NaN where the sampler failed). */
+int vxb_weak_info_test(vxb_ctx* ctx, const vxb_weakinfo_cfg* cfg, double* lambda, double* gamma,
+                       uint8_t* weakly, uint64_t* completed, double* evidence);
+
 /* ------------------------------------------------ tau-leap MLMC (C4) */
 typedef struct vxb_mlmc_cfg {
     uint32_t levels;       /* L+1 levels, l = 0..L              */

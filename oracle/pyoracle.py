@@ -62,6 +62,41 @@ class _Base:
     def _call(self, name, *args):
         self._check(getattr(self.lib, self.prefix + name)(*args))
 
+    # ---- likelihood-annealed SMC / weak-informativity test
+    @staticmethod
+    def _design(dose, group_size, deaths=None):
+        d = _f64(dose)
+        g = np.ascontiguousarray(group_size, dtype=np.uint32)
+        y = None if deaths is None else np.ascontiguousarray(deaths, dtype=np.uint32)
+        return d, g, y
+
+    def bioassay_ll(self, beta, dose, group_size, deaths):
+        b = _f64(beta).reshape(-1, 2)
+        d, g, y = self._design(dose, group_size, deaths)
+        out = np.zeros(b.shape[0])
+        self._call("bioassay_ll", _ptr(b), u64(b.shape[0]), _ptr(d), _ptr(g), _ptr(y), u32(d.size),
+                   _ptr(out))
+        return out
+
+    def bioassay_sample(self, lambda1, lambda2, dose, group_size, seed):
+        d, g, _ = self._design(dose, group_size)
+        theta, deaths = np.zeros(2), np.zeros(d.size, dtype=np.uint32)
+        self._call("bioassay_sample", f64(lambda1), f64(lambda2), _ptr(d), _ptr(g), u32(d.size),
+                   u64(seed), _ptr(theta), _ptr(deaths))
+        return theta, deaths
+
+    def weak_info_test(self, hyper_count, datasets, particles, alpha=0.05, c=0.01,
+                       scale=1.6828427124746189, workers=1, block_width=4, seed=0,
+                       redraw_base=False, csv_path=None):
+        k = hyper_count + 1
+        lam, gamma = np.zeros((k, 2)), np.zeros(k)
+        weakly, completed = np.zeros(k, dtype=np.uint8), np.zeros(k, dtype=np.uint64)
+        self._call("weak_info_test", u64(hyper_count), u64(datasets), u64(particles), f64(alpha),
+                   f64(c), f64(scale), u64(workers), u64(block_width), u64(seed),
+                   C.c_int(1 if redraw_base else 0), _ptr(lam), _ptr(gamma), _ptr(weakly),
+                   _ptr(completed), C.c_char_p(os.fsencode(csv_path)) if csv_path else None)
+        return dict(lambda_=lam, gamma=gamma, weakly=weakly, completed=completed)
+
 
 class Oracle(_Base):
     prefix = "vxo_"
@@ -79,6 +114,19 @@ class Oracle(_Base):
         self.lib.vxo_canon_sum.restype = f64
 
     # ---- substrate
+    def smc_bioassay(self, dose, group_size, deaths, lambda1, lambda2, particles, block_width, c,
+                     scale, seed, want_trace=False):
+        """trace columns: temperature, ess, steps (R_n), pilot acceptance."""
+        d, g, y = self._design(dose, group_size, deaths)
+        ev, it = f64(), u64()
+        tr = np.zeros((1000, 4)) if want_trace else None
+        self._call("smc_bioassay", _ptr(d), _ptr(g), _ptr(y), u32(d.size), f64(lambda1),
+                   f64(lambda2), u64(particles), u64(block_width), f64(c), f64(scale), u64(seed),
+                   C.byref(ev), C.byref(it), _ptr(tr), u64(1000))
+        if not want_trace:
+            return ev.value, it.value
+        return ev.value, it.value, tr[:it.value]
+
     def splitmix64(self, z):
         return int(self.lib.vxo_splitmix64(z))
 
@@ -310,6 +358,20 @@ class Ref(_Base):
         self.lib.ref_derive_seed.restype = u64
         self.lib.ref_derive_seed.argtypes = [u64, P, C.c_size_t]
         self.lib.ref_discrepancy.restype = f64
+
+    def smc_bioassay(self, dose, group_size, deaths, lambda1, lambda2, particles, block_width, c,
+                     scale, seed, want_trace=False):
+        d, g, y = self._design(dose, group_size, deaths)
+        ev, it = f64(), u64()
+        buf = C.create_string_buffer(1 << 16) if want_trace else None
+        self._call("smc_bioassay", _ptr(d), _ptr(g), _ptr(y), u32(d.size), f64(lambda1),
+                   f64(lambda2), u64(particles), u64(block_width), f64(c), f64(scale), u64(seed),
+                   C.byref(ev), C.byref(it), buf, u64(len(buf) if buf else 0))
+        if not want_trace:
+            return ev.value, it.value
+        rows = [ln.split(",") for ln in buf.value.decode().strip().splitlines()[1:]]
+        full = np.array([[float(x) for x in r] for r in rows])  # n,t_n,ess,log_evidence,R_n,p_acc,h
+        return ev.value, it.value, full[:, [1, 2, 4, 5]]       # temperature, ess, steps, p_acc
 
     def splitmix64(self, z):
         return int(self.lib.ref_splitmix64(z))

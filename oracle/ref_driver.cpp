@@ -27,6 +27,8 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <fstream>
+#include <sstream>
 #include <limits>
 #include <string>
 #include <thread>
@@ -504,6 +506,108 @@ int ref_bench_csv(std::uint64_t n, const std::int32_t* experiment, const std::in
 
 int ref_amdahl_bound(double serial, double parallel, double units, double* out) {
     return guarded([&] { *out = bench::amdahl_bound(serial, parallel, units); });
+}
+
+// ------------------------------------ likelihood-annealed SMC / weak-info test
+//   The bioassay model (weak_info.cpp:18-160), the adaptive
+// sampler smc::run_smc (smc.cpp:352-488) and run_weak_info_test
+// (weak_info.cpp:163-277), called as they are.
+static weakinfo::BioassayData make_data(const double* dose, const std::uint32_t* group_size,
+                                        const std::uint32_t* deaths, std::uint32_t groups) {
+    weakinfo::BioassayData d;
+    d.dose.assign(dose, dose + groups);
+    d.group_size.assign(group_size, group_size + groups);
+    if (deaths) d.deaths.assign(deaths, deaths + groups);
+    return d;
+}
+
+int ref_bioassay_ll(const double* beta, std::uint64_t lanes, const double* dose,
+                    const std::uint32_t* group_size, const std::uint32_t* deaths,
+                    std::uint32_t groups, double* out) {
+    return guarded([&] {
+        const auto data = make_data(dose, group_size, deaths, groups);
+        weakinfo::bioassay_block_log_likelihood(std::span<const double>(beta, 2 * lanes), lanes,
+                                                data, std::span<double>(out, lanes));
+    });
+}
+
+int ref_bioassay_sample(double lambda1, double lambda2, const double* dose,
+                        const std::uint32_t* group_size, std::uint32_t groups, std::uint64_t seed,
+                        double* theta, std::uint32_t* deaths) {
+    return guarded([&] {
+        RngStream stream(seed, 0);
+        const auto draw = weakinfo::sample_prior_predictive({lambda1, lambda2},
+                                                            make_data(dose, group_size, nullptr, groups),
+                                                            stream);
+        theta[0] = draw.theta[0];
+        theta[1] = draw.theta[1];
+        std::copy(draw.data.deaths.begin(), draw.data.deaths.end(), deaths);
+    });
+}
+
+// One evidence estimate (the evidence_of closure of weak_info.cpp:200-215);
+// trace receives the sampler's per-iteration CSV (smc.hpp:125).
+int ref_smc_bioassay(const double* dose, const std::uint32_t* group_size,
+                     const std::uint32_t* deaths, std::uint32_t groups, double lambda1,
+                     double lambda2, std::uint64_t particles, std::uint64_t block_width, double c,
+                     double scale, std::uint64_t seed, double* log_evidence,
+                     std::uint64_t* iterations, char* trace, std::uint64_t trace_cap) {
+    return guarded([&] {
+        smc::SmcConfig cfg;
+        cfg.particles = particles;
+        cfg.block_width = block_width;
+        cfg.workers = 1;
+        cfg.c = c;
+        cfg.scale = scale;
+        cfg.seed = seed;
+        std::ostringstream text;
+        text.precision(17);
+        if (trace) cfg.trace = &text;
+        const auto model = weakinfo::make_bioassay_model(make_data(dose, group_size, deaths, groups),
+                                                         {lambda1, lambda2});
+        const smc::SmcResult res = smc::run_smc(model, cfg);
+        *log_evidence = res.log_evidence;
+        *iterations = res.iterations;
+        if (trace && trace_cap) {
+            const std::string t = text.str();
+            const std::size_t k = std::min<std::size_t>(t.size(), trace_cap - 1);
+            std::memcpy(trace, t.data(), k);
+            trace[k] = 0;
+        }
+    });
+}
+
+int ref_weak_info_test(std::uint64_t hyper_count, std::uint64_t datasets, std::uint64_t particles,
+                       double alpha, double c, double scale, std::uint64_t workers,
+                       std::uint64_t block_width, std::uint64_t seed, int redraw_base,
+                       double* lambda /* (K+1) x 2 */, double* gamma, std::uint8_t* weakly,
+                       std::uint64_t* completed, const char* csv_path) {
+    return guarded([&] {
+        weakinfo::WeakInfoConfig cfg;
+        cfg.hyper_count = hyper_count;
+        cfg.datasets = datasets;
+        cfg.particles = particles;
+        cfg.alpha = alpha;
+        cfg.c = c;
+        cfg.scale = scale;
+        cfg.workers = workers;
+        cfg.block_width = block_width;
+        cfg.seed = seed;
+        cfg.redraw_base = redraw_base != 0;
+        const weakinfo::CutoffTable table = weakinfo::run_weak_info_test(cfg);
+        for (std::size_t k = 0; k < table.rows.size(); ++k) {
+            const auto& row = table.rows[k];
+            lambda[2 * k] = row.lambda.lambda1;
+            lambda[2 * k + 1] = row.lambda.lambda2;
+            gamma[k] = row.gamma;
+            weakly[k] = row.weakly_informative ? 1 : 0;
+            completed[k] = row.completed;
+        }
+        if (csv_path) {
+            std::ofstream out(csv_path);
+            weakinfo::write_csv(table, out);
+        }
+    });
 }
 
 }  // extern "C"

@@ -1339,4 +1339,358 @@ int vxo_mm_gillespie(const vxb_model* m, double t_end, std::uint64_t paths, std:
     });
 }
 
+// ------------------------- likelihood-annealed SMC on the bioassay model (8f-3)
+// Restates, operation for operation, what the weak-informativity test runs for
+// every (dataset, prior) pair: the model of weak_info.cpp:18-160 inside the
+// adaptive sampler smc::run_smc (smc.cpp:352-488) with workers = 1, fixed scale
+// (no ESJD).  Particles are independent given the iteration's temperature and
+// kernel, and every variate has a fixed stream position (smc.cpp:66-76), so the
+// loops below run over particles where the reference runs over lane blocks.
+struct Bioassay {
+    std::uint32_t groups;
+    double dose[16], miss[16], hit[16], log_choose[16];
+    double l1, l2, log_norm;
+    // -log p = log(1 + e^b), weak_info.cpp:20-24
+    static double softplus(double b) {
+        const double pos = b > 0.0 ? b : 0.0;
+        const double mag = b > 0.0 ? b : -b;
+        return pos + ln_pos(1.0 + exp2_clamped(-mag * kInvLn2));
+    }
+    // ll_lane: weak_info.cpp:26-40
+    double log_lik(double b0, double b1) const {
+        double total = 0.0;
+        for (std::uint32_t g = 0; g < groups; ++g) {
+            const double b = b0 + b1 * dose[g];
+            const double lse = softplus(b);
+            total += log_choose[g];
+            if (hit[g] > 0.0) total -= hit[g] * lse;
+            if (miss[g] > 0.0) total += miss[g] * (b - lse);
+        }
+        return total;
+    }
+    // log_prior hook: weak_info.cpp:144-148
+    double log_prior(double b0, double b1) const {
+        const double a = b0 / l1;
+        const double b = b1 / l2;
+        return log_norm - 0.5 * (a * a + b * b);
+    }
+};
+
+static Bioassay make_bioassay(const double* dose, const std::uint32_t* group_size,
+                              const std::uint32_t* deaths, std::uint32_t groups, double l1,
+                              double l2) {
+    require(groups >= 1 && groups <= 16, "invalid-argument", "between 1 and 16 dose groups");
+    require(l1 > 0.0 && l2 > 0.0, "invalid-argument", "prior scales must be positive");
+    Bioassay m{};
+    m.groups = groups;
+    m.l1 = l1;
+    m.l2 = l2;
+    m.log_norm = -std::log(2.0 * 3.141592653589793238462643 * l1 * l2);  // weak_info.cpp:135
+    for (std::uint32_t g = 0; g < groups; ++g) {
+        require(deaths[g] <= group_size[g], "invalid-argument", "more deaths than animals in a group");
+        m.dose[g] = dose[g];
+        m.hit[g] = deaths[g];
+        m.miss[g] = group_size[g] - deaths[g];
+        // log_binomial: numeric.cpp:98-102
+        m.log_choose[g] = std::lgamma(group_size[g] + 1.0) - std::lgamma(deaths[g] + 1.0) -
+                          std::lgamma(static_cast<double>(group_size[g] - deaths[g]) + 1.0);
+    }
+    return m;
+}
+
+// sample_prior_predictive (weak_info.cpp:82-106) from RngStream(seed, 0)
+static void bioassay_draw(double l1, double l2, const double* dose, const std::uint32_t* group_size,
+                          std::uint32_t groups, std::uint64_t seed, double* theta,
+                          std::uint32_t* deaths) {
+    require(l1 >= 0.0 && l2 >= 0.0, "invalid-argument", "prior scales must be nonnegative");
+    Stream s(seed, 0);
+    s.align_even();
+    const double z0 = s.next_gaussian(0.0, 1.0), z1 = s.next_gaussian(0.0, 1.0);
+    theta[0] = l1 * z0;
+    theta[1] = l2 * z1;
+    for (std::uint32_t g = 0; g < groups; ++g) {
+        const double b = theta[0] + theta[1] * dose[g];
+        const double p = exp2_clamped(-Bioassay::softplus(b) * kInvLn2);
+        std::uint32_t k = 0;
+        for (std::uint32_t j = 0; j < group_size[g]; ++j) k += s.next_unit() < p ? 1 : 0;
+        deaths[g] = k;
+    }
+}
+
+struct AnnealTrace {
+    std::vector<double> temperature, ess, accept;
+    std::vector<std::uint64_t> steps;
+};
+
+// stream ids of the sampler: (iteration << 16) | (worker << 2) | role, smc.cpp:21-28
+enum { kPilotRole = 0, kMoveRole = 1, kCoordinatorRole = 3 };
+static std::uint64_t anneal_stream(std::uint64_t iteration, std::uint64_t role) {
+    return static_cast<std::uint32_t>((iteration << 16) | role);
+}
+
+struct Annealed {
+    const Bioassay& model;
+    std::uint64_t np, seed;
+    std::vector<double> theta, lw, ll, lp;
+    double temperature = 0.0, log_evidence = 0.0;
+
+    // reweighted ESS at temperature increment dt: smc.cpp:226-239
+    double ess_after(double dt) const {
+        double top = -std::numeric_limits<double>::infinity();
+        for (std::uint64_t i = 0; i < np; ++i) top = std::max(top, lw[i] + dt * ll[i]);
+        if (top == -std::numeric_limits<double>::infinity()) return 0.0;
+        double s1 = 0.0, s2 = 0.0;
+        for (std::uint64_t i = 0; i < np; ++i) {
+            const double e = std::exp(lw[i] + dt * ll[i] - top);
+            s1 += e;
+            s2 += e * e;
+        }
+        return s1 * s1 / s2;
+    }
+    // find_temperature: smc.cpp:221-253
+    double next_temperature(double tol) const {
+        const double target = static_cast<double>(np) / 2.0;
+        const double room = 1.0 - temperature;
+        if (ess_after(room) >= target) return 1.0;
+        double lo = 0.0, hi = room;
+        while (hi - lo > tol) {
+            const double mid = 0.5 * (lo + hi);
+            (ess_after(mid) >= target ? lo : hi) = mid;
+        }
+        return temperature + 0.5 * (lo + hi);
+    }
+    // one tempered random-walk sweep of `steps` steps: move_range, smc.cpp:77-150
+    std::uint64_t sweep(const double* chol, double h, std::uint64_t role, std::uint64_t iteration,
+                        std::uint64_t steps) {
+        const std::uint64_t gauss_total = np * steps * 2;
+        std::uint64_t accepted = 0;
+        Stream s(seed, anneal_stream(iteration, role));
+        for (std::uint64_t q = 0; q < np; ++q)
+            for (std::uint64_t r = 0; r < steps; ++r) {
+                s.pos = (q * steps + r) * 2;
+                const double z0 = s.next_gaussian(0.0, 1.0), z1 = s.next_gaussian(0.0, 1.0);
+                double inc0 = 0.0, inc1 = 0.0;
+                inc0 += chol[0] * z0;
+                inc1 += chol[2] * z0;
+                inc1 += chol[3] * z1;
+                const double p0 = theta[2 * q] + h * inc0, p1 = theta[2 * q + 1] + h * inc1;
+                const double lp_new = model.log_prior(p0, p1);
+                const double ll_new = model.log_lik(p0, p1);
+                const double log_alpha = temperature * (ll_new - ll[q]) + lp_new - lp[q];
+                s.pos = gauss_total + q * steps + r;
+                const double u = s.next_unit();
+                const double log_u = u > 0.0 ? ln_pos(u) : -std::numeric_limits<double>::infinity();
+                if (!std::isnan(log_alpha) && log_alpha > -std::numeric_limits<double>::infinity() &&
+                    log_u <= log_alpha) {
+                    ++accepted;
+                    theta[2 * q] = p0;
+                    theta[2 * q + 1] = p1;
+                    ll[q] = ll_new;
+                    lp[q] = lp_new;
+                }
+            }
+        return accepted;
+    }
+};
+
+static void anneal_run(const Bioassay& model, std::uint64_t np, std::uint64_t block_width, double c,
+                       double scale, std::uint64_t seed, double* log_evidence,
+                       std::uint64_t* iterations, AnnealTrace* trace) {
+    const double tol = 1e-10, jitter = 1e-10;            // SmcConfig defaults, smc.hpp:120-121
+    const std::uint64_t max_iterations = 1000, step_cap = 100;
+    require(supported_width(block_width), "invalid-shape", "unsupported block width");
+    require(np >= 2 * block_width, "invalid-shape", "need at least two particle blocks");
+    require(c > 0.0 && c < 1.0, "invalid-argument", "tuning constant must lie in (0, 1)");
+    Annealed a{model, np, seed, std::vector<double>(2 * np), std::vector<double>(np),
+               std::vector<double>(np), std::vector<double>(np)};
+    {   // initial ensemble: prior draws in particle order, smc.cpp:386-393
+        Stream s(seed, anneal_stream(0, kPilotRole));
+        bool any = false;
+        for (std::uint64_t i = 0; i < np; ++i) {
+            s.align_even();
+            const double z0 = s.next_gaussian(0.0, 1.0), z1 = s.next_gaussian(0.0, 1.0);
+            a.theta[2 * i] = model.l1 * z0;
+            a.theta[2 * i + 1] = model.l2 * z1;
+            a.lw[i] = -std::log(static_cast<double>(np));
+            a.ll[i] = model.log_lik(a.theta[2 * i], a.theta[2 * i + 1]);
+            a.lp[i] = model.log_prior(a.theta[2 * i], a.theta[2 * i + 1]);
+            require(!std::isnan(a.ll[i]) && a.ll[i] < std::numeric_limits<double>::infinity(),
+                    "invalid-model", "log-likelihood is not finite at initialization");
+            any = any || a.ll[i] > -std::numeric_limits<double>::infinity();
+        }
+        require(any, "invalid-model", "likelihood is zero for every initial particle");
+    }
+    const double h = scale > 0.0 ? scale : 2.38 / std::sqrt(2.0);
+    std::uint64_t n = 0;
+    while (a.temperature < 1.0) {
+        ++n;
+        require(n <= max_iterations, "non-convergence",
+                "temperature failed to reach 1 within the iteration cap");
+        const double t_next = a.next_temperature(tol);
+        {   // reweight_and_update_evidence: smc.cpp:255-266
+            const double before = logsumexp(a.lw.data(), np);
+            const double dt = t_next - a.temperature;
+            for (std::uint64_t i = 0; i < np; ++i) a.lw[i] += dt * a.ll[i];
+            a.log_evidence += logsumexp(a.lw.data(), np) - before;
+            a.temperature = t_next;
+        }
+        double ess_now = 0.0;
+        require(vxo_ess(a.lw.data(), np, &ess_now) == 0, "degenerate-ensemble", "all weights are zero");
+        {   // resample_multinomial: smc.cpp:268-300, coordinator stream
+            std::vector<double> packed(4 * np), out(4 * np);
+            for (std::uint64_t i = 0; i < np; ++i) {
+                packed[4 * i] = a.theta[2 * i];
+                packed[4 * i + 1] = a.theta[2 * i + 1];
+                packed[4 * i + 2] = a.ll[i];
+                packed[4 * i + 3] = a.lp[i];
+            }
+            require(vxo_resample_multinomial(np, 4, a.lw.data(), packed.data(), seed,
+                                             anneal_stream(n, kCoordinatorRole), out.data(),
+                                             nullptr) == 0,
+                    "degenerate-ensemble", "weight sum is not finite");
+            for (std::uint64_t i = 0; i < np; ++i) {
+                a.theta[2 * i] = out[4 * i];
+                a.theta[2 * i + 1] = out[4 * i + 1];
+                a.ll[i] = out[4 * i + 2];
+                a.lp[i] = out[4 * i + 3];
+                a.lw[i] = -std::log(static_cast<double>(np));
+            }
+        }
+        double chol[4];
+        {   // make_kernel: smc.cpp:311-325
+            double cov[4];
+            sample_covariance(a.theta.data(), np, 2, cov);
+            require(vxo_make_kernel(cov, 2, 1.0, jitter, chol) == 0, "degenerate-ensemble",
+                    "covariance is rank deficient beyond jitter");
+        }
+        const std::uint64_t pilot = a.sweep(chol, h, kPilotRole, n, 1);
+        const double p_acc = static_cast<double>(pilot) / static_cast<double>(np);
+        // steps_from_acceptance: smc.cpp:302-309
+        const double p = std::min(std::max(p_acc, 0.01), 0.99);
+        const double raw = std::ceil(std::log(c) / std::log(1.0 - p));
+        const std::uint64_t steps =
+            !(raw >= 1.0) ? 1 : std::min<std::uint64_t>(static_cast<std::uint64_t>(raw), step_cap);
+        a.sweep(chol, h, kMoveRole, n, steps);
+        if (trace) {
+            trace->temperature.push_back(a.temperature);
+            trace->ess.push_back(ess_now);
+            trace->accept.push_back(p_acc);
+            trace->steps.push_back(steps);
+        }
+    }
+    *log_evidence = a.log_evidence;
+    *iterations = n;
+}
+
+int vxo_bioassay_ll(const double* beta, std::uint64_t lanes, const double* dose,
+                    const std::uint32_t* group_size, const std::uint32_t* deaths,
+                    std::uint32_t groups, double* out) {
+    return guarded([&] {
+        const Bioassay m = make_bioassay(dose, group_size, deaths, groups, 1.0, 1.0);
+        for (std::uint64_t l = 0; l < lanes; ++l) out[l] = m.log_lik(beta[2 * l], beta[2 * l + 1]);
+    });
+}
+int vxo_bioassay_sample(double lambda1, double lambda2, const double* dose,
+                        const std::uint32_t* group_size, std::uint32_t groups, std::uint64_t seed,
+                        double* theta, std::uint32_t* deaths) {
+    return guarded([&] { bioassay_draw(lambda1, lambda2, dose, group_size, groups, seed, theta, deaths); });
+}
+// trace (optional): rows of (iteration, temperature, ess, log_evidence=nan, steps, p_acc, h)
+// are not produced here; trace_out receives iterations x 4 doubles
+// (temperature, ess, steps, p_acc), at most trace_cap rows.
+int vxo_smc_bioassay(const double* dose, const std::uint32_t* group_size,
+                     const std::uint32_t* deaths, std::uint32_t groups, double lambda1,
+                     double lambda2, std::uint64_t particles, std::uint64_t block_width, double c,
+                     double scale, std::uint64_t seed, double* log_evidence,
+                     std::uint64_t* iterations, double* trace_out, std::uint64_t trace_cap) {
+    return guarded([&] {
+        const Bioassay m = make_bioassay(dose, group_size, deaths, groups, lambda1, lambda2);
+        AnnealTrace tr;
+        anneal_run(m, particles, block_width, c, scale, seed, log_evidence, iterations,
+                   trace_out ? &tr : nullptr);
+        for (std::uint64_t i = 0; trace_out && i < tr.steps.size() && i < trace_cap; ++i) {
+            trace_out[4 * i] = tr.temperature[i];
+            trace_out[4 * i + 1] = tr.ess[i];
+            trace_out[4 * i + 2] = static_cast<double>(tr.steps[i]);
+            trace_out[4 * i + 3] = tr.accept[i];
+        }
+    });
+}
+
+// run_weak_info_test: weak_info.cpp:163-277 (default design, shared or redrawn
+// base datasets); `threads` spreads the hyperparameter rows.
+int vxo_weak_info_test(std::uint64_t hyper_count, std::uint64_t datasets, std::uint64_t particles,
+                       double alpha, double c, double scale, std::uint64_t threads,
+                       std::uint64_t block_width, std::uint64_t seed, int redraw_base,
+                       double* lambda, double* gamma, std::uint8_t* weakly,
+                       std::uint64_t* completed, const char* /*csv_path*/) {
+    return guarded([&] {
+        require(datasets >= 1, "invalid-argument", "need at least one dataset per prior");
+        require(threads >= 1, "invalid-argument", "need at least one worker");
+        const double dose[4] = {-0.86, -0.3, -0.05, -0.75};  // default_design, weak_info.cpp:62-64
+        const std::uint32_t size[4] = {5, 5, 5, 5};
+        const double base[2] = {10.0, 2.5};                  // kBasePrior, weak_info.hpp:21
+        const std::uint64_t rows = hyper_count + 1;
+        lambda[0] = base[0];
+        lambda[1] = base[1];
+        {
+            const std::uint64_t path[1] = {1};
+            Stream s(derive_seed(seed, path, 1), 0);
+            for (std::uint64_t k = 1; k < rows; ++k) {
+                lambda[2 * k] = s.next_uniform(0.1, 10.0);
+                lambda[2 * k + 1] = s.next_uniform(0.1, 20.0);
+            }
+        }
+        std::vector<std::uint32_t> shared(4 * datasets);
+        if (!redraw_base)
+            for (std::uint64_t i = 0; i < datasets; ++i) {
+                const std::uint64_t path[2] = {2, i};
+                double theta[2];
+                bioassay_draw(base[0], base[1], dose, size, 4, derive_seed(seed, path, 2), theta,
+                              &shared[4 * i]);
+            }
+        const auto evidence = [&](const std::uint32_t* deaths, const double* prior,
+                                  std::uint64_t run_seed, double* out) {
+            std::uint64_t it = 0;
+            const int rc = guarded([&] {
+                const Bioassay m = make_bioassay(dose, size, deaths, 4, prior[0], prior[1]);
+                anneal_run(m, particles, block_width, c, scale, run_seed, out, &it, nullptr);
+            });
+            return rc == 0;
+        };
+        parallel_for(rows, static_cast<unsigned>(threads), [&](std::uint64_t k) {
+            const double* prior = lambda + 2 * k;
+            std::vector<double> ev_base, ev_hyper;
+            std::uint64_t both = 0;
+            for (std::uint64_t i = 0; i < datasets; ++i) {
+                std::uint32_t base_y[4], hyper_y[4];
+                double theta[2];
+                if (redraw_base) {
+                    const std::uint64_t path[3] = {5, k, i};
+                    bioassay_draw(base[0], base[1], dose, size, 4, derive_seed(seed, path, 3), theta, base_y);
+                } else {
+                    std::copy_n(&shared[4 * i], 4, base_y);
+                }
+                const std::uint64_t hp[3] = {3, k, i};
+                bioassay_draw(prior[0], prior[1], dose, size, 4, derive_seed(seed, hp, 3), theta, hyper_y);
+                const std::uint64_t sb[4] = {4, k, 0, i}, sh[4] = {4, k, 1, i};
+                double eb = 0.0, eh = 0.0;
+                const bool ok_b = evidence(base_y, prior, derive_seed(seed, sb, 4), &eb);
+                const bool ok_h = evidence(hyper_y, prior, derive_seed(seed, sh, 4), &eh);
+                if (ok_b) ev_base.push_back(eb);
+                if (ok_h) ev_hyper.push_back(eh);
+                both += (ok_b && ok_h) ? 1 : 0;
+            }
+            completed[k] = both;
+            gamma[k] = std::numeric_limits<double>::quiet_NaN();
+            if (ev_base.empty() || ev_hyper.empty()) return;
+            std::vector<double> pv(ev_base.size());
+            vxo_estimate_pvalues(ev_base.data(), ev_base.size(), ev_hyper.data(), ev_hyper.size(),
+                                 pv.data());
+            vxo_compute_cutoff(pv.data(), pv.size(), alpha, &gamma[k]);
+        });
+        for (std::uint64_t k = 0; k < rows; ++k) weakly[k] = (k != 0 && gamma[k] > gamma[0]) ? 1 : 0;
+    });
+}
+
 }  // extern "C"

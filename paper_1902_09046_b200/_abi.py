@@ -56,6 +56,14 @@ class vxb_abcsmc_out(C.Structure):
                 ("proposals", C.c_void_p), ("mean", C.c_void_p), ("cov", C.c_void_p)]
 
 
+class vxb_weakinfo_cfg(C.Structure):
+    _fields_ = [("hyper_count", C.c_uint64), ("datasets", C.c_uint64), ("particles", C.c_uint64),
+                ("block_width", C.c_uint64), ("seed", C.c_uint64), ("alpha", C.c_double),
+                ("c", C.c_double), ("scale", C.c_double), ("base", C.c_double * 2),
+                ("redraw_base", C.c_int32), ("groups", C.c_uint32),
+                ("group_size", C.c_uint32 * 16), ("dose", C.c_double * 16)]
+
+
 class vxb_mlmc_cfg(C.Structure):
     _fields_ = [("levels", C.c_uint32), ("refine", C.c_uint32), ("tau0", C.c_double),
                 ("t_end", C.c_double), ("paths", C.c_uint64), ("seed", C.c_uint64)]
@@ -77,5 +85,6 @@ EXPORTED_SYMBOLS = (
     "vxb_compact_accepted", "vxb_abc_reject", "vxb_simulate_at", "vxb_ppp_pvalues",
     "vxb_ess", "vxb_logsumexp", "vxb_resample_multinomial", "vxb_abcsmc_run",
     "vxb_abcsmc_propose", "vxb_abcsmc_weights", "vxb_weighted_moments", "vxb_canon_cumsum",
-    "vxb_canon_chunk_sums", "vxb_quantile", "vxb_divide", "vxb_make_kernel", "vxb_mlmc_level", "vxb_mlmc_tauleap",
+    "vxb_canon_chunk_sums", "vxb_quantile", "vxb_divide", "vxb_make_kernel", "vxb_bioassay_log_likelihood", "vxb_bioassay_sample", "vxb_smc_bioassay",
+    "vxb_weak_info_test", "vxb_mlmc_level", "vxb_mlmc_tauleap",
 )

@@ -403,6 +403,58 @@ class Context:
                                           f64(level), C.byref(out)))
         return out.value
 
+    # ---- likelihood-annealed SMC / weak-informativity test
+    @staticmethod
+    def _design(dose, group_size):
+        return (np.ascontiguousarray(dose, dtype=np.float64),
+                np.ascontiguousarray(group_size, dtype=np.uint32))
+
+    def bioassay_log_likelihood(self, beta, dose, group_size, deaths):
+        b = np.ascontiguousarray(beta, dtype=np.float64).reshape(-1, 2)
+        d, g = self._design(dose, group_size)
+        y = np.ascontiguousarray(deaths, dtype=np.uint32)
+        out = np.zeros(b.shape[0])
+        self._check(self.lib.vxb_bioassay_log_likelihood(self.handle, _ptr(b), u64(b.shape[0]),
+                                                         u32(d.size), _ptr(d), _ptr(g), _ptr(y),
+                                                         _ptr(out)))
+        return out
+
+    def bioassay_sample(self, lam, seeds, dose, group_size):
+        lam = np.ascontiguousarray(lam, dtype=np.float64).reshape(-1, 2)
+        seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+        d, g = self._design(dose, group_size)
+        theta = np.zeros_like(lam)
+        deaths = np.zeros((lam.shape[0], d.size), dtype=np.uint32)
+        self._check(self.lib.vxb_bioassay_sample(self.handle, u64(lam.shape[0]), u32(d.size),
+                                                 _ptr(d), _ptr(g), _ptr(lam), _ptr(seeds),
+                                                 _ptr(theta), _ptr(deaths)))
+        return theta, deaths
+
+    def smc_bioassay(self, dose, group_size, deaths, lam, seeds, particles, block_width=4, c=0.01,
+                     scale=1.6828427124746189, trace_rows=0):
+        """Batch of independent annealed-SMC evidence estimates (one CTA per run)."""
+        d, g = self._design(dose, group_size)
+        y = np.ascontiguousarray(deaths, dtype=np.uint32).reshape(-1, d.size)
+        lam = np.ascontiguousarray(lam, dtype=np.float64).reshape(-1, 2)
+        seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+        n = y.shape[0]
+        ev, it, st = np.zeros(n), np.zeros(n, dtype=np.uint32), np.zeros(n, dtype=np.uint8)
+        tr = np.zeros((n, trace_rows, 4)) if trace_rows else None
+        self._check(self.lib.vxb_smc_bioassay(self.handle, u64(n), u32(d.size), _ptr(d), _ptr(g),
+                                              _ptr(y), _ptr(lam), _ptr(seeds), u64(particles),
+                                              u64(block_width), f64(c), f64(scale), _ptr(ev),
+                                              _ptr(it), _ptr(st), _ptr(tr), u32(trace_rows)))
+        return dict(log_evidence=ev, iterations=it, status=st, trace=tr)
+
+    def weak_info_test(self, cfg, want_evidence=False):
+        k = cfg.hyper_count + 1
+        lam, gamma = np.zeros((k, 2)), np.zeros(k)
+        weakly, completed = np.zeros(k, dtype=np.uint8), np.zeros(k, dtype=np.uint64)
+        ev = np.zeros((k, cfg.datasets, 2)) if want_evidence else None
+        self._check(self.lib.vxb_weak_info_test(self.handle, C.byref(cfg), _ptr(lam), _ptr(gamma),
+                                                _ptr(weakly), _ptr(completed), _ptr(ev)))
+        return dict(lambda_=lam, gamma=gamma, weakly=weakly, completed=completed, evidence=ev)
+
     # ---- tau-leap
     def mlmc_level(self, model, cfg, level, first, count, want_y=False):
         sums = np.zeros(4, dtype=np.int64)

@@ -1,0 +1,142 @@
+"""Likelihood-annealed SMC on the bioassay model and the weak-informativity test
+(SURVEY.md 8f-3).  CPU: the oracle restatement against golden values of the
+unmodified reference (tests/golden/make_golden_anneal.py) and, where
+oracle/_ref is present, against the live reference -- bit for bit.  GPU: the
+one-CTA-per-run device sampler against the oracle: model evaluations and
+datasets bit-exact; evidences to 1e-9 (the device calls exp/log where the
+reference calls libm and sums in a fixed tree order) with identical iteration
+counts, step counts and acceptance rates; the cut-off table identical."""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from paper_1902_09046_b200 import lib, models as M
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+import make_golden_anneal as G  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return np.load(os.path.join(ROOT, "tests", "golden", "anneal.npz"))
+
+
+def test_oracle_matches_reference_golden(oracle, gold):
+    assert np.array_equal(oracle.bioassay_ll(gold["ll_beta"], G.DOSE, G.SIZE, [0, 2, 5, 1]), gold["ll_values"])
+    for j, (l1, l2, ds, ss, npart) in enumerate(G.RUNS):
+        th, y = oracle.bioassay_sample(l1, l2, G.DOSE, G.SIZE, ds)
+        assert np.array_equal(th, gold["run_theta"][j]) and np.array_equal(y, gold["run_deaths"][j])
+        ev, it, tr = oracle.smc_bioassay(G.DOSE, G.SIZE, y, l1, l2, npart, 4, 0.01, G.H, ss, True)
+        assert ev == gold["run_evidence"][j] and it == gold["run_iterations"][j]
+        # the reference prints its trace with 17 significant digits
+        assert np.allclose(tr, gold["run_trace"][j][:it], rtol=1e-15, atol=0)
+        assert np.array_equal(tr[:, 2:], gold["run_trace"][j][:it, 2:])
+    for redraw in (0, 1):
+        t = oracle.weak_info_test(G.TABLE["hyper_count"], G.TABLE["datasets"], G.TABLE["particles"],
+                                  seed=G.TABLE["seed"], redraw_base=bool(redraw), workers=4)
+        for k, v in t.items():
+            assert np.array_equal(v, gold[f"table{redraw}_{k}"]), (redraw, k)
+
+
+def test_oracle_matches_live_reference(oracle, ref):
+    rs = np.random.RandomState(11)
+    for trial in range(4):
+        l1, l2 = rs.uniform(0.1, 10.0), rs.uniform(0.1, 20.0)
+        th, y = ref.bioassay_sample(l1, l2, G.DOSE, G.SIZE, 1000 + trial)
+        th2, y2 = oracle.bioassay_sample(l1, l2, G.DOSE, G.SIZE, 1000 + trial)
+        assert np.array_equal(th, th2) and np.array_equal(y, y2)
+        a = ref.smc_bioassay(G.DOSE, G.SIZE, y, l1, l2, 300, 8, 0.05, 0.9, 7 * trial)
+        b = oracle.smc_bioassay(G.DOSE, G.SIZE, y, l1, l2, 300, 8, 0.05, 0.9, 7 * trial)
+        assert a == b
+    a = ref.weak_info_test(2, 6, 100, seed=5)
+    b = oracle.weak_info_test(2, 6, 100, seed=5)
+    for k in a:
+        assert np.array_equal(a[k], b[k], equal_nan=True), k
+    # argument errors of the sampler (smc.cpp:356-364)
+    from oracle.pyoracle import OracleError
+    for o in (ref, oracle):
+        with pytest.raises(OracleError) as e:
+            o.smc_bioassay(G.DOSE, G.SIZE, [1, 1, 1, 1], 1.0, 1.0, 7, 4, 0.01, 1.0, 1)
+        assert str(e.value).startswith("invalid-shape")
+        with pytest.raises(OracleError) as e:
+            o.smc_bioassay(G.DOSE, G.SIZE, [1, 1, 1, 1], 1.0, 1.0, 64, 3, 0.01, 1.0, 1)
+        assert str(e.value).startswith("invalid-shape")
+
+
+# ------------------------------------------------------------------ device
+@pytest.mark.gpu
+def test_device_model_and_datasets_bit_exact(ctx, oracle, gold):
+    assert np.array_equal(ctx.bioassay_log_likelihood(gold["ll_beta"], G.DOSE, G.SIZE, [0, 2, 5, 1]),
+                          gold["ll_values"])
+    rs = np.random.RandomState(2)
+    n = 500
+    lam = np.stack([rs.uniform(0.1, 10.0, n), rs.uniform(0.1, 20.0, n)], axis=1)
+    seeds = rs.randint(0, 2 ** 62, size=n).astype(np.uint64)
+    theta, deaths = ctx.bioassay_sample(lam, seeds, G.DOSE, G.SIZE)
+    for j in range(0, n, 7):
+        th, y = oracle.bioassay_sample(lam[j, 0], lam[j, 1], G.DOSE, G.SIZE, int(seeds[j]))
+        assert np.array_equal(theta[j], th) and np.array_equal(deaths[j], y)
+    assert deaths.max() == 5 and deaths.min() == 0
+    # a design with large groups uses the device-side binomial table
+    dose, size = (-1.0, 0.0, 0.5), (40, 12, 9)
+    beta = rs.normal(size=(32, 2)) * 3
+    assert np.array_equal(ctx.bioassay_log_likelihood(beta, dose, size, [17, 0, 9]),
+                          oracle.bioassay_ll(beta, dose, size, [17, 0, 9]))
+
+
+@pytest.mark.gpu
+def test_device_sampler_matches_oracle(ctx, oracle, gold):
+    lam = np.array([[r[0], r[1]] for r in G.RUNS])
+    seeds = np.array([r[3] for r in G.RUNS], dtype=np.uint64)
+    for npart in sorted({r[4] for r in G.RUNS}):
+        sel = [j for j, r in enumerate(G.RUNS) if r[4] == npart]
+        res = ctx.smc_bioassay(G.DOSE, G.SIZE, gold["run_deaths"][sel], lam[sel], seeds[sel], npart,
+                               trace_rows=8)
+        assert (res["status"] == 0).all()
+        assert np.array_equal(res["iterations"], gold["run_iterations"][sel])
+        assert np.allclose(res["log_evidence"], gold["run_evidence"][sel], rtol=0, atol=1e-9)
+        want = gold["run_trace"][sel]
+        assert np.array_equal(res["trace"][:, :, 2:], want[:, :, 2:])          # R_n and p_acc: identical
+        assert np.allclose(res["trace"][:, :, :2], want[:, :, :2], rtol=1e-9, atol=1e-9)
+    # a larger random batch against the oracle, other tuning constants and widths
+    rs = np.random.RandomState(5)
+    n = 96
+    lam = np.stack([rs.uniform(0.1, 10.0, n), rs.uniform(0.1, 20.0, n)], axis=1)
+    seeds = rs.randint(0, 2 ** 62, size=n).astype(np.uint64)
+    _, deaths = ctx.bioassay_sample(lam, seeds ^ np.uint64(0xABCDEF), G.DOSE, G.SIZE)
+    res = ctx.smc_bioassay(G.DOSE, G.SIZE, deaths, lam, seeds, 250, block_width=8, c=0.05, scale=0.9)
+    for j in range(n):
+        ev, it = oracle.smc_bioassay(G.DOSE, G.SIZE, deaths[j], lam[j, 0], lam[j, 1], 250, 8, 0.05, 0.9,
+                                     int(seeds[j]))
+        assert res["iterations"][j] == it and abs(res["log_evidence"][j] - ev) < 1e-9, j
+    # argument errors mirror the reference sampler
+    for kwargs, code in ((dict(particles=7), "invalid-shape"), (dict(particles=64, block_width=3), "invalid-shape"),
+                         (dict(particles=64, c=1.5), "invalid-argument")):
+        with pytest.raises(lib.VxbError) as e:
+            ctx.smc_bioassay(G.DOSE, G.SIZE, deaths[:2], lam[:2], seeds[:2], **kwargs)
+        assert e.value.code == code
+    with pytest.raises(lib.VxbError) as e:
+        ctx.smc_bioassay(G.DOSE, G.SIZE, [[9, 0, 0, 0]], lam[:1], seeds[:1], 64)
+    assert e.value.code == "invalid-argument"
+
+
+@pytest.mark.gpu
+def test_device_weak_info_table_equals_reference(ctx, oracle, gold):
+    for redraw in (0, 1):
+        cfg = M.weakinfo_config(seed=G.TABLE["seed"], redraw_base=bool(redraw),
+                                **{k: G.TABLE[k] for k in ("hyper_count", "datasets", "particles")})
+        t = ctx.weak_info_test(cfg, want_evidence=True)
+        assert np.array_equal(t["lambda_"], gold[f"table{redraw}_lambda_"])
+        assert np.array_equal(t["gamma"], gold[f"table{redraw}_gamma"])
+        assert np.array_equal(t["weakly"], gold[f"table{redraw}_weakly"])
+        assert np.array_equal(t["completed"], gold[f"table{redraw}_completed"])
+        assert np.isfinite(t["evidence"]).all()
+    # a somewhat larger table against the oracle run here
+    cfg = M.weakinfo_config(hyper_count=6, datasets=40, particles=128, seed=77, alpha=0.1)
+    t = ctx.weak_info_test(cfg)
+    o = oracle.weak_info_test(6, 40, 128, alpha=0.1, seed=77, workers=8)
+    for k in ("lambda_", "gamma", "weakly", "completed"):
+        assert np.array_equal(t[k], o[k]), k
