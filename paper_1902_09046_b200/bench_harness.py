@@ -9,8 +9,8 @@ experiment body runs on the GPU through the C ABI: `threads` and `block_width`
 keep their meaning as the (P, V) of the reference keying (VXB_KEY_WORKER), which
 makes the produced samples identical to the CPU run of the same cell.
 
-Only the experiments on the GPU path are runnable (toggle-abc); the names of the
-others are kept so that reference files parse.
+Only the experiments on the GPU path are runnable (toggle-abc, weakinfo); the names
+of the others are kept so that reference files parse.
 """
 import math
 import time
@@ -69,6 +69,9 @@ class ExperimentSizes:          # bench.hpp:32-43
     samples: int = 64
     cells: int = 256
     steps: int = 100
+    particles: int = 200  # SMC N_p
+    hypers: int = 2       # weak-info K
+    datasets: int = 8     # weak-info N
 
 
 @dataclass
@@ -115,7 +118,11 @@ def toggle_observed_summaries(ctx, steps, cells, seed, block_width):
 
 def run_experiment_once(ctx, experiment, sizes, threads, block_width, seed):
     """bench.cpp:94-137, the toggle-abc body on the GPU."""
-    if experiment_from_string(experiment) != "toggle-abc":
+    if experiment_from_string(experiment) == "weakinfo":   # bench.cpp:113-123
+        cfg = M.weakinfo_config(hyper_count=sizes.hypers, datasets=sizes.datasets,
+                                particles=sizes.particles, block_width=block_width, seed=seed)
+        return ctx.weak_info_test(cfg)
+    if experiment != "toggle-abc":
         raise VxbError("unsupported-model: experiment " + experiment + " has no device path")
     observed = toggle_observed_summaries(ctx, sizes.steps, sizes.cells, seed, block_width)
     key = M.keying(seed, A.VXB_KEY_WORKER, threads, block_width)

@@ -9,7 +9,7 @@
 // (P, V) of the reference keying, so a cell simulates the very samples the CPU
 // run of that cell simulates.
 // What changes: the body runs on the GPU; only the experiments with a device
-// path can run (toggle-abc) -- the others raise unsupported-model.
+// path can run (toggle-abc, weakinfo) -- the others raise unsupported-model.
 #pragma once
 
 #include <chrono>
@@ -27,6 +27,7 @@
 
 #include "abc.hpp"
 #include "toggle_switch.hpp"
+#include "weak_info.hpp"
 
 namespace vexbayes::bench {
 
@@ -78,6 +79,9 @@ struct ExperimentSizes {
     std::size_t samples = 64;  // prior predictive draws
     std::size_t cells = 256;   // toggle C
     std::size_t steps = 100;   // toggle T
+    std::size_t particles = 200;  // SMC N_p
+    std::size_t hypers = 2;       // weak-info K
+    std::size_t datasets = 8;     // weak-info N
 };
 
 struct BenchConfig {
@@ -122,6 +126,17 @@ inline std::vector<double> toggle_observed_summaries(std::size_t steps, std::siz
 
 inline void run_experiment_once(Experiment experiment, const ExperimentSizes& sizes,
                                 std::size_t threads, std::size_t block_width, std::uint64_t seed) {
+    if (experiment == Experiment::weakinfo) {  // bench.cpp:113-123
+        weakinfo::WeakInfoConfig config;
+        config.hyper_count = sizes.hypers;
+        config.datasets = sizes.datasets;
+        config.particles = sizes.particles;
+        config.workers = threads;
+        config.block_width = block_width;
+        config.seed = seed;
+        weakinfo::run_weak_info_test(config);
+        return;
+    }
     require(experiment == Experiment::toggle_abc, "unsupported-model",
             "experiment " + to_string(experiment) + " has no device path");
     const auto observed = toggle_observed_summaries(sizes.steps, sizes.cells, seed, block_width);

@@ -1,0 +1,32 @@
+"""The paper's case study 1 at its published size: weak-informativity test with
+K = 400 hyperparameters, N = 400 datasets, N_p = 500 particles:
+2 (K+1) N = 320 800 annealed-SMC runs.  Published best: 90 s on 16 AVX-512 cores
+(PAPER.md:742-746)."""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np
+from paper_1902_09046_b200 import lib, models as M
+
+ctx = lib.Context(0)
+k = int(sys.argv[1]) if len(sys.argv) > 1 else 400
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 400
+cfg = M.weakinfo_config(hyper_count=k, datasets=n, particles=500, seed=1337)
+ctx.weak_info_test(M.weakinfo_config(hyper_count=4, datasets=16, particles=500, seed=1))  # warm-up
+times = []
+for rep in range(3):
+    t0 = time.perf_counter()
+    t = ctx.weak_info_test(cfg, want_evidence=True)
+    times.append(time.perf_counter() - t0)
+runs = 2 * (k + 1) * n
+ev = t["evidence"]
+out = {"hyper_count": k, "datasets": n, "particles": 500, "sampler_runs": runs,
+       "seconds": times, "runs_per_s": runs / min(times), "published_best_s": 90.0,
+       "weakly_informative": int(t["weakly"].sum()), "gamma0": float(t["gamma"][0]),
+       "completed_min": int(t["completed"].min()), "evidence_mean": float(np.nanmean(ev)),
+       "failed_runs": int(np.isnan(ev).sum())}
+print(json.dumps(out))

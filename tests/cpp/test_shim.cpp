@@ -51,6 +51,27 @@ static int csv_mode(const char* bench_golden, const char* out_dir) {
     const auto observed = logistic::simulate_at(ok, std::vector<double>{0.5, 100.0, 0.05}, 5, 0, 0);
     abc::write_csv(abc::run_prior_predictive(bad, 24, 3, 2, 21, observed), dir + "/set.csv");
 
+    // the weak-informativity test through the reference's own interface
+    weakinfo::WeakInfoConfig wcfg;
+    wcfg.hyper_count = 3;
+    wcfg.datasets = 12;
+    wcfg.particles = 200;
+    wcfg.seed = 1337;
+    {
+        std::ofstream wout(dir + "/weakinfo_table.csv");
+        weakinfo::write_csv(weakinfo::run_weak_info_test(wcfg), wout);
+    }
+    auto design = weakinfo::default_design();
+    const auto draw = weakinfo::sample_prior_predictive({10.0, 2.5}, design, 1234);
+    std::size_t its = 0;
+    const double ev = weakinfo::log_evidence(draw.data, {10.0, 2.5}, 500, 4, 0.01, 1.6828427124746189, 3702, &its);
+    std::printf("evidence %.17g %zu %u%u%u%u\n", ev, its, draw.data.deaths[0], draw.data.deaths[1],
+                draw.data.deaths[2], draw.data.deaths[3]);
+    {
+        bench::ExperimentSizes ws;
+        bench::run_experiment_once(bench::Experiment::weakinfo, ws, 2, 4, 1337);
+    }
+
     bench::BenchConfig cfg;
     cfg.threads = {1, 3};
     cfg.block_widths = {1, 4};

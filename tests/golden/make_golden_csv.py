@@ -6,6 +6,7 @@
                      run_prior_predictive returns for the logistic hooks with a
                      prior box that makes some rows fail (NaN rho, failed = 1);
                      (n, workers, block_width, seed) = (24, 3, 2, 21).
+* weakinfo_table.csv weakinfo::write_csv of the reference's run_weak_info_test.
 * bench_records.csv  bench::write_csv (bench.cpp:215-230) of the synthetic
                      records below (a failed replicate included).
 """
@@ -49,6 +50,8 @@ def main():
     r.logistic_abc_csv(set_model(), SET_CASE["n"], SET_CASE["workers"], SET_CASE["block_width"],
                        SET_CASE["seed"], obs, os.path.join(HERE, "logistic_set.csv"))
     r.bench_csv(bench_records(), os.path.join(HERE, "bench_records.csv"))
+    # weakinfo::write_csv (weak_info.cpp:279-293) of run_weak_info_test(K=3, N=12, N_p=200, seed 1337)
+    r.weak_info_test(3, 12, 200, seed=1337, csv_path=os.path.join(HERE, "weakinfo_table.csv"))
     text = open(os.path.join(HERE, "logistic_set.csv")).read()
     assert ",1\n" in text and ",0\n" in text, "want failed and good rows in the fixture"
     print("wrote logistic_set.csv", len(text), "bytes; bench_records.csv")

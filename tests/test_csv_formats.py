@@ -103,3 +103,16 @@ def test_gpu_bench_harness_runs_the_toggle_experiment(ctx, golden):
     with pytest.raises(lib.VxbError) as e:
         B.run_experiment_once(ctx, "bege", cfg.sizes, 1, 1, 1)
     assert e.value.code == "unsupported-model"
+
+
+@pytest.mark.gpu
+def test_gpu_weak_info_csv_equals_reference_file(ctx, tmp_path):
+    from paper_1902_09046_b200 import weak_info as W
+    table = W.run_weak_info_test(ctx, W.WeakInfoConfig(hyper_count=3, datasets=12, particles=200, seed=1337))
+    out = io.StringIO()
+    W.write_csv(table, out)
+    assert out.getvalue() == golden_text("weakinfo_table.csv")
+    assert [r.weakly_informative for r in table.rows][0] is False
+    recs = B.run_benchmark(ctx, B.BenchConfig(experiment="weakinfo", threads=[1], block_widths=[4], replicates=1))
+    assert len(recs) == 1 and not recs[0].failed
+    assert np.array_equal(W.estimate_pvalues([2.0, 5.0], [1.0, 3.0, 4.0, 6.0]), [0.25, 0.75])

@@ -89,6 +89,11 @@ def test_cpp_shim_reference_format_outputs(tmp_path, golden):
     assert read(tmp_path / "bench_rewritten.csv") == want.getvalue()
     cut = text.index(B.SUMMARY_HEADER)
     assert read(tmp_path / "bench_rewritten.csv")[:cut] == text[:cut]   # records section: reference bytes
+    assert read(tmp_path / "weakinfo_table.csv") == read(os.path.join(gold, "weakinfo_table.csv"))
+    anneal = np.load(os.path.join(gold, "anneal.npz"))
+    assert abs(float(r["evidence"][0]) - anneal["run_evidence"][0]) < 1e-9
+    assert int(r["evidence"][1]) == anneal["run_iterations"][0]
+    assert r["evidence"][2] == "".join(str(v) for v in anneal["run_deaths"][0])
     sweep = B.parse_csv(read(tmp_path / "sweep.csv"))
     assert [(x.block_width, x.threads, x.replicate) for x in sweep] == \
         [(v, p, k) for v in (1, 4) for p in (1, 3) for k in (0, 1)]
