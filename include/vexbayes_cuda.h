@@ -42,7 +42,7 @@ typedef struct vxb_ctx vxb_ctx;
 
 /* ------------------------------------------------------------------ enums */
 enum { VXB_MODEL_LOGISTIC_SDE = 1, VXB_MODEL_NORMAL_MEAN = 2, VXB_MODEL_MM_TAULEAP = 3,
-       VXB_MODEL_TOGGLE = 4 };
+       VXB_MODEL_TOGGLE = 4, VXB_MODEL_TB = 5 };
 enum { VXB_F64 = 0, VXB_F32 = 1 };
 /* VXB_RNG_REF      : Philox2x64-10 + Box-Muller through the reference's own
  *                    polynomials; every variate bit-identical to RngStream
@@ -78,6 +78,13 @@ enum { VXB_KEY_PARTICLE = 0, VXB_KEY_WORKER = 1 };
  *   steps = n (data per dataset).
  * VXB_MODEL_MM_TAULEAP    S+E->C (k1), C->S+E (k2), C->E+P (k3)
  *   consts[0..3] = initial (S,E,C,P), consts[4..6] = (k1,k2,k3).
+ * VXB_MODEL_TB            the multi-genotype TB transmission model (tb_model.hpp),
+ *   exact Gillespie; theta = (alpha, delta, tau) with the prior of
+ *   tb::sample_prior, dim = 3, summaries (G, H), summary_dim = 2;
+ *   consts[0] = initial cases, consts[1] = time horizon, consts[2] = case target
+ *   (<= 60000 on the device), consts[3] = attempts of vxb_simulate_at (> 1: the
+ *   retry-while-extinct loop of bench::tb_observed_summaries, bench.cpp:79-92).
+ *   VXB_KEY_PARTICLE only (a row consumes a data-dependent number of variates).
  */
 typedef struct vxb_model {
     int32_t model;      /* VXB_MODEL_*            */

@@ -97,8 +97,35 @@ class _Base:
                    _ptr(completed), C.c_char_p(os.fsencode(csv_path)) if csv_path else None)
         return dict(lambda_=lam, gamma=gamma, weakly=weakly, completed=completed)
 
+    # ---- TB Gillespie ABC
+    def tb_simulate(self, theta, initial, horizon, target, seed, sid, pos, block_width=4):
+        th = _f64(theta)
+        out, after, n = np.zeros(5), u64(), u64()
+        counts = np.zeros(1 << 16)
+        self._call("tb_simulate", _ptr(th), u64(initial), f64(horizon), f64(target), u64(seed),
+                   self._sid(sid), u64(pos), u64(block_width), _ptr(out), C.byref(after), _ptr(counts),
+                   u64(counts.size), C.byref(n))
+        return dict(time=out[0], total=out[1], genotypes=int(out[2]), summaries=out[3:5].copy(),
+                    pos_after=after.value, counts=counts[:n.value].copy())
+
+    def tb_abc_particle(self, initial, horizon, target, first, count, seed, observed, threads=None):
+        obs = _f64(observed)
+        params, summ = np.zeros((count, 3)), np.zeros((count, 2))
+        rho, failed = np.zeros(count), np.zeros(count, dtype=np.uint8)
+        self._call("tb_abc_particle", u64(initial), f64(horizon), f64(target), u64(first), u64(count),
+                   u64(seed), _ptr(obs), _ptr(params), _ptr(summ), _ptr(rho), _ptr(failed),
+                   C.c_uint(threads or os.cpu_count() or 1))
+        return params, summ, rho, failed
+
+    def tb_observed(self, initial, horizon, target, seed, block_width=4):
+        out = np.zeros(2)
+        self._call("tb_observed", u64(initial), f64(horizon), f64(target), u64(seed), u64(block_width),
+                   _ptr(out))
+        return out
+
 
 class Oracle(_Base):
+    _sid = staticmethod(u64)
     prefix = "vxo_"
 
     def __init__(self, threads=None):
@@ -342,6 +369,7 @@ class Oracle(_Base):
 
 
 class Ref(_Base):
+    _sid = staticmethod(u32)
     """The unmodified reference library behind ref_driver.cpp."""
     prefix = "ref_"
 

@@ -43,6 +43,7 @@
 #include "vexbayes/numeric.hpp"
 #include "vexbayes/rng.hpp"
 #include "vexbayes/smc.hpp"
+#include "vexbayes/tb_model.hpp"
 #include "vexbayes/toggle_switch.hpp"
 #include "vexbayes/weak_info.hpp"
 
@@ -607,6 +608,83 @@ int ref_weak_info_test(std::uint64_t hyper_count, std::uint64_t datasets, std::u
             std::ofstream out(csv_path);
             weakinfo::write_csv(table, out);
         }
+    });
+}
+
+// ----------------------------------------------- TB Gillespie ABC
+// tb::gillespie_simulate / tb_summaries / make_abc_model (tb_model.cpp:39-167) as
+// they are.  ref_tb_simulate: one path at theta from RngStream(seed, id) at pos;
+// out = (time, total, genotypes, G summary, H summary or NaN when extinct),
+// pos_after = the stream position the path stopped at.
+int ref_tb_simulate(const double* theta, std::uint64_t initial, double horizon, double target,
+                    std::uint64_t seed, std::uint32_t id, std::uint64_t pos,
+                    std::uint64_t block_width, double* out, std::uint64_t* pos_after,
+                    double* counts_out, std::uint64_t counts_cap, std::uint64_t* n_counts) {
+    return guarded([&] {
+        RngStream stream(seed, id);
+        stream.set_counter(pos);
+        const tb::TbState st = tb::gillespie_simulate({theta[0], theta[1], theta[2]}, initial,
+                                                      {horizon, target}, stream, block_width);
+        out[0] = st.time;
+        out[1] = st.total;
+        out[2] = static_cast<double>(st.genotypes);
+        out[3] = out[4] = std::numeric_limits<double>::quiet_NaN();
+        if (st.total >= 1.0) {
+            const tb::TbSummaries sm = tb::tb_summaries(st);
+            out[3] = sm.genotypes;
+            out[4] = sm.diversity;
+        }
+        if (pos_after) *pos_after = stream.counter_lo();
+        if (n_counts) *n_counts = st.counts.size();
+        for (std::size_t k = 0; counts_out && k < st.counts.size() && k < counts_cap; ++k)
+            counts_out[k] = st.counts[k];
+    });
+}
+
+// Rows [first, first+count) keyed per particle: row i owns RngStream(seed, i) and
+// runs the row sequence of abc.cpp:51-60 on tb::make_abc_model.
+int ref_tb_abc_particle(std::uint64_t initial, double horizon, double target, std::uint64_t first,
+                        std::uint64_t count, std::uint64_t seed, const double* observed,
+                        double* params, double* summaries, double* rho, std::uint8_t* failed,
+                        unsigned threads) {
+    return guarded([&] {
+        const ModelHooks hooks = tb::make_abc_model(initial, {horizon, target});
+        const std::vector<double> obs(observed, observed + 2);
+        if (threads < 1) threads = 1;
+        auto body = [&](unsigned t) {
+            std::vector<double> theta(3), summary(2);
+            for (std::uint64_t r = t; r < count; r += threads) {
+                RngStream stream(seed, static_cast<std::uint32_t>(first + r));
+                hooks.sample_prior(stream, theta);
+                stream.align_even();
+                double dist = std::numeric_limits<double>::quiet_NaN();
+                std::uint8_t bad = 0;
+                try {
+                    hooks.simulate(theta, stream, 4, summary);
+                    dist = abc::discrepancy(summary, obs);
+                } catch (const Error&) {
+                    bad = 1;
+                    std::fill(summary.begin(), summary.end(), 0.0);
+                }
+                if (params) std::copy(theta.begin(), theta.end(), params + r * 3);
+                if (summaries) std::copy(summary.begin(), summary.end(), summaries + r * 2);
+                if (rho) rho[r] = dist;
+                if (failed) failed[r] = bad;
+            }
+        };
+        std::vector<std::thread> pool;
+        for (unsigned t = 0; t < threads; ++t) pool.emplace_back(body, t);
+        for (auto& th : pool) th.join();
+    });
+}
+
+// bench::tb_observed_summaries (bench.cpp:79-92)
+int ref_tb_observed(std::uint64_t initial, double horizon, double target, std::uint64_t seed,
+                    std::uint64_t block_width, double* out) {
+    return guarded([&] {
+        const auto s = bench::tb_observed_summaries(initial, {horizon, target}, seed, block_width);
+        out[0] = s[0];
+        out[1] = s[1];
     });
 }
 

@@ -1693,4 +1693,138 @@ int vxo_weak_info_test(std::uint64_t hyper_count, std::uint64_t datasets, std::u
     });
 }
 
+// ----------------------------------------- TB Gillespie ABC
+// Restates tb::gillespie_simulate (tb_model.cpp:39-127), tb_summaries (:129-138),
+// sample_prior (:151-156) and the row sequence of abc.cpp:51-60.  The state keeps
+// the genotype counts in slot order; the lookup is "first slot whose running
+// count exceeds the target" (upper_bound over the cumulative array,
+// tb_model.cpp:31-34) -- the reference's cumulative array and its compaction
+// (:108-118) are bookkeeping that never changes which slot that is.
+struct TbPath {
+    std::vector<std::uint32_t> slots;
+    double time = 0.0, total = 0.0;
+    std::uint64_t genotypes = 0;
+};
+static TbPath tb_path(const double* theta, std::uint64_t initial, double horizon, double target,
+                      Stream& s) {
+    require(initial >= 1, "invalid-shape", "need at least one initial case");
+    require(theta[0] >= 0 && theta[1] >= 0 && theta[2] >= 0, "invalid-argument",
+            "rates must be nonnegative");
+    TbPath p;
+    p.slots.assign(1, static_cast<std::uint32_t>(initial));
+    p.total = static_cast<double>(initial);
+    p.genotypes = 1;
+    while (p.time < horizon && p.total < target && p.total > 0) {
+        const double birth = theta[0] * p.total, death = theta[1] * p.total, mut = theta[2] * p.total;
+        const double rate = birth + death + mut;
+        if (rate <= 0.0) {
+            p.time = horizon;
+            break;
+        }
+        const double wait = -ln_pos(1.0 - s.next_unit()) / rate;
+        if (p.time + wait > horizon) {
+            p.time = horizon;
+            break;
+        }
+        p.time += wait;
+        const double kind = s.next_unit() * rate;
+        const double pick = s.next_unit() * p.total;
+        std::size_t idx = 0;
+        double run = 0.0;
+        for (; idx < p.slots.size(); ++idx) {
+            run += p.slots[idx];
+            if (run > pick) break;
+        }
+        require(idx < p.slots.size(), "internal", "genotype lookup ran past the population");
+        const auto take_one = [&] {
+            if (--p.slots[idx] == 0) --p.genotypes;
+        };
+        if (kind < birth) {
+            ++p.slots[idx];
+            p.total += 1.0;
+        } else if (kind < birth + death) {
+            take_one();
+            p.total -= 1.0;
+        } else {
+            take_one();
+            p.slots.push_back(1);
+            ++p.genotypes;
+        }
+    }
+    return p;
+}
+// (G, H) with H = 1 - sum (X_i / N)^2 evaluated as 1 - ss / (n n); false when extinct
+static bool tb_summaries(const TbPath& p, double* out) {
+    if (!(p.total >= 1.0)) return false;
+    double ss = 0.0;
+    for (std::uint32_t c : p.slots) ss += static_cast<double>(c) * static_cast<double>(c);
+    out[0] = static_cast<double>(p.genotypes);
+    out[1] = 1.0 - ss / (p.total * p.total);
+    return true;
+}
+
+int vxo_tb_simulate(const double* theta, std::uint64_t initial, double horizon, double target,
+                    std::uint64_t seed, std::uint64_t id, std::uint64_t pos,
+                    std::uint64_t /*block_width*/, double* out, std::uint64_t* pos_after,
+                    double* counts_out, std::uint64_t counts_cap, std::uint64_t* n_counts) {
+    return guarded([&] {
+        Stream s(seed, id);
+        s.pos = pos;
+        const TbPath p = tb_path(theta, initial, horizon, target, s);
+        out[0] = p.time;
+        out[1] = p.total;
+        out[2] = static_cast<double>(p.genotypes);
+        out[3] = out[4] = std::numeric_limits<double>::quiet_NaN();
+        tb_summaries(p, out + 3);
+        if (pos_after) *pos_after = s.pos;
+        std::uint64_t k = 0;
+        for (std::uint32_t c : p.slots)
+            if (c) {
+                if (counts_out && k < counts_cap) counts_out[k] = c;
+                ++k;
+            }
+        if (n_counts) *n_counts = k;
+    });
+}
+
+int vxo_tb_abc_particle(std::uint64_t initial, double horizon, double target, std::uint64_t first,
+                        std::uint64_t count, std::uint64_t seed, const double* observed,
+                        double* params, double* summaries, double* rho, std::uint8_t* failed,
+                        unsigned threads) {
+    return guarded([&] {
+        require(initial >= 1, "invalid-shape", "need at least one initial case");
+        parallel_for(count, threads, [&](std::uint64_t r) {
+            Stream s(seed, first + r);
+            double theta[3];  // sample_prior: tb_model.cpp:151-156
+            theta[0] = s.next_uniform(0.0, 2.0);
+            theta[1] = s.next_uniform(0.0, theta[0]);
+            theta[2] = s.next_uniform(0.0, 1.0);
+            s.align_even();
+            const TbPath p = tb_path(theta, initial, horizon, target, s);
+            double sm[2] = {0.0, 0.0};
+            const bool ok = tb_summaries(p, sm);
+            if (params) std::copy(theta, theta + 3, params + r * 3);
+            if (summaries) std::copy(sm, sm + 2, summaries + r * 2);
+            if (rho) rho[r] = ok ? discrepancy<double>(sm, observed, 2)
+                                 : std::numeric_limits<double>::quiet_NaN();
+            if (failed) failed[r] = ok ? 0 : 1;
+        });
+    });
+}
+
+// bench::tb_observed_summaries (bench.cpp:79-92): theta = (0.2, 0.1, 0.05), stream
+// RngStream(derive_seed(seed,{91}), 0) consumed across up to 64 attempts
+int vxo_tb_observed(std::uint64_t initial, double horizon, double target, std::uint64_t seed,
+                    std::uint64_t /*block_width*/, double* out) {
+    return guarded([&] {
+        const double theta[3] = {0.2, 0.1, 0.05};
+        Stream s(derive_seed1(seed, 91), 0);
+        for (int attempt = 0; attempt < 64; ++attempt) {
+            const TbPath p = tb_path(theta, initial, horizon, target, s);
+            if (tb_summaries(p, out)) return;
+        }
+        require(false, "empty-set", "synthetic tb population kept going extinct");
+    });
+}
+
 }  // extern "C"

@@ -9,6 +9,7 @@ import ctypes as C
 VXB_ABI_VERSION = 1
 
 VXB_MODEL_LOGISTIC_SDE, VXB_MODEL_NORMAL_MEAN, VXB_MODEL_MM_TAULEAP, VXB_MODEL_TOGGLE = 1, 2, 3, 4
+VXB_MODEL_TB = 5
 VXB_F64, VXB_F32 = 0, 1
 VXB_RNG_REF, VXB_RNG_FAST, VXB_RNG_EXTERNAL = 0, 1, 2
 VXB_ARITH_EXACT, VXB_ARITH_FMA = 0, 1

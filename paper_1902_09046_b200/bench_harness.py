@@ -9,8 +9,8 @@ experiment body runs on the GPU through the C ABI: `threads` and `block_width`
 keep their meaning as the (P, V) of the reference keying (VXB_KEY_WORKER), which
 makes the produced samples identical to the CPU run of the same cell.
 
-Only the experiments on the GPU path are runnable (toggle-abc, weakinfo); the names
-of the others are kept so that reference files parse.
+Only the experiments on the GPU path are runnable (toggle-abc, weakinfo, tb); bege is
+kept as a name so that reference files parse.
 """
 import math
 import time
@@ -72,6 +72,9 @@ class ExperimentSizes:          # bench.hpp:32-43
     particles: int = 200  # SMC N_p
     hypers: int = 2       # weak-info K
     datasets: int = 8     # weak-info N
+    tb_initial: int = 10
+    tb_horizon: float = 10.0
+    tb_target: float = 10000.0
 
 
 @dataclass
@@ -116,12 +119,26 @@ def toggle_observed_summaries(ctx, steps, cells, seed, block_width):
                            derive_seed(seed, [90]), 0, 0)
 
 
+def tb_observed_summaries(ctx, initial_cases, horizon, target, seed, block_width):
+    """bench.cpp:79-92: theta = (0.2, 0.1, 0.05) from RngStream(derive_seed(seed,{91}), 0),
+    retried off the same stream while the population dies out."""
+    del block_width
+    return ctx.simulate_at(M.tb_model(initial_cases, horizon, target, attempts=64),
+                           M.TB_TRUE_THETA, derive_seed(seed, [91]), 0, 0)
+
+
 def run_experiment_once(ctx, experiment, sizes, threads, block_width, seed):
     """bench.cpp:94-137, the toggle-abc body on the GPU."""
     if experiment_from_string(experiment) == "weakinfo":   # bench.cpp:113-123
         cfg = M.weakinfo_config(hyper_count=sizes.hypers, datasets=sizes.datasets,
                                 particles=sizes.particles, block_width=block_width, seed=seed)
         return ctx.weak_info_test(cfg)
+    if experiment == "tb":                                 # bench.cpp:104-111; particle keying
+        observed = tb_observed_summaries(ctx, sizes.tb_initial, sizes.tb_horizon, sizes.tb_target,
+                                         seed, block_width)
+        model = M.tb_model(sizes.tb_initial, sizes.tb_horizon, sizes.tb_target)
+        return ctx.abc_prior_predictive_host(model, M.keying(seed), sizes.samples, 0, sizes.samples,
+                                             observed)
     if experiment != "toggle-abc":
         raise VxbError("unsupported-model: experiment " + experiment + " has no device path")
     observed = toggle_observed_summaries(ctx, sizes.steps, sizes.cells, seed, block_width)

@@ -82,6 +82,15 @@ inline PriorPredictiveSet run_prior_predictive(const ModelHooks& model, std::siz
     set.failed.resize(n);
     vxb_keying key{VXB_KEY_WORKER, static_cast<std::uint32_t>(workers),
                    static_cast<std::uint32_t>(block_width), 0, seed};
+    if (dm.model == VXB_MODEL_TB) {
+        // a TB path consumes a data-dependent number of variates: rows are keyed per
+        // particle (tb_model.hpp of this shim); block_width is validated as the
+        // reference does (blocked.cpp:10-12)
+        require(block_width == 1 || block_width == 2 || block_width == 4 || block_width == 8 ||
+                    block_width == 16,
+                "invalid-shape", "unsupported block width");
+        key = vxb_keying{VXB_KEY_PARTICLE, 1, 1, 0, seed};
+    }
     cuda::check(vxb_abc_prior_predictive(cuda::context(), &dm, &key, n, 0, n, observed.data(),
                                          set.params.data(), set.summaries.data(),
                                          set.discrepancies.data(), set.failed.data(), nullptr));

@@ -9,7 +9,7 @@
 // (P, V) of the reference keying, so a cell simulates the very samples the CPU
 // run of that cell simulates.
 // What changes: the body runs on the GPU; only the experiments with a device
-// path can run (toggle-abc, weakinfo) -- the others raise unsupported-model.
+// path can run (toggle-abc, weakinfo, tb) -- bege raises unsupported-model.
 #pragma once
 
 #include <chrono>
@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "abc.hpp"
+#include "tb_model.hpp"
 #include "toggle_switch.hpp"
 #include "weak_info.hpp"
 
@@ -82,6 +83,9 @@ struct ExperimentSizes {
     std::size_t particles = 200;  // SMC N_p
     std::size_t hypers = 2;       // weak-info K
     std::size_t datasets = 8;     // weak-info N
+    std::size_t tb_initial = 10;
+    double tb_horizon = 10.0;
+    double tb_target = 10000.0;
 };
 
 struct BenchConfig {
@@ -124,6 +128,16 @@ inline std::vector<double> toggle_observed_summaries(std::size_t steps, std::siz
                                       vxb_derive_seed(seed, path, 1), 0, 0);
 }
 
+// bench.cpp:79-92: theta = (0.2, 0.1, 0.05) from RngStream(derive_seed(seed,{91}), 0),
+// retried (up to 64 paths off the same stream) while the population dies out.
+inline std::vector<double> tb_observed_summaries(std::size_t initial_cases, tb::StopRule stop,
+                                                 std::uint64_t seed, std::size_t) {
+    const std::uint64_t path[1] = {91};
+    const tb::TbSummaries s = tb::simulate_summaries({0.2, 0.1, 0.05}, initial_cases, stop,
+                                                     vxb_derive_seed(seed, path, 1), 0, 0, 64);
+    return {s.genotypes, s.diversity};
+}
+
 inline void run_experiment_once(Experiment experiment, const ExperimentSizes& sizes,
                                 std::size_t threads, std::size_t block_width, std::uint64_t seed) {
     if (experiment == Experiment::weakinfo) {  // bench.cpp:113-123
@@ -135,6 +149,13 @@ inline void run_experiment_once(Experiment experiment, const ExperimentSizes& si
         config.block_width = block_width;
         config.seed = seed;
         weakinfo::run_weak_info_test(config);
+        return;
+    }
+    if (experiment == Experiment::tb) {  // bench.cpp:104-111
+        const tb::StopRule stop{sizes.tb_horizon, sizes.tb_target};
+        const auto observed = tb_observed_summaries(sizes.tb_initial, stop, seed, block_width);
+        abc::run_prior_predictive(tb::make_abc_model(sizes.tb_initial, stop), sizes.samples, threads,
+                                  block_width, seed, observed);
         return;
     }
     require(experiment == Experiment::toggle_abc, "unsupported-model",

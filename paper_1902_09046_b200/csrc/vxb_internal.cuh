@@ -15,6 +15,14 @@ void toggle_launch(vxb_ctx* ctx, const vxb_model& m, const Keying& key, uint64_t
                    const double* theta_dev, double* params, double* summaries, double* rho,
                    uint8_t* failed);
 
+// vxb_tb.cu
+void tb_launch(vxb_ctx* ctx, const vxb_model& m, uint64_t seed, uint64_t first, uint64_t count,
+               const double* observed_host, double* params, double* summaries, double* rho,
+               uint8_t* failed);
+void tb_simulate_fixed(vxb_ctx* ctx, const vxb_model& m, const double* theta_dev, uint64_t key,
+                       uint64_t pos, uint32_t attempts, double* summary_dev, uint8_t* failed_dev,
+                       double* detail_dev);
+
 // vxb_select.cu
 void compact_accepted_device(vxb_ctx* ctx, int precision, const void* rho_dev,
                              const uint8_t* failed_dev, uint64_t n, double epsilon,

@@ -264,6 +264,24 @@ extern "C" int vxb_abc_prior_predictive(vxb_ctx* ctx, const vxb_model* model,
         require(model && key && observed, "invalid-argument", "null argument");
         require(n_total >= 1, "invalid-shape", "need at least one prior predictive sample");
         require(first + count <= n_total, "invalid-shape", "row range exceeds the job");
+        if (model->model == VXB_MODEL_TB) {  // exact Gillespie TB model: vxb_tb.cu
+            require(key->mode == VXB_KEY_PARTICLE, "invalid-argument",
+                    "the TB model consumes a data-dependent number of variates per row: "
+                    "particle keying only");
+            Staged t_params(ctx, params, count * 3 * 8, false, true);
+            Staged t_summ(ctx, summaries, count * 2 * 8, false, true);
+            Staged t_rho(ctx, rho, count * 8, false, true);
+            Staged t_failed(ctx, failed, count, false, true);
+            tb_launch(ctx, *model, key->seed, first, count, observed, t_params.as<double>(),
+                      t_summ.as<double>(), t_rho.as<double>(), t_failed.as<uint8_t>());
+            t_params.finish();
+            t_summ.finish();
+            t_rho.finish();
+            t_failed.finish();
+            if (t_params.staged() || t_summ.staged() || t_rho.staged() || t_failed.staged())
+                VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+            return;
+        }
         if (model->model == VXB_MODEL_TOGGLE) {  // the reference's own SDE: vxb_toggle.cu
             const Keying tk = make_keying(*key, *model, n_total);
             Staged t_params(ctx, params, count * 7 * 8, false, true);
@@ -322,6 +340,27 @@ extern "C" int vxb_simulate_at(vxb_ctx* ctx, const vxb_model* model, const doubl
         require(model && theta && summary, "invalid-argument", "null argument");
         require(model->rng == VXB_RNG_REF, "invalid-argument",
                 "simulate_at is defined for the reference generator");
+        if (model->model == VXB_MODEL_TB) {
+            // consts[3] > 1: retry from where the stream stands while the population dies
+            // out, the way bench.cpp:79-92 builds observed summaries
+            const uint32_t attempts = model->consts[3] >= 1.0 ? static_cast<uint32_t>(model->consts[3]) : 1;
+            if (!is_device_pointer(theta))
+                require(theta[0] >= 0 && theta[1] >= 0 && theta[2] >= 0, "invalid-argument",
+                        "rates must be nonnegative");  // tb_model.cpp:43-44
+            Staged t_theta(ctx, theta, 3 * sizeof(double), true, false);
+            Staged t_summ(ctx, summary, 2 * sizeof(double), false, true);
+            Scratch t_failed(ctx, 1);
+            tb_simulate_fixed(ctx, *model, t_theta.as<double>(), stream_key(splitmix64(seed), stream_id),
+                              pos, attempts, t_summ.as<double>(), t_failed.as<uint8_t>(), nullptr);
+            uint8_t bad = 0;
+            VXB_CUDA(cudaMemcpyAsync(&bad, t_failed.as<uint8_t>(), 1, cudaMemcpyDeviceToHost, ctx->stream));
+            t_summ.finish();
+            VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+            require(!bad, attempts > 1 ? "empty-set" : "extinct-population",
+                    attempts > 1 ? "synthetic tb population kept going extinct"
+                                 : "summaries need a surviving population");
+            return;
+        }
         if (model->model == VXB_MODEL_TOGGLE) {
             require(model->steps >= 2, "invalid-horizon",
                     "toggle simulation needs at least two time points");

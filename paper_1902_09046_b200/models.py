@@ -101,3 +101,19 @@ def weakinfo_config(hyper_count=400, datasets=400, particles=500, alpha=0.05, c=
     for g in range(len(dose)):
         cfg.dose[g], cfg.group_size[g] = dose[g], group_size[g]
     return cfg
+
+
+TB_TRUE_THETA = (0.2, 0.1, 0.05)   # bench.cpp:81 "true" parameters of the synthetic observation
+
+
+def tb_model(initial_cases=10, time_horizon=50.0, case_target=10000.0, attempts=1):
+    """The reference's TB transmission model (tb_model.hpp:12-76): theta = (alpha,
+    delta, tau), exact Gillespie simulation, summaries (G, H).  StopRule defaults as
+    tb_model.hpp:41-44."""
+    m = A.vxb_model()
+    m.model = A.VXB_MODEL_TB
+    m.precision, m.rng, m.arith = A.VXB_F64, A.VXB_RNG_REF, A.VXB_ARITH_EXACT
+    m.dim, m.summary_dim = 3, 2
+    m.consts[0], m.consts[1], m.consts[2], m.consts[3] = initial_cases, time_horizon, case_target, attempts
+    m.prior_hi[0], m.prior_hi[2] = 2.0, 1.0
+    return m

@@ -70,6 +70,11 @@ static int csv_mode(const char* bench_golden, const char* out_dir) {
     {
         bench::ExperimentSizes ws;
         bench::run_experiment_once(bench::Experiment::weakinfo, ws, 2, 4, 1337);
+        bench::run_experiment_once(bench::Experiment::tb, ws, 2, 4, 1337);
+        const auto tb_obs = bench::tb_observed_summaries(10, {10.0, 10000.0}, 1337, 4);
+        const auto tb_set = abc::run_prior_predictive(tb::make_abc_model(10, {10.0, 10000.0}), 40, 2, 4, 1337, tb_obs);
+        std::printf("tb %.17g %.17g %.17g %.17g %d\n", tb_obs[0], tb_obs[1], tb_set.summaries[0],
+                    tb_set.discrepancies[1], static_cast<int>(tb_set.failed[0] + tb_set.failed[1]));
     }
 
     bench::BenchConfig cfg;

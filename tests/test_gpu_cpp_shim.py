@@ -65,7 +65,7 @@ def test_cpp_shim_matches_oracle(tmp_path, oracle, golden):
     assert [float(t) for t in r["pvalues"]] == [0.25, 0.75]
 
 
-def test_cpp_shim_reference_format_outputs(tmp_path, golden):
+def test_cpp_shim_reference_format_outputs(tmp_path, golden, oracle):
     """abc::write_csv and the bench harness of the C++ shim: the set file equals
     the file the reference wrote; the bench file survives parse -> write."""
     from paper_1902_09046_b200 import bench_harness as B
@@ -94,6 +94,10 @@ def test_cpp_shim_reference_format_outputs(tmp_path, golden):
     assert abs(float(r["evidence"][0]) - anneal["run_evidence"][0]) < 1e-9
     assert int(r["evidence"][1]) == anneal["run_iterations"][0]
     assert r["evidence"][2] == "".join(str(v) for v in anneal["run_deaths"][0])
+    tb_obs = oracle.tb_observed(10, 10.0, 10000.0, 1337)
+    tb_rows = oracle.tb_abc_particle(10, 10.0, 10000.0, 0, 40, 1337, tb_obs)
+    assert [float(t) for t in r["tb"][:4]] == [tb_obs[0], tb_obs[1], tb_rows[1][0, 0], tb_rows[2][1]]
+    assert int(r["tb"][4]) == int(tb_rows[3][0]) + int(tb_rows[3][1])
     sweep = B.parse_csv(read(tmp_path / "sweep.csv"))
     assert [(x.block_width, x.threads, x.replicate) for x in sweep] == \
         [(v, p, k) for v in (1, 4) for p in (1, 3) for k in (0, 1)]

@@ -299,3 +299,48 @@ def test_toggle_switch_parity(ctx, oracle, golden):
         assert (got[3] == 1).all() and np.isnan(got[2]).all() and (got[1] == 0).all()
         for g, w in zip(got, want):
             assert eq(g, w)
+
+
+# ------------------------------------------- TB Gillespie ABC
+@pytest.mark.timeout(900)
+def test_tb_gillespie_parity(ctx, oracle):
+    """The reference's exact-simulation model, one warp per path: summaries,
+    distances and failure flags bit-identical to tb::gillespie_simulate run row by
+    row on RngStream(seed, row) (oracle pinned to the unmodified reference in
+    tests/test_oracle_pins.py)."""
+    m = M.tb_model(10, 10.0, 10000.0)                      # bench.hpp:39-42 sizes
+    for theta, seed, sid, pos in [((0.2, 0.1, 0.05), 5, 2, 3), ((1.5, 0.3, 0.9), 6, 0, 0),
+                                  ((0.4, 0.39, 0.2), 7, 1, 8), ((0.3, 0.0, 0.0), 9, 0, 1),
+                                  ((0.0, 0.0, 0.0), 8, 0, 0)]:
+        want = oracle.tb_simulate(theta, 10, 10.0, 10000.0, seed, sid, pos)
+        assert eq(ctx.simulate_at(m, theta, seed, sid, pos), want["summaries"]), theta
+    # the synthetic observation of the harness: retries while the population dies out
+    obs = ctx.simulate_at(M.tb_model(10, 10.0, 10000.0, attempts=64), M.TB_TRUE_THETA,
+                          lib.derive_seed(1337, [91]), 0, 0)
+    assert eq(obs, oracle.tb_observed(10, 10.0, 10000.0, 1337))
+    with pytest.raises(lib.VxbError) as e:                 # certain extinction: delta >> alpha, long horizon
+        ctx.simulate_at(M.tb_model(1, 1e6, 100.0), (0.0, 5.0, 0.0), 3, 0, 0)
+    assert e.value.code == "extinct-population"
+    with pytest.raises(lib.VxbError) as e:
+        ctx.simulate_at(m, (-0.1, 0.1, 0.1), 3, 0, 0)
+    assert e.value.code == "invalid-argument"
+    n = 300
+    want = oracle.tb_abc_particle(10, 10.0, 10000.0, 0, n, 1337, obs)
+    got = ctx.abc_prior_predictive_host(m, M.keying(1337), n, 0, n, obs)
+    for g, w in zip(got, want):
+        assert eq(g, w)
+    assert got[3].any() and not got[3].all()               # extinct rows are flagged, not fatal
+    assert got[1][:, 0].max() > 1000                       # paths that reach thousands of genotypes
+    # shards reproduce the job; other stop rules and small targets (slot array refills)
+    part = ctx.abc_prior_predictive_host(m, M.keying(1337), n, 100, 50, obs)
+    for g, w in zip(part, want):
+        assert eq(g, w[100:150])
+    for initial, horizon, target in ((10, 50.0, 10000.0), (3, 25.0, 400.0), (500, 4.0, 700.0)):
+        mm = M.tb_model(initial, horizon, target)
+        want = oracle.tb_abc_particle(initial, horizon, target, 0, 96, 77, [50.0, 0.9])
+        got = ctx.abc_prior_predictive_host(mm, M.keying(77), 96, 0, 96, np.array([50.0, 0.9]))
+        for g, w in zip(got, want):
+            assert eq(g, w), (initial, horizon, target)
+    with pytest.raises(lib.VxbError) as e:
+        ctx.abc_prior_predictive_host(m, M.keying(1, A.VXB_KEY_WORKER, 2, 4), 8, 0, 8, obs)
+    assert e.value.code == "invalid-argument"

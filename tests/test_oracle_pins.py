@@ -307,3 +307,23 @@ def test_logistic_analytic_anchors(oracle):
     b2 = oracle.abc_prior_predictive(m3, M.keying(5), 1000, 400, 600, np.ones(10), threads=8)
     for x0, x1, x2 in zip(a, b1, b2):
         assert eq(x0, np.concatenate([x1, x2]))
+
+
+def test_tb_gillespie_restatement_equals_reference(oracle, ref):
+    """tb::gillespie_simulate / tb_summaries / sample_prior / tb_observed_summaries:
+    the oracle's restatement against the unmodified reference, bit for bit (state,
+    summaries and the stream position a path stops at)."""
+    for theta, seed in [((0.2, 0.1, 0.05), 5), ((1.5, 0.3, 0.9), 6), ((0.4, 0.39, 0.2), 7),
+                        ((0.0, 0.0, 0.0), 8), ((0.3, 0.0, 0.0), 9), ((0.1, 1.9, 0.5), 10)]:
+        a = ref.tb_simulate(theta, 10, 10.0, 10000.0, seed, 2, 3)
+        b = oracle.tb_simulate(theta, 10, 10.0, 10000.0, seed, 2, 3)
+        for k in a:
+            assert np.array_equal(a[k], b[k], equal_nan=True), (theta, k)
+    assert np.array_equal(ref.tb_observed(10, 10.0, 10000.0, 1337), oracle.tb_observed(10, 10.0, 10000.0, 1337))
+    obs = [10.0, 0.7]
+    for initial, horizon, target in ((10, 10.0, 10000.0), (3, 25.0, 400.0)):
+        a = ref.tb_abc_particle(initial, horizon, target, 5, 64, 1337, obs)
+        b = oracle.tb_abc_particle(initial, horizon, target, 5, 64, 1337, obs)
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y, equal_nan=True)
+        assert a[3].any()
