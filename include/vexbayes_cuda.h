@@ -386,6 +386,18 @@ typedef struct vxb_weakinfo_cfg {
  * [k][i][1] data drawn under prior k (NaN where the sampler failed). */
 int vxb_weak_info_test(vxb_ctx* ctx, const vxb_weakinfo_cfg* cfg, double* lambda, double* gamma,
                        uint8_t* weakly, uint64_t* completed, double* evidence);
+/* The three stages of the test, exposed so that a multi-GPU host can shard the
+ * rows (hyperparameters) over ranks -- the reference's own task parallelism
+ * (weak_info.cpp:248-262) -- and all-gather the evidences:
+ * lambdas:  the K+1 hyperparameter rows (host output, (K+1) x 2).
+ * evidence: rows [first_row, first_row+n_rows): n_rows x N x 2 log evidences.
+ * cutoffs:  p-values, alpha-cut-offs and flags from the full evidence table
+ *           ((K+1) x N x 2, NaN = failed run); host only, no GPU needed. */
+int vxb_weak_info_lambdas(vxb_ctx* ctx, const vxb_weakinfo_cfg* cfg, double* lambda);
+int vxb_weak_info_evidence(vxb_ctx* ctx, const vxb_weakinfo_cfg* cfg, const double* lambda,
+                           uint64_t first_row, uint64_t n_rows, double* evidence);
+int vxb_weak_info_cutoffs(const vxb_weakinfo_cfg* cfg, const double* evidence, double* gamma,
+                          uint8_t* weakly, uint64_t* completed);
 
 /* ------------------------------------------------ tau-leap MLMC (C4) */
 typedef struct vxb_mlmc_cfg {

@@ -87,5 +87,6 @@ EXPORTED_SYMBOLS = (
     "vxb_ess", "vxb_logsumexp", "vxb_resample_multinomial", "vxb_abcsmc_run",
     "vxb_abcsmc_propose", "vxb_abcsmc_weights", "vxb_weighted_moments", "vxb_canon_cumsum",
     "vxb_canon_chunk_sums", "vxb_quantile", "vxb_divide", "vxb_make_kernel", "vxb_bioassay_log_likelihood", "vxb_bioassay_sample", "vxb_smc_bioassay",
-    "vxb_weak_info_test", "vxb_mlmc_level", "vxb_mlmc_tauleap",
+    "vxb_weak_info_test", "vxb_weak_info_lambdas", "vxb_weak_info_evidence",
+    "vxb_weak_info_cutoffs", "vxb_mlmc_level", "vxb_mlmc_tauleap",
 )

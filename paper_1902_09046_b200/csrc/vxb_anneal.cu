@@ -514,7 +514,7 @@ __global__ void bioassay_ll_kernel(Design d, const double* beta, uint64_t lanes,
 // dataset i, which = 0 (base data) / 1 (data from prior k): seeds and priors as in
 // weak_info.cpp:217-236.
 struct PlanParams {
-    uint64_t rows, datasets, seed;
+    uint64_t rows, first_row, datasets, seed;  // rows of this shard; k = first_row + local row
     int redraw_base;
     double base0, base1;
     const double* lambda_rows;  // rows x 2
@@ -529,19 +529,19 @@ __global__ void weakinfo_plan_kernel(PlanParams p) {
     const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const uint64_t pairs = p.rows * p.datasets;
     if (t >= pairs) return;
-    const uint64_t k = t / p.datasets, i = t % p.datasets;
+    const uint64_t local = t / p.datasets, k = p.first_row + local, i = t % p.datasets;
     {
         const uint64_t path[3] = {3, k, i};
         p.draw_seed[t] = derive_seed_dev(p.seed, path, 3);
-        p.draw_lambda[2 * t] = p.lambda_rows[2 * k];
-        p.draw_lambda[2 * t + 1] = p.lambda_rows[2 * k + 1];
+        p.draw_lambda[2 * t] = p.lambda_rows[2 * local];
+        p.draw_lambda[2 * t + 1] = p.lambda_rows[2 * local + 1];
     }
     if (p.redraw_base) {
         const uint64_t path[3] = {5, k, i};
         p.draw_seed[pairs + t] = derive_seed_dev(p.seed, path, 3);
         p.draw_lambda[2 * (pairs + t)] = p.base0;
         p.draw_lambda[2 * (pairs + t) + 1] = p.base1;
-    } else if (k == 0) {
+    } else if (local == 0) {  // the shared base datasets: the same for every shard
         const uint64_t path[2] = {2, i};
         p.draw_seed[pairs + i] = derive_seed_dev(p.seed, path, 2);
         p.draw_lambda[2 * (pairs + i)] = p.base0;
@@ -551,8 +551,8 @@ __global__ void weakinfo_plan_kernel(PlanParams p) {
         const uint64_t r = 2 * t + which;  // run index: (k, i, which)
         const uint64_t path[4] = {4, k, which, i};
         p.run_seed[r] = derive_seed_dev(p.seed, path, 4);
-        p.run_lambda[2 * r] = p.lambda_rows[2 * k];
-        p.run_lambda[2 * r + 1] = p.lambda_rows[2 * k + 1];
+        p.run_lambda[2 * r] = p.lambda_rows[2 * local];
+        p.run_lambda[2 * r + 1] = p.lambda_rows[2 * local + 1];
     }
 }
 // deaths of run (k, i, which) from the draws
@@ -769,45 +769,55 @@ extern "C" int vxb_smc_bioassay(vxb_ctx* ctx, uint64_t n_runs, uint32_t groups, 
     });
 }
 
-extern "C" int vxb_weak_info_test(vxb_ctx* ctx, const vxb_weakinfo_cfg* cfg, double* lambda, double* gamma,
-                                  uint8_t* weakly, uint64_t* completed, double* evidence) {
+// hyperparameters: lambda_k ~ U([0.1,10] x [0.1,20]) from RngStream(derive_seed(seed,{1}), 0)
+// (weak_info.cpp:174-182); next_uniform's clamp (rng.cpp:101-110) on the host
+extern "C" int vxb_weak_info_lambdas(vxb_ctx* ctx, const vxb_weakinfo_cfg* cfg, double* lambda) {
     return guarded([&] {
         use(ctx);
-        require(cfg && lambda && gamma && weakly && completed, "invalid-argument", "null argument");
+        require(cfg && lambda, "invalid-argument", "null argument");
+        lambda[0] = cfg->base[0];
+        lambda[1] = cfg->base[1];
+        if (cfg->hyper_count == 0) return;
+        std::vector<uint64_t> words(2 * cfg->hyper_count);
+        const uint64_t one = 1;
+        require(vxb_rng_fill_u64(ctx, vxb_derive_seed(cfg->seed, &one, 1), 0, 0, words.size(),
+                                 words.data()) == 0,
+                "internal", vxb_last_error());
+        for (uint64_t j = 0; j < words.size(); ++j) {
+            const double a = 0.1, b = (j & 1) ? 20.0 : 10.0;
+            const double u = static_cast<double>(words[j] >> 11) * 0x1.0p-53;
+            const double top = std::nextafter(b, a);
+            const double r = a + u * (b - a);
+            lambda[2 + j] = r < a ? a : (r > top ? top : r);
+        }
+    });
+}
+
+// evidences of rows [first_row, first_row + n_rows): n_rows x N x 2 (base data, data
+// drawn under the row's prior); NaN where the sampler failed
+extern "C" int vxb_weak_info_evidence(vxb_ctx* ctx, const vxb_weakinfo_cfg* cfg, const double* lambda,
+                                      uint64_t first_row, uint64_t n_rows, double* evidence) {
+    return guarded([&] {
+        use(ctx);
+        require(cfg && lambda && evidence, "invalid-argument", "null argument");
         require(cfg->datasets >= 1, "invalid-argument", "need at least one dataset per prior");
-        require(cfg->alpha > 0.0 && cfg->alpha < 1.0, "invalid-argument", "alpha must lie in (0, 1)");
+        require(first_row + n_rows <= cfg->hyper_count + 1, "invalid-shape", "row range exceeds the table");
         check_sampler_args(cfg->particles, cfg->block_width, cfg->c);
-        const uint64_t rows = cfg->hyper_count + 1, n = cfg->datasets, pairs = rows * n, runs = 2 * pairs;
+        if (n_rows == 0) return;
+        const uint64_t n = cfg->datasets, pairs = n_rows * n, runs = 2 * pairs;
         Scratch* big = nullptr;
         const Design design = make_design(ctx, cfg->groups, cfg->dose, cfg->group_size, &big);
         const uint32_t groups = cfg->groups;
-
-        // hyperparameters: lambda_k ~ U([0.1,10] x [0.1,20]) from RngStream(derive_seed(seed,{1}), 0)
-        // (weak_info.cpp:174-182); next_uniform's clamp (rng.cpp:101-110) on the host
-        lambda[0] = cfg->base[0];
-        lambda[1] = cfg->base[1];
-        if (cfg->hyper_count) {
-            std::vector<uint64_t> words(2 * cfg->hyper_count);
-            const uint64_t one = 1;
-            require(vxb_rng_fill_u64(ctx, vxb_derive_seed(cfg->seed, &one, 1), 0, 0, words.size(),
-                                     words.data()) == 0,
-                    "internal", vxb_last_error());
-            for (uint64_t j = 0; j < words.size(); ++j) {
-                const double a = 0.1, b = (j & 1) ? 20.0 : 10.0;
-                const double u = static_cast<double>(words[j] >> 11) * 0x1.0p-53;
-                const double top = std::nextafter(b, a);
-                const double r = a + u * (b - a);
-                lambda[2 + j] = r < a ? a : (r > top ? top : r);
-            }
-        }
         const uint64_t base_draws = cfg->redraw_base ? pairs : n, draws = pairs + base_draws;
-        Scratch d_rows(ctx, rows * 16), d_dl(ctx, draws * 16), d_ds(ctx, draws * 8), d_rl(ctx, runs * 16),
+        Scratch d_rows(ctx, n_rows * 16), d_dl(ctx, draws * 16), d_ds(ctx, draws * 8), d_rl(ctx, runs * 16),
             d_rs(ctx, runs * 8), d_dy(ctx, draws * groups * 4), d_ry(ctx, runs * groups * 4),
-            d_ev(ctx, runs * 8), d_it(ctx, runs * 4), d_st(ctx, runs);
-        VXB_CUDA(cudaMemcpyAsync(d_rows.as<void>(), lambda, rows * 16, cudaMemcpyHostToDevice, ctx->stream));
+            d_it(ctx, runs * 4), d_st(ctx, runs);
+        Staged d_ev(ctx, evidence, runs * 8, false, true);
+        VXB_CUDA(cudaMemcpyAsync(d_rows.as<void>(), lambda + 2 * first_row, n_rows * 16,
+                                 cudaMemcpyHostToDevice, ctx->stream));
         {
             LaunchScope scope(ctx, VXB_K_MISC);
-            PlanParams pp{rows, n, cfg->seed, cfg->redraw_base, cfg->base[0], cfg->base[1],
+            PlanParams pp{n_rows, first_row, n, cfg->seed, cfg->redraw_base, cfg->base[0], cfg->base[1],
                           d_rows.as<double>(), d_dl.as<double>(), d_ds.as<uint64_t>(), d_rl.as<double>(),
                           d_rs.as<uint64_t>()};
             weakinfo_plan_kernel<<<grid_for(pairs, 128), 128, 0, ctx->stream>>>(pp);
@@ -820,34 +830,40 @@ extern "C" int vxb_weak_info_test(vxb_ctx* ctx, const vxb_weakinfo_cfg* cfg, dou
             dp.deaths = d_dy.as<uint32_t>();
             bioassay_draw_kernel<<<grid_for(draws, 128), 128, 0, ctx->stream>>>(dp);
             weakinfo_gather_kernel<<<grid_for(pairs, 128), 128, 0, ctx->stream>>>(
-                rows, n, groups, cfg->redraw_base, d_dy.as<uint32_t>(), d_ry.as<uint32_t>());
+                n_rows, n, groups, cfg->redraw_base, d_dy.as<uint32_t>(), d_ry.as<uint32_t>());
             check_launch("weak-info plan kernels");
         }
         std::vector<double> run_lambda(runs * 2);
         for (uint64_t t = 0; t < pairs; ++t)
             for (int which = 0; which < 2; ++which) {
-                run_lambda[2 * (2 * t + which)] = lambda[2 * (t / n)];
-                run_lambda[2 * (2 * t + which) + 1] = lambda[2 * (t / n) + 1];
+                run_lambda[2 * (2 * t + which)] = lambda[2 * (first_row + t / n)];
+                run_lambda[2 * (2 * t + which) + 1] = lambda[2 * (first_row + t / n) + 1];
             }
         anneal_device(ctx, design, runs, cfg->particles, cfg->c, cfg->scale, d_ry.as<uint32_t>(),
                       d_rl.as<double>(), run_lambda.data(), d_rs.as<uint64_t>(), d_ev.as<double>(),
                       d_it.as<uint32_t>(), d_st.as<uint8_t>(), nullptr, 0);
-        std::vector<double> ev(runs);
-        std::vector<uint8_t> st(runs);
-        VXB_CUDA(cudaMemcpyAsync(ev.data(), d_ev.as<void>(), runs * 8, cudaMemcpyDeviceToHost, ctx->stream));
-        VXB_CUDA(cudaMemcpyAsync(st.data(), d_st.as<void>(), runs, cudaMemcpyDeviceToHost, ctx->stream));
+        d_ev.finish();
         VXB_CUDA(cudaStreamSynchronize(ctx->stream));
-        if (evidence) std::copy(ev.begin(), ev.end(), evidence);
+        delete big;
+    });
+}
 
-        // p-values and cut-offs per row (weak_info.cpp:238-246, 108-125), host side
+// p-values and cut-offs per row (weak_info.cpp:238-246, 108-125, 272-275); host only.
+// evidence: (K+1) x N x 2, NaN = failed sampler run.
+extern "C" int vxb_weak_info_cutoffs(const vxb_weakinfo_cfg* cfg, const double* evidence, double* gamma,
+                                     uint8_t* weakly, uint64_t* completed) {
+    return guarded([&] {
+        require(cfg && evidence && gamma && weakly && completed, "invalid-argument", "null argument");
+        require(cfg->alpha > 0.0 && cfg->alpha < 1.0, "invalid-argument", "alpha must lie in (0, 1)");
+        const uint64_t rows = cfg->hyper_count + 1, n = cfg->datasets;
         for (uint64_t k = 0; k < rows; ++k) {
             std::vector<double> base_ev, hyper_ev;
             uint64_t both = 0;
             for (uint64_t i = 0; i < n; ++i) {
-                const uint64_t r = 2 * (k * n + i);
-                const bool ok_b = st[r] == kRunOk, ok_h = st[r + 1] == kRunOk;
-                if (ok_b) base_ev.push_back(ev[r]);
-                if (ok_h) hyper_ev.push_back(ev[r + 1]);
+                const double eb = evidence[2 * (k * n + i)], eh = evidence[2 * (k * n + i) + 1];
+                const bool ok_b = !std::isnan(eb), ok_h = !std::isnan(eh);
+                if (ok_b) base_ev.push_back(eb);
+                if (ok_h) hyper_ev.push_back(eh);
                 both += (ok_b && ok_h) ? 1 : 0;
             }
             completed[k] = both;
@@ -870,6 +886,30 @@ extern "C" int vxb_weak_info_test(vxb_ctx* ctx, const vxb_weakinfo_cfg* cfg, dou
             }
         }
         for (uint64_t k = 0; k < rows; ++k) weakly[k] = (k != 0 && gamma[k] > gamma[0]) ? 1 : 0;
-        delete big;
+    });
+}
+
+extern "C" int vxb_weak_info_test(vxb_ctx* ctx, const vxb_weakinfo_cfg* cfg, double* lambda, double* gamma,
+                                  uint8_t* weakly, uint64_t* completed, double* evidence) {
+    return guarded([&] {
+        require(cfg && lambda && gamma && weakly && completed, "invalid-argument", "null argument");
+        require(cfg->datasets >= 1, "invalid-argument", "need at least one dataset per prior");
+        require(cfg->alpha > 0.0 && cfg->alpha < 1.0, "invalid-argument", "alpha must lie in (0, 1)");
+        const uint64_t rows = cfg->hyper_count + 1;
+        std::vector<double> own;
+        if (!evidence) {
+            own.resize(rows * cfg->datasets * 2);
+            evidence = own.data();
+        }
+        const auto must = [](int rc) {  // pass a stage's "code: message" through unchanged
+            if (rc == 0) return;
+            const std::string text = vxb_last_error();
+            const size_t cut = text.find(": ");
+            if (cut == std::string::npos) throw Error{"internal", text};
+            throw Error{text.substr(0, cut), text.substr(cut + 2)};
+        };
+        must(vxb_weak_info_lambdas(ctx, cfg, lambda));
+        must(vxb_weak_info_evidence(ctx, cfg, lambda, 0, rows, evidence));
+        must(vxb_weak_info_cutoffs(cfg, evidence, gamma, weakly, completed));
     });
 }

@@ -387,8 +387,11 @@ __global__ void __launch_bounds__(256) abcsmc_propose_kernel(const __grid_consta
 // Importance-weight denominator: one new particle per thread, previous
 // population streamed through shared memory in index order, so the sum over j
 // is the oracle's sequential sum (vxo_abcsmc_weights).
+// 64-thread CTAs: at N = 1e5 new particles that is 1563 CTAs = 10.6 per SM, so the
+// last wave costs 4% instead of the 12% of 128-thread CTAs (5.3 per SM).
+constexpr int kWeightsBlock = 64;
 template <int D>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(kWeightsBlock)
 abcsmc_weights_kernel(uint64_t count, const double* __restrict__ theta_new, uint64_t n_prev,
                       const double* __restrict__ theta_prev, const double* __restrict__ w_prev,
                       const double* __restrict__ chol, double* __restrict__ w_out) {
@@ -398,7 +401,7 @@ abcsmc_weights_kernel(uint64_t count, const double* __restrict__ theta_new, uint
     __shared__ double s_chol[D * D], s_invd[D];
     if (threadIdx.x < D * D) s_chol[threadIdx.x] = chol[threadIdx.x];
     if (threadIdx.x < D) s_invd[threadIdx.x] = __ddiv_rn(1.0, chol[threadIdx.x * D + threadIdx.x]);
-    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * 128 + threadIdx.x;
+    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kWeightsBlock + threadIdx.x;
     double ti[D];
 #pragma unroll
     for (int k = 0; k < D; ++k) ti[k] = r < count ? theta_new[r * D + k] : 0.0;
@@ -406,10 +409,13 @@ abcsmc_weights_kernel(uint64_t count, const double* __restrict__ theta_new, uint
     for (uint64_t j0 = 0; j0 < n_prev; j0 += kTile) {
         const uint64_t len = min(static_cast<uint64_t>(kTile), n_prev - j0);
         __syncthreads();
-        for (uint64_t t = threadIdx.x; t < len * D; t += 128) s_theta[t] = theta_prev[j0 * D + t];
-        if (threadIdx.x < len) s_w[threadIdx.x] = w_prev[j0 + threadIdx.x];
+        for (uint64_t t = threadIdx.x; t < len * D; t += kWeightsBlock) s_theta[t] = theta_prev[j0 * D + t];
+        for (uint64_t t = threadIdx.x; t < len; t += kWeightsBlock) s_w[t] = w_prev[j0 + t];
         __syncthreads();
-        for (uint64_t j = 0; j < len; ++j) {
+        // one term w_j exp(-q_ij / 2); terms are independent, only the running sum is
+        // ordered: four terms are evaluated side by side (their Horner chains
+        // interleave) and then added in index order
+        const auto term = [&](uint64_t j) {
             double y[D];
             double q = 0.0;
 #pragma unroll
@@ -420,9 +426,14 @@ abcsmc_weights_kernel(uint64_t count, const double* __restrict__ theta_new, uint
                 y[k] = __dmul_rn(v, s_invd[k]);
                 q = __dadd_rn(q, __dmul_rn(y[k], y[k]));
             }
-            const double e = exp2_clamped<Exact>(__dmul_rn(__dmul_rn(-0.5, q), kInvLn2));
-            sum = __dadd_rn(sum, __dmul_rn(s_w[j], e));
+            return __dmul_rn(s_w[j], exp2_clamped<Exact>(__dmul_rn(__dmul_rn(-0.5, q), kInvLn2)));
+        };
+        uint64_t j = 0;
+        for (; j + 4 <= len; j += 4) {
+            const double t0 = term(j), t1 = term(j + 1), t2 = term(j + 2), t3 = term(j + 3);
+            sum = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(sum, t0), t1), t2), t3);
         }
+        for (; j < len; ++j) sum = __dadd_rn(sum, term(j));
     }
     if (r < count) w_out[r] = __ddiv_rn(1.0, sum);
 }
@@ -525,7 +536,7 @@ __global__ void whiten_kernel(int mode, uint64_t n, const double* __restrict__ t
 }
 
 template <int D>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(kWeightsBlock)
 abcsmc_weights_fast_kernel(uint64_t count, const double* __restrict__ y_new, uint64_t n_prev,
                            const double* __restrict__ y_prev, const double* __restrict__ w_prev,
                            const double2* __restrict__ fast_table, double* __restrict__ w_out) {
@@ -533,8 +544,8 @@ abcsmc_weights_fast_kernel(uint64_t count, const double* __restrict__ y_new, uin
     __shared__ double s_y[kTile * (D + 1)];
     __shared__ double s_w[kTile];
     __shared__ double2 s_tab[kFastTableSize];
-    for (int i = threadIdx.x; i < kFastTableSize; i += 128) s_tab[i] = fast_table[i];
-    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * 128 + threadIdx.x;
+    for (int i = threadIdx.x; i < kFastTableSize; i += kWeightsBlock) s_tab[i] = fast_table[i];
+    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kWeightsBlock + threadIdx.x;
     double yi[D + 1];
 #pragma unroll
     for (int k = 0; k <= D; ++k) yi[k] = r < count ? y_new[r * (D + 1) + k] : 0.0;
@@ -542,16 +553,23 @@ abcsmc_weights_fast_kernel(uint64_t count, const double* __restrict__ y_new, uin
     for (uint64_t j0 = 0; j0 < n_prev; j0 += kTile) {
         const uint64_t len = min(static_cast<uint64_t>(kTile), n_prev - j0);
         __syncthreads();
-        for (uint64_t t = threadIdx.x; t < len * (D + 1); t += 128) s_y[t] = y_prev[j0 * (D + 1) + t];
-        if (threadIdx.x < len) s_w[threadIdx.x] = w_prev[j0 + threadIdx.x];
+        for (uint64_t t = threadIdx.x; t < len * (D + 1); t += kWeightsBlock) s_y[t] = y_prev[j0 * (D + 1) + t];
+        for (uint64_t t = threadIdx.x; t < len; t += kWeightsBlock) s_w[t] = w_prev[j0 + t];
         __syncthreads();
-        for (uint64_t j = 0; j < len; ++j) {
+        const auto kernel_value = [&](uint64_t j) {
             double z = s_y[j * (D + 1) + D];
 #pragma unroll
             for (int k = 0; k < D; ++k) z = fma(yi[k], s_y[j * (D + 1) + k], z);
             z += yi[D];  // -|y_i - y_j|^2 (<= 0 up to rounding)
-            sum = fma(s_w[j], fast_exp2_neg(fmin(z, 0.0), s_tab), sum);
+            return fast_exp2_neg(fmin(z, 0.0), s_tab);
+        };
+        uint64_t j = 0;
+        for (; j + 4 <= len; j += 4) {  // four independent terms side by side, added in index order
+            const double e0 = kernel_value(j), e1 = kernel_value(j + 1), e2 = kernel_value(j + 2),
+                         e3 = kernel_value(j + 3);
+            sum = fma(s_w[j + 3], e3, fma(s_w[j + 2], e2, fma(s_w[j + 1], e1, fma(s_w[j], e0, sum))));
         }
+        for (; j < len; ++j) sum = fma(s_w[j], kernel_value(j), sum);
     }
     if (r < count) w_out[r] = 1.0 / sum;
 }
@@ -607,7 +625,7 @@ void weights_fast_device(vxb_ctx* ctx, uint32_t dim, uint64_t count, const doubl
                                                                     y_prev.as<double>());
     whiten_kernel<3><<<grid_for(count, 256), 256, 0, ctx->stream>>>(1, count, theta_new, chol_dev,
                                                                    y_new.as<double>());
-    abcsmc_weights_fast_kernel<3><<<grid_for(count, 128), 128, 0, ctx->stream>>>(
+    abcsmc_weights_fast_kernel<3><<<grid_for(count, kWeightsBlock), kWeightsBlock, 0, ctx->stream>>>(
         count, y_new.as<double>(), n_prev, y_prev.as<double>(), w_prev, ctx->log_table, w_out);
     check_launch("abcsmc_weights_fast_kernel");
 }
@@ -617,12 +635,12 @@ void weights_device(vxb_ctx* ctx, uint32_t dim, uint64_t count, const double* th
                     const double* chol_dev, double* w_out) {
     if (count == 0) return;
     LaunchScope scope(ctx, VXB_K_WEIGHTS);
-    const unsigned grid = grid_for(count, 128);
+    const unsigned grid = grid_for(count, kWeightsBlock);
     switch (dim) {
-        case 1: abcsmc_weights_kernel<1><<<grid, 128, 0, ctx->stream>>>(count, theta_new, n_prev, theta_prev, w_prev, chol_dev, w_out); break;
-        case 2: abcsmc_weights_kernel<2><<<grid, 128, 0, ctx->stream>>>(count, theta_new, n_prev, theta_prev, w_prev, chol_dev, w_out); break;
-        case 3: abcsmc_weights_kernel<3><<<grid, 128, 0, ctx->stream>>>(count, theta_new, n_prev, theta_prev, w_prev, chol_dev, w_out); break;
-        case 4: abcsmc_weights_kernel<4><<<grid, 128, 0, ctx->stream>>>(count, theta_new, n_prev, theta_prev, w_prev, chol_dev, w_out); break;
+        case 1: abcsmc_weights_kernel<1><<<grid, kWeightsBlock, 0, ctx->stream>>>(count, theta_new, n_prev, theta_prev, w_prev, chol_dev, w_out); break;
+        case 2: abcsmc_weights_kernel<2><<<grid, kWeightsBlock, 0, ctx->stream>>>(count, theta_new, n_prev, theta_prev, w_prev, chol_dev, w_out); break;
+        case 3: abcsmc_weights_kernel<3><<<grid, kWeightsBlock, 0, ctx->stream>>>(count, theta_new, n_prev, theta_prev, w_prev, chol_dev, w_out); break;
+        case 4: abcsmc_weights_kernel<4><<<grid, kWeightsBlock, 0, ctx->stream>>>(count, theta_new, n_prev, theta_prev, w_prev, chol_dev, w_out); break;
         default: raise("invalid-shape", "dimension out of range (1..4)");
     }
     check_launch("abcsmc_weights_kernel");

@@ -395,3 +395,30 @@ def sharded_counts(local_counts, group=None):
     if world > 1:
         allreduce_sum(local_counts, group)
     return local_counts
+
+
+def sharded_weak_info(ctx, cfg, group=None, evidence_fn=None):
+    """The weak-informativity test with the hyperparameter rows sharded over the
+    ranks (the reference's own task parallelism, weak_info.cpp:248-262): rank r
+    estimates the evidences of rows partition(K+1, world, 1)[r]; one all-gather of
+    the (rows x N x 2) evidence blocks (2.6 MB at the paper's size); every rank then
+    computes the same p-values and cut-offs.  Sampler seeds are keyed by (row,
+    dataset), so the table is identical for every world size.  `evidence_fn(first,
+    count)` replaces the device stage in the CPU tests."""
+    import torch
+    from . import lib
+    rank, world = _world(group)
+    rows = int(cfg.hyper_count) + 1
+    begin, end = shard_range(rows, world, rank)
+    lam = ctx.weak_info_lambdas(cfg) if ctx is not None else None
+    if evidence_fn is None:
+        mine = ctx.weak_info_evidence(cfg, lam, begin, end - begin)
+        dev = torch.device("cuda", ctx.device_info()["device"])
+    else:
+        mine = evidence_fn(begin, end - begin)
+        dev = torch.device("cpu")
+    block = torch.from_numpy(np.ascontiguousarray(mine)).to(dev)
+    (ev,), _ = allgather_rows([block], group)
+    ev = ev.cpu().numpy()
+    gamma, weakly, completed = lib.weak_info_cutoffs(cfg, ev)
+    return dict(lambda_=lam, gamma=gamma, weakly=weakly, completed=completed, evidence=ev)

@@ -79,6 +79,17 @@ def make_kernel(cov, scale, jitter=1e-10):
     return chol
 
 
+def weak_info_cutoffs(cfg, evidence):
+    """p-values, cut-offs and flags from the full evidence table (host side)."""
+    ev = np.ascontiguousarray(evidence, dtype=np.float64)
+    k = cfg.hyper_count + 1
+    gamma, weakly, completed = np.zeros(k), np.zeros(k, dtype=np.uint8), np.zeros(k, dtype=np.uint64)
+    rc = load().vxb_weak_info_cutoffs(C.byref(cfg), _ptr(ev), _ptr(gamma), _ptr(weakly), _ptr(completed))
+    if rc:
+        raise VxbError(load().vxb_last_error().decode())
+    return gamma, weakly, completed
+
+
 def partition(total, workers, block_width):
     r = np.zeros((workers, 2), dtype=np.uint64)
     rc = load().vxb_partition(u64(total), u64(workers), u64(block_width), _ptr(r))
@@ -454,6 +465,20 @@ class Context:
         self._check(self.lib.vxb_weak_info_test(self.handle, C.byref(cfg), _ptr(lam), _ptr(gamma),
                                                 _ptr(weakly), _ptr(completed), _ptr(ev)))
         return dict(lambda_=lam, gamma=gamma, weakly=weakly, completed=completed, evidence=ev)
+
+    def weak_info_lambdas(self, cfg):
+        lam = np.zeros((cfg.hyper_count + 1, 2))
+        self._check(self.lib.vxb_weak_info_lambdas(self.handle, C.byref(cfg), _ptr(lam)))
+        return lam
+
+    def weak_info_evidence(self, cfg, lam, first_row, n_rows, out=None):
+        """Evidences of rows [first_row, first_row + n_rows): n_rows x N x 2."""
+        lam = np.ascontiguousarray(lam, dtype=np.float64)
+        if out is None:
+            out = np.zeros((n_rows, cfg.datasets, 2))
+        self._check(self.lib.vxb_weak_info_evidence(self.handle, C.byref(cfg), _ptr(lam),
+                                                    u64(first_row), u64(n_rows), _ptr(out)))
+        return out
 
     # ---- tau-leap
     def mlmc_level(self, model, cfg, level, first, count, want_y=False):

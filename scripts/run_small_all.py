@@ -35,3 +35,10 @@ trho = torch.empty(296, dtype=torch.float64, device="cuda")
 ctx.abc_prior_predictive(tm, M.keying(1337), 296, 0, 296, tobs, rho=trho)
 ctx.synchronize()
 print("toggle", float(trho[0]))
+# annealed SMC: 8 020 sampler runs (K = 9, N = 401) of 500 particles
+wcfg = M.weakinfo_config(hyper_count=9, datasets=401, particles=500, seed=1337)
+print("weakinfo", ctx.weak_info_test(wcfg)["gamma"][:3])
+# TB Gillespie ABC: 4 000 paths at the reference's bench sizes
+tbm = M.tb_model(10, 10.0, 10000.0)
+tb_obs = ctx.simulate_at(M.tb_model(10, 10.0, 10000.0, attempts=64), M.TB_TRUE_THETA, lib.derive_seed(1337, [91]), 0, 0)
+print("tb", ctx.abc_prior_predictive_host(tbm, M.keying(1337), 4000, 0, 4000, tb_obs)[2][:2])

@@ -16,12 +16,11 @@ OUT = os.path.join(ROOT, "build_variants")
 
 VARIANTS = {
     "base": [],
-    "minblk4": ["-DVXB_SIM_MIN_BLOCKS=4"],
-    "minblk5": ["-DVXB_SIM_MIN_BLOCKS=5"],
-    "block128_min8": ["-DVXB_SIM_BLOCK=128", "-DVXB_SIM_MIN_BLOCKS=8"],
-    "block128_min10": ["-DVXB_SIM_BLOCK=128", "-DVXB_SIM_MIN_BLOCKS=10"],
-    "block512_min2": ["-DVXB_SIM_BLOCK=512", "-DVXB_SIM_MIN_BLOCKS=2"],
-    "block64_min16": ["-DVXB_SIM_BLOCK=64", "-DVXB_SIM_MIN_BLOCKS=16"],
+    "minblk3": ["-DVXB_SIM_MIN_BLOCKS=3"],
+    "block128_min5": ["-DVXB_SIM_BLOCK=128", "-DVXB_SIM_MIN_BLOCKS=5"],
+    "block128_min6": ["-DVXB_SIM_BLOCK=128", "-DVXB_SIM_MIN_BLOCKS=6"],
+    "block128_min3": ["-DVXB_SIM_BLOCK=128", "-DVXB_SIM_MIN_BLOCKS=3"],
+    "block64_min8": ["-DVXB_SIM_BLOCK=64", "-DVXB_SIM_MIN_BLOCKS=8"],
 }
 
 

@@ -140,3 +140,20 @@ def test_device_weak_info_table_equals_reference(ctx, oracle, gold):
     o = oracle.weak_info_test(6, 40, 128, alpha=0.1, seed=77, workers=8)
     for k in ("lambda_", "gamma", "weakly", "completed"):
         assert np.array_equal(t[k], o[k]), k
+
+
+@pytest.mark.gpu
+def test_device_weak_info_row_shards(ctx, gold):
+    """Evidences of row ranges equal the rows of the whole table (seeds are keyed by
+    row and dataset), so sharding hyperparameters over GPUs cannot change it."""
+    from paper_1902_09046_b200 import dist as D
+    for redraw in (False, True):
+        cfg = M.weakinfo_config(hyper_count=5, datasets=9, particles=128, seed=3, redraw_base=redraw)
+        whole = ctx.weak_info_test(cfg, want_evidence=True)
+        lam = ctx.weak_info_lambdas(cfg)
+        assert np.array_equal(lam, whole["lambda_"])
+        parts = [ctx.weak_info_evidence(cfg, lam, a, b - a) for a, b in ((0, 2), (2, 3), (3, 6))]
+        assert np.array_equal(np.concatenate(parts), whole["evidence"])
+        t = D.sharded_weak_info(ctx, cfg)
+        for k in ("gamma", "weakly", "completed"):
+            assert np.array_equal(t[k], whole[k])

@@ -217,3 +217,49 @@ def test_sharded_abcsmc_equals_single_run(tmp_path, oracle, world):
     got = D.sharded_abcsmc(OracleStages(oracle), m, cfg, obs)
     for k, v in want.items():
         assert np.array_equal(got[k], v), k
+
+
+# -------------------------------------------------- weak-informativity test
+def _fake_evidence(cfg):
+    """A deterministic stand-in for the device sampler: evidence of (row, dataset,
+    which) as a pure function of its indices, a few NaN (failed runs)."""
+    rows, n = cfg.hyper_count + 1, cfg.datasets
+    k, i, w = np.meshgrid(np.arange(rows), np.arange(n), np.arange(2), indexing="ij")
+    ev = np.sin(1.0 + 0.37 * k + 0.11 * i + 1.3 * w) * (1.0 + 0.05 * k)
+    ev[(k * 7 + i * 3 + w) % 23 == 0] = np.nan
+    return ev
+
+
+def _weakinfo_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = M.weakinfo_config(hyper_count=10, datasets=17, particles=64, alpha=0.1)
+    full = _fake_evidence(cfg)
+    t = D.sharded_weak_info(None, cfg, evidence_fn=lambda first, count: full[first:first + count])
+    np.savez(os.path.join(out_dir, f"wi{rank}.npz"), gamma=t["gamma"], weakly=t["weakly"],
+             completed=t["completed"], evidence=t["evidence"])
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_sharded_weak_info_rows(tmp_path, oracle):
+    """Rows sharded over 3 ranks, evidences all-gathered, cut-offs computed by the
+    library's host stage: equal to the unsharded table and to the oracle's
+    estimate_pvalues / compute_cutoff on the same evidences."""
+    from paper_1902_09046_b200 import lib
+    mp.spawn(_weakinfo_worker, args=(3, free_port(), str(tmp_path)), nprocs=3, join=True)
+    cfg = M.weakinfo_config(hyper_count=10, datasets=17, particles=64, alpha=0.1)
+    full = _fake_evidence(cfg)
+    gamma, weakly, completed = lib.weak_info_cutoffs(cfg, full)
+    for r in range(3):
+        z = np.load(tmp_path / f"wi{r}.npz")
+        assert np.array_equal(z["evidence"], full, equal_nan=True)
+        assert np.array_equal(z["gamma"], gamma) and np.array_equal(z["weakly"], weakly)
+        assert np.array_equal(z["completed"], completed)
+    for k in range(cfg.hyper_count + 1):
+        b, h = full[k, :, 0], full[k, :, 1]
+        pv = oracle.estimate_pvalues(b[~np.isnan(b)], h[~np.isnan(h)])
+        assert gamma[k] == oracle.compute_cutoff(pv, 0.1)
+        assert completed[k] == int((~np.isnan(b) & ~np.isnan(h)).sum())
+    assert np.array_equal(weakly, (np.arange(11) != 0) & (gamma > gamma[0]))
