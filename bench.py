@@ -85,13 +85,16 @@ class ClockSampler:
             self.error = repr(e)
 
     def __enter__(self):
+        if os.environ.get("VXB_BENCH_NO_CLOCKS"):   # diagnostics: is the sampler itself a cost?
+            return self
         self.thread = threading.Thread(target=self._run, daemon=True)
         self.thread.start()
         return self
 
     def __exit__(self, *exc):
         self.stop.set()
-        self.thread.join(timeout=2)
+        if self.thread is not None:
+            self.thread.join(timeout=2)
 
     def summary(self):
         if not self.sm:
@@ -231,8 +234,11 @@ def main():
         return float(ms.item()), out
 
     def device_step(model):
+        buffers = D.reject_buffers(ctx, model, n_total)   # reused by every step
+
         def fn(s):
-            return D.sharded_reject(ctx, model, M.keying(1337 + s), n_total, obs, eps)
+            return D.sharded_reject(ctx, model, M.keying(1337 + s), n_total, obs, eps,
+                                    buffers=buffers)
         return fn
 
     def host_step(model):

@@ -89,28 +89,39 @@ def allreduce_sum(t, group=None):
     return t
 
 
-def sharded_reject(ctx, model, key, n_total, observed, eps, cap_fraction=0.01, group=None):
+def reject_buffers(ctx, model, n_total, cap_fraction=0.01, group=None):
+    """Output buffers of sharded_reject for this rank's shard (idx, theta, rho of the
+    accepted rows at a fixed capacity, and the device-resident count), allocated on
+    the library's stream so that the caching allocator's reuse is ordered with the
+    kernels that fill them.  Reusable across steps."""
+    import torch
+    from . import _abi as A
+    rank, world = _world(group)
+    begin, end = shard_range(n_total, world, rank)
+    cap = max(1024, int((end - begin) * cap_fraction))
+    dev = torch.device("cuda", ctx.device_info()["device"])
+    real = torch.float32 if model.precision == A.VXB_F32 else torch.float64
+    with torch.cuda.stream(torch.cuda.ExternalStream(ctx.stream(), device=dev)):
+        return (torch.empty(cap, dtype=torch.int64, device=dev),
+                torch.empty((cap, model.dim), dtype=real, device=dev),
+                torch.empty(cap, dtype=real, device=dev),
+                torch.empty(1, dtype=torch.int64, device=dev))
+
+
+def sharded_reject(ctx, model, key, n_total, observed, eps, cap_fraction=0.01, group=None,
+                   buffers=None):
     """Config 1 on this rank's shard + the gather of accepted samples.
 
     Device-resident: outputs are torch CUDA tensors filled by the fused kernel
-    path; only the accepted rows travel."""
+    path; only the accepted rows travel.  `buffers` (reject_buffers) lets a caller
+    that steps repeatedly reuse the output tensors."""
     import torch
-    import torch.distributed as dist
-    from . import _abi as A
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank, world = _world(group)
     begin, end = shard_range(n_total, world, rank)
     count = end - begin
-    cap = max(1024, int(count * cap_fraction))
-    dev = torch.device("cuda", ctx.device_info()["device"])
-    real = torch.float32 if model.precision == A.VXB_F32 else torch.float64
-    # allocate on the library's stream so that the caching allocator's reuse of
-    # these buffers is ordered with the kernels that fill them
-    with torch.cuda.stream(torch.cuda.ExternalStream(ctx.stream(), device=dev)):
-        idx = torch.empty(cap, dtype=torch.int64, device=dev)
-        params = torch.empty((cap, model.dim), dtype=real, device=dev)
-        rho = torch.empty(cap, dtype=real, device=dev)
-        n_dev = torch.empty(1, dtype=torch.int64, device=dev)
+    idx, params, rho, n_dev = buffers if buffers is not None else \
+        reject_buffers(ctx, model, n_total, cap_fraction, group)
+    cap = int(idx.shape[0])
     # fully asynchronous: the accepted count stays on the device, the host only
     # enqueues (rows [0, count) of the buffers are valid once the stream drains)
     ctx.abc_reject(model, key, n_total, begin, count, observed, eps, cap, idx=idx,
@@ -119,6 +130,7 @@ def sharded_reject(ctx, model, key, n_total, observed, eps, cap_fraction=0.01, g
         return idx, params, rho, n_dev
     # the gather of accepted samples over NVLink, on the library's stream, padded to
     # the fixed capacity so that no rank has to read a count back first
+    dev = idx.device
     with torch.cuda.stream(torch.cuda.ExternalStream(ctx.stream(), device=dev)):
         return gather_accepted_padded(idx, params, rho, n_dev, group)
 
