@@ -80,7 +80,9 @@ logistic_abc_kernel(const __grid_constant__ AbcParams p) {
     auto emit = [summary](uint32_t k, Real v) {
         if (summary) summary[k] = v;
     };
-    using A = typename std::conditional<kFma, Fused, Exact>::type;
+    using A = typename std::conditional<
+        kFma, typename std::conditional<kRng == VXB_RNG_FAST && sizeof(Real) == 8, FusedCompact, Fused>::type,
+        Exact>::type;
     bool bad;
     Real rho;
     if (kRng == VXB_RNG_REF) {

@@ -175,13 +175,19 @@ struct ExternalNoise {
 };
 
 // One Euler-Maruyama step:  x + (a x)(1 - x/K) + (c x) z  with a = r dt,
-// c = sigma sqrt(dt), 1/K hoisted; evaluated ((x + drift) + diffusion).
+// c = sigma sqrt(dt), 1/K hoisted; evaluated ((x + drift) + diffusion) in the
+// exact mode; four FMAs in the FMA parity mode; fp64 throughput mode: the same
+// polynomial as x (A + B x + c z) with A = 1 + a and B = -a/K hoisted (two FMAs
+// and a multiply).
 template <class Real, class A>
-__device__ __forceinline__ Real logistic_step(Real x, Real a, Real c, Real inv_k, Real z) {
+__device__ __forceinline__ Real logistic_step(Real x, Real a, Real c, Real inv_k, Real z, Real a1,
+                                              Real bk) {
     if (A::kExact) {
         const Real drift = A::mul(A::mul(a, x), A::sub(Real(1), A::mul(x, inv_k)));
         const Real diff = A::mul(A::mul(c, x), z);
         return A::add(A::add(x, drift), diff);
+    } else if (A::kCompactStep) {
+        return x * A::mad(c, z, A::mad(bk, x, a1));
     } else {
         // x (1 + a (1 - x/K) + c z): same polynomial, four FMAs
         const Real sat = A::mad(-x, inv_k, Real(1));
@@ -204,6 +210,7 @@ __device__ __forceinline__ Real logistic_path(const LogisticModel& m, const doub
     const Real a = Exact::mul(r, static_cast<Real>(m.dt));
     const Real c = Exact::mul(sigma, static_cast<Real>(m.sqdt));
     const Real inv_k = Exact::div(Real(1), k);
+    const Real a1 = Real(1) + a, bk = -a * inv_k;  // throughput-mode form of the step
     Real x = static_cast<Real>(m.x0);
     Real ss = 0;
     uint32_t next = 0, since = 0;
@@ -229,7 +236,7 @@ __device__ __forceinline__ Real logistic_path(const LogisticModel& m, const doub
                 Real z[kB];
                 noise.next(z);
 #pragma unroll
-                for (uint32_t q = 0; q < kB; ++q) x = logistic_step<Real, A>(x, a, c, inv_k, z[q]);
+                for (uint32_t q = 0; q < kB; ++q) x = logistic_step<Real, A>(x, a, c, inv_k, z[q], a1, bk);
             }
             observe();
         }
@@ -241,12 +248,12 @@ __device__ __forceinline__ Real logistic_path(const LogisticModel& m, const doub
         noise.next(z);
         if (since + kB < stride) {  // no observation inside this batch (warp-uniform)
 #pragma unroll
-            for (uint32_t q = 0; q < kB; ++q) x = logistic_step<Real, A>(x, a, c, inv_k, z[q]);
+            for (uint32_t q = 0; q < kB; ++q) x = logistic_step<Real, A>(x, a, c, inv_k, z[q], a1, bk);
             since += kB;
         } else {
 #pragma unroll
             for (uint32_t q = 0; q < kB; ++q) {
-                x = logistic_step<Real, A>(x, a, c, inv_k, z[q]);
+                x = logistic_step<Real, A>(x, a, c, inv_k, z[q], a1, bk);
                 if (++since == stride) observe();
             }
         }
@@ -255,7 +262,7 @@ __device__ __forceinline__ Real logistic_path(const LogisticModel& m, const doub
         Real z[kB];
         noise.next(z);
         for (uint32_t q = 0; j + q < steps; ++q) {
-            x = logistic_step<Real, A>(x, a, c, inv_k, z[q]);
+            x = logistic_step<Real, A>(x, a, c, inv_k, z[q], a1, bk);
             if (++since == stride) observe();
         }
     }

@@ -494,7 +494,7 @@ abcsmc_propose_fast_kernel(const __grid_constant__ ProposeFastParams pp) {
         FastNoise64 noise(pp.fast, s_tab, rl, rh, 0u, kDomNoise | (pp.gen << 8));
         bool bad;
         auto emit = [](uint32_t, double) {};
-        rho = logistic_path<double, Fused>(p.model, th, p.observed, noise, emit, bad);
+        rho = logistic_path<double, FusedCompact>(p.model, th, p.observed, noise, emit, bad);
         if (bad) {
             rho = __longlong_as_double(0x7FF8000000000000LL);
             flag = 3;
