@@ -14,7 +14,7 @@
 // K = N = 400, N_p = 500 => 320 800 runs).  The reference spreads hyperparameters
 // over threads and runs each sampler serially; here ONE CTA owns one run for its
 // whole life: the ensemble (theta, log w, log L, log prior) lives in shared
-// memory, the temperature bisection, evidence update, ESS, cumulative weights and
+// memory (six arrays of N_p doubles), the temperature bisection, evidence update, ESS, cumulative weights and
 // covariance are block reductions / scans, and the tempered random-walk moves run
 // one particle per thread with every variate addressed at the reference's stream
 // position (smc.cpp:66-76), so proposals and accept decisions replay the
@@ -92,83 +92,85 @@ __device__ __forceinline__ double log_prior(const RunModel& m, double b0, double
 }
 
 // ------------------------------------------------------------ block collectives
+// One __syncthreads per reduction: warp results go to one of two alternating
+// slots (so the next reduction cannot overwrite values a slow warp is still
+// reading), and every thread finishes the reduction itself in warp order -- the
+// result is the same value in every thread, a pure function of the inputs.
+constexpr int kAnnealWarps = kAnnealBlock / 32;
 struct BlockScratch {
-    double a[kAnnealBlock / 32], b[kAnnealBlock / 32];
-    double out_a, out_b;
-    unsigned long long count;
-    int flag;
+    double a[2][kAnnealWarps], b[2][kAnnealWarps];
+    double scan[kAnnealWarps];  // warp totals of the cumulative-weight scan
+    unsigned long long count;   // accepted proposals of a sweep
 };
-
-__device__ __forceinline__ double block_max(double v, BlockScratch& s) {
-    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if ((threadIdx.x & 31) == 0) s.a[threadIdx.x >> 5] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double m = s.a[0];
-        for (int w = 1; w < kAnnealBlock / 32; ++w) m = fmax(m, s.a[w]);
-        s.out_a = m;
+struct Reducer {
+    BlockScratch& s;
+    int phase = 0;
+    __device__ __forceinline__ double max(double v) {
+        for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if ((threadIdx.x & 31) == 0) s.a[phase][threadIdx.x >> 5] = v;
+        __syncthreads();
+        double m = s.a[phase][0];
+#pragma unroll
+        for (int w = 1; w < kAnnealWarps; ++w) m = fmax(m, s.a[phase][w]);
+        phase ^= 1;
+        return m;
     }
-    __syncthreads();
-    const double r = s.out_a;
-    __syncthreads();
-    return r;
-}
-// two sums at once (fixed order: strided partials, shuffle tree, warps left to right)
-__device__ __forceinline__ void block_sum2(double& x, double& y, BlockScratch& s) {
-    for (int o = 16; o > 0; o >>= 1) {
-        x += __shfl_xor_sync(0xffffffffu, x, o);
-        y += __shfl_xor_sync(0xffffffffu, y, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        s.a[threadIdx.x >> 5] = x;
-        s.b[threadIdx.x >> 5] = y;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double p = 0.0, q = 0.0;
-        for (int w = 0; w < kAnnealBlock / 32; ++w) {
-            p += s.a[w];
-            q += s.b[w];
+    // two sums at once (fixed order: strided partials, shuffle tree, warps left to right)
+    __device__ __forceinline__ void sum2(double& x, double& y) {
+        for (int o = 16; o > 0; o >>= 1) {
+            x += __shfl_xor_sync(0xffffffffu, x, o);
+            y += __shfl_xor_sync(0xffffffffu, y, o);
         }
-        s.out_a = p;
-        s.out_b = q;
+        if ((threadIdx.x & 31) == 0) {
+            s.a[phase][threadIdx.x >> 5] = x;
+            s.b[phase][threadIdx.x >> 5] = y;
+        }
+        __syncthreads();
+        double p = 0.0, q = 0.0;
+#pragma unroll
+        for (int w = 0; w < kAnnealWarps; ++w) {
+            p += s.a[phase][w];
+            q += s.b[phase][w];
+        }
+        x = p;
+        y = q;
+        phase ^= 1;
     }
-    __syncthreads();
-    x = s.out_a;
-    y = s.out_b;
-    __syncthreads();
-}
+};
 
 struct Ensemble {  // views into dynamic shared memory, np entries each
     double *t0, *t1, *lw, *ll, *lp;  // current
-    double *u0, *u1, *ul, *up;       // resampling target (ping-pong)
-    double* cum;
+    double* cum;                     // cumulative weights; staging row of the resampling gather
 };
 
-// reweighted ESS at temperature increment dt: smc.cpp:226-239
-__device__ double ess_after(const Ensemble& e, uint32_t np, double dt, BlockScratch& s) {
-    double top = -INFINITY;
-    for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) top = fmax(top, fma(dt, e.ll[i], e.lw[i]));
-    top = block_max(top, s);
+// Reweighted ESS at temperature increment dt >= 0 (smc.cpp:226-239) for an ensemble
+// whose log weights are all equal to lw0 -- true whenever the sampler looks for a
+// temperature, because it resamples every iteration.  x -> fl(lw0 + dt x) is
+// monotone, so the reference's max_i (lw_i + dt ll_i) is fl(lw0 + dt max_i ll_i):
+// the maximum of the log likelihoods is taken once per iteration, not once per
+// bisection step.
+__device__ double ess_after(const Ensemble& e, uint32_t np, double dt, double lw0, double ll_max,
+                            Reducer& red) {
+    const double top = fma(dt, ll_max, lw0);
     if (top == -INFINITY) return 0.0;
     double s1 = 0.0, s2 = 0.0;
     for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) {
-        const double w = exp(fma(dt, e.ll[i], e.lw[i]) - top);
+        const double w = exp(fma(dt, e.ll[i], lw0) - top);
         s1 += w;
         s2 = fma(w, w, s2);
     }
-    block_sum2(s1, s2, s);
+    red.sum2(s1, s2);
     return s1 * s1 / s2;
 }
 // logsumexp: numeric.cpp:11-18
-__device__ double block_logsumexp(const double* x, uint32_t np, BlockScratch& s) {
+__device__ double block_logsumexp(const double* x, uint32_t np, Reducer& red) {
     double top = -INFINITY;
     for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) top = fmax(top, x[i]);
-    top = block_max(top, s);
+    top = red.max(top);
     if (!isfinite(top)) return top;
     double acc = 0.0, unused = 0.0;
     for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) acc += exp(x[i] - top);
-    block_sum2(acc, unused, s);
+    red.sum2(acc, unused);
     return top + log(acc);
 }
 
@@ -230,9 +232,10 @@ __device__ uint32_t sweep(const Design& d, const RunModel& m, Ensemble& e, uint3
     return accepted;
 }
 
-__global__ void __launch_bounds__(kAnnealBlock) anneal_kernel(const __grid_constant__ AnnealParams p) {
+__global__ void __launch_bounds__(kAnnealBlock, 6) anneal_kernel(const __grid_constant__ AnnealParams p) {
     extern __shared__ double smem[];
     __shared__ BlockScratch scratch;
+    Reducer red{scratch};
     __shared__ RunModel model;
     const uint64_t run = blockIdx.x;
     const uint32_t np = p.np;
@@ -242,11 +245,7 @@ __global__ void __launch_bounds__(kAnnealBlock) anneal_kernel(const __grid_const
     e.lw = e.t1 + np;
     e.ll = e.lw + np;
     e.lp = e.ll + np;
-    e.u0 = e.lp + np;
-    e.u1 = e.u0 + np;
-    e.ul = e.u1 + np;
-    e.up = e.ul + np;
-    e.cum = e.up + np;
+    e.cum = e.lp + np;
     const Design& d = p.design;
 
     if (threadIdx.x == 0) {
@@ -302,28 +301,31 @@ __global__ void __launch_bounds__(kAnnealBlock) anneal_kernel(const __grid_const
         double t_next = 1.0;
         {
             const double room = 1.0 - temperature;
-            if (!(ess_after(e, np, room, scratch) >= half)) {
+            double ll_max = -INFINITY;
+            for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) ll_max = fmax(ll_max, e.ll[i]);
+            ll_max = red.max(ll_max);
+            if (!(ess_after(e, np, room, p.neg_log_np, ll_max, red) >= half)) {
                 double lo = 0.0, hi = room;
                 while (hi - lo > kBisectionTol) {
                     const double mid = 0.5 * (lo + hi);
-                    if (ess_after(e, np, mid, scratch) >= half) lo = mid; else hi = mid;
+                    if (ess_after(e, np, mid, p.neg_log_np, ll_max, red) >= half) lo = mid; else hi = mid;
                 }
                 t_next = temperature + 0.5 * (lo + hi);
             }
         }
         // ---- reweight_and_update_evidence (smc.cpp:255-266)
         {
-            const double before = block_logsumexp(e.lw, np, scratch);
+            const double before = block_logsumexp(e.lw, np, red);
             const double dt = t_next - temperature;
             for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) e.lw[i] = fma(dt, e.ll[i], e.lw[i]);
             __syncthreads();
-            log_evidence += block_logsumexp(e.lw, np, scratch) - before;
+            log_evidence += block_logsumexp(e.lw, np, red) - before;
             temperature = t_next;
         }
         // ---- ess (trace only) and cumulative weights (smc.cpp:208-219, 268-283)
         double top = -INFINITY;
         for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) top = fmax(top, e.lw[i]);
-        top = block_max(top, scratch);
+        top = red.max(top);
         if (top == -INFINITY) {
             status = kRunDegenerate;
             break;
@@ -346,14 +348,14 @@ __global__ void __launch_bounds__(kAnnealBlock) anneal_kernel(const __grid_const
                 const double up = __shfl_up_sync(0xffffffffu, incl, o);
                 if ((threadIdx.x & 31) >= o) incl += up;
             }
-            if ((threadIdx.x & 31) == 31) scratch.a[threadIdx.x >> 5] = incl;
+            if ((threadIdx.x & 31) == 31) scratch.scan[threadIdx.x >> 5] = incl;
             __syncthreads();
             double offset = incl - run_sum;
-            for (int w = 0; w < (threadIdx.x >> 5); ++w) offset += scratch.a[w];
+            for (int w = 0; w < (threadIdx.x >> 5); ++w) offset += scratch.scan[w];
             __syncthreads();
             for (uint32_t i = i0; i < i1; ++i) e.cum[i] += offset;
             double s1 = run_sum;
-            block_sum2(s1, sq, scratch);
+            red.sum2(s1, sq);
             ess_now = s1 * s1 / sq;
         }
         __syncthreads();
@@ -365,6 +367,8 @@ __global__ void __launch_bounds__(kAnnealBlock) anneal_kernel(const __grid_const
         // ---- resample_multinomial draws (smc.cpp:285-299): draw i = position i of the coordinator stream
         {
             const uint64_t key = key_of(n, kRoleCoordinator);
+            // ancestor indices are parked in the log-weight array (reset right after)
+            uint32_t* const anc = reinterpret_cast<uint32_t*>(e.lw);
             for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) {
                 const Words w = philox2x64(key, i >> 1);
                 const double target = __dmul_rn(to_unit((i & 1) ? w.w1 : w.w0), total);
@@ -373,18 +377,19 @@ __global__ void __launch_bounds__(kAnnealBlock) anneal_kernel(const __grid_const
                     const uint32_t mid = lo + ((hi - lo) >> 1);
                     if (target < e.cum[mid]) hi = mid; else lo = mid + 1;
                 }
-                const uint32_t a = lo >= np ? np - 1 : lo;
-                e.u0[i] = e.t0[a];
-                e.u1[i] = e.t1[a];
-                e.ul[i] = e.ll[a];
-                e.up[i] = e.lp[a];
+                anc[i] = lo >= np ? np - 1 : lo;
             }
             __syncthreads();
-            double* t;
-            t = e.t0; e.t0 = e.u0; e.u0 = t;
-            t = e.t1; e.t1 = e.u1; e.u1 = t;
-            t = e.ll; e.ll = e.ul; e.ul = t;
-            t = e.lp; e.lp = e.up; e.up = t;
+            // gather the cached rows one array at a time through `cum` (free once the
+            // ancestors are known): thread i reads X[anc[i]], all threads meet, thread i
+            // writes X[i]
+            double* const rows[4] = {e.t0, e.t1, e.ll, e.lp};
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) e.cum[i] = rows[r][anc[i]];
+                __syncthreads();
+                for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) rows[r][i] = e.cum[i];
+            }
             for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) e.lw[i] = p.neg_log_np;
         }
         // ---- make_kernel: sample covariance + Cholesky + jitter (numeric.cpp:55-96, smc.cpp:311-325)
@@ -395,7 +400,7 @@ __global__ void __launch_bounds__(kAnnealBlock) anneal_kernel(const __grid_const
                 m0 += e.t0[i];
                 m1 += e.t1[i];
             }
-            block_sum2(m0, m1, scratch);
+            red.sum2(m0, m1);
             m0 /= static_cast<double>(np);
             m1 /= static_cast<double>(np);
             double c00 = 0.0, c10 = 0.0, c11 = 0.0, unused = 0.0;
@@ -405,8 +410,8 @@ __global__ void __launch_bounds__(kAnnealBlock) anneal_kernel(const __grid_const
                 c10 = fma(d1, d0, c10);
                 c11 = fma(d1, d1, c11);
             }
-            block_sum2(c00, c10, scratch);
-            block_sum2(c11, unused, scratch);
+            red.sum2(c00, c10);
+            red.sum2(c11, unused);
             const double norm = 1.0 / static_cast<double>(np - 1);
             c00 *= norm;
             c10 *= norm;
@@ -645,7 +650,7 @@ static void anneal_device(vxb_ctx* ctx, const Design& design, uint64_t n_runs, u
     p.status = status;
     p.trace = trace;
     p.trace_rows = trace_rows;
-    const size_t smem = particles * 10 * sizeof(double);
+    const size_t smem = particles * 6 * sizeof(double);
     VXB_CUDA(cudaFuncSetAttribute(anneal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     {
