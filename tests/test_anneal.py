@@ -157,3 +157,31 @@ def test_device_weak_info_row_shards(ctx, gold):
         t = D.sharded_weak_info(ctx, cfg)
         for k in ("gamma", "weakly", "completed"):
             assert np.array_equal(t[k], whole[k])
+
+
+@pytest.mark.gpu
+def test_device_sampler_other_designs_and_sizes(ctx, oracle):
+    """Designs with large groups (device-side binomial table), other group counts,
+    particle counts that are not multiples of the CTA size, near-degenerate priors."""
+    rs = np.random.RandomState(12)
+    for dose, size, npart in (((-1.0, 0.0, 0.5), (40, 12, 9), 333), ((0.2,), (7,), 64),
+                              ((-2.0, -1.0, 0.0, 1.0, 2.0, 3.0), (3, 3, 3, 3, 3, 3), 1000)):
+        n = 10
+        lam = np.stack([rs.uniform(0.05, 10.0, n), rs.uniform(0.05, 20.0, n)], axis=1)
+        seeds = rs.randint(0, 2 ** 62, size=n).astype(np.uint64)
+        theta, deaths = ctx.bioassay_sample(lam, seeds, dose, size)
+        res = ctx.smc_bioassay(dose, size, deaths, lam, seeds + np.uint64(1), npart, trace_rows=6)
+        for j in range(n):
+            th, y = oracle.bioassay_sample(lam[j, 0], lam[j, 1], dose, size, int(seeds[j]))
+            assert np.array_equal(theta[j], th) and np.array_equal(deaths[j], y)
+            ev, it, tr = oracle.smc_bioassay(dose, size, y, lam[j, 0], lam[j, 1], npart, 4, 0.01, G.H,
+                                             int(seeds[j]) + 1, True)
+            assert res["status"][j] == 0 and res["iterations"][j] == it
+            assert abs(res["log_evidence"][j] - ev) < 1e-9
+            k = min(it, 6)
+            assert np.array_equal(res["trace"][j, :k, 2:], tr[:k, 2:])
+    # the whole test on a non-default design
+    cfg = M.weakinfo_config(hyper_count=3, datasets=10, particles=96, seed=5, dose=(-1.0, 0.0, 0.5),
+                            group_size=(8, 4, 6))
+    t = ctx.weak_info_test(cfg)
+    assert np.isfinite(t["gamma"]).all() and (t["completed"] == 10).all()

@@ -344,3 +344,22 @@ def test_tb_gillespie_parity(ctx, oracle):
     with pytest.raises(lib.VxbError) as e:
         ctx.abc_prior_predictive_host(m, M.keying(1, A.VXB_KEY_WORKER, 2, 4), 8, 0, 8, obs)
     assert e.value.code == "invalid-argument"
+
+
+def test_tb_gillespie_edge_cases(ctx, oracle):
+    """Stop rules that end a path before its first event, an unbounded horizon with a
+    small case target, and a target at the device limit."""
+    inf = float("inf")
+    for initial, horizon, target, n in ((50, 10.0, 20.0, 32), (5, inf, 300.0, 64), (1, 0.0, 1000.0, 16),
+                                        (20, 3.0, 60000.0, 24)):
+        mm = M.tb_model(initial, horizon, target)
+        want = oracle.tb_abc_particle(initial, horizon, target, 3, n, 2024, [5.0, 0.5])
+        got = ctx.abc_prior_predictive_host(mm, M.keying(2024), n + 3, 3, n, np.array([5.0, 0.5]))
+        for g, w in zip(got, want):
+            assert eq(g, w), (initial, horizon, target)
+    with pytest.raises(lib.VxbError) as e:
+        ctx.abc_prior_predictive_host(M.tb_model(10, 10.0, 1e6), M.keying(1), 4, 0, 4, np.zeros(2))
+    assert e.value.code == "invalid-argument"
+    with pytest.raises(lib.VxbError) as e:
+        ctx.abc_prior_predictive_host(M.tb_model(0, 10.0, 100.0), M.keying(1), 4, 0, 4, np.zeros(2))
+    assert e.value.code == "invalid-shape"
