@@ -16,7 +16,7 @@
 #include <cmath>
 
 #include "vxb_common.cuh"
-#include "vxb_rng.cuh"
+#include "vxb_logistic.cuh"
 
 namespace vxb {
 
@@ -71,16 +71,34 @@ __global__ void __launch_bounds__(kPppBlock) ppp_kernel(const __grid_constant__ 
             }
             ybar = __ddiv_rn(sum, dn);
         } else {
+            // throughput generator: batches of eight normals from three Philox blocks,
+            // drawn one batch ahead (FastNoise64); normal 0 is the prior draw, normals
+            // 1..n the data
             const uint32_t jl = static_cast<uint32_t>(j), jh = static_cast<uint32_t>(j >> 32);
-            const uint32_t dom = kDomNoise | (k << 8);
-            double z0, z1;
-            fast_box_muller(philox4x32(p.fast, 0u, dom, jl, jh), s_log, z0, z1);
-            const double theta = lambda * z0;
+            FastNoise64 noise(p.fast, s_log, jl, jh, 0u, kDomNoise | (k << 8));
+            double z[8];
+            noise.next(z);
+            const double theta = lambda * z[0];
             double s0 = 0.0, s1 = 0.0;
-            for (uint32_t q = 1; q <= pairs; ++q) {
-                fast_box_muller(philox4x32(p.fast, q, dom, jl, jh), s_log, z0, z1);
-                s0 += z0;
-                s1 += (2 * q <= p.n_data) ? z1 : 0.0;
+            uint32_t left = p.n_data;
+#pragma unroll
+            for (int q = 1; q < 8; ++q) {
+                if (left) {
+                    (q & 1 ? s1 : s0) += z[q];
+                    --left;
+                }
+            }
+            while (left >= 8) {
+                noise.next(z);
+                s0 += (z[0] + z[2]) + (z[4] + z[6]);
+                s1 += (z[1] + z[3]) + (z[5] + z[7]);
+                left -= 8;
+            }
+            if (left) {
+                noise.next(z);
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (static_cast<uint32_t>(q) < left) (q & 1 ? s1 : s0) += z[q];
             }
             ybar = theta + (s0 + s1) / dn;
         }

@@ -18,3 +18,15 @@ ncu -i gpurun_out/prof_logistic_v2.ncu-rep --page source --csv > gpurun_out/sour
 ls -la gpurun_out/*.ncu-rep
 rm -f gpurun_out/prof_others_v2.ncu-rep
 find gpurun_out -name 'prof_logistic_v2.ncu-rep' -size +30M -delete
+# SURVEY 8f kernels (toggle, annealed SMC, TB)
+$CMD2 > gpurun_out/small_plain2.log 2>&1 &&
+ncu --set full --clock-control none --import-source on -k regex:'anneal_kernel|tb_abc_kernel|toggle_abc' -c 6 -o gpurun_out/prof_next_v2 -f $CMD2 > gpurun_out/ncu_next.log 2>&1
+python scripts/summarize_ncu.py gpurun_out/prof_next_v2.ncu-rep gpurun_out/sum_next_v2
+rm -f gpurun_out/prof_next_v2.ncu-rep
+# the three instances of the headline kernel
+CMD3="python scripts/time_kernels.py 2e6"
+$CMD3 > gpurun_out/plain_tk.log 2>&1 &&
+ncu --set full --clock-control none -k regex:logistic_abc -c 10 -o gpurun_out/prof_variants_v2 -f $CMD3 > gpurun_out/ncu_tk.log 2>&1
+python scripts/summarize_ncu.py gpurun_out/prof_variants_v2.ncu-rep gpurun_out/sum_variants_v2
+rm -f gpurun_out/prof_variants_v2.ncu-rep
+du -sh gpurun_out
