@@ -14,6 +14,11 @@
 //   smc::ess / resample_multinomial            (vexbayes/smc.hpp)
 //   weakinfo::estimate_pvalues / compute_cutoff(vexbayes/weak_info.hpp)
 //   toggle::make_abc_model                     (vexbayes/toggle_switch.hpp)
+//   smc::run_smc, weakinfo::make_bioassay_model / sample_prior_predictive /
+//   run_weak_info_test / write_csv             (vexbayes/smc.hpp, weak_info.hpp)
+//   tb::gillespie_simulate / tb_summaries / make_abc_model (vexbayes/tb_model.hpp)
+//   abc::write_csv, bench::write_csv / amdahl_bound / tb_observed_summaries
+//                                              (vexbayes/abc.hpp, bench.hpp)
 //
 // The workloads of BASELINE.json that the reference does not contain (the
 // logistic SDE, the normal-mean p-value) are expressed here as ModelHooks /

@@ -9,11 +9,14 @@
 // reference's flags, proj/CMakeLists.txt:15-18 -- per-operation IEEE rounding,
 // no FMA contraction).
 //
-// Pinning (tests/test_oracle_pins.py): the RNG, fastmath, numeric, partition,
-// ABC sampler, epsilon selection, resampling, ESS and p-value counting are
-// checked bit-for-bit against oracle/_ref (the unmodified reference compiled
-// from /root/reference) where that library is present, and everywhere against
-// the golden vectors it generated (tests/golden/, script tests/golden/make_golden.py).
+// Pinning (tests/test_oracle_pins.py, tests/test_anneal.py): the RNG, fastmath,
+// numeric, partition, ABC sampler, epsilon selection, resampling, ESS, p-value
+// counting, the toggle-switch model, the bioassay model with the likelihood-
+// annealed sampler (smc::run_smc) and run_weak_info_test, and the TB Gillespie
+// model are checked bit-for-bit against oracle/_ref (the unmodified reference
+// compiled from /root/reference) where that library is present, and everywhere
+// against the golden vectors it generated (tests/golden/, scripts
+// tests/golden/make_golden*.py).
 // Workloads the reference does not contain -- ABC-SMC generation loop, weighted
 // covariance, Poisson variates, tau-leap and its MLMC coupling -- are
 // "parity unpinned": they are defined HERE and anchored by
