@@ -153,25 +153,47 @@ template <class Real>
 __device__ __forceinline__ bool row_accepted(const Real* rho, const uint8_t* failed, uint64_t i,
                                              uint64_t n, double eps) {
     // compared in double so that an fp32 rho is tested against the unrounded
-    // epsilon, as the host rule does; NaN compares false
-    return i < n && !(failed && failed[i]) && static_cast<double>(rho[i]) <= eps;
+    // epsilon, as the host rule does; NaN compares false.  Both loads are issued
+    // unconditionally (no short-circuit between them): a streaming pass wants every
+    // load of a thread in flight at once, not a flag load followed by a dependent
+    // value load.
+    const bool inside = i < n;
+    const uint8_t flag = (inside && failed) ? __ldg(failed + i) : uint8_t(0);
+    const Real value = inside ? __ldg(rho + i) : Real(0);
+    return inside & (flag == 0) & (static_cast<double>(value) <= eps);
 }
 
+// Row of (warp, pass s, lane) inside a block tile: every warp owns 32*kSelItems
+// consecutive rows and sweeps them in kSelItems coalesced passes, so that the
+// ascending order inside a warp is (pass, lane) and no block-wide exchange is
+// needed per pass.  All kSelItems loads of a thread are independent and in flight
+// together: the kernels are HBM-bound streaming passes.
+__device__ __forceinline__ uint64_t tile_row(uint64_t tile0, unsigned warp, int s, unsigned lane) {
+    return tile0 + static_cast<uint64_t>(warp) * (32 * kSelItems) + static_cast<uint64_t>(s) * 32 + lane;
+}
+
+// Pass 1 (the only pass over rho): per-block accept counts, and every thread's
+// accept flags (bit s = pass s; one bit per row, n/8 bytes) so that the write pass
+// never has to read the 8-9 B/row again.
 template <class Real>
-__global__ void __launch_bounds__(kSelBlock)
+__global__ void __launch_bounds__(kSelBlock, 8)
 accept_count_kernel(const Real* __restrict__ rho, const uint8_t* __restrict__ failed, uint64_t n,
-                    double eps, unsigned int* __restrict__ block_counts) {
+                    double eps, unsigned int* __restrict__ block_counts,
+                    unsigned short* __restrict__ thread_flags /* n_blocks x kSelBlock, optional */) {
+    static_assert(kSelItems <= 16, "flags are stored as 16 bits per thread");
     const uint64_t tile0 = static_cast<uint64_t>(blockIdx.x) * kSelBlock * kSelItems;
-    unsigned c = 0;
-#pragma unroll 4
-    for (int s = 0; s < kSelItems; ++s)
-        c += row_accepted(rho, failed, tile0 + static_cast<uint64_t>(s) * kSelBlock + threadIdx.x,
-                          n, eps)
-                 ? 1u
-                 : 0u;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned flags = 0;
+#pragma unroll
+    for (int s = 0; s < kSelItems; ++s)  // all loads of the thread in flight together
+        flags |= (row_accepted(rho, failed, tile_row(tile0, warp, s, lane), n, eps) ? 1u : 0u) << s;
+    if (thread_flags)
+        thread_flags[static_cast<uint64_t>(blockIdx.x) * kSelBlock + threadIdx.x] =
+            static_cast<unsigned short>(flags);
+    unsigned c = __popc(flags);
     for (int o = 16; o; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
     __shared__ unsigned int warp_sum[kSelBlock / 32];
-    if ((threadIdx.x & 31) == 0) warp_sum[threadIdx.x >> 5] = c;
+    if (lane == 0) warp_sum[warp] = c;
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned t = 0;
@@ -217,36 +239,33 @@ scan_blocks_kernel(const unsigned int* __restrict__ counts, uint64_t n_blocks,
     if (threadIdx.x == 0) *total = carry;
 }
 
-template <class Real>
+// Pass 2: ascending indices of the accepted rows from the stored flags (n/8 bytes
+// read) and the scanned block offsets: warp ballots of each pass give the order
+// (pass, lane) inside a warp.
 __global__ void __launch_bounds__(kSelBlock)
-accept_write_kernel(const Real* __restrict__ rho, const uint8_t* __restrict__ failed, uint64_t n,
-                    double eps, const unsigned long long* __restrict__ offsets, uint64_t index_base,
-                    uint64_t cap, uint64_t* __restrict__ idx) {
+accept_write_kernel(const unsigned short* __restrict__ thread_flags,
+                    const unsigned long long* __restrict__ offsets, uint64_t index_base, uint64_t cap,
+                    uint64_t* __restrict__ idx) {
     __shared__ unsigned int warp_cnt[kSelBlock / 32];
-    __shared__ unsigned long long run;
     const uint64_t tile0 = static_cast<uint64_t>(blockIdx.x) * kSelBlock * kSelItems;
-    if (threadIdx.x == 0) run = offsets[blockIdx.x];
-    __syncthreads();
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned flags = thread_flags[static_cast<uint64_t>(blockIdx.x) * kSelBlock + threadIdx.x];
+    unsigned mine = __popc(flags);
+    for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if (lane == 0) warp_cnt[warp] = mine;
+    __syncthreads();
+    if (mine == 0) return;  // nothing accepted in this warp's rows (the common case)
+    unsigned long long dst = offsets[blockIdx.x];
+    for (unsigned w = 0; w < warp; ++w) dst += warp_cnt[w];
+    const unsigned below = (1u << lane) - 1;
+#pragma unroll
     for (int s = 0; s < kSelItems; ++s) {
-        const uint64_t i = tile0 + static_cast<uint64_t>(s) * kSelBlock + threadIdx.x;
-        const bool acc = row_accepted(rho, failed, i, n, eps);
-        const unsigned ballot = __ballot_sync(0xffffffffu, acc);
-        if (lane == 0) warp_cnt[warp] = __popc(ballot);
-        __syncthreads();
-        unsigned before = 0, total = 0;
-        for (int w = 0; w < kSelBlock / 32; ++w) {
-            const unsigned c = warp_cnt[w];
-            before += w < static_cast<int>(warp) ? c : 0;
-            total += c;
+        const unsigned ballot = __ballot_sync(0xffffffffu, (flags >> s) & 1u);
+        if ((flags >> s) & 1u) {
+            const unsigned long long at = dst + __popc(ballot & below);
+            if (at < cap) idx[at] = tile_row(tile0, warp, s, lane) + index_base;
         }
-        if (acc) {
-            const unsigned long long dst = run + before + __popc(ballot & ((1u << lane) - 1));
-            if (dst < cap) idx[dst] = i + index_base;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) run += total;
-        __syncthreads();
+        dst += __popc(ballot);
     }
 }
 
@@ -329,11 +348,14 @@ void compact_device_t(vxb_ctx* ctx, const Real* rho, const uint8_t* failed, uint
     }
     Scratch d_counts(ctx, n_blocks * sizeof(unsigned int));
     Scratch d_offsets(ctx, n_blocks * sizeof(unsigned long long));
+    const bool want_idx = idx_dev && cap;
+    Scratch d_flags(ctx, want_idx ? n_blocks * kSelBlock * sizeof(unsigned short) : 0);
     Scratch d_total(ctx, sizeof(unsigned long long));
     {
         LaunchScope scope(ctx, VXB_K_COMPACT);
         accept_count_kernel<Real><<<static_cast<unsigned>(n_blocks), kSelBlock, 0, ctx->stream>>>(
-            rho, failed, n, eps, d_counts.as<unsigned int>());
+            rho, failed, n, eps, d_counts.as<unsigned int>(),
+            want_idx ? d_flags.as<unsigned short>() : nullptr);
         check_launch("accept_count_kernel");
     }
     {
@@ -343,10 +365,10 @@ void compact_device_t(vxb_ctx* ctx, const Real* rho, const uint8_t* failed, uint
                                                         d_total.as<unsigned long long>());
         check_launch("scan_blocks_kernel");
     }
-    if (idx_dev && cap) {
+    if (want_idx) {
         LaunchScope scope(ctx, VXB_K_COMPACT);
-        accept_write_kernel<Real><<<static_cast<unsigned>(n_blocks), kSelBlock, 0, ctx->stream>>>(
-            rho, failed, n, eps, d_offsets.as<unsigned long long>(), index_base, cap, idx_dev);
+        accept_write_kernel<<<static_cast<unsigned>(n_blocks), kSelBlock, 0, ctx->stream>>>(
+            d_flags.as<unsigned short>(), d_offsets.as<unsigned long long>(), index_base, cap, idx_dev);
         check_launch("accept_write_kernel");
     }
     if (is_device_pointer(n_accepted_host)) {
