@@ -50,9 +50,14 @@ __host__ inline float key_to_float(uint64_t k64) {
     return v;
 }
 
+// flag and value are loaded unconditionally (two independent loads, no
+// short-circuit between them)
 template <class Real>
-__device__ __forceinline__ bool row_valid(const Real* rho, const uint8_t* failed, uint64_t i) {
-    return !(failed && failed[i]) && !isnan(rho[i]);
+__device__ __forceinline__ bool row_valid(const Real* rho, const uint8_t* failed, uint64_t i,
+                                          Real& value) {
+    const uint8_t flag = failed ? __ldg(failed + i) : uint8_t(0);
+    value = __ldg(rho + i);
+    return (flag == 0) & !isnan(value);
 }
 
 struct SelectState {
@@ -68,7 +73,10 @@ __global__ void count_valid_kernel(const Real* __restrict__ rho,
     uint64_t c = 0;
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-        c += row_valid(rho, failed, i) ? 1 : 0;
+    {
+        Real v;
+        c += row_valid(rho, failed, i, v) ? 1 : 0;
+    }
     for (int o = 16; o; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, static_cast<unsigned long long>(c));
 }
@@ -89,8 +97,9 @@ radix_hist_kernel(const Real* __restrict__ rho, const uint8_t* __restrict__ fail
     const uint64_t mask = (1ull << bits) - 1;
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kSelBlock + threadIdx.x; i < n;
          i += static_cast<uint64_t>(gridDim.x) * kSelBlock) {
-        if (!row_valid(rho, failed, i)) continue;
-        const uint64_t key = order_key(rho[i]);
+        Real v;
+        if (!row_valid(rho, failed, i, v)) continue;
+        const uint64_t key = order_key(v);
         const uint64_t high = hi_shift >= 64 ? 0 : (key >> hi_shift);
         const unsigned digit = static_cast<unsigned>((key >> shift) & mask);
         for (int q = 0; q < n_ranks; ++q) {
