@@ -71,11 +71,15 @@ __global__ void count_valid_kernel(const Real* __restrict__ rho,
                                    const uint8_t* __restrict__ failed, uint64_t n,
                                    unsigned long long* out) {
     uint64_t c = 0;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    {
-        Real v;
-        c += row_valid(rho, failed, i, v) ? 1 : 0;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n;
+         i0 += 16 * stride) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {  // sixteen independent loads per trip
+            const uint64_t i = i0 + static_cast<uint64_t>(u) * stride;
+            Real v = Real(0);
+            c += (i < n && row_valid(rho, failed, i, v)) ? 1 : 0;
+        }
     }
     for (int o = 16; o; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, static_cast<unsigned long long>(c));
@@ -91,20 +95,40 @@ radix_hist_kernel(const Real* __restrict__ rho, const uint8_t* __restrict__ fail
     __shared__ unsigned int sh[kMaxRanks * kBins];
     for (int i = threadIdx.x; i < n_ranks * kBins; i += kSelBlock) sh[i] = 0;
     __syncthreads();
-    uint64_t prefix[kMaxRanks];
-    for (int q = 0; q < n_ranks; ++q) prefix[q] = state->prefix[q];
     const int hi_shift = shift + bits;  // bits above the current digit
     const uint64_t mask = (1ull << bits) - 1;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kSelBlock + threadIdx.x; i < n;
-         i += static_cast<uint64_t>(gridDim.x) * kSelBlock) {
-        Real v;
-        if (!row_valid(rho, failed, i, v)) continue;
-        const uint64_t key = order_key(v);
-        const uint64_t high = hi_shift >= 64 ? 0 : (key >> hi_shift);
-        const unsigned digit = static_cast<unsigned>((key >> shift) & mask);
-        for (int q = 0; q < n_ranks; ++q) {
-            const uint64_t want = hi_shift >= 64 ? 0 : (prefix[q] >> hi_shift);
-            if (high == want) atomicAdd(&sh[q * kBins + digit], 1u);
+    // per-rank comparison values, hoisted: the row loop below is fully unrolled over
+    // kMaxRanks so that these stay in registers (the rows are what must stream)
+    uint64_t want[kMaxRanks];
+    bool active[kMaxRanks];
+#pragma unroll
+    for (int q = 0; q < kMaxRanks; ++q) {
+        active[q] = q < n_ranks;
+        want[q] = (active[q] && hi_shift < 64) ? (state->prefix[q] >> hi_shift) : 0;
+    }
+    // eight rows per thread and trip: their loads are issued together (a streaming
+    // pass is bound by the bytes in flight, not by the histogram updates)
+    constexpr int kInFlight = 8;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kSelBlock;
+    for (uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * kSelBlock + threadIdx.x; i0 < n;
+         i0 += stride * kInFlight) {
+        Real v[kInFlight];
+        bool ok[kInFlight];
+#pragma unroll
+        for (int u = 0; u < kInFlight; ++u) {
+            const uint64_t i = i0 + static_cast<uint64_t>(u) * stride;
+            v[u] = Real(0);
+            ok[u] = i < n && row_valid(rho, failed, i, v[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < kInFlight; ++u) {
+            if (!ok[u]) continue;
+            const uint64_t key = order_key(v[u]);
+            const uint64_t high = hi_shift >= 64 ? 0 : (key >> hi_shift);
+            const unsigned digit = static_cast<unsigned>((key >> shift) & mask);
+#pragma unroll
+            for (int q = 0; q < kMaxRanks; ++q)
+                if (active[q] && high == want[q]) atomicAdd(&sh[q * kBins + digit], 1u);
         }
     }
     __syncthreads();
@@ -292,9 +316,12 @@ void order_statistics_device(vxb_ctx* ctx, const Real* rho, const uint8_t* faile
                              ctx->stream));
     const int key_bits = sizeof(Real) == 8 ? 64 : 32;
     const int low = 64 - key_bits;  // float keys live in the high half
+    // persistent grid: the 32 KB shared-memory histogram lets 7 CTAs live on an SM;
+    // 4 per SM keeps every CTA in the first (only) wave -- with 8 per SM the last 1/8
+    // of the grid ran as a second wave that took as long as the first
     const unsigned grid = static_cast<unsigned>(
         std::min<uint64_t>((n + kSelBlock - 1) / kSelBlock,
-                           static_cast<uint64_t>(ctx->prop.multiProcessorCount) * 8));
+                           static_cast<uint64_t>(ctx->prop.multiProcessorCount) * 4));
     int top = 64;
     while (top > low) {
         const int bits = std::min(kDigitBits, top - low);
