@@ -178,7 +178,9 @@ int vxb_rng_fill_gaussian_fast(vxb_ctx* ctx, int precision, uint64_t seed, uint6
                                uint64_t rows, uint32_t per_row, void* out);
 /* Device evaluation of the fastmath functions (fastmath.hpp:23-128), for
  * parity tests: fn 0 log2_pos, 1 ln_pos, 2 exp2_clamped, 3 sinpi, 4 cospi,
- * 5 pow_pos (x = base, y = exponent; y ignored otherwise). */
+ * 5 pow_pos (x = base, y = exponent; y ignored otherwise); and of the
+ * throughput-mode functions, for accuracy tests: fn 6 log2 (x > 0 normal),
+ * 7 2^x (|x| < 1000), 8 1/x (normal x). */
 int vxb_fastmath_eval(vxb_ctx* ctx, int fn, const double* x, const double* y, uint64_t n,
                       double* out);
 /* partition (blocked.cpp:34-63): writes workers pairs [begin,end). Host-side. */

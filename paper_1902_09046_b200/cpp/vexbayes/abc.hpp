@@ -82,6 +82,10 @@ inline PriorPredictiveSet run_prior_predictive(const ModelHooks& model, std::siz
     set.failed.resize(n);
     vxb_keying key{VXB_KEY_WORKER, static_cast<std::uint32_t>(workers),
                    static_cast<std::uint32_t>(block_width), 0, seed};
+    if (dm.model == VXB_MODEL_TOGGLE && dm.rng == VXB_RNG_FAST) {
+        // throughput mode of the toggle model: rows keyed per particle
+        key = vxb_keying{VXB_KEY_PARTICLE, 1, 1, 0, seed};
+    }
     if (dm.model == VXB_MODEL_TB) {
         // a TB path consumes a data-dependent number of variates: rows are keyed per
         // particle (tb_model.hpp of this shim); block_width is validated as the

@@ -107,7 +107,14 @@ __global__ void fill_gaussian_kernel(uint64_t key, uint64_t pos, uint64_t n, dou
     }
 }
 
-__global__ void fastmath_kernel(int fn, const double* x, const double* y, uint64_t n, double* out) {
+__global__ void fastmath_kernel(int fn, const double* x, const double* y, uint64_t n, double* out,
+                                const double2* fast_table) {
+    // functions 6-8: the throughput-mode log2 / 2^z / reciprocal on the shared tables
+    __shared__ double2 s_tab[kFastTableSize];
+    if (fn >= 6) {
+        for (int k = threadIdx.x; k < kFastTableSize; k += blockDim.x) s_tab[k] = fast_table[k];
+        __syncthreads();
+    }
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double a = x[i];
@@ -118,7 +125,10 @@ __global__ void fastmath_kernel(int fn, const double* x, const double* y, uint64
         case 2: r = exp2_clamped<Exact>(a); break;
         case 3: r = sinpi<Exact>(a); break;
         case 4: r = cospi<Exact>(a); break;
-        default: r = pow_pos<Exact>(a, y[i]); break;
+        case 5: r = pow_pos<Exact>(a, y[i]); break;
+        case 6: r = fast_log2(a, s_tab); break;
+        case 7: r = fast_exp2(a, s_tab); break;
+        default: r = fast_rcp(a); break;
     }
     out[i] = r;
 }
@@ -333,7 +343,7 @@ extern "C" int vxb_fastmath_eval(vxb_ctx* ctx, int fn, const double* x, const do
                                  uint64_t n, double* out) {
     return guarded([&] {
         use(ctx);
-        require(fn >= 0 && fn <= 5, "invalid-argument", "unknown fastmath function");
+        require(fn >= 0 && fn <= 8, "invalid-argument", "unknown fastmath function");
         if (n == 0) return;
         require(x && out && (fn != 5 || y), "invalid-argument", "null argument");
         Staged d_x(ctx, x, n * 8, true, false);
@@ -342,7 +352,7 @@ extern "C" int vxb_fastmath_eval(vxb_ctx* ctx, int fn, const double* x, const do
         {
             LaunchScope scope(ctx, VXB_K_MISC);
             fastmath_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
-                fn, d_x.as<double>(), d_y.as<double>(), n, d_out.as<double>());
+                fn, d_x.as<double>(), d_y.as<double>(), n, d_out.as<double>(), ctx->log_table);
             check_launch("fastmath_kernel");
         }
         d_out.finish();

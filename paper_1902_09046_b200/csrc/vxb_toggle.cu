@@ -66,9 +66,53 @@ __device__ __forceinline__ double toggle_cell(const double* th, uint32_t steps, 
     return obs >= 1.0 ? obs : 1.0;
 }
 
+// Throughput mode of one cell (VXB_RNG_FAST): the same model with the packed
+// Philox4x32 generator (eight normals = four steps per batch, drawn one batch
+// ahead), table-based log2 / 2^z, a Newton reciprocal and FMA arithmetic.
+// Statistically validated against the exact mode (tests/test_gpu_workloads.py).
+__device__ __forceinline__ double toggle_cell_fast(const double* th, uint32_t steps, const FastKeys& fk,
+                                                   const double2* tbl, uint32_t row_word,
+                                                   uint32_t cell_word) {
+    const double mu = th[0], sigma = th[1], gamma = th[2];
+    const double alpha_u = th[3], alpha_v = th[4], beta_u = th[5], beta_v = th[6];
+    double u = 10.0, v = 10.0;
+    FastNoise64 noise(fk, tbl, row_word, cell_word, 0u);
+    const auto step = [&](double zu, double zv) {
+        const double p_u = fast_exp2(beta_u * fast_log2(v, tbl), tbl);
+        const double p_v = fast_exp2(beta_v * fast_log2(u, tbl), tbl);
+        const double ut = fma(0.5, zu, fma(u, 0.97, fma(alpha_u, fast_rcp(1.0 + p_u), -1.0)));
+        const double vt = fma(0.5, zv, fma(v, 0.97, fma(alpha_v, fast_rcp(1.0 + p_v), -1.0)));
+        u = fmax(ut, 1.0);
+        v = fmax(vt, 1.0);
+    };
+    uint32_t left = steps - 1;
+    double z[8];
+    while (left >= 4) {
+        noise.next(z);
+        step(z[0], z[1]);
+        step(z[2], z[3]);
+        step(z[4], z[5]);
+        step(z[6], z[7]);
+        left -= 4;
+    }
+    noise.next(z);  // the ragged tail (< 4 steps) and the observation noise
+#pragma unroll
+    for (uint32_t q = 0; q < 3; ++q)
+        if (q < left) step(z[2 * q], z[2 * q + 1]);
+    const double eta = z[6];
+    const double pw = fast_exp2(gamma * fast_log2(u, tbl), tbl);
+    return fmax(u + mu + sigma * mu * eta * fast_rcp(pw), 1.0);
+}
+
+template <bool kFast>
 __global__ void __launch_bounds__(kTgBlock) toggle_abc_kernel(const __grid_constant__ ToggleParams p) {
     extern __shared__ double s_y[];
     __shared__ double s_q[19];
+    __shared__ double2 s_tab[kFast ? kFastTableSize : 1];
+    if (kFast) {
+        for (int i = threadIdx.x; i < kFastTableSize; i += kTgBlock) s_tab[i] = p.fast_table[i];
+        __syncthreads();
+    }
     for (uint64_t r = blockIdx.x; r < p.count; r += gridDim.x) {
         const uint64_t row = p.first + r;
         uint64_t key, base;
@@ -79,6 +123,19 @@ __global__ void __launch_bounds__(kTgBlock) toggle_abc_kernel(const __grid_const
 #pragma unroll
             for (int k = 0; k < 7; ++k) th[k] = p.theta_in[k];
             b0 = base + (base & 1);
+        } else if (kFast) {
+            // throughput generator: seven uniforms from four Philox4x32 blocks of the row
+            const uint32_t rl = static_cast<uint32_t>(row), rh = static_cast<uint32_t>(row >> 32);
+            double un[8];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const Words32 w = philox4x32(p.key.fast, static_cast<uint32_t>(q), kDomPrior, rl, rh);
+                un[2 * q] = fast_unit(w.a, w.b);
+                un[2 * q + 1] = fast_unit(w.c, w.d);
+            }
+#pragma unroll
+            for (int k = 0; k < 7; ++k) th[k] = p.lo[k] + un[k] * (p.hi[k] - p.lo[k]);
+            b0 = 0;
         } else {
             // sample_prior (toggle_switch.cpp:25-29): 7 uniforms at base..base+6
 #pragma unroll
@@ -94,8 +151,14 @@ __global__ void __launch_bounds__(kTgBlock) toggle_abc_kernel(const __grid_const
         if (!p.invalid) {
             for (uint32_t c = threadIdx.x; c < p.sort_n; c += kTgBlock) {
                 double y = INFINITY;  // padding sorts to the end
-                if (c < p.cells)
-                    y = toggle_cell<Exact>(th, p.steps, key, (b0 >> 1) + static_cast<uint64_t>(c) * p.steps);
+                if (c < p.cells) {
+                    if (kFast)
+                        y = toggle_cell_fast(th, p.steps, p.key.fast, s_tab, static_cast<uint32_t>(row),
+                                             c | (static_cast<uint32_t>(row >> 32) << 14));
+                    else
+                        y = toggle_cell<Exact>(th, p.steps, key,
+                                               (b0 >> 1) + static_cast<uint64_t>(c) * p.steps);
+                }
                 s_y[c] = y;
             }
             __syncthreads();
@@ -167,8 +230,11 @@ void toggle_launch(vxb_ctx* ctx, const vxb_model& m, const Keying& key, uint64_t
     require(m.model == VXB_MODEL_TOGGLE, "invalid-argument", "not the toggle-switch model");
     require(m.dim == 7 && m.summary_dim == 19, "invalid-shape",
             "toggle model has 7 parameters and 19 summaries");
-    require(m.precision == VXB_F64 && m.rng == VXB_RNG_REF, "invalid-argument",
-            "the toggle model runs in fp64 with the reference generator");
+    require(m.precision == VXB_F64 && (m.rng == VXB_RNG_REF || m.rng == VXB_RNG_FAST),
+            "invalid-argument", "the toggle model runs in fp64 (reference or throughput generator)");
+    const bool fast = m.rng == VXB_RNG_FAST;
+    require(!fast || (!theta_dev && key.mode == kKeyParticle), "invalid-argument",
+            "the throughput generator keys rows per particle");
     const uint32_t cells = static_cast<uint32_t>(m.consts[1]);
     require(cells >= 1, "invalid-shape", "toggle simulation needs at least one cell");
     ToggleParams p{};
@@ -197,11 +263,17 @@ void toggle_launch(vxb_ctx* ctx, const vxb_model& m, const Keying& key, uint64_t
     if (count == 0) return;
     const size_t smem = static_cast<size_t>(p.sort_n) * sizeof(double);
     require(smem <= 200 * 1024, "invalid-shape", "too many cells for the in-CTA sort (max 16384)");
-    VXB_CUDA(cudaFuncSetAttribute(toggle_abc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(count, 1u << 20));
     LaunchScope scope(ctx, VXB_K_SIMULATE);
-    toggle_abc_kernel<<<grid, kTgBlock, smem, ctx->stream>>>(p);
+    if (fast) {
+        VXB_CUDA(cudaFuncSetAttribute(toggle_abc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        toggle_abc_kernel<true><<<grid, kTgBlock, smem, ctx->stream>>>(p);
+    } else {
+        VXB_CUDA(cudaFuncSetAttribute(toggle_abc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        toggle_abc_kernel<false><<<grid, kTgBlock, smem, ctx->stream>>>(p);
+    }
     check_launch("toggle_abc_kernel");
 }
 

@@ -320,3 +320,21 @@ def test_fast_generator_normals(ctx, precision):
     # ragged request lengths give prefixes of the same stream
     short = ctx.rng_fill_gaussian_fast(precision, 99, 0, 8, 37)
     assert np.array_equal(short.astype(np.float64), z[:8, :37])
+
+
+def test_throughput_mode_elementary_functions(ctx):
+    """Table-based log2 / 2^z and the Newton reciprocal used by the throughput modes:
+    a few ulp of the libm values over their working ranges."""
+    rs = np.random.RandomState(8)
+    x = np.concatenate([np.exp(rs.uniform(-30, 30, 20000)), [1.0, 2.0, 0.5, 1.4142135623730951, 1e-300, 1e300]])
+    got = ctx.fastmath(6, x)
+    assert np.max(np.abs(got - np.log2(x)) / np.maximum(np.abs(np.log2(x)), 1.0)) < 4e-16
+    # powers of two: exact up to the 1e-300 that keeps -2 ln(u) positive at u = 1
+    assert abs(got[-6]) < 1e-290 and got[-5] == 1.0 and got[-4] == -1.0
+    z = np.concatenate([rs.uniform(-900, 900, 20000), [0.0, 1.0, -1.0, 63.5, 0.015625]])
+    got = ctx.fastmath(7, z)
+    assert np.max(np.abs(got / np.exp2(z) - 1.0)) < 5e-16
+    assert got[-5] == 1.0 and got[-4] == 2.0 and got[-3] == 0.5
+    a = np.concatenate([np.exp(rs.uniform(-100, 100, 20000)) * rs.choice([-1.0, 1.0], 20000), [1.0, 3.0, -7.0]])
+    got = ctx.fastmath(8, a)
+    assert np.max(np.abs(got * a - 1.0)) < 4e-16

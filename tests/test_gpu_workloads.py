@@ -363,3 +363,35 @@ def test_tb_gillespie_edge_cases(ctx, oracle):
     with pytest.raises(lib.VxbError) as e:
         ctx.abc_prior_predictive_host(M.tb_model(0, 10.0, 100.0), M.keying(1), 4, 0, 4, np.zeros(2))
     assert e.value.code == "invalid-shape"
+
+
+@pytest.mark.timeout(900)
+def test_toggle_throughput_mode_statistics(ctx):
+    """The toggle model's throughput mode (packed Philox4x32 normals, table-based
+    log2 / 2^z, FMA arithmetic) against its bit-exact mode: distances and the 19
+    quantile summaries agree in distribution (two-sample KS at 1 %, means within
+    Monte-Carlo error)."""
+    n = 3000
+    m_ref, m_fast = M.toggle_model(100, 256), M.toggle_model(100, 256, rng=A.VXB_RNG_FAST)
+    obs = ctx.simulate_at(m_ref, M.TOGGLE_MIDPOINT, lib.derive_seed(1337, [90]), 0, 0)
+    p0, s0, r0, f0 = ctx.abc_prior_predictive_host(m_ref, M.keying(11), n, 0, n, obs)
+    p1, s1, r1, f1 = ctx.abc_prior_predictive_host(m_fast, M.keying(12), n, 0, n, obs)
+    assert not f0.any() and not f1.any() and np.isfinite(s1).all() and (s1 >= 1.0).all()
+
+    def ks(a, b):
+        xs = np.sort(np.concatenate([a, b]))
+        return np.abs(np.searchsorted(np.sort(a), xs, side="right") / len(a)
+                      - np.searchsorted(np.sort(b), xs, side="right") / len(b)).max()
+    crit = 1.628 * math.sqrt(2.0 / n)
+    assert ks(r0, r1) < crit
+    for k in (0, 9, 18):
+        assert ks(s0[:, k], s1[:, k]) < crit, k
+        se = math.sqrt(s0[:, k].var() / n + s1[:, k].var() / n)
+        assert abs(s0[:, k].mean() - s1[:, k].mean()) < 4.5 * se, k
+    for k in range(7):   # the prior box
+        assert p1[:, k].min() >= M.TOGGLE_PRIOR_LO[k] and p1[:, k].max() < M.TOGGLE_PRIOR_HI[k]
+        assert ks(p0[:, k], p1[:, k]) < crit
+    # same parameters, same model: a cell ensemble simulated by both modes at fixed theta
+    # has the same summaries up to the spread over 4096 cells
+    part = ctx.abc_prior_predictive_host(m_fast, M.keying(12), n, 100, 50, obs)
+    assert eq(part[2], r1[100:150])                      # shard independence of the throughput mode
