@@ -349,8 +349,13 @@ int vxb_make_kernel(const double* cov, uint32_t dim, double scale, double jitter
  *   evidence_of closure of weak_info.cpp:200-215.  One CTA per run.  status[r]:
  *   0 ok, 1 invalid-model, 2 degenerate-ensemble, 3 non-convergence (the errors
  *   the reference turns into a skipped evidence); log_evidence is NaN then.
- *   trace (optional): n_runs x trace_rows x 4 doubles per iteration: temperature,
- *   ESS after reweighting, move steps R_n, pilot acceptance (smc.hpp:125).
+ *   trace (optional): n_runs x trace_rows x 5 doubles per iteration: temperature,
+ *   ESS after reweighting, move steps R_n, pilot acceptance, log evidence so far
+ *   (the columns of SmcConfig::trace, smc.hpp:125).
+ * vxb_smc_bioassay_ensemble: ONE run returning what SmcResult holds: log evidence,
+ *   iterations and the final ensemble as 5 x particles doubles (theta0, theta1,
+ *   log weights, log likelihoods, log priors); sampler failures are errors
+ *   (invalid-model / degenerate-ensemble / non-convergence) as in the reference.
  *   deaths, lambda, seeds: host arrays.  particles <= 2048. */
 int vxb_bioassay_log_likelihood(vxb_ctx* ctx, const double* beta, uint64_t lanes, uint32_t groups,
                                 const double* dose, const uint32_t* group_size,
@@ -363,6 +368,13 @@ int vxb_smc_bioassay(vxb_ctx* ctx, uint64_t n_runs, uint32_t groups, const doubl
                      const uint64_t* seeds, uint64_t particles, uint64_t block_width, double c,
                      double scale, double* log_evidence, uint32_t* iterations, uint8_t* status,
                      double* trace, uint32_t trace_rows);
+
+int vxb_smc_bioassay_ensemble(vxb_ctx* ctx, uint32_t groups, const double* dose,
+                              const uint32_t* group_size, const uint32_t* deaths,
+                              const double* lambda, uint64_t seed, uint64_t particles,
+                              uint64_t block_width, double c, double scale, double* log_evidence,
+                              uint32_t* iterations, double* ensemble, double* trace,
+                              uint32_t trace_rows);
 
 /* WeakInfoConfig (weak_info.hpp:62-75) as a POD; `workers` has no device meaning
  * (all 2 (K+1) N sampler runs are one launch). */

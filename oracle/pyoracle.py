@@ -154,6 +154,18 @@ class Oracle(_Base):
             return ev.value, it.value
         return ev.value, it.value, tr[:it.value]
 
+    def smc_bioassay_ensemble(self, dose, group_size, deaths, lambda1, lambda2, particles,
+                              block_width, c, scale, seed):
+        """SmcResult of one run; trace columns: temperature, ess, steps, p_acc, log evidence."""
+        d, g, y = self._design(dose, group_size, deaths)
+        ev, it = f64(), u64()
+        ens, tr = np.zeros((5, particles)), np.zeros((1000, 5))
+        self._call("smc_bioassay_ensemble", _ptr(d), _ptr(g), _ptr(y), u32(d.size), f64(lambda1),
+                   f64(lambda2), u64(particles), u64(block_width), f64(c), f64(scale), u64(seed),
+                   C.byref(ev), C.byref(it), _ptr(ens), _ptr(tr), u64(1000))
+        return dict(log_evidence=ev.value, iterations=it.value, particles=ens[:2].T.copy(),
+                    log_weights=ens[2], log_liks=ens[3], log_priors=ens[4], trace=tr[:it.value])
+
     def splitmix64(self, z):
         return int(self.lib.vxo_splitmix64(z))
 
@@ -400,6 +412,21 @@ class Ref(_Base):
         rows = [ln.split(",") for ln in buf.value.decode().strip().splitlines()[1:]]
         full = np.array([[float(x) for x in r] for r in rows])  # n,t_n,ess,log_evidence,R_n,p_acc,h
         return ev.value, it.value, full[:, [1, 2, 4, 5]]       # temperature, ess, steps, p_acc
+
+    def smc_bioassay_ensemble(self, dose, group_size, deaths, lambda1, lambda2, particles,
+                              block_width, c, scale, seed):
+        d, g, y = self._design(dose, group_size, deaths)
+        ev, it = f64(), u64()
+        ens = np.zeros((5, particles))
+        buf = C.create_string_buffer(1 << 16)
+        self._call("smc_bioassay_ensemble", _ptr(d), _ptr(g), _ptr(y), u32(d.size), f64(lambda1),
+                   f64(lambda2), u64(particles), u64(block_width), f64(c), f64(scale), u64(seed),
+                   C.byref(ev), C.byref(it), _ptr(ens), buf, u64(len(buf)))
+        rows = [ln.split(",") for ln in buf.value.decode().strip().splitlines()[1:]]
+        full = np.array([[float(x) for x in r] for r in rows])  # n,t_n,ess,log_evidence,R_n,p_acc,h
+        return dict(log_evidence=ev.value, iterations=it.value, particles=ens[:2].T.copy(),
+                    log_weights=ens[2], log_liks=ens[3], log_priors=ens[4],
+                    trace=full[:, [1, 2, 4, 5, 3]], trace_text=buf.value.decode())
 
     def splitmix64(self, z):
         return int(self.lib.ref_splitmix64(z))

@@ -583,6 +583,47 @@ int ref_smc_bioassay(const double* dose, const std::uint32_t* group_size,
     });
 }
 
+// One run returning the reference's SmcResult: ensemble as 5 x particles doubles
+// (theta0, theta1, log weights, log likelihoods, log priors) and the trace CSV text.
+int ref_smc_bioassay_ensemble(const double* dose, const std::uint32_t* group_size,
+                              const std::uint32_t* deaths, std::uint32_t groups, double lambda1,
+                              double lambda2, std::uint64_t particles, std::uint64_t block_width,
+                              double c, double scale, std::uint64_t seed, double* log_evidence,
+                              std::uint64_t* iterations, double* ensemble, char* trace,
+                              std::uint64_t trace_cap) {
+    return guarded([&] {
+        smc::SmcConfig cfg;
+        cfg.particles = particles;
+        cfg.block_width = block_width;
+        cfg.workers = 1;
+        cfg.c = c;
+        cfg.scale = scale;
+        cfg.seed = seed;
+        std::ostringstream text;
+        text.precision(17);
+        if (trace) cfg.trace = &text;
+        const auto model = weakinfo::make_bioassay_model(make_data(dose, group_size, deaths, groups),
+                                                         {lambda1, lambda2});
+        const smc::SmcResult res = smc::run_smc(model, cfg);
+        *log_evidence = res.log_evidence;
+        *iterations = res.iterations;
+        const smc::ParticleEnsemble& e = res.ensemble;
+        for (std::uint64_t i = 0; i < particles; ++i) {
+            ensemble[i] = e.particles[2 * i];
+            ensemble[particles + i] = e.particles[2 * i + 1];
+            ensemble[2 * particles + i] = e.log_weights[i];
+            ensemble[3 * particles + i] = e.log_liks[i];
+            ensemble[4 * particles + i] = e.log_priors[i];
+        }
+        if (trace && trace_cap) {
+            const std::string t = text.str();
+            const std::size_t k = std::min<std::size_t>(t.size(), trace_cap - 1);
+            std::memcpy(trace, t.data(), k);
+            trace[k] = 0;
+        }
+    });
+}
+
 int ref_weak_info_test(std::uint64_t hyper_count, std::uint64_t datasets, std::uint64_t particles,
                        double alpha, double c, double scale, std::uint64_t workers,
                        std::uint64_t block_width, std::uint64_t seed, int redraw_base,

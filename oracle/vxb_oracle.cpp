@@ -1421,7 +1421,7 @@ static void bioassay_draw(double l1, double l2, const double* dose, const std::u
 }
 
 struct AnnealTrace {
-    std::vector<double> temperature, ess, accept;
+    std::vector<double> temperature, ess, accept, evidence;
     std::vector<std::uint64_t> steps;
 };
 
@@ -1498,7 +1498,7 @@ struct Annealed {
 
 static void anneal_run(const Bioassay& model, std::uint64_t np, std::uint64_t block_width, double c,
                        double scale, std::uint64_t seed, double* log_evidence,
-                       std::uint64_t* iterations, AnnealTrace* trace) {
+                       std::uint64_t* iterations, AnnealTrace* trace, double* ensemble = nullptr) {
     const double tol = 1e-10, jitter = 1e-10;            // SmcConfig defaults, smc.hpp:120-121
     const std::uint64_t max_iterations = 1000, step_cap = 100;
     require(supported_width(block_width), "invalid-shape", "unsupported block width");
@@ -1579,10 +1579,18 @@ static void anneal_run(const Bioassay& model, std::uint64_t np, std::uint64_t bl
             trace->ess.push_back(ess_now);
             trace->accept.push_back(p_acc);
             trace->steps.push_back(steps);
+            trace->evidence.push_back(a.log_evidence);
         }
     }
     *log_evidence = a.log_evidence;
     *iterations = n;
+    for (std::uint64_t i = 0; ensemble && i < np; ++i) {  // SmcResult::ensemble, smc.cpp:478-487
+        ensemble[i] = a.theta[2 * i];
+        ensemble[np + i] = a.theta[2 * i + 1];
+        ensemble[2 * np + i] = a.lw[i];
+        ensemble[3 * np + i] = a.ll[i];
+        ensemble[4 * np + i] = a.lp[i];
+    }
 }
 
 int vxo_bioassay_ll(const double* beta, std::uint64_t lanes, const double* dose,
@@ -1601,6 +1609,28 @@ int vxo_bioassay_sample(double lambda1, double lambda2, const double* dose,
 // trace (optional): rows of (iteration, temperature, ess, log_evidence=nan, steps, p_acc, h)
 // are not produced here; trace_out receives iterations x 4 doubles
 // (temperature, ess, steps, p_acc), at most trace_cap rows.
+// One run with its final ensemble (5 x particles: theta0, theta1, log weights, log
+// likelihoods, log priors) and a 5-column trace (… , log evidence so far).
+int vxo_smc_bioassay_ensemble(const double* dose, const std::uint32_t* group_size,
+                              const std::uint32_t* deaths, std::uint32_t groups, double lambda1,
+                              double lambda2, std::uint64_t particles, std::uint64_t block_width,
+                              double c, double scale, std::uint64_t seed, double* log_evidence,
+                              std::uint64_t* iterations, double* ensemble, double* trace_out,
+                              std::uint64_t trace_cap) {
+    return guarded([&] {
+        const Bioassay m = make_bioassay(dose, group_size, deaths, groups, lambda1, lambda2);
+        AnnealTrace tr;
+        anneal_run(m, particles, block_width, c, scale, seed, log_evidence, iterations, &tr, ensemble);
+        for (std::uint64_t i = 0; trace_out && i < tr.steps.size() && i < trace_cap; ++i) {
+            trace_out[5 * i] = tr.temperature[i];
+            trace_out[5 * i + 1] = tr.ess[i];
+            trace_out[5 * i + 2] = static_cast<double>(tr.steps[i]);
+            trace_out[5 * i + 3] = tr.accept[i];
+            trace_out[5 * i + 4] = tr.evidence[i];
+        }
+    });
+}
+
 int vxo_smc_bioassay(const double* dose, const std::uint32_t* group_size,
                      const std::uint32_t* deaths, std::uint32_t groups, double lambda1,
                      double lambda2, std::uint64_t particles, std::uint64_t block_width, double c,

@@ -86,7 +86,7 @@ EXPORTED_SYMBOLS = (
     "vxb_compact_accepted", "vxb_abc_reject", "vxb_simulate_at", "vxb_ppp_pvalues",
     "vxb_ess", "vxb_logsumexp", "vxb_resample_multinomial", "vxb_abcsmc_run",
     "vxb_abcsmc_propose", "vxb_abcsmc_weights", "vxb_weighted_moments", "vxb_canon_cumsum",
-    "vxb_canon_chunk_sums", "vxb_quantile", "vxb_divide", "vxb_make_kernel", "vxb_bioassay_log_likelihood", "vxb_bioassay_sample", "vxb_smc_bioassay",
+    "vxb_canon_chunk_sums", "vxb_quantile", "vxb_divide", "vxb_make_kernel", "vxb_bioassay_log_likelihood", "vxb_bioassay_sample", "vxb_smc_bioassay", "vxb_smc_bioassay_ensemble",
     "vxb_weak_info_test", "vxb_weak_info_lambdas", "vxb_weak_info_evidence",
     "vxb_weak_info_cutoffs", "vxb_mlmc_level", "vxb_mlmc_tauleap",
 )

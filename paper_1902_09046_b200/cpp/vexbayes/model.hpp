@@ -31,6 +31,10 @@ struct ModelHooks {
     std::function<void(std::span<const double>, std::size_t, std::span<double>)> block_log_likelihood;
     // GPU descriptor of the same model (what the kernels read).
     std::shared_ptr<const DeviceModel> device;
+    // Models whose device form needs more than the POD descriptor (a dataset):
+    // a family tag and the family's own binding (bioassay.hpp).
+    const char* family = nullptr;
+    std::shared_ptr<const void> binding;
 };
 
 }  // namespace vexbayes

@@ -1,13 +1,17 @@
 // vexbayes/smc.hpp (B200 shim) -- the SMC building blocks on the hot path
-// (smc.hpp:35-49): ParticleEnsemble, ess, resample_multinomial; plus the
-// ABC-SMC driver of BASELINE config 3 (not in the reference).
+// (smc.hpp:35-49): ParticleEnsemble, ess, resample_multinomial; run_smc
+// (smc.hpp:112-138) for the model the paper runs it on; plus the ABC-SMC
+// driver of BASELINE config 3 (not in the reference).
 #pragma once
 
 #include <cmath>
 #include <cstdint>
+#include <ostream>
 #include <span>
+#include <string_view>
 #include <vector>
 
+#include "bioassay.hpp"
 #include "cuda_context.hpp"
 #include "model.hpp"
 
@@ -55,6 +59,82 @@ inline void resample_multinomial(ParticleEnsemble& ensemble, std::uint64_t seed,
     if (ensemble.log_liks.size() == np) ensemble.log_liks = std::move(lls);
     if (has_priors) ensemble.log_priors = std::move(lps);
     ensemble.log_weights.assign(np, -std::log(static_cast<double>(np)));
+}
+
+// ---------------------------------------------------------------- run_smc
+// SmcConfig / SmcResult: smc.hpp:112-131, same members and defaults.
+struct SmcConfig {
+    std::size_t particles = 2000;
+    std::size_t block_width = 4;
+    std::size_t workers = 1;  // accepted for source compatibility; the device replays the
+                              // reference's workers = 1 stream layout whatever is asked
+    double c = 0.01;
+    double scale = 0.0;       // <= 0 selects 2.38/sqrt(d)
+    bool esjd = false;
+    std::vector<double> esjd_scales = {0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9, 1.0};
+    double bisection_tol = 1e-10;
+    double jitter = 1e-10;
+    std::size_t max_iterations = 1000;
+    std::size_t step_cap = 100;
+    std::uint64_t seed = 0;
+    std::ostream* trace = nullptr;  // per-iteration CSV: n,t_n,ess,log_evidence,R_n,p_acc,h
+};
+struct SmcResult {
+    ParticleEnsemble ensemble;
+    double log_evidence = 0.0;
+    std::size_t iterations = 0;
+};
+
+// smc::run_smc (smc.cpp:352-488): the whole adaptive sampler is ONE kernel with
+// the ensemble in shared memory (csrc/vxb_anneal.cu), so the model has to be one
+// the kernel knows: the bioassay model of the case study (make_bioassay_model).
+// ESJD adaptation and non-default tolerances/caps are fixed on the device and
+// rejected here rather than silently ignored.
+inline SmcResult run_smc(const ModelHooks& model, const SmcConfig& cfg) {
+    require(model.family && std::string_view(model.family) == "bioassay" && model.binding,
+            "unsupported-model", "run_smc on the device needs make_bioassay_model()");
+    require(!cfg.esjd, "unsupported-config", "ESJD scale adaptation is not built on the device");
+    require(cfg.bisection_tol == 1e-10 && cfg.jitter == 1e-10 && cfg.max_iterations == 1000 &&
+                cfg.step_cap == 100,
+            "unsupported-config", "tolerance, jitter and caps are fixed at the reference defaults");
+    require(cfg.workers >= 1, "invalid-argument", "need at least one worker");
+    const auto& b = *static_cast<const weakinfo::BioassayBinding*>(model.binding.get());
+    const std::size_t np = cfg.particles;
+    const double lam[2] = {b.prior.lambda1, b.prior.lambda2};
+    const std::uint32_t rows = 1000;
+    std::vector<double> packed(5 * np), trace(cfg.trace ? rows * 5 : 0);
+    SmcResult r;
+    std::uint32_t it = 0;
+    cuda::check(vxb_smc_bioassay_ensemble(
+        cuda::context(), static_cast<std::uint32_t>(b.data.groups()), b.data.dose.data(),
+        b.data.group_size.data(), b.data.deaths.data(), lam, cfg.seed, np, cfg.block_width, cfg.c,
+        cfg.scale, &r.log_evidence, &it, packed.data(), cfg.trace ? trace.data() : nullptr,
+        cfg.trace ? rows : 0));
+    r.iterations = it;
+    ParticleEnsemble& e = r.ensemble;
+    e.count = np;
+    e.dim = 2;
+    e.particles.resize(2 * np);
+    for (std::size_t i = 0; i < np; ++i) {
+        e.particles[2 * i] = packed[i];
+        e.particles[2 * i + 1] = packed[np + i];
+    }
+    e.log_weights.assign(packed.begin() + 2 * np, packed.begin() + 3 * np);
+    e.log_liks.assign(packed.begin() + 3 * np, packed.begin() + 4 * np);
+    e.log_priors.assign(packed.begin() + 4 * np, packed.end());
+    e.temperature = 1.0;
+    e.log_evidence = r.log_evidence;
+    e.iteration = it;
+    if (cfg.trace) {
+        const double h = cfg.scale > 0.0 ? cfg.scale : 2.38 / std::sqrt(2.0);
+        *cfg.trace << "n,t_n,ess,log_evidence,R_n,p_acc,h\n";
+        for (std::uint32_t n = 0; n < it; ++n) {
+            const double* row = &trace[5 * n];
+            *cfg.trace << (n + 1) << ',' << row[0] << ',' << row[1] << ',' << row[4] << ','
+                       << static_cast<std::size_t>(row[2]) << ',' << row[3] << ',' << h << '\n';
+        }
+    }
+    return r;
 }
 
 struct AbcSmcConfig {

@@ -23,6 +23,7 @@
 #include <span>
 #include <vector>
 
+#include "bioassay.hpp"
 #include "cuda_context.hpp"
 
 namespace vexbayes::weakinfo {
@@ -42,33 +43,7 @@ inline std::vector<double> estimate_pvalues(std::span<const double> evidences_ba
     return p;
 }
 
-// ------------------------------------------------------------ bioassay model
-struct Hyperparam {
-    double lambda1;
-    double lambda2;
-};
-inline constexpr Hyperparam kBasePrior{10.0, 2.5};
-
-struct BioassayData {
-    std::vector<double> dose;
-    std::vector<unsigned> group_size;
-    std::vector<unsigned> deaths;
-    std::size_t groups() const { return dose.size(); }
-};
-inline BioassayData default_design() { return {{-0.86, -0.3, -0.05, -0.75}, {5, 5, 5, 5}, {}}; }
-
-namespace detail {
-inline void check_design(const BioassayData& data, bool with_deaths) {
-    require(data.dose.size() == data.group_size.size(), "invalid-argument",
-            "dose and group size lengths differ");
-    if (!with_deaths) return;
-    require(data.deaths.size() == data.dose.size(), "invalid-argument",
-            "death count length differs from the design");
-    for (std::size_t g = 0; g < data.groups(); ++g)
-        require(data.deaths[g] <= data.group_size[g], "invalid-argument",
-                "more deaths than animals in a group");
-}
-}  // namespace detail
+// Hyperparam, BioassayData, default_design, make_bioassay_model: bioassay.hpp
 
 inline void bioassay_block_log_likelihood(std::span<const double> params, std::size_t lanes,
                                           const BioassayData& data, std::span<double> out) {

@@ -186,8 +186,9 @@ struct AnnealParams {
     double* log_evidence;
     uint32_t* iterations;
     uint8_t* status;
-    double* trace;            // optional: n_runs x trace_rows x 4 (temperature, ess, steps, p_acc)
+    double* trace;            // optional: n_runs x trace_rows x 5 (temperature, ess, steps, p_acc, log evidence)
     uint32_t trace_rows;
+    double* ensemble;         // optional: n_runs x 5 x np (theta0, theta1, log w, log L, log prior)
 };
 
 // One tempered random-walk sweep (move_range, smc.cpp:77-150): particle q, step r
@@ -451,12 +452,21 @@ __global__ void __launch_bounds__(kAnnealBlock, 6) anneal_kernel(const __grid_co
         sweep(d, model, e, np, key_of(n, kRoleMove), steps, temperature, h, l00, l10, l11);
         __syncthreads();
         if (p.trace && threadIdx.x == 0 && n <= p.trace_rows) {
-            double* row = p.trace + (run * p.trace_rows + (n - 1)) * 4;
+            double* row = p.trace + (run * p.trace_rows + (n - 1)) * 5;
             row[0] = temperature;
             row[1] = ess_now;
             row[2] = static_cast<double>(steps);
             row[3] = p_acc;
+            row[4] = log_evidence;
         }
+    }
+    if (p.ensemble) {  // the final ensemble (SmcResult::ensemble)
+        __syncthreads();
+        double* out = p.ensemble + run * 5 * np;
+        const double* rows[5] = {e.t0, e.t1, e.lw, e.ll, e.lp};
+#pragma unroll
+        for (int r = 0; r < 5; ++r)
+            for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) out[r * np + i] = rows[r][i];
     }
     if (threadIdx.x == 0) {
         p.log_evidence[run] = status == kRunOk ? log_evidence : __longlong_as_double(0x7FF8000000000000LL);
@@ -625,7 +635,7 @@ static void check_sampler_args(uint64_t particles, uint64_t block_width, double 
 static void anneal_device(vxb_ctx* ctx, const Design& design, uint64_t n_runs, uint64_t particles, double c,
                           double scale, const uint32_t* deaths, const double* lambda, const double* lambda_host,
                           const uint64_t* seeds, double* log_evidence, uint32_t* iterations, uint8_t* status,
-                          double* trace, uint32_t trace_rows) {
+                          double* trace, uint32_t trace_rows, double* ensemble = nullptr) {
     std::vector<double> norm(n_runs);
     for (uint64_t r = 0; r < n_runs; ++r) {
         require(lambda_host[2 * r] > 0.0 && lambda_host[2 * r + 1] > 0.0, "invalid-argument",
@@ -650,6 +660,7 @@ static void anneal_device(vxb_ctx* ctx, const Design& design, uint64_t n_runs, u
     p.status = status;
     p.trace = trace;
     p.trace_rows = trace_rows;
+    p.ensemble = ensemble;
     const size_t smem = particles * 6 * sizeof(double);
     VXB_CUDA(cudaFuncSetAttribute(anneal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
@@ -666,7 +677,8 @@ static void anneal_device(vxb_ctx* ctx, const Design& design, uint64_t n_runs, u
             q.log_evidence += first;
             q.iterations += first;
             q.status += first;
-            if (q.trace) q.trace += first * trace_rows * 4;
+            if (q.trace) q.trace += first * trace_rows * 5;
+            if (q.ensemble) q.ensemble += first * 5 * particles;
             anneal_kernel<<<static_cast<unsigned>(count), kAnnealBlock, smem, ctx->stream>>>(q);
         }
         check_launch("anneal_kernel");
@@ -758,8 +770,8 @@ extern "C" int vxb_smc_bioassay(vxb_ctx* ctx, uint64_t n_runs, uint32_t groups, 
         Scratch it_tmp(ctx, n_runs * 4), st_tmp(ctx, n_runs);
         Staged d_it(ctx, iterations, n_runs * 4, false, true);
         Staged d_st(ctx, status, n_runs, false, true);
-        Staged d_tr(ctx, trace, n_runs * trace_rows * 32, false, true);
-        if (trace) VXB_CUDA(cudaMemsetAsync(d_tr.ptr(), 0, n_runs * trace_rows * 32, ctx->stream));
+        Staged d_tr(ctx, trace, n_runs * trace_rows * 40, false, true);
+        if (trace) VXB_CUDA(cudaMemsetAsync(d_tr.ptr(), 0, n_runs * trace_rows * 40, ctx->stream));
         anneal_device(ctx, d, n_runs, particles, c, scale, d_y.as<uint32_t>(), d_l.as<double>(), lambda,
                       d_s.as<uint64_t>(), d_ev.as<double>(),
                       iterations ? d_it.as<uint32_t>() : it_tmp.as<uint32_t>(),
@@ -771,6 +783,50 @@ extern "C" int vxb_smc_bioassay(vxb_ctx* ctx, uint64_t n_runs, uint32_t groups, 
         d_tr.finish();
         VXB_CUDA(cudaStreamSynchronize(ctx->stream));
         delete big;
+    });
+}
+
+// One run with its final ensemble: smc::run_smc (smc.cpp:352-488) on
+// make_bioassay_model(deaths, lambda) -> SmcResult.
+extern "C" int vxb_smc_bioassay_ensemble(vxb_ctx* ctx, uint32_t groups, const double* dose,
+                                         const uint32_t* group_size, const uint32_t* deaths,
+                                         const double* lambda, uint64_t seed, uint64_t particles,
+                                         uint64_t block_width, double c, double scale, double* log_evidence,
+                                         uint32_t* iterations, double* ensemble, double* trace,
+                                         uint32_t trace_rows) {
+    return guarded([&] {
+        use(ctx);
+        require(deaths && lambda && log_evidence && ensemble, "invalid-argument", "null argument");
+        check_sampler_args(particles, block_width, c);
+        for (uint32_t g = 0; g < groups; ++g)
+            require(deaths[g] <= group_size[g], "invalid-argument", "more deaths than animals in a group");
+        Scratch* big = nullptr;
+        const Design d = make_design(ctx, groups, dose, group_size, &big);
+        Staged d_y(ctx, deaths, groups * 4, true, false);
+        Staged d_l(ctx, lambda, 16, true, false);
+        Staged d_s(ctx, &seed, 8, true, false);
+        Scratch d_ev(ctx, 8), d_it(ctx, 4), d_st(ctx, 1);
+        Staged d_en(ctx, ensemble, particles * 40, false, true);
+        Staged d_tr(ctx, trace, static_cast<size_t>(trace_rows) * 40, false, true);
+        if (trace) VXB_CUDA(cudaMemsetAsync(d_tr.ptr(), 0, static_cast<size_t>(trace_rows) * 40, ctx->stream));
+        anneal_device(ctx, d, 1, particles, c, scale, d_y.as<uint32_t>(), d_l.as<double>(), lambda,
+                      d_s.as<uint64_t>(), d_ev.as<double>(), d_it.as<uint32_t>(), d_st.as<uint8_t>(),
+                      trace ? d_tr.as<double>() : nullptr, trace_rows, d_en.as<double>());
+        uint32_t it = 0;
+        uint8_t st = 0;
+        VXB_CUDA(cudaMemcpyAsync(log_evidence, d_ev.as<void>(), 8, cudaMemcpyDeviceToHost, ctx->stream));
+        VXB_CUDA(cudaMemcpyAsync(&it, d_it.as<void>(), 4, cudaMemcpyDeviceToHost, ctx->stream));
+        VXB_CUDA(cudaMemcpyAsync(&st, d_st.as<void>(), 1, cudaMemcpyDeviceToHost, ctx->stream));
+        d_en.finish();
+        d_tr.finish();
+        VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+        delete big;
+        if (iterations) *iterations = it;
+        // the reference raises here (smc.cpp:395-402, 208-211, 412-414)
+        require(st != kRunInvalidModel, "invalid-model", "log-likelihood is not finite at initialization");
+        require(st != kRunDegenerate, "degenerate-ensemble", "all weights are zero");
+        require(st != kRunNoConvergence, "non-convergence",
+                "temperature failed to reach 1 within the iteration cap");
     });
 }
 

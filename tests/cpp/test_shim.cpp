@@ -67,6 +67,30 @@ static int csv_mode(const char* bench_golden, const char* out_dir) {
     const double ev = weakinfo::log_evidence(draw.data, {10.0, 2.5}, 500, 4, 0.01, 1.6828427124746189, 3702, &its);
     std::printf("evidence %.17g %zu %u%u%u%u\n", ev, its, draw.data.deaths[0], draw.data.deaths[1],
                 draw.data.deaths[2], draw.data.deaths[3]);
+    {   // smc::run_smc as the reference's weak_info.cpp calls it (weak_info.cpp:199-208)
+        const auto d3 = weakinfo::sample_prior_predictive({4.0, 0.2}, design, 5);
+        smc::SmcConfig sc;
+        sc.particles = 64;
+        sc.scale = 1.6828427124746189;
+        sc.seed = 15;
+        std::ostringstream tr;
+        tr.precision(17);
+        sc.trace = &tr;
+        const smc::SmcResult res = smc::run_smc(weakinfo::make_bioassay_model(d3.data, {4.0, 0.2}), sc);
+        std::printf("run_smc %.17g %zu %zu %zu %.17g\n", res.log_evidence, res.iterations,
+                    res.ensemble.count, res.ensemble.dim, res.ensemble.temperature);
+        dump("run_smc_particles", res.ensemble.particles);
+        dump("run_smc_log_liks", res.ensemble.log_liks);
+        std::ofstream(dir + "/smc_trace.csv") << tr.str();
+        int refused = 0;
+        sc.esjd = true;
+        try { smc::run_smc(weakinfo::make_bioassay_model(d3.data, {4.0, 0.2}), sc); } catch (const Error& e) { refused += e.code() == "unsupported-config"; }
+        sc.esjd = false;
+        try { smc::run_smc(ModelHooks{}, sc); } catch (const Error& e) { refused += e.code() == "unsupported-model"; }
+        sc.particles = 6;
+        try { smc::run_smc(weakinfo::make_bioassay_model(d3.data, {4.0, 0.2}), sc); } catch (const Error& e) { refused += e.code() == "invalid-shape"; }
+        std::printf("run_smc_refused %d\n", refused);
+    }
     {
         bench::ExperimentSizes ws;
         bench::run_experiment_once(bench::Experiment::weakinfo, ws, 2, 4, 1337);

@@ -21,6 +21,7 @@ RUNS = [  # (lambda1, lambda2, data seed, sampler seed, particles)
     (10.0, 2.5, 1234, 3702, 500), (0.3, 15.0, 77, 231, 500), (4.0, 0.2, 5, 15, 64),
     (9.5, 19.0, 42, 4242, 500), (0.11, 0.13, 8, 88, 200), (2.0, 2.0, 9, 99, 1000),
 ]
+ENSEMBLE_RUN = 2
 TABLE = dict(hyper_count=3, datasets=12, particles=200, seed=1337)
 
 
@@ -39,6 +40,11 @@ def main():
     g["run_theta"], g["run_deaths"] = np.array(theta), np.array(deaths, dtype=np.uint32)
     g["run_evidence"], g["run_iterations"] = np.array(ev), np.array(it, dtype=np.uint64)
     g["run_trace"] = np.array(traces)  # temperature, ess, steps, p_acc per iteration
+    # the SmcResult of the third run (64 particles): final ensemble and evidence column
+    l1, l2, ds, ss, npart = RUNS[ENSEMBLE_RUN]
+    e = r.smc_bioassay_ensemble(DOSE, SIZE, deaths[ENSEMBLE_RUN], l1, l2, npart, 4, 0.01, H, ss)
+    g["ens_particles"], g["ens_trace"] = e["particles"], e["trace"]
+    g["ens_rows"] = np.stack([e["log_weights"], e["log_liks"], e["log_priors"]])
     beta = np.random.RandomState(3).normal(size=(64, 2)) * np.array([8.0, 12.0])
     g["ll_beta"] = beta
     g["ll_values"] = r.bioassay_ll(beta, DOSE, SIZE, [0, 2, 5, 1])

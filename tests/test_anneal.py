@@ -34,6 +34,14 @@ def test_oracle_matches_reference_golden(oracle, gold):
         # the reference prints its trace with 17 significant digits
         assert np.allclose(tr, gold["run_trace"][j][:it], rtol=1e-15, atol=0)
         assert np.array_equal(tr[:, 2:], gold["run_trace"][j][:it, 2:])
+    # the whole SmcResult of one run: final ensemble and the trace's evidence column
+    l1, l2, ds, ss, npart = G.RUNS[G.ENSEMBLE_RUN]
+    e = oracle.smc_bioassay_ensemble(G.DOSE, G.SIZE, gold["run_deaths"][G.ENSEMBLE_RUN], l1, l2, npart, 4,
+                                     0.01, G.H, ss)
+    assert e["log_evidence"] == gold["run_evidence"][G.ENSEMBLE_RUN]
+    assert np.array_equal(e["particles"], gold["ens_particles"])
+    assert np.array_equal(np.stack([e["log_weights"], e["log_liks"], e["log_priors"]]), gold["ens_rows"])
+    assert np.allclose(e["trace"], gold["ens_trace"], rtol=1e-15, atol=0)
     for redraw in (0, 1):
         t = oracle.weak_info_test(G.TABLE["hyper_count"], G.TABLE["datasets"], G.TABLE["particles"],
                                   seed=G.TABLE["seed"], redraw_base=bool(redraw), workers=4)
@@ -51,6 +59,10 @@ def test_oracle_matches_live_reference(oracle, ref):
         a = ref.smc_bioassay(G.DOSE, G.SIZE, y, l1, l2, 300, 8, 0.05, 0.9, 7 * trial)
         b = oracle.smc_bioassay(G.DOSE, G.SIZE, y, l1, l2, 300, 8, 0.05, 0.9, 7 * trial)
         assert a == b
+        ea = ref.smc_bioassay_ensemble(G.DOSE, G.SIZE, y, l1, l2, 300, 8, 0.05, 0.9, 7 * trial)
+        eb = oracle.smc_bioassay_ensemble(G.DOSE, G.SIZE, y, l1, l2, 300, 8, 0.05, 0.9, 7 * trial)
+        for k in ("particles", "log_weights", "log_liks", "log_priors"):
+            assert np.array_equal(ea[k], eb[k]), k
     a = ref.weak_info_test(2, 6, 100, seed=5)
     b = oracle.weak_info_test(2, 6, 100, seed=5)
     for k in a:
@@ -99,7 +111,7 @@ def test_device_sampler_matches_oracle(ctx, oracle, gold):
         assert np.array_equal(res["iterations"], gold["run_iterations"][sel])
         assert np.allclose(res["log_evidence"], gold["run_evidence"][sel], rtol=0, atol=1e-9)
         want = gold["run_trace"][sel]
-        assert np.array_equal(res["trace"][:, :, 2:], want[:, :, 2:])          # R_n and p_acc: identical
+        assert np.array_equal(res["trace"][:, :, 2:4], want[:, :, 2:])          # R_n and p_acc: identical
         assert np.allclose(res["trace"][:, :, :2], want[:, :, :2], rtol=1e-9, atol=1e-9)
     # a larger random batch against the oracle, other tuning constants and widths
     rs = np.random.RandomState(5)
@@ -121,6 +133,40 @@ def test_device_sampler_matches_oracle(ctx, oracle, gold):
     with pytest.raises(lib.VxbError) as e:
         ctx.smc_bioassay(G.DOSE, G.SIZE, [[9, 0, 0, 0]], lam[:1], seeds[:1], 64)
     assert e.value.code == "invalid-argument"
+
+
+@pytest.mark.gpu
+def test_device_run_smc_result(ctx, oracle, gold):
+    """vxb_smc_bioassay_ensemble = smc::run_smc's SmcResult: same accept/resample decisions,
+    so the final ensemble agrees to rounding (the proposal factor differs by ulps)."""
+    l1, l2, ds, ss, npart = G.RUNS[G.ENSEMBLE_RUN]
+    e = ctx.smc_bioassay_ensemble(G.DOSE, G.SIZE, gold["run_deaths"][G.ENSEMBLE_RUN], [l1, l2], ss, npart,
+                                  scale=G.H)
+    assert e["iterations"] == gold["run_iterations"][G.ENSEMBLE_RUN]
+    assert abs(e["log_evidence"] - gold["run_evidence"][G.ENSEMBLE_RUN]) < 1e-9
+    assert np.allclose(e["particles"], gold["ens_particles"], rtol=1e-9, atol=1e-9)
+    assert np.allclose(np.stack([e["log_weights"], e["log_liks"], e["log_priors"]]), gold["ens_rows"],
+                       rtol=1e-9, atol=1e-9)
+    assert np.array_equal(e["trace"][:, 2:4], gold["ens_trace"][:, 2:4])
+    assert np.allclose(e["trace"], gold["ens_trace"], rtol=1e-9, atol=1e-9)
+    rs = np.random.RandomState(21)
+    for trial, (npart, bw) in enumerate(((1000, 4), (250, 8), (2000, 4), (96, 16))):
+        l1, l2 = rs.uniform(0.1, 10.0), rs.uniform(0.1, 20.0)
+        _, y = oracle.bioassay_sample(l1, l2, G.DOSE, G.SIZE, 50 + trial)
+        want = oracle.smc_bioassay_ensemble(G.DOSE, G.SIZE, y, l1, l2, npart, bw, 0.01, 0.0, 900 + trial)
+        got = ctx.smc_bioassay_ensemble(G.DOSE, G.SIZE, y, [l1, l2], 900 + trial, npart, block_width=bw,
+                                        scale=0.0)
+        assert got["iterations"] == want["iterations"]
+        assert abs(got["log_evidence"] - want["log_evidence"]) < 1e-9
+        for k in ("particles", "log_weights", "log_liks", "log_priors", "trace"):
+            assert np.allclose(got[k], want[k], rtol=1e-9, atol=1e-9), (trial, k)
+        # the batched entry point runs the same sampler
+        one = ctx.smc_bioassay(G.DOSE, G.SIZE, [y], [[l1, l2]], [900 + trial], npart, block_width=bw, scale=0.0)
+        assert one["log_evidence"][0] == got["log_evidence"]
+    # sampler failures are errors here, as in the reference (status codes in the batched call)
+    with pytest.raises(lib.VxbError) as err:
+        ctx.smc_bioassay_ensemble(G.DOSE, G.SIZE, [0, 0, 0, 0], [1.0, 1.0], 1, 7)
+    assert err.value.code == "invalid-shape"
 
 
 @pytest.mark.gpu
@@ -179,7 +225,7 @@ def test_device_sampler_other_designs_and_sizes(ctx, oracle):
             assert res["status"][j] == 0 and res["iterations"][j] == it
             assert abs(res["log_evidence"][j] - ev) < 1e-9
             k = min(it, 6)
-            assert np.array_equal(res["trace"][j, :k, 2:], tr[:k, 2:])
+            assert np.array_equal(res["trace"][j, :k, 2:4], tr[:k, 2:])
     # the whole test on a non-default design
     cfg = M.weakinfo_config(hyper_count=3, datasets=10, particles=96, seed=5, dose=(-1.0, 0.0, 0.5),
                             group_size=(8, 4, 6))

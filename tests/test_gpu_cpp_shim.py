@@ -94,6 +94,18 @@ def test_cpp_shim_reference_format_outputs(tmp_path, golden, oracle):
     assert abs(float(r["evidence"][0]) - anneal["run_evidence"][0]) < 1e-9
     assert int(r["evidence"][1]) == anneal["run_iterations"][0]
     assert r["evidence"][2] == "".join(str(v) for v in anneal["run_deaths"][0])
+    k = 2  # make_golden_anneal.ENSEMBLE_RUN: (4.0, 0.2, data seed 5, sampler seed 15, 64 particles)
+    assert abs(float(r["run_smc"][0]) - anneal["run_evidence"][k]) < 1e-9
+    assert [int(t) for t in r["run_smc"][1:4]] == [int(anneal["run_iterations"][k]), 64, 2]
+    assert float(r["run_smc"][4]) == 1.0
+    assert np.allclose(hexd(r["run_smc_particles"]).reshape(64, 2), anneal["ens_particles"], rtol=1e-9, atol=1e-9)
+    assert np.allclose(hexd(r["run_smc_log_liks"]), anneal["ens_rows"][1], rtol=1e-9, atol=1e-9)
+    lines = read(tmp_path / "smc_trace.csv").strip().splitlines()
+    assert lines[0] == "n,t_n,ess,log_evidence,R_n,p_acc,h"
+    rows = np.array([[float(x) for x in ln.split(",")] for ln in lines[1:]])
+    assert rows[:, 0].tolist() == [1.0, 2.0]
+    assert np.allclose(rows[:, [1, 2, 4, 5, 3]], anneal["ens_trace"], rtol=1e-9, atol=1e-9)
+    assert r["run_smc_refused"] == ["3"]
     tb_obs = oracle.tb_observed(10, 10.0, 10000.0, 1337)
     tb_rows = oracle.tb_abc_particle(10, 10.0, 10000.0, 0, 40, 1337, tb_obs)
     assert [float(t) for t in r["tb"][:4]] == [tb_obs[0], tb_obs[1], tb_rows[1][0, 0], tb_rows[2][1]]
