@@ -16,10 +16,14 @@ n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 100000
 m = M.tb_model(10, 10.0, 10000.0)
 obs = B.tb_observed_summaries(ctx, 10, 10.0, 10000.0, 1337, 4)
 ctx.abc_prior_predictive_host(m, M.keying(1), 2000, 0, 2000, obs)
+ctx.profile_enable(True)
+ctx.profile_reset()
 t0 = time.perf_counter()
 p, s, rho, f = ctx.abc_prior_predictive_host(m, M.keying(1337), n, 0, n, obs)
 dt = time.perf_counter() - t0
-out = {"rows": n, "seconds": dt, "rows_per_s": n / dt, "failed": int(f.sum()),
+kernel_ms = ctx.profile_read()["simulate"]["total_ms"]
+ctx.profile_enable(False)
+out = {"rows": n, "seconds": dt, "rows_per_s": n / dt, "kernel_ms": kernel_ms, "failed": int(f.sum()),
        "mean_genotypes": float(s[f == 0, 0].mean()), "max_genotypes": float(s[:, 0].max())}
 try:
     from oracle.pyoracle import Ref
