@@ -35,6 +35,10 @@ trho = torch.empty(296, dtype=torch.float64, device="cuda")
 ctx.abc_prior_predictive(tm, M.keying(1337), 296, 0, 296, tobs, rho=trho)
 ctx.synchronize()
 print("toggle", float(trho[0]))
+tmf = M.toggle_model(600, 8000, rng=A.VXB_RNG_FAST)   # throughput instance, same sizes
+ctx.abc_prior_predictive(tmf, M.keying(1337), 296, 0, 296, tobs, rho=trho)
+ctx.synchronize()
+print("toggle throughput mode", float(trho[0]))
 # annealed SMC: 8 020 sampler runs (K = 9, N = 401) of 500 particles
 wcfg = M.weakinfo_config(hyper_count=9, datasets=401, particles=500, seed=1337)
 print("weakinfo", ctx.weak_info_test(wcfg)["gamma"][:3])
