@@ -18,6 +18,10 @@
 #include "vxb_common.cuh"
 #include "vxb_logistic.cuh"
 
+#ifndef VXB_PPP_MINB
+#define VXB_PPP_MINB 1
+#endif
+
 namespace vxb {
 
 constexpr int kPppBlock = 256;
@@ -38,7 +42,7 @@ struct PppParams {
 };
 
 template <int kRng>
-__global__ void __launch_bounds__(kPppBlock) ppp_kernel(const __grid_constant__ PppParams p) {
+__global__ void __launch_bounds__(kPppBlock, VXB_PPP_MINB) ppp_kernel(const __grid_constant__ PppParams p) {
     __shared__ double2 s_log[kRng == VXB_RNG_FAST ? kFastTableSize : 1];
     __shared__ unsigned int s_count;
     if (kRng == VXB_RNG_FAST)

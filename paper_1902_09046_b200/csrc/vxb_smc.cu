@@ -21,6 +21,10 @@
 
 #include "vxb_internal.cuh"
 
+#ifndef VXB_PROP_MINB
+#define VXB_PROP_MINB 1
+#endif
+
 namespace vxb {
 
 constexpr int kChunk = 256;  // canonical reduction chunk (oracle: kChunk)
@@ -343,7 +347,7 @@ struct ProposeParams {
 // One proposal per thread (layout: vxo_abcsmc_propose): position 0 ancestor
 // uniform, positions 2..4 the Gaussian increments, position 6+j the normal of
 // simulation step j+1.
-__global__ void __launch_bounds__(256) abcsmc_propose_kernel(const __grid_constant__ ProposeParams p) {
+__global__ void __launch_bounds__(256, VXB_PROP_MINB) abcsmc_propose_kernel(const __grid_constant__ ProposeParams p) {
     const uint64_t r = static_cast<uint64_t>(blockIdx.x) * 256 + threadIdx.x;
     if (r >= p.count) return;
     const uint64_t key = stream_key(p.seed_hash, p.first + r);

@@ -28,6 +28,10 @@
 #include "vxb_common.cuh"
 #include "vxb_rng.cuh"
 
+#ifndef VXB_TL_MINB
+#define VXB_TL_MINB 4  // swept 1, 4, 6, 8: config 4 exact 1.01 / 0.94 / 0.99 / 0.99 s
+#endif
+
 namespace vxb {
 
 constexpr int kTlBlock = 128;
@@ -107,7 +111,7 @@ __device__ __forceinline__ void draw_pair(const TauParams& p, uint64_t key, uint
 }
 
 template <int kRng>
-__global__ void __launch_bounds__(kTlBlock) tauleap_kernel(const __grid_constant__ TauParams p) {
+__global__ void __launch_bounds__(kTlBlock, VXB_TL_MINB) tauleap_kernel(const __grid_constant__ TauParams p) {
     using PA = typename std::conditional<kRng == VXB_RNG_REF, Exact, Fused>::type;
     __shared__ double s_inv[kMaxPoisson + 1];
     __shared__ long long s_sum[4];
