@@ -32,7 +32,7 @@ void order_statistics_any(vxb_ctx* ctx, int precision, const void* rho_dev,
                           const uint8_t* failed_dev, uint64_t n, const uint64_t* ranks,
                           int n_ranks, double* values);
 uint64_t count_valid_any(vxb_ctx* ctx, int precision, const void* rho_dev,
-                         const uint8_t* failed_dev, uint64_t n);
+                         const uint8_t* failed_dev, uint64_t n, uint64_t* only_flag = nullptr);
 // type-7 quantile (numeric.cpp:20-36) of n device-resident values (all valid)
 double quantile_device(vxb_ctx* ctx, const double* values_dev, uint64_t n, double level);
 
