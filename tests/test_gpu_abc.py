@@ -227,6 +227,25 @@ def test_order_statistics_f32_and_f64(ctx):
         ranks = [0, 1, 25000, 50000]
         vals, nv = ctx.order_statistics(x, None, ranks)
         assert nv == x.size and eq(vals, np.sort(x)[ranks].astype(np.float64))
+        # ranks that share their prefixes to the last digit pass (neighbours, repeats), a
+        # batch of more ranks than one selection carries, values of both signs with ties
+        y = np.round(rs.standard_normal(200003) * 3, 2).astype(dt)
+        ranks = [7, 7, 8, 100001, 100002, 100001, 200002, 0, 150000]
+        vals, nv = ctx.order_statistics(y, None, ranks)
+        assert nv == y.size and eq(vals, np.sort(y)[ranks].astype(np.float64))
+        # flags that exclude finite rows (the digit passes must read them) and NaN rows
+        # whose flags add nothing (they may skip them): same answer as a host sort
+        z = (rs.standard_normal(70001) * 10).astype(dt)
+        z[rs.randint(0, z.size, 500)] = np.nan
+        only_nan = np.isnan(z).astype(np.uint8)
+        extra = only_nan.copy()
+        extra[rs.randint(0, z.size, 900)] = 1
+        for flags in (only_nan, extra, None):
+            keep = ~np.isnan(z) if flags is None else (~np.isnan(z)) & (flags == 0)
+            want = np.sort(z[keep])
+            ranks = [0, 1, want.size // 2, want.size // 2 + 1, want.size - 1]
+            vals, nv = ctx.order_statistics(z, flags, ranks)
+            assert nv == want.size and eq(vals, want[ranks].astype(np.float64))
 
 
 @pytest.mark.parametrize("precision", [A.VXB_F64, A.VXB_F32])
