@@ -349,13 +349,16 @@ int vxb_make_kernel(const double* cov, uint32_t dim, double scale, double jitter
  *   evidence_of closure of weak_info.cpp:200-215.  One CTA per run.  status[r]:
  *   0 ok, 1 invalid-model, 2 degenerate-ensemble, 3 non-convergence (the errors
  *   the reference turns into a skipped evidence); log_evidence is NaN then.
- *   trace (optional): n_runs x trace_rows x 5 doubles per iteration: temperature,
- *   ESS after reweighting, move steps R_n, pilot acceptance, log evidence so far
- *   (the columns of SmcConfig::trace, smc.hpp:125).
+ *   trace (optional): n_runs x trace_rows x 6 doubles per iteration: temperature,
+ *   ESS after reweighting, move steps R_n, pilot acceptance, log evidence so far,
+ *   proposal scale h (the columns of SmcConfig::trace, smc.hpp:125).
  * vxb_smc_bioassay_ensemble: ONE run returning what SmcResult holds: log evidence,
  *   iterations and the final ensemble as 5 x particles doubles (theta0, theta1,
  *   log weights, log likelihoods, log priors); sampler failures are errors
  *   (invalid-model / degenerate-ensemble / non-convergence) as in the reference.
+ *   n_scales > 0 (at most 16): SmcConfig::esjd = true with esjd_scales as the grid --
+ *   the ESJD scale adaptation (esjd_core, smc.cpp:156-204) replaces the pilot sweep
+ *   and the fixed number of move steps; `scale` is then unused.
  *   deaths, lambda, seeds: host arrays.  particles <= 2048. */
 int vxb_bioassay_log_likelihood(vxb_ctx* ctx, const double* beta, uint64_t lanes, uint32_t groups,
                                 const double* dose, const uint32_t* group_size,
@@ -374,7 +377,7 @@ int vxb_smc_bioassay_ensemble(vxb_ctx* ctx, uint32_t groups, const double* dose,
                               const double* lambda, uint64_t seed, uint64_t particles,
                               uint64_t block_width, double c, double scale, double* log_evidence,
                               uint32_t* iterations, double* ensemble, double* trace,
-                              uint32_t trace_rows);
+                              uint32_t trace_rows, const double* esjd_scales, uint32_t n_scales);
 
 /* WeakInfoConfig (weak_info.hpp:62-75) as a POD; `workers` has no device meaning
  * (all 2 (K+1) N sampler runs are one launch). */

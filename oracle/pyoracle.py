@@ -155,14 +155,17 @@ class Oracle(_Base):
         return ev.value, it.value, tr[:it.value]
 
     def smc_bioassay_ensemble(self, dose, group_size, deaths, lambda1, lambda2, particles,
-                              block_width, c, scale, seed):
-        """SmcResult of one run; trace columns: temperature, ess, steps, p_acc, log evidence."""
+                              block_width, c, scale, seed, esjd_scales=None):
+        """SmcResult of one run; trace columns: temperature, ess, steps, p_acc, log evidence,
+        proposal scale.  esjd_scales: the scale grid of the ESJD adaptation (None: fixed scale)."""
         d, g, y = self._design(dose, group_size, deaths)
         ev, it = f64(), u64()
-        ens, tr = np.zeros((5, particles)), np.zeros((1000, 5))
+        ens, tr = np.zeros((5, particles)), np.zeros((1000, 6))
+        sc = None if esjd_scales is None else np.ascontiguousarray(esjd_scales, dtype=np.float64)
         self._call("smc_bioassay_ensemble", _ptr(d), _ptr(g), _ptr(y), u32(d.size), f64(lambda1),
                    f64(lambda2), u64(particles), u64(block_width), f64(c), f64(scale), u64(seed),
-                   C.byref(ev), C.byref(it), _ptr(ens), _ptr(tr), u64(1000))
+                   C.byref(ev), C.byref(it), _ptr(ens), _ptr(tr), u64(1000), _ptr(sc),
+                   u64(0 if sc is None else sc.size))
         return dict(log_evidence=ev.value, iterations=it.value, particles=ens[:2].T.copy(),
                     log_weights=ens[2], log_liks=ens[3], log_priors=ens[4], trace=tr[:it.value])
 
@@ -414,19 +417,21 @@ class Ref(_Base):
         return ev.value, it.value, full[:, [1, 2, 4, 5]]       # temperature, ess, steps, p_acc
 
     def smc_bioassay_ensemble(self, dose, group_size, deaths, lambda1, lambda2, particles,
-                              block_width, c, scale, seed):
+                              block_width, c, scale, seed, esjd_scales=None):
         d, g, y = self._design(dose, group_size, deaths)
         ev, it = f64(), u64()
         ens = np.zeros((5, particles))
         buf = C.create_string_buffer(1 << 16)
+        sc = None if esjd_scales is None else np.ascontiguousarray(esjd_scales, dtype=np.float64)
         self._call("smc_bioassay_ensemble", _ptr(d), _ptr(g), _ptr(y), u32(d.size), f64(lambda1),
                    f64(lambda2), u64(particles), u64(block_width), f64(c), f64(scale), u64(seed),
-                   C.byref(ev), C.byref(it), _ptr(ens), buf, u64(len(buf)))
+                   C.byref(ev), C.byref(it), _ptr(ens), buf, u64(len(buf)), _ptr(sc),
+                   u64(0 if sc is None else sc.size))
         rows = [ln.split(",") for ln in buf.value.decode().strip().splitlines()[1:]]
         full = np.array([[float(x) for x in r] for r in rows])  # n,t_n,ess,log_evidence,R_n,p_acc,h
         return dict(log_evidence=ev.value, iterations=it.value, particles=ens[:2].T.copy(),
                     log_weights=ens[2], log_liks=ens[3], log_priors=ens[4],
-                    trace=full[:, [1, 2, 4, 5, 3]], trace_text=buf.value.decode())
+                    trace=full[:, [1, 2, 4, 5, 3, 6]], trace_text=buf.value.decode())
 
     def splitmix64(self, z):
         return int(self.lib.ref_splitmix64(z))

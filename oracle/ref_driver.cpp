@@ -590,7 +590,8 @@ int ref_smc_bioassay_ensemble(const double* dose, const std::uint32_t* group_siz
                               double lambda2, std::uint64_t particles, std::uint64_t block_width,
                               double c, double scale, std::uint64_t seed, double* log_evidence,
                               std::uint64_t* iterations, double* ensemble, char* trace,
-                              std::uint64_t trace_cap) {
+                              std::uint64_t trace_cap, const double* esjd_scales,
+                              std::uint64_t n_scales) {
     return guarded([&] {
         smc::SmcConfig cfg;
         cfg.particles = particles;
@@ -599,6 +600,10 @@ int ref_smc_bioassay_ensemble(const double* dose, const std::uint32_t* group_siz
         cfg.c = c;
         cfg.scale = scale;
         cfg.seed = seed;
+        if (n_scales) {
+            cfg.esjd = true;
+            cfg.esjd_scales.assign(esjd_scales, esjd_scales + n_scales);
+        }
         std::ostringstream text;
         text.precision(17);
         if (trace) cfg.trace = &text;

@@ -1421,12 +1421,12 @@ static void bioassay_draw(double l1, double l2, const double* dose, const std::u
 }
 
 struct AnnealTrace {
-    std::vector<double> temperature, ess, accept, evidence;
+    std::vector<double> temperature, ess, accept, evidence, scale;
     std::vector<std::uint64_t> steps;
 };
 
 // stream ids of the sampler: (iteration << 16) | (worker << 2) | role, smc.cpp:21-28
-enum { kPilotRole = 0, kMoveRole = 1, kCoordinatorRole = 3 };
+enum { kPilotRole = 0, kMoveRole = 1, kTrialRole = 2, kCoordinatorRole = 3 };
 static std::uint64_t anneal_stream(std::uint64_t iteration, std::uint64_t role) {
     return static_cast<std::uint32_t>((iteration << 16) | role);
 }
@@ -1463,14 +1463,19 @@ struct Annealed {
         return temperature + 0.5 * (lo + hi);
     }
     // one tempered random-walk sweep of `steps` steps: move_range, smc.cpp:77-150
-    std::uint64_t sweep(const double* chol, double h, std::uint64_t role, std::uint64_t iteration,
-                        std::uint64_t steps) {
+    // `base`: stream position the sweep starts at (even); `scales`: per-particle
+    // proposal scales, assigned cyclically (ESJD trial); `jumps`: h^2 |z|^2 of the
+    // accepted proposals is added per particle (smc.cpp:138-144)
+    std::uint64_t sweep(const double* chol, double h_all, std::uint64_t role, std::uint64_t iteration,
+                        std::uint64_t steps, std::uint64_t base = 0, const double* scales = nullptr,
+                        std::uint64_t n_scales = 0, double* jumps = nullptr) {
         const std::uint64_t gauss_total = np * steps * 2;
         std::uint64_t accepted = 0;
         Stream s(seed, anneal_stream(iteration, role));
         for (std::uint64_t q = 0; q < np; ++q)
             for (std::uint64_t r = 0; r < steps; ++r) {
-                s.pos = (q * steps + r) * 2;
+                const double h = n_scales ? scales[q % n_scales] : h_all;
+                s.pos = base + (q * steps + r) * 2;
                 const double z0 = s.next_gaussian(0.0, 1.0), z1 = s.next_gaussian(0.0, 1.0);
                 double inc0 = 0.0, inc1 = 0.0;
                 inc0 += chol[0] * z0;
@@ -1480,7 +1485,7 @@ struct Annealed {
                 const double lp_new = model.log_prior(p0, p1);
                 const double ll_new = model.log_lik(p0, p1);
                 const double log_alpha = temperature * (ll_new - ll[q]) + lp_new - lp[q];
-                s.pos = gauss_total + q * steps + r;
+                s.pos = base + gauss_total + q * steps + r;
                 const double u = s.next_unit();
                 const double log_u = u > 0.0 ? ln_pos(u) : -std::numeric_limits<double>::infinity();
                 if (!std::isnan(log_alpha) && log_alpha > -std::numeric_limits<double>::infinity() &&
@@ -1490,15 +1495,34 @@ struct Annealed {
                     theta[2 * q + 1] = p1;
                     ll[q] = ll_new;
                     lp[q] = lp_new;
+                    if (jumps) {
+                        double zz = 0.0;
+                        zz += z0 * z0;
+                        zz += z1 * z1;
+                        jumps[q] += h * h * zz;
+                    }
                 }
             }
         return accepted;
     }
 };
 
+// type-7 median of a sample (numeric.cpp:20-36,53)
+static double median_of(std::vector<double> v) {
+    std::sort(v.begin(), v.end());
+    const std::size_t n = v.size();
+    if (n == 1) return v[0];
+    const double h = static_cast<double>(n - 1) * 0.5;
+    const std::size_t lo = static_cast<std::size_t>(h);
+    if (lo + 1 >= n) return v[n - 1];
+    const double frac = h - static_cast<double>(lo);
+    return v[lo] + frac * (v[lo + 1] - v[lo]);
+}
+
 static void anneal_run(const Bioassay& model, std::uint64_t np, std::uint64_t block_width, double c,
                        double scale, std::uint64_t seed, double* log_evidence,
-                       std::uint64_t* iterations, AnnealTrace* trace, double* ensemble = nullptr) {
+                       std::uint64_t* iterations, AnnealTrace* trace, double* ensemble = nullptr,
+                       const double* esjd_scales = nullptr, std::uint64_t n_scales = 0) {
     const double tol = 1e-10, jitter = 1e-10;            // SmcConfig defaults, smc.hpp:120-121
     const std::uint64_t max_iterations = 1000, step_cap = 100;
     require(supported_width(block_width), "invalid-shape", "unsupported block width");
@@ -1566,20 +1590,60 @@ static void anneal_run(const Bioassay& model, std::uint64_t np, std::uint64_t bl
             require(vxo_make_kernel(cov, 2, 1.0, jitter, chol) == 0, "degenerate-ensemble",
                     "covariance is rank deficient beyond jitter");
         }
-        const std::uint64_t pilot = a.sweep(chol, h, kPilotRole, n, 1);
-        const double p_acc = static_cast<double>(pilot) / static_cast<double>(np);
-        // steps_from_acceptance: smc.cpp:302-309
-        const double p = std::min(std::max(p_acc, 0.01), 0.99);
-        const double raw = std::ceil(std::log(c) / std::log(1.0 - p));
-        const std::uint64_t steps =
-            !(raw >= 1.0) ? 1 : std::min<std::uint64_t>(static_cast<std::uint64_t>(raw), step_cap);
-        a.sweep(chol, h, kMoveRole, n, steps);
+        double p_acc, h_used;
+        std::uint64_t steps;
+        if (!n_scales) {
+            const std::uint64_t pilot = a.sweep(chol, h, kPilotRole, n, 1);
+            p_acc = static_cast<double>(pilot) / static_cast<double>(np);
+            // steps_from_acceptance: smc.cpp:302-309
+            const double p = std::min(std::max(p_acc, 0.01), 0.99);
+            const double raw = std::ceil(std::log(c) / std::log(1.0 - p));
+            steps = !(raw >= 1.0) ? 1 : std::min<std::uint64_t>(static_cast<std::uint64_t>(raw), step_cap);
+            a.sweep(chol, h, kMoveRole, n, steps);
+            h_used = h;
+        } else {
+            // esjd_core: smc.cpp:156-204 (streams: trial role for the trial step, move role,
+            // continued from sweep to sweep, for the moves)
+            std::vector<double> jumps(np, 0.0);
+            const std::uint64_t trial = a.sweep(chol, 0.0, kTrialRole, n, 1, 0, esjd_scales, n_scales, jumps.data());
+            p_acc = static_cast<double>(trial) / static_cast<double>(np);
+            const double trial_median = median_of(jumps);
+            double best = -1.0;
+            bool any_jump = false;
+            h_used = 0.0;
+            for (std::uint64_t sidx = 0; sidx < n_scales; ++sidx) {
+                std::vector<double> part;
+                for (std::uint64_t i = sidx; i < np; i += n_scales) part.push_back(jumps[i]);
+                if (part.empty()) continue;
+                const double med = median_of(part);
+                if (med > 0.0) any_jump = true;
+                if (med > best) {
+                    best = med;
+                    h_used = esjd_scales[sidx];
+                }
+            }
+            if (!any_jump)
+                for (double j : jumps) any_jump = any_jump || j > 0.0;
+            if (!any_jump) h_used = 2.38 / std::sqrt(2.0);
+            steps = 0;
+            std::uint64_t pos = 0;  // position of the move stream
+            while (steps < step_cap) {
+                std::uint64_t moved = 0;
+                for (double cj : jumps) moved += cj > trial_median ? 1 : 0;
+                if (2 * moved >= np) break;
+                pos += pos & 1;  // align_even
+                a.sweep(chol, h_used, kMoveRole, n, 1, pos, nullptr, 0, jumps.data());
+                pos += 3 * np;
+                ++steps;
+            }
+        }
         if (trace) {
             trace->temperature.push_back(a.temperature);
             trace->ess.push_back(ess_now);
             trace->accept.push_back(p_acc);
             trace->steps.push_back(steps);
             trace->evidence.push_back(a.log_evidence);
+            trace->scale.push_back(h_used);
         }
     }
     *log_evidence = a.log_evidence;
@@ -1616,17 +1680,20 @@ int vxo_smc_bioassay_ensemble(const double* dose, const std::uint32_t* group_siz
                               double lambda2, std::uint64_t particles, std::uint64_t block_width,
                               double c, double scale, std::uint64_t seed, double* log_evidence,
                               std::uint64_t* iterations, double* ensemble, double* trace_out,
-                              std::uint64_t trace_cap) {
+                              std::uint64_t trace_cap, const double* esjd_scales,
+                              std::uint64_t n_scales) {
     return guarded([&] {
         const Bioassay m = make_bioassay(dose, group_size, deaths, groups, lambda1, lambda2);
         AnnealTrace tr;
-        anneal_run(m, particles, block_width, c, scale, seed, log_evidence, iterations, &tr, ensemble);
+        anneal_run(m, particles, block_width, c, scale, seed, log_evidence, iterations, &tr, ensemble,
+                   esjd_scales, n_scales);
         for (std::uint64_t i = 0; trace_out && i < tr.steps.size() && i < trace_cap; ++i) {
-            trace_out[5 * i] = tr.temperature[i];
-            trace_out[5 * i + 1] = tr.ess[i];
-            trace_out[5 * i + 2] = static_cast<double>(tr.steps[i]);
-            trace_out[5 * i + 3] = tr.accept[i];
-            trace_out[5 * i + 4] = tr.evidence[i];
+            trace_out[6 * i] = tr.temperature[i];
+            trace_out[6 * i + 1] = tr.ess[i];
+            trace_out[6 * i + 2] = static_cast<double>(tr.steps[i]);
+            trace_out[6 * i + 3] = tr.accept[i];
+            trace_out[6 * i + 4] = tr.evidence[i];
+            trace_out[6 * i + 5] = tr.scale[i];
         }
     });
 }

@@ -88,12 +88,14 @@ struct SmcResult {
 // smc::run_smc (smc.cpp:352-488): the whole adaptive sampler is ONE kernel with
 // the ensemble in shared memory (csrc/vxb_anneal.cu), so the model has to be one
 // the kernel knows: the bioassay model of the case study (make_bioassay_model).
-// ESJD adaptation and non-default tolerances/caps are fixed on the device and
-// rejected here rather than silently ignored.
+// Non-default tolerances/caps are fixed on the device and rejected here rather than
+// silently ignored; the ESJD scale adaptation (config.esjd) runs on the device with a
+// grid of up to 16 scales.
 inline SmcResult run_smc(const ModelHooks& model, const SmcConfig& cfg) {
     require(model.family && std::string_view(model.family) == "bioassay" && model.binding,
             "unsupported-model", "run_smc on the device needs make_bioassay_model()");
-    require(!cfg.esjd, "unsupported-config", "ESJD scale adaptation is not built on the device");
+    require(!cfg.esjd || (!cfg.esjd_scales.empty() && cfg.esjd_scales.size() <= 16), "invalid-argument",
+            cfg.esjd_scales.empty() ? "scale grid must not be empty" : "at most 16 ESJD scales on the device");
     require(cfg.bisection_tol == 1e-10 && cfg.jitter == 1e-10 && cfg.max_iterations == 1000 &&
                 cfg.step_cap == 100,
             "unsupported-config", "tolerance, jitter and caps are fixed at the reference defaults");
@@ -102,14 +104,15 @@ inline SmcResult run_smc(const ModelHooks& model, const SmcConfig& cfg) {
     const std::size_t np = cfg.particles;
     const double lam[2] = {b.prior.lambda1, b.prior.lambda2};
     const std::uint32_t rows = 1000;
-    std::vector<double> packed(5 * np), trace(cfg.trace ? rows * 5 : 0);
+    std::vector<double> packed(5 * np), trace(cfg.trace ? rows * 6 : 0);
     SmcResult r;
     std::uint32_t it = 0;
     cuda::check(vxb_smc_bioassay_ensemble(
         cuda::context(), static_cast<std::uint32_t>(b.data.groups()), b.data.dose.data(),
         b.data.group_size.data(), b.data.deaths.data(), lam, cfg.seed, np, cfg.block_width, cfg.c,
         cfg.scale, &r.log_evidence, &it, packed.data(), cfg.trace ? trace.data() : nullptr,
-        cfg.trace ? rows : 0));
+        cfg.trace ? rows : 0, cfg.esjd ? cfg.esjd_scales.data() : nullptr,
+        cfg.esjd ? static_cast<std::uint32_t>(cfg.esjd_scales.size()) : 0));
     r.iterations = it;
     ParticleEnsemble& e = r.ensemble;
     e.count = np;
@@ -126,12 +129,11 @@ inline SmcResult run_smc(const ModelHooks& model, const SmcConfig& cfg) {
     e.log_evidence = r.log_evidence;
     e.iteration = it;
     if (cfg.trace) {
-        const double h = cfg.scale > 0.0 ? cfg.scale : 2.38 / std::sqrt(2.0);
         *cfg.trace << "n,t_n,ess,log_evidence,R_n,p_acc,h\n";
         for (std::uint32_t n = 0; n < it; ++n) {
-            const double* row = &trace[5 * n];
+            const double* row = &trace[6 * n];
             *cfg.trace << (n + 1) << ',' << row[0] << ',' << row[1] << ',' << row[4] << ','
-                       << static_cast<std::size_t>(row[2]) << ',' << row[3] << ',' << h << '\n';
+                       << static_cast<std::size_t>(row[2]) << ',' << row[3] << ',' << row[5] << '\n';
         }
     }
     return r;

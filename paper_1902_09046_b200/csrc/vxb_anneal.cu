@@ -42,7 +42,7 @@ constexpr uint32_t kMaxIterations = 1000;  // SmcConfig defaults, smc.hpp:119-12
 constexpr uint32_t kStepCap = 100;
 constexpr double kBisectionTol = 1e-10;
 constexpr double kJitter = 1e-10;
-enum { kRolePilot = 0, kRoleMove = 1, kRoleCoordinator = 3 };       // smc.cpp:21-24
+enum { kRolePilot = 0, kRoleMove = 1, kRoleTrial = 2, kRoleCoordinator = 3 };       // smc.cpp:21-24
 enum { kRunOk = 0, kRunInvalidModel = 1, kRunDegenerate = 2, kRunNoConvergence = 3 };
 
 __host__ __device__ inline uint64_t derive_seed_dev(uint64_t seed, const uint64_t* path, int n) {
@@ -97,6 +97,7 @@ __device__ __forceinline__ double log_prior(const RunModel& m, double b0, double
 // reading), and every thread finishes the reduction itself in warp order -- the
 // result is the same value in every thread, a pure function of the inputs.
 constexpr int kAnnealWarps = kAnnealBlock / 32;
+constexpr int kMaxEsjdScales = 16;
 struct BlockScratch {
     double a[2][kAnnealWarps], b[2][kAnnealWarps];
     double scan[kAnnealWarps];  // warp totals of the cumulative-weight scan
@@ -186,23 +187,31 @@ struct AnnealParams {
     double* log_evidence;
     uint32_t* iterations;
     uint8_t* status;
-    double* trace;            // optional: n_runs x trace_rows x 5 (temperature, ess, steps, p_acc, log evidence)
+    double* trace;            // optional: n_runs x trace_rows x 6 (temperature, ess, steps, p_acc, log evidence, scale)
     uint32_t trace_rows;
     double* ensemble;         // optional: n_runs x 5 x np (theta0, theta1, log w, log L, log prior)
+    uint32_t n_scales;        // ESJD scale adaptation (kEsjd instance): the scale grid
+    double scales[kMaxEsjdScales];
 };
 
 // One tempered random-walk sweep (move_range, smc.cpp:77-150): particle q, step r
 // reads the Gaussian pair q*R + r and the uniform at 2 np R + q R + r of stream
 // (seed, id).  Returns this thread's number of accepted proposals.
+// The ESJD instance (kJumps) starts at stream position `base` (even), takes the
+// proposal scale of particle q from a cyclic grid when one is given, and adds
+// h^2 |z|^2 of every accepted proposal to jumps[q] (smc.cpp:138-144).
+template <bool kJumps = false>
 __device__ uint32_t sweep(const Design& d, const RunModel& m, Ensemble& e, uint32_t np, uint64_t key,
-                          uint32_t steps, double temperature, double h, double l00, double l10,
-                          double l11) {
+                          uint32_t steps, double temperature, double h_all, double l00, double l10,
+                          double l11, uint64_t base = 0, const double* scales = nullptr,
+                          uint32_t n_scales = 0, double* jumps = nullptr) {
     uint32_t accepted = 0;
-    const uint64_t unif_base = static_cast<uint64_t>(np) * steps * 2;
+    const uint64_t unif_base = base + static_cast<uint64_t>(np) * steps * 2;
     for (uint32_t q = threadIdx.x; q < np; q += kAnnealBlock) {
         double c0 = e.t0[q], c1 = e.t1[q], cll = e.ll[q], clp = e.lp[q];
+        const double h = (kJumps && n_scales) ? scales[q % n_scales] : h_all;
         for (uint32_t r = 0; r < steps; ++r) {
-            const uint64_t pair = static_cast<uint64_t>(q) * steps + r;
+            const uint64_t pair = (kJumps ? base / 2 : 0) + static_cast<uint64_t>(q) * steps + r;
             double z0, z1;
             box_muller<Exact>(philox2x64(key, pair), z0, z1);
             const double inc0 = __dadd_rn(0.0, __dmul_rn(l00, z0));
@@ -213,7 +222,7 @@ __device__ uint32_t sweep(const Design& d, const RunModel& m, Ensemble& e, uint3
             const double ll_new = log_lik(d, m, p0, p1);
             const double log_alpha =
                 __dsub_rn(__dadd_rn(__dmul_rn(temperature, __dsub_rn(ll_new, cll)), lp_new), clp);
-            const uint64_t upos = unif_base + pair;
+            const uint64_t upos = unif_base + static_cast<uint64_t>(q) * steps + r;
             const Words w = philox2x64(key, upos >> 1);
             const double u = to_unit((upos & 1) ? w.w1 : w.w0);
             const double log_u = u > 0.0 ? ln_pos<Exact>(u) : -INFINITY;
@@ -223,6 +232,10 @@ __device__ uint32_t sweep(const Design& d, const RunModel& m, Ensemble& e, uint3
                 c1 = p1;
                 cll = ll_new;
                 clp = lp_new;
+                if (kJumps) {
+                    const double zz = __dadd_rn(__dadd_rn(0.0, __dmul_rn(z0, z0)), __dmul_rn(z1, z1));
+                    jumps[q] = __dadd_rn(jumps[q], __dmul_rn(__dmul_rn(h, h), zz));
+                }
             }
         }
         e.t0[q] = c0;
@@ -233,6 +246,38 @@ __device__ uint32_t sweep(const Design& d, const RunModel& m, Ensemble& e, uint3
     return accepted;
 }
 
+// Type-7 median (numeric.cpp:20-36,53) of the `count` values x[offset + j * stride] by
+// rank counting (no sort: the samples are a few hundred values in shared memory).
+// Every thread returns the same value.
+__device__ double block_median(const double* x, uint32_t count, uint32_t stride, uint32_t offset,
+                               BlockScratch& s) {
+    const double hpos = static_cast<double>(count - 1) * 0.5;
+    const uint32_t lo = static_cast<uint32_t>(hpos);
+    const uint32_t want_hi = (count > 1 && lo + 1 < count) ? lo + 1 : lo;
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < count; j += kAnnealBlock) {
+        const double v = x[offset + j * stride];
+        uint32_t rank = 0;
+        for (uint32_t k = 0; k < count; ++k) {
+            const double o = x[offset + k * stride];
+            rank += (o < v || (o == v && k < j)) ? 1 : 0;
+        }
+        if (rank == lo) s.a[0][0] = v;
+        if (rank == want_hi) s.a[0][1] = v;
+    }
+    __syncthreads();
+    const double v_lo = s.a[0][0], v_hi = s.a[0][1];
+    __syncthreads();
+    if (count == 1) return v_lo;
+    if (lo + 1 >= count) return v_hi;  // (not reached at level 0.5; kept for the general rule)
+    const double frac = hpos - static_cast<double>(lo);
+    return __dadd_rn(v_lo, __dmul_rn(frac, __dsub_rn(v_hi, v_lo)));
+}
+
+// kEsjd: the ESJD scale adaptation of run_smc (esjd_core, smc.cpp:156-204) instead of
+// the fixed-scale pilot + move sweeps.  A separate instance so that the fixed-scale
+// kernel (the weak-informativity test's) keeps its register budget.
+template <bool kEsjd>
 __global__ void __launch_bounds__(kAnnealBlock, 6) anneal_kernel(const __grid_constant__ AnnealParams p) {
     extern __shared__ double smem[];
     __shared__ BlockScratch scratch;
@@ -435,29 +480,88 @@ __global__ void __launch_bounds__(kAnnealBlock, 6) anneal_kernel(const __grid_co
                 break;
             }
         }
-        // ---- pilot sweep, step count, move sweep (smc.cpp:441-452)
-        uint32_t acc = sweep(d, model, e, np, key_of(n, kRolePilot), 1, temperature, h, l00, l10, l11);
-        if (threadIdx.x == 0) scratch.count = 0;
-        __syncthreads();
-        atomicAdd(&scratch.count, static_cast<unsigned long long>(acc));
-        __syncthreads();
-        const double p_acc = static_cast<double>(scratch.count) / static_cast<double>(np);
-        __syncthreads();
+        double p_acc, h_used = h;
         uint32_t steps;
-        {   // steps_from_acceptance: smc.cpp:302-309
-            const double pc = fmin(fmax(p_acc, 0.01), 0.99);
-            const double raw = ceil(log(p.c) / log(1.0 - pc));
-            steps = !(raw >= 1.0) ? 1u : static_cast<uint32_t>(fmin(raw, static_cast<double>(kStepCap)));
+        if (!kEsjd) {
+            // ---- pilot sweep, step count, move sweep (smc.cpp:441-452)
+            uint32_t acc = sweep(d, model, e, np, key_of(n, kRolePilot), 1, temperature, h, l00, l10, l11);
+            if (threadIdx.x == 0) scratch.count = 0;
+            __syncthreads();
+            atomicAdd(&scratch.count, static_cast<unsigned long long>(acc));
+            __syncthreads();
+            p_acc = static_cast<double>(scratch.count) / static_cast<double>(np);
+            __syncthreads();
+            {   // steps_from_acceptance: smc.cpp:302-309
+                const double pc = fmin(fmax(p_acc, 0.01), 0.99);
+                const double raw = ceil(log(p.c) / log(1.0 - pc));
+                steps = !(raw >= 1.0) ? 1u : static_cast<uint32_t>(fmin(raw, static_cast<double>(kStepCap)));
+            }
+            sweep(d, model, e, np, key_of(n, kRoleMove), steps, temperature, h, l00, l10, l11);
+            __syncthreads();
+        } else {
+            // ---- esjd_core (smc.cpp:156-204).  The jump distances live in the log-weight
+            // array (every log weight is -log N after the resampling; restored below).
+            double* const jumps = e.lw;
+            for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) jumps[i] = 0.0;
+            __syncthreads();
+            uint32_t acc = sweep<true>(d, model, e, np, key_of(n, kRoleTrial), 1, temperature, 0.0, l00, l10,
+                                       l11, 0, p.scales, p.n_scales, jumps);
+            if (threadIdx.x == 0) scratch.count = 0;
+            __syncthreads();
+            atomicAdd(&scratch.count, static_cast<unsigned long long>(acc));
+            __syncthreads();
+            p_acc = static_cast<double>(scratch.count) / static_cast<double>(np);
+            const double trial_median = block_median(jumps, np, 1, 0, scratch);
+            double best = -1.0;
+            bool any_jump = false;
+            h_used = 0.0;
+            for (uint32_t sidx = 0; sidx < p.n_scales; ++sidx) {
+                if (sidx >= np) continue;  // no particle carries this scale
+                const uint32_t count = (np - sidx + p.n_scales - 1) / p.n_scales;
+                const double med = block_median(jumps, count, p.n_scales, sidx, scratch);
+                if (med > 0.0) any_jump = true;
+                if (med > best) {
+                    best = med;
+                    h_used = p.scales[sidx];
+                }
+            }
+            if (!any_jump) {
+                int some = 0;
+                for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) some |= jumps[i] > 0.0 ? 1 : 0;
+                any_jump = __syncthreads_or(some) != 0;
+            }
+            if (!any_jump) h_used = 2.38 / sqrt(2.0);
+            steps = 0;
+            uint64_t pos = 0;  // position of the move stream (continues from sweep to sweep)
+            const uint64_t move_key = key_of(n, kRoleMove);
+            while (steps < kStepCap) {
+                int moved = 0;
+                for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) moved += jumps[i] > trial_median ? 1 : 0;
+                if (threadIdx.x == 0) scratch.count = 0;
+                __syncthreads();
+                atomicAdd(&scratch.count, static_cast<unsigned long long>(moved));
+                __syncthreads();
+                const bool enough = 2 * scratch.count >= np;
+                __syncthreads();
+                if (enough) break;
+                pos += pos & 1;  // align_even
+                sweep<true>(d, model, e, np, move_key, 1, temperature, h_used, l00, l10, l11, pos, nullptr, 0,
+                            jumps);
+                __syncthreads();
+                pos += 3ull * np;
+                ++steps;
+            }
+            for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) e.lw[i] = p.neg_log_np;
+            __syncthreads();
         }
-        sweep(d, model, e, np, key_of(n, kRoleMove), steps, temperature, h, l00, l10, l11);
-        __syncthreads();
         if (p.trace && threadIdx.x == 0 && n <= p.trace_rows) {
-            double* row = p.trace + (run * p.trace_rows + (n - 1)) * 5;
+            double* row = p.trace + (run * p.trace_rows + (n - 1)) * 6;
             row[0] = temperature;
             row[1] = ess_now;
             row[2] = static_cast<double>(steps);
             row[3] = p_acc;
             row[4] = log_evidence;
+            row[5] = h_used;
         }
     }
     if (p.ensemble) {  // the final ensemble (SmcResult::ensemble)
@@ -635,7 +739,11 @@ static void check_sampler_args(uint64_t particles, uint64_t block_width, double 
 static void anneal_device(vxb_ctx* ctx, const Design& design, uint64_t n_runs, uint64_t particles, double c,
                           double scale, const uint32_t* deaths, const double* lambda, const double* lambda_host,
                           const uint64_t* seeds, double* log_evidence, uint32_t* iterations, uint8_t* status,
-                          double* trace, uint32_t trace_rows, double* ensemble = nullptr) {
+                          double* trace, uint32_t trace_rows, double* ensemble = nullptr,
+                          const double* esjd_scales = nullptr, uint32_t n_scales = 0) {
+    require(n_scales <= kMaxEsjdScales, "invalid-argument", "at most 16 ESJD scales");
+    for (uint32_t k = 0; k < n_scales; ++k)
+        require(esjd_scales[k] > 0.0, "invalid-scale", "ESJD scales must be positive");
     std::vector<double> norm(n_runs);
     for (uint64_t r = 0; r < n_runs; ++r) {
         require(lambda_host[2 * r] > 0.0 && lambda_host[2 * r + 1] > 0.0, "invalid-argument",
@@ -661,9 +769,11 @@ static void anneal_device(vxb_ctx* ctx, const Design& design, uint64_t n_runs, u
     p.trace = trace;
     p.trace_rows = trace_rows;
     p.ensemble = ensemble;
+    p.n_scales = n_scales;
+    for (uint32_t k = 0; k < n_scales; ++k) p.scales[k] = esjd_scales[k];
     const size_t smem = particles * 6 * sizeof(double);
-    VXB_CUDA(cudaFuncSetAttribute(anneal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
+    auto kernel = n_scales ? anneal_kernel<true> : anneal_kernel<false>;
+    VXB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     {
         LaunchScope scope(ctx, VXB_K_RESAMPLE);
         // the grid is one CTA per run; launch in slices below the grid limit
@@ -677,9 +787,9 @@ static void anneal_device(vxb_ctx* ctx, const Design& design, uint64_t n_runs, u
             q.log_evidence += first;
             q.iterations += first;
             q.status += first;
-            if (q.trace) q.trace += first * trace_rows * 5;
+            if (q.trace) q.trace += first * trace_rows * 6;
             if (q.ensemble) q.ensemble += first * 5 * particles;
-            anneal_kernel<<<static_cast<unsigned>(count), kAnnealBlock, smem, ctx->stream>>>(q);
+            kernel<<<static_cast<unsigned>(count), kAnnealBlock, smem, ctx->stream>>>(q);
         }
         check_launch("anneal_kernel");
     }
@@ -770,8 +880,8 @@ extern "C" int vxb_smc_bioassay(vxb_ctx* ctx, uint64_t n_runs, uint32_t groups, 
         Scratch it_tmp(ctx, n_runs * 4), st_tmp(ctx, n_runs);
         Staged d_it(ctx, iterations, n_runs * 4, false, true);
         Staged d_st(ctx, status, n_runs, false, true);
-        Staged d_tr(ctx, trace, n_runs * trace_rows * 40, false, true);
-        if (trace) VXB_CUDA(cudaMemsetAsync(d_tr.ptr(), 0, n_runs * trace_rows * 40, ctx->stream));
+        Staged d_tr(ctx, trace, n_runs * trace_rows * 48, false, true);
+        if (trace) VXB_CUDA(cudaMemsetAsync(d_tr.ptr(), 0, n_runs * trace_rows * 48, ctx->stream));
         anneal_device(ctx, d, n_runs, particles, c, scale, d_y.as<uint32_t>(), d_l.as<double>(), lambda,
                       d_s.as<uint64_t>(), d_ev.as<double>(),
                       iterations ? d_it.as<uint32_t>() : it_tmp.as<uint32_t>(),
@@ -793,7 +903,8 @@ extern "C" int vxb_smc_bioassay_ensemble(vxb_ctx* ctx, uint32_t groups, const do
                                          const double* lambda, uint64_t seed, uint64_t particles,
                                          uint64_t block_width, double c, double scale, double* log_evidence,
                                          uint32_t* iterations, double* ensemble, double* trace,
-                                         uint32_t trace_rows) {
+                                         uint32_t trace_rows, const double* esjd_scales,
+                                         uint32_t n_scales) {
     return guarded([&] {
         use(ctx);
         require(deaths && lambda && log_evidence && ensemble, "invalid-argument", "null argument");
@@ -807,11 +918,12 @@ extern "C" int vxb_smc_bioassay_ensemble(vxb_ctx* ctx, uint32_t groups, const do
         Staged d_s(ctx, &seed, 8, true, false);
         Scratch d_ev(ctx, 8), d_it(ctx, 4), d_st(ctx, 1);
         Staged d_en(ctx, ensemble, particles * 40, false, true);
-        Staged d_tr(ctx, trace, static_cast<size_t>(trace_rows) * 40, false, true);
-        if (trace) VXB_CUDA(cudaMemsetAsync(d_tr.ptr(), 0, static_cast<size_t>(trace_rows) * 40, ctx->stream));
+        Staged d_tr(ctx, trace, static_cast<size_t>(trace_rows) * 48, false, true);
+        if (trace) VXB_CUDA(cudaMemsetAsync(d_tr.ptr(), 0, static_cast<size_t>(trace_rows) * 48, ctx->stream));
+        require(n_scales == 0 || esjd_scales, "invalid-argument", "null scale grid");
         anneal_device(ctx, d, 1, particles, c, scale, d_y.as<uint32_t>(), d_l.as<double>(), lambda,
                       d_s.as<uint64_t>(), d_ev.as<double>(), d_it.as<uint32_t>(), d_st.as<uint8_t>(),
-                      trace ? d_tr.as<double>() : nullptr, trace_rows, d_en.as<double>());
+                      trace ? d_tr.as<double>() : nullptr, trace_rows, d_en.as<double>(), esjd_scales, n_scales);
         uint32_t it = 0;
         uint8_t st = 0;
         VXB_CUDA(cudaMemcpyAsync(log_evidence, d_ev.as<void>(), 8, cudaMemcpyDeviceToHost, ctx->stream));

@@ -450,7 +450,7 @@ class Context:
         seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
         n = y.shape[0]
         ev, it, st = np.zeros(n), np.zeros(n, dtype=np.uint32), np.zeros(n, dtype=np.uint8)
-        tr = np.zeros((n, trace_rows, 5)) if trace_rows else None
+        tr = np.zeros((n, trace_rows, 6)) if trace_rows else None
         self._check(self.lib.vxb_smc_bioassay(self.handle, u64(n), u32(d.size), _ptr(d), _ptr(g),
                                               _ptr(y), _ptr(lam), _ptr(seeds), u64(particles),
                                               u64(block_width), f64(c), f64(scale), _ptr(ev),
@@ -458,18 +458,20 @@ class Context:
         return dict(log_evidence=ev, iterations=it, status=st, trace=tr)
 
     def smc_bioassay_ensemble(self, dose, group_size, deaths, lam, seed, particles, block_width=4,
-                              c=0.01, scale=1.6828427124746189, trace_rows=16):
-        """One run with its final ensemble (the reference's SmcResult)."""
+                              c=0.01, scale=1.6828427124746189, trace_rows=16, esjd_scales=None):
+        """One run with its final ensemble (the reference's SmcResult).  esjd_scales: the
+        scale grid of SmcConfig::esjd = true (None: fixed-scale sampler)."""
         d, g = self._design(dose, group_size)
         y = np.ascontiguousarray(deaths, dtype=np.uint32)
         lam = np.ascontiguousarray(lam, dtype=np.float64)
         ev, it = f64(), u32()
         ens = np.zeros((5, particles))
-        tr = np.zeros((trace_rows, 5))
+        tr = np.zeros((trace_rows, 6))
+        sc = None if esjd_scales is None else np.ascontiguousarray(esjd_scales, dtype=np.float64)
         self._check(self.lib.vxb_smc_bioassay_ensemble(
             self.handle, u32(d.size), _ptr(d), _ptr(g), _ptr(y), _ptr(lam), u64(seed), u64(particles),
             u64(block_width), f64(c), f64(scale), C.byref(ev), C.byref(it), _ptr(ens), _ptr(tr),
-            u32(trace_rows)))
+            u32(trace_rows), _ptr(sc), u32(0 if sc is None else sc.size)))
         return dict(log_evidence=ev.value, iterations=it.value, particles=ens[:2].T.copy(),
                     log_weights=ens[2], log_liks=ens[3], log_priors=ens[4], trace=tr[:it.value])
 

@@ -83,9 +83,20 @@ static int csv_mode(const char* bench_golden, const char* out_dir) {
         dump("run_smc_log_liks", res.ensemble.log_liks);
         std::ofstream(dir + "/smc_trace.csv") << tr.str();
         int refused = 0;
-        sc.esjd = true;
-        try { smc::run_smc(weakinfo::make_bioassay_model(d3.data, {4.0, 0.2}), sc); } catch (const Error& e) { refused += e.code() == "unsupported-config"; }
-        sc.esjd = false;
+        {   // SmcConfig::esjd = true: the scale adaptation, default grid
+            smc::SmcConfig se;
+            se.particles = 333;
+            se.seed = 15;
+            se.esjd = true;
+            std::ostringstream te;
+            te.precision(17);
+            se.trace = &te;
+            const smc::SmcResult re = smc::run_smc(weakinfo::make_bioassay_model(d3.data, {4.0, 0.2}), se);
+            std::printf("run_smc_esjd %.17g %zu\n", re.log_evidence, re.iterations);
+            std::ofstream(dir + "/smc_trace_esjd.csv") << te.str();
+            se.esjd_scales.assign(17, 0.1);
+            try { smc::run_smc(weakinfo::make_bioassay_model(d3.data, {4.0, 0.2}), se); } catch (const Error& e) { refused += e.code() == "invalid-argument"; }
+        }
         try { smc::run_smc(ModelHooks{}, sc); } catch (const Error& e) { refused += e.code() == "unsupported-model"; }
         sc.particles = 6;
         try { smc::run_smc(weakinfo::make_bioassay_model(d3.data, {4.0, 0.2}), sc); } catch (const Error& e) { refused += e.code() == "invalid-shape"; }

@@ -22,6 +22,11 @@ RUNS = [  # (lambda1, lambda2, data seed, sampler seed, particles)
     (9.5, 19.0, 42, 4242, 500), (0.11, 0.13, 8, 88, 200), (2.0, 2.0, 9, 99, 1000),
 ]
 ENSEMBLE_RUN = 2
+GRID = (0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9, 1.0)   # SmcConfig::esjd_scales default (smc.hpp:119)
+ESJD_RUNS = [  # (lambda1, lambda2, data seed, sampler seed, particles, scale grid)
+    (10.0, 2.5, 1234, 3702, 500, GRID), (4.0, 0.2, 5, 15, 333, GRID),
+    (9.5, 19.0, 42, 4242, 200, (4.0, 9.0, 20.0)), (2.0, 2.0, 9, 99, 127, (0.05,)),
+]
 TABLE = dict(hyper_count=3, datasets=12, particles=200, seed=1337)
 
 
@@ -45,6 +50,14 @@ def main():
     e = r.smc_bioassay_ensemble(DOSE, SIZE, deaths[ENSEMBLE_RUN], l1, l2, npart, 4, 0.01, H, ss)
     g["ens_particles"], g["ens_trace"] = e["particles"], e["trace"]
     g["ens_rows"] = np.stack([e["log_weights"], e["log_liks"], e["log_priors"]])
+    # SmcConfig::esjd = true (scale adaptation): evidence, iterations, trace per case
+    for j, (l1, l2, ds, ss, npart, scales) in enumerate(ESJD_RUNS):
+        _, y = r.bioassay_sample(l1, l2, DOSE, SIZE, ds)
+        e = r.smc_bioassay_ensemble(DOSE, SIZE, y, l1, l2, npart, 4, 0.01, 0.0, ss, esjd_scales=scales)
+        g[f"esjd{j}_deaths"] = np.array(y, dtype=np.uint32)
+        g[f"esjd{j}_evidence"] = np.array([e["log_evidence"]])
+        g[f"esjd{j}_trace"] = e["trace"]
+        g[f"esjd{j}_particles"] = e["particles"]
     beta = np.random.RandomState(3).normal(size=(64, 2)) * np.array([8.0, 12.0])
     g["ll_beta"] = beta
     g["ll_values"] = r.bioassay_ll(beta, DOSE, SIZE, [0, 2, 5, 1])

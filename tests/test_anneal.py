@@ -42,6 +42,14 @@ def test_oracle_matches_reference_golden(oracle, gold):
     assert np.array_equal(e["particles"], gold["ens_particles"])
     assert np.array_equal(np.stack([e["log_weights"], e["log_liks"], e["log_priors"]]), gold["ens_rows"])
     assert np.allclose(e["trace"], gold["ens_trace"], rtol=1e-15, atol=0)
+    # SmcConfig::esjd = true: scale adaptation (sweeps until half the ensemble has moved)
+    for j, (l1, l2, ds, ss, npart, scales) in enumerate(G.ESJD_RUNS):
+        e = oracle.smc_bioassay_ensemble(G.DOSE, G.SIZE, gold[f"esjd{j}_deaths"], l1, l2, npart, 4, 0.01, 0.0,
+                                         ss, esjd_scales=scales)
+        assert e["log_evidence"] == gold[f"esjd{j}_evidence"][0], j
+        assert np.array_equal(e["particles"], gold[f"esjd{j}_particles"]), j
+        assert np.array_equal(e["trace"][:, [2, 3]], gold[f"esjd{j}_trace"][:, [2, 3]]), j   # sweeps, acceptance
+        assert np.allclose(e["trace"], gold[f"esjd{j}_trace"], rtol=1e-15, atol=0), j
     for redraw in (0, 1):
         t = oracle.weak_info_test(G.TABLE["hyper_count"], G.TABLE["datasets"], G.TABLE["particles"],
                                   seed=G.TABLE["seed"], redraw_base=bool(redraw), workers=4)
@@ -63,6 +71,12 @@ def test_oracle_matches_live_reference(oracle, ref):
         eb = oracle.smc_bioassay_ensemble(G.DOSE, G.SIZE, y, l1, l2, 300, 8, 0.05, 0.9, 7 * trial)
         for k in ("particles", "log_weights", "log_liks", "log_priors"):
             assert np.array_equal(ea[k], eb[k]), k
+        for scales in ((0.3, 0.6, 0.9, 1.2), (6.0, 12.0)):
+            ea = ref.smc_bioassay_ensemble(G.DOSE, G.SIZE, y, l1, l2, 301, 8, 0.05, 0.0, 7 * trial, esjd_scales=scales)
+            eb = oracle.smc_bioassay_ensemble(G.DOSE, G.SIZE, y, l1, l2, 301, 8, 0.05, 0.0, 7 * trial,
+                                              esjd_scales=scales)
+            assert ea["log_evidence"] == eb["log_evidence"] and ea["iterations"] == eb["iterations"]
+            assert np.array_equal(ea["particles"], eb["particles"]) and np.array_equal(ea["trace"], eb["trace"])
     a = ref.weak_info_test(2, 6, 100, seed=5)
     b = oracle.weak_info_test(2, 6, 100, seed=5)
     for k in a:
@@ -167,6 +181,45 @@ def test_device_run_smc_result(ctx, oracle, gold):
     with pytest.raises(lib.VxbError) as err:
         ctx.smc_bioassay_ensemble(G.DOSE, G.SIZE, [0, 0, 0, 0], [1.0, 1.0], 1, 7)
     assert err.value.code == "invalid-shape"
+
+
+@pytest.mark.gpu
+def test_device_run_smc_esjd(ctx, oracle, gold):
+    """SmcConfig::esjd = true on the device (esjd_core, smc.cpp:156-204): the same trial
+    acceptance, chosen scale and number of sweeps per iteration as the reference, the
+    same accept decisions, evidences and ensembles to rounding."""
+    for j, (l1, l2, ds, ss, npart, scales) in enumerate(G.ESJD_RUNS):
+        e = ctx.smc_bioassay_ensemble(G.DOSE, G.SIZE, gold[f"esjd{j}_deaths"], [l1, l2], ss, npart, scale=0.0,
+                                      esjd_scales=scales)
+        want = gold[f"esjd{j}_trace"]
+        assert e["iterations"] == len(want)
+        assert abs(e["log_evidence"] - gold[f"esjd{j}_evidence"][0]) < 1e-9, j
+        assert np.array_equal(e["trace"][:, [2, 3, 5]], want[:, [2, 3, 5]]), j   # sweeps, acceptance, scale
+        assert np.allclose(e["trace"], want, rtol=1e-9, atol=1e-9), j
+        assert np.allclose(e["particles"], gold[f"esjd{j}_particles"], rtol=1e-9, atol=1e-9), j
+    rs = np.random.RandomState(31)
+    many_sweeps = 0
+    for trial, (npart, scales) in enumerate(((1000, G.GRID), (255, (5.0, 10.0, 15.0)), (96, (0.4,)),
+                                             (2000, G.GRID), (501, (8.0,)), (128, tuple(0.05 * k for k in range(1, 17))))):
+        l1, l2 = rs.uniform(0.1, 10.0), rs.uniform(0.1, 20.0)
+        _, y = oracle.bioassay_sample(l1, l2, G.DOSE, G.SIZE, 70 + trial)
+        want = oracle.smc_bioassay_ensemble(G.DOSE, G.SIZE, y, l1, l2, npart, 4, 0.01, 0.0, 500 + trial,
+                                            esjd_scales=scales)
+        got = ctx.smc_bioassay_ensemble(G.DOSE, G.SIZE, y, [l1, l2], 500 + trial, npart, scale=0.0,
+                                        esjd_scales=scales)
+        assert got["iterations"] == want["iterations"]
+        assert abs(got["log_evidence"] - want["log_evidence"]) < 1e-9
+        assert np.array_equal(got["trace"][:, [2, 3, 5]], want["trace"][:, [2, 3, 5]]), trial
+        for k in ("particles", "log_weights", "log_liks", "log_priors"):
+            assert np.allclose(got[k], want[k], rtol=1e-9, atol=1e-9), (trial, k)
+        many_sweeps += int((want["trace"][:, 2] >= 3).any())
+    assert many_sweeps >= 1                                # the repeated-sweep loop was exercised
+    with pytest.raises(lib.VxbError) as err:               # the device carries at most 16 scales
+        ctx.smc_bioassay_ensemble(G.DOSE, G.SIZE, [0, 1, 2, 3], [1.0, 1.0], 1, 64, esjd_scales=[0.1] * 17)
+    assert err.value.code == "invalid-argument"
+    with pytest.raises(lib.VxbError) as err:
+        ctx.smc_bioassay_ensemble(G.DOSE, G.SIZE, [0, 1, 2, 3], [1.0, 1.0], 1, 64, esjd_scales=[0.5, -1.0])
+    assert err.value.code == "invalid-scale"
 
 
 @pytest.mark.gpu

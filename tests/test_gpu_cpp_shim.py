@@ -104,8 +104,15 @@ def test_cpp_shim_reference_format_outputs(tmp_path, golden, oracle):
     assert lines[0] == "n,t_n,ess,log_evidence,R_n,p_acc,h"
     rows = np.array([[float(x) for x in ln.split(",")] for ln in lines[1:]])
     assert rows[:, 0].tolist() == [1.0, 2.0]
-    assert np.allclose(rows[:, [1, 2, 4, 5, 3]], anneal["ens_trace"], rtol=1e-9, atol=1e-9)
+    assert np.allclose(rows[:, [1, 2, 4, 5, 3, 6]], anneal["ens_trace"], rtol=1e-9, atol=1e-9)
     assert r["run_smc_refused"] == ["3"]
+    # SmcConfig::esjd = true through the shim = golden case 1 (same data, prior, seed, 333 particles)
+    want = anneal["esjd1_trace"]
+    assert abs(float(r["run_smc_esjd"][0]) - anneal["esjd1_evidence"][0]) < 1e-9
+    assert int(r["run_smc_esjd"][1]) == len(want)
+    rows = np.array([[float(x) for x in ln.split(",")]
+                     for ln in read(tmp_path / "smc_trace_esjd.csv").strip().splitlines()[1:]])
+    assert np.array_equal(rows[:, [4, 5, 6]], want[:, [2, 3, 5]])      # sweeps, trial acceptance, scale
     tb_obs = oracle.tb_observed(10, 10.0, 10000.0, 1337)
     tb_rows = oracle.tb_abc_particle(10, 10.0, 10000.0, 0, 40, 1337, tb_obs)
     assert [float(t) for t in r["tb"][:4]] == [tb_obs[0], tb_obs[1], tb_rows[1][0, 0], tb_rows[2][1]]
