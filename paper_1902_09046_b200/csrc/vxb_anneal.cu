@@ -277,8 +277,11 @@ __device__ double block_median(const double* x, uint32_t count, uint32_t stride,
 // kEsjd: the ESJD scale adaptation of run_smc (esjd_core, smc.cpp:156-204) instead of
 // the fixed-scale pilot + move sweeps.  A separate instance so that the fixed-scale
 // kernel (the weak-informativity test's) keeps its register budget.
+#ifndef VXB_ANNEAL_CTAS
+#define VXB_ANNEAL_CTAS 6  // swept 4-8 at the paper size of the weak-informativity test: 0.40 / 0.37 / 0.353 / 0.366 / 0.367 s
+#endif
 template <bool kEsjd>
-__global__ void __launch_bounds__(kAnnealBlock, 6) anneal_kernel(const __grid_constant__ AnnealParams p) {
+__global__ void __launch_bounds__(kAnnealBlock, VXB_ANNEAL_CTAS) anneal_kernel(const __grid_constant__ AnnealParams p) {
     extern __shared__ double smem[];
     __shared__ BlockScratch scratch;
     Reducer red{scratch};
