@@ -395,6 +395,9 @@ typedef struct vxb_weakinfo_cfg {
     uint32_t groups;
     uint32_t group_size[16];
     double dose[16];
+    int32_t arith;         /* VXB_ARITH_EXACT (0, the reference's arithmetic) or VXB_ARITH_FMA:
+                              same random numbers and polynomials, multiply-adds contracted */
+    int32_t reserved;
 } vxb_weakinfo_cfg;
 
 /* run_weak_info_test (weak_info.cpp:163-277): outputs per row k = 0..K (row 0 is

@@ -61,10 +61,16 @@ struct Design {
 };
 
 // -log p = log(1 + e^b): weak_info.cpp:20-24
+// A: Exact (separate multiply and add, the reference's arithmetic bit for bit) or Fused
+// (VXB_ARITH_FMA: the same polynomials and the same random numbers with the compiler
+// free to contract a * b + c, about half the FP64 instructions; results agree with the
+// exact mode to rounding as long as no accept decision sits within rounding of its
+// threshold)
+template <class A>
 __device__ __forceinline__ double softplus(double b) {
     const double pos = b > 0.0 ? b : 0.0;
     const double mag = b > 0.0 ? b : -b;
-    return __dadd_rn(pos, ln_pos<Exact>(__dadd_rn(1.0, exp2_clamped<Exact>(__dmul_rn(-mag, kInvLn2)))));
+    return A::add(pos, ln_pos<A>(A::add(1.0, exp2_clamped<A>(A::mul(-mag, kInvLn2)))));
 }
 
 struct RunModel {  // one dataset under one prior
@@ -73,22 +79,24 @@ struct RunModel {  // one dataset under one prior
 };
 
 // ll_lane: weak_info.cpp:26-40
+template <class A = Exact>
 __device__ __forceinline__ double log_lik(const Design& d, const RunModel& m, double b0, double b1) {
     double total = 0.0;
     for (uint32_t g = 0; g < d.groups; ++g) {
-        const double b = __dadd_rn(b0, __dmul_rn(b1, d.dose[g]));
-        const double lse = softplus(b);
-        total = __dadd_rn(total, m.choose[g]);
-        if (m.hit[g] > 0.0) total = __dsub_rn(total, __dmul_rn(m.hit[g], lse));
-        if (m.miss[g] > 0.0) total = __dadd_rn(total, __dmul_rn(m.miss[g], __dsub_rn(b, lse)));
+        const double b = A::mad(b1, d.dose[g], b0);
+        const double lse = softplus<A>(b);
+        total = A::add(total, m.choose[g]);
+        if (m.hit[g] > 0.0) total = A::mad(-m.hit[g], lse, total);
+        if (m.miss[g] > 0.0) total = A::mad(m.miss[g], A::sub(b, lse), total);
     }
     return total;
 }
 // log_prior hook: weak_info.cpp:144-148
+template <class A = Exact>
 __device__ __forceinline__ double log_prior(const RunModel& m, double b0, double b1) {
-    const double a = __ddiv_rn(b0, m.l1);
-    const double b = __ddiv_rn(b1, m.l2);
-    return __dsub_rn(m.log_norm, __dmul_rn(0.5, __dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b))));
+    const double a = A::div(b0, m.l1);
+    const double b = A::div(b1, m.l2);
+    return A::sub(m.log_norm, A::mul(0.5, A::mad(b, b, A::mul(a, a))));
 }
 
 // ------------------------------------------------------------ block collectives
@@ -200,7 +208,7 @@ struct AnnealParams {
 // The ESJD instance (kJumps) starts at stream position `base` (even), takes the
 // proposal scale of particle q from a cyclic grid when one is given, and adds
 // h^2 |z|^2 of every accepted proposal to jumps[q] (smc.cpp:138-144).
-template <bool kJumps = false>
+template <bool kJumps = false, class A = Exact>
 __device__ uint32_t sweep(const Design& d, const RunModel& m, Ensemble& e, uint32_t np, uint64_t key,
                           uint32_t steps, double temperature, double h_all, double l00, double l10,
                           double l11, uint64_t base = 0, const double* scales = nullptr,
@@ -213,19 +221,18 @@ __device__ uint32_t sweep(const Design& d, const RunModel& m, Ensemble& e, uint3
         for (uint32_t r = 0; r < steps; ++r) {
             const uint64_t pair = (kJumps ? base / 2 : 0) + static_cast<uint64_t>(q) * steps + r;
             double z0, z1;
-            box_muller<Exact>(philox2x64(key, pair), z0, z1);
-            const double inc0 = __dadd_rn(0.0, __dmul_rn(l00, z0));
-            const double inc1 = __dadd_rn(__dadd_rn(0.0, __dmul_rn(l10, z0)), __dmul_rn(l11, z1));
-            const double p0 = __dadd_rn(c0, __dmul_rn(h, inc0));
-            const double p1 = __dadd_rn(c1, __dmul_rn(h, inc1));
-            const double lp_new = log_prior(m, p0, p1);
-            const double ll_new = log_lik(d, m, p0, p1);
-            const double log_alpha =
-                __dsub_rn(__dadd_rn(__dmul_rn(temperature, __dsub_rn(ll_new, cll)), lp_new), clp);
+            box_muller<A>(philox2x64(key, pair), z0, z1);
+            const double inc0 = A::mad(l00, z0, 0.0);
+            const double inc1 = A::mad(l11, z1, A::mad(l10, z0, 0.0));
+            const double p0 = A::mad(h, inc0, c0);
+            const double p1 = A::mad(h, inc1, c1);
+            const double lp_new = log_prior<A>(m, p0, p1);
+            const double ll_new = log_lik<A>(d, m, p0, p1);
+            const double log_alpha = A::sub(A::add(A::mul(temperature, A::sub(ll_new, cll)), lp_new), clp);
             const uint64_t upos = unif_base + static_cast<uint64_t>(q) * steps + r;
             const Words w = philox2x64(key, upos >> 1);
             const double u = to_unit((upos & 1) ? w.w1 : w.w0);
-            const double log_u = u > 0.0 ? ln_pos<Exact>(u) : -INFINITY;
+            const double log_u = u > 0.0 ? ln_pos<A>(u) : -INFINITY;
             if (!isnan(log_alpha) && log_alpha > -INFINITY && log_u <= log_alpha) {
                 ++accepted;
                 c0 = p0;
@@ -280,8 +287,9 @@ __device__ double block_median(const double* x, uint32_t count, uint32_t stride,
 #ifndef VXB_ANNEAL_CTAS
 #define VXB_ANNEAL_CTAS 6  // swept 4-8 at the paper size of the weak-informativity test: 0.40 / 0.37 / 0.353 / 0.366 / 0.367 s
 #endif
-template <bool kEsjd>
+template <bool kEsjd, bool kFma>
 __global__ void __launch_bounds__(kAnnealBlock, VXB_ANNEAL_CTAS) anneal_kernel(const __grid_constant__ AnnealParams p) {
+    using A = typename std::conditional<kFma, Fused, Exact>::type;
     extern __shared__ double smem[];
     __shared__ BlockScratch scratch;
     Reducer red{scratch};
@@ -320,14 +328,14 @@ __global__ void __launch_bounds__(kAnnealBlock, VXB_ANNEAL_CTAS) anneal_kernel(c
         const uint64_t key = key_of(0, kRolePilot);
         for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) {
             double z0, z1;
-            box_muller<Exact>(philox2x64(key, i), z0, z1);
-            const double b0 = __dmul_rn(model.l1, z0), b1 = __dmul_rn(model.l2, z1);
-            const double ll = log_lik(d, model, b0, b1);
+            box_muller<A>(philox2x64(key, i), z0, z1);
+            const double b0 = A::mul(model.l1, z0), b1 = A::mul(model.l2, z1);
+            const double ll = log_lik<A>(d, model, b0, b1);
             e.t0[i] = b0;
             e.t1[i] = b1;
             e.lw[i] = p.neg_log_np;
             e.ll[i] = ll;
-            e.lp[i] = log_prior(model, b0, b1);
+            e.lp[i] = log_prior<A>(model, b0, b1);
             bad |= (isnan(ll) || ll == INFINITY) ? 1 : 0;
             finite_any |= ll > -INFINITY ? 1 : 0;
         }
@@ -487,7 +495,7 @@ __global__ void __launch_bounds__(kAnnealBlock, VXB_ANNEAL_CTAS) anneal_kernel(c
         uint32_t steps;
         if (!kEsjd) {
             // ---- pilot sweep, step count, move sweep (smc.cpp:441-452)
-            uint32_t acc = sweep(d, model, e, np, key_of(n, kRolePilot), 1, temperature, h, l00, l10, l11);
+            uint32_t acc = sweep<false, A>(d, model, e, np, key_of(n, kRolePilot), 1, temperature, h, l00, l10, l11);
             if (threadIdx.x == 0) scratch.count = 0;
             __syncthreads();
             atomicAdd(&scratch.count, static_cast<unsigned long long>(acc));
@@ -499,7 +507,7 @@ __global__ void __launch_bounds__(kAnnealBlock, VXB_ANNEAL_CTAS) anneal_kernel(c
                 const double raw = ceil(log(p.c) / log(1.0 - pc));
                 steps = !(raw >= 1.0) ? 1u : static_cast<uint32_t>(fmin(raw, static_cast<double>(kStepCap)));
             }
-            sweep(d, model, e, np, key_of(n, kRoleMove), steps, temperature, h, l00, l10, l11);
+            sweep<false, A>(d, model, e, np, key_of(n, kRoleMove), steps, temperature, h, l00, l10, l11);
             __syncthreads();
         } else {
             // ---- esjd_core (smc.cpp:156-204).  The jump distances live in the log-weight
@@ -608,7 +616,7 @@ __global__ void bioassay_draw_kernel(const __grid_constant__ DrawParams p) {
     uint64_t pos = 2;
     for (uint32_t g = 0; g < d.groups; ++g) {
         const double b = __dadd_rn(b0, __dmul_rn(b1, d.dose[g]));
-        const double prob = exp2_clamped<Exact>(__dmul_rn(-softplus(b), kInvLn2));
+        const double prob = exp2_clamped<Exact>(__dmul_rn(-softplus<Exact>(b), kInvLn2));
         uint32_t k = 0;
         const uint32_t animals = static_cast<uint32_t>(d.size[g]);
         for (uint32_t j = 0; j < animals; ++j, ++pos) {
@@ -743,7 +751,9 @@ static void anneal_device(vxb_ctx* ctx, const Design& design, uint64_t n_runs, u
                           double scale, const uint32_t* deaths, const double* lambda, const double* lambda_host,
                           const uint64_t* seeds, double* log_evidence, uint32_t* iterations, uint8_t* status,
                           double* trace, uint32_t trace_rows, double* ensemble = nullptr,
-                          const double* esjd_scales = nullptr, uint32_t n_scales = 0) {
+                          const double* esjd_scales = nullptr, uint32_t n_scales = 0,
+                          int arith = VXB_ARITH_EXACT) {
+    require(arith == VXB_ARITH_EXACT || arith == VXB_ARITH_FMA, "invalid-argument", "bad arithmetic mode");
     require(n_scales <= kMaxEsjdScales, "invalid-argument", "at most 16 ESJD scales");
     for (uint32_t k = 0; k < n_scales; ++k)
         require(esjd_scales[k] > 0.0, "invalid-scale", "ESJD scales must be positive");
@@ -775,7 +785,10 @@ static void anneal_device(vxb_ctx* ctx, const Design& design, uint64_t n_runs, u
     p.n_scales = n_scales;
     for (uint32_t k = 0; k < n_scales; ++k) p.scales[k] = esjd_scales[k];
     const size_t smem = particles * 6 * sizeof(double);
-    auto kernel = n_scales ? anneal_kernel<true> : anneal_kernel<false>;
+    require(!(n_scales && arith == VXB_ARITH_FMA), "invalid-argument",
+            "the ESJD instance runs in the reference's arithmetic");
+    auto kernel = n_scales ? anneal_kernel<true, false>
+                           : (arith == VXB_ARITH_FMA ? anneal_kernel<false, true> : anneal_kernel<false, false>);
     VXB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     {
         LaunchScope scope(ctx, VXB_K_RESAMPLE);
@@ -1017,7 +1030,7 @@ extern "C" int vxb_weak_info_evidence(vxb_ctx* ctx, const vxb_weakinfo_cfg* cfg,
             }
         anneal_device(ctx, design, runs, cfg->particles, cfg->c, cfg->scale, d_ry.as<uint32_t>(),
                       d_rl.as<double>(), run_lambda.data(), d_rs.as<uint64_t>(), d_ev.as<double>(),
-                      d_it.as<uint32_t>(), d_st.as<uint8_t>(), nullptr, 0);
+                      d_it.as<uint32_t>(), d_st.as<uint8_t>(), nullptr, 0, nullptr, nullptr, 0, cfg->arith);
         d_ev.finish();
         VXB_CUDA(cudaStreamSynchronize(ctx->stream));
         delete big;

@@ -10,7 +10,7 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import numpy as np
-from paper_1902_09046_b200 import lib, models as M
+from paper_1902_09046_b200 import _abi as A, lib, models as M
 
 ctx = lib.Context(0)
 k = int(sys.argv[1]) if len(sys.argv) > 1 else 400
@@ -29,4 +29,15 @@ out = {"hyper_count": k, "datasets": n, "particles": 500, "sampler_runs": runs,
        "weakly_informative": int(t["weakly"].sum()), "gamma0": float(t["gamma"][0]),
        "completed_min": int(t["completed"].min()), "evidence_mean": float(np.nanmean(ev)),
        "failed_runs": int(np.isnan(ev).sum())}
+# the same test with contracted multiply-adds (VXB_ARITH_FMA: same random numbers)
+cfg_fma = M.weakinfo_config(hyper_count=k, datasets=n, particles=500, seed=1337, arith=A.VXB_ARITH_FMA)
+ctx.weak_info_test(cfg_fma)
+fma_times = []
+for rep in range(3):
+    t0 = time.perf_counter()
+    tf = ctx.weak_info_test(cfg_fma, want_evidence=True)
+    fma_times.append(time.perf_counter() - t0)
+out["fma_mode"] = {"seconds": fma_times, "max_abs_evidence_difference": float(np.nanmax(np.abs(tf["evidence"] - ev))),
+                   "table_identical": bool(np.array_equal(tf["gamma"], t["gamma"]) and
+                                           np.array_equal(tf["weakly"], t["weakly"]))}
 print(json.dumps(out))

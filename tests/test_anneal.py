@@ -242,6 +242,25 @@ def test_device_weak_info_table_equals_reference(ctx, oracle, gold):
 
 
 @pytest.mark.gpu
+def test_device_weak_info_fma_mode(ctx):
+    """VXB_ARITH_FMA: the same random numbers and polynomials with contracted multiply-adds.
+    Evidences agree with the reference-exact mode to rounding, the cut-off table is the same."""
+    from paper_1902_09046_b200 import _abi as A
+    kw = dict(hyper_count=6, datasets=40, particles=300, seed=77)
+    for redraw in (False, True):
+        exact = ctx.weak_info_test(M.weakinfo_config(redraw_base=redraw, **kw), want_evidence=True)
+        fused = ctx.weak_info_test(M.weakinfo_config(redraw_base=redraw, arith=A.VXB_ARITH_FMA, **kw),
+                                   want_evidence=True)
+        assert np.allclose(exact["evidence"], fused["evidence"], rtol=0, atol=1e-9, equal_nan=True)
+        assert not np.array_equal(exact["evidence"], fused["evidence"])      # it is a different instance
+        for k in ("gamma", "weakly", "completed", "lambda_"):
+            assert np.array_equal(exact[k], fused[k]), k
+    with pytest.raises(lib.VxbError) as err:
+        ctx.weak_info_test(M.weakinfo_config(arith=7, **kw))
+    assert err.value.code == "invalid-argument"
+
+
+@pytest.mark.gpu
 def test_device_weak_info_row_shards(ctx, gold):
     """Evidences of row ranges equal the rows of the whole table (seeds are keyed by
     row and dataset), so sharding hyperparameters over GPUs cannot change it."""
