@@ -125,6 +125,9 @@ struct WeakInfoConfig {
     bool redraw_base = false;
     Hyperparam base = kBasePrior;
     BioassayData design;
+    // not in the reference: run the sampler with contracted multiply-adds
+    // (VXB_ARITH_FMA -- same random numbers, evidences equal to rounding, ~10 % faster)
+    bool fused_arithmetic = false;
 };
 struct CutoffRow {
     std::size_t index;
@@ -157,6 +160,7 @@ inline CutoffTable run_weak_info_test(const WeakInfoConfig& config) {
     cfg.base[0] = config.base.lambda1;
     cfg.base[1] = config.base.lambda2;
     cfg.redraw_base = config.redraw_base ? 1 : 0;
+    cfg.arith = config.fused_arithmetic ? VXB_ARITH_FMA : VXB_ARITH_EXACT;
     cfg.groups = static_cast<std::uint32_t>(design.groups());
     for (std::size_t g = 0; g < design.groups(); ++g) {
         cfg.dose[g] = design.dose[g];
