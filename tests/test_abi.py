@@ -36,6 +36,22 @@ def test_header_and_python_mirror_agree():
     assert ctypes.sizeof(A.vxb_abcsmc_cfg) == 64
     assert ctypes.sizeof(A.vxb_mlmc_cfg) == 40
     assert ctypes.sizeof(A.vxb_profile) == 16 * A.VXB_K_COUNT
+    assert ctypes.sizeof(A.vxb_weakinfo_cfg) == 5 * 8 + 5 * 8 + 2 * 4 + 16 * 4 + 16 * 8 + 2 * 4
+
+
+def test_struct_sizes_match_the_c_compiler(tmp_path):
+    """The ctypes mirrors against sizeof() as gcc sees the header (plain C)."""
+    import subprocess
+    names = ["vxb_model", "vxb_keying", "vxb_abcsmc_cfg", "vxb_mlmc_cfg", "vxb_weakinfo_cfg", "vxb_profile"]
+    src = tmp_path / "sizes.c"
+    src.write_text('#include <stdio.h>\n#include "vexbayes_cuda.h"\nint main(void) {\n' +
+                   "".join(f'    printf("{n} %zu\\n", sizeof({n}));\n' for n in names) + "    return 0;\n}\n")
+    exe = tmp_path / "sizes"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.dirname(HEADER), str(src), "-o", str(exe)], check=True)
+    out = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                        check=True).stdout.splitlines())
+    for n in names:
+        assert int(out[n]) == ctypes.sizeof(getattr(A, n)), n
 
 
 def test_library_exports_every_declared_symbol(so):
