@@ -28,7 +28,7 @@ out = {"rows": n, "seconds": dt, "rows_per_s": n / dt, "kernel_ms": kernel_ms, "
 try:
     from oracle.pyoracle import Ref
     r = Ref()
-    k = min(n, 8192)
+    k = min(n, int(sys.argv[2]) if len(sys.argv) > 2 else 8192)
     t0 = time.perf_counter()
     ref_rows = r.tb_abc_particle(10, 10.0, 10000.0, 0, k, 1337, obs)
     out["cpu_reference"] = {"rows": k, "seconds": time.perf_counter() - t0, "cores": os.cpu_count(),
