@@ -329,18 +329,20 @@ __device__ __forceinline__ bool row_accepted(const Real* rho, const uint8_t* fai
     return inside & (flag == 0) & (static_cast<double>(value) <= eps);
 }
 
-// Row of (warp, pass s, lane) inside a block tile: every warp owns 32*kSelItems
-// consecutive rows and sweeps them in kSelItems coalesced passes, so that the
-// ascending order inside a warp is (pass, lane) and no block-wide exchange is
-// needed per pass.  All kSelItems loads of a thread are independent and in flight
-// together: the kernels are HBM-bound streaming passes.
+// Row of (warp, bit s, lane) inside a block tile: every warp owns 32*kSelItems
+// consecutive rows and sweeps them in kSelItems/4 groups of 128 rows; in a group a lane
+// owns FOUR consecutive rows (bits 4g .. 4g+3), so that aligned fp64 rows are read as
+// two 16-byte loads and their flags as one 4-byte load (a byte load per row wastes most
+// of its 32-byte sector).  Ascending row order inside a warp is (group, lane, bit).
+static_assert(kSelItems % 4 == 0, "rows are taken four at a time");
 __device__ __forceinline__ uint64_t tile_row(uint64_t tile0, unsigned warp, int s, unsigned lane) {
-    return tile0 + static_cast<uint64_t>(warp) * (32 * kSelItems) + static_cast<uint64_t>(s) * 32 + lane;
+    return tile0 + static_cast<uint64_t>(warp) * (32 * kSelItems) + static_cast<uint64_t>(s >> 2) * 128 +
+           lane * 4 + (s & 3);
 }
 
 // Pass 1 (the only pass over rho): per-block accept counts, and every thread's
-// accept flags (bit s = pass s; one bit per row, n/8 bytes) so that the write pass
-// never has to read the 8-9 B/row again.
+// accept flags (bit s = row tile_row(.., s, lane); one bit per row, n/8 bytes) so that
+// the write pass never has to read the 8-9 B/row again.
 template <class Real>
 __global__ void __launch_bounds__(kSelBlock, 8)
 accept_count_kernel(const Real* __restrict__ rho, const uint8_t* __restrict__ failed, uint64_t n,
@@ -350,9 +352,35 @@ accept_count_kernel(const Real* __restrict__ rho, const uint8_t* __restrict__ fa
     const uint64_t tile0 = static_cast<uint64_t>(blockIdx.x) * kSelBlock * kSelItems;
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned flags = 0;
+    const bool whole = tile0 + static_cast<uint64_t>(kSelBlock) * kSelItems <= n;
+    if (sizeof(Real) == 8 && whole && (reinterpret_cast<uintptr_t>(rho) & 15) == 0 &&
+        (!failed || (reinterpret_cast<uintptr_t>(failed) & 3) == 0)) {
+        // whole tile, aligned fp64: all 16-byte loads (and the 4-byte flag words) of the
+        // thread are issued before anything depends on them
+        constexpr int kGroups = kSelItems / 4;
+        double2 a[kGroups], b[kGroups];
+        uint32_t f[kGroups];
 #pragma unroll
-    for (int s = 0; s < kSelItems; ++s)  // all loads of the thread in flight together
-        flags |= (row_accepted(rho, failed, tile_row(tile0, warp, s, lane), n, eps) ? 1u : 0u) << s;
+        for (int g = 0; g < kGroups; ++g) {
+            const uint64_t row = tile_row(tile0, warp, 4 * g, lane);
+            const double2* src = reinterpret_cast<const double2*>(rho + row);
+            a[g] = __ldg(src);
+            b[g] = __ldg(src + 1);
+            f[g] = failed ? __ldg(reinterpret_cast<const uint32_t*>(failed + row)) : 0u;
+        }
+#pragma unroll
+        for (int g = 0; g < kGroups; ++g) {
+            const double v[4] = {static_cast<double>(a[g].x), static_cast<double>(a[g].y),
+                                 static_cast<double>(b[g].x), static_cast<double>(b[g].y)};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                flags |= ((((f[g] >> (8 * e)) & 0xFFu) == 0) & (v[e] <= eps) ? 1u : 0u) << (4 * g + e);
+        }
+    } else {
+#pragma unroll
+        for (int s = 0; s < kSelItems; ++s)  // all loads of the thread in flight together
+            flags |= (row_accepted(rho, failed, tile_row(tile0, warp, s, lane), n, eps) ? 1u : 0u) << s;
+    }
     if (thread_flags)
         thread_flags[static_cast<uint64_t>(blockIdx.x) * kSelBlock + threadIdx.x] =
             static_cast<unsigned short>(flags);
@@ -406,8 +434,8 @@ scan_blocks_kernel(const unsigned int* __restrict__ counts, uint64_t n_blocks,
 }
 
 // Pass 2: ascending indices of the accepted rows from the stored flags (n/8 bytes
-// read) and the scanned block offsets: warp ballots of each pass give the order
-// (pass, lane) inside a warp.
+// read) and the scanned block offsets: the ballots of a group's four bits give the
+// order (group, lane, bit) inside a warp.
 __global__ void __launch_bounds__(kSelBlock)
 accept_write_kernel(const unsigned short* __restrict__ thread_flags,
                     const unsigned long long* __restrict__ offsets, uint64_t index_base, uint64_t cap,
@@ -425,13 +453,22 @@ accept_write_kernel(const unsigned short* __restrict__ thread_flags,
     for (unsigned w = 0; w < warp; ++w) dst += warp_cnt[w];
     const unsigned below = (1u << lane) - 1;
 #pragma unroll
-    for (int s = 0; s < kSelItems; ++s) {
-        const unsigned ballot = __ballot_sync(0xffffffffu, (flags >> s) & 1u);
-        if ((flags >> s) & 1u) {
-            const unsigned long long at = dst + __popc(ballot & below);
-            if (at < cap) idx[at] = tile_row(tile0, warp, s, lane) + index_base;
+    for (int g = 0; g < kSelItems / 4; ++g) {  // ascending rows: (group, lane, bit)
+        const unsigned nib = (flags >> (4 * g)) & 0xFu;
+        unsigned before = 0, all = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const unsigned ballot = __ballot_sync(0xffffffffu, (nib >> e) & 1u);
+            before += __popc(ballot & below);
+            all += __popc(ballot);
         }
-        dst += __popc(ballot);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if ((nib >> e) & 1u) {
+                const unsigned long long at = dst + before + __popc(nib & ((1u << e) - 1));
+                if (at < cap) idx[at] = tile_row(tile0, warp, 4 * g + e, lane) + index_base;
+            }
+        dst += all;
     }
 }
 
