@@ -397,7 +397,9 @@ typedef struct vxb_weakinfo_cfg {
     double dose[16];
     int32_t arith;         /* VXB_ARITH_EXACT (0, the reference's arithmetic) or VXB_ARITH_FMA:
                               same random numbers and polynomials, multiply-adds contracted */
-    int32_t reserved;
+    int32_t rng;           /* VXB_RNG_REF (0, the reference's streams) or VXB_RNG_FAST: throughput
+                              generator (Philox4x32, table-based normals / log / softplus, FMA);
+                              statistically validated, not variate-for-variate */
 } vxb_weakinfo_cfg;
 
 /* run_weak_info_test (weak_info.cpp:163-277): outputs per row k = 0..K (row 0 is

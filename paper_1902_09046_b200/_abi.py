@@ -63,7 +63,7 @@ class vxb_weakinfo_cfg(C.Structure):
                 ("c", C.c_double), ("scale", C.c_double), ("base", C.c_double * 2),
                 ("redraw_base", C.c_int32), ("groups", C.c_uint32),
                 ("group_size", C.c_uint32 * 16), ("dose", C.c_double * 16),
-                ("arith", C.c_int32), ("reserved", C.c_int32)]
+                ("arith", C.c_int32), ("rng", C.c_int32)]
 
 
 class vxb_mlmc_cfg(C.Structure):

@@ -128,6 +128,9 @@ struct WeakInfoConfig {
     // not in the reference: run the sampler with contracted multiply-adds
     // (VXB_ARITH_FMA -- same random numbers, evidences equal to rounding, ~10 % faster)
     bool fused_arithmetic = false;
+    // not in the reference: the throughput generator (VXB_RNG_FAST -- other random numbers,
+    // statistically equivalent estimates, ~1.75x faster); implies fused arithmetic
+    bool throughput_generator = false;
 };
 struct CutoffRow {
     std::size_t index;
@@ -161,6 +164,7 @@ inline CutoffTable run_weak_info_test(const WeakInfoConfig& config) {
     cfg.base[1] = config.base.lambda2;
     cfg.redraw_base = config.redraw_base ? 1 : 0;
     cfg.arith = config.fused_arithmetic ? VXB_ARITH_FMA : VXB_ARITH_EXACT;
+    cfg.rng = config.throughput_generator ? VXB_RNG_FAST : VXB_RNG_REF;
     cfg.groups = static_cast<std::uint32_t>(design.groups());
     for (std::size_t g = 0; g < design.groups(); ++g) {
         cfg.dose[g] = design.dose[g];

@@ -79,12 +79,19 @@ struct RunModel {  // one dataset under one prior
 };
 
 // ll_lane: weak_info.cpp:26-40
-template <class A = Exact>
-__device__ __forceinline__ double log_lik(const Design& d, const RunModel& m, double b0, double b1) {
+// throughput-generator instance: table-based 2^z / log2 (vxb_rng.cuh), FMA
+__device__ __forceinline__ double softplus_fast(double b, const double2* tbl) {
+    const double pos = b > 0.0 ? b : 0.0;
+    const double mag = b > 0.0 ? b : -b;
+    return fma(kLn2, fast_log2(1.0 + fast_exp2_neg(-mag * kInvLn2, tbl), tbl), pos);
+}
+template <class A = Exact, bool kFast = false>
+__device__ __forceinline__ double log_lik(const Design& d, const RunModel& m, double b0, double b1,
+                                          const double2* tbl = nullptr) {
     double total = 0.0;
     for (uint32_t g = 0; g < d.groups; ++g) {
         const double b = A::mad(b1, d.dose[g], b0);
-        const double lse = softplus<A>(b);
+        const double lse = kFast ? softplus_fast(b, tbl) : softplus<A>(b);
         total = A::add(total, m.choose[g]);
         if (m.hit[g] > 0.0) total = A::mad(-m.hit[g], lse, total);
         if (m.miss[g] > 0.0) total = A::mad(m.miss[g], A::sub(b, lse), total);
@@ -198,6 +205,7 @@ struct AnnealParams {
     double* trace;            // optional: n_runs x trace_rows x 6 (temperature, ess, steps, p_acc, log evidence, scale)
     uint32_t trace_rows;
     double* ensemble;         // optional: n_runs x 5 x np (theta0, theta1, log w, log L, log prior)
+    const double2* fast_table;  // throughput generator: log / trig / exp tables
     uint32_t n_scales;        // ESJD scale adaptation (kEsjd instance): the scale grid
     double scales[kMaxEsjdScales];
 };
@@ -208,11 +216,16 @@ struct AnnealParams {
 // The ESJD instance (kJumps) starts at stream position `base` (even), takes the
 // proposal scale of particle q from a cyclic grid when one is given, and adds
 // h^2 |z|^2 of every accepted proposal to jumps[q] (smc.cpp:138-144).
-template <bool kJumps = false, class A = Exact>
+// kFast: the throughput generator -- proposal (q, r) of stream (iteration, role) takes
+// its normal pair from Philox4x32 block (q R + r, noise domain | stream tag) and its
+// acceptance uniform from block (q R + r, uniform domain | stream tag) of the run's key;
+// table-based Box-Muller, log and softplus.  `key` is then the stream tag.
+template <bool kJumps = false, class A = Exact, bool kFast = false>
 __device__ uint32_t sweep(const Design& d, const RunModel& m, Ensemble& e, uint32_t np, uint64_t key,
                           uint32_t steps, double temperature, double h_all, double l00, double l10,
                           double l11, uint64_t base = 0, const double* scales = nullptr,
-                          uint32_t n_scales = 0, double* jumps = nullptr) {
+                          uint32_t n_scales = 0, double* jumps = nullptr, const FastKeys* fk = nullptr,
+                          const double2* tbl = nullptr) {
     uint32_t accepted = 0;
     const uint64_t unif_base = base + static_cast<uint64_t>(np) * steps * 2;
     for (uint32_t q = threadIdx.x; q < np; q += kAnnealBlock) {
@@ -221,18 +234,30 @@ __device__ uint32_t sweep(const Design& d, const RunModel& m, Ensemble& e, uint3
         for (uint32_t r = 0; r < steps; ++r) {
             const uint64_t pair = (kJumps ? base / 2 : 0) + static_cast<uint64_t>(q) * steps + r;
             double z0, z1;
-            box_muller<A>(philox2x64(key, pair), z0, z1);
+            if (kFast)
+                fast_box_muller(philox4x32(*fk, static_cast<uint32_t>(pair), kDomNoise | static_cast<uint32_t>(key),
+                                           0u, 0u), tbl, z0, z1);
+            else
+                box_muller<A>(philox2x64(key, pair), z0, z1);
             const double inc0 = A::mad(l00, z0, 0.0);
             const double inc1 = A::mad(l11, z1, A::mad(l10, z0, 0.0));
             const double p0 = A::mad(h, inc0, c0);
             const double p1 = A::mad(h, inc1, c1);
             const double lp_new = log_prior<A>(m, p0, p1);
-            const double ll_new = log_lik<A>(d, m, p0, p1);
+            const double ll_new = log_lik<A, kFast>(d, m, p0, p1, tbl);
             const double log_alpha = A::sub(A::add(A::mul(temperature, A::sub(ll_new, cll)), lp_new), clp);
-            const uint64_t upos = unif_base + static_cast<uint64_t>(q) * steps + r;
-            const Words w = philox2x64(key, upos >> 1);
-            const double u = to_unit((upos & 1) ? w.w1 : w.w0);
-            const double log_u = u > 0.0 ? ln_pos<A>(u) : -INFINITY;
+            double u, log_u;
+            if (kFast) {
+                const Words32 w = philox4x32(*fk, static_cast<uint32_t>(pair), kDomProposal | static_cast<uint32_t>(key),
+                                             0u, 0u);
+                u = fast_unit(w.a, w.b);
+                log_u = u > 0.0 ? kLn2 * fast_log2(u, tbl) : -INFINITY;
+            } else {
+                const uint64_t upos = unif_base + static_cast<uint64_t>(q) * steps + r;
+                const Words w = philox2x64(key, upos >> 1);
+                u = to_unit((upos & 1) ? w.w1 : w.w0);
+                log_u = u > 0.0 ? ln_pos<A>(u) : -INFINITY;
+            }
             if (!isnan(log_alpha) && log_alpha > -INFINITY && log_u <= log_alpha) {
                 ++accepted;
                 c0 = p0;
@@ -287,9 +312,14 @@ __device__ double block_median(const double* x, uint32_t count, uint32_t stride,
 #ifndef VXB_ANNEAL_CTAS
 #define VXB_ANNEAL_CTAS 6  // swept 4-8 at the paper size of the weak-informativity test: 0.40 / 0.37 / 0.353 / 0.366 / 0.367 s
 #endif
-template <bool kEsjd, bool kFma>
+// kMode: 0 the reference's arithmetic and streams; 1 the same streams with contracted
+// multiply-adds (VXB_ARITH_FMA); 2 the throughput generator (VXB_RNG_FAST) with FMA.
+template <bool kEsjd, int kMode>
 __global__ void __launch_bounds__(kAnnealBlock, VXB_ANNEAL_CTAS) anneal_kernel(const __grid_constant__ AnnealParams p) {
-    using A = typename std::conditional<kFma, Fused, Exact>::type;
+    using A = typename std::conditional<kMode != 0, Fused, Exact>::type;
+    constexpr bool kFast = kMode == 2;
+    __shared__ double2 s_tab[kFast ? kFastTableSize : 1];
+    __shared__ FastKeys s_fk;
     extern __shared__ double smem[];
     __shared__ BlockScratch scratch;
     Reducer red{scratch};
@@ -316,9 +346,25 @@ __global__ void __launch_bounds__(kAnnealBlock, VXB_ANNEAL_CTAS) anneal_kernel(c
             model.choose[g] = d.log_choose_big ? d.log_choose_big[g * d.big_stride + y] : d.log_choose[g][y];
         }
     }
-    __syncthreads();
     const uint64_t seed_hash = splitmix64(p.seeds[run]);
-    const auto key_of = [&](uint32_t iteration, uint32_t role) {
+    if (kFast) {
+        for (int i = threadIdx.x; i < kFastTableSize; i += kAnnealBlock) s_tab[i] = p.fast_table[i];
+        if (threadIdx.x == 0) {  // the run's Philox4x32 key schedule (make_fast_keys)
+            const uint64_t kk = splitmix64(seed_hash);
+            uint32_t k0 = static_cast<uint32_t>(kk), k1 = static_cast<uint32_t>(kk >> 32);
+            for (int r = 0; r < 10; ++r) {
+                s_fk.rk[2 * r] = k0;
+                s_fk.rk[2 * r + 1] = k1;
+                k0 += 0x9E3779B9u;
+                k1 += 0xBB67AE85u;
+            }
+        }
+    }
+    __syncthreads();
+    // exact / FMA: the reference's stream key of (iteration, role); throughput generator:
+    // the tag that separates the streams inside the counter's domain word
+    const auto key_of = [&](uint32_t iteration, uint32_t role) -> uint64_t {
+        if (kFast) return (role << 8) | (iteration << 12);
         return stream_key(seed_hash, static_cast<uint32_t>((iteration << 16) | role));  // smc.cpp:26-28
     };
 
@@ -328,9 +374,12 @@ __global__ void __launch_bounds__(kAnnealBlock, VXB_ANNEAL_CTAS) anneal_kernel(c
         const uint64_t key = key_of(0, kRolePilot);
         for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) {
             double z0, z1;
-            box_muller<A>(philox2x64(key, i), z0, z1);
+            if (kFast)
+                fast_box_muller(philox4x32(s_fk, i, kDomPrior | static_cast<uint32_t>(key), 0u, 0u), s_tab, z0, z1);
+            else
+                box_muller<A>(philox2x64(key, i), z0, z1);
             const double b0 = A::mul(model.l1, z0), b1 = A::mul(model.l2, z1);
-            const double ll = log_lik<A>(d, model, b0, b1);
+            const double ll = log_lik<A, kFast>(d, model, b0, b1, s_tab);
             e.t0[i] = b0;
             e.t1[i] = b1;
             e.lw[i] = p.neg_log_np;
@@ -423,7 +472,8 @@ __global__ void __launch_bounds__(kAnnealBlock, VXB_ANNEAL_CTAS) anneal_kernel(c
         }
         // ---- resample_multinomial draws (smc.cpp:285-299): draw i = position i of the coordinator stream
         {
-            const uint64_t key = key_of(n, kRoleCoordinator);
+            // (the resampling uniforms stay on the reference stream in every mode)
+            const uint64_t key = stream_key(seed_hash, static_cast<uint32_t>((n << 16) | kRoleCoordinator));
             // ancestor indices are parked in the log-weight array (reset right after)
             uint32_t* const anc = reinterpret_cast<uint32_t*>(e.lw);
             for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) {
@@ -495,7 +545,8 @@ __global__ void __launch_bounds__(kAnnealBlock, VXB_ANNEAL_CTAS) anneal_kernel(c
         uint32_t steps;
         if (!kEsjd) {
             // ---- pilot sweep, step count, move sweep (smc.cpp:441-452)
-            uint32_t acc = sweep<false, A>(d, model, e, np, key_of(n, kRolePilot), 1, temperature, h, l00, l10, l11);
+            uint32_t acc = sweep<false, A, kFast>(d, model, e, np, key_of(n, kRolePilot), 1, temperature, h, l00, l10,
+                                                  l11, 0, nullptr, 0, nullptr, &s_fk, s_tab);
             if (threadIdx.x == 0) scratch.count = 0;
             __syncthreads();
             atomicAdd(&scratch.count, static_cast<unsigned long long>(acc));
@@ -507,7 +558,8 @@ __global__ void __launch_bounds__(kAnnealBlock, VXB_ANNEAL_CTAS) anneal_kernel(c
                 const double raw = ceil(log(p.c) / log(1.0 - pc));
                 steps = !(raw >= 1.0) ? 1u : static_cast<uint32_t>(fmin(raw, static_cast<double>(kStepCap)));
             }
-            sweep<false, A>(d, model, e, np, key_of(n, kRoleMove), steps, temperature, h, l00, l10, l11);
+            sweep<false, A, kFast>(d, model, e, np, key_of(n, kRoleMove), steps, temperature, h, l00, l10, l11, 0,
+                                   nullptr, 0, nullptr, &s_fk, s_tab);
             __syncthreads();
         } else {
             // ---- esjd_core (smc.cpp:156-204).  The jump distances live in the log-weight
@@ -752,7 +804,7 @@ static void anneal_device(vxb_ctx* ctx, const Design& design, uint64_t n_runs, u
                           const uint64_t* seeds, double* log_evidence, uint32_t* iterations, uint8_t* status,
                           double* trace, uint32_t trace_rows, double* ensemble = nullptr,
                           const double* esjd_scales = nullptr, uint32_t n_scales = 0,
-                          int arith = VXB_ARITH_EXACT) {
+                          int arith = VXB_ARITH_EXACT, int rng = VXB_RNG_REF) {
     require(arith == VXB_ARITH_EXACT || arith == VXB_ARITH_FMA, "invalid-argument", "bad arithmetic mode");
     require(n_scales <= kMaxEsjdScales, "invalid-argument", "at most 16 ESJD scales");
     for (uint32_t k = 0; k < n_scales; ++k)
@@ -787,8 +839,13 @@ static void anneal_device(vxb_ctx* ctx, const Design& design, uint64_t n_runs, u
     const size_t smem = particles * 6 * sizeof(double);
     require(!(n_scales && arith == VXB_ARITH_FMA), "invalid-argument",
             "the ESJD instance runs in the reference's arithmetic");
-    auto kernel = n_scales ? anneal_kernel<true, false>
-                           : (arith == VXB_ARITH_FMA ? anneal_kernel<false, true> : anneal_kernel<false, false>);
+    require(rng == VXB_RNG_REF || rng == VXB_RNG_FAST, "invalid-argument", "bad generator mode");
+    require(!(n_scales && rng == VXB_RNG_FAST), "invalid-argument",
+            "the ESJD instance runs on the reference's streams");
+    p.fast_table = ctx->log_table;
+    auto kernel = n_scales ? anneal_kernel<true, 0>
+                  : rng == VXB_RNG_FAST ? anneal_kernel<false, 2>
+                  : arith == VXB_ARITH_FMA ? anneal_kernel<false, 1> : anneal_kernel<false, 0>;
     VXB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     {
         LaunchScope scope(ctx, VXB_K_RESAMPLE);
@@ -1030,7 +1087,7 @@ extern "C" int vxb_weak_info_evidence(vxb_ctx* ctx, const vxb_weakinfo_cfg* cfg,
             }
         anneal_device(ctx, design, runs, cfg->particles, cfg->c, cfg->scale, d_ry.as<uint32_t>(),
                       d_rl.as<double>(), run_lambda.data(), d_rs.as<uint64_t>(), d_ev.as<double>(),
-                      d_it.as<uint32_t>(), d_st.as<uint8_t>(), nullptr, 0, nullptr, nullptr, 0, cfg->arith);
+                      d_it.as<uint32_t>(), d_st.as<uint8_t>(), nullptr, 0, nullptr, nullptr, 0, cfg->arith, cfg->rng);
         d_ev.finish();
         VXB_CUDA(cudaStreamSynchronize(ctx->stream));
         delete big;

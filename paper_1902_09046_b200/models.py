@@ -91,7 +91,7 @@ DEFAULT_GROUP_SIZE = (5, 5, 5, 5)
 def weakinfo_config(hyper_count=400, datasets=400, particles=500, alpha=0.05, c=0.01,
                     scale=1.6828427124746189, block_width=4, seed=0, redraw_base=False,
                     base=(10.0, 2.5), dose=DEFAULT_DOSE, group_size=DEFAULT_GROUP_SIZE,
-                    arith=A.VXB_ARITH_EXACT):
+                    arith=A.VXB_ARITH_EXACT, rng=A.VXB_RNG_REF):
     """WeakInfoConfig (weak_info.hpp:62-75) with the reference defaults.  arith: the
     sampler's arithmetic (VXB_ARITH_FMA: throughput mode, same random numbers)."""
     cfg = A.vxb_weakinfo_cfg()
@@ -100,7 +100,7 @@ def weakinfo_config(hyper_count=400, datasets=400, particles=500, alpha=0.05, c=
     cfg.alpha, cfg.c, cfg.scale = alpha, c, scale
     cfg.base[0], cfg.base[1] = base
     cfg.redraw_base, cfg.groups = int(redraw_base), len(dose)
-    cfg.arith = arith
+    cfg.arith, cfg.rng = arith, rng
     for g in range(len(dose)):
         cfg.dose[g], cfg.group_size[g] = dose[g], group_size[g]
     return cfg

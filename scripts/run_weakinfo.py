@@ -40,4 +40,18 @@ for rep in range(3):
 out["fma_mode"] = {"seconds": fma_times, "max_abs_evidence_difference": float(np.nanmax(np.abs(tf["evidence"] - ev))),
                    "table_identical": bool(np.array_equal(tf["gamma"], t["gamma"]) and
                                            np.array_equal(tf["weakly"], t["weakly"]))}
+# the throughput generator (VXB_RNG_FAST: other random numbers, statistically validated)
+cfg_fast = M.weakinfo_config(hyper_count=k, datasets=n, particles=500, seed=1337, rng=A.VXB_RNG_FAST)
+ctx.weak_info_test(cfg_fast)
+fast_times = []
+for rep in range(3):
+    t0 = time.perf_counter()
+    tg = ctx.weak_info_test(cfg_fast, want_evidence=True)
+    fast_times.append(time.perf_counter() - t0)
+dv = (tg["evidence"] - ev).ravel()
+out["throughput_generator"] = {"seconds": fast_times, "weakly_informative": int(tg["weakly"].sum()),
+                               "gamma0": float(tg["gamma"][0]),
+                               "evidence_mean_difference": float(np.nanmean(dv)),
+                               "evidence_mean_difference_se": float(np.nanstd(dv) / np.sqrt(dv.size)),
+                               "flags_agree": float((tg["weakly"] == t["weakly"]).mean())}
 print(json.dumps(out))

@@ -261,6 +261,37 @@ def test_device_weak_info_fma_mode(ctx):
 
 
 @pytest.mark.gpu
+def test_device_weak_info_throughput_generator(ctx):
+    """VXB_RNG_FAST instance of the sampler (Philox4x32, table-based normals / log / softplus,
+    FMA): other random numbers, so the check is statistical -- on the same datasets the
+    evidence estimates are unbiased against the reference-exact instance (paired difference
+    within 5 standard errors, of the size two independent N_p = 300 estimates differ by),
+    equally distributed (two-sample KS at 1 %), and the p-value estimates move by Monte-Carlo
+    noise only."""
+    from paper_1902_09046_b200 import _abi as A
+    kw = dict(hyper_count=8, datasets=150, particles=300, seed=2024)
+    exact = ctx.weak_info_test(M.weakinfo_config(**kw), want_evidence=True)
+    fast = ctx.weak_info_test(M.weakinfo_config(rng=A.VXB_RNG_FAST, **kw), want_evidence=True)
+    a, b = exact["evidence"].ravel(), fast["evidence"].ravel()
+    assert np.isfinite(b).all() and (fast["completed"] == kw["datasets"]).all()
+    assert np.array_equal(exact["lambda_"], fast["lambda_"])         # same hyperparameters and datasets
+    d = b - a
+    assert abs(d.mean()) < 5.0 * d.std() / np.sqrt(d.size)
+    assert 0.02 < d.std() < 0.5                                      # noise of two sampler runs, not a shift
+    assert abs(b.std() / a.std() - 1.0) < 0.02
+    xs = np.sort(np.concatenate([a, b]))
+    ks = np.abs(np.searchsorted(np.sort(a), xs, side="right") / a.size
+                - np.searchsorted(np.sort(b), xs, side="right") / b.size).max()
+    assert ks < 1.628 * np.sqrt(2.0 / a.size)
+    assert np.abs(exact["gamma"] - fast["gamma"]).max() < 0.06        # alpha-quantiles of 150 p-values each
+    again = ctx.weak_info_test(M.weakinfo_config(rng=A.VXB_RNG_FAST, **kw), want_evidence=True)
+    assert np.array_equal(again["evidence"], fast["evidence"])        # deterministic in the seed
+    with pytest.raises(lib.VxbError) as err:
+        ctx.weak_info_test(M.weakinfo_config(rng=5, **kw))
+    assert err.value.code == "invalid-argument"
+
+
+@pytest.mark.gpu
 def test_device_weak_info_row_shards(ctx, gold):
     """Evidences of row ranges equal the rows of the whole table (seeds are keyed by
     row and dataset), so sharding hyperparameters over GPUs cannot change it."""
