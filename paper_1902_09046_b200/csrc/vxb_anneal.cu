@@ -165,13 +165,15 @@ struct Ensemble {  // views into dynamic shared memory, np entries each
 // monotone, so the reference's max_i (lw_i + dt ll_i) is fl(lw0 + dt max_i ll_i):
 // the maximum of the log likelihoods is taken once per iteration, not once per
 // bisection step.
+template <bool kFast = false>
 __device__ double ess_after(const Ensemble& e, uint32_t np, double dt, double lw0, double ll_max,
-                            Reducer& red) {
+                            Reducer& red, const double2* tbl = nullptr) {
     const double top = fma(dt, ll_max, lw0);
     if (top == -INFINITY) return 0.0;
     double s1 = 0.0, s2 = 0.0;
     for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) {
-        const double w = exp(fma(dt, e.ll[i], lw0) - top);
+        const double x = fma(dt, e.ll[i], lw0) - top;  // <= 0
+        const double w = kFast ? fast_exp2_neg(x * kInvLn2, tbl) : exp(x);
         s1 += w;
         s2 = fma(w, w, s2);
     }
@@ -410,11 +412,11 @@ __global__ void __launch_bounds__(kAnnealBlock, VXB_ANNEAL_CTAS) anneal_kernel(c
             double ll_max = -INFINITY;
             for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) ll_max = fmax(ll_max, e.ll[i]);
             ll_max = red.max(ll_max);
-            if (!(ess_after(e, np, room, p.neg_log_np, ll_max, red) >= half)) {
+            if (!(ess_after<kFast>(e, np, room, p.neg_log_np, ll_max, red, s_tab) >= half)) {
                 double lo = 0.0, hi = room;
                 while (hi - lo > kBisectionTol) {
                     const double mid = 0.5 * (lo + hi);
-                    if (ess_after(e, np, mid, p.neg_log_np, ll_max, red) >= half) lo = mid; else hi = mid;
+                    if (ess_after<kFast>(e, np, mid, p.neg_log_np, ll_max, red, s_tab) >= half) lo = mid; else hi = mid;
                 }
                 t_next = temperature + 0.5 * (lo + hi);
             }
