@@ -545,10 +545,12 @@ abcsmc_propose_fast_kernel(const __grid_constant__ ProposeFastParams pp) {
 
 // Whitening pre-pass for the throughput weights kernel: y = s L^-1 theta with
 // s^2 = log2(e)/2, so that  w_j exp(-q_ij/2) = w_j 2^(2 y_i.y_j - |y_i|^2 - |y_j|^2).
-// mode 0 (previous population): out = (2 y, -|y|^2); mode 1 (new): out = (y, -|y|^2).
+// mode 0 (previous population): out = (2 y, -|y|^2 + log2 w) -- the weight rides in the
+// exponent, so a kernel term is one 2^z and one add; mode 1 (new): out = (y, -|y|^2).
 template <int D>
 __global__ void whiten_kernel(int mode, uint64_t n, const double* __restrict__ theta,
-                              const double* __restrict__ chol, double* __restrict__ out) {
+                              const double* __restrict__ chol, const double* __restrict__ w,
+                              double* __restrict__ out) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double s = 0.84932180028801907;  // sqrt(log2(e) / 2)
@@ -566,44 +568,61 @@ __global__ void whiten_kernel(int mode, uint64_t n, const double* __restrict__ t
         a = fma(y[k], y[k], a);
         out[i * (D + 1) + k] = mode == 0 ? 2.0 * y[k] : y[k];
     }
-    out[i * (D + 1) + D] = -a;
+    out[i * (D + 1) + D] = mode == 0 ? log2(w[i]) - a : -a;
+}
+
+// 2^z for z <= ~0 with a degree-4 polynomial on the 1/64 grid of fast_exp2_neg's table:
+// relative error 4e-14, far below the Monte-Carlo error of an importance weight, one
+// FP64 instruction fewer per kernel term; arguments below -1000 give 0.
+__device__ __forceinline__ double weight_exp2(double z, const double2* tbl) {
+    const double tn = fma(z, 64.0, kMagic);
+    const int n = __double2loint(tn);           // round(64 z)
+    const double w = fma(tn - kMagic, -0.015625, z);
+    double p = 9.6181291076284772e-3;           // ln2^4/24
+    p = fma(p, w, 5.5504108664821580e-2);       // ln2^3/6
+    p = fma(p, w, 2.4022650695910071e-1);       // ln2^2/2
+    p = fma(p, w, 6.9314718055994531e-1);       // ln2
+    p = fma(p, w, 1.0);
+    const double t = reinterpret_cast<const double*>(tbl + kLogTableSize + kTrigTableSize)[n & 63];
+    const double r = p * t;
+    const int hi = __double2hiint(r) + ((n >> 6) << 20);
+    return z < -1000.0 ? 0.0 : __hiloint2double(hi, __double2loint(r));
 }
 
 template <int D>
 __global__ void __launch_bounds__(kWeightsBlock)
 abcsmc_weights_fast_kernel(uint64_t count, const double* __restrict__ y_new, uint64_t n_prev,
-                           const double* __restrict__ y_prev, const double* __restrict__ w_prev,
-                           const double2* __restrict__ fast_table, double* __restrict__ w_out) {
+                           const double* __restrict__ y_prev, const double2* __restrict__ fast_table,
+                           double* __restrict__ w_out) {
+    static_assert(D == 3, "rows of the whitened population are read as two 16-byte halves");
     constexpr int kTile = 128;
-    __shared__ double s_y[kTile * (D + 1)];
-    __shared__ double s_w[kTile];
+    __shared__ double2 s_y[kTile * 2];  // (2 y0, 2 y1), (2 y2, log2 w - |y|^2) per previous particle
     __shared__ double2 s_tab[kFastTableSize];
     for (int i = threadIdx.x; i < kFastTableSize; i += kWeightsBlock) s_tab[i] = fast_table[i];
     const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kWeightsBlock + threadIdx.x;
     double yi[D + 1];
 #pragma unroll
     for (int k = 0; k <= D; ++k) yi[k] = r < count ? y_new[r * (D + 1) + k] : 0.0;
+    const double2* prev = reinterpret_cast<const double2*>(y_prev);
     double sum = 0.0;
     for (uint64_t j0 = 0; j0 < n_prev; j0 += kTile) {
         const uint64_t len = min(static_cast<uint64_t>(kTile), n_prev - j0);
         __syncthreads();
-        for (uint64_t t = threadIdx.x; t < len * (D + 1); t += kWeightsBlock) s_y[t] = y_prev[j0 * (D + 1) + t];
-        for (uint64_t t = threadIdx.x; t < len; t += kWeightsBlock) s_w[t] = w_prev[j0 + t];
+        for (uint64_t t = threadIdx.x; t < len * 2; t += kWeightsBlock) s_y[t] = prev[j0 * 2 + t];
         __syncthreads();
-        const auto kernel_value = [&](uint64_t j) {
-            double z = s_y[j * (D + 1) + D];
-#pragma unroll
-            for (int k = 0; k < D; ++k) z = fma(yi[k], s_y[j * (D + 1) + k], z);
-            z += yi[D];  // -|y_i - y_j|^2 (<= 0 up to rounding)
-            return fast_exp2_neg(fmin(z, 0.0), s_tab);
+        const auto term = [&](uint64_t j) {  // w_j 2^(-|y_i - y_j|^2)
+            const double2 lo = s_y[2 * j], hi = s_y[2 * j + 1];
+            double z = fma(yi[0], lo.x, hi.y);
+            z = fma(yi[1], lo.y, z);
+            z = fma(yi[2], hi.x, z);
+            return weight_exp2(z + yi[D], s_tab);  // z <= 0 up to rounding
         };
         uint64_t j = 0;
         for (; j + 4 <= len; j += 4) {  // four independent terms side by side, added in index order
-            const double e0 = kernel_value(j), e1 = kernel_value(j + 1), e2 = kernel_value(j + 2),
-                         e3 = kernel_value(j + 3);
-            sum = fma(s_w[j + 3], e3, fma(s_w[j + 2], e2, fma(s_w[j + 1], e1, fma(s_w[j], e0, sum))));
+            const double e0 = term(j), e1 = term(j + 1), e2 = term(j + 2), e3 = term(j + 3);
+            sum = (((sum + e0) + e1) + e2) + e3;
         }
-        for (; j < len; ++j) sum = fma(s_w[j], kernel_value(j), sum);
+        for (; j < len; ++j) sum += term(j);
     }
     if (r < count) w_out[r] = 1.0 / sum;
 }
@@ -655,12 +674,12 @@ void weights_fast_device(vxb_ctx* ctx, uint32_t dim, uint64_t count, const doubl
     if (count == 0) return;
     Scratch y_prev(ctx, n_prev * 4 * sizeof(double)), y_new(ctx, count * 4 * sizeof(double));
     LaunchScope scope(ctx, VXB_K_WEIGHTS);
-    whiten_kernel<3><<<grid_for(n_prev, 256), 256, 0, ctx->stream>>>(0, n_prev, theta_prev, chol_dev,
+    whiten_kernel<3><<<grid_for(n_prev, 256), 256, 0, ctx->stream>>>(0, n_prev, theta_prev, chol_dev, w_prev,
                                                                     y_prev.as<double>());
-    whiten_kernel<3><<<grid_for(count, 256), 256, 0, ctx->stream>>>(1, count, theta_new, chol_dev,
+    whiten_kernel<3><<<grid_for(count, 256), 256, 0, ctx->stream>>>(1, count, theta_new, chol_dev, nullptr,
                                                                    y_new.as<double>());
     abcsmc_weights_fast_kernel<3><<<grid_for(count, kWeightsBlock), kWeightsBlock, 0, ctx->stream>>>(
-        count, y_new.as<double>(), n_prev, y_prev.as<double>(), w_prev, ctx->log_table, w_out);
+        count, y_new.as<double>(), n_prev, y_prev.as<double>(), ctx->log_table, w_out);
     check_launch("abcsmc_weights_fast_kernel");
 }
 
