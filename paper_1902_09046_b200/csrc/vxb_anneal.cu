@@ -83,7 +83,7 @@ struct RunModel {  // one dataset under one prior
 __device__ __forceinline__ double softplus_fast(double b, const double2* tbl) {
     const double pos = b > 0.0 ? b : 0.0;
     const double mag = b > 0.0 ? b : -b;
-    return fma(kLn2, fast_log2(1.0 + fast_exp2_neg(-mag * kInvLn2, tbl), tbl), pos);
+    return fma(kLn2, fast_log2_short(1.0 + fast_exp2_neg4(-mag * kInvLn2, tbl), tbl), pos);
 }
 template <class A = Exact, bool kFast = false>
 __device__ __forceinline__ double log_lik(const Design& d, const RunModel& m, double b0, double b1,
@@ -173,7 +173,7 @@ __device__ double ess_after(const Ensemble& e, uint32_t np, double dt, double lw
     double s1 = 0.0, s2 = 0.0;
     for (uint32_t i = threadIdx.x; i < np; i += kAnnealBlock) {
         const double x = fma(dt, e.ll[i], lw0) - top;  // <= 0
-        const double w = kFast ? fast_exp2_neg(x * kInvLn2, tbl) : exp(x);
+        const double w = kFast ? fast_exp2_neg4(x * kInvLn2, tbl) : exp(x);
         s1 += w;
         s2 = fma(w, w, s2);
     }
@@ -253,7 +253,7 @@ __device__ uint32_t sweep(const Design& d, const RunModel& m, Ensemble& e, uint3
                 const Words32 w = philox4x32(*fk, static_cast<uint32_t>(pair), kDomProposal | static_cast<uint32_t>(key),
                                              0u, 0u);
                 u = fast_unit(w.a, w.b);
-                log_u = u > 0.0 ? kLn2 * fast_log2(u, tbl) : -INFINITY;
+                log_u = u > 0.0 ? kLn2 * fast_log2_short(u, tbl) : -INFINITY;
             } else {
                 const uint64_t upos = unif_base + static_cast<uint64_t>(q) * steps + r;
                 const Words w = philox2x64(key, upos >> 1);

@@ -571,24 +571,6 @@ __global__ void whiten_kernel(int mode, uint64_t n, const double* __restrict__ t
     out[i * (D + 1) + D] = mode == 0 ? log2(w[i]) - a : -a;
 }
 
-// 2^z for z <= ~0 with a degree-4 polynomial on the 1/64 grid of fast_exp2_neg's table:
-// relative error 4e-14, far below the Monte-Carlo error of an importance weight, one
-// FP64 instruction fewer per kernel term; arguments below -1000 give 0.
-__device__ __forceinline__ double weight_exp2(double z, const double2* tbl) {
-    const double tn = fma(z, 64.0, kMagic);
-    const int n = __double2loint(tn);           // round(64 z)
-    const double w = fma(tn - kMagic, -0.015625, z);
-    double p = 9.6181291076284772e-3;           // ln2^4/24
-    p = fma(p, w, 5.5504108664821580e-2);       // ln2^3/6
-    p = fma(p, w, 2.4022650695910071e-1);       // ln2^2/2
-    p = fma(p, w, 6.9314718055994531e-1);       // ln2
-    p = fma(p, w, 1.0);
-    const double t = reinterpret_cast<const double*>(tbl + kLogTableSize + kTrigTableSize)[n & 63];
-    const double r = p * t;
-    const int hi = __double2hiint(r) + ((n >> 6) << 20);
-    return z < -1000.0 ? 0.0 : __hiloint2double(hi, __double2loint(r));
-}
-
 template <int D>
 __global__ void __launch_bounds__(kWeightsBlock)
 abcsmc_weights_fast_kernel(uint64_t count, const double* __restrict__ y_new, uint64_t n_prev,
@@ -615,7 +597,7 @@ abcsmc_weights_fast_kernel(uint64_t count, const double* __restrict__ y_new, uin
             double z = fma(yi[0], lo.x, hi.y);
             z = fma(yi[1], lo.y, z);
             z = fma(yi[2], hi.x, z);
-            return weight_exp2(z + yi[D], s_tab);  // z <= 0 up to rounding
+            return fast_exp2_neg4(z + yi[D], s_tab);  // z <= 0 up to rounding
         };
         uint64_t j = 0;
         for (; j + 4 <= len; j += 4) {  // four independent terms side by side, added in index order
