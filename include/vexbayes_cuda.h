@@ -180,7 +180,9 @@ int vxb_rng_fill_gaussian_fast(vxb_ctx* ctx, int precision, uint64_t seed, uint6
  * parity tests: fn 0 log2_pos, 1 ln_pos, 2 exp2_clamped, 3 sinpi, 4 cospi,
  * 5 pow_pos (x = base, y = exponent; y ignored otherwise); and of the
  * throughput-mode functions, for accuracy tests: fn 6 log2 (x > 0 normal),
- * 7 2^x (|x| < 1000), 8 1/x (normal x). */
+ * 7 2^x (|x| < 1000), 8 1/x (normal x); fn 9: exp exactly as the host libm
+ * evaluates it (glibc >= 2.28, FMA build) -- what std::exp returns in
+ * smc.cpp:214,278,299 and numeric.cpp:16-17, bit for bit. */
 int vxb_fastmath_eval(vxb_ctx* ctx, int fn, const double* x, const double* y, uint64_t n,
                       double* out);
 /* partition (blocked.cpp:34-63): writes workers pairs [begin,end). Host-side. */

@@ -286,6 +286,22 @@ class Oracle(_Base):
         self._call("compute_cutoff", _ptr(p), u64(p.size), f64(alpha), C.byref(out))
         return out.value
 
+    # ---- the restatement of the host libm's exp (pins csrc/vxb_libmexp.cuh)
+    def exp_restated(self, x):
+        """(restated exp, live std::exp) of every x."""
+        x = _f64(x)
+        out, live = np.zeros_like(x), np.zeros_like(x)
+        self._call("exp_restated", _ptr(x), u64(x.size), _ptr(out), _ptr(live))
+        return out, live
+
+    def exp_restated_sweep(self, seed, n, lo, hi, threads=None):
+        """Number of pseudo-random arguments in [lo, hi) on which the restatement and
+        the live std::exp differ bitwise, and the first such argument (NaN if none)."""
+        m, first = u64(), f64(float("nan"))
+        self._call("exp_restated_sweep", u64(seed), u64(n), f64(lo), f64(hi),
+                   C.c_uint(threads or (os.cpu_count() or 1)), C.byref(m), C.byref(first))
+        return m.value, first.value
+
     # ---- SMC pieces
     def ess(self, lw):
         lw = _f64(lw)

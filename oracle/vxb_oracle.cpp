@@ -858,6 +858,111 @@ int vxo_compute_cutoff(const double* p, std::uint64_t n, double alpha, double* o
     });
 }
 
+// ------------------------------------------------ libm exp, restated
+// std::exp is what the reference's weight algebra calls (smc.cpp:214,278,299,
+// numeric.cpp:16-17).  The oracle itself keeps calling std::exp; this restatement of
+// the algorithm behind it (glibc >= 2.28: N = 128 table, degree-5 polynomial, the
+// multiply-adds contracted as the x86-64 FMA build evaluates them) exists so that the
+// device copy of the same algorithm (csrc/vxb_libmexp.cuh) can be pinned: restated ==
+// std::exp on this machine (tests/test_oracle_pins.py), device == restated == std::exp
+// on the GPU box (tests/test_gpu_workloads.py).
+struct ExpEntry {
+    std::uint64_t tail, sbits;
+};
+static const ExpEntry kExpTable[128] = {
+#define VXB_EXP_PAIR(a, b) {a, b}
+#include "../paper_1902_09046_b200/csrc/vxb_libm_exp_entries.inc"
+#undef VXB_EXP_PAIR
+};
+static double exp_restated_special(double tmp, std::uint64_t sbits, std::uint64_t ki) {
+    if ((ki & 0x80000000ULL) == 0) {
+        sbits -= 1009ULL << 52;
+        const double scale = bit_cast<double>(sbits);
+        return 0x1p1009 * std::fma(scale, tmp, scale);
+    }
+    sbits += 1022ULL << 52;
+    const double scale = bit_cast<double>(sbits);
+    const double m = scale * tmp;
+    double y = scale + m;
+    if (y < 1.0) {
+        const double hi = 1.0 + y;
+        const double lo = (scale - y) + m;
+        double t = (1.0 - hi) + y;
+        t = t + lo;
+        y = (t + hi) - 1.0;
+        if (y == 0.0) y = 0.0;
+    }
+    return 0x1p-1022 * y;
+}
+static double exp_restated(double x) {
+    const std::uint32_t abstop = static_cast<std::uint32_t>(bit_cast<std::uint64_t>(x) >> 52) & 0x7ffu;
+    bool special = false;
+    if (abstop - 0x3c9u >= 0x3fu) {
+        if (static_cast<std::int32_t>(abstop - 0x3c9u) < 0) return 1.0 + x;
+        if (abstop >= 0x409u) {
+            if (bit_cast<std::uint64_t>(x) == 0xfff0000000000000ULL) return 0.0;
+            if (abstop >= 0x7ffu) return 1.0 + x;
+            return x < 0.0 ? 0.0 : std::numeric_limits<double>::infinity();
+        }
+        special = true;
+    }
+    double kd = std::fma(x, 0x1.71547652b82fep+7, 0x1.8p+52);
+    const std::uint64_t ki = bit_cast<std::uint64_t>(kd);
+    kd -= 0x1.8p+52;
+    double r = std::fma(kd, -0x1.62e42fefa0000p-8, x);
+    r = std::fma(kd, -0x1.cf79abc9e3b3ap-47, r);
+    const ExpEntry e = kExpTable[ki & 127u];
+    const std::uint64_t sbits = e.sbits + (ki << 45);
+    const double tail = bit_cast<double>(e.tail);
+    const double r2 = r * r;
+    const double p23 = std::fma(0x1.555555555543cp-3, r, 0x1.ffffffffffdbdp-2);
+    const double t1 = tail + r;
+    const double p45 = std::fma(r, 0x1.1111167a4d017p-7, 0x1.55555cf172b91p-5);
+    const double t2 = std::fma(p23, r2, t1);
+    const double tmp = std::fma(r2 * r2, p45, t2);
+    if (special) return exp_restated_special(tmp, sbits, ki);
+    const double scale = bit_cast<double>(sbits);
+    return std::fma(scale, tmp, scale);
+}
+
+// libm exp restatement: out[i] = exp_restated(x[i]); libm[i] = std::exp(x[i]) (optional)
+int vxo_exp_restated(const double* x, std::uint64_t n, double* out, double* libm) {
+    return guarded([&] {
+        for (std::uint64_t i = 0; i < n; ++i) {
+            out[i] = exp_restated(x[i]);
+            if (libm) libm[i] = std::exp(x[i]);
+        }
+    });
+}
+// n pseudo-random arguments (splitmix64 of seed + i mapped to [lo, hi)): how many
+// differ between the restatement and the live std::exp (bitwise; NaN never occurs);
+// *first_bad receives the first offending argument.
+int vxo_exp_restated_sweep(std::uint64_t seed, std::uint64_t n, double lo, double hi,
+                           unsigned threads, std::uint64_t* mismatches, double* first_bad) {
+    return guarded([&] {
+        if (threads == 0) threads = 1;
+        std::vector<std::uint64_t> bad(threads, 0);
+        std::vector<double> firsts(threads, std::numeric_limits<double>::quiet_NaN());
+        std::vector<std::thread> pool;
+        for (unsigned t = 0; t < threads; ++t)
+            pool.emplace_back([&, t] {
+                for (std::uint64_t i = t; i < n; i += threads) {
+                    const double u = static_cast<double>(splitmix64(seed + i) >> 11) * 0x1p-53;
+                    const double x = lo + u * (hi - lo);
+                    const double a = exp_restated(x), b = std::exp(x);
+                    if (bit_cast<std::uint64_t>(a) != bit_cast<std::uint64_t>(b)) {
+                        if (bad[t]++ == 0) firsts[t] = x;
+                    }
+                }
+            });
+        for (auto& th : pool) th.join();
+        *mismatches = 0;
+        for (unsigned t = 0; t < threads; ++t) {
+            *mismatches += bad[t];
+            if (bad[t] && std::isnan(*first_bad)) *first_bad = firsts[t];
+        }
+    });
+}
 // -------------------------------------------------------------- SMC pieces
 // ess: smc.cpp:208-219
 int vxo_ess(const double* lw, std::uint64_t n, double* out) {

@@ -8,6 +8,7 @@
 
 #include "vxb_common.cuh"
 #include "vxb_rng.cuh"
+#include "vxb_libmexp.cuh"
 
 namespace vxb {
 
@@ -111,7 +112,7 @@ __global__ void fastmath_kernel(int fn, const double* x, const double* y, uint64
                                 const double2* fast_table) {
     // functions 6-8: the throughput-mode log2 / 2^z / reciprocal on the shared tables
     __shared__ double2 s_tab[kFastTableSize];
-    if (fn >= 6) {
+    if (fn >= 6 && fn <= 8) {
         for (int k = threadIdx.x; k < kFastTableSize; k += blockDim.x) s_tab[k] = fast_table[k];
         __syncthreads();
     }
@@ -128,7 +129,8 @@ __global__ void fastmath_kernel(int fn, const double* x, const double* y, uint64
         case 5: r = pow_pos<Exact>(a, y[i]); break;
         case 6: r = fast_log2(a, s_tab); break;
         case 7: r = fast_exp2(a, s_tab); break;
-        default: r = fast_rcp(a); break;
+        case 8: r = fast_rcp(a); break;
+        default: r = libm_exp(a); break;
     }
     out[i] = r;
 }
@@ -155,12 +157,15 @@ extern "C" int vxb_init(vxb_ctx** out, int device) {
         ctx->device = device;
         VXB_CUDA(cudaGetDeviceProperties(&ctx->prop, device));
         VXB_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-        // keep stream-ordered scratch cached between calls
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-            uint64_t threshold = ~0ull;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
-        }
+        // keep stream-ordered scratch cached between calls -- in a pool of our own
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        VXB_CUDA(cudaMemPoolCreate(&ctx->pool, &props));
+        uint64_t threshold = ~0ull;
+        VXB_CUDA(cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &threshold));
         double table[2 * kFastTableSize];
         build_fast_log_table(table);
         VXB_CUDA(cudaMalloc(&ctx->log_table, sizeof(table)));
@@ -179,6 +184,7 @@ extern "C" void vxb_shutdown(vxb_ctx* ctx) {
     }
     for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
     cudaStreamDestroy(ctx->stream);
+    if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
     cudaFree(ctx->log_table);
     for (void* a : ctx->arena) cudaFree(a);
     delete ctx;
@@ -343,7 +349,7 @@ extern "C" int vxb_fastmath_eval(vxb_ctx* ctx, int fn, const double* x, const do
                                  uint64_t n, double* out) {
     return guarded([&] {
         use(ctx);
-        require(fn >= 0 && fn <= 8, "invalid-argument", "unknown fastmath function");
+        require(fn >= 0 && fn <= 9, "invalid-argument", "unknown fastmath function");
         if (n == 0) return;
         require(x && out && (fn != 5 || y), "invalid-argument", "null argument");
         Staged d_x(ctx, x, n * 8, true, false);

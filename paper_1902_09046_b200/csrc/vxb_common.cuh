@@ -53,6 +53,10 @@ int guarded(F&& f) {
 struct vxb_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    // private stream-ordered pool for Staged / Scratch: the release threshold is set
+    // on THIS pool only, and vxb_shutdown destroys it -- the device's default pool
+    // (shared with torch or any other cudaMallocAsync user in the process) is untouched
+    cudaMemPool_t pool = nullptr;
     cudaDeviceProp prop{};
     double2* log_table = nullptr;  // fast fp64 generator table (vxb_rng.cuh)
     bool profiling = false;
@@ -96,7 +100,7 @@ public:
             return;
         }
         owned_ = true;
-        VXB_CUDA(cudaMallocAsync(&dev_, bytes, ctx->stream));
+        VXB_CUDA(cudaMallocFromPoolAsync(&dev_, bytes, ctx->pool, ctx->stream));
         if (is_input)
             VXB_CUDA(cudaMemcpyAsync(dev_, user, bytes, cudaMemcpyHostToDevice, ctx->stream));
     }
@@ -145,7 +149,7 @@ inline void* arena_get(vxb_ctx* ctx, int slot, size_t bytes) {
 class Scratch {
 public:
     Scratch(vxb_ctx* ctx, size_t bytes) : ctx_(ctx) {
-        if (bytes) VXB_CUDA(cudaMallocAsync(&p_, bytes, ctx->stream));
+        if (bytes) VXB_CUDA(cudaMallocFromPoolAsync(&p_, bytes, ctx->pool, ctx->stream));
     }
     Scratch(const Scratch&) = delete;
     Scratch& operator=(const Scratch&) = delete;

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "vxb_internal.cuh"
+#include "vxb_libmexp.cuh"
 
 #ifndef VXB_PROP_MINB
 #define VXB_PROP_MINB 1
@@ -56,47 +57,72 @@ __global__ void max_final_kernel(const double* part, double* out) {
     for (int b = 0; b < kRedGrid; ++b) m = fmax(m, part[b]);
     *out = m;
 }
-__global__ void __launch_bounds__(kRedBlock)
-expsum_partial_kernel(const double* __restrict__ x, uint64_t n, const double* __restrict__ mx,
-                      double* __restrict__ part /* 2 x kRedGrid */) {
-    __shared__ double s1[kRedBlock], s2[kRedBlock];
+// Strictly sequential sums in the reference's order (smc.cpp:208-219, 276-283,
+// numeric.cpp:11-18): s1 = sum_i exp(x_i - max), s2 = sum_i exp(x_i - max)^2, added
+// left to right, every exp the host libm's (vxb_libmexp.cuh) -- so ess, logsumexp and
+// the cumulative weights of resample_multinomial are bit-identical to the CPU.  A
+// floating-point running sum cannot be re-associated without changing its roundings,
+// so the chain itself is one thread; what is parallel is everything around it: warps
+// 1..3 evaluate the exponentials of the NEXT tile into shared memory (and, for the
+// cumulative form, all threads store the finished tile) while thread 0 walks the
+// current one.  The chain costs one dependent DADD per element.
+constexpr int kSeqTile = 2048;
+constexpr int kSeqThreads = 128;
+template <bool kCum>
+__global__ void __launch_bounds__(kSeqThreads)
+seq_expsum_kernel(const double* __restrict__ x, const double* __restrict__ mx, uint64_t n,
+                  double* __restrict__ cum, double* __restrict__ sums /* 2 */) {
+    __shared__ double buf[2][kSeqTile];
     const double m = *mx;
-    double a = 0.0, b = 0.0;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kRedBlock + threadIdx.x; i < n;
-         i += static_cast<uint64_t>(kRedGrid) * kRedBlock) {
-        const double e = exp(x[i] - m);
-        a += e;
-        b += e * e;
-    }
-    s1[threadIdx.x] = a;
-    s2[threadIdx.x] = b;
+    const uint32_t tid = threadIdx.x;
+    const uint64_t tiles = (n + kSeqTile - 1) / kSeqTile;
+    for (uint64_t k = tid; k < min(static_cast<uint64_t>(kSeqTile), n); k += kSeqThreads)
+        buf[0][k] = libm_exp(__dsub_rn(x[k], m));
     __syncthreads();
-    for (int s = kRedBlock / 2; s > 0; s >>= 1) {
-        if (threadIdx.x < s) {
-            s1[threadIdx.x] += s1[threadIdx.x + s];
-            s2[threadIdx.x] += s2[threadIdx.x + s];
+    double s1 = 0.0, s2 = 0.0;
+    for (uint64_t t = 0; t < tiles; ++t) {
+        const uint64_t t0 = t * kSeqTile;
+        const uint32_t len = static_cast<uint32_t>(min(static_cast<uint64_t>(kSeqTile), n - t0));
+        double* cur = buf[t & 1];
+        if (tid == 0) {
+            if (kCum) {
+#pragma unroll 8
+                for (uint32_t k = 0; k < len; ++k) {
+                    s1 = __dadd_rn(s1, cur[k]);
+                    cur[k] = s1;
+                }
+            } else {
+#pragma unroll 8
+                for (uint32_t k = 0; k < len; ++k) {
+                    const double e = cur[k];
+                    s1 = __dadd_rn(s1, e);
+                    s2 = __dadd_rn(s2, __dmul_rn(e, e));
+                }
+            }
+        } else if (tid >= 32 && t + 1 < tiles) {
+            const uint64_t n0 = t0 + kSeqTile;
+            const uint32_t nlen = static_cast<uint32_t>(min(static_cast<uint64_t>(kSeqTile), n - n0));
+            double* nxt = buf[(t + 1) & 1];
+            for (uint32_t k = tid - 32; k < nlen; k += kSeqThreads - 32)
+                nxt[k] = libm_exp(__dsub_rn(x[n0 + k], m));
         }
         __syncthreads();
+        if (kCum) {
+            for (uint32_t k = tid; k < len; k += kSeqThreads) cum[t0 + k] = cur[k];
+            __syncthreads();  // the tile after next is written into this buffer
+        }
     }
-    if (threadIdx.x == 0) {
-        part[blockIdx.x] = s1[0];
-        part[kRedGrid + blockIdx.x] = s2[0];
+    if (tid == 0) {
+        sums[0] = s1;
+        sums[1] = s2;
     }
-}
-__global__ void expsum_final_kernel(const double* part, double* out /* 2 */) {
-    double a = 0.0, b = 0.0;
-    for (int i = 0; i < kRedGrid; ++i) {
-        a += part[i];
-        b += part[kRedGrid + i];
-    }
-    out[0] = a;
-    out[1] = b;
 }
 
-// max, sum exp(x-max), sum exp(x-max)^2 of a device array -> host
+// max, then the sequential sums above.  cum_dev != nullptr: also the inclusive
+// cumulative sums (resample_multinomial's `cum`); s2 is then not computed.
 void max_and_expsums(vxb_ctx* ctx, const double* x_dev, uint64_t n, double* mx, double* s1,
-                     double* s2) {
-    Scratch part(ctx, sizeof(double) * 2 * kRedGrid);
+                     double* s2, double* cum_dev = nullptr) {
+    Scratch part(ctx, sizeof(double) * kRedGrid);
     Scratch res(ctx, sizeof(double) * 3);
     {
         LaunchScope scope(ctx, VXB_K_RESAMPLE);
@@ -114,10 +140,13 @@ void max_and_expsums(vxb_ctx* ctx, const double* x_dev, uint64_t n, double* mx, 
     }
     {
         LaunchScope scope(ctx, VXB_K_RESAMPLE);
-        expsum_partial_kernel<<<kRedGrid, kRedBlock, 0, ctx->stream>>>(x_dev, n, res.as<double>(),
-                                                                     part.as<double>());
-        expsum_final_kernel<<<1, 1, 0, ctx->stream>>>(part.as<double>(), res.as<double>() + 1);
-        check_launch("expsum kernels");
+        if (cum_dev)
+            seq_expsum_kernel<true><<<1, kSeqThreads, 0, ctx->stream>>>(x_dev, res.as<double>(), n,
+                                                                        cum_dev, res.as<double>() + 1);
+        else
+            seq_expsum_kernel<false><<<1, kSeqThreads, 0, ctx->stream>>>(x_dev, res.as<double>(), n, nullptr,
+                                                                         res.as<double>() + 1);
+        check_launch("seq_expsum_kernel");
     }
     VXB_CUDA(cudaMemcpyAsync(h, res.as<double>(), 24, cudaMemcpyDeviceToHost, ctx->stream));
     VXB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -126,30 +155,6 @@ void max_and_expsums(vxb_ctx* ctx, const double* x_dev, uint64_t n, double* mx, 
 }
 
 // --------------------------------------------- resample_multinomial pieces
-__global__ void expw_kernel(const double* __restrict__ lw, const double* __restrict__ mx, uint64_t n,
-                            double* __restrict__ e) {
-    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i < n) e[i] = exp(lw[i] - *mx);
-}
-// Strictly sequential running sum (the order of smc.cpp:276-280): one warp
-// stages 1024-element tiles through shared memory, lane 0 accumulates.
-__global__ void __launch_bounds__(32) sequential_cumsum_kernel(double* __restrict__ e, uint64_t n) {
-    __shared__ double tile[1024];
-    double run = 0.0;
-    for (uint64_t t0 = 0; t0 < n; t0 += 1024) {
-        const uint64_t len = min(static_cast<uint64_t>(1024), n - t0);
-        for (uint64_t k = threadIdx.x; k < len; k += 32) tile[k] = e[t0 + k];
-        __syncwarp();
-        if (threadIdx.x == 0)
-            for (uint64_t k = 0; k < len; ++k) {
-                run = __dadd_rn(run, tile[k]);
-                tile[k] = run;
-            }
-        __syncwarp();
-        for (uint64_t k = threadIdx.x; k < len; k += 32) e[t0 + k] = tile[k];
-        __syncwarp();
-    }
-}
 __device__ __forceinline__ uint64_t upper_bound_dev(const double* __restrict__ cum, uint64_t n,
                                                     double target) {
     uint64_t lo = 0, hi = n;  // std::upper_bound (smc.cpp:287), clamped (smc.cpp:289)
@@ -725,17 +730,12 @@ extern "C" int vxb_resample_multinomial(vxb_ctx* ctx, uint64_t n, uint32_t dim, 
         Staged d_out(ctx, particles_out, n * dim * 8, false, true);
         Staged d_anc(ctx, ancestors, n * 8, false, true);
         double mx, s1, s2;
-        max_and_expsums(ctx, d_lw.as<double>(), n, &mx, &s1, &s2);
+        Scratch d_cum(ctx, n * 8);
+        max_and_expsums(ctx, d_lw.as<double>(), n, &mx, &s1, &s2, d_cum.as<double>());
         require(mx > -INFINITY, "degenerate-ensemble", "all weights are zero");
         require(std::isfinite(s1) && s1 > 0.0, "degenerate-ensemble", "weight sum is not finite");
-        Scratch d_cum(ctx, n * 8);
-        Scratch d_mx(ctx, 8);
-        VXB_CUDA(cudaMemcpyAsync(d_mx.as<void>(), &mx, 8, cudaMemcpyHostToDevice, ctx->stream));
         {
             LaunchScope scope(ctx, VXB_K_RESAMPLE);
-            expw_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(d_lw.as<double>(), d_mx.as<double>(),
-                                                                 n, d_cum.as<double>());
-            sequential_cumsum_kernel<<<1, 32, 0, ctx->stream>>>(d_cum.as<double>(), n);
             resample_draw_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
                 d_cum.as<double>(), n, dim, stream_key(splitmix64(seed), stream_id), d_in.as<double>(),
                 d_out.as<double>(), d_anc.as<uint64_t>());

@@ -327,3 +327,24 @@ def test_tb_gillespie_restatement_equals_reference(oracle, ref):
         for x, y in zip(a, b):
             assert np.array_equal(x, y, equal_nan=True)
         assert a[3].any()
+
+
+def test_libm_exp_restatement_equals_live_libm(oracle):
+    """The exp algorithm csrc/vxb_libmexp.cuh runs on the device (glibc's N = 128 table
+    scheme, FMA build) restated on the CPU: identical, bit for bit, to this machine's
+    std::exp -- the function the reference's weight algebra calls (smc.cpp:214,278,299,
+    numeric.cpp:16-17).  Sweeps cover the weight domain (x <= 0), the subnormal and
+    underflow range, overflow, tiny arguments and the special values."""
+    for lo, hi, n in ((-50.0, 0.0, 6_000_000), (-760.0, -690.0, 2_000_000),
+                      (-1100.0, 800.0, 2_000_000), (-1e-3, 1e-3, 1_000_000),
+                      (700.0, 712.0, 500_000), (-1e-15, 1e-15, 200_000)):
+        bad, first = oracle.exp_restated_sweep(20240 + int(n), n, lo, hi)
+        assert bad == 0, (lo, hi, first)
+    x = np.array([0.0, -0.0, 1e-300, -1e-300, 1e-17, -745.2, -745.13321910194122, -746.0,
+                  -708.4, -709.0, 709.78, 709.79, 710.0, np.inf, -np.inf, np.nan, -1023.9,
+                  -1024.0, -5e-324, 2.0 ** -54, -(2.0 ** -55), 512.0, -512.0, -511.99999,
+                  1.0, -1.0, 0.5 * math.log(2.0), -math.log(2.0) / 256.0])
+    got, live = oracle.exp_restated(x)
+    assert np.array_equal(got.view(np.uint64), live.view(np.uint64))
+    assert np.array_equal(live[:11].view(np.uint64),
+                          np.array([math.exp(v) for v in x[:11]]).view(np.uint64))
