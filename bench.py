@@ -8,15 +8,21 @@ evenly over the GPUs (strong scaling, as config 1 states), accepted samples
 gathered over NCCL.  One "step" = one full pass over the N particles.
 
     python bench.py --gpus 1 --steps 5 --warmup 3
+    python bench.py --gpus N ...              # starts N ranks itself (torch.distributed.run)
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
     python bench.py --impl reference ...      # the reference's CPU path, host cores
 
 Prints ONE JSON line (rank 0).  Inputs are synthetic (seeded); see DESIGN.md.
+At N = 1 the line also carries `configs`: every other BASELINE config (0, 2, 3, 4) and
+the reference's own workloads (toggle switch, weak-informativity test, TB Gillespie,
+resample_multinomial) at full size, each timed with CUDA events under the same NVML
+clock sampler as the headline.
 """
 import argparse
 import json
 import math
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -44,7 +50,65 @@ def parse():
                     choices=["f64_fast", "f64_ref", "f32_fast", "f32_ref"])
     ap.add_argument("--no-extras", action="store_true", help="skip variants and cpu baseline")
     ap.add_argument("--cpu-sample", type=float, default=4e5)
+    ap.add_argument("--comm", default="torch", choices=["torch", "native"],
+                    help="N > 1: gather over torch.distributed's NCCL or the library's own "
+                         "communicator (vxb_comm_*, bootstrapped through torch.distributed)")
+    ap.add_argument("--selftest-dist", action="store_true",
+                    help="CPU check of the launch path: gloo ranks, one packed gather, no GPU work")
     return ap.parse_args()
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(args):
+    """`python bench.py --gpus N` without a launcher: start the N ranks ourselves, the
+    way the driver does (torch.distributed.run, one process per GPU, rendezvous on
+    127.0.0.1).  NCCL's communicator lines go to stderr (NCCL_DEBUG=INFO, INIT only)."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def selftest_dist(args, rank, world):
+    """The launch + exchange path on CPU (gloo): every rank builds a packed accepted
+    block (include/vexbayes_cuda.h: vxb_accept_layout) with known contents, ONE
+    all_gather_into_tensor moves them, rank 0 checks the rank-order concatenation."""
+    import torch
+    import torch.distributed as dist
+    from paper_1902_09046_b200 import _abi as A, dist as D, lib
+    if world > 1:
+        dist.init_process_group("gloo")
+    lay = lib.accept_layout(A.VXB_F64, 3, 64)
+    block = torch.zeros(int(lay.stride), dtype=torch.uint8)
+    idx, params, rho, count = D.packed_views(block, lay, A.VXB_F64, 3)
+    k = 5 + rank
+    begin, _ = D.shard_range(1000, world, rank)
+    idx[0, :k] = torch.arange(begin, begin + k)
+    rho[0, :k] = 0.5 + rank
+    count[0] = k
+    allb = D.gather_packed(block, world) if world > 1 else block
+    n_acc, g_idx, _, g_rho, over = lib.accept_unpack(lay, A.VXB_F64, 3, world, allb.numpy())
+    ok = (n_acc == sum(5 + r for r in range(world)) and not over and bool((np.diff(g_idx.astype(np.int64)) > 0).all()))
+    if rank == 0:
+        print(json.dumps({"selftest": "dist", "ok": bool(ok), "n_gpus": world, "backend": "gloo",
+                          "accepted": int(n_acc), "pid": os.getpid(),
+                          "launched_by": "torch.distributed.run" if "TORCHELASTIC_RUN_ID" in os.environ
+                          else "direct"}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0 if ok else 1
 
 
 class ClockSampler:
@@ -181,21 +245,50 @@ def run_reference(args, rank, world):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        sys.exit(spawn_ranks(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
+                 "(python bench.py --gpus N starts them itself)")
+    if args.selftest_dist:
+        sys.exit(selftest_dist(args, rank, world))
 
     import torch
     import torch.distributed as dist
     from paper_1902_09046_b200 import _abi as A, dist as D, lib, models as M
 
     torch.cuda.set_device(local)
+    comm, comm_note = None, "single GPU: no collective"
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = lib.Context(local)
+    if world > 1:
+        comm_note = "torch.distributed NCCL all_gather_into_tensor of the packed accepted block"
+        if args.comm == "native":
+            # the library's own NCCL communicator; its unique id travels through
+            # torch.distributed.  Every rank must agree on the outcome.
+            ok = torch.ones(1, dtype=torch.int32, device=f"cuda:{local}")
+            try:
+                uid = [lib.comm_unique_id().tobytes() if rank == 0 else None]
+                dist.broadcast_object_list(uid, src=0)
+                comm = lib.Comm(ctx, np.frombuffer(uid[0], dtype=np.uint8), rank, world)
+            except Exception as e:  # fall back to torch.distributed rather than lose the run
+                ok.zero_()
+                comm_err = repr(e)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()) == 1:
+                comm_note = f"library NCCL (vxb_sharded_abc_reject, NCCL {lib.comm_version()})"
+            else:
+                if comm is not None:
+                    comm.close()
+                comm = None
+                comm_note += " (native communicator failed on some rank: fell back)"
     info = ctx.device_info()
     ext = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
     n_total = int(args.particles)
@@ -238,7 +331,7 @@ def main():
 
         def fn(s):
             return D.sharded_reject(ctx, model, M.keying(1337 + s), n_total, obs, eps,
-                                    buffers=buffers)
+                                    buffers=buffers, comm=comm)
         return fn
 
     def host_step(model):
@@ -291,7 +384,7 @@ def main():
                                f"fixed epsilon from config0, {args.variant}",
                    "particles_per_step": n_total, "sde_steps_per_particle": STEPS_PER_SIM,
                    "epsilon": eps, "accepted_per_step": n_acc, "variant": args.variant,
-                   "sharding": f"particles/{world}",
+                   "sharding": f"particles/{world}", "exchange": comm_note,
                    "l2": "no reusable input (compute-bound); per-step rho scratch "
                          f"{(end - begin) * real / 1e6:.0f} MB exceeds L2"},
         "e2e": {"value": e2e_sims, "unit": "sims/s", "h2d_bytes_per_step": h2d,
@@ -323,12 +416,150 @@ def main():
                               "frac_of_nominal_peak": sv * FLOPS_PER_SIM / 1e12 / pk}
         line["variants"] = variants
         if rank == 0 and world == 1:
+            line["configs"] = all_configs(ctx, timed, obs, local)
             line["cpu_baseline"] = cpu_baseline(args, obs, eps)
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def all_configs(ctx, timed, obs, device):
+    """Every other workload at full size, one JSON object each: CUDA-event time per
+    pass (W >= 1 warm-up, K >= 3 timed passes, enough of them to give the clock sampler a
+    window), units/s, the algorithmic flop rate under SURVEY.md 8(d)'s prices against
+    the nominal FP64 peak, and the NVML clock summary of that timed region."""
+    import torch
+    from paper_1902_09046_b200 import _abi as A, bench_harness as B, lib, models as M
+    peak = NOMINAL_PEAK["f64"] * 1e12
+    res = {}
+
+    def run(name, fn, units, unit, flops_per_unit=None, target_s=0.6, extra=None):
+        # calibrate the repetition count on one untimed pass (which is also a warm-up)
+        ms1, _ = timed(lambda s: fn(), 1, 1)
+        k = max(3, min(200, int(math.ceil(target_s * 1e3 / max(ms1, 1e-3)))))
+        with ClockSampler(device, period=0.05) as clocks:
+            ms, out = timed(lambda s: fn(), 1, k)
+        per = ms / k
+        e = {"ms": per, "passes": k, "units": units, "unit": unit,
+             "units_per_s": units / (per * 1e-3), "clocks": clocks.summary()}
+        if flops_per_unit:
+            e["flops_per_unit"] = flops_per_unit
+            e["tflops_algorithmic"] = units * flops_per_unit / (per * 1e-3) / 1e12
+            e["frac_of_nominal_fp64"] = units * flops_per_unit / (per * 1e-3) / peak
+        if extra:
+            e.update(extra(out))
+        res[name] = e
+        return out
+
+    m = M.logistic_model()
+    # ---- config 0: N = 1e6, reference-exact streams, accept the 0.1% nearest
+    n0 = 1_000_000
+    rho = torch.empty(n0, dtype=torch.float64, device=f"cuda:{device}")
+    failed = torch.empty(n0, dtype=torch.uint8, device=f"cuda:{device}")
+
+    def c0(model):
+        def fn():
+            ctx.abc_prior_predictive(model, M.keying(1337), n0, 0, n0, obs, rho=rho, failed=failed)
+            return ctx.select_epsilon(rho, failed, 1e-3, cap=2000, precision=A.VXB_F64, n=n0)
+        return fn
+    run("config0_exact", c0(m), n0, "sims", FLOPS_PER_SIM,
+        extra=lambda o: {"epsilon": o[0], "accepted": o[2]})
+    run("config0_fast", c0(M.logistic_model(rng=A.VXB_RNG_FAST)), n0, "sims", FLOPS_PER_SIM,
+        extra=lambda o: {"epsilon": o[0], "accepted": o[2]})
+
+    # ---- config 2: 64 lambdas x 1e6 datasets x n = 100
+    nl, mt, nd = 64, 1_000_000, 100
+    lam = np.array(M.lambda_grid(nl))
+    ln = np.array([-0.5 * math.log(2.0 * math.pi * (l * l + 1.0 / nd)) for l in lam])
+    ybar = float((3.0 + ctx.rng_fill_gaussian(lib.derive_seed(2, [90]), 0, 0, nd)).mean())
+    exact_p = np.array([math.erfc(abs(ybar) / math.sqrt(2.0 * (l * l + 1.0 / nd))) for l in lam])
+    for name, rng in (("config2_exact", A.VXB_RNG_REF), ("config2_fast", A.VXB_RNG_FAST)):
+        mdl = M.normal_mean_model(nd, rng=rng)
+        run(name, lambda mdl=mdl: ctx.ppp_pvalues(mdl, lam, ln, mt, 0, mt, 1337, ybar), nl * mt,
+            "datasets", 4960,
+            extra=lambda o: {"max_abs_err_vs_closed_form": float(np.abs(o[1] - exact_p).max()),
+                             "mc_standard_error_bound": 5e-4})
+
+    # ---- config 3: ABC-SMC, N = 1e5 x 10 generations
+    cfg = A.vxb_abcsmc_cfg()
+    cfg.particles, cfg.generations = 100_000, 10
+    cfg.quantile, cfg.kernel_scale, cfg.jitter, cfg.round_size, cfg.max_rounds, cfg.seed = 0.5, 2.0, 1e-10, 0, 0, 1337
+    for name, mdl in (("config3_exact", m), ("config3_fast", M.logistic_model(rng=A.VXB_RNG_FAST))):
+        run(name, lambda mdl=mdl: ctx.abcsmc_run(mdl, cfg, obs), cfg.particles * cfg.generations,
+            "particle-generations", target_s=1.0,
+            extra=lambda o: {"proposals_simulated_upper_bound": int(o["proposals"].sum()),
+                             "epsilon_last": float(o["epsilon"][-1]), "ess_last": float(o["ess"][-1]),
+                             "weight_pairs": int(cfg.particles) ** 2 * (cfg.generations - 1)})
+    for name in ("config3_exact", "config3_fast"):
+        # flop rate: every proposal priced as a simulation (an upper bound: proposals
+        # outside the prior box are not simulated) + 50 flop per importance-weight pair
+        e = res[name]
+        fl = e["proposals_simulated_upper_bound"] * FLOPS_PER_SIM + e["weight_pairs"] * 50
+        e["tflops_algorithmic_upper_bound"] = fl / (e["ms"] * 1e-3) / 1e12
+        e["frac_of_nominal_fp64_upper_bound"] = fl / (e["ms"] * 1e-3) / peak
+
+    # ---- config 4: MLMC tau-leap, 6 levels x 1e6 paths
+    mc = A.vxb_mlmc_cfg()
+    mc.levels, mc.refine, mc.tau0, mc.t_end, mc.paths, mc.seed = 6, 4, 1.0, 30.0, 1_000_000, 1337
+    fine = [30 * 4 ** l for l in range(6)]
+    steps = mc.paths * sum(f if l == 0 else f + f // 4 for l, f in enumerate(fine))
+    flops = mc.paths * (fine[0] * 130 + sum(f * 370 for f in fine[1:]))
+    for name, rng in (("config4_exact", A.VXB_RNG_REF), ("config4_fast", A.VXB_RNG_FAST)):
+        mm = M.mm_tauleap_model(rng=rng)
+        run(name, lambda mm=mm: ctx.mlmc_tauleap(mm, mc), steps, "path-steps", flops / steps,
+            target_s=1.5, extra=lambda o: {"estimate": o["estimate"], "std_error": o["std_error"]})
+
+    # ---- the paper's toggle-switch ABC: N = 8064, C = 8000, T = 600 (PAPER.md:355,402)
+    n_t, c_t, t_t = 8064, 8000, 600
+    tm = M.toggle_model(t_t, c_t)
+    tobs = ctx.simulate_at(tm, M.TOGGLE_MIDPOINT, lib.derive_seed(1337, [90]), 0, 0)
+    trho = torch.empty(n_t, dtype=torch.float64, device=f"cuda:{device}")
+    cell_steps = n_t * c_t * (t_t - 1)
+    run("toggle_exact", lambda: ctx.abc_prior_predictive(tm, M.keying(1337, A.VXB_KEY_WORKER, 16, 4),
+                                                         n_t, 0, n_t, tobs, rho=trho),
+        cell_steps, "cell-steps", 228, target_s=2.0, extra=lambda o: {"published_best_s": 69.0})
+    tmf = M.toggle_model(t_t, c_t, rng=A.VXB_RNG_FAST)
+    run("toggle_fast", lambda: ctx.abc_prior_predictive(tmf, M.keying(1337), n_t, 0, n_t, tobs, rho=trho),
+        cell_steps, "cell-steps", 228, target_s=1.0, extra=lambda o: {"published_best_s": 69.0})
+
+    # ---- the paper's weak-informativity test: K = N = 400, N_p = 500 (PAPER.md:561)
+    for name, kw in (("weakinfo_exact", {}), ("weakinfo_fast", {"rng": A.VXB_RNG_FAST})):
+        wcfg = M.weakinfo_config(hyper_count=400, datasets=400, particles=500, seed=1337, **kw)
+        run(name, lambda wcfg=wcfg: ctx.weak_info_test(wcfg), 2 * 401 * 400, "sampler-runs",
+            target_s=1.0, extra=lambda o: {"weakly_informative": int(o["weakly"].sum()),
+                                           "published_best_s": 90.0})
+
+    # ---- TB Gillespie ABC at the reference's bench sizes (bench.hpp:39-42), 1e6 rows
+    n_tb = 1_000_000
+    tbm = M.tb_model(10, 10.0, 10000.0)
+    tb_obs = B.tb_observed_summaries(ctx, 10, 10.0, 10000.0, 1337, 4)
+    tb_rho = torch.empty(n_tb, dtype=torch.float64, device=f"cuda:{device}")
+    tb_failed = torch.empty(n_tb, dtype=torch.uint8, device=f"cuda:{device}")
+    run("tb_gillespie", lambda: ctx.abc_prior_predictive(tbm, M.keying(1337), n_tb, 0, n_tb, tb_obs,
+                                                        rho=tb_rho, failed=tb_failed),
+        n_tb, "rows", target_s=3.0)
+
+    # ---- smc::resample_multinomial at N = 1e5, d = 3 (reference: 17.8 ms, smc.cpp:268-300)
+    rs = np.random.RandomState(9)
+    n_r = 100_000
+    lw = torch.from_numpy(rs.normal(size=n_r) * 3).to(f"cuda:{device}")
+    parts = torch.from_numpy(rs.normal(size=(n_r, 3))).to(f"cuda:{device}")
+    r_out = torch.empty_like(parts)
+    r_anc = torch.empty(n_r, dtype=torch.int64, device=f"cuda:{device}")
+
+    def resample():
+        ctx._check(ctx.lib.vxb_resample_multinomial(
+            ctx.handle, lib.u64(n_r), lib.u32(3), lib._ptr(lw), lib._ptr(parts), lib.u64(77),
+            lib.u32(9), lib._ptr(r_out), lib._ptr(r_anc)))
+    run("resample_multinomial_1e5", resample, n_r, "particles", target_s=0.3,
+        extra=lambda o: {"reference_cpu_ms": 17.8,
+                         "note": "bit-exact: host-libm exp + strictly sequential running sum "
+                                 "(one dependent DADD per particle)"})
+    return res
 
 
 def cpu_baseline(args, obs, eps):

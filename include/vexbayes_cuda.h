@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define VXB_ABI_VERSION 1
+#define VXB_ABI_VERSION 2
 
 typedef struct vxb_ctx vxb_ctx;
 
@@ -304,12 +304,16 @@ int vxb_abcsmc_run(vxb_ctx* ctx, const vxb_model* model, const vxb_abcsmc_cfg* c
  *   flag (1 accepted, 0 rejected by distance, 2 outside the prior, 3 failed).
  * weights: for `count` new particles (theta_new: count x dim): the unnormalised
  *   importance weight 1 / sum_j w_j phi(theta_i; theta_j, Sigma), summed over
- *   j in index order. */
+ *   j in index order.  rng = the model's generator: VXB_RNG_REF is the bit-exact
+ *   kernel, VXB_RNG_FAST the throughput form (whitening + table 2^z) that
+ *   vxb_abcsmc_run uses for a VXB_RNG_FAST model -- a sharded run must pass the same
+ *   mode to stay identical to the one-GPU run.  count == 0 is allowed (empty shard).
+ *   With device-resident buffers the call does not synchronise. */
 int vxb_abcsmc_propose(vxb_ctx* ctx, const vxb_model* model, uint64_t seed, uint32_t gen,
                        uint64_t first, uint64_t count, uint64_t n_prev, const double* theta_prev,
                        const double* cum_prev, const double* chol, const double* observed,
                        double epsilon, double* theta_out, double* rho_out, uint8_t* flag_out);
-int vxb_abcsmc_weights(vxb_ctx* ctx, uint32_t dim, uint64_t count, const double* theta_new,
+int vxb_abcsmc_weights(vxb_ctx* ctx, int rng, uint32_t dim, uint64_t count, const double* theta_new,
                        uint64_t n_prev, const double* theta_prev,
                        const double* w_prev, const double* chol, double* w_out);
 
@@ -450,6 +454,103 @@ typedef struct vxb_mlmc_out {
 } vxb_mlmc_out;
 int vxb_mlmc_tauleap(vxb_ctx* ctx, const vxb_model* model, const vxb_mlmc_cfg* cfg,
                      vxb_mlmc_out* out);
+
+/* ------------------------------------------------------------ multi-GPU */
+/* The path shards by rows with no data-path collective: every variate is keyed by
+ * a global row number, so rank r of G simulating partition(n, G, 1)[r]
+ * (blocked.cpp:34-63) produces exactly the rows one GPU would.  What the reference
+ * does with `workers` std::threads (abc.cpp:43-71, smc.cpp:58-61,
+ * weak_info.cpp:258-270) the library does with one vxb_ctx per GPU.  NCCL is used
+ * INSIDE the library (loaded with dlopen("libnccl.so.2") on first use, so a
+ * single-GPU host needs no NCCL) and only for the exchange of results: the
+ * gather of accepted samples below.
+ *
+ * Two ways to drive several GPUs:
+ *  - one PROCESS per GPU (torchrun, MPI): each rank creates its vxb_ctx, rank 0
+ *    calls vxb_comm_unique_id and ships the 128 bytes to the others by its own
+ *    means, every rank calls vxb_comm_init_rank; the vxb_sharded_* entry points
+ *    are then called by all ranks (SPMD);
+ *  - one process, several GPUs (the C++ shim): vxb_multi_init creates a context
+ *    and a communicator per device; the vxb_multi_* entry points fork one host
+ *    thread per device and join, as the reference's drivers do. */
+typedef struct vxb_comm vxb_comm;
+typedef struct vxb_multi vxb_multi;
+#define VXB_COMM_ID_BYTES 128
+enum { VXB_DT_U8 = 0, VXB_DT_I64 = 1, VXB_DT_U64 = 2, VXB_DT_F64 = 3 };
+enum { VXB_OP_SUM = 0, VXB_OP_MAX = 1 };
+
+int vxb_device_count(int* count);
+/* NCCL version code (e.g. 22809) of the library that was loaded; fails with
+ * device-error when libnccl.so.2 cannot be loaded. */
+int vxb_comm_version(int* version);
+int vxb_comm_unique_id(void* id /* VXB_COMM_ID_BYTES */);
+/* Collective over the n_ranks callers; the communicator runs on ctx's stream. */
+int vxb_comm_init_rank(vxb_ctx* ctx, const void* id, int rank, int n_ranks, vxb_comm** comm);
+void vxb_comm_destroy(vxb_comm* comm);
+int vxb_comm_rank(const vxb_comm* comm);
+int vxb_comm_size(const vxb_comm* comm);
+/* Stream-ordered collectives on device buffers of the communicator's GPU
+ * (asynchronous: they are queued on the context's stream).  allgather: recv holds
+ * n_ranks blocks of `bytes` in rank order.  allreduce: in place. */
+int vxb_comm_allgather(vxb_comm* comm, const void* send, void* recv, size_t bytes);
+int vxb_comm_allreduce(vxb_comm* comm, void* buf, size_t count, int dtype, int op);
+
+/* One rank's accepted set of the fused fixed-epsilon path as ONE block of device
+ * memory, so that a single all-gather moves it: [count u64, padded to 16 B]
+ * [idx u64 x cap][theta real x cap x dim][rho real x cap], each field 16-byte
+ * aligned; `stride` = bytes of a block.  Rows [0, min(count, cap)) are valid. */
+typedef struct vxb_accept_layout {
+    uint64_t cap;
+    uint64_t off_count, off_idx, off_params, off_rho;
+    uint64_t stride;
+} vxb_accept_layout;
+int vxb_accept_layout_of(int precision, uint32_t dim, uint64_t cap, vxb_accept_layout* out);
+
+/* SPMD form of config 1 (every rank calls it): rank r simulates the rows
+ * partition(n_total, n_ranks, 1)[r] with vxb_abc_reject writing into
+ * `packed_local` (device, layout->stride bytes), then ONE all-gather places every
+ * rank's block into `packed_all` (device, n_ranks * stride bytes, rank order =
+ * ascending row order).  Fully asynchronous: nothing returns to the host and the
+ * stream is not synchronised.  comm == NULL: one rank, no gather (packed_all may
+ * be NULL). */
+int vxb_sharded_abc_reject(vxb_ctx* ctx, vxb_comm* comm, const vxb_model* model,
+                           const vxb_keying* key, uint64_t n_total, const double* observed,
+                           double epsilon, const vxb_accept_layout* layout, void* packed_local,
+                           void* packed_all);
+/* Host-side concatenation of gathered blocks (a HOST copy of packed_all) in rank
+ * order: at most cap_out rows are written; *n_accepted is the full count (a rank
+ * whose count exceeded layout->cap contributes only its first cap rows -- check
+ * *overflowed). */
+int vxb_accept_unpack(const vxb_accept_layout* layout, int precision, uint32_t dim, int n_ranks,
+                      const void* packed_all_host, uint64_t cap_out, uint64_t* n_accepted,
+                      uint64_t* idx, void* params, void* rho, int* overflowed);
+
+/* One process, several GPUs.  device_ids == NULL or n_dev == 0: every visible
+ * device.  With one device no communicator is created (NCCL is not loaded). */
+int vxb_multi_init(vxb_multi** multi, const int* device_ids, int n_dev);
+void vxb_multi_shutdown(vxb_multi* multi);
+int vxb_multi_size(const vxb_multi* multi);
+vxb_ctx* vxb_multi_ctx(vxb_multi* multi, int rank);
+vxb_comm* vxb_multi_comm(vxb_multi* multi, int rank); /* NULL with one device */
+/* abc::run_prior_predictive (abc.cpp:26-73) with the rows split over the devices
+ * by partition(n, G, 1): device g fills rows [begin_g, end_g) of the caller's HOST
+ * buffers (no collective; the keying -- VXB_KEY_WORKER included -- addresses rows
+ * globally, so the result does not depend on G). */
+int vxb_multi_abc_prior_predictive(vxb_multi* multi, const vxb_model* model, const vxb_keying* key,
+                                   uint64_t n, const double* observed, void* params,
+                                   void* summaries, void* rho, uint8_t* failed);
+/* Fused fixed-epsilon rejection over all devices + the NCCL gather of the
+ * accepted samples; host outputs as vxb_abc_reject (cap = total rows kept). */
+int vxb_multi_abc_reject(vxb_multi* multi, const vxb_model* model, const vxb_keying* key,
+                         uint64_t n_total, const double* observed, double epsilon, uint64_t cap,
+                         uint64_t* n_accepted, uint64_t* idx, void* params, void* rho);
+/* Configs 2 and 4 over all devices: disjoint dataset / path ranges, exact integer
+ * counters added on the host (no collective). */
+int vxb_multi_ppp_pvalues(vxb_multi* multi, const vxb_model* model, const double* lambda,
+                          const double* log_norm, uint32_t n_lambda, uint64_t m_total,
+                          uint64_t seed, double ybar_obs, uint64_t* counts, double* pvalues);
+int vxb_multi_mlmc_tauleap(vxb_multi* multi, const vxb_model* model, const vxb_mlmc_cfg* cfg,
+                           vxb_mlmc_out* out);
 
 #ifdef __cplusplus
 }

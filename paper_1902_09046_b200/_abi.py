@@ -6,7 +6,7 @@ C ABI takes.  Field order and types must match the header exactly.
 """
 import ctypes as C
 
-VXB_ABI_VERSION = 1
+VXB_ABI_VERSION = 2
 
 VXB_MODEL_LOGISTIC_SDE, VXB_MODEL_NORMAL_MEAN, VXB_MODEL_MM_TAULEAP, VXB_MODEL_TOGGLE = 1, 2, 3, 4
 VXB_MODEL_TB = 5
@@ -76,6 +76,16 @@ class vxb_mlmc_out(C.Structure):
                 ("estimate", C.c_double), ("std_error", C.c_double)]
 
 
+VXB_COMM_ID_BYTES = 128
+VXB_DT_U8, VXB_DT_I64, VXB_DT_U64, VXB_DT_F64 = 0, 1, 2, 3
+VXB_OP_SUM, VXB_OP_MAX = 0, 1
+
+
+class vxb_accept_layout(C.Structure):
+    _fields_ = [("cap", C.c_uint64), ("off_count", C.c_uint64), ("off_idx", C.c_uint64),
+                ("off_params", C.c_uint64), ("off_rho", C.c_uint64), ("stride", C.c_uint64)]
+
+
 # Every symbol include/vexbayes_cuda.h declares (tests check the .so exports all).
 EXPORTED_SYMBOLS = (
     "vxb_abi_version", "vxb_init", "vxb_shutdown", "vxb_last_error", "vxb_device_info",
@@ -90,4 +100,10 @@ EXPORTED_SYMBOLS = (
     "vxb_canon_chunk_sums", "vxb_quantile", "vxb_divide", "vxb_make_kernel", "vxb_bioassay_log_likelihood", "vxb_bioassay_sample", "vxb_smc_bioassay", "vxb_smc_bioassay_ensemble",
     "vxb_weak_info_test", "vxb_weak_info_lambdas", "vxb_weak_info_evidence",
     "vxb_weak_info_cutoffs", "vxb_mlmc_level", "vxb_mlmc_tauleap",
+    "vxb_device_count", "vxb_comm_version", "vxb_comm_unique_id", "vxb_comm_init_rank",
+    "vxb_comm_destroy", "vxb_comm_rank", "vxb_comm_size", "vxb_comm_allgather",
+    "vxb_comm_allreduce", "vxb_accept_layout_of", "vxb_sharded_abc_reject", "vxb_accept_unpack",
+    "vxb_multi_init", "vxb_multi_shutdown", "vxb_multi_size", "vxb_multi_ctx", "vxb_multi_comm",
+    "vxb_multi_abc_prior_predictive", "vxb_multi_abc_reject", "vxb_multi_ppp_pvalues",
+    "vxb_multi_mlmc_tauleap",
 )

@@ -2,14 +2,20 @@
 // interface (abc.hpp:16-58): same names, argument meaning and error behaviour,
 // executed by libvexbayes_cuda.so.
 //
-//   run_prior_predictive   -> vxb_abc_prior_predictive with VXB_KEY_WORKER, so
+//   run_prior_predictive   -> vxb_multi_abc_prior_predictive with VXB_KEY_WORKER, so
 //       the result is bit-identical to the reference for the same
-//       (seed, workers, block_width)  (abc.cpp:26-73);
+//       (seed, workers, block_width)  (abc.cpp:26-73).  `workers` keeps its
+//       meaning for the STREAM LAYOUT (worker w owns stream (seed, w)); the rows
+//       themselves are split over the GPUs in use (cuda::set_devices, default:
+//       every visible device) by partition(n, G, 1) -- a device where the
+//       reference has a worker thread (abc.cpp:43-71);
 //   select_epsilon         -> vxb_select_epsilon           (abc.cpp:75-97);
 //   discrepancy            -> host arithmetic, left-to-right (abc.cpp:16-24);
 //   write_csv              -> same column layout, %.17g      (abc.cpp:99-124).
 // Extension for jobs that do not fit the fixed-N container (config 1):
-//   reject_fixed_epsilon   -> vxb_abc_reject (only accepted rows leave the GPU).
+//   reject_fixed_epsilon   -> vxb_abc_reject (only accepted rows leave the GPU);
+//   reject_fixed_epsilon (whole job) -> vxb_multi_abc_reject: rows sharded over the
+//       GPUs in use, accepted samples gathered over NCCL inside the library.
 #pragma once
 
 #include <cmath>
@@ -95,9 +101,9 @@ inline PriorPredictiveSet run_prior_predictive(const ModelHooks& model, std::siz
                 "invalid-shape", "unsupported block width");
         key = vxb_keying{VXB_KEY_PARTICLE, 1, 1, 0, seed};
     }
-    cuda::check(vxb_abc_prior_predictive(cuda::context(), &dm, &key, n, 0, n, observed.data(),
-                                         set.params.data(), set.summaries.data(),
-                                         set.discrepancies.data(), set.failed.data(), nullptr));
+    cuda::check(vxb_multi_abc_prior_predictive(cuda::multi(), &dm, &key, n, observed.data(),
+                                               set.params.data(), set.summaries.data(),
+                                               set.discrepancies.data(), set.failed.data()));
     return set;
 }
 
@@ -139,6 +145,31 @@ inline AcceptedSet reject_fixed_epsilon(const ModelHooks& model, std::uint64_t n
     cuda::check(vxb_abc_reject(cuda::context(), &dm, &key, n_total, first, count, observed.data(),
                                epsilon, cap, &out.total_accepted, out.rows.data(),
                                out.params.data(), out.discrepancies.data()));
+    const std::uint64_t kept = out.total_accepted < cap ? out.total_accepted : cap;
+    out.rows.resize(kept);
+    out.params.resize(kept * model.dim);
+    out.discrepancies.resize(kept);
+    return out;
+}
+
+// The whole n_total-row job over every GPU in use (config 1): device g simulates
+// partition(n_total, G, 1)[g]; the accepted samples are gathered over NCCL inside
+// the library; identical to the one-GPU result for any G.  `cap` = rows kept.
+inline AcceptedSet reject_fixed_epsilon(const ModelHooks& model, std::uint64_t n_total,
+                                        std::uint64_t seed, std::span<const double> observed,
+                                        double epsilon, std::uint64_t cap) {
+    require(observed.size() == model.summary_dim, "invalid-summary",
+            "observed summary length differs from the model summary dimension");
+    const DeviceModel& dm = device_model(model);
+    require(dm.precision == VXB_F64, "invalid-argument", "this container is fp64");
+    AcceptedSet out;
+    out.rows.resize(cap);
+    out.params.resize(cap * model.dim);
+    out.discrepancies.resize(cap);
+    vxb_keying key{VXB_KEY_PARTICLE, 1, 1, 0, seed};
+    cuda::check(vxb_multi_abc_reject(cuda::multi(), &dm, &key, n_total, observed.data(), epsilon,
+                                     cap, &out.total_accepted, out.rows.data(), out.params.data(),
+                                     out.discrepancies.data()));
     const std::uint64_t kept = out.total_accepted < cap ? out.total_accepted : cap;
     out.rows.resize(kept);
     out.params.resize(kept * model.dim);

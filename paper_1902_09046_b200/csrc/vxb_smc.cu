@@ -774,24 +774,33 @@ extern "C" int vxb_abcsmc_propose(vxb_ctx* ctx, const vxb_model* model, uint64_t
     });
 }
 
-extern "C" int vxb_abcsmc_weights(vxb_ctx* ctx, uint32_t dim, uint64_t count,
+extern "C" int vxb_abcsmc_weights(vxb_ctx* ctx, int rng, uint32_t dim, uint64_t count,
                                   const double* theta_new, uint64_t n_prev,
                                   const double* theta_prev, const double* w_prev,
                                   const double* chol, double* w_out) {
     return guarded([&] {
         use(ctx);
+        require(rng == VXB_RNG_REF || rng == VXB_RNG_FAST, "invalid-argument", "bad rng mode");
+        require(dim >= 1 && dim <= 4, "invalid-shape", "dimension out of range (1..4)");
+        if (count == 0) return;  // an empty shard (more ranks than chunks) is not an error
         require(theta_new && theta_prev && w_prev && chol && w_out, "invalid-argument",
                 "null argument");
-        require(dim >= 1 && dim <= 4, "invalid-shape", "dimension out of range (1..4)");
         Staged d_tn(ctx, theta_new, count * dim * 8, true, false);
         Staged d_tp(ctx, theta_prev, n_prev * dim * 8, true, false);
         Staged d_wp(ctx, w_prev, n_prev * 8, true, false);
         Staged d_ch(ctx, chol, dim * dim * 8, true, false);
         Staged d_out(ctx, w_out, count * 8, false, true);
-        weights_device(ctx, dim, count, d_tn.as<double>(), n_prev, d_tp.as<double>(),
-                       d_wp.as<double>(), d_ch.as<double>(), d_out.as<double>());
+        if (rng == VXB_RNG_FAST)  // the form vxb_abcsmc_run uses for a VXB_RNG_FAST model
+            weights_fast_device(ctx, dim, count, d_tn.as<double>(), n_prev, d_tp.as<double>(),
+                                d_wp.as<double>(), d_ch.as<double>(), d_out.as<double>());
+        else
+            weights_device(ctx, dim, count, d_tn.as<double>(), n_prev, d_tp.as<double>(),
+                           d_wp.as<double>(), d_ch.as<double>(), d_out.as<double>());
         d_out.finish();
-        VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+        // device-resident output: stay asynchronous (the multi-GPU host queues the
+        // collectives behind it on the same stream)
+        if (d_out.staged() || d_tn.staged() || d_tp.staged() || d_wp.staged() || d_ch.staged())
+            VXB_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }
 

@@ -54,22 +54,32 @@ def gather_accepted(idx, params, rho, group=None):
     return outs[0], outs[1], outs[2], counts
 
 
-def gather_accepted_padded(idx, params, rho, n_dev, group=None):
-    """Asynchronous form: fixed-capacity buffers (rows [0, n_dev) valid) and the
-    device-resident count are all-gathered as they are -- no host round trip, so
-    steps queue back to back on every rank.  Returns tensors shaped
-    [world, cap, ...] plus the [world] count tensor; ``compact_gathered`` turns
-    them into the ascending concatenation once the host needs it."""
+def packed_views(buf, layout, precision, dim, blocks=1):
+    """Typed views of `blocks` consecutive packed accepted sets (vxb_accept_layout) held
+    in the uint8 tensor `buf`: idx [blocks, cap] int64, params [blocks, cap, dim],
+    rho [blocks, cap], count [blocks] int64.  No copy."""
+    import torch
+    from . import _abi as A
+    real, rb = (torch.float32, 4) if precision == A.VXB_F32 else (torch.float64, 8)
+    cap, stride = int(layout.cap), int(layout.stride)
+    as64, asr = buf.view(torch.int64), buf.view(real)
+    idx = torch.as_strided(as64, (blocks, cap), (stride // 8, 1), int(layout.off_idx) // 8)
+    count = torch.as_strided(as64, (blocks,), (stride // 8,), int(layout.off_count) // 8)
+    params = torch.as_strided(asr, (blocks, cap, dim), (stride // rb, dim, 1), int(layout.off_params) // rb)
+    rho = torch.as_strided(asr, (blocks, cap), (stride // rb, 1), int(layout.off_rho) // rb)
+    return idx, params, rho, count
+
+
+def gather_packed(packed_local, world, out=None, group=None):
+    """THE exchange of config 1: one all_gather_into_tensor of the fixed-capacity
+    (count | idx | theta | rho) block of every rank -- no host round trip, so steps
+    queue back to back on every rank.  Works on NCCL (CUDA) and gloo (CPU) alike."""
     import torch
     import torch.distributed as dist
-    world = dist.get_world_size(group)
-    outs = []
-    for t in (idx, params, rho, n_dev):
-        buf = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
-        # per-rank views of one buffer: works on gloo (tests) and NCCL alike
-        dist.all_gather([buf[r] for r in range(world)], t.contiguous(), group=group)
-        outs.append(buf)
-    return outs[0], outs[1], outs[2], outs[3].reshape(world)
+    if out is None:
+        out = torch.empty(world * packed_local.numel(), dtype=torch.uint8, device=packed_local.device)
+    dist.all_gather_into_tensor(out, packed_local, group=group)
+    return out
 
 
 def compact_gathered(idx, params, rho, counts):
@@ -89,50 +99,69 @@ def allreduce_sum(t, group=None):
     return t
 
 
+class RejectBuffers:
+    """Output buffers of sharded_reject for this rank: its packed accepted set and
+    (several ranks) the gathered blocks of all ranks, allocated on the library's
+    stream so that the caching allocator's reuse is ordered with the kernels that
+    fill them.  Reusable across steps."""
+
+    def __init__(self, ctx, model, n_total, cap_fraction=0.01, group=None, world=None, rank=None):
+        import torch
+        from . import lib
+        if world is None:
+            rank, world = _world(group)
+        self.world, self.rank = world, rank
+        begin, end = shard_range(n_total, world, rank)
+        # every rank uses the capacity of the largest shard: equal block sizes
+        largest = shard_range(n_total, world, 0)
+        cap = max(1024, int((largest[1] - largest[0]) * cap_fraction))
+        self.layout = lib.accept_layout(model.precision, model.dim, cap)
+        self.precision, self.dim = model.precision, model.dim
+        dev = torch.device("cuda", ctx.device_info()["device"])
+        with torch.cuda.stream(torch.cuda.ExternalStream(ctx.stream(), device=dev)):
+            self.local = torch.empty(int(self.layout.stride), dtype=torch.uint8, device=dev)
+            self.all = (torch.empty(world * int(self.layout.stride), dtype=torch.uint8, device=dev)
+                        if world > 1 else None)
+
+    def local_views(self):
+        idx, params, rho, count = packed_views(self.local, self.layout, self.precision, self.dim)
+        return idx[0], params[0], rho[0], count
+
+    def gathered_views(self):
+        return packed_views(self.all, self.layout, self.precision, self.dim, self.world)
+
+
 def reject_buffers(ctx, model, n_total, cap_fraction=0.01, group=None):
-    """Output buffers of sharded_reject for this rank's shard (idx, theta, rho of the
-    accepted rows at a fixed capacity, and the device-resident count), allocated on
-    the library's stream so that the caching allocator's reuse is ordered with the
-    kernels that fill them.  Reusable across steps."""
-    import torch
-    from . import _abi as A
-    rank, world = _world(group)
-    begin, end = shard_range(n_total, world, rank)
-    cap = max(1024, int((end - begin) * cap_fraction))
-    dev = torch.device("cuda", ctx.device_info()["device"])
-    real = torch.float32 if model.precision == A.VXB_F32 else torch.float64
-    with torch.cuda.stream(torch.cuda.ExternalStream(ctx.stream(), device=dev)):
-        return (torch.empty(cap, dtype=torch.int64, device=dev),
-                torch.empty((cap, model.dim), dtype=real, device=dev),
-                torch.empty(cap, dtype=real, device=dev),
-                torch.empty(1, dtype=torch.int64, device=dev))
+    return RejectBuffers(ctx, model, n_total, cap_fraction, group)
 
 
 def sharded_reject(ctx, model, key, n_total, observed, eps, cap_fraction=0.01, group=None,
-                   buffers=None):
+                   buffers=None, comm=None):
     """Config 1 on this rank's shard + the gather of accepted samples.
 
-    Device-resident: outputs are torch CUDA tensors filled by the fused kernel
-    path; only the accepted rows travel.  `buffers` (reject_buffers) lets a caller
-    that steps repeatedly reuse the output tensors."""
+    Device-resident and fully asynchronous: the fused kernel path writes the accepted
+    rows (and their count) into this rank's packed block; with several ranks ONE
+    collective gathers the blocks over NVLink -- torch.distributed's NCCL
+    (all_gather_into_tensor) or, with ``comm`` (lib.Comm), the library's own
+    communicator through vxb_sharded_abc_reject.  Returns views (idx, theta, rho,
+    count): of this rank's block for one rank, of all blocks ([world, ...]) otherwise.
+    `buffers` (reject_buffers) lets a caller that steps repeatedly reuse the memory."""
     import torch
-    rank, world = _world(group)
+    rank, world = (comm.rank, comm.size) if comm is not None else _world(group)
+    b = buffers if buffers is not None else RejectBuffers(ctx, model, n_total, cap_fraction, group,
+                                                          world, rank)
+    if comm is not None:
+        ctx.sharded_abc_reject(comm, model, key, n_total, observed, eps, b.layout, b.local, b.all)
+        return b.local_views() if world == 1 else b.gathered_views()
     begin, end = shard_range(n_total, world, rank)
-    count = end - begin
-    idx, params, rho, n_dev = buffers if buffers is not None else \
-        reject_buffers(ctx, model, n_total, cap_fraction, group)
-    cap = int(idx.shape[0])
-    # fully asynchronous: the accepted count stays on the device, the host only
-    # enqueues (rows [0, count) of the buffers are valid once the stream drains)
-    ctx.abc_reject(model, key, n_total, begin, count, observed, eps, cap, idx=idx,
-                   params=params, rho=rho, n_accepted=n_dev)
+    idx, params, rho, n_dev = b.local_views()
+    ctx.abc_reject(model, key, n_total, begin, end - begin, observed, eps, int(b.layout.cap),
+                   idx=idx, params=params, rho=rho, n_accepted=n_dev)
     if world == 1:
         return idx, params, rho, n_dev
-    # the gather of accepted samples over NVLink, on the library's stream, padded to
-    # the fixed capacity so that no rank has to read a count back first
-    dev = idx.device
-    with torch.cuda.stream(torch.cuda.ExternalStream(ctx.stream(), device=dev)):
-        return gather_accepted_padded(idx, params, rho, n_dev, group)
+    with torch.cuda.stream(torch.cuda.ExternalStream(ctx.stream(), device=b.local.device)):
+        gather_packed(b.local, world, out=b.all, group=group)
+    return b.gathered_views()
 
 
 # --------------------------------------------------------------------------
@@ -199,6 +228,8 @@ class DeviceStages:
         import torch
         from . import _abi as A
         count = int(rho.shape[0])
+        if count == 0:  # empty shard (more ranks than rows in the round)
+            return theta, rho
         idx = torch.empty(max(count, 1), dtype=torch.int64, device=self.device)
         _, k = self.ctx.compact_accepted(rho, failed, eps, 0, count, A.VXB_F64, count, idx)
         keep = idx[:k]
@@ -208,6 +239,8 @@ class DeviceStages:
         import torch
         from . import models as M
         theta, rho = self._rows(count, model.dim)
+        if count == 0:
+            return theta, rho
         failed = torch.empty(count, dtype=torch.uint8, device=self.device)
         self.ctx.abc_prior_predictive(model, M.keying(seed0), n_total, first, count, observed,
                                       params=theta, rho=rho, failed=failed)
@@ -218,6 +251,8 @@ class DeviceStages:
         import torch
         from .lib import _ptr, u32, u64, f64
         theta, rho = self._rows(count, model.dim)
+        if count == 0:
+            return theta, rho
         flag = torch.empty(count, dtype=torch.uint8, device=self.device)
         ch = np.ascontiguousarray(chol, dtype=np.float64)
         obs = np.ascontiguousarray(observed, dtype=np.float64)
@@ -228,13 +263,17 @@ class DeviceStages:
                                           f64(eps), _ptr(theta), _ptr(rho), _ptr(flag)))
         return self._compacted(theta, rho, None, eps)
 
-    def weights(self, theta_new, theta_prev, w_prev, chol):
+    def weights(self, theta_new, theta_prev, w_prev, chol, rng=0):
+        """rng: the model's generator -- VXB_RNG_FAST selects the throughput form of the
+        weights that the one-GPU driver uses for such a model."""
         import torch
-        from .lib import _ptr, u32, u64
+        from .lib import _ptr, i32, u32, u64
         out = torch.empty(int(theta_new.shape[0]), dtype=torch.float64, device=self.device)
+        if out.numel() == 0:
+            return out
         ch = np.ascontiguousarray(chol, dtype=np.float64)
         c = self.ctx
-        c._check(c.lib.vxb_abcsmc_weights(c.handle, u32(int(theta_new.shape[1])),
+        c._check(c.lib.vxb_abcsmc_weights(c.handle, i32(rng), u32(int(theta_new.shape[1])),
                                           u64(int(theta_new.shape[0])), _ptr(theta_new),
                                           u64(int(theta_prev.shape[0])), _ptr(theta_prev),
                                           _ptr(w_prev), _ptr(ch), _ptr(out)))
@@ -335,7 +374,7 @@ def sharded_abcsmc(stages, model, cfg, observed, group=None):
             if g == 0:
                 w_new = torch.full((n,), 1.0 / n, dtype=torch.float64, device=theta_new.device)
             else:
-                w_local = stages.weights(theta_new[w_begin:w_end], theta, w, chol)
+                w_local = stages.weights(theta_new[w_begin:w_end], theta, w, chol, rng=int(model.rng))
                 (w_raw,), _ = allgather_rows([w_local], group)
                 totals = torch.zeros(n_chunks, dtype=torch.float64, device=w_raw.device)
                 if w_end > w_begin:

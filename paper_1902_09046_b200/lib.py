@@ -44,6 +44,17 @@ def load():
         _lib.vxb_splitmix64.argtypes = [u64]
         _lib.vxb_derive_seed.restype = u64
         _lib.vxb_derive_seed.argtypes = [u64, P, C.c_size_t]
+        _lib.vxb_multi_ctx.restype = P
+        _lib.vxb_multi_ctx.argtypes = [P, C.c_int]
+        _lib.vxb_multi_comm.restype = P
+        _lib.vxb_multi_comm.argtypes = [P, C.c_int]
+        _lib.vxb_multi_size.argtypes = [P]
+        _lib.vxb_multi_shutdown.argtypes = [P]
+        _lib.vxb_multi_shutdown.restype = None
+        _lib.vxb_comm_destroy.argtypes = [P]
+        _lib.vxb_comm_destroy.restype = None
+        _lib.vxb_comm_rank.argtypes = [P]
+        _lib.vxb_comm_size.argtypes = [P]
     return _lib
 
 
@@ -96,6 +107,166 @@ def partition(total, workers, block_width):
     if rc:
         raise VxbError(load().vxb_last_error().decode())
     return r
+
+
+def _raise_last():
+    raise VxbError(load().vxb_last_error().decode())
+
+
+def device_count():
+    n = C.c_int()
+    if load().vxb_device_count(C.byref(n)):
+        _raise_last()
+    return n.value
+
+
+def accept_layout(precision, dim, cap):
+    """Layout of one rank's packed accepted set (vxb_accept_layout_of)."""
+    lay = A.vxb_accept_layout()
+    if load().vxb_accept_layout_of(i32(precision), u32(dim), u64(cap), C.byref(lay)):
+        _raise_last()
+    return lay
+
+
+def accept_unpack(layout, precision, dim, n_ranks, packed_all_host, cap_out=None):
+    """Concatenate gathered blocks (a host uint8 array) in rank order.
+    Returns (n_accepted, idx, params, rho, overflowed)."""
+    buf = np.ascontiguousarray(packed_all_host, dtype=np.uint8)
+    assert buf.size >= n_ranks * layout.stride
+    cap_out = n_ranks * layout.cap if cap_out is None else cap_out
+    dt = np.float32 if precision == A.VXB_F32 else np.float64
+    idx = np.zeros(cap_out, dtype=np.uint64)
+    params, rho = np.zeros((cap_out, dim), dtype=dt), np.zeros(cap_out, dtype=dt)
+    n_acc, over = u64(), C.c_int()
+    if load().vxb_accept_unpack(C.byref(layout), i32(precision), u32(dim), C.c_int(n_ranks),
+                                _ptr(buf), u64(cap_out), C.byref(n_acc), _ptr(idx), _ptr(params),
+                                _ptr(rho), C.byref(over)):
+        _raise_last()
+    k = min(n_acc.value, cap_out)
+    return n_acc.value, idx[:k], params[:k], rho[:k], bool(over.value)
+
+
+def comm_unique_id():
+    """128-byte NCCL unique id (rank 0 creates it and ships it to the other ranks)."""
+    buf = np.zeros(A.VXB_COMM_ID_BYTES, dtype=np.uint8)
+    if load().vxb_comm_unique_id(_ptr(buf)):
+        _raise_last()
+    return buf
+
+
+def comm_version():
+    v = C.c_int()
+    if load().vxb_comm_version(C.byref(v)):
+        _raise_last()
+    return v.value
+
+
+class Comm:
+    """The library's own NCCL communicator of one rank (vxb_comm); collectives are
+    queued on the context's stream."""
+
+    def __init__(self, ctx, unique_id, rank, n_ranks, handle=None):
+        self.ctx, self.lib = ctx, load()
+        self.owned = handle is None
+        self.handle = P(handle) if handle is not None else P()
+        if self.owned:
+            uid = np.ascontiguousarray(unique_id, dtype=np.uint8)
+            ctx._check(self.lib.vxb_comm_init_rank(ctx.handle, _ptr(uid), C.c_int(rank),
+                                                   C.c_int(n_ranks), C.byref(self.handle)))
+
+    @property
+    def rank(self):
+        return int(self.lib.vxb_comm_rank(self.handle))
+
+    @property
+    def size(self):
+        return int(self.lib.vxb_comm_size(self.handle))
+
+    def allgather(self, send, recv, nbytes):
+        self.ctx._check(self.lib.vxb_comm_allgather(self.handle, _ptr(send), _ptr(recv),
+                                                    C.c_size_t(nbytes)))
+
+    def allreduce(self, buf, count, dtype=A.VXB_DT_F64, op=A.VXB_OP_SUM):
+        self.ctx._check(self.lib.vxb_comm_allreduce(self.handle, _ptr(buf), C.c_size_t(count),
+                                                    i32(dtype), i32(op)))
+
+    def close(self):
+        if self.owned and self.handle:
+            self.lib.vxb_comm_destroy(self.handle)
+        self.handle = P()
+
+
+class Multi:
+    """One process, several GPUs (vxb_multi): a context (and an NCCL communicator)
+    per device; the calls fork one host thread per device and join."""
+
+    def __init__(self, device_ids=None):
+        self.lib = load()
+        self.handle = P()
+        ids = None if device_ids is None else np.ascontiguousarray(device_ids, dtype=np.int32)
+        if self.lib.vxb_multi_init(C.byref(self.handle), _ptr(ids), C.c_int(0 if ids is None else ids.size)):
+            _raise_last()
+
+    def _check(self, rc):
+        if rc:
+            _raise_last()
+
+    @property
+    def size(self):
+        return int(self.lib.vxb_multi_size(self.handle))
+
+    def close(self):
+        if self.handle:
+            self.lib.vxb_multi_shutdown(self.handle)
+            self.handle = P()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def abc_prior_predictive(self, model, key, n, observed, want_summaries=True):
+        dt = np.float32 if model.precision == A.VXB_F32 else np.float64
+        obs = np.ascontiguousarray(observed, dtype=np.float64)
+        params = np.zeros((n, model.dim), dtype=dt)
+        summ = np.zeros((n, model.summary_dim), dtype=dt) if want_summaries else None
+        rho, failed = np.zeros(n, dtype=dt), np.zeros(n, dtype=np.uint8)
+        self._check(self.lib.vxb_multi_abc_prior_predictive(
+            self.handle, C.byref(model), C.byref(key), u64(n), _ptr(obs), _ptr(params), _ptr(summ),
+            _ptr(rho), _ptr(failed)))
+        return params, summ, rho, failed
+
+    def abc_reject(self, model, key, n_total, observed, eps, cap):
+        dt = np.float32 if model.precision == A.VXB_F32 else np.float64
+        obs = np.ascontiguousarray(observed, dtype=np.float64)
+        idx = np.zeros(cap, dtype=np.uint64)
+        params, rho = np.zeros((cap, model.dim), dtype=dt), np.zeros(cap, dtype=dt)
+        nacc = u64()
+        self._check(self.lib.vxb_multi_abc_reject(self.handle, C.byref(model), C.byref(key),
+                                                  u64(n_total), _ptr(obs), f64(eps), u64(cap),
+                                                  C.byref(nacc), _ptr(idx), _ptr(params), _ptr(rho)))
+        k = min(nacc.value, cap)
+        return nacc.value, idx[:k], params[:k], rho[:k]
+
+    def ppp_pvalues(self, model, lam, log_norm, m_total, seed, ybar_obs):
+        lam = np.ascontiguousarray(lam, dtype=np.float64)
+        ln = np.ascontiguousarray(log_norm, dtype=np.float64)
+        counts, pv = np.zeros(lam.size, dtype=np.uint64), np.zeros(lam.size)
+        self._check(self.lib.vxb_multi_ppp_pvalues(self.handle, C.byref(model), _ptr(lam), _ptr(ln),
+                                                   u32(lam.size), u64(m_total), u64(seed),
+                                                   f64(ybar_obs), _ptr(counts), _ptr(pv)))
+        return counts, pv
+
+    def mlmc_tauleap(self, model, cfg):
+        L = cfg.levels
+        res = dict(level_mean=np.zeros(L), level_var=np.zeros(L), level_cost=np.zeros(L))
+        out = A.vxb_mlmc_out(res["level_mean"].ctypes.data, res["level_var"].ctypes.data,
+                             res["level_cost"].ctypes.data, 0.0, 0.0)
+        self._check(self.lib.vxb_multi_mlmc_tauleap(self.handle, C.byref(model), C.byref(cfg),
+                                                    C.byref(out)))
+        res["estimate"], res["std_error"] = out.estimate, out.std_error
+        return res
 
 
 class Context:
@@ -301,6 +472,15 @@ class Context:
             return nacc.value, idx[:k], params[:k], rho[:k]
         return nacc.value, idx, params, rho
 
+    def sharded_abc_reject(self, comm, model, key, n_total, observed, eps, layout, packed_local,
+                           packed_all=None):
+        """SPMD config 1: this rank's shard into `packed_local`, one NCCL all-gather into
+        `packed_all` (device uint8 buffers; comm None = one rank).  Asynchronous."""
+        obs = np.ascontiguousarray(observed, dtype=np.float64)
+        self._check(self.lib.vxb_sharded_abc_reject(
+            self.handle, comm.handle if comm is not None else None, C.byref(model), C.byref(key),
+            u64(n_total), _ptr(obs), f64(eps), C.byref(layout), _ptr(packed_local), _ptr(packed_all)))
+
     # ---- p-values
     def ppp_pvalues(self, model, lam, log_norm, m_total, first, count, seed, ybar_obs,
                     want_ybar=False):
@@ -354,13 +534,13 @@ class Context:
                                                 _ptr(rho), _ptr(flag)))
         return th, rho, flag
 
-    def abcsmc_weights(self, theta_new, theta_prev, w_prev, chol):
+    def abcsmc_weights(self, theta_new, theta_prev, w_prev, chol, rng=A.VXB_RNG_REF):
         tn = np.ascontiguousarray(theta_new, dtype=np.float64)
         tp = np.ascontiguousarray(theta_prev, dtype=np.float64)
         wp = np.ascontiguousarray(w_prev, dtype=np.float64)
         ch = np.ascontiguousarray(chol, dtype=np.float64)
         out = np.zeros(tn.shape[0])
-        self._check(self.lib.vxb_abcsmc_weights(self.handle, u32(tn.shape[1]), u64(tn.shape[0]),
+        self._check(self.lib.vxb_abcsmc_weights(self.handle, i32(rng), u32(tn.shape[1]), u64(tn.shape[0]),
                                                 _ptr(tn), u64(tp.shape[0]), _ptr(tp), _ptr(wp),
                                                 _ptr(ch), _ptr(out)))
         return out

@@ -37,12 +37,14 @@ def test_header_and_python_mirror_agree():
     assert ctypes.sizeof(A.vxb_mlmc_cfg) == 40
     assert ctypes.sizeof(A.vxb_profile) == 16 * A.VXB_K_COUNT
     assert ctypes.sizeof(A.vxb_weakinfo_cfg) == 5 * 8 + 5 * 8 + 2 * 4 + 16 * 4 + 16 * 8 + 2 * 4
+    assert ctypes.sizeof(A.vxb_accept_layout) == 48
 
 
 def test_struct_sizes_match_the_c_compiler(tmp_path):
     """The ctypes mirrors against sizeof() as gcc sees the header (plain C)."""
     import subprocess
-    names = ["vxb_model", "vxb_keying", "vxb_abcsmc_cfg", "vxb_mlmc_cfg", "vxb_weakinfo_cfg", "vxb_profile"]
+    names = ["vxb_model", "vxb_keying", "vxb_abcsmc_cfg", "vxb_mlmc_cfg", "vxb_weakinfo_cfg", "vxb_profile",
+             "vxb_accept_layout"]
     src = tmp_path / "sizes.c"
     src.write_text('#include <stdio.h>\n#include "vexbayes_cuda.h"\nint main(void) {\n' +
                    "".join(f'    printf("{n} %zu\\n", sizeof({n}));\n' for n in names) + "    return 0;\n}\n")
@@ -88,10 +90,18 @@ def test_cpp_shim_compiles_and_links(so, tmp_path):
     import subprocess
     pkg = os.path.join(ROOT, "paper_1902_09046_b200")
     exe = tmp_path / "test_shim"
-    subprocess.run(["g++", "-std=c++20", "-O1", "-Wall", "-Wextra", "-I", os.path.join(pkg, "cpp"),
-                    os.path.join(ROOT, "tests", "cpp", "test_shim.cpp"), "-o", str(exe),
-                    "-L", pkg, "-lvexbayes_cuda", f"-Wl,-rpath,{pkg}"], check=True)
-    assert exe.exists()
+    for name in ("test_shim", "test_multi"):
+        exe = tmp_path / name
+        subprocess.run(["g++", "-std=c++20", "-O1", "-Wall", "-Wextra", "-pthread",
+                        "-I", os.path.join(pkg, "cpp"),
+                        os.path.join(ROOT, "tests", "cpp", name + ".cpp"), "-o", str(exe),
+                        "-L", pkg, "-lvexbayes_cuda", f"-Wl,-rpath,{pkg}"], check=True)
+        assert exe.exists()
+    # without a GPU the multi-GPU program stops at its first check, loudly
+    import torch
+    if not torch.cuda.is_available():
+        run = subprocess.run([str(tmp_path / "test_multi")], capture_output=True, text=True)
+        assert run.returncode != 0 and "devices 0" in run.stdout
 
 
 def test_product_package_never_imports_the_oracle():

@@ -42,14 +42,23 @@ def _worker(rank, world, port, n_total, eps, obs, out_dir):
     g_idx, g_p, g_rho, counts = D.gather_accepted(idx, torch.from_numpy(p[keep]),
                                                   torch.from_numpy(rho[keep]))
     total = D.allreduce_sum(torch.tensor([int(keep.sum())], dtype=torch.int64))
-    # asynchronous form: fixed-capacity buffers + device-resident count
+    # asynchronous form: this rank's fixed-capacity packed block (count | idx | theta |
+    # rho, include/vexbayes_cuda.h vxb_accept_layout) and ONE all_gather_into_tensor
+    from paper_1902_09046_b200 import _abi as A, lib
     cap, k = 400, int(keep.sum())
-    b_idx = torch.full((cap,), -1, dtype=torch.int64)
-    b_p = torch.zeros((cap, 3), dtype=torch.float64)
-    b_rho = torch.zeros(cap, dtype=torch.float64)
-    b_idx[:k], b_p[:k], b_rho[:k] = idx, torch.from_numpy(p[keep]), torch.from_numpy(rho[keep])
-    pi, pp, pr, pc = D.gather_accepted_padded(b_idx, b_p, b_rho, torch.tensor([k], dtype=torch.int64))
+    lay = lib.accept_layout(A.VXB_F64, 3, cap)
+    block = torch.zeros(int(lay.stride), dtype=torch.uint8)
+    b_idx, b_p, b_rho, b_n = D.packed_views(block, lay, A.VXB_F64, 3)
+    b_idx[0].fill_(-1)
+    b_idx[0, :k], b_p[0, :k], b_rho[0, :k], b_n[0] = idx, torch.from_numpy(p[keep]), torch.from_numpy(rho[keep]), k
+    gathered = D.gather_packed(block, world)
+    pi, pp, pr, pc = D.packed_views(gathered, lay, A.VXB_F64, 3, world)
     ci, cp, cr, cc = D.compact_gathered(pi, pp, pr, pc)
+    # the C-ABI's host-side unpacking of the same gathered bytes agrees
+    n_acc, u_idx, u_p, u_rho, over = lib.accept_unpack(lay, A.VXB_F64, 3, world, gathered.numpy())
+    assert n_acc == sum(cc) and not over
+    assert np.array_equal(u_idx.astype(np.int64), ci.numpy()) and np.array_equal(u_p, cp.numpy())
+    assert np.array_equal(u_rho, cr.numpy())
     assert torch.equal(ci, g_idx) and torch.equal(cp, g_p) and torch.equal(cr, g_rho) and cc == counts
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), idx=g_idx.numpy(), p=g_p.numpy(),
              rho=g_rho.numpy(), counts=np.array(counts), total=total.numpy())
@@ -154,7 +163,7 @@ class OracleStages:
                                               cum_prev.numpy(), chol, observed, eps)
         return self._keep(th, rho, flag == 1)
 
-    def weights(self, theta_new, theta_prev, w_prev, chol):
+    def weights(self, theta_new, theta_prev, w_prev, chol, rng=0):
         return torch.from_numpy(self.o.abcsmc_weights(theta_new.numpy(), theta_prev.numpy(),
                                                       w_prev.numpy(), chol))
 

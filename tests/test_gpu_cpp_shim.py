@@ -120,3 +120,36 @@ def test_cpp_shim_reference_format_outputs(tmp_path, golden, oracle):
     sweep = B.parse_csv(read(tmp_path / "sweep.csv"))
     assert [(x.block_width, x.threads, x.replicate) for x in sweep] == \
         [(v, p, k) for v in (1, 4) for p in (1, 3) for k in (0, 1)]
+
+
+def test_cpp_multi_gpu_drivers(tmp_path, oracle):
+    """tests/cpp/test_multi.cpp: the shim's drivers over every visible GPU (vxb_multi_*),
+    the library's own NCCL communicator (a real 1-rank communicator on one GPU; the SPMD
+    per-device form on two or more), the packed accepted-set exchange.  The C++ side
+    checks G devices == 1 device itself; here its output is compared with the oracle."""
+    exe = tmp_path / "test_multi"
+    pkg = os.path.join(ROOT, "paper_1902_09046_b200")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-pthread", "-I", os.path.join(pkg, "cpp"),
+                    os.path.join(ROOT, "tests", "cpp", "test_multi.cpp"), "-o", str(exe),
+                    "-L", pkg, "-lvexbayes_cuda", f"-Wl,-rpath,{pkg}"], check=True)
+    run = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    assert run.returncode == 0, run.stdout[-2000:] + run.stderr[-2000:]
+    r = parse(run.stdout)
+    import torch
+    assert int(r["devices"][0]) == torch.cuda.device_count() == int(r["in_use"][0])
+    assert r["nccl_one_rank"] == ["ok"] and int(r["nccl_version"][0]) >= 21800
+    if torch.cuda.device_count() >= 2:
+        assert r["multi_gpu"][0] == "ok"
+    m = M.logistic_model()
+    obs = oracle.simulate_at(m, [0.5, 100.0, 0.05], 0x9b1d6f0c5a3e7c21, 0, 0)
+    assert np.array_equal(hexd(r["observed"]), obs)
+    p, s, rho, f = oracle.abc_prior_predictive(m, M.keying(1337, A.VXB_KEY_WORKER, 3, 4), 1003, 0, 1003, obs)
+    assert np.array_equal(hexd(r["rho"]), rho) and np.array_equal(hexd(r["params"]), p.ravel())
+    eps, _ = oracle.select_epsilon(rho, f, 0.05)
+    assert float(r["epsilon"][1]) == eps
+    p2, _, rho2, f2 = oracle.abc_prior_predictive(m, M.keying(1337), 30001, 0, 30001, obs, want_summaries=False)
+    want = np.nonzero((rho2 <= eps) & (f2 == 0))[0]
+    assert int(r["reject_total"][0]) == len(want)
+    assert [int(t) for t in r["reject_rows"][1:]] == want.tolist()
+    assert np.array_equal(hexd(r["reject_rho"]), rho2[want])
+    assert np.array_equal(hexd(r["reject_params"]), p2[want].ravel())

@@ -1,0 +1,90 @@
+"""GPU tests of the multi-GPU layer behind the C ABI (include/vexbayes_cuda.h, section
+"multi-GPU"), run with however many GPUs the box has: vxb_multi_* over every visible
+device against the oracle and against the one-context calls, and the library's own NCCL
+communicator (vxb_comm_*) -- with one GPU a real 1-rank communicator, so NCCL is
+loaded, initialised and runs its collectives on the device."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_1902_09046_b200 import _abi as A, dist as D, lib, models as M
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def multi():
+    m = lib.Multi()
+    yield m
+    m.close()
+
+
+def test_multi_drivers_equal_one_context_and_oracle(ctx, multi, oracle, golden):
+    import torch
+    assert multi.size == torch.cuda.device_count() == lib.device_count()
+    obs = golden["logistic_observed"]
+    m = M.logistic_model()
+    # run_prior_predictive, reference keying (workers = stream layout, not devices)
+    key = M.keying(1337, A.VXB_KEY_WORKER, 5, 4)
+    got = multi.abc_prior_predictive(m, key, 2003, obs)
+    want = oracle.abc_prior_predictive(m, key, 2003, 0, 2003, obs)
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w, equal_nan=True)
+    # fused rejection + gather of the accepted samples
+    p, _, rho, f = oracle.abc_prior_predictive(m, M.keying(7), 40000, 0, 40000, obs, want_summaries=False)
+    eps, idx_o = oracle.select_epsilon(rho, f, 0.02)
+    nacc, idx, params, rho_acc = multi.abc_reject(m, M.keying(7), 40000, obs, eps, cap=40000)
+    assert nacc == len(idx_o) and np.array_equal(idx, idx_o)
+    assert np.array_equal(params, p[idx_o]) and np.array_equal(rho_acc, rho[idx_o])
+    nacc2, idx2, _, _ = multi.abc_reject(m, M.keying(7), 40000, obs, eps, cap=9)
+    assert nacc2 == nacc and np.array_equal(idx2, idx_o[:9])
+    # fp32 throughput variant: equal to the one-context call
+    mf = M.logistic_model(precision=A.VXB_F32, rng=A.VXB_RNG_FAST)
+    a = multi.abc_reject(mf, M.keying(7), 40000, obs, eps, cap=4000)
+    b = ctx.abc_reject(mf, M.keying(7), 40000, 0, 40000, obs, eps, cap=4000)
+    assert a[0] == b[0] and all(np.array_equal(x, y) for x, y in zip(a[1:], b[1:]))
+    # configs 2 and 4: integer counters of disjoint ranges
+    lam = np.array(M.lambda_grid(8))
+    ln = np.array([-0.5 * math.log(2.0 * math.pi * (l * l + 0.01)) for l in lam])
+    mdl = M.normal_mean_model(100)
+    c1, p1, _ = ctx.ppp_pvalues(mdl, lam, ln, 30001, 0, 30001, 1337, 2.9)
+    c2, p2 = multi.ppp_pvalues(mdl, lam, ln, 30001, 1337, 2.9)
+    assert np.array_equal(c1, c2) and np.array_equal(p1, p2)
+    mc = A.vxb_mlmc_cfg()
+    mc.levels, mc.refine, mc.tau0, mc.t_end, mc.paths, mc.seed = 3, 4, 1.0, 30.0, 20001, 1337
+    r1, r2 = ctx.mlmc_tauleap(M.mm_tauleap_model(), mc), multi.mlmc_tauleap(M.mm_tauleap_model(), mc)
+    for k in ("level_mean", "level_var", "level_cost"):
+        assert np.array_equal(r1[k], r2[k])
+    assert r1["estimate"] == r2["estimate"] and r1["std_error"] == r2["std_error"]
+
+
+def test_library_nccl_communicator_one_rank(ctx, oracle, golden):
+    """vxb_comm_* with n_ranks = 1: NCCL is dlopen'ed, a communicator is created on the
+    context's stream and its all-gather / all-reduce run on the GPU; the SPMD entry point
+    vxb_sharded_abc_reject through dist.sharded_reject(comm=...) equals the plain path."""
+    import torch
+    assert lib.comm_version() >= 21800
+    comm = lib.Comm(ctx, lib.comm_unique_id(), 0, 1)
+    assert (comm.rank, comm.size) == (0, 1)
+    dev = torch.device("cuda", ctx.device_info()["device"])
+    with torch.cuda.stream(torch.cuda.ExternalStream(ctx.stream(), device=dev)):
+        a = torch.arange(1000, dtype=torch.float64, device=dev)
+        b = torch.empty_like(a)
+        comm.allgather(a, b, a.numel() * 8)
+        comm.allreduce(b, b.numel(), A.VXB_DT_F64, A.VXB_OP_SUM)
+        c = torch.arange(64, dtype=torch.int64, device=dev)
+        comm.allreduce(c, 64, A.VXB_DT_I64, A.VXB_OP_MAX)
+    ctx.synchronize()
+    assert torch.equal(a, b) and torch.equal(c, torch.arange(64, dtype=torch.int64, device=dev))
+    obs = golden["logistic_observed"]
+    m = M.logistic_model()
+    _, _, rho, f = oracle.abc_prior_predictive(m, M.keying(3), 20000, 0, 20000, obs, want_summaries=False)
+    eps, idx_o = oracle.select_epsilon(rho, f, 0.03)
+    for kw in ({}, {"comm": comm}):
+        idx, params, r, n_dev = D.sharded_reject(ctx, m, M.keying(3), 20000, obs, eps, cap_fraction=0.1, **kw)
+        ctx.synchronize()
+        k = int(n_dev.item())
+        assert k == len(idx_o) and np.array_equal(idx[:k].cpu().numpy(), idx_o.astype(np.int64))
+        assert np.array_equal(r[:k].cpu().numpy(), rho[idx_o])
+    comm.close()

@@ -181,6 +181,14 @@ def test_sharded_abcsmc_driver_on_device(ctx, oracle, golden):
             assert eq(got[k], native[k]), k
     want = oracle.abcsmc_run(m, cfg, obs)
     assert eq(got["theta"], want["theta"]) and eq(got["weight"], want["weight"])
+    # throughput generator: the sharded driver must take the throughput form of the
+    # weights too (vxb_abcsmc_weights rng argument), or it drifts from the native run
+    mf = M.logistic_model(rng=A.VXB_RNG_FAST)
+    cfg = smc_cfg(n=1500, gens=4, seed=21)
+    native = ctx.abcsmc_run(mf, cfg, obs)
+    got = D.sharded_abcsmc(D.DeviceStages(ctx), mf, cfg, obs)
+    for k in ("epsilon", "proposals", "accept_rate", "theta", "rho", "weight", "ess", "mean", "cov"):
+        assert eq(got[k], native[k]), k
     # stage entry points against the oracle (host and device buffers)
     rs = np.random.RandomState(3)
     theta = rs.normal(size=(1000, 3))
