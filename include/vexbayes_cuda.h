@@ -252,6 +252,17 @@ int vxb_ppp_pvalues(vxb_ctx* ctx, const vxb_model* model, const double* lambda,
                     uint64_t count, uint64_t seed, double ybar_obs, uint64_t* counts,
                     double* pvalues, double* ybar_out);
 
+/* One rank's accepted set of the fused fixed-epsilon path as ONE block of device
+ * memory, so that a single all-gather moves it: [count u64, padded to 16 B]
+ * [idx u64 x cap][theta real x cap x dim][rho real x cap], each field 16-byte
+ * aligned; `stride` = bytes of a block.  Rows [0, min(count, cap)) are valid. */
+typedef struct vxb_accept_layout {
+    uint64_t cap;
+    uint64_t off_count, off_idx, off_params, off_rho;
+    uint64_t stride;
+} vxb_accept_layout;
+int vxb_accept_layout_of(int precision, uint32_t dim, uint64_t cap, vxb_accept_layout* out);
+
 /* ------------------------------------------- SMC building blocks (C3) */
 /* smc::ess (smc.cpp:208-219) and logsumexp (numeric.cpp:11-18). */
 int vxb_ess(vxb_ctx* ctx, const double* log_w, uint64_t n, double* ess);
@@ -302,6 +313,10 @@ int vxb_abcsmc_run(vxb_ctx* ctx, const vxb_model* model, const vxb_abcsmc_cfg* c
  *   theta* = theta_a + L z, reject outside the prior box, else simulate and
  *   compare with epsilon.  Outputs per proposal: theta* (count x dim), rho,
  *   flag (1 accepted, 0 rejected by distance, 2 outside the prior, 3 failed).
+ *   state (optional, DEVICE uint64[4], see vxb_abcsmc_append_round): the round is
+ *   skipped on the device when state[0] >= n_target already -- this is what lets a
+ *   multi-GPU host issue rounds ahead of its knowledge of how many are needed.
+ *   With device-resident buffers the call does not synchronise.
  * weights: for `count` new particles (theta_new: count x dim): the unnormalised
  *   importance weight 1 / sum_j w_j phi(theta_i; theta_j, Sigma), summed over
  *   j in index order.  rng = the model's generator: VXB_RNG_REF is the bit-exact
@@ -312,10 +327,38 @@ int vxb_abcsmc_run(vxb_ctx* ctx, const vxb_model* model, const vxb_abcsmc_cfg* c
 int vxb_abcsmc_propose(vxb_ctx* ctx, const vxb_model* model, uint64_t seed, uint32_t gen,
                        uint64_t first, uint64_t count, uint64_t n_prev, const double* theta_prev,
                        const double* cum_prev, const double* chol, const double* observed,
-                       double epsilon, double* theta_out, double* rho_out, uint8_t* flag_out);
+                       double epsilon, double* theta_out, double* rho_out, uint8_t* flag_out,
+                       const uint64_t* state, uint64_t n_target);
 int vxb_abcsmc_weights(vxb_ctx* ctx, int rng, uint32_t dim, uint64_t count, const double* theta_new,
                        uint64_t n_prev, const double* theta_prev,
                        const double* w_prev, const double* chol, double* w_out);
+
+/* Rounds without host round trips (the multi-GPU ABC-SMC host, dist.sharded_abcsmc).
+ * state: DEVICE uint64[4] = { rows of the new population filled so far, accepted
+ * proposals counted while filling, rounds used, reserved }, zeroed by the caller at
+ * the start of a generation.
+ * pack_round: the accepted rows (finite rho <= epsilon, !failed) of this rank's
+ *   `count` evaluated rows -> one block laid out as vxb_accept_layout_of(VXB_F64, dim,
+ *   cap >= count): count | local row numbers | theta | rho; nothing is packed once
+ *   state[0] >= n_target.
+ * append_round: the gathered blocks of all ranks of a round, in rank order
+ *   (= ascending proposal index), are appended behind the filled rows of the new
+ *   population up to n rows -- "the first n accepted by proposal index", as the
+ *   one-GPU loop of vxb_abcsmc_run takes them -- and the state advances; a round that
+ *   arrives after the population is full changes nothing.
+ * normalise_by_chunk_totals: w /= (chunk totals added left to right), the divisor
+ *   formed on the device; chunk_totals is the all-reduced vector of
+ *   vxb_canon_chunk_sums values.
+ * Device buffers only; none of the three synchronises. */
+int vxb_abcsmc_pack_round(vxb_ctx* ctx, uint32_t dim, const double* theta, const double* rho,
+                          const uint8_t* failed, uint64_t count, double epsilon,
+                          const vxb_accept_layout* layout, void* block, const uint64_t* state,
+                          uint64_t n_target);
+int vxb_abcsmc_append_round(vxb_ctx* ctx, uint32_t dim, const void* blocks, uint32_t n_blocks,
+                            const vxb_accept_layout* layout, double* pop_theta, double* pop_rho,
+                            uint64_t n, uint64_t* state);
+int vxb_normalise_by_chunk_totals(vxb_ctx* ctx, double* w, uint64_t n, const double* chunk_totals,
+                                  uint64_t n_chunks, double* total_out);
 
 /* Population statistics of a generation in the canonical two-level summation
  * order (chunks of 256 rows left to right, then chunk totals left to right) --
@@ -495,16 +538,6 @@ int vxb_comm_size(const vxb_comm* comm);
 int vxb_comm_allgather(vxb_comm* comm, const void* send, void* recv, size_t bytes);
 int vxb_comm_allreduce(vxb_comm* comm, void* buf, size_t count, int dtype, int op);
 
-/* One rank's accepted set of the fused fixed-epsilon path as ONE block of device
- * memory, so that a single all-gather moves it: [count u64, padded to 16 B]
- * [idx u64 x cap][theta real x cap x dim][rho real x cap], each field 16-byte
- * aligned; `stride` = bytes of a block.  Rows [0, min(count, cap)) are valid. */
-typedef struct vxb_accept_layout {
-    uint64_t cap;
-    uint64_t off_count, off_idx, off_params, off_rho;
-    uint64_t stride;
-} vxb_accept_layout;
-int vxb_accept_layout_of(int precision, uint32_t dim, uint64_t cap, vxb_accept_layout* out);
 
 /* SPMD form of config 1 (every rank calls it): rank r simulates the rows
  * partition(n_total, n_ranks, 1)[r] with vxb_abc_reject writing into

@@ -377,6 +377,10 @@ struct ProposeParams {
     double* theta_out;
     double* rho_out;
     uint8_t* flag_out;
+    // optional gate (multi-GPU rounds issued ahead of the host's knowledge): the round
+    // is skipped when the population is already full, state[0] >= gate_target
+    const unsigned long long* gate;
+    uint64_t gate_target;
 };
 
 // One proposal per thread (layout: vxo_abcsmc_propose): position 0 ancestor
@@ -385,6 +389,7 @@ struct ProposeParams {
 __global__ void __launch_bounds__(256, VXB_PROP_MINB) abcsmc_propose_kernel(const __grid_constant__ ProposeParams p) {
     const uint64_t r = static_cast<uint64_t>(blockIdx.x) * 256 + threadIdx.x;
     if (r >= p.count) return;
+    if (p.gate && *p.gate >= p.gate_target) return;
     const uint64_t key = stream_key(p.seed_hash, p.first + r);
     const Words w0 = philox2x64(key, 0);
     const double target = __dmul_rn(to_unit(w0.w0), p.cum_prev[p.n_prev - 1]);
@@ -506,6 +511,7 @@ abcsmc_propose_fast_kernel(const __grid_constant__ ProposeFastParams pp) {
     const ProposeParams& p = pp.base;
     const uint64_t r = static_cast<uint64_t>(blockIdx.x) * 256 + threadIdx.x;
     if (r >= p.count) return;
+    if (p.gate && *p.gate >= p.gate_target) return;
     const uint64_t row = p.first + r;
     const uint32_t rl = static_cast<uint32_t>(row), rh = static_cast<uint32_t>(row >> 32);
     const uint32_t dom = kDomProposal | (pp.gen << 8);
@@ -614,10 +620,77 @@ abcsmc_weights_fast_kernel(uint64_t count, const double* __restrict__ y_new, uin
     if (r < count) w_out[r] = 1.0 / sum;
 }
 
+// ---- rounds without host round trips (multi-GPU ABC-SMC, dist.sharded_abcsmc)
+// state (device, 4 x uint64): [0] rows of the new population filled so far, [1]
+// accepted proposals counted while filling, [2] rounds used, [3] reserved.
+// pack: the accepted rows of this rank's slice of a round -> its packed block
+// (vxb_accept_layout: count | idx | theta | rho); a round issued after the population
+// filled up packs nothing.  append: the gathered blocks of all ranks, in rank order
+// (= ascending proposal index), onto the population -- the first n accepted by
+// proposal index, exactly as the one-GPU loop takes them.
+__global__ void pack_rows_kernel(const uint64_t* __restrict__ idx, unsigned long long* count,
+                                 uint64_t cap, uint32_t dim, const double* __restrict__ theta,
+                                 const double* __restrict__ rho, double* __restrict__ dst_theta,
+                                 double* __restrict__ dst_rho, const unsigned long long* gate,
+                                 uint64_t gate_target) {
+    const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (gate && *gate >= gate_target) {
+        if (t == 0) *count = 0;
+        return;
+    }
+    const uint64_t n_take = min(static_cast<uint64_t>(*count), cap);
+    if (t >= n_take) return;
+    const uint64_t s = idx[t];
+    for (uint32_t k = 0; k < dim; ++k) dst_theta[t * dim + k] = theta[s * dim + k];
+    dst_rho[t] = rho[s];
+}
+__global__ void append_rows_kernel(const char* __restrict__ blocks, uint32_t n_blocks,
+                                   vxb_accept_layout lay, uint32_t dim, double* __restrict__ pop_theta,
+                                   double* __restrict__ pop_rho, uint64_t n,
+                                   const unsigned long long* __restrict__ state) {
+    const uint64_t base = state[0];
+    if (base >= n) return;
+    const uint32_t r = blockIdx.y;
+    const uint64_t row = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    uint64_t before = 0, mine = 0;
+    for (uint32_t q = 0; q <= r; ++q) {
+        const uint64_t c = min(*reinterpret_cast<const unsigned long long*>(blocks + q * lay.stride + lay.off_count),
+                               static_cast<unsigned long long>(lay.cap));
+        if (q < r) before += c; else mine = c;
+    }
+    if (row >= mine) return;
+    const uint64_t dest = base + before + row;
+    if (dest >= n) return;
+    const char* b = blocks + r * lay.stride;
+    const double* th = reinterpret_cast<const double*>(b + lay.off_params);
+    const double* rh = reinterpret_cast<const double*>(b + lay.off_rho);
+    for (uint32_t k = 0; k < dim; ++k) pop_theta[dest * dim + k] = th[row * dim + k];
+    pop_rho[dest] = rh[row];
+}
+__global__ void append_state_kernel(const char* __restrict__ blocks, uint32_t n_blocks,
+                                    vxb_accept_layout lay, uint64_t n, unsigned long long* state) {
+    if (state[0] >= n) return;
+    unsigned long long total = 0;
+    for (uint32_t q = 0; q < n_blocks; ++q)
+        total += min(*reinterpret_cast<const unsigned long long*>(blocks + q * lay.stride + lay.off_count),
+                     static_cast<unsigned long long>(lay.cap));
+    state[1] += total;
+    state[2] += 1;
+    state[0] = min(static_cast<unsigned long long>(n), state[0] + total);
+}
+// total of the chunk totals, left to right (the canonical order), then w /= total
+__global__ void chunk_total_kernel(const double* __restrict__ totals, uint64_t nchunks,
+                                   double* __restrict__ out) {
+    double t = 0.0;
+    for (uint64_t c = 0; c < nchunks; ++c) t = __dadd_rn(t, totals[c]);
+    *out = t;
+}
+
 void propose_device(vxb_ctx* ctx, const vxb_model& model, uint64_t seed, uint32_t gen,
                     uint64_t first, uint64_t count, uint64_t n_prev, const double* theta_prev,
                     const double* cum_prev, const double* chol_host, const double* observed_host,
-                    double epsilon, double* theta_out, double* rho_out, uint8_t* flag_out) {
+                    double epsilon, double* theta_out, double* rho_out, uint8_t* flag_out,
+                    const uint64_t* gate = nullptr, uint64_t gate_target = 0) {
     require(gen >= 1, "invalid-argument", "generation 0 is the prior predictive set");
     require(n_prev >= 1, "insufficient-data", "empty previous population");
     require(model.precision == VXB_F64 && (model.rng == VXB_RNG_REF || model.rng == VXB_RNG_FAST),
@@ -637,6 +710,8 @@ void propose_device(vxb_ctx* ctx, const vxb_model& model, uint64_t seed, uint32_
     p.theta_out = theta_out;
     p.rho_out = rho_out;
     p.flag_out = flag_out;
+    p.gate = reinterpret_cast<const unsigned long long*>(gate);
+    p.gate_target = gate_target;
     if (count == 0) return;
     LaunchScope scope(ctx, VXB_K_PROPOSE);
     if (model.rng == VXB_RNG_FAST) {
@@ -751,12 +826,16 @@ extern "C" int vxb_abcsmc_propose(vxb_ctx* ctx, const vxb_model* model, uint64_t
                                   uint64_t first, uint64_t count, uint64_t n_prev,
                                   const double* theta_prev, const double* cum_prev,
                                   const double* chol, const double* observed, double epsilon,
-                                  double* theta_out, double* rho_out, uint8_t* flag_out) {
+                                  double* theta_out, double* rho_out, uint8_t* flag_out,
+                                  const uint64_t* state, uint64_t n_target) {
     return guarded([&] {
         use(ctx);
+        if (count == 0) return;  // an empty shard (more ranks than proposals in the round)
         require(model && theta_prev && cum_prev && chol && observed && theta_out && rho_out &&
                     flag_out,
                 "invalid-argument", "null argument");
+        require(!state || is_device_pointer(state), "invalid-argument",
+                "the round state lives in device memory");
         require(!is_device_pointer(chol) && !is_device_pointer(observed), "invalid-argument",
                 "chol and observed are host arrays");
         Staged d_tp(ctx, theta_prev, n_prev * 3 * 8, true, false);
@@ -766,11 +845,95 @@ extern "C" int vxb_abcsmc_propose(vxb_ctx* ctx, const vxb_model* model, uint64_t
         Staged d_flag(ctx, flag_out, count, false, true);
         propose_device(ctx, *model, seed, gen, first, count, n_prev, d_tp.as<double>(),
                        d_cp.as<double>(), chol, observed, epsilon, d_th.as<double>(),
-                       d_rho.as<double>(), d_flag.as<uint8_t>());
+                       d_rho.as<double>(), d_flag.as<uint8_t>(), state, n_target);
         d_th.finish();
         d_rho.finish();
         d_flag.finish();
-        VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+        // all-device buffers: stay asynchronous (rounds are queued back to back)
+        if (d_tp.staged() || d_cp.staged() || d_th.staged() || d_rho.staged() || d_flag.staged())
+            VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+// The accepted rows (finite rho <= epsilon, !failed) of `count` evaluated rows, packed
+// into one block (vxb_accept_layout of (VXB_F64, dim, cap)): count | local row numbers |
+// theta | rho.  Device buffers only; asynchronous.
+extern "C" int vxb_abcsmc_pack_round(vxb_ctx* ctx, uint32_t dim, const double* theta,
+                                     const double* rho, const uint8_t* failed, uint64_t count,
+                                     double epsilon, const vxb_accept_layout* layout, void* block,
+                                     const uint64_t* state, uint64_t n_target) {
+    return guarded([&] {
+        use(ctx);
+        require(layout && block && is_device_pointer(block), "invalid-argument",
+                "block is a device buffer");
+        require(!state || is_device_pointer(state), "invalid-argument",
+                "the round state lives in device memory");
+        char* base = static_cast<char*>(block);
+        auto* cnt = reinterpret_cast<unsigned long long*>(base + layout->off_count);
+        if (count == 0) {
+            VXB_CUDA(cudaMemsetAsync(cnt, 0, 8, ctx->stream));
+            return;
+        }
+        require(theta && rho && is_device_pointer(theta) && is_device_pointer(rho) &&
+                    (!failed || is_device_pointer(failed)),
+                "invalid-argument", "theta, rho and failed are device buffers");
+        require(count <= layout->cap, "invalid-shape", "the block is smaller than the slice");
+        auto* idx = reinterpret_cast<uint64_t*>(base + layout->off_idx);
+        compact_accepted_device(ctx, VXB_F64, rho, failed, count, epsilon, 0, layout->cap,
+                                reinterpret_cast<uint64_t*>(cnt), idx);
+        LaunchScope scope(ctx, VXB_K_COMPACT);
+        pack_rows_kernel<<<grid_for(count, 256), 256, 0, ctx->stream>>>(
+            idx, cnt, layout->cap, dim, theta, rho, reinterpret_cast<double*>(base + layout->off_params),
+            reinterpret_cast<double*>(base + layout->off_rho),
+            reinterpret_cast<const unsigned long long*>(state), n_target);
+        check_launch("pack_rows_kernel");
+    });
+}
+
+// Appends the gathered blocks of a round (n_blocks of them, rank order) to the new
+// population (pop_theta: n x dim, pop_rho: n) behind the rows already filled, up to n
+// rows, and advances the state.  A round that arrives after the population filled up
+// changes nothing.  Device buffers only; asynchronous.
+extern "C" int vxb_abcsmc_append_round(vxb_ctx* ctx, uint32_t dim, const void* blocks,
+                                       uint32_t n_blocks, const vxb_accept_layout* layout,
+                                       double* pop_theta, double* pop_rho, uint64_t n,
+                                       uint64_t* state) {
+    return guarded([&] {
+        use(ctx);
+        require(blocks && layout && pop_theta && pop_rho && state && n_blocks >= 1,
+                "invalid-argument", "null argument");
+        require(is_device_pointer(blocks) && is_device_pointer(pop_theta) &&
+                    is_device_pointer(pop_rho) && is_device_pointer(state),
+                "invalid-argument", "device buffers only");
+        LaunchScope scope(ctx, VXB_K_COMPACT);
+        const dim3 grid(grid_for(layout->cap, 256), n_blocks);
+        append_rows_kernel<<<grid, 256, 0, ctx->stream>>>(
+            static_cast<const char*>(blocks), n_blocks, *layout, dim, pop_theta, pop_rho, n,
+            reinterpret_cast<const unsigned long long*>(state));
+        append_state_kernel<<<1, 1, 0, ctx->stream>>>(static_cast<const char*>(blocks), n_blocks, *layout,
+                                                     n, reinterpret_cast<unsigned long long*>(state));
+        check_launch("append kernels");
+    });
+}
+
+// w[i] <- w[i] / (sum of the chunk totals, added left to right): the weight
+// normalisation with the divisor formed on the device in the canonical order.
+// total_out (optional, device): the divisor.  Device buffers only; asynchronous.
+extern "C" int vxb_normalise_by_chunk_totals(vxb_ctx* ctx, double* w, uint64_t n,
+                                             const double* chunk_totals, uint64_t n_chunks_in,
+                                             double* total_out) {
+    return guarded([&] {
+        use(ctx);
+        require(w && chunk_totals && n >= 1 && n_chunks_in >= 1, "invalid-argument", "null argument");
+        require(is_device_pointer(w) && is_device_pointer(chunk_totals) &&
+                    (!total_out || is_device_pointer(total_out)),
+                "invalid-argument", "device buffers only");
+        Scratch d_total(ctx, total_out ? 0 : 8);
+        double* t = total_out ? total_out : d_total.as<double>();
+        LaunchScope scope(ctx, VXB_K_MISC);
+        chunk_total_kernel<<<1, 1, 0, ctx->stream>>>(chunk_totals, n_chunks_in, t);
+        scale_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(w, n, t);
+        check_launch("normalise kernels");
     });
 }
 

@@ -180,7 +180,9 @@ def _world(group):
 def allgather_rows(tensors, group=None):
     """All-gather row blocks of different length: one all_gather of the counts,
     then one padded all_gather per tensor; returns the rank-order concatenations
-    and the per-rank counts.  With one rank it is the identity."""
+    and the per-rank counts.  With one rank it is the identity.  Synchronises (the
+    counts travel through the host): used by the one-shot paths (config 0, the
+    weak-informativity test), not inside the ABC-SMC rounds."""
     import torch
     import torch.distributed as dist
     rank, world = _world(group)
@@ -206,62 +208,73 @@ class DeviceStages:
     """The per-rank stage operations of an ABC-SMC generation on this rank's GPU,
     each one call into the C ABI (include/vexbayes_cuda.h).  Tensors are torch
     CUDA tensors that live on the library's stream; torch only allocates, slices
-    and carries them into the collectives."""
+    and carries them into the collectives.  Every round operation is asynchronous:
+    counts and fill levels stay in device memory (the `state` vector)."""
 
     def __init__(self, ctx):
         import torch
         self.ctx = ctx
         self.device = torch.device("cuda", ctx.device_info()["device"])
         self._stream = torch.cuda.ExternalStream(ctx.stream(), device=self.device)
+        self._scratch = {}
 
     def scope(self):
         import torch
         return torch.cuda.stream(self._stream)
 
-    def _rows(self, count, dim):
+    def _buffers(self, count, dim):
+        """Per-round evaluation scratch (theta*, rho, flag), reused across rounds."""
         import torch
-        return (torch.empty((count, dim), dtype=torch.float64, device=self.device),
-                torch.empty(count, dtype=torch.float64, device=self.device))
+        key = (count, dim)
+        if key not in self._scratch:
+            self._scratch = {key: (
+                torch.empty((max(count, 1), dim), dtype=torch.float64, device=self.device),
+                torch.empty(max(count, 1), dtype=torch.float64, device=self.device),
+                torch.empty(max(count, 1), dtype=torch.uint8, device=self.device))}
+        return self._scratch[key]
 
-    def _compacted(self, theta, rho, failed, eps):
-        """Ascending rows with !failed and rho <= eps (ballot/scan compaction kernel)."""
-        import torch
-        from . import _abi as A
-        count = int(rho.shape[0])
-        if count == 0:  # empty shard (more ranks than rows in the round)
-            return theta, rho
-        idx = torch.empty(max(count, 1), dtype=torch.int64, device=self.device)
-        _, k = self.ctx.compact_accepted(rho, failed, eps, 0, count, A.VXB_F64, count, idx)
-        keep = idx[:k]
-        return theta.index_select(0, keep), rho.index_select(0, keep)
-
-    def prior_rows(self, model, seed0, n_total, first, count, observed):
-        import torch
-        from . import models as M
-        theta, rho = self._rows(count, model.dim)
-        if count == 0:
-            return theta, rho
-        failed = torch.empty(count, dtype=torch.uint8, device=self.device)
-        self.ctx.abc_prior_predictive(model, M.keying(seed0), n_total, first, count, observed,
-                                      params=theta, rho=rho, failed=failed)
-        return self._compacted(theta, rho, failed, float("inf"))
-
-    def propose(self, model, seed, gen, first, count, theta_prev, cum_prev, chol, observed, eps):
+    def _pack(self, dim, theta, rho, failed, count, eps, layout, block, state, n):
         import ctypes as C
-        import torch
         from .lib import _ptr, u32, u64, f64
-        theta, rho = self._rows(count, model.dim)
-        if count == 0:
-            return theta, rho
-        flag = torch.empty(count, dtype=torch.uint8, device=self.device)
+        c = self.ctx
+        c._check(c.lib.vxb_abcsmc_pack_round(c.handle, u32(dim), _ptr(theta), _ptr(rho), _ptr(failed),
+                                             u64(count), f64(eps), C.byref(layout), _ptr(block),
+                                             _ptr(state), u64(n)))
+
+    def prior_round(self, model, seed0, n_total, first, count, observed, layout, block, state, n):
+        """Generation 0: rows [first, first+count) of the prior predictive job, the
+        non-failed ones packed into `block`."""
+        from . import models as M
+        theta, rho, failed = self._buffers(count, model.dim)
+        if count:
+            self.ctx.abc_prior_predictive(model, M.keying(seed0), n_total, first, count, observed,
+                                          params=theta, rho=rho, failed=failed)
+        self._pack(model.dim, theta, rho, failed, count, float("inf"), layout, block, state, n)
+
+    def propose_round(self, model, seed, gen, first, count, theta_prev, cum_prev, chol, observed,
+                      eps, layout, block, state, n):
+        """Generation >= 1: proposals [first, first+count), the accepted ones packed into
+        `block`; skipped on the device once the population is full."""
+        import ctypes as C
+        from .lib import _ptr, u32, u64, f64
+        theta, rho, flag = self._buffers(count, model.dim)
         ch = np.ascontiguousarray(chol, dtype=np.float64)
         obs = np.ascontiguousarray(observed, dtype=np.float64)
         c = self.ctx
         c._check(c.lib.vxb_abcsmc_propose(c.handle, C.byref(model), u64(seed), u32(gen), u64(first),
                                           u64(count), u64(int(theta_prev.shape[0])),
                                           _ptr(theta_prev), _ptr(cum_prev), _ptr(ch), _ptr(obs),
-                                          f64(eps), _ptr(theta), _ptr(rho), _ptr(flag)))
-        return self._compacted(theta, rho, None, eps)
+                                          f64(eps), _ptr(theta), _ptr(rho), _ptr(flag),
+                                          _ptr(state), u64(n)))
+        self._pack(model.dim, theta, rho, None, count, eps, layout, block, state, n)
+
+    def append_round(self, blocks, world, layout, pop_theta, pop_rho, n, state):
+        import ctypes as C
+        from .lib import _ptr, u32, u64
+        c = self.ctx
+        c._check(c.lib.vxb_abcsmc_append_round(c.handle, u32(int(pop_theta.shape[1])), _ptr(blocks),
+                                               u32(world), C.byref(layout), _ptr(pop_theta),
+                                               _ptr(pop_rho), u64(n), _ptr(state)))
 
     def weights(self, theta_new, theta_prev, w_prev, chol, rng=0):
         """rng: the model's generator -- VXB_RNG_FAST selects the throughput form of the
@@ -271,10 +284,10 @@ class DeviceStages:
         out = torch.empty(int(theta_new.shape[0]), dtype=torch.float64, device=self.device)
         if out.numel() == 0:
             return out
-        ch = np.ascontiguousarray(chol, dtype=np.float64)
+        ch = torch.from_numpy(np.ascontiguousarray(chol, dtype=np.float64)).to(self.device)
         c = self.ctx
         c._check(c.lib.vxb_abcsmc_weights(c.handle, i32(rng), u32(int(theta_new.shape[1])),
-                                          u64(int(theta_new.shape[0])), _ptr(theta_new),
+                                          u64(int(theta_new.shape[0])), _ptr(theta_new.contiguous()),
                                           u64(int(theta_prev.shape[0])), _ptr(theta_prev),
                                           _ptr(w_prev), _ptr(ch), _ptr(out)))
         return out
@@ -295,9 +308,13 @@ class DeviceStages:
         return self.ctx.canon_chunk_sums(
             v, torch.empty((n + CHUNK - 1) // CHUNK, dtype=torch.float64, device=self.device))
 
-    def normalise(self, w_raw, total):
-        # not `w_raw / total`: torch multiplies by the reciprocal of a host scalar
-        return self.ctx.divide(w_raw.contiguous(), total)
+    def normalise_by_totals(self, w_raw, totals):
+        """In place: w_raw /= (chunk totals added left to right), all on the device."""
+        from .lib import _ptr, u64
+        c = self.ctx
+        c._check(c.lib.vxb_normalise_by_chunk_totals(c.handle, _ptr(w_raw), u64(int(w_raw.shape[0])),
+                                                     _ptr(totals), u64(int(totals.shape[0])), None))
+        return w_raw
 
     def make_kernel(self, cov, scale, jitter):
         from . import lib
@@ -307,22 +324,33 @@ class DeviceStages:
 def sharded_abcsmc(stages, model, cfg, observed, group=None):
     """ABC-SMC (BASELINE config 3; scheme of DESIGN.md section 3.3) with the
     proposals of every round and the new particles of every generation sharded
-    over the ranks by global index.  Exchanges per generation:
+    over the ranks by global index.  Exchanges:
 
-    * all-gather of each round's accepted proposals (theta*, rho), rank order =
-      ascending proposal index, so "the first N accepted by proposal index" is
-      the same set on every rank and for every world size;
-    * all-gather of the unnormalised importance weights (shards are aligned to
-      the 256-row canonical chunks);
-    * all-reduce(SUM) of the vector of chunk totals -- every entry has exactly
-      one non-zero contributor, so the reduction is exact and the weight sum
-      (chunk totals added left to right) is bit-identical to the one-GPU run.
+    * per round ONE all_gather_into_tensor of each rank's packed block of accepted
+      proposals (count | theta* | rho at a fixed capacity); the blocks are appended in
+      rank order = ascending proposal index, so "the first N accepted by proposal
+      index" is the same set on every rank and for every world size;
+    * per generation one all-gather of the unnormalised importance weights (shards
+      aligned to the 256-row canonical chunks, fixed size) and one all-reduce(SUM) of
+      the vector of chunk totals -- every entry has exactly one non-zero contributor,
+      so the reduction is exact and the weight sum (chunk totals added left to right,
+      on the device) is bit-identical to the one-GPU run.
 
-    The previous population (theta, w, rho) is replicated; its statistics
-    (epsilon, weighted covariance, cumulative weights) are recomputed on every
-    rank.  `stages` supplies the per-rank compute (DeviceStages on a GPU).
-    Returns the dictionary of Context.abcsmc_run."""
+    No per-round host round trip: accepted counts, the fill level of the new
+    population and the number of rounds used live in device memory (`state`); rounds
+    are issued AHEAD of the host's knowledge from the previous acceptance rate, and a
+    round that arrives after the population is full is skipped on the device.  The
+    host reads the 4-word state once per batch of rounds (normally once per
+    generation, together with the population statistics it needs anyway).
+
+    The previous population (theta, w, rho) is replicated; its statistics (epsilon,
+    weighted covariance, cumulative weights) are recomputed on every rank.  `stages`
+    supplies the per-rank compute (DeviceStages on a GPU).  Returns the dictionary of
+    Context.abcsmc_run."""
+    import math
     import torch
+    import torch.distributed as dist
+    from . import _abi as A, lib
     from .lib import derive_seed
     rank, world = _world(group)
     n, gens, d = int(cfg.particles), int(cfg.generations), int(model.dim)
@@ -336,9 +364,22 @@ def sharded_abcsmc(stages, model, cfg, observed, group=None):
     n_chunks = (n + CHUNK - 1) // CHUNK
     c_begin, c_end = shard_range(n_chunks, world, rank)
     w_begin, w_end = min(n, c_begin * CHUNK), min(n, c_end * CHUNK)
+    w_pad = (shard_range(n_chunks, world, 0)[1]) * CHUNK          # largest weight shard
+    w_spans = [(min(n, shard_range(n_chunks, world, r)[0] * CHUNK),
+                min(n, shard_range(n_chunks, world, r)[1] * CHUNK)) for r in range(world)]
     seed0 = derive_seed(cfg.seed, [0])
-    theta = w = rho = None
+    b, e = shard_range(round_size, world, rank)
+    cap = max(1, shard_range(round_size, world, 0)[1])            # largest slice of a round
+    layout = lib.accept_layout(A.VXB_F64, d, cap)
+    dev = stages.device
     with stages.scope():
+        block = torch.zeros(int(layout.stride), dtype=torch.uint8, device=dev)
+        blocks = torch.zeros(world * int(layout.stride), dtype=torch.uint8, device=dev) if world > 1 else block
+        state = torch.zeros(4, dtype=torch.int64, device=dev)
+        pops = [(torch.zeros((n, d), dtype=torch.float64, device=dev),
+                 torch.zeros(n, dtype=torch.float64, device=dev)) for _ in range(2)]
+        theta = w = rho = None
+        rate = 1.0
         for g in range(gens):
             eps, chol, cum = float("inf"), None, None
             if g >= 1:
@@ -346,49 +387,56 @@ def sharded_abcsmc(stages, model, cfg, observed, group=None):
                 _, cov, _ = stages.moments(theta, w)
                 chol = stages.make_kernel(cov, cfg.kernel_scale, cfg.jitter)
                 cum = stages.cumsum(w)
-            got = evaluated = accepted_total = 0
-            kept_theta, kept_rho = [], []
-            for t in range(max_rounds):
-                if got >= n:
-                    break
-                b, e = shard_range(round_size, world, rank)
-                first, count = t * round_size + b, e - b
-                if g == 0:
-                    th, r = stages.prior_rows(model, seed0, (t + 1) * round_size, first, count,
-                                              observed)
-                else:
-                    th, r = stages.propose(model, cfg.seed, g, first, count, theta, cum, chol,
-                                           observed, eps)
-                (th, r), counts = allgather_rows([th, r], group)
-                accepted = sum(counts)
-                take = min(accepted, n - got)
-                kept_theta.append(th[:take])
-                kept_rho.append(r[:take])
-                got += take
-                accepted_total += accepted
-                evaluated += round_size
+            theta_new, rho_new = pops[g & 1]
+            state.zero_()
+            issued, got, accepted_total, used = 0, 0, 0, 0
+            while got < n and issued < max_rounds:
+                # generation 0 accepts every non-failed row: no slack; later generations:
+                # the rounds the estimated rate asks for, plus half as many again
+                need = (n - got) / (round_size * rate)
+                ahead = int(math.ceil(need)) if g == 0 else int(math.ceil(1.5 * need)) + 1
+                ahead = max(1, min(ahead, max_rounds - issued))
+                for t in range(issued, issued + ahead):
+                    first, count = t * round_size + b, e - b
+                    if g == 0:
+                        stages.prior_round(model, seed0, (t + 1) * round_size, first, count, observed,
+                                           layout, block, state, n)
+                    else:
+                        stages.propose_round(model, cfg.seed, g, first, count, theta, cum, chol,
+                                             observed, eps, layout, block, state, n)
+                    if world > 1:
+                        gather_packed(block, world, out=blocks, group=group)
+                    stages.append_round(blocks, world, layout, theta_new, rho_new, n, state)
+                issued += ahead
+                got, accepted_total, used, _ = (int(v) for v in state.cpu().numpy())  # one read per batch
+                if used:
+                    rate = max(accepted_total / (used * round_size), 1e-9)
             if got != n:
                 raise RuntimeError("empty-set: generation did not fill within max_rounds")
-            theta_new = torch.cat(kept_theta).contiguous()
-            rho_new = torch.cat(kept_rho).contiguous()
+            evaluated = used * round_size
+            rate *= 0.8   # the acceptance rate falls from one generation to the next
             if g == 0:
-                w_new = torch.full((n,), 1.0 / n, dtype=torch.float64, device=theta_new.device)
+                w_new = torch.full((n,), 1.0 / n, dtype=torch.float64, device=dev)
             else:
                 w_local = stages.weights(theta_new[w_begin:w_end], theta, w, chol, rng=int(model.rng))
-                (w_raw,), _ = allgather_rows([w_local], group)
-                totals = torch.zeros(n_chunks, dtype=torch.float64, device=w_raw.device)
+                totals = torch.zeros(n_chunks, dtype=torch.float64, device=dev)
                 if w_end > w_begin:
                     totals[c_begin:c_end] = stages.chunk_sums(w_local)
                 if world > 1:
+                    padded = torch.zeros(w_pad, dtype=torch.float64, device=dev)
+                    padded[:w_end - w_begin] = w_local
+                    gathered = torch.empty(world * w_pad, dtype=torch.float64, device=dev)
+                    dist.all_gather_into_tensor(gathered, padded, group=group)
+                    w_new = torch.cat([gathered[r * w_pad:r * w_pad + (hi - lo)]
+                                       for r, (lo, hi) in enumerate(w_spans)])
                     allreduce_sum(totals, group)
-                total = 0.0
-                for v in totals.tolist():  # chunk totals, left to right
-                    total += v
-                if not (np.isfinite(total) and total > 0.0):
-                    raise RuntimeError("degenerate-ensemble: weight sum is not finite")
-                w_new = stages.normalise(w_raw, total)
-            theta, w, rho = theta_new, w_new.contiguous(), rho_new
+                else:
+                    w_new = w_local
+                w_new = stages.normalise_by_totals(w_new.contiguous(), totals)
+            theta, w, rho = theta_new, w_new, rho_new
             mean, cov, s2 = stages.moments(theta, w)
+            if not (np.isfinite(s2) and s2 > 0.0):
+                raise RuntimeError("degenerate-ensemble: weight sum is not finite")
             res["epsilon"][g], res["ess"][g] = eps, 1.0 / s2
             res["accept_rate"][g] = accepted_total / evaluated
             res["proposals"][g] = evaluated

@@ -531,7 +531,7 @@ class Context:
         self._check(self.lib.vxb_abcsmc_propose(self.handle, C.byref(model), u64(seed), u32(gen),
                                                 u64(first), u64(count), u64(tp.shape[0]), _ptr(tp),
                                                 _ptr(cp), _ptr(ch), _ptr(obs), f64(eps), _ptr(th),
-                                                _ptr(rho), _ptr(flag)))
+                                                _ptr(rho), _ptr(flag), None, u64(0)))
         return th, rho, flag
 
     def abcsmc_weights(self, theta_new, theta_prev, w_prev, chol, rng=A.VXB_RNG_REF):

@@ -139,31 +139,65 @@ def test_two_rank_gather_equals_single_rank(tmp_path, oracle):
 class OracleStages:
     """Test stand-in for dist.DeviceStages: the same stage interface, computed by
     the CPU oracle on torch CPU tensors (so the gloo run exercises exactly the
-    host logic that moves CUDA tensors over NCCL on the GPU box)."""
+    host logic that moves CUDA tensors over NCCL on the GPU box), including the
+    device-resident round state: state[0] rows filled, [1] accepted, [2] rounds used."""
 
     def __init__(self, oracle):
         self.o = oracle
+        self.device = torch.device("cpu")
 
     def scope(self):
         import contextlib
         return contextlib.nullcontext()
 
     @staticmethod
-    def _keep(theta, rho, mask):
-        return (torch.from_numpy(np.ascontiguousarray(theta[mask])),
-                torch.from_numpy(np.ascontiguousarray(rho[mask])))
+    def _pack(theta, rho, mask, layout, block, state, n):
+        from paper_1902_09046_b200 import _abi as A
+        idx, p, r, count = D.packed_views(block, layout, A.VXB_F64, theta.shape[1] if theta.ndim == 2 else 3)
+        if int(state[0]) >= n or rho.size == 0:      # the gate of pack_rows_kernel
+            count[0] = 0
+            return
+        k = int(mask.sum())
+        assert k <= int(layout.cap)
+        p[0, :k] = torch.from_numpy(np.ascontiguousarray(theta[mask]))
+        r[0, :k] = torch.from_numpy(np.ascontiguousarray(rho[mask]))
+        count[0] = k
 
-    def prior_rows(self, model, seed0, n_total, first, count, observed):
+    def prior_round(self, model, seed0, n_total, first, count, observed, layout, block, state, n):
+        if count == 0:
+            return self._pack(np.zeros((0, 3)), np.zeros(0), np.zeros(0, bool), layout, block, state, n)
         p, _, rho, f = self.o.abc_prior_predictive(model, M.keying(seed0), n_total, first, count,
                                                    observed, want_summaries=False)
-        return self._keep(p, rho, f == 0)
+        self._pack(p, rho, f == 0, layout, block, state, n)
 
-    def propose(self, model, seed, gen, first, count, theta_prev, cum_prev, chol, observed, eps):
+    def propose_round(self, model, seed, gen, first, count, theta_prev, cum_prev, chol, observed, eps,
+                      layout, block, state, n):
+        if count == 0 or int(state[0]) >= n:         # the gate of the propose kernel
+            return self._pack(np.zeros((0, 3)), np.zeros(0), np.zeros(0, bool), layout, block, state, n)
         th, rho, flag = self.o.abcsmc_propose(model, seed, gen, first, count, theta_prev.numpy(),
                                               cum_prev.numpy(), chol, observed, eps)
-        return self._keep(th, rho, flag == 1)
+        self._pack(th, rho, flag == 1, layout, block, state, n)
+
+    def append_round(self, blocks, world, layout, pop_theta, pop_rho, n, state):
+        from paper_1902_09046_b200 import _abi as A
+        got = int(state[0])
+        if got >= n:
+            return
+        idx, p, r, count = D.packed_views(blocks, layout, A.VXB_F64, pop_theta.shape[1], world)
+        total = 0
+        for q in range(world):
+            c = min(int(count[q]), int(layout.cap))
+            take = max(0, min(c, n - (got + total)))
+            pop_theta[got + total:got + total + take] = p[q, :take]
+            pop_rho[got + total:got + total + take] = r[q, :take]
+            total += c
+        state[1] += total
+        state[2] += 1
+        state[0] = min(n, got + total)
 
     def weights(self, theta_new, theta_prev, w_prev, chol, rng=0):
+        if theta_new.shape[0] == 0:
+            return torch.zeros(0, dtype=torch.float64)
         return torch.from_numpy(self.o.abcsmc_weights(theta_new.numpy(), theta_prev.numpy(),
                                                       w_prev.numpy(), chol))
 
@@ -181,7 +215,10 @@ class OracleStages:
         return torch.tensor([self.o.canon_sum(v[i:i + D.CHUNK]) for i in range(0, v.size, D.CHUNK)],
                             dtype=torch.float64)
 
-    def normalise(self, w_raw, total):
+    def normalise_by_totals(self, w_raw, totals):
+        total = 0.0
+        for v in totals.tolist():  # chunk totals, left to right
+            total += v
         return torch.from_numpy(w_raw.numpy() / total)
 
     def make_kernel(self, cov, scale, jitter):
@@ -209,11 +246,13 @@ def _smc_worker(rank, world, port, obs, out_dir):
 
 
 @pytest.mark.timeout(600)
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_sharded_abcsmc_equals_single_run(tmp_path, oracle, world):
-    """Proposals and new particles sharded over ranks; accepted rows all-gathered,
-    chunk totals of the weights all-reduced: bit-identical to the one-process run
-    (oracle.abcsmc_run) for every world size."""
+    """Proposals and new particles sharded over ranks; the packed blocks of accepted
+    rows all-gathered once per round (rounds issued ahead of the host, state on the
+    "device"), chunk totals of the weights all-reduced: bit-identical to the
+    one-process run (oracle.abcsmc_run) for every world size.  With 4 ranks the 700
+    particles make 3 canonical chunks: one rank owns an EMPTY weight shard."""
     m, cfg = smc_case()
     obs = oracle.simulate_at(m, [0.5, 100.0, 0.05], 5, 0, 0)
     want = oracle.abcsmc_run(m, cfg, obs)
