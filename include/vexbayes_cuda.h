@@ -149,6 +149,14 @@ int vxb_device_alloc(vxb_ctx* ctx, size_t bytes, void** out);
 int vxb_device_free(vxb_ctx* ctx, void* p);
 int vxb_copy(vxb_ctx* ctx, void* dst, const void* src, size_t bytes); /* any direction */
 
+/* Guard mode (diagnostics; environment VXB_GUARD=1 when vxb_init runs): every
+ * library-owned device allocation (staging, scratch, arenas) is bracketed by 256-byte
+ * canary zones that are verified when it is released; a violation prints a line
+ * "vxb guard: ..." on stderr and is counted.  *violations = the count so far.
+ * selftest != 0: first provoke one violation (a kernel writes one byte past a
+ * scratch buffer); *detected = 1 if the guard saw it (it is not counted). */
+int vxb_guard_report(vxb_ctx* ctx, int selftest, unsigned long long* violations, int* detected);
+
 /* Roofline denominator: measured throughput (TFLOP/s, FMA = 2 flops) of a
  * dependency-free FMA chain kernel in the given precision on this GPU, timed
  * with events over `iters` iterations per thread.  Diagnostics only. */

@@ -166,6 +166,8 @@ extern "C" int vxb_init(vxb_ctx** out, int device) {
         VXB_CUDA(cudaMemPoolCreate(&ctx->pool, &props));
         uint64_t threshold = ~0ull;
         VXB_CUDA(cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+        const char* guard = getenv("VXB_GUARD");
+        ctx->guard = guard && *guard && *guard != '0';
         double table[2 * kFastTableSize];
         build_fast_log_table(table);
         VXB_CUDA(cudaMalloc(&ctx->log_table, sizeof(table)));
@@ -183,11 +185,44 @@ extern "C" void vxb_shutdown(vxb_ctx* ctx) {
         cudaEventDestroy(std::get<2>(t));
     }
     for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
+    cudaFree(ctx->log_table);
+    for (int k = 0; k < 4; ++k) {
+        if (!ctx->arena[k]) continue;
+        if (ctx->guard)
+            guard_release(ctx, ctx->arena[k], ctx->arena_bytes[k], false, "arena");
+        else
+            cudaFree(ctx->arena[k]);
+    }
+    if (ctx->guard)
+        std::fprintf(stderr, "vxb guard: %llu violation(s) in this context\n", ctx->guard_violations);
     cudaStreamDestroy(ctx->stream);
     if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
-    cudaFree(ctx->log_table);
-    for (void* a : ctx->arena) cudaFree(a);
     delete ctx;
+}
+
+// guard mode (VXB_GUARD=1): the number of canary violations seen so far in this
+// context; with selftest != 0 first provokes one (a kernel writes one byte past a
+// 100-byte scratch buffer) and reports through *detected whether the guard saw it.
+__global__ void guard_poke_kernel(unsigned char* p, size_t offset) { p[offset] = 0x3C; }
+extern "C" int vxb_guard_report(vxb_ctx* ctx, int selftest, unsigned long long* violations,
+                                int* detected) {
+    return guarded([&] {
+        use(ctx);
+        require(violations != nullptr, "invalid-argument", "null output");
+        if (selftest) {
+            require(ctx->guard && detected, "invalid-argument",
+                    "the self-test needs guard mode (VXB_GUARD=1 at vxb_init)");
+            const unsigned long long before = ctx->guard_violations;
+            {
+                Scratch buf(ctx, 100);
+                guard_poke_kernel<<<1, 1, 0, ctx->stream>>>(buf.as<unsigned char>(), 100);
+                check_launch("guard_poke_kernel");
+            }
+            *detected = ctx->guard_violations == before + 1;
+            ctx->guard_violations = before;  // the provoked one does not count
+        }
+        *violations = ctx->guard_violations;
+    });
 }
 
 extern "C" int vxb_device_info(vxb_ctx* ctx, vxb_device_props* out) {

@@ -67,6 +67,12 @@ struct vxb_ctx {
     // calls so that the steady state performs no allocation at all)
     void* arena[4] = {nullptr, nullptr, nullptr, nullptr};
     size_t arena_bytes[4] = {0, 0, 0, 0};
+    // guard mode (environment VXB_GUARD=1 at vxb_init; diagnostics, slow): every
+    // library-owned device allocation is bracketed by canary zones that are verified
+    // when it is released -- the library's own out-of-bounds-write check, for pools
+    // where compute-sanitizer is not available
+    bool guard = false;
+    unsigned long long guard_violations = 0;
 };
 
 namespace vxb {
@@ -86,6 +92,44 @@ inline bool is_device_pointer(const void* p) {
     return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
 }
 
+// ---- guard mode: canaries around library-owned device allocations
+constexpr size_t kGuardBytes = 256;
+constexpr int kGuardPattern = 0xA5;
+inline void* guard_alloc(vxb_ctx* ctx, size_t bytes, bool pooled) {
+    char* raw = nullptr;
+    const size_t total = bytes + 2 * kGuardBytes;
+    if (pooled)
+        VXB_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&raw), total, ctx->pool, ctx->stream));
+    else
+        VXB_CUDA(cudaMalloc(reinterpret_cast<void**>(&raw), total));
+    VXB_CUDA(cudaMemsetAsync(raw, kGuardPattern, kGuardBytes, ctx->stream));
+    VXB_CUDA(cudaMemsetAsync(raw + kGuardBytes + bytes, kGuardPattern, kGuardBytes, ctx->stream));
+    return raw + kGuardBytes;
+}
+// verifies both canaries (synchronises) and releases the allocation
+inline void guard_release(vxb_ctx* ctx, void* p, size_t bytes, bool pooled, const char* what) {
+    char* raw = static_cast<char*>(p) - kGuardBytes;
+    unsigned char h[2 * kGuardBytes];
+    cudaMemcpyAsync(h, raw, kGuardBytes, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaMemcpyAsync(h + kGuardBytes, raw + kGuardBytes + bytes, kGuardBytes, cudaMemcpyDeviceToHost,
+                    ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    size_t before = 0, after = 0;
+    for (size_t i = 0; i < kGuardBytes; ++i) {
+        before += h[i] != kGuardPattern;
+        after += h[kGuardBytes + i] != kGuardPattern;
+    }
+    if (before || after) {
+        ++ctx->guard_violations;
+        std::fprintf(stderr, "vxb guard: out-of-bounds write on a %zu-byte %s buffer (%zu bytes before, %zu after)\n",
+                     bytes, what, before, after);
+    }
+    if (pooled)
+        cudaFreeAsync(raw, ctx->stream);
+    else
+        cudaFree(raw);
+}
+
 // A device view of a caller buffer.  Device pointers pass through; host
 // pointers are staged through stream-ordered scratch (input: copied in on
 // construction; output: copied back by finish()).
@@ -100,14 +144,21 @@ public:
             return;
         }
         owned_ = true;
-        VXB_CUDA(cudaMallocFromPoolAsync(&dev_, bytes, ctx->pool, ctx->stream));
+        if (ctx->guard)
+            dev_ = guard_alloc(ctx, bytes, true);
+        else
+            VXB_CUDA(cudaMallocFromPoolAsync(&dev_, bytes, ctx->pool, ctx->stream));
         if (is_input)
             VXB_CUDA(cudaMemcpyAsync(dev_, user, bytes, cudaMemcpyHostToDevice, ctx->stream));
     }
     Staged(const Staged&) = delete;
     Staged& operator=(const Staged&) = delete;
     ~Staged() {
-        if (owned_ && dev_) cudaFreeAsync(dev_, ctx_->stream);
+        if (!owned_ || !dev_) return;
+        if (ctx_->guard)
+            guard_release(ctx_, dev_, bytes_, true, "staged");
+        else
+            cudaFreeAsync(dev_, ctx_->stream);
     }
     // queue the device->host copy of an output (no-op for device buffers)
     void finish(size_t bytes = ~size_t(0)) {
@@ -134,6 +185,12 @@ private:
 // Persistent scratch slot `slot` of at least `bytes` (grow-only; the contents do
 // not survive a growth).  Stream-ordered use only.
 inline void* arena_get(vxb_ctx* ctx, int slot, size_t bytes) {
+    if (ctx->guard) {  // guard mode: a fresh bracketed allocation per request
+        if (ctx->arena[slot]) guard_release(ctx, ctx->arena[slot], ctx->arena_bytes[slot], false, "arena");
+        ctx->arena[slot] = guard_alloc(ctx, bytes, false);
+        ctx->arena_bytes[slot] = bytes;
+        return ctx->arena[slot];
+    }
     if (ctx->arena_bytes[slot] < bytes) {
         VXB_CUDA(cudaStreamSynchronize(ctx->stream));
         if (ctx->arena[slot]) VXB_CUDA(cudaFree(ctx->arena[slot]));
@@ -148,13 +205,21 @@ inline void* arena_get(vxb_ctx* ctx, int slot, size_t bytes) {
 // Stream-ordered scratch with RAII.
 class Scratch {
 public:
-    Scratch(vxb_ctx* ctx, size_t bytes) : ctx_(ctx) {
-        if (bytes) VXB_CUDA(cudaMallocFromPoolAsync(&p_, bytes, ctx->pool, ctx->stream));
+    Scratch(vxb_ctx* ctx, size_t bytes) : ctx_(ctx), bytes_(bytes) {
+        if (!bytes) return;
+        if (ctx->guard)
+            p_ = guard_alloc(ctx, bytes, true);
+        else
+            VXB_CUDA(cudaMallocFromPoolAsync(&p_, bytes, ctx->pool, ctx->stream));
     }
     Scratch(const Scratch&) = delete;
     Scratch& operator=(const Scratch&) = delete;
     ~Scratch() {
-        if (p_) cudaFreeAsync(p_, ctx_->stream);
+        if (!p_) return;
+        if (ctx_->guard)
+            guard_release(ctx_, p_, bytes_, true, "scratch");
+        else
+            cudaFreeAsync(p_, ctx_->stream);
     }
     template <class T>
     T* as() const {
@@ -164,6 +229,7 @@ public:
 private:
     vxb_ctx* ctx_;
     void* p_ = nullptr;
+    size_t bytes_ = 0;
 };
 
 // Counts a launch of family `kind`; with profiling on, brackets it by events.

@@ -324,6 +324,13 @@ class Context:
                                           C.byref(ms)))
         return tf.value, ms.value
 
+    def guard_report(self, selftest=False):
+        """Guard mode (VXB_GUARD=1): (violations so far, self-test detected or None)."""
+        v, d = C.c_ulonglong(), C.c_int(-1)
+        self._check(self.lib.vxb_guard_report(self.handle, i32(1 if selftest else 0), C.byref(v),
+                                              C.byref(d)))
+        return v.value, (bool(d.value) if selftest else None)
+
     def device_alloc(self, nbytes):
         out = P()
         self._check(self.lib.vxb_device_alloc(self.handle, C.c_size_t(nbytes), C.byref(out)))

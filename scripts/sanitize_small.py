@@ -3,6 +3,7 @@ for compute-sanitizer (ONE tool per gpurun call, profiling guide):
 
     compute-sanitizer --tool memcheck  python scripts/sanitize_small.py
     compute-sanitizer --tool racecheck python scripts/sanitize_small.py
+    VXB_GUARD=1 python scripts/sanitize_small.py    # the library's own canary check
 
 Covers vxb_select.cu (radix_hist / pick, accept_count / scan_blocks / accept_write),
 vxb_smc.cu (canonical reductions, sequential exp-sum, resample, pack / append rounds,
@@ -72,5 +73,7 @@ print("esjd", ctx.smc_bioassay_ensemble(M.DEFAULT_DOSE, M.DEFAULT_GROUP_SIZE, [0
 tbm = M.tb_model(10, 3.0, 300.0)
 tb_obs = ctx.simulate_at(M.tb_model(10, 3.0, 300.0, attempts=64), M.TB_TRUE_THETA, lib.derive_seed(1337, [91]), 0, 0)
 print("tb", ctx.abc_prior_predictive_host(tbm, M.keying(1337), 300, 0, 300, tb_obs)[2][:2])
+if os.environ.get("VXB_GUARD"):
+    print("guard", ctx.guard_report(selftest=True), ctx.guard_report())
 ctx.close()
 print("sanitize_small done")
