@@ -184,6 +184,17 @@ int vxb_rng_fill_gaussian(vxb_ctx* ctx, uint64_t seed, uint32_t stream_id, uint6
  * -> out[r*per_row + j]; element type by precision.  For statistical validation. */
 int vxb_rng_fill_gaussian_fast(vxb_ctx* ctx, int precision, uint64_t seed, uint64_t first_row,
                                uint64_t rows, uint32_t per_row, void* out);
+/* Statistics of the same normals over rows x per_row samples with only counters
+ * leaving the GPU (1e10+ samples per call): tail_counts[k] = #{|z| > thresholds[k]}
+ * (at most 8 thresholds); moments[0..8] = n, sum z, sum z^2, sum z^3, sum z^4, max |z|,
+ * and for VXB_F32 the error of the MUFU evaluation against a double-precision
+ * evaluation of the same uniforms: max |z32 - z64|, the same over |z64| > 4, and
+ * sum (z32 - z64)^2.
+ * The fp32 generator's radius uniform has 23 bits, refined by 12 more below 2^-15
+ * (see csrc/vxb_rng.cuh): |z| reaches 7.06 sigma; the fp64 generator's has 52 bits. */
+int vxb_rng_fast_stats(vxb_ctx* ctx, int precision, uint64_t seed, uint64_t first_row,
+                       uint64_t rows, uint32_t per_row, const double* thresholds,
+                       uint32_t n_thresholds, uint64_t* tail_counts, double* moments);
 /* Device evaluation of the fastmath functions (fastmath.hpp:23-128), for
  * parity tests: fn 0 log2_pos, 1 ln_pos, 2 exp2_clamped, 3 sinpi, 4 cospi,
  * 5 pow_pos (x = base, y = exponent; y ignored otherwise); and of the

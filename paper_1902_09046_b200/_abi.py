@@ -106,5 +106,5 @@ EXPORTED_SYMBOLS = (
     "vxb_multi_init", "vxb_multi_shutdown", "vxb_multi_size", "vxb_multi_ctx", "vxb_multi_comm",
     "vxb_multi_abc_prior_predictive", "vxb_multi_abc_reject", "vxb_multi_ppp_pvalues",
     "vxb_multi_mlmc_tauleap", "vxb_abcsmc_pack_round", "vxb_abcsmc_append_round",
-    "vxb_normalise_by_chunk_totals", "vxb_guard_report",
+    "vxb_normalise_by_chunk_totals", "vxb_guard_report", "vxb_rng_fast_stats",
 )

@@ -499,6 +499,152 @@ extern "C" int vxb_abc_reject(vxb_ctx* ctx, const vxb_model* model, const vxb_ke
     });
 }
 
+// Device-side statistics of the throughput generator over rows x per_row normals,
+// nothing but counters leaves the GPU (1e10+ samples in milliseconds): tail counts
+// |z| > t_k, power sums, the largest |z|, and for fp32 the error of the MUFU
+// evaluation against a double-precision evaluation of the SAME uniforms.
+struct FastStats {
+    unsigned long long tail[8];
+    unsigned long long n;
+    double sum[4];      // z, z^2, z^3, z^4
+    double max_abs;
+    double err_max;     // fp32: max |z32 - z64|
+    double err_max_tail;  // ... over |z64| > 4
+    double err_sq;      // sum (z32 - z64)^2
+};
+template <class Real>
+__global__ void __launch_bounds__(256) fast_stats_kernel(FastKeys fk, const double2* table,
+                                                         uint64_t first, uint64_t rows,
+                                                         uint32_t per_row, const double* thr,
+                                                         uint32_t n_thr, FastStats* out) {
+    __shared__ double2 s_tab[sizeof(Real) == 8 ? kFastTableSize : 1];
+    if (sizeof(Real) == 8) {
+        for (int i = threadIdx.x; i < kFastTableSize; i += 256) s_tab[i] = table[i];
+        __syncthreads();
+    }
+    constexpr uint32_t kB = sizeof(Real) == 8 ? 8 : 16;
+    const uint32_t q = blockIdx.y * 256 + threadIdx.x;
+    const bool live = q * kB < per_row;
+    double t[8];
+    for (uint32_t k = 0; k < 8; ++k) t[k] = k < n_thr ? thr[k] : 1e300;
+    unsigned long long tail[8] = {0, 0, 0, 0, 0, 0, 0, 0}, n = 0;
+    double s1 = 0, s2 = 0, s3 = 0, s4 = 0, mx = 0, emax = 0, etail = 0, esq = 0;
+    if (live)
+        for (uint64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+            const uint64_t row = first + r;
+            const uint32_t rl = static_cast<uint32_t>(row), rh = static_cast<uint32_t>(row >> 32);
+            const Words32 u = philox4x32(fk, 3 * q, kDomNoise, rl, rh);
+            const Words32 v = philox4x32(fk, 3 * q + 1, kDomNoise, rl, rh);
+            const Words32 w = philox4x32(fk, 3 * q + 2, kDomNoise, rl, rh);
+            Real z[kB];
+            double ze[kB];
+            if constexpr (sizeof(Real) == 8) {
+                fast_box_muller_x4(u, v, w, s_tab, z);
+            } else {
+                box_muller_f32_x8(u, v, w, z);
+                uint32_t m1[8], m2[8];
+                f32_batch_fields(u, v, w, m1, m2);
+                for (int k = 0; k < 8; ++k) {  // the same uniforms, evaluated in fp64
+                    const float u1 = m1[k] >= kF32TailFrom ? f32_u1_tail(m1[k], f32_batch_spare(u, v, w, k))
+                                                           : f32_u1(m1[k]);
+                    const double rad = sqrt(-2.0 * log(static_cast<double>(u1)));
+                    const double ang = static_cast<double>(__uint_as_float(0x3F800000u | m2[k])) *
+                                           6.283185307179586476925 - 9.424777960769379715;
+                    ze[2 * k] = rad * cos(ang);
+                    ze[2 * k + 1] = rad * sin(ang);
+                }
+            }
+            const uint32_t valid = min(kB, per_row - q * kB);
+            for (uint32_t e = 0; e < valid; ++e) {
+                const double x = static_cast<double>(z[e]), a = fabs(x);
+                ++n;
+                s1 += x;
+                s2 += x * x;
+                s3 += x * x * x;
+                s4 += x * x * x * x;
+                mx = fmax(mx, a);
+                for (uint32_t k = 0; k < 8; ++k) tail[k] += a > t[k];
+                if constexpr (sizeof(Real) == 4) {
+                    const double d = fabs(x - ze[e]);
+                    emax = fmax(emax, d);
+                    if (fabs(ze[e]) > 4.0) etail = fmax(etail, d);
+                    esq += d * d;
+                }
+            }
+        }
+    // warp reduction, then one atomic per warp and field
+    for (int o = 16; o; o >>= 1) {
+        for (int k = 0; k < 8; ++k) tail[k] += __shfl_down_sync(0xffffffffu, tail[k], o);
+        n += __shfl_down_sync(0xffffffffu, n, o);
+        s1 += __shfl_down_sync(0xffffffffu, s1, o);
+        s2 += __shfl_down_sync(0xffffffffu, s2, o);
+        s3 += __shfl_down_sync(0xffffffffu, s3, o);
+        s4 += __shfl_down_sync(0xffffffffu, s4, o);
+        esq += __shfl_down_sync(0xffffffffu, esq, o);
+        mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+        emax = fmax(emax, __shfl_down_sync(0xffffffffu, emax, o));
+        etail = fmax(etail, __shfl_down_sync(0xffffffffu, etail, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        for (int k = 0; k < 8; ++k)
+            if (tail[k]) atomicAdd(&out->tail[k], tail[k]);
+        atomicAdd(&out->n, n);
+        atomicAdd(&out->sum[0], s1);
+        atomicAdd(&out->sum[1], s2);
+        atomicAdd(&out->sum[2], s3);
+        atomicAdd(&out->sum[3], s4);
+        atomicAdd(&out->err_sq, esq);
+        // non-negative doubles order like their bit patterns
+        atomicMax(reinterpret_cast<unsigned long long*>(&out->max_abs), __double_as_longlong(mx));
+        atomicMax(reinterpret_cast<unsigned long long*>(&out->err_max), __double_as_longlong(emax));
+        atomicMax(reinterpret_cast<unsigned long long*>(&out->err_max_tail), __double_as_longlong(etail));
+    }
+}
+
+extern "C" int vxb_rng_fast_stats(vxb_ctx* ctx, int precision, uint64_t seed, uint64_t first_row,
+                                  uint64_t rows, uint32_t per_row, const double* thresholds,
+                                  uint32_t n_thresholds, uint64_t* tail_counts, double* moments) {
+    return guarded([&] {
+        use(ctx);
+        require(precision == VXB_F64 || precision == VXB_F32, "invalid-argument", "unknown precision");
+        require(n_thresholds <= 8 && (n_thresholds == 0 || (thresholds && tail_counts)) && moments,
+                "invalid-argument", "at most 8 thresholds; null argument");
+        require(rows >= 1 && per_row >= 1, "invalid-shape", "empty sample");
+        Scratch d_thr(ctx, 8 * sizeof(double)), d_out(ctx, sizeof(FastStats));
+        double h_thr[8] = {0};
+        for (uint32_t k = 0; k < n_thresholds; ++k) h_thr[k] = thresholds[k];
+        VXB_CUDA(cudaMemcpyAsync(d_thr.as<void>(), h_thr, sizeof(h_thr), cudaMemcpyHostToDevice, ctx->stream));
+        VXB_CUDA(cudaMemsetAsync(d_out.as<void>(), 0, sizeof(FastStats), ctx->stream));
+        const FastKeys fk = make_fast_keys(splitmix64(seed));
+        {
+            LaunchScope scope(ctx, VXB_K_RNGFILL);
+            const uint32_t per_batch = precision == VXB_F32 ? 16 : 8;
+            const uint32_t chunks = ((per_row + per_batch - 1) / per_batch + 255) / 256;
+            require(chunks <= 65535, "invalid-shape", "too many values per row");
+            const dim3 grid(static_cast<unsigned>(std::min<uint64_t>(rows, 148u * 64u)), chunks);
+            if (precision == VXB_F32)
+                fast_stats_kernel<float><<<grid, 256, 0, ctx->stream>>>(
+                    fk, ctx->log_table, first_row, rows, per_row, d_thr.as<double>(), n_thresholds,
+                    d_out.as<FastStats>());
+            else
+                fast_stats_kernel<double><<<grid, 256, 0, ctx->stream>>>(
+                    fk, ctx->log_table, first_row, rows, per_row, d_thr.as<double>(), n_thresholds,
+                    d_out.as<FastStats>());
+            check_launch("fast_stats_kernel");
+        }
+        FastStats h;
+        VXB_CUDA(cudaMemcpyAsync(&h, d_out.as<void>(), sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+        VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (uint32_t k = 0; k < n_thresholds; ++k) tail_counts[k] = h.tail[k];
+        moments[0] = static_cast<double>(h.n);
+        for (int k = 0; k < 4; ++k) moments[1 + k] = h.sum[k];
+        moments[5] = h.max_abs;
+        moments[6] = h.err_max;
+        moments[7] = h.err_max_tail;
+        moments[8] = h.err_sq;
+    });
+}
+
 extern "C" int vxb_rng_fill_gaussian_fast(vxb_ctx* ctx, int precision, uint64_t seed,
                                           uint64_t first_row, uint64_t rows, uint32_t per_row,
                                           void* out) {

@@ -228,8 +228,12 @@ __device__ __forceinline__ Real logistic_path(const LogisticModel& m, const doub
         }
     };
     if (stride % kB == 0 && steps == stride * m.n_obs) {
-        // regular grid (the BASELINE configs): whole batches between observations,
-        // no per-step bookkeeping
+        // observation stride a multiple of the batch (e.g. the exact instance, batch 2,
+        // on the BASELINE grid of 100): whole batches between observations, no per-step
+        // bookkeeping.  The throughput instances on the BASELINE grid (100 = 12 x 8 + 4 =
+        // 6 x 16 + 4) take the general loop below -- measured on B200 it is no slower
+        // (fp64: 70.8 ms per 2e7 rows at stride 100 against 71.9-72.3 ms at strides 80 /
+        // 200 / 400, which come through here; profiles/r2_stride_probe.json)
         const uint32_t per = stride / kB;
         for (uint32_t k = 0; k < m.n_obs; ++k) {
             for (uint32_t i = 0; i < per; ++i) {

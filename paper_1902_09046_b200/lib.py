@@ -370,6 +370,19 @@ class Context:
                                                         _ptr(out)))
         return out
 
+    def rng_fast_stats(self, precision, seed, first_row, rows, per_row, thresholds=()):
+        """Device-side tail counts / moments / fp32 MUFU error of the throughput generator."""
+        thr = np.ascontiguousarray(thresholds, dtype=np.float64)
+        tails = np.zeros(max(thr.size, 1), dtype=np.uint64)
+        mom = np.zeros(9)
+        self._check(self.lib.vxb_rng_fast_stats(self.handle, i32(precision), u64(seed), u64(first_row),
+                                                u64(rows), u32(per_row), _ptr(thr), u32(thr.size),
+                                                _ptr(tails), _ptr(mom)))
+        n = mom[0]
+        return dict(n=int(n), tails=tails[:thr.size], mean=mom[1] / n, var=mom[2] / n - (mom[1] / n) ** 2,
+                    skew=mom[3] / n, kurt=mom[4] / n, max_abs=mom[5], err_max=mom[6],
+                    err_max_tail=mom[7], err_rms=float(np.sqrt(mom[8] / n)))
+
     def fastmath(self, fn, x, y=None):
         x = np.ascontiguousarray(x, dtype=np.float64)
         y = np.ascontiguousarray(y, dtype=np.float64) if y is not None else None
