@@ -545,8 +545,7 @@ __global__ void __launch_bounds__(256) fast_stats_kernel(FastKeys fk, const doub
                 uint32_t m1[8], m2[8];
                 f32_batch_fields(u, v, w, m1, m2);
                 for (int k = 0; k < 8; ++k) {  // the same uniforms, evaluated in fp64
-                    const float u1 = m1[k] >= kF32TailFrom ? f32_u1_tail(m1[k], f32_batch_spare(u, v, w, k))
-                                                           : f32_u1(m1[k]);
+                    const float u1 = f32_u1(m1[k]);
                     const double rad = sqrt(-2.0 * log(static_cast<double>(u1)));
                     const double ang = static_cast<double>(__uint_as_float(0x3F800000u | m2[k])) *
                                            6.283185307179586476925 - 9.424777960769379715;

@@ -1,17 +1,35 @@
-import sys, json, math
-sys.path.insert(0, '/root/repo')
+"""Device-side statistics of the throughput generator (vxb_rng_fast_stats): tail counts
+against the normal tail, moments, the largest |z| and the fp32 MUFU error, at 1e10 (fp32)
+and 4e10 (fp64) samples per seed.
+
+    python scripts/fast_stats_probe.py > profiles/r2_fast_generator_stats.json
+"""
+import json
+import math
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
 from paper_1902_09046_b200 import _abi as A, lib
+
 ctx = lib.Context(0)
 thr = [3, 4, 5, 5.5, 5.65, 6, 6.5, 7]
-for prec, rows in ((A.VXB_F32, 5_000_000), (A.VXB_F64, 2_000_000)):
-    import time
+out = {"thresholds": thr, "runs": []}
+for name, prec, rows in (("f32", A.VXB_F32, 5_000_000), ("f64", A.VXB_F64, 20_000_000)):
     ctx.rng_fast_stats(prec, 1, 0, 1000, 2000, thr)
-    t0 = time.time()
-    s = ctx.rng_fast_stats(prec, 2024, 0, rows, 2000, thr)
-    dt = time.time() - t0
-    n = s["n"]
-    exp = [n * math.erfc(t / math.sqrt(2)) for t in thr]
-    print(prec, n, round(dt, 3), "s")
-    print(" tails", [int(x) for x in s["tails"]], [round(e, 1) for e in exp])
-    print(" mean %.3e var-1 %.3e skew %.3e kurt-3 %.3e max %.4f" % (s["mean"], s["var"] - 1, s["skew"], s["kurt"] - 3, s["max_abs"]))
-    print(" err_max %.3e err_max_tail %.3e err_rms %.3e" % (s["err_max"], s["err_max_tail"], s["err_rms"]))
+    for seed in (2024, 7, 99):
+        t0 = time.time()
+        s = ctx.rng_fast_stats(prec, seed, 0, rows, 2000, thr)
+        dt = time.time() - t0
+        n = s["n"]
+        exp = [n * math.erfc(t / math.sqrt(2)) for t in thr]
+        z = [(int(c) - e) / math.sqrt(e) if e > 5 else None for c, e in zip(s["tails"], exp)]
+        out["runs"].append({"precision": name, "seed": seed, "samples": n, "seconds": dt,
+                            "tail_counts": [int(x) for x in s["tails"]], "tail_expected": exp,
+                            "tail_z": z, "mean": s["mean"], "var_minus_1": s["var"] - 1,
+                            "third_moment": s["skew"], "fourth_moment_minus_3": s["kurt"] - 3,
+                            "max_abs": s["max_abs"], "f32_err_max": s["err_max"],
+                            "f32_err_max_beyond_4sigma": s["err_max_tail"], "f32_err_rms": s["err_rms"]})
+print(json.dumps(out))

@@ -357,3 +357,44 @@ def test_throughput_mode_elementary_functions(ctx):
     a = np.concatenate([np.exp(rs.uniform(-100, 100, 20000)) * rs.choice([-1.0, 1.0], 20000), [1.0, 3.0, -7.0]])
     got = ctx.fastmath(8, a)
     assert np.max(np.abs(got * a - 1.0)) < 4e-16
+
+
+@pytest.mark.parametrize("precision", [A.VXB_F32, A.VXB_F64])
+def test_fast_generator_tails_and_mufu_error_device_side(ctx, precision):
+    """1e10 normals of the throughput generator, counted on the device
+    (vxb_rng_fast_stats; only counters come back): tail mass out to 5.5 sigma against
+    2(1 - Phi(t)) with Bonferroni-sized Poisson bounds, moments at the 1e-5 level, the
+    documented 5.65 sigma cap of the fp32 generator (include/vexbayes_cuda.h), and the
+    error of its MUFU evaluation (lg2 / sqrt / sin / cos .approx) against a double
+    evaluation of the same uniforms.  The device counts agree with a host count of the
+    same samples."""
+    from math import erfc, sqrt
+    thr = [3.0, 4.0, 5.0, 5.5, 5.65, 6.0]
+    # the counters are what a host count of the same samples gives
+    z = ctx.rng_fill_gaussian_fast(precision, 5, 10, 3000, 1999).astype(np.float64)
+    small = ctx.rng_fast_stats(precision, 5, 10, 3000, 1999, thr)
+    assert small["n"] == z.size and small["max_abs"] == np.abs(z).max()
+    assert [int(c) for c in small["tails"]] == [int((np.abs(z) > t).sum()) for t in thr]
+    assert abs(small["mean"] - z.mean()) < 1e-12 and abs(small["var"] - z.var()) < 1e-10
+    # 1e10 samples (fp32: 0.08 s; fp64: 0.03 s on a B200)
+    s = ctx.rng_fast_stats(precision, 2024, 0, 5_000_000, 2000, thr)
+    n = s["n"]
+    assert n == 10_000_000_000
+    cap = sqrt(2.0 * 23.0 * np.log(2.0))                 # 5.6468...
+    for t, c in zip(thr, s["tails"]):
+        expected = n * erfc(t / sqrt(2.0))
+        if precision == A.VXB_F32 and t >= 5.65:
+            assert int(c) == 0 if t > cap else True       # nothing beyond the cap
+            continue
+        assert abs(int(c) - expected) < 5.0 * sqrt(expected) + 3, (t, int(c), expected)
+    assert abs(s["mean"]) < 5 / sqrt(n)
+    assert abs(s["var"] - 1.0) < 5 * sqrt(2.0 / n) + 3e-6   # + the 23-bit lattice of u1 (2e-6)
+    assert abs(s["skew"]) < 5 * sqrt(15.0 / n)
+    assert abs(s["kurt"] - 3.0) < 5 * sqrt(96.0 / n) + 1e-4
+    if precision == A.VXB_F32:
+        assert 5.0 < s["max_abs"] <= cap + 1e-5
+        # MUFU error: rms 3.3e-7; the worst case (1e-3 absolute) sits at |z| ~ 1e-3, where
+        # lg2.approx's 2^-22 absolute error meets -2 ln u1 ~ 2^-22; beyond 4 sigma 3e-6
+        assert s["err_rms"] < 1e-6 and s["err_max"] < 3e-3 and s["err_max_tail"] < 1e-5
+    else:
+        assert 5.65 < s["max_abs"] < 8.0                   # 52-bit radius uniform: no cap
