@@ -363,8 +363,9 @@ def test_throughput_mode_elementary_functions(ctx):
 def test_fast_generator_tails_and_mufu_error_device_side(ctx, precision):
     """1e10 normals of the throughput generator, counted on the device
     (vxb_rng_fast_stats; only counters come back): tail mass out to 5.5 sigma against
-    2(1 - Phi(t)) with Bonferroni-sized Poisson bounds, moments at the 1e-5 level, the
-    documented 5.65 sigma cap of the fp32 generator (include/vexbayes_cuda.h), and the
+    2(1 - Phi(t)) with Bonferroni-sized Poisson bounds (fp64 everywhere, fp32 up to 4
+    sigma), moments at the 1e-5 level, the documented far tail of the fp32 generator
+    (mass low beyond 5 sigma, nothing beyond 5.65; include/vexbayes_cuda.h), and the
     error of its MUFU evaluation (lg2 / sqrt / sin / cos .approx) against a double
     evaluation of the same uniforms.  The device counts agree with a host count of the
     same samples."""
@@ -383,8 +384,17 @@ def test_fast_generator_tails_and_mufu_error_device_side(ctx, precision):
     cap = sqrt(2.0 * 23.0 * np.log(2.0))                 # 5.6468...
     for t, c in zip(thr, s["tails"]):
         expected = n * erfc(t / sqrt(2.0))
-        if precision == A.VXB_F32 and t >= 5.65:
-            assert int(c) == 0 if t > cap else True       # nothing beyond the cap
+        if precision == A.VXB_F32 and t >= 5.0:
+            # the documented tail of the fp32 generator: u1 lives on a 2^-23 lattice whose
+            # points stand for the bucket below them, so beyond 5 sigma (u1 < 31 lattice
+            # steps) the mass comes out low -- measured -5% at 5 sigma, -37% at 5.5 sigma --
+            # and there is nothing beyond the cap
+            if t > cap:
+                assert int(c) == 0
+            elif t == 5.0:
+                assert 0.90 * expected < int(c) < 1.02 * expected, (int(c), expected)
+            else:
+                assert 0.45 * expected < int(c) < 1.02 * expected, (t, int(c), expected)
             continue
         assert abs(int(c) - expected) < 5.0 * sqrt(expected) + 3, (t, int(c), expected)
     assert abs(s["mean"]) < 5 / sqrt(n)
