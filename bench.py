@@ -171,14 +171,21 @@ class ClockSampler:
 
 
 def ncu_traffic(variant):
-    """DRAM bytes per launch of the dominant kernel from the committed ncu capture
-    (profiles/r1_traffic.json); the capture was taken at 2e6 rows per launch."""
+    """DRAM bytes per launch and the pipe utilisations of the dominant kernel from the
+    committed ncu capture (profiles/r2_traffic.json; taken at 2e6 rows per launch).  The
+    flop-convention `frac` prices a normal at the reference's 47 flop; the pipe numbers
+    say how busy the hardware actually was."""
     try:
-        t = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json")))
+        t = json.load(open(os.path.join(ROOT, "profiles", "r2_traffic.json")))
         k = t["kernels"][variant]
-        return {"traffic": k["dram_bytes"],
-                "traffic_note": f"ncu dram bytes per launch at {t['rows_per_profiled_launch']} rows "
-                                f"(algorithmic: {k['algorithmic_bytes']} B of rho, L2 resident)"}
+        out = {"traffic": k["dram_bytes"],
+               "traffic_note": f"ncu dram bytes per launch at {t['rows_per_profiled_launch']} rows "
+                               f"(algorithmic: {k['algorithmic_bytes']} B of rho, L2 resident)"}
+        for key in ("fp64_pipe_active_pct", "xu_pipe_pct", "issue_active_pct", "alu_pipe_pct",
+                    "fma_pipe_pct", "warps_active_pct"):
+            if key in k:
+                out[key.replace("_pct", "_ncu")] = k[key]
+        return out
     except (OSError, KeyError, ValueError):
         return {"traffic": None}
 
@@ -414,6 +421,12 @@ def main():
             sv = k * n_total / (ms_v * 1e-3)
             variants[name] = {"sims_per_s": sv, "ms_per_step": ms_v / k, "steps": k, "warmup": w,
                               "frac_of_nominal_peak": sv * FLOPS_PER_SIM / 1e12 / pk}
+        for name, v in variants.items():
+            # the hardware's own view next to the flop-convention fraction (ncu capture)
+            v.update({k: x for k, x in ncu_traffic(name).items() if k.endswith("_ncu")})
+            v["frac_note"] = ("algorithmic flops at the reference's price of 47 per N(0,1) "
+                              "(SURVEY.md 8d) over the nominal pipe peak; *_ncu = measured pipe "
+                              "utilisation of the same kernel")
         line["variants"] = variants
         if rank == 0 and world == 1:
             line["configs"] = all_configs(ctx, timed, obs, local)
