@@ -78,3 +78,70 @@ def test_config1_full_size_properties(ctx, config0, variant):
     assert n1 + n2 == k
     assert np.array_equal(np.concatenate([i1, i2]).astype(np.int64), i)
     assert np.array_equal(np.concatenate([r1, r2]).astype(np.float64), r)
+
+
+# ---------------------------------------------------------------------------
+# Throughput generator against the reference-exact streams at FULL size
+# (round-1 review: the GPU tests of these modes ran 2.5x smaller than BASELINE and
+# could not have seen the two anomalies of profiles/r1_all_configs_1gpu.json; the
+# many-seed record is profiles/r2_fastmode_stats.json)
+# ---------------------------------------------------------------------------
+def _mlmc(ctx, rng, paths, seed):
+    mc = A.vxb_mlmc_cfg()
+    mc.levels, mc.refine, mc.tau0, mc.t_end, mc.paths, mc.seed = 6, 4, 1.0, 30.0, paths, seed
+    return ctx.mlmc_tauleap(M.mm_tauleap_model(rng=rng), mc)
+
+
+@pytest.mark.timeout(600)
+def test_config4_full_size_generators_agree(ctx):
+    """6 levels x 1e6 paths, two seeds: the level means of the two generators are
+    independent estimates of the same quantities.  24 z-scores (2 seeds x 6 levels x
+    {mean, variance}) at a per-test level of 1e-4 (|z| < 3.89: Bonferroni 2.4e-3
+    overall), the pooled estimate at |z| < 3.3; the conservation law makes every Y an
+    integer, so the sums are exact."""
+    paths = 1_000_000
+    d_sum = v_sum = 0.0
+    for seed in (1337, 4337):
+        e, f = _mlmc(ctx, A.VXB_RNG_REF, paths, seed), _mlmc(ctx, A.VXB_RNG_FAST, paths, seed)
+        for l in range(6):
+            z = (f["level_mean"][l] - e["level_mean"][l]) / math.sqrt((f["level_var"][l] + e["level_var"][l]) / paths)
+            assert abs(z) < 3.89, (seed, l, z)
+            # variance of a sample variance ~ 2 var^2 / n for near-normal Y; levels >= 1 are
+            # heavy-tailed (mostly zeros), so compare on the log scale with a generous bound
+            assert abs(math.log(f["level_var"][l] / e["level_var"][l])) < 0.08, (seed, l)
+        d_sum += f["estimate"] - e["estimate"]
+        v_sum += f["std_error"] ** 2 + e["std_error"] ** 2
+        assert abs(e["estimate"] - 22.72) < 0.03 and abs(f["estimate"] - 22.72) < 0.03
+    assert abs(d_sum / math.sqrt(v_sum)) < 3.3
+
+
+@pytest.mark.timeout(900)
+def test_config3_full_size_generators_agree(ctx, golden):
+    """N = 1e5 x 10 generations in both modes, two seeds each: the epsilon schedules
+    agree to 2%, the final weighted means agree within Monte-Carlo error (Bonferroni over
+    3 coordinates x 2 seeds at 1e-3 each), weights are normalised, ESS in [1, N].  An ESS
+    dip is ONE dominant importance weight (any mode, profiles/r2_fastmode_stats.json):
+    removing the largest weight of the final population restores ESS > 0.6 N."""
+    obs = golden["logistic_observed"]
+    n = 100_000
+    cfg = A.vxb_abcsmc_cfg()
+    cfg.particles, cfg.generations, cfg.quantile, cfg.kernel_scale = n, 10, 0.5, 2.0
+    cfg.jitter, cfg.round_size, cfg.max_rounds = 1e-10, 0, 0
+    for seed in (1337, 5337):
+        cfg.seed = seed
+        out = {name: ctx.abcsmc_run(M.logistic_model(rng=rng), cfg, obs)
+               for name, rng in (("exact", A.VXB_RNG_REF), ("fast", A.VXB_RNG_FAST))}
+        for r in out.values():
+            assert abs(r["weight"].sum() - 1.0) < 1e-9 and (r["weight"] > 0).all()
+            assert ((r["ess"] >= 1.0) & (r["ess"] <= n + 1e-6)).all()
+            assert (np.diff(r["epsilon"][1:]) < 0).all()          # the schedule tightens
+            w = np.sort(r["weight"])[:-1]
+            w = w / w.sum()
+            assert 1.0 / (w ** 2).sum() > 0.6 * n
+        e, f = out["exact"], out["fast"]
+        assert np.abs(f["epsilon"][1:] / e["epsilon"][1:] - 1.0).max() < 0.02
+        for k in range(3):
+            se = math.sqrt(e["cov"][-1][k, k] / e["ess"][-1] + f["cov"][-1][k, k] / f["ess"][-1])
+            # the epsilon of the last generation differs slightly between the runs, which
+            # moves the posterior itself: allow that on top of the Monte-Carlo error
+            assert abs(f["mean"][-1][k] - e["mean"][-1][k]) < 3.5 * se + 0.01 * abs(e["mean"][-1][k]), (seed, k)
