@@ -611,6 +611,18 @@ int vxb_multi_ppp_pvalues(vxb_multi* multi, const vxb_model* model, const double
                           uint64_t seed, double ybar_obs, uint64_t* counts, double* pvalues);
 int vxb_multi_mlmc_tauleap(vxb_multi* multi, const vxb_model* model, const vxb_mlmc_cfg* cfg,
                            vxb_mlmc_out* out);
+/* Config 3 over several GPUs.  SPMD form (every rank calls it; comm == NULL: one rank)
+ * and the one-process form.  Same scheme and the same bits as vxb_abcsmc_run for any
+ * number of ranks: proposals of a round and new particles of a generation sharded by
+ * global index; per round ONE ncclAllGather of the packed accepted proposals, per
+ * generation one ncclAllGather of the unnormalised weights and one ncclAllReduce(SUM)
+ * of the chunk totals of the weight sum (exact: one non-zero contributor per entry);
+ * rounds issued ahead of the host, state on the device (vxb_abcsmc_append_round). */
+int vxb_sharded_abcsmc_run(vxb_ctx* ctx, vxb_comm* comm, const vxb_model* model,
+                           const vxb_abcsmc_cfg* cfg, const double* observed,
+                           vxb_abcsmc_out* out);
+int vxb_multi_abcsmc_run(vxb_multi* multi, const vxb_model* model, const vxb_abcsmc_cfg* cfg,
+                         const double* observed, vxb_abcsmc_out* out);
 
 #ifdef __cplusplus
 }

@@ -177,7 +177,10 @@ inline AbcSmcResult run_abc_smc(const ModelHooks& model, const AbcSmcConfig& cfg
     vxb_abcsmc_out out{r.particles.data(), r.weights.data(), r.discrepancies.data(),
                        r.epsilon.data(), r.ess.data(), r.accept_rate.data(), r.proposals.data(),
                        r.mean.data(), r.covariance.data()};
-    cuda::check(vxb_abcsmc_run(cuda::context(), model.device.get(), &c, observed.data(), &out));
+    // every GPU in use (cuda::set_devices): proposals and new particles sharded by global
+    // index, accepted proposals / weights gathered and the weight sum reduced over NCCL
+    // inside the library; the same bits as one GPU (vxb_abcsmc_run) for any device count
+    cuda::check(vxb_multi_abcsmc_run(cuda::multi(), model.device.get(), &c, observed.data(), &out));
     return r;
 }
 

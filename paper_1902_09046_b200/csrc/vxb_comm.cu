@@ -20,7 +20,7 @@
 
 #include <nccl.h>
 
-#include "vxb_common.cuh"
+#include "vxb_internal.cuh"
 
 namespace vxb {
 
@@ -90,7 +90,7 @@ static void nccl_check(ncclResult_t r, const char* what) {
 static uint64_t align16(uint64_t v) { return (v + 15) & ~uint64_t(15); }
 
 // partition(total, workers, 1) (blocked.cpp:34-63): range of worker `rank`
-static void shard_of(uint64_t total, uint64_t world, uint64_t rank, uint64_t* begin, uint64_t* end) {
+void shard_of(uint64_t total, uint64_t world, uint64_t rank, uint64_t* begin, uint64_t* end) {
     const uint64_t base = total / world, extra = total % world;
     *begin = rank * base + std::min(rank, extra);
     *end = *begin + base + (rank < extra ? 1 : 0);
@@ -108,6 +108,19 @@ struct vxb_multi {
     std::vector<vxb_ctx*> ctx;
     std::vector<vxb_comm*> comm;  // empty with one device
 };
+
+namespace vxb {
+int comm_rank(const vxb_comm* comm) { return comm ? comm->rank : 0; }
+int comm_size(const vxb_comm* comm) { return comm ? comm->size : 1; }
+void comm_allgather(vxb_comm* comm, const void* send, void* recv, size_t bytes) {
+    require(comm != nullptr, "invalid-argument", "null communicator");
+    VXB_NCCL(nccl().AllGather(send, recv, bytes, ncclUint8, comm->comm, comm->ctx->stream));
+}
+void comm_allreduce_sum_f64(vxb_comm* comm, double* buf, size_t count) {
+    require(comm != nullptr, "invalid-argument", "null communicator");
+    VXB_NCCL(nccl().AllReduce(buf, buf, count, ncclFloat64, ncclSum, comm->comm, comm->ctx->stream));
+}
+}  // namespace vxb
 
 using namespace vxb;
 
@@ -499,5 +512,20 @@ extern "C" int vxb_multi_mlmc_tauleap(vxb_multi* m, const vxb_model* model, cons
         }
         out->estimate = est;
         out->std_error = std::sqrt(var);
+    });
+}
+
+// ABC-SMC over all devices: every device runs the SPMD driver on its own host thread;
+// device 0's copy of the (replicated) result goes to the caller.
+extern "C" int vxb_multi_abcsmc_run(vxb_multi* m, const vxb_model* model, const vxb_abcsmc_cfg* cfg,
+                                    const double* observed, vxb_abcsmc_out* out) {
+    return guarded([&] {
+        require(m && model && cfg && observed && out, "invalid-argument", "null argument");
+        const int g = static_cast<int>(m->ctx.size());
+        fork_join(m, [&](int r) {
+            vxb_abcsmc_out none{};  // the other ranks compute the same numbers and drop them
+            abi(vxb_sharded_abcsmc_run(m->ctx[r], g > 1 ? m->comm[r] : nullptr, model, cfg, observed,
+                                       r == 0 ? out : &none));
+        });
     });
 }

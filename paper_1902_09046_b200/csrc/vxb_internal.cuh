@@ -36,4 +36,14 @@ uint64_t count_valid_any(vxb_ctx* ctx, int precision, const void* rho_dev,
 // type-7 quantile (numeric.cpp:20-36) of n device-resident values (all valid)
 double quantile_device(vxb_ctx* ctx, const double* values_dev, uint64_t n, double level);
 
+// vxb_comm.cu -- the communicator as the other translation units see it (comm may be
+// null: one rank).  The collectives are queued on the communicator's context stream
+// and raise vxb::Error on failure.
+int comm_rank(const vxb_comm* comm);
+int comm_size(const vxb_comm* comm);
+void comm_allgather(vxb_comm* comm, const void* send, void* recv, size_t bytes);
+void comm_allreduce_sum_f64(vxb_comm* comm, double* buf, size_t count);
+// partition(total, world, 1) (blocked.cpp:34-63): range of worker `rank`
+void shard_of(uint64_t total, uint64_t world, uint64_t rank, uint64_t* begin, uint64_t* end);
+
 }  // namespace vxb

@@ -1169,3 +1169,190 @@ extern "C" int vxb_abcsmc_run(vxb_ctx* ctx, const vxb_model* model, const vxb_ab
         VXB_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }
+
+// ---------------------------------------------------------------------------
+// ABC-SMC over several GPUs, SPMD: every rank calls this with its context and
+// communicator (comm == NULL: one rank).  The scheme and every number are those of
+// vxb_abcsmc_run -- the result is bit-identical for any number of ranks -- with the
+// proposals of a round and the new particles of a generation sharded by global index
+// (partition(., ranks, 1)):
+//   * per round ONE all-gather of each rank's packed block of accepted proposals
+//     (vxb_accept_layout), appended in rank order = ascending proposal index;
+//   * per generation one all-gather of the unnormalised weights (shards aligned to the
+//     256-row canonical chunks, padded to the largest) and one all-reduce(SUM) of the
+//     chunk totals (one non-zero contributor per entry: exact); the divisor is formed
+//     on the device, chunk totals left to right.
+// Rounds are issued ahead of the host's knowledge (device-resident state, gated
+// kernels); the host reads the 4-word state once per batch of rounds.  The previous
+// population is replicated; its statistics are recomputed on every rank.
+// The Python mirror of this loop is dist.sharded_abcsmc (gloo-testable).
+extern "C" int vxb_sharded_abcsmc_run(vxb_ctx* ctx, vxb_comm* comm, const vxb_model* model,
+                                      const vxb_abcsmc_cfg* cfg, const double* observed,
+                                      vxb_abcsmc_out* out) {
+    return guarded([&] {
+        use(ctx);
+        require(model && cfg && observed && out, "invalid-argument", "null argument");
+        require(model->precision == VXB_F64 &&
+                    (model->rng == VXB_RNG_REF || model->rng == VXB_RNG_FAST),
+                "invalid-argument", "ABC-SMC runs in fp64 (reference or throughput generator)");
+        const bool fast = model->rng == VXB_RNG_FAST;
+        const uint64_t n = cfg->particles;
+        const uint32_t d = 3;
+        require(n >= 2, "insufficient-data", "need at least two particles");
+        require(cfg->generations >= 1, "invalid-argument", "need at least one generation");
+        require(cfg->quantile > 0.0 && cfg->quantile <= 1.0, "invalid-argument",
+                "quantile must lie in (0, 1]");
+        const uint64_t round = cfg->round_size ? cfg->round_size : n;
+        const uint64_t max_rounds = cfg->max_rounds ? cfg->max_rounds : 1000;
+        const uint64_t world = comm_size(comm), rank = comm_rank(comm);
+        const uint64_t zero = 0;
+        const uint64_t seed0 = vxb_derive_seed(cfg->seed, &zero, 1);
+
+        // this rank's slice of a round and of the weights
+        uint64_t rb, re, cap_b, cap_e;
+        shard_of(round, world, rank, &rb, &re);
+        shard_of(round, world, 0, &cap_b, &cap_e);
+        const uint64_t slice = re - rb, cap = std::max<uint64_t>(1, cap_e - cap_b);
+        const uint64_t nc = n_chunks(n);
+        uint64_t cb, ce, c0b, c0e;
+        shard_of(nc, world, rank, &cb, &ce);
+        shard_of(nc, world, 0, &c0b, &c0e);
+        const uint64_t w_begin = std::min(n, cb * kChunk), w_end = std::min(n, ce * kChunk);
+        const uint64_t w_pad = std::max<uint64_t>(1, (c0e - c0b) * kChunk);
+
+        vxb_accept_layout lay;
+        require(vxb_accept_layout_of(VXB_F64, d, cap, &lay) == 0, "internal", vxb_last_error());
+        Scratch theta_a(ctx, n * d * 8), theta_b(ctx, n * d * 8), rho_a(ctx, n * 8), rho_b(ctx, n * 8);
+        Scratch w_a(ctx, n * 8), w_b(ctx, n * 8), cum(ctx, n * 8);
+        Scratch p_theta(ctx, cap * d * 8), p_rho(ctx, cap * 8), p_flag(ctx, cap);
+        Scratch block(ctx, lay.stride), blocks(ctx, world > 1 ? world * lay.stride : 0);
+        Scratch state(ctx, 4 * 8), d_chol(ctx, 9 * 8), totals(ctx, nc * 8);
+        Scratch w_send(ctx, world > 1 ? w_pad * 8 : 0), w_recv(ctx, world > 1 ? world * w_pad * 8 : 0);
+        VXB_CUDA(cudaMemsetAsync(block.as<void>(), 0, lay.stride, ctx->stream));
+        double* th[2] = {theta_a.as<double>(), theta_b.as<double>()};
+        double* rh[2] = {rho_a.as<double>(), rho_b.as<double>()};
+        double* ww[2] = {w_a.as<double>(), w_b.as<double>()};
+        const void* gathered = world > 1 ? blocks.as<void>() : block.as<void>();
+        auto* st = state.as<uint64_t>();
+
+        double rate = 1.0;
+        for (uint32_t g = 0; g < cfg->generations; ++g) {
+            const double* cur_theta = th[(g + 1) & 1];
+            const double* cur_w = ww[(g + 1) & 1];
+            const double* cur_rho = rh[(g + 1) & 1];
+            double* nxt_theta = th[g & 1];
+            double* nxt_w = ww[g & 1];
+            double* nxt_rho = rh[g & 1];
+            double eps = std::numeric_limits<double>::infinity();
+            double chol[9] = {0};
+            if (g >= 1) {
+                eps = quantile_device(ctx, cur_rho, n, cfg->quantile);
+                double mean[3], cov[9];
+                weighted_moments_device(ctx, cur_theta, cur_w, n, d, mean, cov);
+                make_kernel_host(cov, d, cfg->kernel_scale, cfg->jitter, chol);
+                canon_cumsum_device(ctx, cur_w, n, cum.as<double>());
+                VXB_CUDA(cudaMemcpyAsync(d_chol.as<void>(), chol, sizeof(chol), cudaMemcpyHostToDevice,
+                                         ctx->stream));
+            }
+            VXB_CUDA(cudaMemsetAsync(st, 0, 4 * 8, ctx->stream));
+            uint64_t issued = 0, h_state[4] = {0, 0, 0, 0};
+            while (h_state[0] < n && issued < max_rounds) {
+                // generation 0 accepts every non-failed row: no slack; later: what the
+                // estimated acceptance rate asks for, half as much again, plus one
+                const double need = static_cast<double>(n - h_state[0]) / (static_cast<double>(round) * rate);
+                uint64_t ahead = static_cast<uint64_t>(std::ceil(g == 0 ? need : 1.5 * need)) + (g == 0 ? 0 : 1);
+                ahead = std::max<uint64_t>(1, std::min(ahead, max_rounds - issued));
+                for (uint64_t t = issued; t < issued + ahead; ++t) {
+                    const uint64_t first = t * round + rb;
+                    if (g == 0) {
+                        if (slice) {
+                            vxb_keying key{VXB_KEY_PARTICLE, 1, 1, 0, seed0};
+                            require(vxb_abc_prior_predictive(ctx, model, &key, (t + 1) * round, first, slice,
+                                                             observed, p_theta.as<double>(), nullptr,
+                                                             p_rho.as<double>(), p_flag.as<uint8_t>(),
+                                                             nullptr) == 0,
+                                    "internal", vxb_last_error());
+                        }
+                    } else {
+                        propose_device(ctx, *model, cfg->seed, g, first, slice, n, cur_theta,
+                                       cum.as<double>(), chol, observed, eps, p_theta.as<double>(),
+                                       p_rho.as<double>(), p_flag.as<uint8_t>(), st, n);
+                    }
+                    require(vxb_abcsmc_pack_round(ctx, d, p_theta.as<double>(), p_rho.as<double>(),
+                                                  g == 0 ? p_flag.as<uint8_t>() : nullptr, slice, eps, &lay,
+                                                  block.as<void>(), st, n) == 0,
+                            "internal", vxb_last_error());
+                    if (world > 1) comm_allgather(comm, block.as<void>(), blocks.as<void>(), lay.stride);
+                    require(vxb_abcsmc_append_round(ctx, d, gathered, static_cast<uint32_t>(world), &lay,
+                                                    nxt_theta, nxt_rho, n, st) == 0,
+                            "internal", vxb_last_error());
+                }
+                issued += ahead;
+                VXB_CUDA(cudaMemcpyAsync(h_state, st, sizeof(h_state), cudaMemcpyDeviceToHost, ctx->stream));
+                VXB_CUDA(cudaStreamSynchronize(ctx->stream));  // one read per batch of rounds
+                if (h_state[2])
+                    rate = std::max(static_cast<double>(h_state[1]) /
+                                        (static_cast<double>(h_state[2]) * static_cast<double>(round)),
+                                    1e-9);
+            }
+            require(h_state[0] == n, "empty-set", "generation did not fill within max_rounds");
+            const uint64_t evaluated = h_state[2] * round, accepted_total = h_state[1];
+            rate *= 0.8;  // the acceptance rate falls from one generation to the next
+            if (g == 0) {
+                LaunchScope scope(ctx, VXB_K_MISC);
+                fill_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(nxt_w, n, 1.0 / static_cast<double>(n));
+                check_launch("fill_kernel");
+            } else {
+                const uint64_t mine = w_end - w_begin;
+                double* w_local = world > 1 ? w_send.as<double>() : nxt_w;
+                if (world > 1) VXB_CUDA(cudaMemsetAsync(w_local, 0, w_pad * 8, ctx->stream));
+                if (mine) {
+                    if (fast)
+                        weights_fast_device(ctx, d, mine, nxt_theta + w_begin * d, n, cur_theta, cur_w,
+                                            d_chol.as<double>(), w_local);
+                    else
+                        weights_device(ctx, d, mine, nxt_theta + w_begin * d, n, cur_theta, cur_w,
+                                       d_chol.as<double>(), w_local);
+                }
+                VXB_CUDA(cudaMemsetAsync(totals.as<void>(), 0, nc * 8, ctx->stream));
+                if (mine) {
+                    LaunchScope scope(ctx, VXB_K_RESAMPLE);
+                    const uint64_t my_chunks = n_chunks(mine);
+                    canon_partial_kernel<<<grid_for(my_chunks, kCanonWarps), kCanonWarps * 32, canon_smem(1),
+                                           ctx->stream>>>(2, nullptr, w_local, nullptr, mine, 1, 1,
+                                                          totals.as<double>() + cb);
+                    check_launch("canon_partial_kernel");
+                }
+                if (world > 1) {
+                    comm_allgather(comm, w_send.as<void>(), w_recv.as<void>(), w_pad * 8);
+                    for (uint64_t r = 0; r < world; ++r) {  // rank order = index order
+                        uint64_t b2, e2;
+                        shard_of(nc, world, r, &b2, &e2);
+                        const uint64_t lo = std::min(n, b2 * kChunk), hi = std::min(n, e2 * kChunk);
+                        if (hi > lo)
+                            VXB_CUDA(cudaMemcpyAsync(nxt_w + lo, w_recv.as<double>() + r * w_pad, (hi - lo) * 8,
+                                                     cudaMemcpyDeviceToDevice, ctx->stream));
+                    }
+                    comm_allreduce_sum_f64(comm, totals.as<double>(), nc);
+                }
+                require(vxb_normalise_by_chunk_totals(ctx, nxt_w, n, totals.as<double>(), nc, nullptr) == 0,
+                        "internal", vxb_last_error());
+            }
+            double mean[3], cov[9];
+            const double s2 = weighted_moments_device(ctx, nxt_theta, nxt_w, n, d, mean, cov);
+            require(std::isfinite(s2) && s2 > 0.0, "degenerate-ensemble", "weight sum is not finite");
+            if (out->epsilon) out->epsilon[g] = eps;
+            if (out->ess) out->ess[g] = 1.0 / s2;
+            if (out->accept_rate)
+                out->accept_rate[g] = static_cast<double>(accepted_total) / static_cast<double>(evaluated);
+            if (out->proposals) out->proposals[g] = evaluated;
+            if (out->mean) std::copy(mean, mean + d, out->mean + g * d);
+            if (out->cov) std::copy(cov, cov + d * d, out->cov + g * d * d);
+        }
+        const uint32_t last = (cfg->generations - 1) & 1;
+        if (out->theta) VXB_CUDA(cudaMemcpyAsync(out->theta, th[last], n * d * 8, cudaMemcpyDefault, ctx->stream));
+        if (out->weight) VXB_CUDA(cudaMemcpyAsync(out->weight, ww[last], n * 8, cudaMemcpyDefault, ctx->stream));
+        if (out->rho) VXB_CUDA(cudaMemcpyAsync(out->rho, rh[last], n * 8, cudaMemcpyDefault, ctx->stream));
+        VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}

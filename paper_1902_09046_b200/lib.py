@@ -258,6 +258,20 @@ class Multi:
                                                    f64(ybar_obs), _ptr(counts), _ptr(pv)))
         return counts, pv
 
+    def abcsmc_run(self, model, cfg, observed):
+        n, g, d = cfg.particles, cfg.generations, model.dim
+        obs = np.ascontiguousarray(observed, dtype=np.float64)
+        res = dict(theta=np.zeros((n, d)), weight=np.zeros(n), rho=np.zeros(n),
+                   epsilon=np.zeros(g), ess=np.zeros(g), accept_rate=np.zeros(g),
+                   proposals=np.zeros(g, dtype=np.uint64), mean=np.zeros((g, d)),
+                   cov=np.zeros((g, d, d)))
+        out = A.vxb_abcsmc_out(*[res[k].ctypes.data for k in
+                                 ("theta", "weight", "rho", "epsilon", "ess", "accept_rate",
+                                  "proposals", "mean", "cov")])
+        self._check(self.lib.vxb_multi_abcsmc_run(self.handle, C.byref(model), C.byref(cfg), _ptr(obs),
+                                                  C.byref(out)))
+        return res
+
     def mlmc_tauleap(self, model, cfg):
         L = cfg.levels
         res = dict(level_mean=np.zeros(L), level_var=np.zeros(L), level_cost=np.zeros(L))
@@ -577,6 +591,23 @@ class Context:
                                   "proposals", "mean", "cov")])
         self._check(self.lib.vxb_abcsmc_run(self.handle, C.byref(model), C.byref(cfg), _ptr(obs),
                                             C.byref(out)))
+        return res
+
+    def sharded_abcsmc_run(self, comm, model, cfg, observed):
+        """The native SPMD ABC-SMC driver (every rank calls it; comm None = one rank):
+        same dictionary and the same bits as abcsmc_run."""
+        n, g, d = cfg.particles, cfg.generations, model.dim
+        obs = np.ascontiguousarray(observed, dtype=np.float64)
+        res = dict(theta=np.zeros((n, d)), weight=np.zeros(n), rho=np.zeros(n),
+                   epsilon=np.zeros(g), ess=np.zeros(g), accept_rate=np.zeros(g),
+                   proposals=np.zeros(g, dtype=np.uint64), mean=np.zeros((g, d)),
+                   cov=np.zeros((g, d, d)))
+        out = A.vxb_abcsmc_out(*[res[k].ctypes.data for k in
+                                 ("theta", "weight", "rho", "epsilon", "ess", "accept_rate",
+                                  "proposals", "mean", "cov")])
+        self._check(self.lib.vxb_sharded_abcsmc_run(
+            self.handle, comm.handle if comm is not None else None, C.byref(model), C.byref(cfg),
+            _ptr(obs), C.byref(out)))
         return res
 
     # ---- population statistics (canonical order) for the multi-GPU host

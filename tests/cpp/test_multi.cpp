@@ -17,6 +17,7 @@
 
 #include "vexbayes/abc.hpp"
 #include "vexbayes/logistic.hpp"
+#include "vexbayes/smc.hpp"
 
 using namespace vexbayes;
 
@@ -67,6 +68,17 @@ int main() {
     const auto capped = abc::reject_fixed_epsilon(model, 30001, 1337, observed, sel.epsilon, 5);
     CHECK(capped.total_accepted == acc.total_accepted && capped.rows.size() == 5);
     for (int k = 0; k < 5; ++k) CHECK(capped.rows[k] == acc.rows[k]);
+
+    // ABC-SMC through the shim: every GPU in use, weight sum / particles over NCCL
+    smc::AbcSmcConfig scfg;
+    scfg.particles = 1500;
+    scfg.generations = 3;
+    scfg.round_size = 700;
+    scfg.seed = 77;
+    const auto pop = smc::run_abc_smc(model, scfg, observed);
+    dump("smc_particles", pop.particles);
+    dump("smc_weights", pop.weights);
+    dump("smc_epsilon", pop.epsilon);
 
     // ---- the library's NCCL with one rank: a real communicator, real collectives
     {
@@ -135,6 +147,9 @@ int main() {
     CHECK(set1.failed == set.failed);
     CHECK(acc1.total_accepted == acc.total_accepted && acc1.rows == acc.rows);
     CHECK(acc1.discrepancies == acc.discrepancies && acc1.params == acc.params);
+    const auto pop1 = smc::run_abc_smc(model, scfg, observed);
+    CHECK(pop1.particles == pop.particles && pop1.weights == pop.weights && pop1.epsilon == pop.epsilon);
+    CHECK(pop1.proposals == pop.proposals && pop1.ess == pop.ess);
 
     // ---- SPMD: one host thread per device, own ctx + comm from a shared unique id
     unsigned char id[VXB_COMM_ID_BYTES];

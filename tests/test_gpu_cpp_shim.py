@@ -153,3 +153,10 @@ def test_cpp_multi_gpu_drivers(tmp_path, oracle):
     assert [int(t) for t in r["reject_rows"][1:]] == want.tolist()
     assert np.array_equal(hexd(r["reject_rho"]), rho2[want])
     assert np.array_equal(hexd(r["reject_params"]), p2[want].ravel())
+    cfg = A.vxb_abcsmc_cfg()
+    cfg.particles, cfg.generations, cfg.quantile, cfg.kernel_scale = 1500, 3, 0.5, 2.0
+    cfg.jitter, cfg.round_size, cfg.max_rounds, cfg.seed = 1e-10, 700, 0, 77
+    pop = oracle.abcsmc_run(m, cfg, obs)
+    assert np.array_equal(hexd(r["smc_particles"]), pop["theta"].ravel())
+    assert np.array_equal(hexd(r["smc_weights"]), pop["weight"])
+    assert np.array_equal(hexd(r["smc_epsilon"]), pop["epsilon"])

@@ -90,6 +90,28 @@ def test_library_nccl_communicator_one_rank(ctx, oracle, golden):
     comm.close()
 
 
+def test_native_sharded_abcsmc_equals_one_gpu_driver(ctx, multi, golden):
+    """vxb_sharded_abcsmc_run (SPMD, NCCL inside the library) and vxb_multi_abcsmc_run:
+    bit-identical to vxb_abcsmc_run in both generator modes, with rounds smaller than
+    the population (several rounds per generation, issued ahead of the host); as one
+    rank without a communicator, as one rank WITH a real NCCL communicator, and over
+    every visible device."""
+    obs = golden["logistic_observed"]
+    comm = lib.Comm(ctx, lib.comm_unique_id(), 0, 1)
+    for rng, n, gens, round_size, seed in ((A.VXB_RNG_REF, 2000, 4, 0, 1337), (A.VXB_RNG_REF, 777, 3, 300, 9),
+                                           (A.VXB_RNG_FAST, 1500, 4, 0, 21)):
+        m = M.logistic_model(rng=rng)
+        cfg = A.vxb_abcsmc_cfg()
+        cfg.particles, cfg.generations, cfg.quantile, cfg.kernel_scale = n, gens, 0.5, 2.0
+        cfg.jitter, cfg.round_size, cfg.max_rounds, cfg.seed = 1e-10, round_size, 0, seed
+        want = ctx.abcsmc_run(m, cfg, obs)
+        for got in (ctx.sharded_abcsmc_run(None, m, cfg, obs), ctx.sharded_abcsmc_run(comm, m, cfg, obs),
+                    multi.abcsmc_run(m, cfg, obs)):
+            for k, v in want.items():
+                assert np.array_equal(got[k], v), (k, rng, n)
+    comm.close()
+
+
 def test_guard_mode_finds_no_out_of_bounds_write():
     """compute-sanitizer is closed on this pool, so the library carries its own check:
     with VXB_GUARD=1 every library-owned device buffer is bracketed by canaries that are
