@@ -507,6 +507,12 @@ def all_configs(ctx, timed, obs, device):
             extra=lambda o: {"proposals_simulated_upper_bound": int(o["proposals"].sum()),
                              "epsilon_last": float(o["epsilon"][-1]), "ess_last": float(o["ess"][-1]),
                              "weight_pairs": int(cfg.particles) ** 2 * (cfg.generations - 1)})
+    # the SPMD multi-GPU driver (vxb_sharded_abcsmc_run) as ONE rank: same bits, rounds
+    # issued ahead of the host with the state on the device
+    run("config3_fast_spmd_driver_1rank",
+        lambda: ctx.sharded_abcsmc_run(None, M.logistic_model(rng=A.VXB_RNG_FAST), cfg, obs),
+        cfg.particles * cfg.generations, "particle-generations", target_s=0.6,
+        extra=lambda o: {"epsilon_last": float(o["epsilon"][-1]), "rounds_total": int(o["proposals"].sum() // cfg.particles)})
     for name in ("config3_exact", "config3_fast"):
         # flop rate: every proposal priced as a simulation (an upper bound: proposals
         # outside the prior box are not simulated) + 50 flop per importance-weight pair
