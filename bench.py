@@ -392,6 +392,7 @@ def main():
                    "particles_per_step": n_total, "sde_steps_per_particle": STEPS_PER_SIM,
                    "epsilon": eps, "accepted_per_step": n_acc, "variant": args.variant,
                    "sharding": f"particles/{world}", "exchange": comm_note,
+                   "philox4x32_rounds": int(lib.load().vxb_fast_generator_rounds()),
                    "l2": "no reusable input (compute-bound); per-step rho scratch "
                          f"{(end - begin) * real / 1e6:.0f} MB exceeds L2"},
         "e2e": {"value": e2e_sims, "unit": "sims/s", "h2d_bytes_per_step": h2d,

@@ -35,19 +35,31 @@ def needs_build():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_library(force=False, verbose=False, extra=()):
-    if not force and not needs_build():
-        return LIB
+LIB_ROUNDS7 = os.path.join(HERE, "libvexbayes_cuda_rounds7.so")
+
+
+def build_library(force=False, verbose=False, extra=(), out=None):
+    """out=None: the product library.  out=LIB_ROUNDS7 with extra=["-DVXB_FAST_ROUNDS=7"]:
+    the documented opt-in whose throughput generator runs Philox4x32-7 (load it with the
+    environment variable VXB_LIBRARY; profiles/r2_philox7_*.json is its record)."""
+    if out is None:
+        if not force and not needs_build():
+            return LIB
+        out = LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc] + NVCC_FLAGS + list(extra) + ["-o", LIB] + sources()
-    out = subprocess.run(cmd, capture_output=True, text=True, cwd=CSRC)
-    if verbose or out.returncode:
-        sys.stderr.write(out.stdout + out.stderr)
+    cmd = [nvcc] + NVCC_FLAGS + list(extra) + ["-o", out] + sources()
+    res = subprocess.run(cmd, capture_output=True, text=True, cwd=CSRC)
+    if verbose or res.returncode:
+        sys.stderr.write(res.stdout + res.stderr)
+    out = res
     if out.returncode:
         raise RuntimeError("nvcc failed building libvexbayes_cuda.so")
-    return LIB
+    return cmd[cmd.index("-o") + 1]
 
 
 if __name__ == "__main__":
-    build_library(force=True, verbose=True, extra=["-Xptxas", "-v"] if "-v" in sys.argv else [])
-    print(LIB)
+    if "--rounds7" in sys.argv:
+        print(build_library(force=True, verbose=True, extra=["-DVXB_FAST_ROUNDS=7"], out=LIB_ROUNDS7))
+    else:
+        build_library(force=True, verbose=True, extra=["-Xptxas", "-v"] if "-v" in sys.argv else [])
+        print(LIB)

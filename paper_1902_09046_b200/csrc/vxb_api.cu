@@ -140,6 +140,7 @@ __global__ void fastmath_kernel(int fn, const double* x, const double* y, uint64
 using namespace vxb;
 
 extern "C" int vxb_abi_version(void) { return VXB_ABI_VERSION; }
+extern "C" int vxb_fast_generator_rounds(void) { return VXB_FAST_ROUNDS; }
 
 extern "C" const char* vxb_last_error(void) { return g_last_error.c_str(); }
 

@@ -13,7 +13,9 @@ import numpy as np
 from . import _abi as A
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libvexbayes_cuda.so")
+# VXB_LIBRARY selects another build of the same ABI (the Philox4x32-7 opt-in of
+# paper_1902_09046_b200/build.py --rounds7); the default is the product library.
+LIB_PATH = os.environ.get("VXB_LIBRARY") or os.path.join(HERE, "libvexbayes_cuda.so")
 
 u64, u32, f64, i32 = C.c_uint64, C.c_uint32, C.c_double, C.c_int32
 P = C.c_void_p

@@ -408,3 +408,35 @@ def test_fast_generator_tails_and_mufu_error_device_side(ctx, precision):
         assert s["err_rms"] < 1e-6 and s["err_max"] < 3e-3 and s["err_max_tail"] < 1e-5
     else:
         assert 5.65 < s["max_abs"] < 8.0                   # 52-bit radius uniform: no cap
+
+
+def test_philox7_opt_in_build_statistics():
+    """The opt-in build whose throughput generator runs Philox4x32-7 (build.py --rounds7,
+    loaded through VXB_LIBRARY): same ABI, and its normals pass the same device-side
+    checks (1e9 samples: tails to 5 sigma, moments) as the 10-round product build."""
+    import os
+    import subprocess
+    import sys
+    from paper_1902_09046_b200 import build
+    if not os.path.exists(build.LIB_ROUNDS7):
+        pytest.skip("libvexbayes_cuda_rounds7.so not built (python -m paper_1902_09046_b200.build --rounds7)")
+    code = """
+import math, sys
+sys.path.insert(0, %r)
+from paper_1902_09046_b200 import _abi as A, lib
+assert lib.load().vxb_fast_generator_rounds() == 7 and lib.load().vxb_abi_version() == A.VXB_ABI_VERSION
+ctx = lib.Context(0)
+for prec in (A.VXB_F64, A.VXB_F32):
+    s = ctx.rng_fast_stats(prec, 11, 0, 500000, 2000, [3.0, 4.0, 5.0])
+    n = s["n"]
+    for t, c in zip([3.0, 4.0, 5.0], s["tails"]):
+        e = n * math.erfc(t / math.sqrt(2.0))
+        lo = 0.88 * e if (prec == A.VXB_F32 and t == 5.0) else e - 5 * math.sqrt(e) - 3
+        assert lo < int(c) < e + 5 * math.sqrt(e) + 3, (prec, t, int(c), e)
+    assert abs(s["mean"]) < 5 / math.sqrt(n) and abs(s["var"] - 1) < 5 * math.sqrt(2.0 / n) + 3e-6
+    assert abs(s["skew"]) < 5 * math.sqrt(15.0 / n) and abs(s["kurt"] - 3) < 5 * math.sqrt(96.0 / n) + 1e-4
+print("philox7 ok")
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    run = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                         env=dict(os.environ, VXB_LIBRARY=build.LIB_ROUNDS7))
+    assert run.returncode == 0 and "philox7 ok" in run.stdout, run.stdout[-1500:] + run.stderr[-1500:]
