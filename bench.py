@@ -272,22 +272,31 @@ def main():
 
     torch.cuda.set_device(local)
     comm, comm_note = None, "single GPU: no collective"
-    if world > 1:
+    # VXB_FORCE_GATHER=1 (diagnostics, under a launcher): one rank walks the N > 1 path
+    dist_on = world > 1 or (bool(os.environ.get("VXB_FORCE_GATHER")) and "RANK" in os.environ)
+    if dist_on:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = lib.Context(local)
-    if world > 1:
+    if dist_on:
         comm_note = "torch.distributed NCCL all_gather_into_tensor of the packed accepted block"
         if args.comm == "native":
             # the library's own NCCL communicator; its unique id travels through
             # torch.distributed.  Every rank must agree on the outcome.
             ok = torch.ones(1, dtype=torch.int32, device=f"cuda:{local}")
+            uid = [None]
+            if rank == 0:
+                try:
+                    uid = [lib.comm_unique_id().tobytes()]
+                except Exception as e:     # NCCL not loadable: every rank falls back together
+                    print(f"bench.py: native communicator unavailable: {e!r}", file=sys.stderr)
+            dist.broadcast_object_list(uid, src=0)
             try:
-                uid = [lib.comm_unique_id().tobytes() if rank == 0 else None]
-                dist.broadcast_object_list(uid, src=0)
+                if uid[0] is None:
+                    raise RuntimeError("no unique id")
                 comm = lib.Comm(ctx, np.frombuffer(uid[0], dtype=np.uint8), rank, world)
             except Exception as e:  # fall back to torch.distributed rather than lose the run
                 ok.zero_()
-                comm_err = repr(e)
+                print(f"bench.py: rank {rank}: native communicator failed: {e!r}", file=sys.stderr)
             dist.all_reduce(ok, op=dist.ReduceOp.MIN)
             if int(ok.item()) == 1:
                 comm_note = f"library NCCL (vxb_sharded_abc_reject, NCCL {lib.comm_version()})"
@@ -311,7 +320,7 @@ def main():
     del rho0
 
     def barrier():
-        if world > 1:
+        if dist_on:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -329,7 +338,7 @@ def main():
             e1.record(ext)
             barrier()
         ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=f"cuda:{local}")
-        if world > 1:
+        if dist_on:
             dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         return float(ms.item()), out
 
@@ -437,7 +446,7 @@ def main():
     if comm is not None:
         comm.close()
     ctx.close()
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
 
 

@@ -99,6 +99,13 @@ def allreduce_sum(t, group=None):
     return t
 
 
+def _force_gather():
+    """Diagnostics: VXB_FORCE_GATHER=1 runs the collective even with one rank, so that a
+    one-GPU box executes exactly the code path of N > 1 (NCCL init, packed all-gather)."""
+    import os
+    return bool(os.environ.get("VXB_FORCE_GATHER"))
+
+
 class RejectBuffers:
     """Output buffers of sharded_reject for this rank: its packed accepted set and
     (several ranks) the gathered blocks of all ranks, allocated on the library's
@@ -121,7 +128,7 @@ class RejectBuffers:
         with torch.cuda.stream(torch.cuda.ExternalStream(ctx.stream(), device=dev)):
             self.local = torch.empty(int(self.layout.stride), dtype=torch.uint8, device=dev)
             self.all = (torch.empty(world * int(self.layout.stride), dtype=torch.uint8, device=dev)
-                        if world > 1 else None)
+                        if world > 1 or _force_gather() else None)
 
     def local_views(self):
         idx, params, rho, count = packed_views(self.local, self.layout, self.precision, self.dim)
@@ -152,12 +159,12 @@ def sharded_reject(ctx, model, key, n_total, observed, eps, cap_fraction=0.01, g
                                                           world, rank)
     if comm is not None:
         ctx.sharded_abc_reject(comm, model, key, n_total, observed, eps, b.layout, b.local, b.all)
-        return b.local_views() if world == 1 else b.gathered_views()
+        return b.local_views() if b.all is None else b.gathered_views()
     begin, end = shard_range(n_total, world, rank)
     idx, params, rho, n_dev = b.local_views()
     ctx.abc_reject(model, key, n_total, begin, end - begin, observed, eps, int(b.layout.cap),
                    idx=idx, params=params, rho=rho, n_accepted=n_dev)
-    if world == 1:
+    if b.all is None:
         return idx, params, rho, n_dev
     with torch.cuda.stream(torch.cuda.ExternalStream(ctx.stream(), device=b.local.device)):
         gather_packed(b.local, world, out=b.all, group=group)

@@ -131,3 +131,30 @@ def test_guard_mode_finds_no_out_of_bounds_write():
     lines = [l for l in run.stderr.splitlines() if l.startswith("vxb guard:")]
     assert len([l for l in lines if "out-of-bounds" in l]) == 1  # the provoked one
     assert all(re.search(r"\b0 violation", l) for l in lines if "violation(s)" in l)
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("comm", ["torch", "native"])
+def test_bench_walks_the_multi_rank_path_with_one_rank(comm):
+    """bench.py under the launcher with VXB_FORCE_GATHER=1: ONE rank executes exactly the
+    code of N > 1 -- NCCL process group, the packed all_gather_into_tensor (or the
+    library's communicator with --comm native), barrier and max-over-ranks timing."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, VXB_FORCE_GATHER="1")
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        env.pop(k, None)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+           "--master-addr", "127.0.0.1", "--master-port", "29611" if comm == "torch" else "29612",
+           os.path.join(root, "bench.py"), "--gpus", "1", "--steps", "2", "--warmup", "3",
+           "--particles", "2e6", "--no-extras", "--comm", comm]
+    run = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    assert run.returncode == 0, run.stdout[-1500:] + run.stderr[-3000:]
+    line = json.loads([l for l in run.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 1 and line["value"] > 1e8
+    assert line["config"]["accepted_per_step"] > 1500
+    want = "library NCCL" if comm == "native" else "torch.distributed NCCL"
+    assert want in line["config"]["exchange"], line["config"]["exchange"]
