@@ -582,12 +582,13 @@ int vxb_sharded_abc_reject(vxb_ctx* ctx, vxb_comm* comm, const vxb_model* model,
                            double epsilon, const vxb_accept_layout* layout, void* packed_local,
                            void* packed_all);
 /* Host-side concatenation of gathered blocks (a HOST copy of packed_all) in rank
- * order: at most cap_out rows are written; *n_accepted is the full count (a rank
- * whose count exceeded layout->cap contributes only its first cap rows -- check
- * *overflowed). */
+ * order: at most cap_out rows are written (*n_written of them); *n_accepted is the
+ * full count (a rank whose count exceeded layout->cap contributes only its first cap
+ * rows -- check *overflowed).  overflowed and n_written may be NULL. */
 int vxb_accept_unpack(const vxb_accept_layout* layout, int precision, uint32_t dim, int n_ranks,
                       const void* packed_all_host, uint64_t cap_out, uint64_t* n_accepted,
-                      uint64_t* idx, void* params, void* rho, int* overflowed);
+                      uint64_t* idx, void* params, void* rho, int* overflowed,
+                      uint64_t* n_written);
 
 /* One process, several GPUs.  device_ids == NULL or n_dev == 0: every visible
  * device.  With one device no communicator is created (NCCL is not loaded). */

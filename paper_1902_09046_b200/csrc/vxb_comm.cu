@@ -300,7 +300,7 @@ extern "C" int vxb_sharded_abc_reject(vxb_ctx* ctx, vxb_comm* comm, const vxb_mo
 extern "C" int vxb_accept_unpack(const vxb_accept_layout* layout, int precision, uint32_t dim,
                                  int n_ranks, const void* packed_all_host, uint64_t cap_out,
                                  uint64_t* n_accepted, uint64_t* idx, void* params, void* rho,
-                                 int* overflowed) {
+                                 int* overflowed, uint64_t* n_written) {
     return guarded([&] {
         require(layout && packed_all_host && n_accepted && n_ranks >= 1, "invalid-argument",
                 "null argument");
@@ -330,6 +330,7 @@ extern "C" int vxb_accept_unpack(const vxb_accept_layout* layout, int precision,
         }
         *n_accepted = total;
         if (overflowed) *overflowed = over ? 1 : 0;
+        if (n_written) *n_written = kept;
     });
 }
 
@@ -446,7 +447,7 @@ extern "C" int vxb_multi_abc_reject(vxb_multi* m, const vxb_model* model, const 
         });
         int over = 0;
         abi(vxb_accept_unpack(&lay, model->precision, model->dim, g, host.data(), cap, n_accepted, idx,
-                              params, rho, &over));
+                              params, rho, &over, nullptr));
     });
 }
 

@@ -85,19 +85,37 @@ seq_expsum_kernel(const double* __restrict__ x, const double* __restrict__ mx, u
         const uint32_t len = static_cast<uint32_t>(min(static_cast<uint64_t>(kSeqTile), n - t0));
         double* cur = buf[t & 1];
         if (tid == 0) {
-            if (kCum) {
-#pragma unroll 8
-                for (uint32_t k = 0; k < len; ++k) {
-                    s1 = __dadd_rn(s1, cur[k]);
-                    cur[k] = s1;
+            // the chain: one dependent DADD per element.  Blocks of 32 with the NEXT
+            // block's loads issued before this block's adds, so that the shared-memory
+            // latency (~30 cycles) hides behind the 32 adds instead of preceding every 8
+            constexpr uint32_t kW = 32;
+            double v[kW], nx[kW];
+            uint32_t k0 = 0;
+            if (len >= kW) {
+#pragma unroll
+                for (uint32_t q = 0; q < kW; ++q) v[q] = cur[q];
+                for (; k0 + 2 * kW <= len; k0 += kW) {
+#pragma unroll
+                    for (uint32_t q = 0; q < kW; ++q) nx[q] = cur[k0 + kW + q];
+#pragma unroll
+                    for (uint32_t q = 0; q < kW; ++q) {
+                        s1 = __dadd_rn(s1, v[q]);
+                        if (kCum) cur[k0 + q] = s1; else s2 = __dadd_rn(s2, __dmul_rn(v[q], v[q]));
+                    }
+#pragma unroll
+                    for (uint32_t q = 0; q < kW; ++q) v[q] = nx[q];
                 }
-            } else {
-#pragma unroll 8
-                for (uint32_t k = 0; k < len; ++k) {
-                    const double e = cur[k];
-                    s1 = __dadd_rn(s1, e);
-                    s2 = __dadd_rn(s2, __dmul_rn(e, e));
+#pragma unroll
+                for (uint32_t q = 0; q < kW; ++q) {  // the last full block
+                    s1 = __dadd_rn(s1, v[q]);
+                    if (kCum) cur[k0 + q] = s1; else s2 = __dadd_rn(s2, __dmul_rn(v[q], v[q]));
                 }
+                k0 += kW;
+            }
+            for (uint32_t k = k0; k < len; ++k) {  // ragged tail of the last tile
+                const double e = cur[k];
+                s1 = __dadd_rn(s1, e);
+                if (kCum) cur[k] = s1; else s2 = __dadd_rn(s2, __dmul_rn(e, e));
             }
         } else if (tid >= 32 && t + 1 < tiles) {
             const uint64_t n0 = t0 + kSeqTile;

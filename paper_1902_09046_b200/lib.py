@@ -139,12 +139,12 @@ def accept_unpack(layout, precision, dim, n_ranks, packed_all_host, cap_out=None
     dt = np.float32 if precision == A.VXB_F32 else np.float64
     idx = np.zeros(cap_out, dtype=np.uint64)
     params, rho = np.zeros((cap_out, dim), dtype=dt), np.zeros(cap_out, dtype=dt)
-    n_acc, over = u64(), C.c_int()
+    n_acc, over, written = u64(), C.c_int(), u64()
     if load().vxb_accept_unpack(C.byref(layout), i32(precision), u32(dim), C.c_int(n_ranks),
                                 _ptr(buf), u64(cap_out), C.byref(n_acc), _ptr(idx), _ptr(params),
-                                _ptr(rho), C.byref(over)):
+                                _ptr(rho), C.byref(over), C.byref(written)):
         _raise_last()
-    k = min(n_acc.value, cap_out)
+    k = written.value
     return n_acc.value, idx[:k], params[:k], rho[:k], bool(over.value)
 
 

@@ -117,7 +117,7 @@ int main() {
         std::vector<double> rho(4000);
         int over = 1;
         cuda::check(vxb_accept_unpack(&lay, VXB_F64, 3, 1, host.data(), 4000, &n_acc, rows.data(),
-                                      nullptr, rho.data(), &over));
+                                      nullptr, rho.data(), &over, nullptr));
         CHECK(n_acc == acc.total_accepted && over == 0);
         for (std::uint64_t k = 0; k < n_acc; ++k)
             CHECK(rows[k] == acc.rows[k] && rho[k] == acc.discrepancies[k]);
@@ -189,7 +189,7 @@ int main() {
     std::vector<double> rho(4000), params(3 * 4000);
     int over = 1;
     cuda::check(vxb_accept_unpack(&lay, VXB_F64, 3, n_dev, gathered[0].data(), 4000, &n_acc, rows.data(),
-                                  params.data(), rho.data(), &over));
+                                  params.data(), rho.data(), &over, nullptr));
     CHECK(n_acc == acc.total_accepted && over == 0);
     rows.resize(n_acc);
     rho.resize(n_acc);

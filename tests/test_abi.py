@@ -123,3 +123,38 @@ def test_product_package_never_imports_the_oracle():
     import subprocess
     deps = subprocess.run(["ldd", lib.LIB_PATH], capture_output=True, text=True).stdout
     assert "vxb_oracle" not in deps and "vxb_ref" not in deps
+
+
+def test_multi_gpu_entry_points_argument_errors(so):
+    """Host-side behaviour of the multi-GPU section of the ABI (no GPU needed): the
+    packed accepted-set layout and its unpacking, argument checks, and the loud failure
+    of vxb_multi_init without a CUDA device."""
+    import torch
+    lay = lib.accept_layout(A.VXB_F64, 3, 1000)
+    assert (lay.off_count, lay.off_idx) == (0, 16) and lay.off_params == 16 + 8000
+    assert lay.off_rho == lay.off_params + 24000 and lay.stride == lay.off_rho + 8000
+    lay32 = lib.accept_layout(A.VXB_F32, 3, 7)           # every field stays 16-byte aligned
+    assert all(v % 16 == 0 for v in (lay32.off_idx, lay32.off_params, lay32.off_rho, lay32.stride))
+    for bad in ((A.VXB_F64, 0, 10), (A.VXB_F64, 3, 0), (5, 3, 10)):
+        with pytest.raises(lib.VxbError) as e:
+            lib.accept_layout(*bad)
+        assert e.value.code in ("invalid-shape", "invalid-argument")
+    # unpack: two blocks, the second one over capacity -> only `cap` rows, flagged
+    buf = np.zeros(2 * lay32.stride, dtype=np.uint8)
+    for r, count in enumerate((3, 9)):
+        base = r * lay32.stride
+        buf[base:base + 8].view(np.uint64)[0] = count
+        buf[base + lay32.off_idx:base + lay32.off_idx + 56].view(np.uint64)[:] = np.arange(7) + 100 * r
+        buf[base + lay32.off_rho:base + lay32.off_rho + 28].view(np.float32)[:] = r + 0.5
+    n_acc, idx, params, rho, over = lib.accept_unpack(lay32, A.VXB_F32, 3, 2, buf)
+    assert n_acc == 12 and over and idx.tolist() == [0, 1, 2, 100, 101, 102, 103, 104, 105, 106]
+    assert rho.tolist() == [0.5] * 3 + [1.5] * 7
+    n_acc, idx, _, _, _ = lib.accept_unpack(lay32, A.VXB_F32, 3, 2, buf, cap_out=4)
+    assert n_acc == 12 and idx.tolist() == [0, 1, 2, 100]
+    assert lib.device_count() == (torch.cuda.device_count() if torch.cuda.is_available() else 0)
+    if not torch.cuda.is_available():
+        with pytest.raises(lib.VxbError) as e:
+            lib.Multi()
+        assert e.value.code == "device-error"
+    # the library finds NCCL by itself (dlopen); the version is the loaded library's
+    assert lib.comm_version() >= 21800
