@@ -593,6 +593,12 @@ int vxb_accept_unpack(const vxb_accept_layout* layout, int precision, uint32_t d
 /* One process, several GPUs.  device_ids == NULL or n_dev == 0: every visible
  * device.  With one device no communicator is created (NCCL is not loaded). */
 int vxb_multi_init(vxb_multi** multi, const int* device_ids, int n_dev);
+/* Diagnostics for boxes with fewer GPUs than ranks: n_ranks contexts on ONE device
+ * joined by a LOOPBACK group instead of NCCL -- a collective is a host rendezvous of the
+ * ranks' threads (stream drained, barrier, device-to-device copies, barrier); no kernel
+ * ever waits for another rank.  Every vxb_multi_* driver then runs its multi-rank logic
+ * (sharding, packed gathers, chunk-total reduction, append order) for real. */
+int vxb_multi_init_loopback(vxb_multi** multi, int device, int n_ranks);
 void vxb_multi_shutdown(vxb_multi* multi);
 int vxb_multi_size(const vxb_multi* multi);
 vxb_ctx* vxb_multi_ctx(vxb_multi* multi, int rank);

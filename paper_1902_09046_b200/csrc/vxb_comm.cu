@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <condition_variable>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -98,26 +99,88 @@ void shard_of(uint64_t total, uint64_t world, uint64_t rank, uint64_t* begin, ui
 
 }  // namespace vxb
 
+// Loopback group (diagnostics): the ranks are host threads of ONE process, each with
+// its own vxb_ctx -- all of them may sit on the same GPU -- and a collective is a host
+// rendezvous: every rank drains its stream, the ranks meet at a barrier, each copies the
+// others' buffers device-to-device on its own stream, and they meet again.  No kernel
+// ever waits for another rank (the profiling guide's rule for one-GPU emulation), so the
+// multi-rank drivers (sharding offsets, packed gathers, chunk-total reduction, append
+// order) run for real on a one-GPU box.  Same results as NCCL by construction: an
+// all-gather is a copy, and the only all-reduce of the path adds vectors with one
+// non-zero contributor per entry (added here in rank order).
+struct vxb_loopback {
+    int size = 0;
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    unsigned long long generation = 0;
+    std::vector<const void*> slot;
+    void barrier() {
+        std::unique_lock<std::mutex> lock(m);
+        const unsigned long long gen = generation;
+        if (++arrived == size) {
+            arrived = 0;
+            ++generation;
+            cv.notify_all();
+        } else {
+            cv.wait(lock, [&] { return generation != gen; });
+        }
+    }
+};
+
 struct vxb_comm {
     vxb_ctx* ctx = nullptr;
     ncclComm_t comm = nullptr;
     int rank = 0, size = 1;
+    vxb_loopback* loop = nullptr;  // non-null: loopback group instead of NCCL
 };
 
 struct vxb_multi {
     std::vector<vxb_ctx*> ctx;
     std::vector<vxb_comm*> comm;  // empty with one device
+    vxb_loopback* loop = nullptr;  // owned (vxb_multi_init_loopback)
 };
+
+namespace vxb {
+__global__ void loopback_sum_kernel(const double* __restrict__ all, int ranks, size_t count,
+                                    double* __restrict__ out) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    double s = 0.0;
+    for (int r = 0; r < ranks; ++r) s = __dadd_rn(s, all[static_cast<size_t>(r) * count + i]);
+    out[i] = s;
+}
+static void loopback_allgather(vxb_comm* c, const void* send, void* recv, size_t bytes) {
+    vxb_loopback* g = c->loop;
+    VXB_CUDA(cudaStreamSynchronize(c->ctx->stream));  // my block is complete
+    g->slot[c->rank] = send;
+    g->barrier();
+    for (int r = 0; r < c->size; ++r)
+        VXB_CUDA(cudaMemcpyAsync(static_cast<char*>(recv) + static_cast<size_t>(r) * bytes, g->slot[r], bytes,
+                                 cudaMemcpyDefault, c->ctx->stream));
+    VXB_CUDA(cudaStreamSynchronize(c->ctx->stream));
+    g->barrier();  // nobody reuses its send buffer before everyone has copied it
+}
+static void loopback_allreduce_sum_f64(vxb_comm* c, double* buf, size_t count) {
+    Scratch all(c->ctx, static_cast<size_t>(c->size) * count * sizeof(double));
+    loopback_allgather(c, buf, all.as<void>(), count * sizeof(double));
+    loopback_sum_kernel<<<grid_for(count, 256), 256, 0, c->ctx->stream>>>(all.as<double>(), c->size, count, buf);
+    check_launch("loopback_sum_kernel");
+    VXB_CUDA(cudaStreamSynchronize(c->ctx->stream));
+}
+}  // namespace vxb
 
 namespace vxb {
 int comm_rank(const vxb_comm* comm) { return comm ? comm->rank : 0; }
 int comm_size(const vxb_comm* comm) { return comm ? comm->size : 1; }
 void comm_allgather(vxb_comm* comm, const void* send, void* recv, size_t bytes) {
     require(comm != nullptr, "invalid-argument", "null communicator");
+    if (comm->loop) return loopback_allgather(comm, send, recv, bytes);
     VXB_NCCL(nccl().AllGather(send, recv, bytes, ncclUint8, comm->comm, comm->ctx->stream));
 }
 void comm_allreduce_sum_f64(vxb_comm* comm, double* buf, size_t count) {
     require(comm != nullptr, "invalid-argument", "null communicator");
+    if (comm->loop) return loopback_allreduce_sum_f64(comm, buf, count);
     VXB_NCCL(nccl().AllReduce(buf, buf, count, ncclFloat64, ncclSum, comm->comm, comm->ctx->stream));
 }
 }  // namespace vxb
@@ -214,7 +277,7 @@ extern "C" int vxb_comm_init_rank(vxb_ctx* ctx, const void* id, int rank, int n_
 
 extern "C" void vxb_comm_destroy(vxb_comm* comm) {
     if (!comm) return;
-    if (comm->comm) {
+    if (comm->comm && !comm->loop) {
         cudaSetDevice(comm->ctx->device);
         cudaStreamSynchronize(comm->ctx->stream);
         nccl().CommDestroy(comm->comm);
@@ -229,7 +292,7 @@ extern "C" int vxb_comm_allgather(vxb_comm* comm, const void* send, void* recv, 
     return guarded([&] {
         require(comm && send && recv, "invalid-argument", "null argument");
         use(comm->ctx);
-        VXB_NCCL(nccl().AllGather(send, recv, bytes, ncclUint8, comm->comm, comm->ctx->stream));
+        comm_allgather(comm, send, recv, bytes);
     });
 }
 
@@ -237,6 +300,11 @@ extern "C" int vxb_comm_allreduce(vxb_comm* comm, void* buf, size_t count, int d
     return guarded([&] {
         require(comm && buf, "invalid-argument", "null argument");
         use(comm->ctx);
+        if (comm->loop) {
+            require(dtype == VXB_DT_F64 && op == VXB_OP_SUM, "invalid-argument",
+                    "the loopback group reduces doubles by SUM only");
+            return comm_allreduce_sum_f64(comm, static_cast<double*>(buf), count);
+        }
         ncclDataType_t dt;
         switch (dtype) {
             case VXB_DT_U8: dt = ncclUint8; break;
@@ -289,8 +357,7 @@ extern "C" int vxb_sharded_abc_reject(vxb_ctx* ctx, vxb_comm* comm, const vxb_mo
                            reinterpret_cast<uint64_t*>(base + layout->off_idx),
                            base + layout->off_params, base + layout->off_rho));
         if (world > 1)
-            VXB_NCCL(nccl().AllGather(packed_local, packed_all, layout->stride, ncclUint8, comm->comm,
-                                      ctx->stream));
+            comm_allgather(comm, packed_local, packed_all, layout->stride);
         else if (packed_all && packed_all != packed_local)
             VXB_CUDA(cudaMemcpyAsync(packed_all, packed_local, layout->stride,
                                      cudaMemcpyDeviceToDevice, ctx->stream));
@@ -384,10 +451,43 @@ extern "C" int vxb_multi_init(vxb_multi** multi, const int* device_ids, int n_de
     });
 }
 
+// Diagnostics: n_ranks contexts on ONE device joined by a loopback group, so that every
+// vxb_multi_* driver runs its multi-rank logic on a one-GPU box.
+extern "C" int vxb_multi_init_loopback(vxb_multi** multi, int device, int n_ranks) {
+    return guarded([&] {
+        require(multi != nullptr && n_ranks >= 1 && n_ranks <= 64, "invalid-argument", "bad rank count");
+        auto* m = new vxb_multi();
+        try {
+            m->loop = new vxb_loopback();
+            m->loop->size = n_ranks;
+            m->loop->slot.assign(n_ranks, nullptr);
+            for (int r = 0; r < n_ranks; ++r) {
+                vxb_ctx* c = nullptr;
+                abi(vxb_init(&c, device));
+                m->ctx.push_back(c);
+            }
+            if (n_ranks > 1)
+                for (int r = 0; r < n_ranks; ++r) {
+                    auto* c = new vxb_comm();
+                    c->ctx = m->ctx[r];
+                    c->rank = r;
+                    c->size = n_ranks;
+                    c->loop = m->loop;
+                    m->comm.push_back(c);
+                }
+        } catch (...) {
+            vxb_multi_shutdown(m);
+            throw;
+        }
+        *multi = m;
+    });
+}
+
 extern "C" void vxb_multi_shutdown(vxb_multi* m) {
     if (!m) return;
     for (vxb_comm* c : m->comm) vxb_comm_destroy(c);
     for (vxb_ctx* c : m->ctx) vxb_shutdown(c);
+    delete m->loop;
     delete m;
 }
 

@@ -202,9 +202,16 @@ class Multi:
     """One process, several GPUs (vxb_multi): a context (and an NCCL communicator)
     per device; the calls fork one host thread per device and join."""
 
-    def __init__(self, device_ids=None):
+    def __init__(self, device_ids=None, loopback_ranks=None, device=0):
+        """loopback_ranks=n (diagnostics): n contexts on ONE device joined by the
+        library's loopback group instead of NCCL (vxb_multi_init_loopback)."""
         self.lib = load()
         self.handle = P()
+        if loopback_ranks is not None:
+            if self.lib.vxb_multi_init_loopback(C.byref(self.handle), C.c_int(device),
+                                                C.c_int(loopback_ranks)):
+                _raise_last()
+            return
         ids = None if device_ids is None else np.ascontiguousarray(device_ids, dtype=np.int32)
         if self.lib.vxb_multi_init(C.byref(self.handle), _ptr(ids), C.c_int(0 if ids is None else ids.size)):
             _raise_last()

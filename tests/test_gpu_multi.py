@@ -158,3 +158,45 @@ def test_bench_walks_the_multi_rank_path_with_one_rank(comm):
     assert line["config"]["accepted_per_step"] > 1500
     want = "library NCCL" if comm == "native" else "torch.distributed NCCL"
     assert want in line["config"]["exchange"], line["config"]["exchange"]
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("ranks", [2, 3, 4])
+def test_multi_rank_drivers_on_one_gpu_through_the_loopback_group(ctx, oracle, golden, ranks):
+    """The multi-rank native code -- row sharding, the packed accepted-set gather,
+    vxb_sharded_abcsmc_run's rounds (gated propose, pack, gather, append in rank order),
+    the padded weight gather and the all-reduce of the chunk totals -- executed for real
+    with 2, 3 and 4 ranks: `ranks` contexts on this one GPU joined by the library's
+    loopback group (host rendezvous + device-to-device copies in place of NCCL; no kernel
+    waits for another rank).  Everything must equal the one-context result bit for bit.
+    With 4 ranks the 600-particle ABC-SMC run has 3 canonical chunks: one rank owns an
+    empty weight shard; round_size 250 gives ragged slices (63/63/62/62)."""
+    multi = lib.Multi(loopback_ranks=ranks)
+    assert multi.size == ranks
+    obs = golden["logistic_observed"]
+    m = M.logistic_model()
+    key = M.keying(1337, A.VXB_KEY_WORKER, 5, 4)
+    got = multi.abc_prior_predictive(m, key, 2003, obs)
+    want = oracle.abc_prior_predictive(m, key, 2003, 0, 2003, obs)
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w, equal_nan=True)
+    p, _, rho, f = oracle.abc_prior_predictive(m, M.keying(7), 40001, 0, 40001, obs, want_summaries=False)
+    eps, idx_o = oracle.select_epsilon(rho, f, 0.02)
+    nacc, idx, params, rho_acc = multi.abc_reject(m, M.keying(7), 40001, obs, eps, cap=40001)
+    assert nacc == len(idx_o) and np.array_equal(idx, idx_o)
+    assert np.array_equal(params, p[idx_o]) and np.array_equal(rho_acc, rho[idx_o])
+    for rng, n, gens, round_size, seed in ((A.VXB_RNG_REF, 600, 3, 250, 9), (A.VXB_RNG_FAST, 1500, 4, 0, 21),
+                                           (A.VXB_RNG_REF, 2000, 3, 0, 1337)):
+        mm = M.logistic_model(rng=rng)
+        cfg = A.vxb_abcsmc_cfg()
+        cfg.particles, cfg.generations, cfg.quantile, cfg.kernel_scale = n, gens, 0.5, 2.0
+        cfg.jitter, cfg.round_size, cfg.max_rounds, cfg.seed = 1e-10, round_size, 0, seed
+        one, many = ctx.abcsmc_run(mm, cfg, obs), multi.abcsmc_run(mm, cfg, obs)
+        for k, v in one.items():
+            assert np.array_equal(many[k], v), (k, rng, n, ranks)
+    lam = np.array(M.lambda_grid(8))
+    ln = np.array([-0.5 * math.log(2.0 * math.pi * (l * l + 0.01)) for l in lam])
+    c1, p1, _ = ctx.ppp_pvalues(M.normal_mean_model(100), lam, ln, 30001, 0, 30001, 1337, 2.9)
+    c2, p2 = multi.ppp_pvalues(M.normal_mean_model(100), lam, ln, 30001, 1337, 2.9)
+    assert np.array_equal(c1, c2) and np.array_equal(p1, p2)
+    multi.close()
