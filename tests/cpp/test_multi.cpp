@@ -129,6 +129,37 @@ int main() {
         std::printf("nccl_one_rank ok\n");
     }
 
+    // ---- three ranks on ONE device through the loopback group: the multi-rank code of
+    // the C ABI (sharding, packed gather, rounds, weight gather, chunk-total reduction)
+    // runs for real on a one-GPU box and must reproduce the results above
+    {
+        vxb_multi* loop = nullptr;
+        cuda::check(vxb_multi_init_loopback(&loop, 0, 3));
+        CHECK(vxb_multi_size(loop) == 3 && vxb_multi_comm(loop, 2) != nullptr);
+        vxb_keying key{VXB_KEY_PARTICLE, 1, 1, 0, 1337};
+        std::uint64_t n_acc = 0;
+        std::vector<std::uint64_t> rows(4000);
+        std::vector<double> rho(4000), params(3 * 4000);
+        cuda::check(vxb_multi_abc_reject(loop, model.device.get(), &key, 30001, observed.data(), sel.epsilon,
+                                         4000, &n_acc, rows.data(), params.data(), rho.data()));
+        CHECK(n_acc == acc.total_accepted);
+        rows.resize(n_acc);
+        rho.resize(n_acc);
+        params.resize(3 * n_acc);
+        CHECK(rows == acc.rows && rho == acc.discrepancies && params == acc.params);
+        std::vector<double> th(pop.particles.size()), w(pop.weights.size()), r(pop.weights.size());
+        std::vector<double> eps(3), ess(3), rate(3), mean(9), cov(27);
+        std::vector<std::uint64_t> props(3);
+        vxb_abcsmc_cfg c{scfg.particles, 3, 0, scfg.quantile, scfg.kernel_scale, scfg.jitter,
+                         scfg.round_size, scfg.max_rounds, scfg.seed};
+        vxb_abcsmc_out o{th.data(), w.data(), r.data(), eps.data(), ess.data(), rate.data(), props.data(),
+                         mean.data(), cov.data()};
+        cuda::check(vxb_multi_abcsmc_run(loop, model.device.get(), &c, observed.data(), &o));
+        CHECK(th == pop.particles && w == pop.weights && eps == pop.epsilon && props == pop.proposals);
+        vxb_multi_shutdown(loop);
+        std::printf("loopback_three_ranks ok\n");
+    }
+
     if (n_dev < 2) {
         std::printf("multi_gpu skipped (1 device)\n");
         return 0;

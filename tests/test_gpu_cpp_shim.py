@@ -138,6 +138,7 @@ def test_cpp_multi_gpu_drivers(tmp_path, oracle):
     import torch
     assert int(r["devices"][0]) == torch.cuda.device_count() == int(r["in_use"][0])
     assert r["nccl_one_rank"] == ["ok"] and int(r["nccl_version"][0]) >= 21800
+    assert r["loopback_three_ranks"] == ["ok"]
     if torch.cuda.device_count() >= 2:
         assert r["multi_gpu"][0] == "ok"
     m = M.logistic_model()
