@@ -199,4 +199,12 @@ def test_multi_rank_drivers_on_one_gpu_through_the_loopback_group(ctx, oracle, g
     c1, p1, _ = ctx.ppp_pvalues(M.normal_mean_model(100), lam, ln, 30001, 0, 30001, 1337, 2.9)
     c2, p2 = multi.ppp_pvalues(M.normal_mean_model(100), lam, ln, 30001, 1337, 2.9)
     assert np.array_equal(c1, c2) and np.array_equal(p1, p2)
+    # fewer rows than ranks: some ranks own EMPTY shards
+    tiny = multi.abc_prior_predictive(m, M.keying(7), ranks - 1, obs)
+    for g, w in zip(tiny, oracle.abc_prior_predictive(m, M.keying(7), ranks - 1, 0, ranks - 1, obs)):
+        assert np.array_equal(g, w, equal_nan=True)
+    nacc, idx, _, _ = multi.abc_reject(m, M.keying(7), ranks - 1, obs, 1e9, cap=16)
+    assert nacc == ranks - 1 and idx.tolist() == list(range(ranks - 1))
+    c3, _ = multi.ppp_pvalues(M.normal_mean_model(100), lam, ln, ranks - 1, 1337, 2.9)
+    assert np.array_equal(c3, ctx.ppp_pvalues(M.normal_mean_model(100), lam, ln, ranks - 1, 0, ranks - 1, 1337, 2.9)[0])
     multi.close()
