@@ -634,6 +634,13 @@ int vxb_sharded_abcsmc_run(vxb_ctx* ctx, vxb_comm* comm, const vxb_model* model,
                            vxb_abcsmc_out* out);
 int vxb_multi_abcsmc_run(vxb_multi* multi, const vxb_model* model, const vxb_abcsmc_cfg* cfg,
                          const double* observed, vxb_abcsmc_out* out);
+/* run_weak_info_test (weak_info.cpp:163-277) with the hyperparameter rows split over
+ * the devices -- the reference's own task split over `workers` (weak_info.cpp:248-270);
+ * sampler seeds are keyed by (row, dataset): the table does not depend on the device
+ * count.  Arguments as vxb_weak_info_test. */
+int vxb_multi_weak_info_test(vxb_multi* multi, const vxb_weakinfo_cfg* cfg, double* lambda,
+                             double* gamma, uint8_t* weakly, uint64_t* completed,
+                             double* evidence);
 
 #ifdef __cplusplus
 }

@@ -15,7 +15,7 @@ LIB = os.path.join(HERE, "libvexbayes_cuda.so")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
-    "-lineinfo", "-O3", "-std=c++17",
+    "-lineinfo", "-O3", "-std=c++17", "--threads", "0",   # one nvcc job per source file
     "-Xcompiler", "-fPIC", "-shared",
     # IEEE division / square root / no flush-to-zero (the defaults, stated):
     "-prec-div=true", "-prec-sqrt=true", "-ftz=false",

@@ -7,7 +7,8 @@
 // bioassay_block_log_likelihood, sample_prior_predictive, estimate_pvalues,
 // compute_cutoff, WeakInfoConfig, CutoffRow/CutoffTable, run_weak_info_test,
 // write_csv.  Every sampler run of the test (2 (K+1) N of them) is one CTA of one
-// launch (vxb_weak_info_test); `workers` is accepted and has no device meaning.
+// launch per GPU in use (vxb_multi_weak_info_test: rows split over the devices, the
+// reference's own task split); `workers` is accepted and has no device meaning.
 // Differences at the boundary: sample_prior_predictive takes the stream's
 // identity (seed) instead of an RngStream&; log_evidence adds the single-run
 // entry (the evidence_of closure of weak_info.cpp:200-215).
@@ -174,7 +175,7 @@ inline CutoffTable run_weak_info_test(const WeakInfoConfig& config) {
     std::vector<double> lambda(2 * rows), gamma(rows);
     std::vector<std::uint8_t> weakly(rows);
     std::vector<std::uint64_t> completed(rows);
-    cuda::check(vxb_weak_info_test(cuda::context(), &cfg, lambda.data(), gamma.data(), weakly.data(),
+    cuda::check(vxb_multi_weak_info_test(cuda::multi(), &cfg, lambda.data(), gamma.data(), weakly.data(),
                                    completed.data(), nullptr));
     CutoffTable table;
     table.alpha = config.alpha;

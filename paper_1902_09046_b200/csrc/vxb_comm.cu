@@ -630,3 +630,32 @@ extern "C" int vxb_multi_abcsmc_run(vxb_multi* m, const vxb_model* model, const 
         });
     });
 }
+
+// run_weak_info_test (weak_info.cpp:163-277) with the hyperparameter rows split over
+// the devices -- the reference's own task parallelism (weak_info.cpp:248-270: `workers`
+// threads over rows); sampler seeds are keyed by (row, dataset), so the table does not
+// depend on the device count.  No collective: every device writes its rows of the
+// caller's host evidence table.
+extern "C" int vxb_multi_weak_info_test(vxb_multi* m, const vxb_weakinfo_cfg* cfg, double* lambda,
+                                        double* gamma, uint8_t* weakly, uint64_t* completed,
+                                        double* evidence) {
+    return guarded([&] {
+        require(m && cfg && lambda && gamma && weakly && completed, "invalid-argument", "null argument");
+        require(cfg->datasets >= 1, "invalid-argument", "need at least one dataset per prior");
+        require(cfg->alpha > 0.0 && cfg->alpha < 1.0, "invalid-argument", "alpha must lie in (0, 1)");
+        const uint64_t rows = cfg->hyper_count + 1, g = m->ctx.size();
+        std::vector<double> own;
+        if (!evidence) {
+            own.resize(rows * cfg->datasets * 2);
+            evidence = own.data();
+        }
+        abi(vxb_weak_info_lambdas(m->ctx[0], cfg, lambda));
+        fork_join(m, [&](int r) {
+            uint64_t b, e;
+            shard_of(rows, g, r, &b, &e);
+            if (e == b) return;
+            abi(vxb_weak_info_evidence(m->ctx[r], cfg, lambda, b, e - b, evidence + b * cfg->datasets * 2));
+        });
+        abi(vxb_weak_info_cutoffs(cfg, evidence, gamma, weakly, completed));
+    });
+}

@@ -281,6 +281,15 @@ class Multi:
                                                   C.byref(out)))
         return res
 
+    def weak_info_test(self, cfg, want_evidence=False):
+        k = cfg.hyper_count + 1
+        lam, gamma = np.zeros((k, 2)), np.zeros(k)
+        weakly, completed = np.zeros(k, dtype=np.uint8), np.zeros(k, dtype=np.uint64)
+        ev = np.zeros((k, cfg.datasets, 2)) if want_evidence else None
+        self._check(self.lib.vxb_multi_weak_info_test(self.handle, C.byref(cfg), _ptr(lam), _ptr(gamma),
+                                                      _ptr(weakly), _ptr(completed), _ptr(ev)))
+        return dict(lambda_=lam, gamma=gamma, weakly=weakly, completed=completed, evidence=ev)
+
     def mlmc_tauleap(self, model, cfg):
         L = cfg.levels
         res = dict(level_mean=np.zeros(L), level_var=np.zeros(L), level_cost=np.zeros(L))

@@ -199,6 +199,11 @@ def test_multi_rank_drivers_on_one_gpu_through_the_loopback_group(ctx, oracle, g
     c1, p1, _ = ctx.ppp_pvalues(M.normal_mean_model(100), lam, ln, 30001, 0, 30001, 1337, 2.9)
     c2, p2 = multi.ppp_pvalues(M.normal_mean_model(100), lam, ln, 30001, 1337, 2.9)
     assert np.array_equal(c1, c2) and np.array_equal(p1, p2)
+    # the weak-informativity test: hyperparameter rows over the ranks
+    wcfg = M.weakinfo_config(hyper_count=6, datasets=9, particles=100, seed=1337)
+    w1, w2 = ctx.weak_info_test(wcfg, want_evidence=True), multi.weak_info_test(wcfg, want_evidence=True)
+    for k in ("lambda_", "gamma", "weakly", "completed", "evidence"):
+        assert np.array_equal(w1[k], w2[k], equal_nan=True), k
     # fewer rows than ranks: some ranks own EMPTY shards
     tiny = multi.abc_prior_predictive(m, M.keying(7), ranks - 1, obs)
     for g, w in zip(tiny, oracle.abc_prior_predictive(m, M.keying(7), ranks - 1, 0, ranks - 1, obs)):
