@@ -155,6 +155,15 @@ int vxb_device_alloc(vxb_ctx* ctx, size_t bytes, void** out);
 int vxb_device_free(vxb_ctx* ctx, void* p);
 int vxb_copy(vxb_ctx* ctx, void* dst, const void* src, size_t bytes); /* any direction */
 
+/* glibc ships two builds of its exp on x86-64 (FMA-contracted for CPUs with FMA + AVX2,
+ * plain otherwise; they differ in the last ulp of about one result in 10^3).  vxb_init
+ * probes the live std::exp of the process and the device reproduces the matching build in
+ * vxb_ess / vxb_logsumexp / vxb_resample_multinomial: *variant = 0 FMA build, 1 plain
+ * build, -1 neither matched (a different libm: the FMA build is used and those three
+ * entry points agree with the host to an ulp instead of bit for bit).  ctx == NULL:
+ * probe the calling process now (host only, no GPU needed). */
+int vxb_host_exp_variant(vxb_ctx* ctx, int* variant);
+
 /* Guard mode (diagnostics; environment VXB_GUARD=1 when vxb_init runs): every
  * library-owned device allocation (staging, scratch, arenas) is bracketed by 256-byte
  * canary zones that are verified when it is released; a violation prints a line
@@ -212,8 +221,9 @@ int vxb_rng_fast_stats(vxb_ctx* ctx, int precision, uint64_t seed, uint64_t firs
  * 5 pow_pos (x = base, y = exponent; y ignored otherwise); and of the
  * throughput-mode functions, for accuracy tests: fn 6 log2 (x > 0 normal),
  * 7 2^x (|x| < 1000), 8 1/x (normal x); fn 9: exp exactly as the host libm
- * evaluates it (glibc >= 2.28, FMA build) -- what std::exp returns in
- * smc.cpp:214,278,299 and numeric.cpp:16-17, bit for bit. */
+ * evaluates it (glibc >= 2.28) -- what std::exp returns in smc.cpp:214,278,299 and
+ * numeric.cpp:16-17, bit for bit: the build of the algorithm this host's libm runs
+ * (vxb_host_exp_variant); fn 10 / 11: its FMA / plain build regardless of the host. */
 int vxb_fastmath_eval(vxb_ctx* ctx, int fn, const double* x, const double* y, uint64_t n,
                       double* out);
 /* partition (blocked.cpp:34-63): writes workers pairs [begin,end). Host-side. */

@@ -287,19 +287,21 @@ class Oracle(_Base):
         return out.value
 
     # ---- the restatement of the host libm's exp (pins csrc/vxb_libmexp.cuh)
-    def exp_restated(self, x):
-        """(restated exp, live std::exp) of every x."""
+    def exp_restated(self, x, plain_build=False):
+        """(restated exp, live std::exp) of every x.  plain_build: the library's build
+        without FMA contraction (what its ifunc selects on CPUs without FMA + AVX2)."""
         x = _f64(x)
         out, live = np.zeros_like(x), np.zeros_like(x)
-        self._call("exp_restated", _ptr(x), u64(x.size), _ptr(out), _ptr(live))
+        self._call("exp_restated", _ptr(x), u64(x.size), _ptr(out), _ptr(live), i32(1 if plain_build else 0))
         return out, live
 
-    def exp_restated_sweep(self, seed, n, lo, hi, threads=None):
+    def exp_restated_sweep(self, seed, n, lo, hi, threads=None, plain_build=False):
         """Number of pseudo-random arguments in [lo, hi) on which the restatement and
         the live std::exp differ bitwise, and the first such argument (NaN if none)."""
         m, first = u64(), f64(float("nan"))
         self._call("exp_restated_sweep", u64(seed), u64(n), f64(lo), f64(hi),
-                   C.c_uint(threads or (os.cpu_count() or 1)), C.byref(m), C.byref(first))
+                   C.c_uint(threads or (os.cpu_count() or 1)), C.byref(m), C.byref(first),
+                   i32(1 if plain_build else 0))
         return m.value, first.value
 
     # ---- SMC pieces

@@ -874,11 +874,17 @@ static const ExpEntry kExpTable[128] = {
 #include "../paper_1902_09046_b200/csrc/vxb_libm_exp_entries.inc"
 #undef VXB_EXP_PAIR
 };
-static double exp_restated_special(double tmp, std::uint64_t sbits, std::uint64_t ki) {
+// fused = true: the FMA build of the library (a*b + c contracted where the x86-64 FMA
+// build contracts it); fused = false: its plain build (this file is compiled with
+// -ffp-contract=off, so a * b + c rounds twice).
+static double exp_mad(bool fused, double a, double b, double c) {
+    return fused ? std::fma(a, b, c) : a * b + c;
+}
+static double exp_restated_special(bool fused, double tmp, std::uint64_t sbits, std::uint64_t ki) {
     if ((ki & 0x80000000ULL) == 0) {
         sbits -= 1009ULL << 52;
         const double scale = bit_cast<double>(sbits);
-        return 0x1p1009 * std::fma(scale, tmp, scale);
+        return 0x1p1009 * exp_mad(fused, scale, tmp, scale);
     }
     sbits += 1022ULL << 52;
     const double scale = bit_cast<double>(sbits);
@@ -894,7 +900,7 @@ static double exp_restated_special(double tmp, std::uint64_t sbits, std::uint64_
     }
     return 0x1p-1022 * y;
 }
-static double exp_restated(double x) {
+static double exp_restated(double x, bool fused = true) {
     const std::uint32_t abstop = static_cast<std::uint32_t>(bit_cast<std::uint64_t>(x) >> 52) & 0x7ffu;
     bool special = false;
     if (abstop - 0x3c9u >= 0x3fu) {
@@ -906,30 +912,30 @@ static double exp_restated(double x) {
         }
         special = true;
     }
-    double kd = std::fma(x, 0x1.71547652b82fep+7, 0x1.8p+52);
+    double kd = exp_mad(fused, x, 0x1.71547652b82fep+7, 0x1.8p+52);
     const std::uint64_t ki = bit_cast<std::uint64_t>(kd);
     kd -= 0x1.8p+52;
-    double r = std::fma(kd, -0x1.62e42fefa0000p-8, x);
-    r = std::fma(kd, -0x1.cf79abc9e3b3ap-47, r);
+    double r = exp_mad(fused, kd, -0x1.62e42fefa0000p-8, x);
+    r = exp_mad(fused, kd, -0x1.cf79abc9e3b3ap-47, r);
     const ExpEntry e = kExpTable[ki & 127u];
     const std::uint64_t sbits = e.sbits + (ki << 45);
     const double tail = bit_cast<double>(e.tail);
     const double r2 = r * r;
-    const double p23 = std::fma(0x1.555555555543cp-3, r, 0x1.ffffffffffdbdp-2);
+    const double p23 = exp_mad(fused, 0x1.555555555543cp-3, r, 0x1.ffffffffffdbdp-2);
     const double t1 = tail + r;
-    const double p45 = std::fma(r, 0x1.1111167a4d017p-7, 0x1.55555cf172b91p-5);
-    const double t2 = std::fma(p23, r2, t1);
-    const double tmp = std::fma(r2 * r2, p45, t2);
-    if (special) return exp_restated_special(tmp, sbits, ki);
+    const double p45 = exp_mad(fused, r, 0x1.1111167a4d017p-7, 0x1.55555cf172b91p-5);
+    const double t2 = exp_mad(fused, p23, r2, t1);
+    const double tmp = exp_mad(fused, r2 * r2, p45, t2);
+    if (special) return exp_restated_special(fused, tmp, sbits, ki);
     const double scale = bit_cast<double>(sbits);
-    return std::fma(scale, tmp, scale);
+    return exp_mad(fused, scale, tmp, scale);
 }
 
 // libm exp restatement: out[i] = exp_restated(x[i]); libm[i] = std::exp(x[i]) (optional)
-int vxo_exp_restated(const double* x, std::uint64_t n, double* out, double* libm) {
+int vxo_exp_restated(const double* x, std::uint64_t n, double* out, double* libm, int plain_build) {
     return guarded([&] {
         for (std::uint64_t i = 0; i < n; ++i) {
-            out[i] = exp_restated(x[i]);
+            out[i] = exp_restated(x[i], plain_build == 0);
             if (libm) libm[i] = std::exp(x[i]);
         }
     });
@@ -938,7 +944,8 @@ int vxo_exp_restated(const double* x, std::uint64_t n, double* out, double* libm
 // differ between the restatement and the live std::exp (bitwise; NaN never occurs);
 // *first_bad receives the first offending argument.
 int vxo_exp_restated_sweep(std::uint64_t seed, std::uint64_t n, double lo, double hi,
-                           unsigned threads, std::uint64_t* mismatches, double* first_bad) {
+                           unsigned threads, std::uint64_t* mismatches, double* first_bad,
+                           int plain_build) {
     return guarded([&] {
         if (threads == 0) threads = 1;
         std::vector<std::uint64_t> bad(threads, 0);
@@ -949,7 +956,7 @@ int vxo_exp_restated_sweep(std::uint64_t seed, std::uint64_t n, double lo, doubl
                 for (std::uint64_t i = t; i < n; i += threads) {
                     const double u = static_cast<double>(splitmix64(seed + i) >> 11) * 0x1p-53;
                     const double x = lo + u * (hi - lo);
-                    const double a = exp_restated(x), b = std::exp(x);
+                    const double a = exp_restated(x, plain_build == 0), b = std::exp(x);
                     if (bit_cast<std::uint64_t>(a) != bit_cast<std::uint64_t>(b)) {
                         if (bad[t]++ == 0) firsts[t] = x;
                     }

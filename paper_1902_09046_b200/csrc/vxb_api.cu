@@ -109,7 +109,7 @@ __global__ void fill_gaussian_kernel(uint64_t key, uint64_t pos, uint64_t n, dou
 }
 
 __global__ void fastmath_kernel(int fn, const double* x, const double* y, uint64_t n, double* out,
-                                const double2* fast_table) {
+                                const double2* fast_table, int exp_variant) {
     // functions 6-8: the throughput-mode log2 / 2^z / reciprocal on the shared tables
     __shared__ double2 s_tab[kFastTableSize];
     if (fn >= 6 && fn <= 8) {
@@ -130,7 +130,9 @@ __global__ void fastmath_kernel(int fn, const double* x, const double* y, uint64
         case 6: r = fast_log2(a, s_tab); break;
         case 7: r = fast_exp2(a, s_tab); break;
         case 8: r = fast_rcp(a); break;
-        default: r = libm_exp(a); break;
+        case 9: r = libm_exp(a, exp_variant); break;  // the variant of this host
+        case 10: r = libm_exp_t<true>(a); break;     // FMA build
+        default: r = libm_exp_t<false>(a); break;    // plain build
     }
     out[i] = r;
 }
@@ -167,6 +169,7 @@ extern "C" int vxb_init(vxb_ctx** out, int device) {
         VXB_CUDA(cudaMemPoolCreate(&ctx->pool, &props));
         uint64_t threshold = ~0ull;
         VXB_CUDA(cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+        ctx->exp_variant = host_exp_variant();
         const char* guard = getenv("VXB_GUARD");
         ctx->guard = guard && *guard && *guard != '0';
         double table[2 * kFastTableSize];
@@ -223,6 +226,13 @@ extern "C" int vxb_guard_report(vxb_ctx* ctx, int selftest, unsigned long long* 
             ctx->guard_violations = before;  // the provoked one does not count
         }
         *violations = ctx->guard_violations;
+    });
+}
+
+extern "C" int vxb_host_exp_variant(vxb_ctx* ctx, int* variant) {
+    return guarded([&] {
+        require(variant != nullptr, "invalid-argument", "null argument");
+        *variant = ctx ? ctx->exp_variant : host_exp_variant();  // no context: probe this process
     });
 }
 
@@ -385,7 +395,7 @@ extern "C" int vxb_fastmath_eval(vxb_ctx* ctx, int fn, const double* x, const do
                                  uint64_t n, double* out) {
     return guarded([&] {
         use(ctx);
-        require(fn >= 0 && fn <= 9, "invalid-argument", "unknown fastmath function");
+        require(fn >= 0 && fn <= 11, "invalid-argument", "unknown fastmath function");
         if (n == 0) return;
         require(x && out && (fn != 5 || y), "invalid-argument", "null argument");
         Staged d_x(ctx, x, n * 8, true, false);
@@ -394,7 +404,8 @@ extern "C" int vxb_fastmath_eval(vxb_ctx* ctx, int fn, const double* x, const do
         {
             LaunchScope scope(ctx, VXB_K_MISC);
             fastmath_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
-                fn, d_x.as<double>(), d_y.as<double>(), n, d_out.as<double>(), ctx->log_table);
+                fn, d_x.as<double>(), d_y.as<double>(), n, d_out.as<double>(), ctx->log_table,
+                ctx->exp_variant);
             check_launch("fastmath_kernel");
         }
         d_out.finish();

@@ -73,6 +73,9 @@ struct vxb_ctx {
     // where compute-sanitizer is not available
     bool guard = false;
     unsigned long long guard_violations = 0;
+    // which build of the host libm's exp the device reproduces (csrc/vxb_libmexp.cuh):
+    // 0 FMA build, 1 plain build, -1 neither matched the live std::exp (FMA build used)
+    int exp_variant = 0;
 };
 
 namespace vxb {

@@ -71,13 +71,13 @@ constexpr int kSeqThreads = 128;
 template <bool kCum>
 __global__ void __launch_bounds__(kSeqThreads)
 seq_expsum_kernel(const double* __restrict__ x, const double* __restrict__ mx, uint64_t n,
-                  double* __restrict__ cum, double* __restrict__ sums /* 2 */) {
+                  double* __restrict__ cum, double* __restrict__ sums /* 2 */, int exp_variant) {
     __shared__ double buf[2][kSeqTile];
     const double m = *mx;
     const uint32_t tid = threadIdx.x;
     const uint64_t tiles = (n + kSeqTile - 1) / kSeqTile;
     for (uint64_t k = tid; k < min(static_cast<uint64_t>(kSeqTile), n); k += kSeqThreads)
-        buf[0][k] = libm_exp(__dsub_rn(x[k], m));
+        buf[0][k] = libm_exp(__dsub_rn(x[k], m), exp_variant);
     __syncthreads();
     double s1 = 0.0, s2 = 0.0;
     for (uint64_t t = 0; t < tiles; ++t) {
@@ -122,7 +122,7 @@ seq_expsum_kernel(const double* __restrict__ x, const double* __restrict__ mx, u
             const uint32_t nlen = static_cast<uint32_t>(min(static_cast<uint64_t>(kSeqTile), n - n0));
             double* nxt = buf[(t + 1) & 1];
             for (uint32_t k = tid - 32; k < nlen; k += kSeqThreads - 32)
-                nxt[k] = libm_exp(__dsub_rn(x[n0 + k], m));
+                nxt[k] = libm_exp(__dsub_rn(x[n0 + k], m), exp_variant);
         }
         __syncthreads();
         if (kCum) {
@@ -160,10 +160,12 @@ void max_and_expsums(vxb_ctx* ctx, const double* x_dev, uint64_t n, double* mx, 
         LaunchScope scope(ctx, VXB_K_RESAMPLE);
         if (cum_dev)
             seq_expsum_kernel<true><<<1, kSeqThreads, 0, ctx->stream>>>(x_dev, res.as<double>(), n,
-                                                                        cum_dev, res.as<double>() + 1);
+                                                                        cum_dev, res.as<double>() + 1,
+                                                                        ctx->exp_variant);
         else
             seq_expsum_kernel<false><<<1, kSeqThreads, 0, ctx->stream>>>(x_dev, res.as<double>(), n, nullptr,
-                                                                         res.as<double>() + 1);
+                                                                         res.as<double>() + 1,
+                                                                         ctx->exp_variant);
         check_launch("seq_expsum_kernel");
     }
     VXB_CUDA(cudaMemcpyAsync(h, res.as<double>(), 24, cudaMemcpyDeviceToHost, ctx->stream));

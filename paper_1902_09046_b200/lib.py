@@ -115,6 +115,15 @@ def _raise_last():
     raise VxbError(load().vxb_last_error().decode())
 
 
+def host_exp_variant():
+    """Probe of the calling process' std::exp (no GPU needed): 0 FMA build of the
+    library's algorithm, 1 plain build, -1 neither."""
+    v = C.c_int()
+    if load().vxb_host_exp_variant(None, C.byref(v)):
+        _raise_last()
+    return v.value
+
+
 def device_count():
     n = C.c_int()
     if load().vxb_device_count(C.byref(n)):
@@ -355,6 +364,12 @@ class Context:
         self._check(self.lib.vxb_fma_peak(self.handle, i32(precision), u32(iters), C.byref(tf),
                                           C.byref(ms)))
         return tf.value, ms.value
+
+    def host_exp_variant(self):
+        """Which build of the host libm's exp the device reproduces: 0 FMA, 1 plain, -1 none."""
+        v = C.c_int()
+        self._check(self.lib.vxb_host_exp_variant(self.handle, C.byref(v)))
+        return v.value
 
     def guard_report(self, selftest=False):
         """Guard mode (VXB_GUARD=1): (violations so far, self-test detected or None)."""

@@ -158,3 +158,16 @@ def test_multi_gpu_entry_points_argument_errors(so):
         assert e.value.code == "device-error"
     # the library finds NCCL by itself (dlopen); the version is the loaded library's
     assert lib.comm_version() >= 21800
+
+
+def test_host_libm_exp_probe(so):
+    """vxb_init probes which build of glibc's exp this process runs so that the device can
+    reproduce it (csrc/vxb_libmexp.cuh).  Here: the FMA build; with the ifunc told to
+    ignore FMA / AVX2 (GLIBC_TUNABLES -- a host CPU without FMA) the plain build."""
+    import subprocess
+    import sys
+    assert lib.host_exp_variant() == 0
+    code = "import sys; sys.path.insert(0, %r); from paper_1902_09046_b200 import lib; print('variant', lib.host_exp_variant())" % ROOT
+    run = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                         env=dict(os.environ, GLIBC_TUNABLES="glibc.cpu.hwcaps=-AVX2,-FMA"))
+    assert run.returncode == 0 and "variant 1" in run.stdout, run.stdout + run.stderr[-800:]

@@ -85,6 +85,42 @@ def test_device_exp_is_the_host_libm_exp(ctx, oracle):
     assert np.array_equal(dev.view(np.uint64), live.view(np.uint64))
     assert np.array_equal(dev.view(np.uint64), restated.view(np.uint64))
     assert np.isnan(ctx.fastmath(9, np.array([np.nan]))[0])
+    # the library's other build (CPUs without FMA): fn 11 against its own restatement
+    assert ctx.host_exp_variant() == 0
+    assert np.array_equal(ctx.fastmath(10, x).view(np.uint64), dev.view(np.uint64))
+    plain, _ = oracle.exp_restated(x, plain_build=True)
+    dev_plain = ctx.fastmath(11, x)
+    assert np.array_equal(dev_plain.view(np.uint64), plain.view(np.uint64))
+    assert 100 < (dev_plain.view(np.uint64) != dev.view(np.uint64)).sum() < 50_000
+
+
+def test_resample_follows_the_host_libm_build(golden):
+    """A host whose libm runs the PLAIN build of exp (no FMA: simulated with
+    GLIBC_TUNABLES in a subprocess): vxb_init detects it and resample_multinomial / ess /
+    logsumexp stay bit-identical to that host's reference arithmetic."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = """
+import sys
+sys.path.insert(0, %r)
+import numpy as np
+from oracle.pyoracle import Oracle
+from paper_1902_09046_b200 import lib
+ctx, o = lib.Context(0), Oracle()
+assert ctx.host_exp_variant() == 1, ctx.host_exp_variant()
+rs = np.random.RandomState(9)
+for n, spread in ((100000, 3.0), (40001, 40.0)):
+    lw, parts = rs.normal(size=n) * spread, rs.normal(size=(n, 3))
+    g, h = ctx.resample_multinomial(lw, parts, 77, 9), o.resample_multinomial(lw, parts, 77, 9)
+    assert np.array_equal(g[1], h[1]) and np.array_equal(g[0], h[0])
+    assert ctx.ess(lw) == o.ess(lw) and ctx.logsumexp(lw) == o.logsumexp(lw)
+print("plain host ok")
+""" % root
+    run = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                         env=dict(os.environ, GLIBC_TUNABLES="glibc.cpu.hwcaps=-AVX2,-FMA"))
+    assert run.returncode == 0 and "plain host ok" in run.stdout, run.stdout[-800:] + run.stderr[-1500:]
 
 
 def test_ess_logsumexp_resample(ctx, oracle, golden):

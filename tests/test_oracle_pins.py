@@ -9,6 +9,7 @@
    examples for the pieces whose reference tests are empty.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -348,3 +349,30 @@ def test_libm_exp_restatement_equals_live_libm(oracle):
     assert np.array_equal(got.view(np.uint64), live.view(np.uint64))
     assert np.array_equal(live[:11].view(np.uint64),
                           np.array([math.exp(v) for v in x[:11]]).view(np.uint64))
+    # the two builds of the library differ (about one argument in 10^3): this process
+    # runs the FMA build, so the plain restatement must NOT match everywhere ...
+    bad_plain, _ = oracle.exp_restated_sweep(1, 2_000_000, -50.0, 0.0, plain_build=True)
+    assert 100 < bad_plain < 20_000
+
+
+def test_libm_exp_plain_build_restatement_equals_live_libm_without_fma():
+    """... and in a process whose libm is told to ignore FMA / AVX2 (GLIBC_TUNABLES, the
+    ifunc then picks the plain build -- what a host CPU without FMA runs), the PLAIN
+    restatement equals the live std::exp bit for bit and the FMA one does not."""
+    import subprocess
+    import sys
+    code = """
+import sys
+sys.path.insert(0, %r)
+from oracle.pyoracle import Oracle
+o = Oracle()
+for lo, hi, n in ((-50.0, 0.0, 4000000), (-760.0, -690.0, 1000000), (-1100.0, 800.0, 1000000), (-1e-3, 1e-3, 500000)):
+    bad, first = o.exp_restated_sweep(77 + n, n, lo, hi, plain_build=True)
+    assert bad == 0, (lo, hi, first)
+bad_fma, _ = o.exp_restated_sweep(1, 2000000, -50.0, 0.0, plain_build=False)
+assert 100 < bad_fma < 20000, bad_fma
+print("plain build ok", bad_fma)
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GLIBC_TUNABLES="glibc.cpu.hwcaps=-AVX2,-FMA")
+    run = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, env=env)
+    assert run.returncode == 0 and "plain build ok" in run.stdout, run.stdout[-800:] + run.stderr[-1500:]
