@@ -136,7 +136,8 @@ typedef struct vxb_profile {
 int vxb_abi_version(void);
 /* Philox4x32 rounds of the throughput generator in this build: 10 (the product
  * library) or 7 (the opt-in build, -DVXB_FAST_ROUNDS=7: the minimum Salmon et al.
- * report as Crush-resistant; +8% on the headline kernel; profiles/r2_philox7.json). */
+ * report as Crush-resistant; +11.6% on the fp64 headline kernel, +16% in fp32;
+ * profiles/r2_philox7.json). */
 int vxb_fast_generator_rounds(void);
 /* device < 0: use the current CUDA device. */
 int vxb_init(vxb_ctx** ctx, int device);
