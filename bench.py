@@ -353,9 +353,18 @@ def main():
     def host_step(model):
         begin, end = D.shard_range(n_total, world, rank)
         cap = max(1024, int((end - begin) * 0.01))
+        # the caller's HOST buffers, pinned and reused by every step (a pageable,
+        # freshly zeroed 40 MB set per step costs 2 ms of host time against 354 ms)
+        real = torch.float32 if model.precision == A.VXB_F32 else torch.float64
+        h_idx = torch.empty(cap, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
+        h_par = torch.empty((cap, model.dim), dtype=real, pin_memory=True).numpy()
+        h_rho = torch.empty(cap, dtype=real, pin_memory=True).numpy()
 
         def fn(s):  # public host-buffer call: H2D of the observation, D2H of the accepted rows
-            return ctx.abc_reject(model, M.keying(1337 + s), n_total, begin, end - begin, obs, eps, cap)
+            k, _, _, _ = ctx.abc_reject(model, M.keying(1337 + s), n_total, begin, end - begin, obs,
+                                        eps, cap, idx=h_idx, params=h_par, rho=h_rho)
+            k = min(k, cap)
+            return k, h_idx[:k], h_par[:k], h_rho[:k]
         return fn
 
     # ---- headline: device-resident

@@ -518,10 +518,10 @@ class Context:
         obs = np.ascontiguousarray(observed, dtype=np.float64)
         dt = np.float32 if model.precision == A.VXB_F32 else np.float64
         own = idx is None
-        if own:
-            idx = np.zeros(cap, dtype=np.uint64)
-            params = np.zeros((cap, model.dim), dtype=dt)
-            rho = np.zeros(cap, dtype=dt)
+        if own:  # every valid row is overwritten: no need to zero cap rows per call
+            idx = np.empty(cap, dtype=np.uint64)
+            params = np.empty((cap, model.dim), dtype=dt)
+            rho = np.empty(cap, dtype=dt)
         if n_accepted is not None:
             # asynchronous form: the count is written to device memory, no host sync
             self._check(self.lib.vxb_abc_reject(self.handle, C.byref(model), C.byref(key),
