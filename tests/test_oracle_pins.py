@@ -376,3 +376,19 @@ print("plain build ok", bad_fma)
     env = dict(os.environ, GLIBC_TUNABLES="glibc.cpu.hwcaps=-AVX2,-FMA")
     run = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, env=env)
     assert run.returncode == 0 and "plain build ok" in run.stdout, run.stdout[-800:] + run.stderr[-1500:]
+
+
+def test_libm_exp_table_is_what_the_generator_emits():
+    """csrc/vxb_libm_exp_entries.inc is generated (exact integer arithmetic); the committed
+    file must be exactly the generator's output, and entry 0 / 64 are 1 and sqrt(2)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "scripts", "gen_libm_exp_table.py")],
+                         capture_output=True, text=True, check=True).stdout
+    committed = open(os.path.join(root, "paper_1902_09046_b200", "csrc", "vxb_libm_exp_entries.inc")).read()
+    assert out == committed
+    rows = [l for l in committed.splitlines() if l.startswith("VXB_EXP_PAIR")]
+    assert len(rows) == 128 and "0x3ff0000000000000ull" in rows[0]
+    h64 = int(rows[64].split(",")[1].strip(" )ull").replace("ull", ""), 16) + ((64 << 52) // 128)
+    assert np.array([h64], dtype=np.uint64).view(np.float64)[0] == math.sqrt(2.0)
