@@ -449,6 +449,7 @@ def main():
         line["variants"] = variants
         if rank == 0 and world == 1:
             line["configs"] = all_configs(ctx, timed, obs, local)
+            line["opt_in_philox7"] = philox7_arm(args)
             line["cpu_baseline"] = cpu_baseline(args, obs, eps)
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -598,6 +599,28 @@ def all_configs(ctx, timed, obs, device):
                          "note": "bit-exact: host-libm exp + strictly sequential running sum "
                                  "(one dependent DADD per particle)"})
     return res
+
+
+def philox7_arm(args):
+    """The documented opt-in build (Philox4x32-7 throughput generator, build.py --rounds7)
+    through this same script in a subprocess, so that its number sits under the same
+    clock sampler: headline value, kernel fraction, clocks.  Not the product default."""
+    from paper_1902_09046_b200 import build
+    if not os.path.exists(build.LIB_ROUNDS7) or os.environ.get("VXB_LIBRARY"):
+        return None
+    try:
+        run = subprocess.run([sys.executable, os.path.abspath(__file__), "--gpus", "1", "--steps", "3",
+                              "--warmup", "3", "--no-extras", "--particles", str(args.particles)],
+                             capture_output=True, text=True, timeout=300,
+                             env=dict(os.environ, VXB_LIBRARY=build.LIB_ROUNDS7))
+        b = json.loads([l for l in run.stdout.splitlines() if l.startswith("{")][-1])
+        return {"philox4x32_rounds": b["config"]["philox4x32_rounds"], "value": b["value"], "unit": b["unit"],
+                "ms_per_step": b["ms_per_step"], "e2e": b["e2e"]["value"],
+                "frac_of_nominal": b["roofline"]["frac_of_nominal"], "clocks": b["clocks"],
+                "accepted_per_step": b["config"]["accepted_per_step"],
+                "note": "opt-in build, statistics in profiles/r2_philox7.json; the product library runs 10 rounds"}
+    except Exception as e:  # the opt-in arm must never cost the main line
+        return {"error": repr(e)}
 
 
 def cpu_baseline(args, obs, eps):
