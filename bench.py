@@ -449,6 +449,7 @@ def main():
         line["variants"] = variants
         if rank == 0 and world == 1:
             line["configs"] = all_configs(ctx, timed, obs, local)
+            cpu_configs(line["configs"], obs)
             line["opt_in_philox7"] = philox7_arm(args)
             line["cpu_baseline"] = cpu_baseline(args, obs, eps)
     if rank == 0:
@@ -599,6 +600,91 @@ def all_configs(ctx, timed, obs, device):
                          "note": "bit-exact: host-libm exp + strictly sequential running sum "
                                  "(one dependent DADD per particle)"})
     return res
+
+
+def cpu_configs(configs, obs):
+    """The CPU path of every workload on this box's host cores, on a BOUNDED sample each
+    (2-5 s of CPU work; the sample is stated), attached to the matching `configs` entries:
+    the unmodified reference (oracle/_ref) where it has the code -- the ABC sampler on
+    the logistic hooks + select_epsilon, toggle ABC, the weak-informativity test, TB ABC,
+    resample_multinomial -- and this repository's CPU restatement (oracle port) for the
+    workloads the reference lacks (configs 2, 3, 4).  Reported baselines, not targets."""
+    from oracle.pyoracle import Oracle, Ref
+    from paper_1902_09046_b200 import _abi as A, models as M
+    cores = os.cpu_count() or 1
+    o = Oracle(threads=cores)
+    r = Ref() if Ref.available() else None
+
+    def attach(names, kind, sample, units, seconds, unit):
+        for name in names:
+            if name in configs:
+                cpu_rate = units / seconds
+                configs[name]["cpu"] = {"kind": kind, "cores": cores, "sample": sample,
+                                        "seconds": seconds, "units_per_s": cpu_rate, "unit": unit,
+                                        "gpu_over_cpu": configs[name]["units_per_s"] / cpu_rate}
+
+    def clock(fn):
+        t0 = time.perf_counter()
+        out = fn()
+        return out, time.perf_counter() - t0
+
+    m = M.logistic_model()
+    try:
+        # config 0 on 3e5 of its 1e6 rows: prior-predictive set + select_epsilon
+        n0 = 300_000
+        if r is not None:
+            (_, dt) = clock(lambda: r.select_epsilon(*r.logistic_abc(m, n0, cores, 1, 1337, obs)[2:4], 1e-3))
+            kind = "reference"
+        else:
+            (_, dt) = clock(lambda: o.select_epsilon(*o.abc_prior_predictive(m, M.keying(1337), n0, 0, n0, obs)[2:4], 1e-3))
+            kind = "port"
+        attach(("config0_exact", "config0_fast"), kind, "3e5 of 1e6 sims + select_epsilon over them", n0, dt, "sims")
+        # config 2: 64 lambdas x 1e5 of the 1e6 datasets
+        nl, mt, nd = 64, 100_000, 100
+        lam = np.array(M.lambda_grid(nl))
+        ln = np.array([-0.5 * math.log(2.0 * math.pi * (l * l + 1.0 / nd)) for l in lam])
+        (_, dt) = clock(lambda: o.ppp_pvalues(M.normal_mean_model(nd), lam, ln, mt, 0, mt, 1337, 2.9))
+        attach(("config2_exact", "config2_fast"), "port", "64 lambdas x 1e5 of 1e6 datasets", nl * mt, dt, "datasets")
+        # config 3: N = 5e3 x 10 generations (the weights are O(N^2): not a linear sample)
+        cfg = A.vxb_abcsmc_cfg()
+        cfg.particles, cfg.generations = 5_000, 10
+        cfg.quantile, cfg.kernel_scale, cfg.jitter, cfg.round_size, cfg.max_rounds, cfg.seed = 0.5, 2.0, 1e-10, 0, 0, 1337
+        (_, dt) = clock(lambda: o.abcsmc_run(m, cfg, obs))
+        for name in ("config3_exact", "config3_fast"):
+            if name in configs:
+                configs[name]["cpu"] = {"kind": "port", "cores": cores, "seconds": dt,
+                                        "sample": "N = 5e3 x 10 generations (1/20 of the particles, 1/400 "
+                                                  "of the weight pairs): not comparable unit for unit"}
+        # config 4: 6 levels x 2e3 of the 1e6 paths
+        mc = A.vxb_mlmc_cfg()
+        mc.levels, mc.refine, mc.tau0, mc.t_end, mc.paths, mc.seed = 6, 4, 1.0, 30.0, 2_000, 1337
+        fine = [30 * 4 ** l for l in range(6)]
+        steps = mc.paths * sum(f if l == 0 else f + f // 4 for l, f in enumerate(fine))
+        (_, dt) = clock(lambda: o.mlmc_tauleap(M.mm_tauleap_model(), mc))
+        attach(("config4_exact", "config4_fast"), "port", "6 levels x 2e3 of 1e6 paths", steps, dt, "path-steps")
+        if r is not None:
+            # toggle ABC: 32 of the 8064 samples at the paper's C = 8000, T = 600
+            n_t = 32
+            (_, dt) = clock(lambda: r.toggle_abc(600, 8000, n_t, cores, 4, 1337))
+            attach(("toggle_exact", "toggle_fast"), "reference", "32 of 8064 samples (C = 8000, T = 600)",
+                   n_t * 8000 * 599, dt, "cell-steps")
+            # weak-informativity test: K = 10, N = 40 (880 of the 320 800 sampler runs)
+            (_, dt) = clock(lambda: r.weak_info_test(10, 40, 500, workers=cores, seed=1337))
+            attach(("weakinfo_exact", "weakinfo_fast"), "reference", "K = 10, N = 40: 880 of 320 800 sampler runs",
+                   2 * 11 * 40, dt, "sampler-runs")
+            # TB Gillespie ABC: 4096 of the 1e6 rows
+            tb_obs = r.tb_observed(10, 10.0, 10000.0, 1337)
+            (_, dt) = clock(lambda: r.tb_abc_particle(10, 10.0, 10000.0, 0, 4096, 1337, tb_obs))
+            attach(("tb_gillespie",), "reference", "4096 of 1e6 rows", 4096, dt, "rows")
+            # resample_multinomial, full size, single thread (as the reference runs it)
+            rs = np.random.RandomState(9)
+            lw, parts = rs.normal(size=100_000) * 3, rs.normal(size=(100_000, 3))
+            r.resample_multinomial(lw, parts, 77, 9)
+            (_, dt) = clock(lambda: [r.resample_multinomial(lw, parts, 77, 9) for _ in range(5)])
+            attach(("resample_multinomial_1e5",), "reference", "full size, one thread, mean of 5 calls", 100_000, dt / 5, "particles")
+            configs["resample_multinomial_1e5"]["cpu"]["cores"] = 1
+    except Exception as e:   # a CPU figure must never cost the line
+        configs["cpu_error"] = repr(e)
 
 
 def philox7_arm(args):
