@@ -471,7 +471,7 @@ def all_configs(ctx, timed, obs, device):
     peak = NOMINAL_PEAK["f64"] * 1e12
     res = {}
 
-    def run(name, fn, units, unit, flops_per_unit=None, target_s=0.6, extra=None):
+    def run(name, fn, units, unit, flops_per_unit=None, target_s=0.6, extra=None, pipe="f64"):
         # calibrate the repetition count on one untimed pass (which is also a warm-up)
         ms1, _ = timed(lambda s: fn(), 1, 1)
         k = max(3, min(200, int(math.ceil(target_s * 1e3 / max(ms1, 1e-3)))))
@@ -483,7 +483,8 @@ def all_configs(ctx, timed, obs, device):
         if flops_per_unit:
             e["flops_per_unit"] = flops_per_unit
             e["tflops_algorithmic"] = units * flops_per_unit / (per * 1e-3) / 1e12
-            e["frac_of_nominal_fp64"] = units * flops_per_unit / (per * 1e-3) / peak
+            e[f"frac_of_nominal_fp{pipe[1:]}"] = (units * flops_per_unit / (per * 1e-3) /
+                                                  (NOMINAL_PEAK[pipe] * 1e12))
         if extra:
             e.update(extra(out))
         res[name] = e
@@ -548,10 +549,12 @@ def all_configs(ctx, timed, obs, device):
     fine = [30 * 4 ** l for l in range(6)]
     steps = mc.paths * sum(f if l == 0 else f + f // 4 for l, f in enumerate(fine))
     flops = mc.paths * (fine[0] * 130 + sum(f * 370 for f in fine[1:]))
-    for name, rng in (("config4_exact", A.VXB_RNG_REF), ("config4_fast", A.VXB_RNG_FAST)):
-        mm = M.mm_tauleap_model(rng=rng)
+    for name, rng, prec in (("config4_exact", A.VXB_RNG_REF, A.VXB_F64), ("config4_fast", A.VXB_RNG_FAST, A.VXB_F64),
+                            ("config4_fast_f32", A.VXB_RNG_FAST, A.VXB_F32)):
+        mm = M.mm_tauleap_model(rng=rng, precision=prec)
         run(name, lambda mm=mm: ctx.mlmc_tauleap(mm, mc), steps, "path-steps", flops / steps,
-            target_s=1.5, extra=lambda o: {"estimate": o["estimate"], "std_error": o["std_error"]})
+            target_s=1.5, extra=lambda o: {"estimate": o["estimate"], "std_error": o["std_error"]},
+            pipe="f32" if prec == A.VXB_F32 else "f64")
 
     # ---- the paper's toggle-switch ABC: N = 8064, C = 8000, T = 600
     n_t, c_t, t_t = 8064, 8000, 600

@@ -79,7 +79,9 @@ enum { VXB_KEY_PARTICLE = 0, VXB_KEY_WORKER = 1 };
  * VXB_MODEL_NORMAL_MEAN   y_i ~ N(theta,1), i<steps, theta ~ N(0, lambda^2)
  *   steps = n (data per dataset).
  * VXB_MODEL_MM_TAULEAP    S+E->C (k1), C->S+E (k2), C->E+P (k3)
- *   consts[0..3] = initial (S,E,C,P), consts[4..6] = (k1,k2,k3).
+ *   consts[0..3] = initial (S,E,C,P), consts[4..6] = (k1,k2,k3).  precision VXB_F32
+ *   (with VXB_RNG_FAST only): propensities and the Poisson inversion in float, exp by one
+ *   MUFU; the state stays integer.  Statistically validated, like every throughput mode.
  * VXB_MODEL_TB            the multi-genotype TB transmission model (tb_model.hpp),
  *   exact Gillespie; theta = (alpha, delta, tau) with the prior of
  *   tb::sample_prior, dim = 3, summaries (G, H), summary_dim = 2;

@@ -91,6 +91,130 @@ __device__ __forceinline__ int poisson_inv(double lam, double u, const double* _
     return k;
 }
 
+// ---- fp32 throughput instance (VXB_F32 + VXB_RNG_FAST): propensities, rates and the
+// CDF inversion in float, p0 = 2^(-lam log2 e) by ONE MUFU (ex2.approx), 23-bit uniforms
+// from mantissa bits.  Statistically validated against the fp64 instances
+// (tests/test_gpu_workloads.py); the state is integer in every instance, so the
+// conservation laws hold exactly here too.
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// (m + 1/2) 2^-23 for a 23-bit m: the MIDPOINT of the bucket, exact in float (no int->float
+// conversion).  With the bucket's lower edge P(u <= p0) would be too large by up to 2^-23
+// for every draw -- at event probabilities of 1e-3 per step a -6e-5 relative bias of the
+// firing rate, visible in E[P(T)] at 1e8 paths; midpoints make the error symmetric.
+__device__ __forceinline__ float unit_f32(uint32_t w) {
+    return __uint_as_float(0x3F800000u | (w >> 9)) - (1.0f - 0x1p-24f);
+}
+__device__ __forceinline__ int poisson_inv_f32(float lam, float u, const float* __restrict__ inv,
+                                               long long& iters) {
+    if (!(lam > 0.0f)) return 0;
+    // k = 0 iff u <= p0 = exp(-lam) >= 1 - lam; the computed p0 is within 4e-7 (relative)
+    if (u <= (1.0f - lam) - 1e-6f) return 0;
+    float p = ex2_approx(-1.4426950408889634f * lam);
+    float cdf = p;
+    int k = 0;
+    while (u > cdf && k < kMaxPoisson) {
+        ++k;
+        p = p * lam * inv[k];
+        cdf += p;
+        ++iters;
+    }
+    return k;
+}
+struct MMf {  // propensities in float from the integer state
+    __device__ __forceinline__ static void prop(const MM& x, const float* k, float* a) {
+        const float ds = static_cast<float>(x.s > 0 ? x.s : 0);
+        const float de = static_cast<float>(x.e > 0 ? x.e : 0);
+        const float dc = static_cast<float>(x.c > 0 ? x.c : 0);
+        a[0] = k[0] * ds * de;
+        a[1] = k[1] * dc;
+        a[2] = k[2] * dc;
+    }
+};
+
+__global__ void __launch_bounds__(kTlBlock, VXB_TL_MINB) tauleap_f32_kernel(const __grid_constant__ TauParams p) {
+    __shared__ float s_inv[kMaxPoisson + 1];
+    __shared__ long long s_sum[4];
+    for (int k = threadIdx.x; k <= kMaxPoisson; k += kTlBlock) s_inv[k] = k ? 1.0f / static_cast<float>(k) : 0.0f;
+    if (threadIdx.x < 4) s_sum[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kTlBlock + threadIdx.x;
+    long long sy = 0, sy2 = 0, sp = 0, it = 0;
+    if (r < p.count) {
+        const uint64_t path = p.first + r;
+        const uint32_t pl = static_cast<uint32_t>(path), ph = static_cast<uint32_t>(path >> 32);
+        const float tau = static_cast<float>(p.tau);
+        const float rate[3] = {static_cast<float>(p.rate[0]), static_cast<float>(p.rate[1]),
+                               static_cast<float>(p.rate[2])};
+        // the fp32 instance draws from its own domain (bit 7 of the domain word)
+        const uint32_t dom = kDomNoise | 0x80u | (p.level << 8);
+        MM f{p.init[0], p.init[1], p.init[2], p.init[3]};
+        MM c = f;
+        float af[3], ac[3];
+        if (p.level == 0) {
+            for (uint64_t st = 0; st < p.n_fine; ++st) {
+                MMf::prop(f, rate, af);
+                const Words32 w = philox4x32(p.fast, static_cast<uint32_t>(st),
+                                             dom | (static_cast<uint32_t>(st >> 32) << 16), pl, ph);
+                const int k0 = poisson_inv_f32(af[0] * tau, unit_f32(w.a), s_inv, it);
+                const int k1 = poisson_inv_f32(af[1] * tau, unit_f32(w.b), s_inv, it);
+                const int k2 = poisson_inv_f32(af[2] * tau, unit_f32(w.c), s_inv, it);
+                f.fire(k0, k1, k2);
+            }
+        } else {
+            uint32_t phase = 0;
+            for (uint64_t st = 0; st < p.n_fine; ++st) {
+                if (phase == 0) MMf::prop(c, rate, ac);
+                if (++phase == p.refine) phase = 0;
+                MMf::prop(f, rate, af);
+                // two Philox blocks per fine step: (a, b), (c, d) of the first and (a, b) of
+                // the second drive reactions 0, 1, 2 (common Poisson, residual Poisson)
+                const uint32_t hi = dom | (static_cast<uint32_t>((2 * st) >> 32) << 16);
+                const Words32 w0 = philox4x32(p.fast, static_cast<uint32_t>(2 * st), hi, pl, ph);
+                const Words32 w1 = philox4x32(p.fast, static_cast<uint32_t>(2 * st + 1), hi, pl, ph);
+                const uint32_t word[6] = {w0.a, w0.b, w0.c, w0.d, w1.a, w1.b};
+                int kf[3], kc[3];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const bool fine_larger = af[q] > ac[q];
+                    const float mn = af[q] < ac[q] ? af[q] : ac[q];
+                    const float mx = fine_larger ? af[q] : ac[q];
+                    const int p1 = poisson_inv_f32(mn * tau, unit_f32(word[2 * q]), s_inv, it);
+                    const int pr = poisson_inv_f32((mx - mn) * tau, unit_f32(word[2 * q + 1]), s_inv, it);
+                    kf[q] = p1 + (fine_larger ? pr : 0);
+                    kc[q] = p1 + (fine_larger ? 0 : pr);
+                }
+                f.fire(kf[0], kf[1], kf[2]);
+                c.fire(kc[0], kc[1], kc[2]);
+            }
+        }
+        const int32_t y = p.level == 0 ? f.p : f.p - c.p;
+        if (p.y_out) p.y_out[r] = y;
+        sy = y;
+        sy2 = static_cast<long long>(y) * y;
+        sp = f.p;
+    }
+    for (int o = 16; o; o >>= 1) {
+        sy += __shfl_down_sync(0xffffffffu, sy, o);
+        sy2 += __shfl_down_sync(0xffffffffu, sy2, o);
+        sp += __shfl_down_sync(0xffffffffu, sp, o);
+        it += __shfl_down_sync(0xffffffffu, it, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s_sum[0]), static_cast<unsigned long long>(sy));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s_sum[1]), static_cast<unsigned long long>(sy2));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s_sum[2]), static_cast<unsigned long long>(sp));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s_sum[3]), static_cast<unsigned long long>(it));
+    }
+    __syncthreads();
+    if (threadIdx.x < 4)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&p.sums[threadIdx.x]),
+                  static_cast<unsigned long long>(s_sum[threadIdx.x]));
+}
+
 // Two uniforms of random block `block` of this path: the reference stream's pair
 // block (positions 2*block, 2*block+1) or, for the throughput generator, the
 // Philox4x32 block (block, level domain, path).
@@ -208,6 +332,8 @@ void mlmc_level_device(vxb_ctx* ctx, const vxb_model& model, const vxb_mlmc_cfg&
     p.seed_hash = splitmix64(vxb_derive_seed(cfg.seed, &lv, 1));
     p.fast = make_fast_keys(splitmix64(cfg.seed));
     require(model.rng == VXB_RNG_REF || model.rng == VXB_RNG_FAST, "invalid-argument", "bad rng mode");
+    require(model.precision == VXB_F64 || (model.precision == VXB_F32 && model.rng == VXB_RNG_FAST),
+            "invalid-argument", "the fp32 tau-leap instance exists for the throughput generator only");
     p.n_fine = level_steps(cfg, level);
     p.level = level;
     p.refine = cfg.refine;
@@ -220,7 +346,9 @@ void mlmc_level_device(vxb_ctx* ctx, const vxb_model& model, const vxb_mlmc_cfg&
     p.y_out = y_dev;
     if (count) {
         LaunchScope scope(ctx, VXB_K_TAULEAP);
-        if (model.rng == VXB_RNG_FAST)
+        if (model.precision == VXB_F32)
+            tauleap_f32_kernel<<<grid_for(count, kTlBlock), kTlBlock, 0, ctx->stream>>>(p);
+        else if (model.rng == VXB_RNG_FAST)
             tauleap_kernel<VXB_RNG_FAST><<<grid_for(count, kTlBlock), kTlBlock, 0, ctx->stream>>>(p);
         else
             tauleap_kernel<VXB_RNG_REF><<<grid_for(count, kTlBlock), kTlBlock, 0, ctx->stream>>>(p);

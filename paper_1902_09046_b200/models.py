@@ -59,11 +59,13 @@ def normal_mean_model(n_data=100, rng=A.VXB_RNG_REF, arith=A.VXB_ARITH_EXACT):
     return m
 
 
-def mm_tauleap_model(x0=(100, 20, 0, 0), rates=(1e-3, 1e-4, 0.1), rng=A.VXB_RNG_REF):
-    """Michaelis-Menten network S+E->C, C->S+E, C->E+P (config 4)."""
+def mm_tauleap_model(x0=(100, 20, 0, 0), rates=(1e-3, 1e-4, 0.1), rng=A.VXB_RNG_REF,
+                     precision=A.VXB_F64):
+    """Michaelis-Menten network S+E->C, C->S+E, C->E+P (config 4).  precision VXB_F32:
+    rates and the Poisson inversion in float (throughput generator only)."""
     m = A.vxb_model()
     m.model = A.VXB_MODEL_MM_TAULEAP
-    m.precision, m.rng, m.arith = A.VXB_F64, rng, A.VXB_ARITH_EXACT
+    m.precision, m.rng, m.arith = precision, rng, A.VXB_ARITH_EXACT
     m.dim, m.summary_dim = 3, 1
     for k in range(4):
         m.consts[k] = float(x0[k])

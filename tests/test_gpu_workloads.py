@@ -339,6 +339,31 @@ def test_tauleap_fast_generator_statistics(ctx):
 
 
 # ------------------------------------------- toggle switch
+@pytest.mark.timeout(600)
+def test_tauleap_fp32_instance_statistics(ctx):
+    """The fp32 throughput instance of the tau-leap kernel (float propensities and CDF
+    inversion, exp by one MUFU, 23-bit midpoint uniforms): level means and variances
+    agree with the reference-exact fp64 instance within Monte-Carlo error (Bonferroni over
+    6 levels), the estimate too; counts are integers, so shard sums add exactly; the
+    REF + fp32 combination is refused."""
+    cfg = mm_cfg(levels=6, paths=400000, seed=77)
+    e = ctx.mlmc_tauleap(M.mm_tauleap_model(), cfg)
+    mf = M.mm_tauleap_model(rng=A.VXB_RNG_FAST, precision=A.VXB_F32)
+    f = ctx.mlmc_tauleap(mf, cfg)
+    for l in range(6):
+        z = (f["level_mean"][l] - e["level_mean"][l]) / math.sqrt((f["level_var"][l] + e["level_var"][l]) / cfg.paths)
+        assert abs(z) < 3.9, (l, z)
+        assert abs(math.log(f["level_var"][l] / e["level_var"][l])) < 0.1, l
+    assert abs(f["estimate"] - e["estimate"]) < 4.0 * math.hypot(f["std_error"], e["std_error"])
+    whole, _ = ctx.mlmc_level(mf, cfg, 3, 0, 20000)
+    a, _ = ctx.mlmc_level(mf, cfg, 3, 0, 7001)
+    b, ys = ctx.mlmc_level(mf, cfg, 3, 7001, 12999, want_y=True)
+    assert eq(whole[:3], (a + b)[:3]) and int(ys.sum()) == int(b[0])
+    with pytest.raises(lib.VxbError) as err:
+        ctx.mlmc_tauleap(M.mm_tauleap_model(rng=A.VXB_RNG_REF, precision=A.VXB_F32), cfg)
+    assert err.value.code == "invalid-argument"
+
+
 def test_toggle_switch_parity(ctx, oracle, golden):
     """The reference's own SDE, through the reference's own sampler keying:
     bit-identical summaries, distances and selection (KAT of SURVEY.md 8c)."""
