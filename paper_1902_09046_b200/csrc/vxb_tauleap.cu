@@ -119,8 +119,12 @@ __device__ __forceinline__ int poisson_inv_f32(float lam, float u, const float* 
     while (u > cdf && k < kMaxPoisson) {
         ++k;
         p = p * lam * inv[k];
-        cdf += p;
+        const float next = cdf + p;
         ++iters;
+        // a float CDF saturates a few ulp below 1: a uniform in the top buckets (2^-23 of
+        // the draws) would otherwise walk all the way to kMaxPoisson
+        if (next == cdf) break;
+        cdf = next;
     }
     return k;
 }
