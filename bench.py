@@ -664,7 +664,8 @@ def cpu_configs(configs, obs):
         fine = [30 * 4 ** l for l in range(6)]
         steps = mc.paths * sum(f if l == 0 else f + f // 4 for l, f in enumerate(fine))
         (_, dt) = clock(lambda: o.mlmc_tauleap(M.mm_tauleap_model(), mc))
-        attach(("config4_exact", "config4_fast"), "port", "6 levels x 2e3 of 1e6 paths", steps, dt, "path-steps")
+        attach(("config4_exact", "config4_fast", "config4_fast_f32"), "port", "6 levels x 2e3 of 1e6 paths", steps, dt,
+               "path-steps")
         if r is not None:
             # toggle ABC: 32 of the 8064 samples at the paper's C = 8000, T = 600
             n_t = 32

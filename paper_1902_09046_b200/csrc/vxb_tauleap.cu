@@ -118,6 +118,7 @@ __device__ __forceinline__ float unit_f32(uint32_t w) {
 __device__ __forceinline__ int poisson_inv_f32(float lam, float v, const float* __restrict__ inv,
                                                long long& iters) {
     if (!(lam > 0.0f)) return 0;
+    if (v >= lam) return 0;  // q0 = 1 - exp(-lam) <= lam (and so is the computed q0): k = 0, no series
     float q0, p;
     if (lam < 0.125f) {
         q0 = lam * (1.0f - 0.5f * lam * (1.0f - (1.0f / 3.0f) * lam * (1.0f - 0.25f * lam * (1.0f - 0.2f * lam))));
