@@ -308,12 +308,16 @@ typedef struct vxb_accept_layout {
 int vxb_accept_layout_of(int precision, uint32_t dim, uint64_t cap, vxb_accept_layout* out);
 
 /* ------------------------------------------- SMC building blocks (C3) */
-/* smc::ess (smc.cpp:208-219) and logsumexp (numeric.cpp:11-18). */
+/* smc::ess (smc.cpp:208-219) and logsumexp (numeric.cpp:11-18): bit-identical to the
+ * reference on this host -- every exp is the host libm's (vxb_host_exp_variant), the sums
+ * run left to right as the reference's loops do, the final log is the host's. */
 int vxb_ess(vxb_ctx* ctx, const double* log_w, uint64_t n, double* ess);
 int vxb_logsumexp(vxb_ctx* ctx, const double* x, uint64_t n, double* out);
 /* smc::resample_multinomial (smc.cpp:268-300): draw i uses position i of
  * RngStream(seed, stream_id); ancestors[i] = upper_bound(cum, u_i * cum[n-1]),
- * clamped; particles_out row i = particles_in row ancestors[i]. */
+ * clamped; particles_out row i = particles_in row ancestors[i].  The cumulative
+ * weights are the reference's (host-libm exp, sequential running sum), so the
+ * ancestors are identical to the reference's, index for index. */
 int vxb_resample_multinomial(vxb_ctx* ctx, uint64_t n, uint32_t dim, const double* log_w,
                              const double* particles_in, uint64_t seed, uint32_t stream_id,
                              double* particles_out, uint64_t* ancestors);
