@@ -55,7 +55,8 @@ def run_prior_predictive(ctx, model, n, workers, block_width, seed, observed):
     ``model`` is a ``vxb_model`` descriptor (models.logistic_model).  Results
     are bit-identical to the reference for the same (seed, workers,
     block_width): the device reproduces the reference's per-worker stream
-    consumption (VXB_KEY_WORKER)."""
+    consumption (VXB_KEY_WORKER).  ``ctx`` may be a ``lib.Context`` (one GPU) or a
+    ``lib.Multi`` (rows split over its devices by partition(n, G, 1); same rows)."""
     if n < 1:
         raise VxbError("invalid-shape: need at least one prior predictive sample")
     if workers < 1:
@@ -65,7 +66,10 @@ def run_prior_predictive(ctx, model, n, workers, block_width, seed, observed):
         raise VxbError("invalid-summary: observed summary length differs from the model "
                        "summary dimension")
     key = M.keying(seed, A.VXB_KEY_WORKER, workers, block_width)
-    p, s, rho, f = ctx.abc_prior_predictive_host(model, key, n, 0, n, observed)
+    if hasattr(ctx, "abc_prior_predictive_host"):
+        p, s, rho, f = ctx.abc_prior_predictive_host(model, key, n, 0, n, observed)
+    else:  # lib.Multi
+        p, s, rho, f = ctx.abc_prior_predictive(model, key, n, observed)
     return PriorPredictiveSet(n, model.dim, model.summary_dim, p, s, rho, f)
 
 

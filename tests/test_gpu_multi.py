@@ -31,6 +31,9 @@ def test_multi_drivers_equal_one_context_and_oracle(ctx, multi, oracle, golden):
     want = oracle.abc_prior_predictive(m, key, 2003, 0, 2003, obs)
     for g, w in zip(got, want):
         assert np.array_equal(g, w, equal_nan=True)
+    from paper_1902_09046_b200 import abc
+    pps = abc.run_prior_predictive(multi, m, 2003, 5, 4, 1337, obs)       # the Python mirror over Multi
+    assert np.array_equal(pps.discrepancies, want[2], equal_nan=True) and np.array_equal(pps.params, want[0])
     # fused rejection + gather of the accepted samples
     p, _, rho, f = oracle.abc_prior_predictive(m, M.keying(7), 40000, 0, 40000, obs, want_summaries=False)
     eps, idx_o = oracle.select_epsilon(rho, f, 0.02)
