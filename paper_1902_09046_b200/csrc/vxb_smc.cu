@@ -599,7 +599,8 @@ __global__ void whiten_kernel(int mode, uint64_t n, const double* __restrict__ t
         a = fma(y[k], y[k], a);
         out[i * (D + 1) + k] = mode == 0 ? 2.0 * y[k] : y[k];
     }
-    out[i * (D + 1) + D] = mode == 0 ? log2(w[i]) - a : -a;
+    // (a weight that underflowed to 0 would put -inf into every exponent it meets)
+    out[i * (D + 1) + D] = mode == 0 ? fmax(log2(w[i]), -1.0e4) - a : -a;
 }
 
 template <int D>
@@ -628,7 +629,7 @@ abcsmc_weights_fast_kernel(uint64_t count, const double* __restrict__ y_new, uin
             double z = fma(yi[0], lo.x, hi.y);
             z = fma(yi[1], lo.y, z);
             z = fma(yi[2], hi.x, z);
-            return fast_exp2_neg4(z + yi[D], s_tab);  // z <= 0 up to rounding
+            return fast_exp2_neg4_finite(z + yi[D], s_tab);  // z <= 0 up to rounding, finite
         };
         uint64_t j = 0;
         for (; j + 4 <= len; j += 4) {  // four independent terms side by side, added in index order
