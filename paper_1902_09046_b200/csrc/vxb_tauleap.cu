@@ -78,7 +78,23 @@ __device__ __forceinline__ int poisson_inv(double lam, double u, const double* _
     // (lam = rate * tau ~ 1e-3) that is the outcome of >99% of the draws, and a warp
     // whose 32 lanes all take it skips the polynomial altogether.  Same k, same
     // iteration count: results stay bit-identical to the oracle.
-    if (u <= __dsub_rn(__dsub_rn(1.0, lam), 0x1p-48)) return 0;
+    const double one_m = __dsub_rn(1.0, lam);
+    if (u <= __dsub_rn(one_m, 0x1p-48)) return 0;
+    // Second shortcut, same argument one term further: exp(-lam) <= 1 - lam + lam^2/2, so
+    // u above that (plus the margin) is beyond the computed p0: k >= 1; and the CDF after
+    // one term, exp(-lam)(1 + lam), is >= 1 - lam^2 (its computed value within 2^-48 of
+    // that), so u <= (1 - lam^2) - 2^-47 ends the oracle's loop at k = 1, after exactly one
+    // iteration.  The exponential is then needed only in two windows of width ~lam^2/2
+    // instead of for every draw above 1 - lam: on the fine levels once in ~1e6 draws
+    // instead of once in ~1e3, and a warp rarely has a lane on the slow path.
+    if (lam < 0.5) {
+        const double l2 = __dmul_rn(lam, lam);
+        if (u > __dadd_rn(__dadd_rn(one_m, __dmul_rn(0.5, l2)), 0x1p-48) &&
+            u <= __dsub_rn(__dsub_rn(1.0, l2), 0x1p-47)) {
+            ++iters;
+            return 1;
+        }
+    }
     double p = exp2_clamped<A>(A::mul(-lam, kInvLn2));
     double cdf = p;
     int k = 0;
