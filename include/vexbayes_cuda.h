@@ -598,6 +598,16 @@ int vxb_sharded_abc_reject(vxb_ctx* ctx, vxb_comm* comm, const vxb_model* model,
                            const vxb_keying* key, uint64_t n_total, const double* observed,
                            double epsilon, const vxb_accept_layout* layout, void* packed_local,
                            void* packed_all);
+/* SPMD forms of configs 2 and 4 (every rank calls them; comm == NULL: one rank): rank r
+ * works on partition(m_total or paths, n_ranks, 1)[r]; ONE ncclAllReduce(SUM) of the
+ * 64-bit integer counters (exact in any order); every rank receives the totals of the
+ * whole job -- counts / p-values, and the MLMC estimator formed from the exact sums. */
+int vxb_sharded_ppp_pvalues(vxb_ctx* ctx, vxb_comm* comm, const vxb_model* model,
+                            const double* lambda, const double* log_norm, uint32_t n_lambda,
+                            uint64_t m_total, uint64_t seed, double ybar_obs, uint64_t* counts,
+                            double* pvalues);
+int vxb_sharded_mlmc_tauleap(vxb_ctx* ctx, vxb_comm* comm, const vxb_model* model,
+                             const vxb_mlmc_cfg* cfg, vxb_mlmc_out* out);
 /* Host-side concatenation of gathered blocks (a HOST copy of packed_all) in rank
  * order: at most cap_out rows are written (*n_written of them); *n_accepted is the
  * full count (a rank whose count exceeded layout->cap contributes only its first cap
@@ -632,8 +642,9 @@ int vxb_multi_abc_prior_predictive(vxb_multi* multi, const vxb_model* model, con
 int vxb_multi_abc_reject(vxb_multi* multi, const vxb_model* model, const vxb_keying* key,
                          uint64_t n_total, const double* observed, double epsilon, uint64_t cap,
                          uint64_t* n_accepted, uint64_t* idx, void* params, void* rho);
-/* Configs 2 and 4 over all devices: disjoint dataset / path ranges, exact integer
- * counters added on the host (no collective). */
+/* Configs 2 and 4 over all devices: the SPMD forms (vxb_sharded_ppp_pvalues /
+ * vxb_sharded_mlmc_tauleap) on one host thread per device -- disjoint dataset / path
+ * ranges, one all-reduce of the exact integer counters. */
 int vxb_multi_ppp_pvalues(vxb_multi* multi, const vxb_model* model, const double* lambda,
                           const double* log_norm, uint32_t n_lambda, uint64_t m_total,
                           uint64_t seed, double ybar_obs, uint64_t* counts, double* pvalues);

@@ -142,12 +142,13 @@ struct vxb_multi {
 };
 
 namespace vxb {
-__global__ void loopback_sum_kernel(const double* __restrict__ all, int ranks, size_t count,
-                                    double* __restrict__ out) {
+template <class T>
+__global__ void loopback_sum_kernel(const T* __restrict__ all, int ranks, size_t count,
+                                    T* __restrict__ out) {
     const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= count) return;
-    double s = 0.0;
-    for (int r = 0; r < ranks; ++r) s = __dadd_rn(s, all[static_cast<size_t>(r) * count + i]);
+    T s = 0;
+    for (int r = 0; r < ranks; ++r) s = s + all[static_cast<size_t>(r) * count + i];  // rank order
     out[i] = s;
 }
 static void loopback_allgather(vxb_comm* c, const void* send, void* recv, size_t bytes) {
@@ -161,10 +162,11 @@ static void loopback_allgather(vxb_comm* c, const void* send, void* recv, size_t
     VXB_CUDA(cudaStreamSynchronize(c->ctx->stream));
     g->barrier();  // nobody reuses its send buffer before everyone has copied it
 }
-static void loopback_allreduce_sum_f64(vxb_comm* c, double* buf, size_t count) {
-    Scratch all(c->ctx, static_cast<size_t>(c->size) * count * sizeof(double));
-    loopback_allgather(c, buf, all.as<void>(), count * sizeof(double));
-    loopback_sum_kernel<<<grid_for(count, 256), 256, 0, c->ctx->stream>>>(all.as<double>(), c->size, count, buf);
+template <class T>
+static void loopback_allreduce_sum(vxb_comm* c, T* buf, size_t count) {
+    Scratch all(c->ctx, static_cast<size_t>(c->size) * count * sizeof(T));
+    loopback_allgather(c, buf, all.as<void>(), count * sizeof(T));
+    loopback_sum_kernel<T><<<grid_for(count, 256), 256, 0, c->ctx->stream>>>(all.as<T>(), c->size, count, buf);
     check_launch("loopback_sum_kernel");
     VXB_CUDA(cudaStreamSynchronize(c->ctx->stream));
 }
@@ -180,8 +182,13 @@ void comm_allgather(vxb_comm* comm, const void* send, void* recv, size_t bytes) 
 }
 void comm_allreduce_sum_f64(vxb_comm* comm, double* buf, size_t count) {
     require(comm != nullptr, "invalid-argument", "null communicator");
-    if (comm->loop) return loopback_allreduce_sum_f64(comm, buf, count);
+    if (comm->loop) return loopback_allreduce_sum<double>(comm, buf, count);
     VXB_NCCL(nccl().AllReduce(buf, buf, count, ncclFloat64, ncclSum, comm->comm, comm->ctx->stream));
+}
+void comm_allreduce_sum_i64(vxb_comm* comm, long long* buf, size_t count) {
+    require(comm != nullptr, "invalid-argument", "null communicator");
+    if (comm->loop) return loopback_allreduce_sum<long long>(comm, buf, count);
+    VXB_NCCL(nccl().AllReduce(buf, buf, count, ncclInt64, ncclSum, comm->comm, comm->ctx->stream));
 }
 }  // namespace vxb
 
@@ -301,9 +308,10 @@ extern "C" int vxb_comm_allreduce(vxb_comm* comm, void* buf, size_t count, int d
         require(comm && buf, "invalid-argument", "null argument");
         use(comm->ctx);
         if (comm->loop) {
-            require(dtype == VXB_DT_F64 && op == VXB_OP_SUM, "invalid-argument",
-                    "the loopback group reduces doubles by SUM only");
-            return comm_allreduce_sum_f64(comm, static_cast<double*>(buf), count);
+            require(op == VXB_OP_SUM && (dtype == VXB_DT_F64 || dtype == VXB_DT_I64 || dtype == VXB_DT_U64),
+                    "invalid-argument", "the loopback group reduces 64-bit elements by SUM only");
+            if (dtype == VXB_DT_F64) return comm_allreduce_sum_f64(comm, static_cast<double*>(buf), count);
+            return comm_allreduce_sum_i64(comm, static_cast<long long*>(buf), count);
         }
         ncclDataType_t dt;
         switch (dtype) {
@@ -557,21 +565,13 @@ extern "C" int vxb_multi_ppp_pvalues(vxb_multi* m, const vxb_model* model, const
                                      double* pvalues) {
     return guarded([&] {
         require(m && model && lambda && log_norm && counts, "invalid-argument", "null argument");
-        const uint64_t g = m->ctx.size();
-        std::vector<uint64_t> part(g * n_lambda, 0);
-        fork_join(m, [&](int r) {
-            uint64_t b, e;
-            shard_of(m_total, g, r, &b, &e);
-            if (e == b) return;
-            abi(vxb_ppp_pvalues(m->ctx[r], model, lambda, log_norm, n_lambda, m_total, b, e - b, seed,
-                                ybar_obs, part.data() + r * n_lambda, nullptr, nullptr));
+        const int g = static_cast<int>(m->ctx.size());
+        fork_join(m, [&](int r) {  // SPMD on one host thread per device; rank 0 reports
+            std::vector<uint64_t> c(n_lambda);
+            abi(vxb_sharded_ppp_pvalues(m->ctx[r], g > 1 ? m->comm[r] : nullptr, model, lambda, log_norm,
+                                        n_lambda, m_total, seed, ybar_obs, r == 0 ? counts : c.data(),
+                                        r == 0 ? pvalues : nullptr));
         });
-        for (uint32_t k = 0; k < n_lambda; ++k) {
-            uint64_t c = 0;
-            for (uint64_t r = 0; r < g; ++r) c += part[r * n_lambda + k];
-            counts[k] = c;
-            if (pvalues) pvalues[k] = static_cast<double>(c) / static_cast<double>(m_total);
-        }
     });
 }
 
@@ -579,40 +579,12 @@ extern "C" int vxb_multi_mlmc_tauleap(vxb_multi* m, const vxb_model* model, cons
                                       vxb_mlmc_out* out) {
     return guarded([&] {
         require(m && model && cfg && out, "invalid-argument", "null argument");
-        require(cfg->paths >= 2, "insufficient-data", "variance needs at least two values");
-        require(cfg->tau0 > 0.0 && cfg->t_end > 0.0, "invalid-horizon", "need a positive horizon");
-        const uint64_t g = m->ctx.size();
-        std::vector<int64_t> part(g * cfg->levels * 4, 0);
+        const int g = static_cast<int>(m->ctx.size());
         fork_join(m, [&](int r) {
-            uint64_t b, e;
-            shard_of(cfg->paths, g, r, &b, &e);
-            if (e == b) return;
-            for (uint32_t l = 0; l < cfg->levels; ++l)
-                abi(vxb_mlmc_level(m->ctx[r], model, cfg, l, b, e - b,
-                                   part.data() + (r * cfg->levels + l) * 4, nullptr));
+            vxb_mlmc_out none{};
+            abi(vxb_sharded_mlmc_tauleap(m->ctx[r], g > 1 ? m->comm[r] : nullptr, model, cfg,
+                                         r == 0 ? out : &none));
         });
-        // estimator of vxb_mlmc_tauleap from the exact integer sums
-        double est = 0.0, var = 0.0;
-        uint64_t steps = static_cast<uint64_t>(std::llround(cfg->t_end / cfg->tau0));
-        const double n = static_cast<double>(cfg->paths);
-        for (uint32_t l = 0; l < cfg->levels; ++l) {
-            int64_t s0 = 0, s1 = 0;
-            for (uint64_t r = 0; r < g; ++r) {
-                s0 += part[(r * cfg->levels + l) * 4 + 0];
-                s1 += part[(r * cfg->levels + l) * 4 + 1];
-            }
-            const double mean = static_cast<double>(s0) / n;
-            const double v = (static_cast<double>(s1) - static_cast<double>(s0) * mean) / (n - 1.0);
-            if (out->level_mean) out->level_mean[l] = mean;
-            if (out->level_var) out->level_var[l] = v;
-            if (out->level_cost)
-                out->level_cost[l] = static_cast<double>(l == 0 ? steps : steps + steps / cfg->refine);
-            est += mean;
-            var += v / n;
-            steps *= cfg->refine;
-        }
-        out->estimate = est;
-        out->std_error = std::sqrt(var);
     });
 }
 
@@ -657,5 +629,80 @@ extern "C" int vxb_multi_weak_info_test(vxb_multi* m, const vxb_weakinfo_cfg* cf
             abi(vxb_weak_info_evidence(m->ctx[r], cfg, lambda, b, e - b, evidence + b * cfg->datasets * 2));
         });
         abi(vxb_weak_info_cutoffs(cfg, evidence, gamma, weakly, completed));
+    });
+}
+
+// ---- SPMD forms of configs 2 and 4 (every rank calls them; comm == NULL: one rank):
+// disjoint dataset / path ranges per rank, ONE all-reduce(SUM) of the 64-bit integer
+// counters (exact in any order), every rank receives the job's totals.
+extern "C" int vxb_sharded_ppp_pvalues(vxb_ctx* ctx, vxb_comm* comm, const vxb_model* model,
+                                       const double* lambda, const double* log_norm,
+                                       uint32_t n_lambda, uint64_t m_total, uint64_t seed,
+                                       double ybar_obs, uint64_t* counts, double* pvalues) {
+    return guarded([&] {
+        use(ctx);
+        require(model && lambda && log_norm && counts && n_lambda >= 1, "invalid-argument", "null argument");
+        require(!comm || comm->ctx == ctx, "invalid-argument", "communicator of another context");
+        const uint64_t world = comm_size(comm), rank = comm_rank(comm);
+        uint64_t b, e;
+        shard_of(m_total, world, rank, &b, &e);
+        std::vector<uint64_t> local(n_lambda, 0);
+        if (e > b)
+            abi(vxb_ppp_pvalues(ctx, model, lambda, log_norm, n_lambda, m_total, b, e - b, seed, ybar_obs,
+                                local.data(), nullptr, nullptr));
+        if (world > 1) {
+            Scratch d(ctx, n_lambda * 8);
+            VXB_CUDA(cudaMemcpyAsync(d.as<void>(), local.data(), n_lambda * 8, cudaMemcpyHostToDevice, ctx->stream));
+            comm_allreduce_sum_i64(comm, d.as<long long>(), n_lambda);
+            VXB_CUDA(cudaMemcpyAsync(local.data(), d.as<void>(), n_lambda * 8, cudaMemcpyDeviceToHost, ctx->stream));
+            VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+        }
+        for (uint32_t k = 0; k < n_lambda; ++k) {
+            counts[k] = local[k];
+            if (pvalues) pvalues[k] = static_cast<double>(local[k]) / static_cast<double>(m_total);
+        }
+    });
+}
+
+extern "C" int vxb_sharded_mlmc_tauleap(vxb_ctx* ctx, vxb_comm* comm, const vxb_model* model,
+                                        const vxb_mlmc_cfg* cfg, vxb_mlmc_out* out) {
+    return guarded([&] {
+        use(ctx);
+        require(model && cfg && out, "invalid-argument", "null argument");
+        require(cfg->paths >= 2, "insufficient-data", "variance needs at least two values");
+        require(cfg->tau0 > 0.0 && cfg->t_end > 0.0, "invalid-horizon", "need a positive horizon");
+        require(!comm || comm->ctx == ctx, "invalid-argument", "communicator of another context");
+        const uint64_t world = comm_size(comm), rank = comm_rank(comm);
+        uint64_t b, e;
+        shard_of(cfg->paths, world, rank, &b, &e);
+        std::vector<long long> sums(cfg->levels * 4, 0);
+        if (e > b)
+            for (uint32_t l = 0; l < cfg->levels; ++l)
+                abi(vxb_mlmc_level(ctx, model, cfg, l, b, e - b, reinterpret_cast<int64_t*>(sums.data() + 4 * l),
+                                   nullptr));
+        if (world > 1) {
+            Scratch d(ctx, sums.size() * 8);
+            VXB_CUDA(cudaMemcpyAsync(d.as<void>(), sums.data(), sums.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+            comm_allreduce_sum_i64(comm, d.as<long long>(), sums.size());
+            VXB_CUDA(cudaMemcpyAsync(sums.data(), d.as<void>(), sums.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+            VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+        }
+        double est = 0.0, var = 0.0;
+        uint64_t steps = static_cast<uint64_t>(std::llround(cfg->t_end / cfg->tau0));
+        const double n = static_cast<double>(cfg->paths);
+        for (uint32_t l = 0; l < cfg->levels; ++l) {
+            const double s0 = static_cast<double>(sums[4 * l]), s1 = static_cast<double>(sums[4 * l + 1]);
+            const double mean = s0 / n;
+            const double v = (s1 - s0 * mean) / (n - 1.0);
+            if (out->level_mean) out->level_mean[l] = mean;
+            if (out->level_var) out->level_var[l] = v;
+            if (out->level_cost)
+                out->level_cost[l] = static_cast<double>(l == 0 ? steps : steps + steps / cfg->refine);
+            est += mean;
+            var += v / n;
+            steps *= cfg->refine;
+        }
+        out->estimate = est;
+        out->std_error = std::sqrt(var);
     });
 }

@@ -43,6 +43,7 @@ int comm_rank(const vxb_comm* comm);
 int comm_size(const vxb_comm* comm);
 void comm_allgather(vxb_comm* comm, const void* send, void* recv, size_t bytes);
 void comm_allreduce_sum_f64(vxb_comm* comm, double* buf, size_t count);
+void comm_allreduce_sum_i64(vxb_comm* comm, long long* buf, size_t count);
 // partition(total, world, 1) (blocked.cpp:34-63): range of worker `rank`
 void shard_of(uint64_t total, uint64_t world, uint64_t rank, uint64_t* begin, uint64_t* end);
 

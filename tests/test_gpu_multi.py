@@ -202,6 +202,13 @@ def test_multi_rank_drivers_on_one_gpu_through_the_loopback_group(ctx, oracle, g
     c1, p1, _ = ctx.ppp_pvalues(M.normal_mean_model(100), lam, ln, 30001, 0, 30001, 1337, 2.9)
     c2, p2 = multi.ppp_pvalues(M.normal_mean_model(100), lam, ln, 30001, 1337, 2.9)
     assert np.array_equal(c1, c2) and np.array_equal(p1, p2)
+    mc = A.vxb_mlmc_cfg()
+    mc.levels, mc.refine, mc.tau0, mc.t_end, mc.paths, mc.seed = 3, 4, 1.0, 30.0, 10001, 1337
+    for mm in (M.mm_tauleap_model(), M.mm_tauleap_model(rng=A.VXB_RNG_FAST, precision=A.VXB_F32)):
+        r1, r2 = ctx.mlmc_tauleap(mm, mc), multi.mlmc_tauleap(mm, mc)   # all-reduce of int64 sums
+        for k in ("level_mean", "level_var", "level_cost"):
+            assert np.array_equal(r1[k], r2[k]), k
+        assert r1["estimate"] == r2["estimate"] and r1["std_error"] == r2["std_error"]
     # the weak-informativity test: hyperparameter rows over the ranks
     wcfg = M.weakinfo_config(hyper_count=6, datasets=9, particles=100, seed=1337)
     w1, w2 = ctx.weak_info_test(wcfg, want_evidence=True), multi.weak_info_test(wcfg, want_evidence=True)
