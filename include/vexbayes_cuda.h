@@ -598,6 +598,25 @@ int vxb_sharded_abc_reject(vxb_ctx* ctx, vxb_comm* comm, const vxb_model* model,
                            const vxb_keying* key, uint64_t n_total, const double* observed,
                            double epsilon, const vxb_accept_layout* layout, void* packed_local,
                            void* packed_all);
+/* SPMD form of config 0's selection (select_epsilon, abc.cpp:74-106) over a distance
+ * vector that stays sharded: rank r holds rows [first_row, first_row + n_local) (device or
+ * host buffers; n_local may be 0).  The valid counts and, in each of the 6 (fp64) / 3
+ * (fp32) digit passes of the radix select, the n_ranks x 2048 integer histograms are
+ * all-reduced (ncclAllReduce SUM on uint32 -- exact), so every rank walks to the order
+ * statistics of the WHOLE vector and returns the same *epsilon, bit-identical to
+ * vxb_select_epsilon on the concatenated rows; no distance leaves its device.  Each rank
+ * then compacts its accepted rows (global indices, ascending) into `block_local`
+ * (device, VXB_INDEX_BLOCK_BYTES(cap): uint64 count at byte 0 -- it may exceed cap --,
+ * indices from byte 16) and ONE all-gather places the blocks in `blocks_all` (device,
+ * n_ranks blocks, rank order = ascending row order).  *n_accepted: accepted rows of the
+ * whole vector.  cap == 0: epsilon and count only (block pointers may be NULL).  The whole
+ * vector holds fewer than 2^32 valid rows.  comm == NULL: one rank. */
+#define VXB_INDEX_BLOCK_BYTES(cap) (16ull + ((((uint64_t)(cap)) * 8ull + 15ull) & ~15ull))
+int vxb_sharded_select_epsilon(vxb_ctx* ctx, vxb_comm* comm, int precision,
+                               const void* rho_local, const uint8_t* failed_local,
+                               uint64_t n_local, uint64_t first_row, double accept_fraction,
+                               double* epsilon, uint64_t* n_accepted, uint64_t cap,
+                               void* block_local, void* blocks_all);
 /* SPMD forms of configs 2 and 4 (every rank calls them; comm == NULL: one rank): rank r
  * works on partition(m_total or paths, n_ranks, 1)[r]; ONE ncclAllReduce(SUM) of the
  * 64-bit integer counters (exact in any order); every rank receives the totals of the
@@ -642,6 +661,12 @@ int vxb_multi_abc_prior_predictive(vxb_multi* multi, const vxb_model* model, con
 int vxb_multi_abc_reject(vxb_multi* multi, const vxb_model* model, const vxb_keying* key,
                          uint64_t n_total, const double* observed, double epsilon, uint64_t cap,
                          uint64_t* n_accepted, uint64_t* idx, void* params, void* rho);
+/* select_epsilon over HOST arrays with every device taking the rows of its partition
+ * range (vxb_sharded_select_epsilon on one host thread per device); arguments and
+ * results as vxb_select_epsilon. */
+int vxb_multi_select_epsilon(vxb_multi* multi, int precision, const void* rho,
+                             const uint8_t* failed, uint64_t n, double accept_fraction,
+                             double* epsilon, uint64_t cap, uint64_t* n_accepted, uint64_t* idx);
 /* Configs 2 and 4 over all devices: the SPMD forms (vxb_sharded_ppp_pvalues /
  * vxb_sharded_mlmc_tauleap) on one host thread per device -- disjoint dataset / path
  * ranges, one all-reduce of the exact integer counters. */

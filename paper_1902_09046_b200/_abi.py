@@ -108,5 +108,5 @@ EXPORTED_SYMBOLS = (
     "vxb_multi_mlmc_tauleap", "vxb_abcsmc_pack_round", "vxb_abcsmc_append_round",
     "vxb_normalise_by_chunk_totals", "vxb_guard_report", "vxb_rng_fast_stats",
     "vxb_sharded_abcsmc_run", "vxb_multi_abcsmc_run", "vxb_fast_generator_rounds", "vxb_multi_init_loopback", "vxb_multi_weak_info_test", "vxb_host_exp_variant",
-    "vxb_sharded_ppp_pvalues", "vxb_sharded_mlmc_tauleap",
+    "vxb_sharded_ppp_pvalues", "vxb_sharded_mlmc_tauleap", "vxb_sharded_select_epsilon", "vxb_multi_select_epsilon",
 )

@@ -9,7 +9,9 @@
 //       themselves are split over the GPUs in use (cuda::set_devices, default:
 //       every visible device) by partition(n, G, 1) -- a device where the
 //       reference has a worker thread (abc.cpp:43-71);
-//   select_epsilon         -> vxb_select_epsilon           (abc.cpp:75-97);
+//   select_epsilon         -> vxb_multi_select_epsilon     (abc.cpp:75-97): the rows are
+//       split over the GPUs in use, the digit histograms of the radix select are
+//       all-reduced -- same epsilon and indices for any device count;
 //   discrepancy            -> host arithmetic, left-to-right (abc.cpp:16-24);
 //   write_csv              -> same column layout, %.17g      (abc.cpp:99-124).
 // Extension for jobs that do not fit the fixed-N container (config 1):
@@ -114,9 +116,9 @@ inline EpsilonSelection select_epsilon(const PriorPredictiveSet& set, double acc
     std::vector<std::uint64_t> idx(set.rows);
     std::uint64_t n_acc = 0;
     EpsilonSelection sel;
-    cuda::check(vxb_select_epsilon(cuda::context(), VXB_F64, set.discrepancies.data(),
-                                   set.failed.data(), set.rows, accept_fraction, &sel.epsilon,
-                                   idx.size(), &n_acc, idx.data()));
+    cuda::check(vxb_multi_select_epsilon(cuda::multi(), VXB_F64, set.discrepancies.data(),
+                                         set.failed.data(), set.rows, accept_fraction, &sel.epsilon,
+                                         idx.size(), &n_acc, idx.data()));
     sel.accepted.assign(idx.begin(), idx.begin() + static_cast<std::ptrdiff_t>(n_acc));
     return sel;
 }

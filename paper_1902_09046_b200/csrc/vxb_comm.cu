@@ -190,6 +190,11 @@ void comm_allreduce_sum_i64(vxb_comm* comm, long long* buf, size_t count) {
     if (comm->loop) return loopback_allreduce_sum<long long>(comm, buf, count);
     VXB_NCCL(nccl().AllReduce(buf, buf, count, ncclInt64, ncclSum, comm->comm, comm->ctx->stream));
 }
+void comm_allreduce_sum_u32(vxb_comm* comm, unsigned int* buf, size_t count) {
+    require(comm != nullptr, "invalid-argument", "null communicator");
+    if (comm->loop) return loopback_allreduce_sum<unsigned int>(comm, buf, count);
+    VXB_NCCL(nccl().AllReduce(buf, buf, count, ncclUint32, ncclSum, comm->comm, comm->ctx->stream));
+}
 }  // namespace vxb
 
 using namespace vxb;
@@ -556,6 +561,53 @@ extern "C" int vxb_multi_abc_reject(vxb_multi* m, const vxb_model* model, const 
         int over = 0;
         abi(vxb_accept_unpack(&lay, model->precision, model->dim, g, host.data(), cap, n_accepted, idx,
                               params, rho, &over, nullptr));
+    });
+}
+
+// select_epsilon (abc.cpp:74-106) over a prior predictive set held in host arrays: every
+// device takes the rows of its partition range, the digit histograms are all-reduced and
+// the accepted indices come back in ascending order (rank order = row order).
+extern "C" int vxb_multi_select_epsilon(vxb_multi* m, int precision, const void* rho,
+                                        const uint8_t* failed, uint64_t n, double accept_fraction,
+                                        double* epsilon, uint64_t cap, uint64_t* n_accepted,
+                                        uint64_t* idx) {
+    return guarded([&] {
+        require(m && rho && epsilon && n_accepted, "invalid-argument", "null argument");
+        require(n >= 1, "empty-set", "every prior predictive row failed");
+        require(!is_device_pointer(rho), "invalid-argument", "vxb_multi_select_epsilon takes host arrays");
+        const int g = static_cast<int>(m->ctx.size());
+        const uint64_t real = precision == VXB_F32 ? 4 : 8;
+        const size_t block = VXB_INDEX_BLOCK_BYTES(cap);
+        std::vector<char> host(cap ? static_cast<size_t>(g) * block : 0);
+        fork_join(m, [&](int r) {
+            vxb_ctx* ctx = m->ctx[r];
+            VXB_CUDA(cudaSetDevice(ctx->device));
+            uint64_t b, e;
+            shard_of(n, g, r, &b, &e);
+            Scratch local(ctx, cap ? block : 0), all(ctx, cap && g > 1 ? g * block : 0);
+            double eps = 0.0;
+            uint64_t total = 0;
+            abi(vxb_sharded_select_epsilon(ctx, g > 1 ? m->comm[r] : nullptr, precision,
+                                           static_cast<const char*>(rho) + b * real,
+                                           failed ? failed + b : nullptr, e - b, b, accept_fraction, &eps,
+                                           &total, cap, local.as<void>(), all.as<void>()));
+            if (r == 0) {
+                *epsilon = eps;
+                *n_accepted = total;
+                if (cap)
+                    VXB_CUDA(cudaMemcpyAsync(host.data(), g > 1 ? all.as<void>() : local.as<void>(),
+                                             host.size(), cudaMemcpyDeviceToHost, ctx->stream));
+            }
+            VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+        });
+        uint64_t kept = 0;
+        for (int r = 0; r < g && idx && cap; ++r) {
+            uint64_t c;
+            std::memcpy(&c, host.data() + r * block, 8);
+            const uint64_t take = std::min(std::min(c, cap), cap - kept);
+            std::memcpy(idx + kept, host.data() + r * block + 16, take * 8);
+            kept += take;
+        }
     });
 }
 

@@ -30,9 +30,10 @@ void compact_accepted_device(vxb_ctx* ctx, int precision, const void* rho_dev,
                              uint64_t* idx_dev);
 void order_statistics_any(vxb_ctx* ctx, int precision, const void* rho_dev,
                           const uint8_t* failed_dev, uint64_t n, const uint64_t* ranks,
-                          int n_ranks, double* values);
+                          int n_ranks, double* values, vxb_comm* comm = nullptr);
 uint64_t count_valid_any(vxb_ctx* ctx, int precision, const void* rho_dev,
-                         const uint8_t* failed_dev, uint64_t n, uint64_t* only_flag = nullptr);
+                         const uint8_t* failed_dev, uint64_t n, uint64_t* only_flag = nullptr,
+                         vxb_comm* comm = nullptr);
 // type-7 quantile (numeric.cpp:20-36) of n device-resident values (all valid)
 double quantile_device(vxb_ctx* ctx, const double* values_dev, uint64_t n, double level);
 
@@ -44,6 +45,7 @@ int comm_size(const vxb_comm* comm);
 void comm_allgather(vxb_comm* comm, const void* send, void* recv, size_t bytes);
 void comm_allreduce_sum_f64(vxb_comm* comm, double* buf, size_t count);
 void comm_allreduce_sum_i64(vxb_comm* comm, long long* buf, size_t count);
+void comm_allreduce_sum_u32(vxb_comm* comm, unsigned int* buf, size_t count);
 // partition(total, world, 1) (blocked.cpp:34-63): range of worker `rank`
 void shard_of(uint64_t total, uint64_t world, uint64_t rank, uint64_t* begin, uint64_t* end);
 

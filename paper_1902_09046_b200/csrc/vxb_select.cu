@@ -16,7 +16,7 @@
 #include <cmath>
 #include <limits>
 
-#include "vxb_common.cuh"
+#include "vxb_internal.cuh"
 
 namespace vxb {
 
@@ -474,7 +474,13 @@ accept_write_kernel(const unsigned short* __restrict__ thread_flags,
 
 template <class Real>
 void order_statistics_device(vxb_ctx* ctx, const Real* rho, const uint8_t* failed, uint64_t n,
-                             const uint64_t* ranks, int n_ranks, double* values) {
+                             const uint64_t* ranks, int n_ranks, double* values, vxb_comm* comm) {
+    // comm (several ranks, each holding n rows of one long vector): the per-digit
+    // histograms are integer counts, so their all-reduce between the counting and the
+    // picking kernel makes every rank walk the digits of the WHOLE vector's order
+    // statistics -- 6 (fp64) or 3 (fp32) all-reduces of n_ranks x 2048 counters, and no
+    // distance ever leaves its device.  n may be zero on a rank.
+    const bool shared = comm_size(comm) > 1;
     require(n_ranks >= 1 && n_ranks <= kMaxRanks, "invalid-argument", "too many ranks");
     Scratch d_state(ctx, sizeof(SelectState));
     Scratch d_hist(ctx, sizeof(unsigned int) * kMaxRanks * kBins);
@@ -501,13 +507,15 @@ void order_statistics_device(vxb_ctx* ctx, const Real* rho, const uint8_t* faile
     while (top > low) {
         const int bits = std::min(kDigitBits, top - low);
         const int shift = top - bits;
-        {
+        if (grid) {
             LaunchScope scope(ctx, VXB_K_SELECT);
             kernel<<<grid, kSelBlock, hist_smem, ctx->stream>>>(
                 rho, failed, n, shift, bits, n_ranks, d_state.as<SelectState>(),
                 d_hist.as<unsigned int>());
             check_launch("radix_hist_kernel");
         }
+        if (shared)
+            comm_allreduce_sum_u32(comm, d_hist.as<unsigned int>(), static_cast<size_t>(n_ranks) * kBins);
         {
             LaunchScope scope(ctx, VXB_K_SELECT);
             radix_pick_kernel<<<n_ranks, 256, 0, ctx->stream>>>(shift, bits, n_ranks,
@@ -528,17 +536,20 @@ void order_statistics_device(vxb_ctx* ctx, const Real* rho, const uint8_t* faile
 
 template <class Real>
 uint64_t count_valid_device(vxb_ctx* ctx, const Real* rho, const uint8_t* failed, uint64_t n,
-                            uint64_t* only_flag) {
+                            uint64_t* only_flag, vxb_comm* comm) {
     Scratch d_cnt(ctx, 2 * sizeof(unsigned long long));
     VXB_CUDA(cudaMemsetAsync(d_cnt.as<void>(), 0, 2 * sizeof(unsigned long long), ctx->stream));
     const unsigned grid = static_cast<unsigned>(
         std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(ctx->prop.multiProcessorCount) * 8));
-    {
+    if (grid) {
         LaunchScope scope(ctx, VXB_K_SELECT);
         count_valid_kernel<Real><<<grid, 256, 0, ctx->stream>>>(rho, failed, n,
                                                                d_cnt.as<unsigned long long>());
         check_launch("count_valid_kernel");
     }
+    // several ranks: both counts are those of the whole vector (every rank must take the
+    // same with / without flags decision, and the same ranks)
+    if (comm_size(comm) > 1) comm_allreduce_sum_i64(comm, d_cnt.as<long long>(), 2);
     unsigned long long c[2] = {0, 0};
     VXB_CUDA(cudaMemcpyAsync(c, d_cnt.as<void>(), sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
     VXB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -611,32 +622,35 @@ void compact_accepted_device(vxb_ctx* ctx, int precision, const void* rho_dev,
 
 void order_statistics_any(vxb_ctx* ctx, int precision, const void* rho_dev,
                           const uint8_t* failed_dev, uint64_t n, const uint64_t* ranks,
-                          int n_ranks, double* values) {
+                          int n_ranks, double* values, vxb_comm* comm) {
     if (precision == VXB_F32)
         order_statistics_device<float>(ctx, static_cast<const float*>(rho_dev), failed_dev, n,
-                                       ranks, n_ranks, values);
+                                       ranks, n_ranks, values, comm);
     else
         order_statistics_device<double>(ctx, static_cast<const double*>(rho_dev), failed_dev, n,
-                                        ranks, n_ranks, values);
+                                        ranks, n_ranks, values, comm);
 }
 
 // only_flag (optional): rows that their flag alone excludes; zero means the digit
 // passes may be run without the flags
 uint64_t count_valid_any(vxb_ctx* ctx, int precision, const void* rho_dev,
-                         const uint8_t* failed_dev, uint64_t n, uint64_t* only_flag) {
+                         const uint8_t* failed_dev, uint64_t n, uint64_t* only_flag, vxb_comm* comm) {
     return precision == VXB_F32
-               ? count_valid_device<float>(ctx, static_cast<const float*>(rho_dev), failed_dev, n, only_flag)
-               : count_valid_device<double>(ctx, static_cast<const double*>(rho_dev), failed_dev, n, only_flag);
+               ? count_valid_device<float>(ctx, static_cast<const float*>(rho_dev), failed_dev, n, only_flag, comm)
+               : count_valid_device<double>(ctx, static_cast<const double*>(rho_dev), failed_dev, n, only_flag, comm);
 }
 
 // The quantile rule of select_epsilon (abc.cpp:85-89 with numeric.cpp:20-30)
 // evaluated on exact order statistics: same operations in the same order as
 // the reference performs on its sorted array.
 double epsilon_from_order_statistics(vxb_ctx* ctx, int precision, const void* rho_dev,
-                                     const uint8_t* failed_dev, uint64_t n, double q) {
+                                     const uint8_t* failed_dev, uint64_t n, double q,
+                                     vxb_comm* comm = nullptr) {
     require(q > 0.0 && q <= 1.0, "invalid-argument", "accept fraction must lie in (0, 1]");
     uint64_t only_flag = 0;
-    const uint64_t nv = count_valid_any(ctx, precision, rho_dev, failed_dev, n, &only_flag);
+    const uint64_t nv = count_valid_any(ctx, precision, rho_dev, failed_dev, n, &only_flag, comm);
+    // the digit counters are 32 bits wide: one device cannot hold that many rows, several can
+    require(nv < (1ull << 32), "invalid-shape", "the radix select counts at most 2^32 - 1 valid rows");
     require(nv >= 1, "empty-set", "every prior predictive row failed");
     if (only_flag == 0) failed_dev = nullptr;  // every failed row is a NaN: the digit passes skip the flags
     uint64_t ranks[3];
@@ -666,7 +680,7 @@ double epsilon_from_order_statistics(vxb_ctx* ctx, int precision, const void* rh
     const int guard_slot = nr;
     if (min_accept >= 1) ranks[nr++] = min_accept - 1;
     double v[3];
-    order_statistics_any(ctx, precision, rho_dev, failed_dev, n, ranks, nr, v);
+    order_statistics_any(ctx, precision, rho_dev, failed_dev, n, ranks, nr, v, comm);
     if (mode == 2)
         eps = v[0] + frac * (v[1] - v[0]);
     else
@@ -769,5 +783,52 @@ extern "C" int vxb_select_epsilon(vxb_ctx* ctx, int precision, const void* rho,
         *n_accepted = total;
         d_idx.finish(std::min(total, cap) * sizeof(uint64_t));
         VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+// Distributed form of vxb_select_epsilon: see the header.  Every rank returns the same
+// epsilon (same integer histograms, same host arithmetic) and compacts its own rows
+// under global indices; the index blocks travel in one all-gather.
+extern "C" int vxb_sharded_select_epsilon(vxb_ctx* ctx, vxb_comm* comm, int precision,
+                                          const void* rho_local, const uint8_t* failed_local,
+                                          uint64_t n_local, uint64_t first_row,
+                                          double accept_fraction, double* epsilon,
+                                          uint64_t* n_accepted, uint64_t cap, void* block_local,
+                                          void* blocks_all) {
+    return guarded([&] {
+        use(ctx);
+        require(epsilon && n_accepted, "invalid-argument", "null argument");
+        require(n_local == 0 || rho_local, "invalid-argument", "null distances");
+        require(accept_fraction > 0.0 && accept_fraction <= 1.0, "invalid-argument",
+                "accept fraction must lie in (0, 1]");
+        const int world = comm_size(comm);
+        require(cap == 0 || (block_local && is_device_pointer(block_local)), "invalid-argument",
+                "block_local is a device buffer of VXB_INDEX_BLOCK_BYTES(cap)");
+        require(cap == 0 || world == 1 || (blocks_all && is_device_pointer(blocks_all)), "invalid-argument",
+                "blocks_all is a device buffer of n_ranks blocks");
+        const size_t real = precision == VXB_F32 ? 4 : 8;
+        Staged d_rho(ctx, rho_local, n_local * real, true, false);
+        Staged d_failed(ctx, failed_local, n_local, true, false);
+        const double eps = epsilon_from_order_statistics(ctx, precision, d_rho.ptr(), d_failed.as<uint8_t>(),
+                                                         n_local, accept_fraction, comm);
+        *epsilon = eps;
+        const size_t block = VXB_INDEX_BLOCK_BYTES(cap);
+        Scratch d_count(ctx, 2 * sizeof(uint64_t));
+        uint64_t* count_dev = cap ? static_cast<uint64_t*>(block_local) : d_count.as<uint64_t>();
+        if (cap) VXB_CUDA(cudaMemsetAsync(block_local, 0, 16, ctx->stream));
+        compact_accepted_device(ctx, precision, d_rho.ptr(), d_failed.as<uint8_t>(), n_local, eps, first_row,
+                                cap, count_dev, cap ? reinterpret_cast<uint64_t*>(static_cast<char*>(block_local) + 16)
+                                                    : nullptr);
+        if (cap && world > 1)
+            comm_allgather(comm, block_local, blocks_all, block);
+        else if (cap && blocks_all && blocks_all != block_local)
+            VXB_CUDA(cudaMemcpyAsync(blocks_all, block_local, block, cudaMemcpyDeviceToDevice, ctx->stream));
+        uint64_t* total_dev = d_count.as<uint64_t>() + 1;
+        VXB_CUDA(cudaMemcpyAsync(total_dev, count_dev, sizeof(uint64_t), cudaMemcpyDeviceToDevice, ctx->stream));
+        if (world > 1) comm_allreduce_sum_i64(comm, reinterpret_cast<long long*>(total_dev), 1);
+        uint64_t total = 0;
+        VXB_CUDA(cudaMemcpyAsync(&total, total_dev, sizeof(total), cudaMemcpyDeviceToHost, ctx->stream));
+        VXB_CUDA(cudaStreamSynchronize(ctx->stream));
+        *n_accepted = total;
     });
 }

@@ -267,6 +267,19 @@ class Multi:
         k = min(nacc.value, cap)
         return nacc.value, idx[:k], params[:k], rho[:k]
 
+    def select_epsilon(self, rho, failed, q, cap=None):
+        """select_epsilon (abc.cpp:74-106) over host arrays, the rows split over the devices."""
+        rho = np.ascontiguousarray(rho)
+        failed = None if failed is None else np.ascontiguousarray(failed, dtype=np.uint8)
+        precision = A.VXB_F32 if rho.dtype == np.float32 else A.VXB_F64
+        cap = rho.size if cap is None else cap
+        idx = np.zeros(cap, dtype=np.uint64)
+        eps, nacc = f64(), u64()
+        self._check(self.lib.vxb_multi_select_epsilon(self.handle, i32(precision), _ptr(rho), _ptr(failed),
+                                                      u64(rho.size), f64(q), C.byref(eps), u64(cap),
+                                                      C.byref(nacc), _ptr(idx)))
+        return eps.value, idx[:min(nacc.value, cap)], nacc.value
+
     def ppp_pvalues(self, model, lam, log_norm, m_total, seed, ybar_obs):
         lam = np.ascontiguousarray(lam, dtype=np.float64)
         ln = np.ascontiguousarray(log_norm, dtype=np.float64)
@@ -547,6 +560,20 @@ class Context:
         self._check(self.lib.vxb_sharded_abc_reject(
             self.handle, comm.handle if comm is not None else None, C.byref(model), C.byref(key),
             u64(n_total), _ptr(obs), f64(eps), C.byref(layout), _ptr(packed_local), _ptr(packed_all)))
+
+    def sharded_select_epsilon(self, comm, rho_local, failed_local, first_row, q, cap=0,
+                               block_local=None, blocks_all=None, precision=None, n_local=None):
+        """SPMD config 0 selection over a sharded distance vector (histogram all-reduce):
+        (epsilon, accepted rows of the whole vector).  Buffers: numpy or device tensors."""
+        if isinstance(rho_local, np.ndarray):
+            n_local = rho_local.size
+            precision = A.VXB_F32 if rho_local.dtype == np.float32 else A.VXB_F64
+        eps, nacc = f64(), u64()
+        self._check(self.lib.vxb_sharded_select_epsilon(
+            self.handle, comm.handle if comm is not None else None, i32(precision), _ptr(rho_local),
+            _ptr(failed_local), u64(n_local), u64(first_row), f64(q), C.byref(eps), C.byref(nacc), u64(cap),
+            _ptr(block_local), _ptr(blocks_all)))
+        return eps.value, nacc.value
 
     # ---- p-values
     def ppp_pvalues(self, model, lam, log_norm, m_total, first, count, seed, ybar_obs,

@@ -34,6 +34,9 @@ for prec, rng in ((A.VXB_F64, A.VXB_RNG_FAST), (A.VXB_F32, A.VXB_RNG_FAST), (A.V
 idx, params, r, n_dev = D.sharded_reject(ctx, m, M.keying(3), n, obs, 30.0, cap_fraction=0.5)
 ctx.synchronize()
 print("sharded_reject", int(n_dev.item()))
+lb = lib.Multi(loopback_ranks=3)   # all-reduced digit histograms (vxb_sharded_select_epsilon)
+print("multi select", lb.select_epsilon(rho, f, 0.01)[0])
+lb.close()
 # config 2
 lam = np.array(M.lambda_grid(4))
 ln = np.array([-0.5 * math.log(2.0 * math.pi * (l * l + 0.01)) for l in lam])

@@ -188,6 +188,32 @@ def test_multi_rank_drivers_on_one_gpu_through_the_loopback_group(ctx, oracle, g
     nacc, idx, params, rho_acc = multi.abc_reject(m, M.keying(7), 40001, obs, eps, cap=40001)
     assert nacc == len(idx_o) and np.array_equal(idx, idx_o)
     assert np.array_equal(params, p[idx_o]) and np.array_equal(rho_acc, rho[idx_o])
+    # config 0's selection over a sharded distance vector: all-reduced digit histograms.
+    # Same epsilon bits and the same indices as the oracle / one context, with failed rows
+    # (flag-only, NaN-only, both), ties, fp32 keys, a capacity below the accepted count,
+    # and fewer rows than ranks
+    rs = np.random.RandomState(ranks)
+    for q in (0.02, 0.5, 1.0, 1e-6):
+        e, idx_s, n_s = multi.select_epsilon(rho, f, q)
+        e_o, i_o = oracle.select_epsilon(rho, f, q)
+        assert e == e_o and n_s == len(i_o) and np.array_equal(idx_s, i_o), q
+    r2, f2 = np.round(rs.gamma(2.0, 3.0, 30011), 1), (rs.uniform(size=30011) < 0.05).astype(np.uint8)
+    r2[rs.uniform(size=30011) < 0.03] = np.nan          # NaN rows, some of them unflagged
+    for arr in (r2, r2.astype(np.float32)):
+        e, idx_s, n_s = multi.select_epsilon(arr, f2, 0.1)
+        e_1, idx_1, n_1 = ctx.select_epsilon(arr, f2, 0.1)
+        e_o, i_o = oracle.select_epsilon(arr.astype(np.float64), f2 | np.isnan(arr).astype(np.uint8), 0.1)
+        assert e == e_1 == e_o and n_s == n_1 == len(i_o)
+        assert np.array_equal(idx_s, idx_1) and np.array_equal(idx_s, i_o)
+        e, idx_s, n_s = multi.select_epsilon(arr, None, 0.1, cap=100)     # NaN-only failures, small cap
+        e_1, idx_1, n_1 = ctx.select_epsilon(arr, None, 0.1)
+        assert e == e_1 and n_s == n_1 > 100 and np.array_equal(idx_s, idx_1[:100])
+    small = np.array([3.0, 1.0][:max(1, ranks - 2)])
+    e, idx_s, n_s = multi.select_epsilon(small, None, 0.5)
+    assert (e, idx_s.tolist(), n_s) == ((2.0, [1], 1) if small.size == 2 else (3.0, [0], 1))
+    with pytest.raises(lib.VxbError) as err:
+        multi.select_epsilon(np.full(5, np.nan), None, 0.5)
+    assert err.value.code == "empty-set"
     for rng, n, gens, round_size, seed in ((A.VXB_RNG_REF, 600, 3, 250, 9), (A.VXB_RNG_FAST, 1500, 4, 0, 21),
                                            (A.VXB_RNG_REF, 2000, 3, 0, 1337)):
         mm = M.logistic_model(rng=rng)
