@@ -643,7 +643,12 @@ int vxb_multi_init(vxb_multi** multi, const int* device_ids, int n_dev);
  * joined by a LOOPBACK group instead of NCCL -- a collective is a host rendezvous of the
  * ranks' threads (stream drained, barrier, device-to-device copies, barrier); no kernel
  * ever waits for another rank.  Every vxb_multi_* driver then runs its multi-rank logic
- * (sharding, packed gathers, chunk-total reduction, append order) for real. */
+ * (sharding, packed gathers, chunk-total reduction, append order) for real.  A rank that
+ * fails releases the ranks waiting for it at the next collective (the call returns the
+ * root cause, the group is reset and stays usable); VXB_LOOPBACK_FAIL_RANK=r injects one
+ * such failure for the tests.  With NCCL, as in any NCCL program, a rank-local failure in
+ * the middle of a call leaves its peers waiting: argument and shape errors are raised
+ * identically on every rank before the first collective. */
 int vxb_multi_init_loopback(vxb_multi** multi, int device, int n_ranks);
 void vxb_multi_shutdown(vxb_multi* multi);
 int vxb_multi_size(const vxb_multi* multi);

@@ -11,6 +11,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <condition_variable>
@@ -108,6 +109,7 @@ void shard_of(uint64_t total, uint64_t world, uint64_t rank, uint64_t* begin, ui
 // order) run for real on a one-GPU box.  Same results as NCCL by construction: an
 // all-gather is a copy, and the only all-reduce of the path adds vectors with one
 // non-zero contributor per entry (added here in rank order).
+static const char* const kPeerFailed = "another rank of the group failed before the collective";
 struct vxb_loopback {
     int size = 0;
     std::mutex m;
@@ -115,16 +117,29 @@ struct vxb_loopback {
     int arrived = 0;
     unsigned long long generation = 0;
     std::vector<const void*> slot;
+    bool aborted = false;  // a rank failed: nobody may wait for it (fork_join)
+    std::atomic<int> fail_rank{-1};  // one-shot fault injection for the tests (VXB_LOOPBACK_FAIL_RANK)
     void barrier() {
         std::unique_lock<std::mutex> lock(m);
         const unsigned long long gen = generation;
-        if (++arrived == size) {
+        if (!aborted && ++arrived == size) {
             arrived = 0;
             ++generation;
             cv.notify_all();
-        } else {
-            cv.wait(lock, [&] { return generation != gen; });
+            return;
         }
+        cv.wait(lock, [&] { return generation != gen || aborted; });
+        if (generation == gen) vxb::raise("device-error", kPeerFailed);
+    }
+    void abort() {
+        std::lock_guard<std::mutex> lock(m);
+        aborted = true;
+        cv.notify_all();
+    }
+    void reset() {  // every rank's thread has been joined
+        std::lock_guard<std::mutex> lock(m);
+        aborted = false;
+        arrived = 0;
     }
 };
 
@@ -207,12 +222,21 @@ static void fork_join(vxb_multi* m, F&& body) {
     std::vector<std::string> err(g);
     auto run = [&](int r) {
         try {
+            int expect = r;
+            if (m->loop && m->loop->fail_rank.compare_exchange_strong(expect, -1))
+                raise("internal", "injected failure (VXB_LOOPBACK_FAIL_RANK)");
             body(r);
         } catch (const Error& e) {
             err[r] = e.code + ": " + e.message;
         } catch (const std::exception& e) {
             err[r] = std::string("internal: ") + e.what();
         }
+        // a rank that failed will not arrive at the next collective: the loopback group
+        // releases the ranks waiting for it (they fail with kPeerFailed) instead of
+        // hanging.  With NCCL a rank-local failure in the middle of a call leaves the
+        // peers waiting, as in any NCCL program; argument and shape errors are raised
+        // identically on every rank before the first collective.
+        if (!err[r].empty() && m->loop) m->loop->abort();
     };
     if (g == 1) {
         run(0);
@@ -221,8 +245,10 @@ static void fork_join(vxb_multi* m, F&& body) {
         for (int r = 0; r < g; ++r) pool.emplace_back(run, r);
         for (auto& t : pool) t.join();
     }
+    if (m->loop) m->loop->reset();
+    for (int pass = 0; pass < 2; ++pass)  // the root cause before the ranks it released
     for (int r = 0; r < g; ++r)
-        if (!err[r].empty()) {
+        if (!err[r].empty() && (pass == 1 || err[r].find(kPeerFailed) == std::string::npos)) {
             const size_t c = err[r].find(": ");
             raise(err[r].substr(0, c).c_str(), err[r].substr(c == std::string::npos ? 0 : c + 2) +
                                                    " (device rank " + std::to_string(r) + ")");
@@ -474,6 +500,7 @@ extern "C" int vxb_multi_init_loopback(vxb_multi** multi, int device, int n_rank
             m->loop = new vxb_loopback();
             m->loop->size = n_ranks;
             m->loop->slot.assign(n_ranks, nullptr);
+            if (const char* f = getenv("VXB_LOOPBACK_FAIL_RANK")) m->loop->fail_rank = atoi(f);
             for (int r = 0; r < n_ranks; ++r) {
                 vxb_ctx* c = nullptr;
                 abi(vxb_init(&c, device));

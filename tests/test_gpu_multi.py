@@ -249,3 +249,35 @@ def test_multi_rank_drivers_on_one_gpu_through_the_loopback_group(ctx, oracle, g
     c3, _ = multi.ppp_pvalues(M.normal_mean_model(100), lam, ln, ranks - 1, 1337, 2.9)
     assert np.array_equal(c3, ctx.ppp_pvalues(M.normal_mean_model(100), lam, ln, ranks - 1, 0, ranks - 1, 1337, 2.9)[0])
     multi.close()
+
+
+@pytest.mark.timeout(600)
+def test_loopback_group_releases_its_ranks_when_one_fails():
+    """A rank that fails never arrives at the next collective.  The loopback group must
+    release the ranks waiting for it -- the call returns the root cause instead of hanging
+    -- and stay usable (the group is reset after the join).  The failure is injected once,
+    on rank 1 of 3, by VXB_LOOPBACK_FAIL_RANK (read by vxb_multi_init_loopback)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = f"""
+import sys; sys.path.insert(0, {root!r})
+import numpy as np
+from paper_1902_09046_b200 import lib, models as M
+obs = np.load({os.path.join(root, 'tests', 'golden', 'golden.npz')!r})["logistic_observed"]
+multi = lib.Multi(loopback_ranks=3)
+for attempt in range(2):                      # the second call finds a clean group
+    try:
+        n = multi.abc_reject(M.logistic_model(), M.keying(7), 5000, obs, 30.0, cap=5000)[0]
+        print("no error", n)
+    except lib.VxbError as e:
+        print("error", e.code, "|", e)
+multi.close()
+"""
+    run = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                         env=dict(os.environ, VXB_LOOPBACK_FAIL_RANK="1"))
+    assert run.returncode == 0, run.stdout[-800:] + run.stderr[-800:]
+    lines = run.stdout.splitlines()
+    assert len(lines) == 2 and lines[0].startswith("error internal") and "injected failure" in lines[0], run.stdout
+    assert "device rank 1" in lines[0] and lines[1].startswith("no error") and int(lines[1].split()[-1]) > 0
