@@ -18,6 +18,15 @@
 //    (position 6s+2r drives P1, position 6s+2r+1 the residual -- at most one of
 //    P2, P3 has a positive rate, so they share it); fine fires P1+P2, coarse P1+P3;
 //  * path i of level l owns RngStream(derive_seed(seed,{l}), i).
+// Quiet steps: on the fine levels rate * tau ~ 1e-3, so in most steps nothing fires and
+// neither the state nor the propensities change.  The coupled loop keeps the six
+// thresholds "uniform <= thr => k = 0" in registers, refreshes them only after an event
+// (or when a new coarse step finds a changed coarse state), and decides a quiet step
+// with six compares and one branch; the three (throughput generator: two) Philox
+// blocks of the step are drawn before that branch so that their round chains
+// interleave.  The decisions are those of the plain loop, so the exact instance stays
+// bit-identical to the oracle.  The throughput instances draw the six uniforms of a
+// fine step from TWO Philox4x32 blocks (42 bits each in fp64, 23-bit midpoints in fp32).
 // One path per thread, integer state in registers; only four 64-bit sums (and
 // optionally Y per path) leave the device, so the level sums are exact integers
 // and identical for any sharding.
@@ -67,6 +76,12 @@ struct MM {
         a[2] = __dmul_rn(k[2], dc);
     }
 };
+
+// u <= zero_threshold(lam) decides k = 0 without the exponential (first shortcut of
+// poisson_inv, same arithmetic); a rate that is not positive never fires.
+__device__ __forceinline__ double zero_threshold(double lam) {
+    return lam > 0.0 ? __dsub_rn(__dsub_rn(1.0, lam), 0x1p-48) : __longlong_as_double(0x7FF0000000000000ll);
+}
 
 template <class A>
 __device__ __forceinline__ int poisson_inv(double lam, double u, const double* __restrict__ inv,
@@ -197,17 +212,43 @@ __global__ void __launch_bounds__(kTlBlock, VXB_TL_MINB) tauleap_f32_kernel(cons
                 f.fire(k0, k1, k2);
             }
         } else {
+            // as in tauleap_kernel: the rates below which a uniform decides k = 0 stay in
+            // registers and are refreshed only after an event; a quiet step is two Philox
+            // blocks, six compares and one branch
             uint32_t phase = 0;
+            bool stale = true, coarse_moved = true;
+            float lam_c[3], lam_r[3];  // v >= lam: the common / residual Poisson is 0
             for (uint64_t st = 0; st < p.n_fine; ++st) {
-                if (phase == 0) MMf::prop(c, rate, ac);
+                if (phase == 0 && coarse_moved) {
+                    MMf::prop(c, rate, ac);
+                    coarse_moved = false;
+                    stale = true;
+                }
                 if (++phase == p.refine) phase = 0;
-                MMf::prop(f, rate, af);
+                if (stale) {
+                    MMf::prop(f, rate, af);
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {
+                        const float mn = af[q] < ac[q] ? af[q] : ac[q];
+                        const float mx = af[q] > ac[q] ? af[q] : ac[q];
+                        lam_c[q] = mn * tau;
+                        lam_r[q] = (mx - mn) * tau;
+                    }
+                    stale = false;
+                }
                 // two Philox blocks per fine step: (a, b), (c, d) of the first and (a, b) of
                 // the second drive reactions 0, 1, 2 (common Poisson, residual Poisson)
                 const uint32_t hi = dom | (static_cast<uint32_t>((2 * st) >> 32) << 16);
                 const Words32 w0 = philox4x32(p.fast, static_cast<uint32_t>(2 * st), hi, pl, ph);
                 const Words32 w1 = philox4x32(p.fast, static_cast<uint32_t>(2 * st + 1), hi, pl, ph);
                 const uint32_t word[6] = {w0.a, w0.b, w0.c, w0.d, w1.a, w1.b};
+                bool quiet = true;
+#pragma unroll
+                for (int q = 0; q < 3; ++q)
+                    quiet = quiet & (unit_f32(word[2 * q]) >= lam_c[q]) & (unit_f32(word[2 * q + 1]) >= lam_r[q]);
+                if (quiet) continue;
+                stale = true;
+                coarse_moved = true;
                 int kf[3], kc[3];
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
@@ -266,6 +307,27 @@ __device__ __forceinline__ void draw_pair(const TauParams& p, uint64_t key, uint
     }
 }
 
+// Throughput generator, coupled levels: the SIX uniforms of a fine step from TWO Philox4x32
+// blocks (2 st, 2 st + 1) -- 42 bits each (one word + 10 bits of the second block's last
+// two words: 2^-42 against event probabilities of ~1e-3 per step), a third less
+// generator work than a block per reaction.
+__device__ __forceinline__ double unit42(uint32_t w, uint32_t x10) {
+    return __dsub_rn(__hiloint2double(0x3FF00000u | (w >> 12), (w << 20) | (x10 << 10)), 1.0);
+}
+__device__ __forceinline__ void draw_six_fast(const TauParams& p, uint64_t path, uint64_t st,
+                                              double* u0, double* u1) {
+    const uint32_t hi = kDomNoise | (p.level << 8) | (static_cast<uint32_t>((2 * st) >> 32) << 16);
+    const uint32_t pl = static_cast<uint32_t>(path), ph = static_cast<uint32_t>(path >> 32);
+    const Words32 a = philox4x32(p.fast, static_cast<uint32_t>(2 * st), hi, pl, ph);
+    const Words32 b = philox4x32(p.fast, static_cast<uint32_t>(2 * st + 1), hi, pl, ph);
+    u0[0] = unit42(a.a, b.c & 1023u);
+    u1[0] = unit42(a.b, (b.c >> 10) & 1023u);
+    u0[1] = unit42(a.c, (b.c >> 20) & 1023u);
+    u1[1] = unit42(a.d, b.d & 1023u);
+    u0[2] = unit42(b.a, (b.d >> 10) & 1023u);
+    u1[2] = unit42(b.b, (b.d >> 20) & 1023u);
+}
+
 template <int kRng>
 __global__ void __launch_bounds__(kTlBlock, VXB_TL_MINB) tauleap_kernel(const __grid_constant__ TauParams p) {
     using PA = typename std::conditional<kRng == VXB_RNG_REF, Exact, Fused>::type;
@@ -295,24 +357,60 @@ __global__ void __launch_bounds__(kTlBlock, VXB_TL_MINB) tauleap_kernel(const __
                 f.fire(k0, k1, k2);
             }
         } else {
+            // On the fine levels (rate * tau ~ 1e-3) a step in which NOTHING fires is the
+            // rule, and then neither state nor propensities change.  The thresholds
+            // below which a uniform decides k = 0 (first shortcut of poisson_inv) are
+            // therefore kept in registers and refreshed only after an event or a new
+            // coarse step with a changed coarse state; a quiet step is three Philox blocks,
+            // six compares and ONE branch.  Same decisions as the oracle's loop, bit for bit.
             uint32_t phase = 0;
+            bool stale = true, coarse_moved = true;
+            double thr_c[3], thr_r[3];  // u <= thr: the common / residual Poisson is 0
             for (uint64_t st = 0; st < p.n_fine; ++st) {
-                if (phase == 0) c.prop(p.rate, ac);
+                if (phase == 0 && coarse_moved) {
+                    c.prop(p.rate, ac);
+                    coarse_moved = false;
+                    stale = true;
+                }
                 if (++phase == p.refine) phase = 0;
-                f.prop(p.rate, af);
+                if (stale) {
+                    f.prop(p.rate, af);
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {
+                        const double mn = af[q] < ac[q] ? af[q] : ac[q];
+                        const double mx = af[q] > ac[q] ? af[q] : ac[q];
+                        thr_c[q] = zero_threshold(__dmul_rn(mn, p.tau));
+                        thr_r[q] = zero_threshold(__dmul_rn(__dsub_rn(mx, mn), p.tau));
+                    }
+                    stale = false;
+                }
                 int kf[3], kc[3];
+                // reaction q of fine step st owns Philox block 3 st + q: word 0 drives the
+                // common Poisson, word 1 the residual one.  The three blocks are drawn
+                // BEFORE the inversions: their round chains are independent and interleave
+                // in one basic block, whereas the branches of an inversion fence off a
+                // block drawn after it
+                double u0[3], u1[3];
+                if (kRng == VXB_RNG_REF) {
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) draw_pair<kRng>(p, key, path, 3 * st + q, u0[q], u1[q]);
+                } else {
+                    draw_six_fast(p, path, st, u0, u1);
+                }
+                bool quiet = true;
+#pragma unroll
+                for (int q = 0; q < 3; ++q) quiet = quiet & (u0[q] <= thr_c[q]) & (u1[q] <= thr_r[q]);
+                if (quiet) continue;
+                stale = true;
+                coarse_moved = true;
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
-                    // reaction q of fine step st owns Philox block 3 st + q: word 0 drives
-                    // the common Poisson, word 1 the residual one
-                    double u0, u1;
-                    draw_pair<kRng>(p, key, path, 3 * st + q, u0, u1);
                     const bool fine_larger = af[q] > ac[q];
                     const double mn = af[q] < ac[q] ? af[q] : ac[q];
                     const double mx = fine_larger ? af[q] : ac[q];
-                    const int p1 = poisson_inv<PA>(__dmul_rn(mn, p.tau), u0, s_inv, it);
+                    const int p1 = poisson_inv<PA>(__dmul_rn(mn, p.tau), u0[q], s_inv, it);
                     // at most one of (af - m), (ac - m) is positive: one inversion serves both
-                    const int pr = poisson_inv<PA>(__dmul_rn(__dsub_rn(mx, mn), p.tau), u1, s_inv, it);
+                    const int pr = poisson_inv<PA>(__dmul_rn(__dsub_rn(mx, mn), p.tau), u1[q], s_inv, it);
                     kf[q] = p1 + (fine_larger ? pr : 0);
                     kc[q] = p1 + (fine_larger ? 0 : pr);
                 }

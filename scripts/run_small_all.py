@@ -28,6 +28,7 @@ print("config3", ctx.abcsmc_run(m, cfg, obs)["epsilon"])
 mc = A.vxb_mlmc_cfg(); mc.levels, mc.refine, mc.tau0, mc.t_end, mc.paths, mc.seed = 4, 4, 1.0, 30.0, 100000, 1337
 for rng in (A.VXB_RNG_REF, A.VXB_RNG_FAST):
     print("config4", ctx.mlmc_tauleap(M.mm_tauleap_model(rng=rng), mc)["estimate"])
+print("config4 f32", ctx.mlmc_tauleap(M.mm_tauleap_model(rng=A.VXB_RNG_FAST, precision=A.VXB_F32), mc)["estimate"])
 # toggle: 296 samples x 8000 cells x 600 steps (two CTAs per SM)
 tm = M.toggle_model(600, 8000)
 tobs = ctx.simulate_at(tm, M.TOGGLE_MIDPOINT, lib.derive_seed(1337, [90]), 0, 0)

@@ -156,6 +156,14 @@ int main() {
                          mean.data(), cov.data()};
         cuda::check(vxb_multi_abcsmc_run(loop, model.device.get(), &c, observed.data(), &o));
         CHECK(th == pop.particles && w == pop.weights && eps == pop.epsilon && props == pop.proposals);
+        // select_epsilon over the sharded distances (all-reduced digit histograms)
+        double eps3 = 0.0;
+        std::vector<std::uint64_t> idx3(set.rows);
+        cuda::check(vxb_multi_select_epsilon(loop, VXB_F64, set.discrepancies.data(), set.failed.data(), set.rows,
+                                             0.05, &eps3, idx3.size(), &n_acc, idx3.data()));
+        idx3.resize(n_acc);
+        CHECK(eps3 == sel.epsilon && idx3.size() == sel.accepted.size());
+        for (std::size_t i = 0; i < idx3.size(); ++i) CHECK(idx3[i] == sel.accepted[i]);
         vxb_multi_shutdown(loop);
         std::printf("loopback_three_ranks ok\n");
     }
