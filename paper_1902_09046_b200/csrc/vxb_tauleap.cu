@@ -77,12 +77,6 @@ struct MM {
     }
 };
 
-// u <= zero_threshold(lam) decides k = 0 without the exponential (first shortcut of
-// poisson_inv, same arithmetic); a rate that is not positive never fires.
-__device__ __forceinline__ double zero_threshold(double lam) {
-    return lam > 0.0 ? __dsub_rn(__dsub_rn(1.0, lam), 0x1p-48) : __longlong_as_double(0x7FF0000000000000ll);
-}
-
 template <class A>
 __device__ __forceinline__ int poisson_inv(double lam, double u, const double* __restrict__ inv,
                                            long long& iters) {
@@ -171,6 +165,14 @@ __device__ __forceinline__ int poisson_inv_f32(float lam, float v, const float* 
     }
     return k;
 }
+// Smallest word whose uniform decides k = 0 for rate lam (a multiple of 512), or the odd
+// value 1 when lam is too large for any uniform to do so.
+__device__ __forceinline__ uint32_t quiet_bound_f32(float lam) {
+    const float t = ceilf(lam * 8388608.0f - 0.5f);
+    if (!(t > 0.0f)) return 0u;         // lam <= 2^-24 (or not positive): every uniform
+    if (!(t < 8388608.0f)) return 1u;   // lam > 1 - 2^-24: none
+    return static_cast<uint32_t>(t) << 9;
+}
 struct MMf {  // propensities in float from the integer state
     __device__ __forceinline__ static void prop(const MM& x, const float* k, float* a) {
         const float ds = static_cast<float>(x.s > 0 ? x.s : 0);
@@ -217,7 +219,11 @@ __global__ void __launch_bounds__(kTlBlock, VXB_TL_MINB) tauleap_f32_kernel(cons
             // blocks, six compares and one branch
             uint32_t phase = 0;
             bool stale = true, coarse_moved = true;
-            float lam_c[3], lam_r[3];  // v >= lam: the common / residual Poisson is 0
+            // word >= bound  <=>  unit_f32(word) >= lam (exactly: the midpoint (m + 1/2) 2^-23
+            // of m = word >> 9 reaches lam iff m >= ceil(lam 2^23 - 1/2), all exact in float)
+            // <=>  the common / residual Poisson is 0 by the pre-test of poisson_inv_f32
+            uint32_t bound_c[3], bound_r[3];
+            bool loud = false;  // a rate >= 1: no uniform decides k = 0 up front
             for (uint64_t st = 0; st < p.n_fine; ++st) {
                 if (phase == 0 && coarse_moved) {
                     MMf::prop(c, rate, ac);
@@ -231,9 +237,10 @@ __global__ void __launch_bounds__(kTlBlock, VXB_TL_MINB) tauleap_f32_kernel(cons
                     for (int q = 0; q < 3; ++q) {
                         const float mn = af[q] < ac[q] ? af[q] : ac[q];
                         const float mx = af[q] > ac[q] ? af[q] : ac[q];
-                        lam_c[q] = mn * tau;
-                        lam_r[q] = (mx - mn) * tau;
+                        bound_c[q] = quiet_bound_f32(mn * tau);
+                        bound_r[q] = quiet_bound_f32((mx - mn) * tau);
                     }
+                    loud = (bound_c[0] | bound_c[1] | bound_c[2] | bound_r[0] | bound_r[1] | bound_r[2]) & 1u;
                     stale = false;
                 }
                 // two Philox blocks per fine step: (a, b), (c, d) of the first and (a, b) of
@@ -242,10 +249,9 @@ __global__ void __launch_bounds__(kTlBlock, VXB_TL_MINB) tauleap_f32_kernel(cons
                 const Words32 w0 = philox4x32(p.fast, static_cast<uint32_t>(2 * st), hi, pl, ph);
                 const Words32 w1 = philox4x32(p.fast, static_cast<uint32_t>(2 * st + 1), hi, pl, ph);
                 const uint32_t word[6] = {w0.a, w0.b, w0.c, w0.d, w1.a, w1.b};
-                bool quiet = true;
+                bool quiet = !loud;
 #pragma unroll
-                for (int q = 0; q < 3; ++q)
-                    quiet = quiet & (unit_f32(word[2 * q]) >= lam_c[q]) & (unit_f32(word[2 * q + 1]) >= lam_r[q]);
+                for (int q = 0; q < 3; ++q) quiet = quiet & (word[2 * q] >= bound_c[q]) & (word[2 * q + 1] >= bound_r[q]);
                 if (quiet) continue;
                 stale = true;
                 coarse_moved = true;
@@ -314,19 +320,59 @@ __device__ __forceinline__ void draw_pair(const TauParams& p, uint64_t key, uint
 __device__ __forceinline__ double unit42(uint32_t w, uint32_t x10) {
     return __dsub_rn(__hiloint2double(0x3FF00000u | (w >> 12), (w << 20) | (x10 << 10)), 1.0);
 }
-__device__ __forceinline__ void draw_six_fast(const TauParams& p, uint64_t path, uint64_t st,
-                                              double* u0, double* u1) {
-    const uint32_t hi = kDomNoise | (p.level << 8) | (static_cast<uint32_t>((2 * st) >> 32) << 16);
-    const uint32_t pl = static_cast<uint32_t>(path), ph = static_cast<uint32_t>(path >> 32);
-    const Words32 a = philox4x32(p.fast, static_cast<uint32_t>(2 * st), hi, pl, ph);
-    const Words32 b = philox4x32(p.fast, static_cast<uint32_t>(2 * st + 1), hi, pl, ph);
-    u0[0] = unit42(a.a, b.c & 1023u);
-    u1[0] = unit42(a.b, (b.c >> 10) & 1023u);
-    u0[1] = unit42(a.c, (b.c >> 20) & 1023u);
-    u1[1] = unit42(a.d, b.d & 1023u);
-    u0[2] = unit42(b.a, (b.d >> 10) & 1023u);
-    u1[2] = unit42(b.b, (b.d >> 20) & 1023u);
-}
+
+// The random bits of one coupled fine step, and the quiet test on them.  A uniform is
+// only ever COMPARED on the common path, so the test is done on the leading 32 bits of
+// the raw word against an integer bound (quiet_bound): `top < bound` implies
+// u <= (1 - lam) - 2^-48, i.e. k = 0 by the first shortcut of poisson_inv.  The bound is
+// conservative by less than one unit of 2^-32: a draw that falls in that sliver (or any
+// draw that fires) takes the full path, which converts the words to doubles and runs the
+// oracle's inversion -- the results are those of the plain loop, bit for bit.
+template <int kRng> struct StepBits;
+template <> struct StepBits<VXB_RNG_REF> {
+    Words w[3];  // reaction q of fine step st owns Philox2x64 block 3 st + q
+    __device__ __forceinline__ void draw(const TauParams&, uint64_t key, uint64_t, uint64_t st) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) w[q] = philox2x64(key, 3 * st + q);
+    }
+    __device__ __forceinline__ uint32_t top_common(int q) const { return static_cast<uint32_t>(w[q].w0 >> 32); }
+    __device__ __forceinline__ uint32_t top_residual(int q) const { return static_cast<uint32_t>(w[q].w1 >> 32); }
+    __device__ __forceinline__ double common(int q) const { return to_unit(w[q].w0); }
+    __device__ __forceinline__ double residual(int q) const { return to_unit(w[q].w1); }
+    // top < bound  =>  x < T 2^11  =>  (x >> 11) < T = floor(thr 2^53)  =>  to_unit(x) <= thr
+    __device__ __forceinline__ static uint32_t bound(double lam) {
+        if (!(lam > 0.0)) return 0xFFFFFFFFu;  // never fires (the sliver still takes the full path)
+        const double thr = __dsub_rn(__dsub_rn(1.0, lam), 0x1p-48);
+        if (!(thr > 0.0)) return 0u;           // lam >= 1: always the full path
+        return static_cast<uint32_t>((__double2ull_rd(thr * 0x1p53) << 11) >> 32);
+    }
+};
+template <> struct StepBits<VXB_RNG_FAST> {
+    Words32 a, b;  // Philox4x32 blocks 2 st and 2 st + 1
+    __device__ __forceinline__ void draw(const TauParams& p, uint64_t, uint64_t path, uint64_t st) {
+        const uint32_t hi = kDomNoise | (p.level << 8) | (static_cast<uint32_t>((2 * st) >> 32) << 16);
+        const uint32_t pl = static_cast<uint32_t>(path), ph = static_cast<uint32_t>(path >> 32);
+        a = philox4x32(p.fast, static_cast<uint32_t>(2 * st), hi, pl, ph);
+        b = philox4x32(p.fast, static_cast<uint32_t>(2 * st + 1), hi, pl, ph);
+    }
+    __device__ __forceinline__ uint32_t top_common(int q) const { return q == 0 ? a.a : q == 1 ? a.c : b.a; }
+    __device__ __forceinline__ uint32_t top_residual(int q) const { return q == 0 ? a.b : q == 1 ? a.d : b.b; }
+    __device__ __forceinline__ double common(int q) const {
+        return q == 0 ? unit42(a.a, b.c & 1023u) : q == 1 ? unit42(a.c, (b.c >> 20) & 1023u)
+                                                           : unit42(b.a, (b.d >> 10) & 1023u);
+    }
+    __device__ __forceinline__ double residual(int q) const {
+        return q == 0 ? unit42(a.b, (b.c >> 10) & 1023u) : q == 1 ? unit42(a.d, b.d & 1023u)
+                                                                  : unit42(b.b, (b.d >> 20) & 1023u);
+    }
+    // top < bound = floor(thr 2^32)  =>  the 42-bit mantissa is below thr 2^42  =>  u < thr
+    __device__ __forceinline__ static uint32_t bound(double lam) {
+        if (!(lam > 0.0)) return 0xFFFFFFFFu;
+        const double thr = __dsub_rn(__dsub_rn(1.0, lam), 0x1p-48);
+        if (!(thr > 0.0)) return 0u;
+        return __double2uint_rd(thr * 0x1p32);
+    }
+};
 
 template <int kRng>
 __global__ void __launch_bounds__(kTlBlock, VXB_TL_MINB) tauleap_kernel(const __grid_constant__ TauParams p) {
@@ -358,14 +404,15 @@ __global__ void __launch_bounds__(kTlBlock, VXB_TL_MINB) tauleap_kernel(const __
             }
         } else {
             // On the fine levels (rate * tau ~ 1e-3) a step in which NOTHING fires is the
-            // rule, and then neither state nor propensities change.  The thresholds
-            // below which a uniform decides k = 0 (first shortcut of poisson_inv) are
+            // rule, and then neither state nor propensities change.  The bounds below
+            // which a draw decides k = 0 (first shortcut of poisson_inv, see StepBits) are
             // therefore kept in registers and refreshed only after an event or a new
-            // coarse step with a changed coarse state; a quiet step is three Philox blocks,
-            // six compares and ONE branch.  Same decisions as the oracle's loop, bit for bit.
+            // coarse step with a changed coarse state; a quiet step is the step's Philox
+            // blocks, six 32-bit compares and ONE branch.  Same decisions as the oracle's
+            // loop, bit for bit.
             uint32_t phase = 0;
             bool stale = true, coarse_moved = true;
-            double thr_c[3], thr_r[3];  // u <= thr: the common / residual Poisson is 0
+            uint32_t bound_c[3], bound_r[3];  // leading word below it: the common / residual Poisson is 0
             for (uint64_t st = 0; st < p.n_fine; ++st) {
                 if (phase == 0 && coarse_moved) {
                     c.prop(p.rate, ac);
@@ -379,8 +426,8 @@ __global__ void __launch_bounds__(kTlBlock, VXB_TL_MINB) tauleap_kernel(const __
                     for (int q = 0; q < 3; ++q) {
                         const double mn = af[q] < ac[q] ? af[q] : ac[q];
                         const double mx = af[q] > ac[q] ? af[q] : ac[q];
-                        thr_c[q] = zero_threshold(__dmul_rn(mn, p.tau));
-                        thr_r[q] = zero_threshold(__dmul_rn(__dsub_rn(mx, mn), p.tau));
+                        bound_c[q] = StepBits<kRng>::bound(__dmul_rn(mn, p.tau));
+                        bound_r[q] = StepBits<kRng>::bound(__dmul_rn(__dsub_rn(mx, mn), p.tau));
                     }
                     stale = false;
                 }
@@ -390,16 +437,12 @@ __global__ void __launch_bounds__(kTlBlock, VXB_TL_MINB) tauleap_kernel(const __
                 // BEFORE the inversions: their round chains are independent and interleave
                 // in one basic block, whereas the branches of an inversion fence off a
                 // block drawn after it
-                double u0[3], u1[3];
-                if (kRng == VXB_RNG_REF) {
-#pragma unroll
-                    for (int q = 0; q < 3; ++q) draw_pair<kRng>(p, key, path, 3 * st + q, u0[q], u1[q]);
-                } else {
-                    draw_six_fast(p, path, st, u0, u1);
-                }
+                StepBits<kRng> bits;
+                bits.draw(p, key, path, st);
                 bool quiet = true;
 #pragma unroll
-                for (int q = 0; q < 3; ++q) quiet = quiet & (u0[q] <= thr_c[q]) & (u1[q] <= thr_r[q]);
+                for (int q = 0; q < 3; ++q)
+                    quiet = quiet & (bits.top_common(q) < bound_c[q]) & (bits.top_residual(q) < bound_r[q]);
                 if (quiet) continue;
                 stale = true;
                 coarse_moved = true;
@@ -408,9 +451,9 @@ __global__ void __launch_bounds__(kTlBlock, VXB_TL_MINB) tauleap_kernel(const __
                     const bool fine_larger = af[q] > ac[q];
                     const double mn = af[q] < ac[q] ? af[q] : ac[q];
                     const double mx = fine_larger ? af[q] : ac[q];
-                    const int p1 = poisson_inv<PA>(__dmul_rn(mn, p.tau), u0[q], s_inv, it);
+                    const int p1 = poisson_inv<PA>(__dmul_rn(mn, p.tau), bits.common(q), s_inv, it);
                     // at most one of (af - m), (ac - m) is positive: one inversion serves both
-                    const int pr = poisson_inv<PA>(__dmul_rn(__dsub_rn(mx, mn), p.tau), u1[q], s_inv, it);
+                    const int pr = poisson_inv<PA>(__dmul_rn(__dsub_rn(mx, mn), p.tau), bits.residual(q), s_inv, it);
                     kf[q] = p1 + (fine_larger ? pr : 0);
                     kc[q] = p1 + (fine_larger ? 0 : pr);
                 }
