@@ -165,13 +165,19 @@ __device__ __forceinline__ int poisson_inv_f32(float lam, float v, const float* 
     }
     return k;
 }
-// Smallest word whose uniform decides k = 0 for rate lam (a multiple of 512), or the odd
-// value 1 when lam is too large for any uniform to do so.
+// 21 bits made of the low 11 bits of two Philox words (the fifth and sixth field of a block)
+__device__ __forceinline__ uint32_t low_field(uint32_t x, uint32_t y) {  // 21 bits of two words' low 11
+    return ((x & 0x7FFu) << 10) | ((y & 0x7FFu) >> 1);
+}
+// The 23-bit uniform m (midpoint (m + 1/2) 2^-23) decides k = 0 for rate lam iff
+// m >= Tm = ceil(lam 2^23 - 1/2) (the pre-test v >= lam of poisson_inv_f32; all exact in
+// float).  The quiet test sees only the leading 21 bits t of m: t >= ceil(Tm / 4) implies it.
+// Returns that bound on t, or 2^21 when no t can decide (lam too large).
 __device__ __forceinline__ uint32_t quiet_bound_f32(float lam) {
-    const float t = ceilf(lam * 8388608.0f - 0.5f);
-    if (!(t > 0.0f)) return 0u;         // lam <= 2^-24 (or not positive): every uniform
-    if (!(t < 8388608.0f)) return 1u;   // lam > 1 - 2^-24: none
-    return static_cast<uint32_t>(t) << 9;
+    const float tm = ceilf(lam * 8388608.0f - 0.5f);
+    if (!(tm > 0.0f)) return 0u;               // lam <= 2^-24 (or not positive): every uniform
+    if (!(tm < 8388608.0f)) return 1u << 21;   // lam > 1 - 2^-24: none
+    return (static_cast<uint32_t>(tm) + 3u) >> 2;
 }
 struct MMf {  // propensities in float from the integer state
     __device__ __forceinline__ static void prop(const MM& x, const float* k, float* a) {
@@ -214,16 +220,15 @@ __global__ void __launch_bounds__(kTlBlock, VXB_TL_MINB) tauleap_f32_kernel(cons
                 f.fire(k0, k1, k2);
             }
         } else {
-            // as in tauleap_kernel: the rates below which a uniform decides k = 0 stay in
-            // registers and are refreshed only after an event; a quiet step is two Philox
-            // blocks, six compares and one branch
+            // as in tauleap_kernel: the bounds above which a draw decides k = 0 stay in
+            // registers and are refreshed only after an event; a quiet step is ONE Philox
+            // block (the leading 21 bits of the six uniforms, fields as in
+            // StepBits<VXB_RNG_FAST>), six compares and one branch; a step that is not quiet
+            // draws the second block for the two trailing bits of the 23-bit uniforms
             uint32_t phase = 0;
             bool stale = true, coarse_moved = true;
-            // word >= bound  <=>  unit_f32(word) >= lam (exactly: the midpoint (m + 1/2) 2^-23
-            // of m = word >> 9 reaches lam iff m >= ceil(lam 2^23 - 1/2), all exact in float)
-            // <=>  the common / residual Poisson is 0 by the pre-test of poisson_inv_f32
-            uint32_t bound_c[3], bound_r[3];
-            bool loud = false;  // a rate >= 1: no uniform decides k = 0 up front
+            uint32_t bound_c[3], bound_r[3];  // reactions 0, 1: on the word (shifted by 11); 2: on the field
+            bool loud = false;  // some rate is too large for any uniform to decide k = 0 up front
             for (uint64_t st = 0; st < p.n_fine; ++st) {
                 if (phase == 0 && coarse_moved) {
                     MMf::prop(c, rate, ac);
@@ -240,21 +245,26 @@ __global__ void __launch_bounds__(kTlBlock, VXB_TL_MINB) tauleap_f32_kernel(cons
                         bound_c[q] = quiet_bound_f32(mn * tau);
                         bound_r[q] = quiet_bound_f32((mx - mn) * tau);
                     }
-                    loud = (bound_c[0] | bound_c[1] | bound_c[2] | bound_r[0] | bound_r[1] | bound_r[2]) & 1u;
+                    loud = ((bound_c[0] | bound_c[1] | bound_c[2] | bound_r[0] | bound_r[1] | bound_r[2]) >> 21) != 0;
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        bound_c[q] <<= 11;
+                        bound_r[q] <<= 11;
+                    }
                     stale = false;
                 }
-                // two Philox blocks per fine step: (a, b), (c, d) of the first and (a, b) of
-                // the second drive reactions 0, 1, 2 (common Poisson, residual Poisson)
                 const uint32_t hi = dom | (static_cast<uint32_t>((2 * st) >> 32) << 16);
                 const Words32 w0 = philox4x32(p.fast, static_cast<uint32_t>(2 * st), hi, pl, ph);
-                const Words32 w1 = philox4x32(p.fast, static_cast<uint32_t>(2 * st + 1), hi, pl, ph);
-                const uint32_t word[6] = {w0.a, w0.b, w0.c, w0.d, w1.a, w1.b};
-                bool quiet = !loud;
-#pragma unroll
-                for (int q = 0; q < 3; ++q) quiet = quiet & (word[2 * q] >= bound_c[q]) & (word[2 * q + 1] >= bound_r[q]);
+                const uint32_t t4 = low_field(w0.a, w0.b), t5 = low_field(w0.c, w0.d);
+                const bool quiet = !loud & (w0.a >= bound_c[0]) & (w0.b >= bound_r[0]) & (w0.c >= bound_c[1]) &
+                                   (w0.d >= bound_r[1]) & (t4 >= bound_c[2]) & (t5 >= bound_r[2]);
                 if (quiet) continue;
-                stale = true;
-                coarse_moved = true;
+                // the full 23-bit uniforms, left-aligned as unit_f32 takes them: 21 leading
+                // bits, then two bits of the second block
+                const Words32 w1 = philox4x32(p.fast, static_cast<uint32_t>(2 * st + 1), hi, pl, ph);
+                const uint32_t word[6] = {(w0.a & ~0x7FFu) | ((w1.a >> 30) << 9),  (w0.b & ~0x7FFu) | ((w1.b >> 30) << 9),
+                                          (w0.c & ~0x7FFu) | ((w1.c >> 30) << 9),  (w0.d & ~0x7FFu) | ((w1.d >> 30) << 9),
+                                          (t4 << 11) | (((w1.a >> 28) & 3u) << 9), (t5 << 11) | (((w1.b >> 28) & 3u) << 9)};
                 int kf[3], kc[3];
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
@@ -268,6 +278,9 @@ __global__ void __launch_bounds__(kTlBlock, VXB_TL_MINB) tauleap_f32_kernel(cons
                 }
                 f.fire(kf[0], kf[1], kf[2]);
                 c.fire(kc[0], kc[1], kc[2]);
+                // the bounds follow the fine state at once, the frozen coarse rates at the next coarse step
+                stale = (kf[0] | kf[1] | kf[2]) != 0;
+                coarse_moved = coarse_moved | ((kc[0] | kc[1] | kc[2]) != 0);
             }
         }
         const int32_t y = p.level == 0 ? f.p : f.p - c.p;
@@ -313,14 +326,6 @@ __device__ __forceinline__ void draw_pair(const TauParams& p, uint64_t key, uint
     }
 }
 
-// Throughput generator, coupled levels: the SIX uniforms of a fine step from TWO Philox4x32
-// blocks (2 st, 2 st + 1) -- 42 bits each (one word + 10 bits of the second block's last
-// two words: 2^-42 against event probabilities of ~1e-3 per step), a third less
-// generator work than a block per reaction.
-__device__ __forceinline__ double unit42(uint32_t w, uint32_t x10) {
-    return __dsub_rn(__hiloint2double(0x3FF00000u | (w >> 12), (w << 20) | (x10 << 10)), 1.0);
-}
-
 // The random bits of one coupled fine step, and the quiet test on them.  A uniform is
 // only ever COMPARED on the common path, so the test is done on the leading 32 bits of
 // the raw word against an integer bound (quiet_bound): `top < bound` implies
@@ -340,37 +345,54 @@ template <> struct StepBits<VXB_RNG_REF> {
     __device__ __forceinline__ double common(int q) const { return to_unit(w[q].w0); }
     __device__ __forceinline__ double residual(int q) const { return to_unit(w[q].w1); }
     // top < bound  =>  x < T 2^11  =>  (x >> 11) < T = floor(thr 2^53)  =>  to_unit(x) <= thr
-    __device__ __forceinline__ static uint32_t bound(double lam) {
+    __device__ __forceinline__ void complete(const TauParams&) {}
+    __device__ __forceinline__ static uint32_t bound(double lam, int) {
         if (!(lam > 0.0)) return 0xFFFFFFFFu;  // never fires (the sliver still takes the full path)
         const double thr = __dsub_rn(__dsub_rn(1.0, lam), 0x1p-48);
         if (!(thr > 0.0)) return 0u;           // lam >= 1: always the full path
         return static_cast<uint32_t>((__double2ull_rd(thr * 0x1p53) << 11) >> 32);
     }
 };
+// Throughput generator: ONE Philox4x32 block (2 st) carries the leading 21 bits of the six
+// uniforms of a fine step -- the leading 21 bits of its four words and two fields made of
+// their low 11 bits -- and decides a quiet step; only a step that is not quiet draws the
+// second block (2 st + 1) for the trailing 21 bits of the 42-bit uniforms.  Field order:
+// (common, residual) of reaction 0, of reaction 1 (words a b c d), of reaction 2 (low bits).
 template <> struct StepBits<VXB_RNG_FAST> {
-    Words32 a, b;  // Philox4x32 blocks 2 st and 2 st + 1
+    Words32 a, b;
+    uint32_t hi, pl, ph, ctr;
     __device__ __forceinline__ void draw(const TauParams& p, uint64_t, uint64_t path, uint64_t st) {
-        const uint32_t hi = kDomNoise | (p.level << 8) | (static_cast<uint32_t>((2 * st) >> 32) << 16);
-        const uint32_t pl = static_cast<uint32_t>(path), ph = static_cast<uint32_t>(path >> 32);
-        a = philox4x32(p.fast, static_cast<uint32_t>(2 * st), hi, pl, ph);
-        b = philox4x32(p.fast, static_cast<uint32_t>(2 * st + 1), hi, pl, ph);
+        hi = kDomNoise | (p.level << 8) | (static_cast<uint32_t>((2 * st) >> 32) << 16);
+        pl = static_cast<uint32_t>(path);
+        ph = static_cast<uint32_t>(path >> 32);
+        ctr = static_cast<uint32_t>(2 * st);
+        a = philox4x32(p.fast, ctr, hi, pl, ph);
     }
-    __device__ __forceinline__ uint32_t top_common(int q) const { return q == 0 ? a.a : q == 1 ? a.c : b.a; }
-    __device__ __forceinline__ uint32_t top_residual(int q) const { return q == 0 ? a.b : q == 1 ? a.d : b.b; }
-    __device__ __forceinline__ double common(int q) const {
-        return q == 0 ? unit42(a.a, b.c & 1023u) : q == 1 ? unit42(a.c, (b.c >> 20) & 1023u)
-                                                           : unit42(b.a, (b.d >> 10) & 1023u);
-    }
-    __device__ __forceinline__ double residual(int q) const {
-        return q == 0 ? unit42(a.b, (b.c >> 10) & 1023u) : q == 1 ? unit42(a.d, b.d & 1023u)
-                                                                  : unit42(b.b, (b.d >> 20) & 1023u);
-    }
-    // top < bound = floor(thr 2^32)  =>  the 42-bit mantissa is below thr 2^42  =>  u < thr
-    __device__ __forceinline__ static uint32_t bound(double lam) {
-        if (!(lam > 0.0)) return 0xFFFFFFFFu;
+    // leading bits in the form the bounds are stored in: the whole word for reactions 0 and 1
+    // (bound shifted left by 11), the 21-bit field for reaction 2
+    __device__ __forceinline__ uint32_t top_common(int q) const { return q == 0 ? a.a : q == 1 ? a.c : low_field(a.a, a.b); }
+    __device__ __forceinline__ uint32_t top_residual(int q) const { return q == 0 ? a.b : q == 1 ? a.d : low_field(a.c, a.d); }
+    // top21 < floor(thr 2^21)  =>  the 42-bit mantissa is below thr 2^42  =>  u < thr
+    __device__ __forceinline__ static uint32_t bound(double lam, int q) {
+        const uint32_t all = q == 2 ? 0x1FFFFFu : 0xFFFFFFFFu;
+        if (!(lam > 0.0)) return all;
         const double thr = __dsub_rn(__dsub_rn(1.0, lam), 0x1p-48);
         if (!(thr > 0.0)) return 0u;
-        return __double2uint_rd(thr * 0x1p32);
+        const uint32_t b21 = __double2uint_rd(thr * 0x1p21);
+        return q == 2 ? b21 : b21 << 11;
+    }
+    __device__ __forceinline__ void complete(const TauParams& p) { b = philox4x32(p.fast, ctr + 1, hi, pl, ph); }
+    // 42-bit uniform from leading and trailing 21 bits: 1.m - 1 with m = top : low : 0...
+    __device__ __forceinline__ static double unit42(uint32_t top, uint32_t low) {
+        return __dsub_rn(__hiloint2double(0x3FF00000u | (top >> 1), (top << 31) | (low << 10)), 1.0);
+    }
+    __device__ __forceinline__ double common(int q) const {
+        return q == 0 ? unit42(a.a >> 11, b.a >> 11) : q == 1 ? unit42(a.c >> 11, b.c >> 11)
+                                                             : unit42(low_field(a.a, a.b), low_field(b.a, b.b));
+    }
+    __device__ __forceinline__ double residual(int q) const {
+        return q == 0 ? unit42(a.b >> 11, b.b >> 11) : q == 1 ? unit42(a.d >> 11, b.d >> 11)
+                                                             : unit42(low_field(a.c, a.d), low_field(b.c, b.d));
     }
 };
 
@@ -426,8 +448,8 @@ __global__ void __launch_bounds__(kTlBlock, VXB_TL_MINB) tauleap_kernel(const __
                     for (int q = 0; q < 3; ++q) {
                         const double mn = af[q] < ac[q] ? af[q] : ac[q];
                         const double mx = af[q] > ac[q] ? af[q] : ac[q];
-                        bound_c[q] = StepBits<kRng>::bound(__dmul_rn(mn, p.tau));
-                        bound_r[q] = StepBits<kRng>::bound(__dmul_rn(__dsub_rn(mx, mn), p.tau));
+                        bound_c[q] = StepBits<kRng>::bound(__dmul_rn(mn, p.tau), q);
+                        bound_r[q] = StepBits<kRng>::bound(__dmul_rn(__dsub_rn(mx, mn), p.tau), q);
                     }
                     stale = false;
                 }
@@ -444,21 +466,28 @@ __global__ void __launch_bounds__(kTlBlock, VXB_TL_MINB) tauleap_kernel(const __
                 for (int q = 0; q < 3; ++q)
                     quiet = quiet & (bits.top_common(q) < bound_c[q]) & (bits.top_residual(q) < bound_r[q]);
                 if (quiet) continue;
-                stale = true;
-                coarse_moved = true;
+                bits.complete(p);
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
                     const bool fine_larger = af[q] > ac[q];
                     const double mn = af[q] < ac[q] ? af[q] : ac[q];
                     const double mx = fine_larger ? af[q] : ac[q];
-                    const int p1 = poisson_inv<PA>(__dmul_rn(mn, p.tau), bits.common(q), s_inv, it);
+                    // a draw that is quiet by itself is 0 without being converted (the few lanes
+                    // of a warp that are here rarely have more than one draw that is not)
+                    int p1 = 0, pr = 0;
+                    if (!(bits.top_common(q) < bound_c[q]))
+                        p1 = poisson_inv<PA>(__dmul_rn(mn, p.tau), bits.common(q), s_inv, it);
                     // at most one of (af - m), (ac - m) is positive: one inversion serves both
-                    const int pr = poisson_inv<PA>(__dmul_rn(__dsub_rn(mx, mn), p.tau), bits.residual(q), s_inv, it);
+                    if (!(bits.top_residual(q) < bound_r[q]))
+                        pr = poisson_inv<PA>(__dmul_rn(__dsub_rn(mx, mn), p.tau), bits.residual(q), s_inv, it);
                     kf[q] = p1 + (fine_larger ? pr : 0);
                     kc[q] = p1 + (fine_larger ? 0 : pr);
                 }
                 f.fire(kf[0], kf[1], kf[2]);
                 c.fire(kc[0], kc[1], kc[2]);
+                // the bounds follow the fine state at once, the frozen coarse rates at the next coarse step
+                stale = (kf[0] | kf[1] | kf[2]) != 0;
+                coarse_moved = coarse_moved | ((kc[0] | kc[1] | kc[2]) != 0);
             }
         }
         const int32_t y = p.level == 0 ? f.p : f.p - c.p;
