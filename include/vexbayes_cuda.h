@@ -82,6 +82,10 @@ enum { VXB_KEY_PARTICLE = 0, VXB_KEY_WORKER = 1 };
  *   consts[0..3] = initial (S,E,C,P), consts[4..6] = (k1,k2,k3).  precision VXB_F32
  *   (with VXB_RNG_FAST only): propensities and the Poisson inversion in float, exp by one
  *   MUFU; the state stays integer.  Statistically validated, like every throughput mode.
+ *   VXB_RNG_REF: reaction r of coupled fine step s owns stream positions 6s+2r, 6s+2r+1
+ *   (bit-exact with the oracle).  VXB_RNG_FAST: the six uniforms of a coupled fine step
+ *   come from Philox4x32 blocks 2s (leading 21 bits) and 2s+1 (trailing bits; drawn only
+ *   when a reaction may fire): 42-bit uniforms in fp64, 23-bit bucket midpoints in fp32.
  * VXB_MODEL_TB            the multi-genotype TB transmission model (tb_model.hpp),
  *   exact Gillespie; theta = (alpha, delta, tau) with the prior of
  *   tb::sample_prior, dim = 3, summaries (G, H), summary_dim = 2;
