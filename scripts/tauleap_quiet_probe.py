@@ -1,5 +1,7 @@
+"""Config 4 with the reaction rates as they are and scaled to ~zero (every fine step quiet):
+the second run is what the generator alone costs, the difference is the inversion path."""
 import os, sys, time
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1902_09046_b200 import _abi as A, lib, models as M
 ctx = lib.Context(0)
 c = A.vxb_mlmc_cfg()
