@@ -154,6 +154,9 @@ int vxb_device_info(vxb_ctx* ctx, vxb_device_props* out);
 void* vxb_stream(vxb_ctx* ctx);
 int vxb_synchronize(vxb_ctx* ctx);
 /* Event-time every kernel launch (adds two events per launch). */
+/* Context options.  VXB_OPT_EARLY_REJECT (0 / 1, default 0): see vxb_abc_reject. */
+enum { VXB_OPT_EARLY_REJECT = 1 };
+int vxb_set_option(vxb_ctx* ctx, int option, int64_t value);
 int vxb_profile_enable(vxb_ctx* ctx, int on);
 int vxb_profile_reset(vxb_ctx* ctx);
 int vxb_profile_read(vxb_ctx* ctx, vxb_profile* out); /* synchronises */
@@ -274,7 +277,11 @@ int vxb_compact_accepted(vxb_ctx* ctx, int precision, const void* rho, const uin
  * leave the GPU.  If n_accepted points to DEVICE memory the call is fully
  * asynchronous: the count is written there, idx/params/rho must be device
  * buffers (or NULL), nothing is copied to the host and the stream is not
- * synchronised -- steps can be queued back to back. */
+ * synchronised -- steps can be queued back to back.
+ * With VXB_OPT_EARLY_REJECT (vxb_set_option; off by default) a row stops as soon as its
+ * partial squared distance can no longer end below epsilon^2 -- the sum of squares only
+ * grows -- and the accepted set, indices, parameters and distances are bit-identical to
+ * the full simulation; only the (never returned) distances of rejected rows differ. */
 int vxb_abc_reject(vxb_ctx* ctx, const vxb_model* model, const vxb_keying* key,
                    uint64_t n_total, uint64_t first, uint64_t count, const double* observed,
                    double epsilon, uint64_t cap, uint64_t* n_accepted, uint64_t* idx,

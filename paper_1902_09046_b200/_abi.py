@@ -6,6 +6,7 @@ C ABI takes.  Field order and types must match the header exactly.
 """
 import ctypes as C
 
+VXB_OPT_EARLY_REJECT = 1
 VXB_ABI_VERSION = 2
 
 VXB_MODEL_LOGISTIC_SDE, VXB_MODEL_NORMAL_MEAN, VXB_MODEL_MM_TAULEAP, VXB_MODEL_TOGGLE = 1, 2, 3, 4
@@ -108,5 +109,5 @@ EXPORTED_SYMBOLS = (
     "vxb_multi_mlmc_tauleap", "vxb_abcsmc_pack_round", "vxb_abcsmc_append_round",
     "vxb_normalise_by_chunk_totals", "vxb_guard_report", "vxb_rng_fast_stats",
     "vxb_sharded_abcsmc_run", "vxb_multi_abcsmc_run", "vxb_fast_generator_rounds", "vxb_multi_init_loopback", "vxb_multi_weak_info_test", "vxb_host_exp_variant",
-    "vxb_sharded_ppp_pvalues", "vxb_sharded_mlmc_tauleap", "vxb_sharded_select_epsilon", "vxb_multi_select_epsilon",
+    "vxb_sharded_ppp_pvalues", "vxb_sharded_mlmc_tauleap", "vxb_sharded_select_epsilon", "vxb_multi_select_epsilon", "vxb_set_option",
 )

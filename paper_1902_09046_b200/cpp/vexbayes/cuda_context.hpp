@@ -69,5 +69,12 @@ inline vxb_multi* multi() {
 inline int devices_in_use() { return vxb_multi_size(multi()); }
 // The first device's context: single-GPU entry points run here.
 inline vxb_ctx* context() { return vxb_multi_ctx(multi(), 0); }
+// Early rejection in abc::reject_fixed_epsilon (VXB_OPT_EARLY_REJECT, off by default): rows
+// stop once their partial distance is beyond epsilon; the accepted set is unchanged, bit
+// for bit.  Applies to the devices in use now (set it again after set_devices).
+inline void set_early_reject(bool on) {
+    for (int r = 0; r < devices_in_use(); ++r)
+        check(vxb_set_option(vxb_multi_ctx(multi(), r), VXB_OPT_EARLY_REJECT, on ? 1 : 0));
+}
 
 }  // namespace vexbayes::cuda

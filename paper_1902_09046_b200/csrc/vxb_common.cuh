@@ -76,6 +76,8 @@ struct vxb_ctx {
     // which build of the host libm's exp the device reproduces (csrc/vxb_libmexp.cuh):
     // 0 FMA build, 1 plain build, -1 neither matched the live std::exp (FMA build used)
     int exp_variant = 0;
+    // vxb_set_option(VXB_OPT_EARLY_REJECT): vxb_abc_reject stops rows that can no longer be accepted
+    bool early_reject = false;
 };
 
 namespace vxb {

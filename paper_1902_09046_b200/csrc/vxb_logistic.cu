@@ -6,7 +6,9 @@
 // The kernel is FP64-pipe bound (fp32: FP32/MUFU bound); HBM traffic is the
 // per-row outputs only (<= 8 B/row on the fused fixed-epsilon path).
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <limits>
 
 #include "vxb_internal.cuh"
@@ -25,6 +27,22 @@ struct AbcParams {
     void* rho;
     uint8_t* failed;
     const void* noise;
+    // early rejection: partial squared distance beyond which a row is lost; +inf: off
+    double ss_bound = std::numeric_limits<double>::infinity();
+    // Early rejection in SEGMENTS (vxb_abc_reject): this launch simulates observations
+    // [obs_begin, obs_end) of its rows; rows that are still alive at the end of a segment
+    // that is not the last are appended to the out-queue (row offset, state, partial sum)
+    // and the next launch takes them from there, densely packed again -- a warp whose rows
+    // died one by one would otherwise run on for its last survivor.
+    uint32_t obs_begin = 0, obs_end = 0xFFFFFFFFu;
+    const uint32_t* in_rows = nullptr;  // null: rows 0 .. count-1 from the initial state
+    const void* in_x = nullptr;
+    const void* in_ss = nullptr;
+    const unsigned long long* in_count = nullptr;
+    uint32_t* out_rows = nullptr;  // null: last segment
+    void* out_x = nullptr;
+    void* out_ss = nullptr;
+    unsigned long long* out_count = nullptr;
 };
 
 #ifndef VXB_SIM_BLOCK
@@ -35,11 +53,16 @@ struct AbcParams {
 #endif
 constexpr int kBlock = VXB_SIM_BLOCK;
 
-template <class Real, int kRng, bool kFma>
+// kSeg: the segment form of early rejection (queues in / out, a range of observations, a
+// strided loop over the items); false compiles to the plain one-row-per-thread kernel.
+template <class Real, int kRng, bool kFma, bool kSeg>
 // (block, CTAs per SM) swept on a B200: fp64 is best with the registers it asks for
 // (2.73e8 sims/s at (256, 1) against 2.49-2.56e8 at 3-4 CTAs per SM); the fp32
 // throughput instance gains 1.6 % from four CTAs per SM.
-__global__ void __launch_bounds__(kBlock, (sizeof(Real) == 4 && kRng == VXB_RNG_FAST) ? 4 : VXB_SIM_MIN_BLOCKS)
+#ifndef VXB_SEG_MIN_BLOCKS
+#define VXB_SEG_MIN_BLOCKS 2  // the segment form asks for 140 registers in fp64: capped at 128 (two CTAs per SM) 116.5 against 132.8 ms
+#endif
+__global__ void __launch_bounds__(kBlock, (sizeof(Real) == 4 && kRng == VXB_RNG_FAST) ? 4 : kSeg ? VXB_SEG_MIN_BLOCKS : VXB_SIM_MIN_BLOCKS)
 logistic_abc_kernel(const __grid_constant__ AbcParams p) {
     // fast fp64 generator: stage the 2 KB log table in shared memory
     __shared__ double2 s_log[(kRng == VXB_RNG_FAST && sizeof(Real) == 8) ? kFastTableSize : 1];
@@ -47,71 +70,101 @@ logistic_abc_kernel(const __grid_constant__ AbcParams p) {
         for (int i = threadIdx.x; i < kFastTableSize; i += kBlock) s_log[i] = p.log_table[i];
         __syncthreads();
     }
-    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
-    if (r >= p.count) return;
-    const uint64_t row = p.first + r;
-    uint64_t key, base;
-    locate_row(p.key, row, key, base);
+    // one item per thread; a launch over a queue runs a fixed grid with a stride
+    const bool queued = kSeg && p.in_rows != nullptr;
+    const uint64_t n_items = queued ? *p.in_count : p.count;
+    auto run_item = [&](const uint64_t item) {
+        const uint64_t r = queued ? p.in_rows[item] : item;
+        const uint64_t row = p.first + r;
+        uint64_t key, base;
+        locate_row(p.key, row, key, base);
 
-    double theta[3];
-    uint64_t noise_pos;
-    if (p.theta_in) {
-        theta[0] = p.theta_in[0];
-        theta[1] = p.theta_in[1];
-        theta[2] = p.theta_in[2];
-        noise_pos = base + (base & 1);
-    } else {
-        if (kRng == VXB_RNG_FAST)
-            draw_prior_fast(p.model, p.key.fast, row, theta);
-        else
-            draw_prior_ref(p.model, key, base, theta);
-        noise_pos = base + 4;  // three uniforms, aligned to the pair boundary
-    }
-    if (sizeof(Real) == 4) {
-        theta[0] = static_cast<double>(static_cast<float>(theta[0]));
-        theta[1] = static_cast<double>(static_cast<float>(theta[1]));
-        theta[2] = static_cast<double>(static_cast<float>(theta[2]));
-    }
-    if (p.params) {
-        Real* out = static_cast<Real*>(p.params) + r * 3;
-        out[0] = static_cast<Real>(theta[0]);
-        out[1] = static_cast<Real>(theta[1]);
-        out[2] = static_cast<Real>(theta[2]);
-    }
-
-    Real* summary = p.summaries ? static_cast<Real*>(p.summaries) + r * p.model.n_obs : nullptr;
-    auto emit = [summary](uint32_t k, Real v) {
-        if (summary) summary[k] = v;
-    };
-    using A = typename std::conditional<
-        kFma, typename std::conditional<kRng == VXB_RNG_FAST && sizeof(Real) == 8, FusedCompact, Fused>::type,
-        Exact>::type;
-    bool bad;
-    Real rho;
-    if (kRng == VXB_RNG_REF) {
-        RefNoise<Real> noise(key, noise_pos >> 1);
-        rho = logistic_path<Real, A>(p.model, theta, p.observed, noise, emit, bad);
-    } else if (kRng == VXB_RNG_FAST) {
-        const uint32_t rl = static_cast<uint32_t>(row), rh = static_cast<uint32_t>(row >> 32);
-        if constexpr (sizeof(Real) == 4) {
-            FastNoise32 noise(p.key.fast, rl, rh, 0u);
-            rho = logistic_path<Real, A>(p.model, theta, p.observed, noise, emit, bad);
+        double theta[3];
+        uint64_t noise_pos;
+        if (p.theta_in) {
+            theta[0] = p.theta_in[0];
+            theta[1] = p.theta_in[1];
+            theta[2] = p.theta_in[2];
+            noise_pos = base + (base & 1);
         } else {
-            FastNoise64 noise(p.key.fast, s_log, rl, rh, 0u);
-            rho = logistic_path<Real, A>(p.model, theta, p.observed, noise, emit, bad);
+            if (kRng == VXB_RNG_FAST)
+                draw_prior_fast(p.model, p.key.fast, row, theta);
+            else
+                draw_prior_ref(p.model, key, base, theta);
+            noise_pos = base + 4;  // three uniforms, aligned to the pair boundary
         }
+        if (sizeof(Real) == 4) {
+            theta[0] = static_cast<double>(static_cast<float>(theta[0]));
+            theta[1] = static_cast<double>(static_cast<float>(theta[1]));
+            theta[2] = static_cast<double>(static_cast<float>(theta[2]));
+        }
+        if (p.params) {
+            Real* out = static_cast<Real*>(p.params) + r * 3;
+            out[0] = static_cast<Real>(theta[0]);
+            out[1] = static_cast<Real>(theta[1]);
+            out[2] = static_cast<Real>(theta[2]);
+        }
+
+        Real* summary = p.summaries ? static_cast<Real*>(p.summaries) + r * p.model.n_obs : nullptr;
+        auto emit = [summary](uint32_t k, Real v) {
+            if (summary) summary[k] = v;
+        };
+        using A = typename std::conditional<
+            kFma, typename std::conditional<kRng == VXB_RNG_FAST && sizeof(Real) == 8, FusedCompact, Fused>::type,
+            Exact>::type;
+        bool bad;
+        const Real ss_bound = static_cast<Real>(p.ss_bound);  // +inf stays +inf
+        Real x = queued ? static_cast<const Real*>(p.in_x)[item] : static_cast<Real>(p.model.x0);
+        Real ss = queued ? static_cast<const Real*>(p.in_ss)[item] : Real(0);
+        const uint32_t obs_begin = kSeg ? p.obs_begin : 0u, obs_end = kSeg ? p.obs_end : 0xFFFFFFFFu;
+        const uint32_t step0 = obs_begin * p.model.obs_stride;  // a multiple of the noise batch
+        if (kRng == VXB_RNG_REF) {
+            RefNoise<Real> noise(key, (noise_pos >> 1) + (step0 >> 1));
+            logistic_segment<Real, A>(p.model, theta, p.observed, noise, emit, bad, ss_bound, obs_begin, obs_end, x, ss);
+        } else if (kRng == VXB_RNG_FAST) {
+            const uint32_t rl = static_cast<uint32_t>(row), rh = static_cast<uint32_t>(row >> 32);
+            if constexpr (sizeof(Real) == 4) {
+                FastNoise32 noise(p.key.fast, rl, rh, 3u * (step0 / FastNoise32::kBatch));
+                logistic_segment<Real, A>(p.model, theta, p.observed, noise, emit, bad, ss_bound, obs_begin, obs_end, x, ss);
+            } else {
+                FastNoise64 noise(p.key.fast, s_log, rl, rh, 3u * (step0 / FastNoise64::kBatch));
+                logistic_segment<Real, A>(p.model, theta, p.observed, noise, emit, bad, ss_bound, obs_begin, obs_end, x, ss);
+            }
+        } else {
+            ExternalNoise<Real> noise{static_cast<const Real*>(p.noise) + r * p.model.steps, step0,
+                                      p.model.steps};
+            logistic_segment<Real, A>(p.model, theta, p.observed, noise, emit, bad, ss_bound, obs_begin, obs_end, x, ss);
+        }
+        if (kSeg && p.out_rows && ss <= ss_bound) {
+            // alive at the end of a segment that is not the last: hand the row on (one
+            // atomic per warp; the order inside the queue is irrelevant, rho is addressed by row)
+            const unsigned alive = __activemask();
+            const unsigned lane = threadIdx.x & 31u;
+            const int leader = __ffs(alive) - 1;
+            unsigned long long slot = 0;
+            if (lane == static_cast<unsigned>(leader)) slot = atomicAdd(p.out_count, static_cast<unsigned long long>(__popc(alive)));
+            slot = __shfl_sync(alive, slot, leader) + __popc(alive & ((1u << lane) - 1u));
+            p.out_rows[slot] = static_cast<uint32_t>(r);
+            static_cast<Real*>(p.out_x)[slot] = x;
+            static_cast<Real*>(p.out_ss)[slot] = ss;
+            return;
+        }
+        Real rho = Exact::sqrt(ss);
+        if (bad) {  // abc.cpp:57-60: flag the row, zero its summary, rho stays NaN
+            rho = static_cast<Real>(__longlong_as_double(0x7FF8000000000000LL));
+            if (summary)
+                for (uint32_t k = 0; k < p.model.n_obs; ++k) summary[k] = Real(0);
+        }
+        if (p.rho) static_cast<Real*>(p.rho)[r] = rho;
+        if (p.failed) p.failed[r] = bad ? 1 : 0;
+    };
+    const uint64_t first_item = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
+    if constexpr (kSeg) {
+        const uint64_t stride_items = static_cast<uint64_t>(gridDim.x) * kBlock;
+        for (uint64_t item = first_item; item < n_items; item += stride_items) run_item(item);
     } else {
-        ExternalNoise<Real> noise{static_cast<const Real*>(p.noise) + r * p.model.steps, 0,
-                                  p.model.steps};
-        rho = logistic_path<Real, A>(p.model, theta, p.observed, noise, emit, bad);
+        if (first_item < n_items) run_item(first_item);
     }
-    if (bad) {  // abc.cpp:57-60: flag the row, zero its summary, rho stays NaN
-        rho = static_cast<Real>(__longlong_as_double(0x7FF8000000000000LL));
-        if (summary)
-            for (uint32_t k = 0; k < p.model.n_obs; ++k) summary[k] = Real(0);
-    }
-    if (p.rho) static_cast<Real*>(p.rho)[r] = rho;
-    if (p.failed) p.failed[r] = bad ? 1 : 0;
 }
 
 // The standard normals the step loop of the throughput generator consumes for
@@ -247,12 +300,30 @@ Keying make_keying(const vxb_keying& k, const vxb_model& m, uint64_t n_total) {
 
 template <class Real, int kRng>
 void launch_abc2(vxb_ctx* ctx, const AbcParams& p, bool fma) {
-    const unsigned grid = grid_for(p.count, kBlock);
+    unsigned grid = grid_for(p.count, kBlock);
+    const bool seg = p.in_rows || p.out_rows || p.obs_begin != 0 || p.obs_end < p.model.n_obs;
+    if (seg) {
+        if constexpr (kRng != VXB_RNG_EXTERNAL) {
+            auto kernel = fma ? logistic_abc_kernel<Real, kRng, true, true> : logistic_abc_kernel<Real, kRng, false, true>;
+            if (p.in_rows) {
+                // over a queue whose length only the device knows: a grid of resident CTAs, strided
+                int per_sm = 0;
+                VXB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, 0));
+                grid = std::min<unsigned>(grid, static_cast<unsigned>(ctx->prop.multiProcessorCount * std::max(per_sm, 1) * 4));
+            }
+            LaunchScope scope(ctx, VXB_K_SIMULATE);
+            kernel<<<grid, kBlock, 0, ctx->stream>>>(p);
+            check_launch("logistic_abc_kernel (segment)");
+        } else {
+            raise("internal", "segments are driven by vxb_abc_reject only");
+        }
+        return;
+    }
     LaunchScope scope(ctx, VXB_K_SIMULATE);
     if (fma)
-        logistic_abc_kernel<Real, kRng, true><<<grid, kBlock, 0, ctx->stream>>>(p);
+        logistic_abc_kernel<Real, kRng, true, false><<<grid, kBlock, 0, ctx->stream>>>(p);
     else
-        logistic_abc_kernel<Real, kRng, false><<<grid, kBlock, 0, ctx->stream>>>(p);
+        logistic_abc_kernel<Real, kRng, false, false><<<grid, kBlock, 0, ctx->stream>>>(p);
     check_launch("logistic_abc_kernel");
 }
 template <class Real>
@@ -425,6 +496,107 @@ extern "C" int vxb_simulate_at(vxb_ctx* ctx, const vxb_model* model, const doubl
     });
 }
 
+// Partial squared distance beyond which a row cannot be accepted any more.  The sum of
+// squares only grows (every term is added as RN(d^2 + ss) >= ss) and rho = RN(sqrt(ss)) is
+// accepted iff rho <= epsilon (compared in double): ss > eps^2 (1 + m) gives
+// sqrt(ss) > eps (1 + m/2 - m^2/8), which survives the rounding of the square root with
+// m = 2^-50 in fp64 (one ulp is <= 2^-52 relative) and m = 2^-21 in fp32 (<= 2^-23).
+// Rounded UP to the working precision; a negative or non-finite epsilon switches it off.
+static double early_reject_bound(double epsilon, bool f32) {
+    if (!(epsilon >= 0.0) || !std::isfinite(epsilon)) return std::numeric_limits<double>::infinity();
+    const double b = epsilon * epsilon * (1.0 + (f32 ? 0x1p-21 : 0x1p-50));
+    if (!std::isfinite(b)) return std::numeric_limits<double>::infinity();
+    if (f32) {
+        float bf = static_cast<float>(b);
+        if (static_cast<double>(bf) < b) bf = std::nextafter(bf, std::numeric_limits<float>::infinity());
+        return static_cast<double>(bf);
+    }
+    return std::nextafter(b, std::numeric_limits<double>::infinity());
+}
+
+// Early rejection in up to five launches (see AbcParams): observations [0, b1) for every
+// row, [b1, b2) for the rows alive at b1, ... -- the survivors are re-packed between the
+// launches, so warps stay full although most rows die early (BASELINE config 1: 34 % alive
+// after 4 of 20 observations, 15 % after 6, 5 % after 8, 0.6 % after 12, 0.1 % at the end;
+// scripts/survivors_probe.py).  Segment boundaries are multiples of the noise batch in steps.  Nothing returns to
+// the host: queue lengths stay on the device.  false: not applicable (plain launch).
+static bool early_reject_segments(vxb_ctx* ctx, const vxb_model& model, AbcParams p) {
+    if (!std::isfinite(p.ss_bound) || p.count < (1u << 16) || p.count >= (1ull << 32)) return false;
+    const uint32_t n_obs = p.model.n_obs, stride = p.model.obs_stride;
+    const uint32_t batch = model.rng == VXB_RNG_FAST ? (model.precision == VXB_F32 ? 16u : 8u) : 2u;
+    uint32_t g = batch, t = stride % batch;  // gcd(stride, batch)
+    while (t) {
+        const uint32_t u = g % t;
+        g = t;
+        t = u;
+    }
+    const uint32_t align = batch / g;  // observations per aligned boundary
+    auto up = [&](uint32_t v) { return (v + align - 1) / align * align; };
+    // boundaries: VXB_EARLY_BOUNDS="b1,b2,..." (experiments) or 20 / 30 / 40 / 60 % of the
+    // observations (BASELINE config 1 at 1e8 rows, fp64 throughput instance: 104 ms with
+    // 4,6,8,12 against 117 ms with 4,8 and 351 ms without early rejection;
+    // scripts/early_reject_sweep.sh)
+    uint32_t bounds[8] = {0};
+    int n_seg = 1;
+    if (const char* env = getenv("VXB_EARLY_BOUNDS")) {
+        for (const char* c = env; *c && n_seg < 6;) {
+            const uint32_t v = up(static_cast<uint32_t>(strtoul(c, const_cast<char**>(&c), 10)));
+            if (v > bounds[n_seg - 1] && v < n_obs) bounds[n_seg++] = v;
+            while (*c == ',') ++c;
+        }
+    } else {
+        for (const uint32_t tenth : {2u, 3u, 4u, 6u}) {
+            const uint32_t v = up((n_obs * tenth + 9) / 10);
+            if (v > bounds[n_seg - 1] && v < n_obs) bounds[n_seg++] = v;
+        }
+    }
+    if (n_seg < 2) return false;
+    bounds[n_seg] = n_obs;
+    const size_t real = model.precision == VXB_F32 ? 4 : 8;
+    // two queues of `count` entries each: rows (u32), x, ss; two counters in front
+    const size_t per_queue = (p.count * (4 + 2 * real) + 64 + 15) & ~size_t(15);
+    char* base = static_cast<char*>(arena_get(ctx, 3, 64 + 2 * per_queue));
+    VXB_CUDA(cudaMemsetAsync(base, 0, 64, ctx->stream));
+    auto* counts = reinterpret_cast<unsigned long long*>(base);
+    struct Queue {
+        uint32_t* rows;
+        void *x, *ss;
+    } q[2];
+    for (int k = 0; k < 2; ++k) {
+        char* b = base + 64 + k * per_queue;
+        q[k].x = b;
+        q[k].ss = b + p.count * real;
+        q[k].rows = reinterpret_cast<uint32_t*>(b + 2 * p.count * real);
+    }
+    for (int seg = 0; seg < n_seg; ++seg) {
+        AbcParams s = p;
+        s.obs_begin = bounds[seg];
+        s.obs_end = seg == n_seg - 1 ? 0xFFFFFFFFu : bounds[seg + 1];
+        if (seg > 0) {  // queues alternate; every segment has its own counter
+            s.in_rows = q[(seg - 1) & 1].rows;
+            s.in_x = q[(seg - 1) & 1].x;
+            s.in_ss = q[(seg - 1) & 1].ss;
+            s.in_count = counts + (seg - 1);
+        }
+        if (seg < n_seg - 1) {
+            s.out_rows = q[seg & 1].rows;
+            s.out_x = q[seg & 1].x;
+            s.out_ss = q[seg & 1].ss;
+            s.out_count = counts + seg;
+        }
+        launch_abc(ctx, model, s);
+    }
+    return true;
+}
+
+extern "C" int vxb_set_option(vxb_ctx* ctx, int option, int64_t value) {
+    return guarded([&] {
+        use(ctx);
+        require(option == VXB_OPT_EARLY_REJECT, "invalid-argument", "unknown option");
+        ctx->early_reject = value != 0;
+    });
+}
+
 extern "C" int vxb_abc_reject(vxb_ctx* ctx, const vxb_model* model, const vxb_keying* key,
                               uint64_t n_total, uint64_t first, uint64_t count,
                               const double* observed, double epsilon, uint64_t cap,
@@ -447,7 +619,8 @@ extern "C" int vxb_abc_reject(vxb_ctx* ctx, const vxb_model* model, const vxb_ke
         const size_t real = f32 ? 4 : 8;
         p.rho = arena_get(ctx, 0, count * real);
         p.failed = static_cast<uint8_t*>(arena_get(ctx, 1, count));
-        launch_abc(ctx, *model, p);
+        if (ctx->early_reject) p.ss_bound = early_reject_bound(epsilon, f32);
+        if (!early_reject_segments(ctx, *model, p)) launch_abc(ctx, *model, p);
 
         Staged d_idx(ctx, idx, cap * sizeof(uint64_t), false, true);
         Scratch d_idx_tmp(ctx, d_idx.ptr() ? 0 : cap * sizeof(uint64_t));

@@ -9,6 +9,8 @@
 // aligned to even (abc.cpp:53), and position 4+j is the normal of step j+1.
 #pragma once
 
+#include <cmath>
+
 #include "vxb_rng.cuh"
 
 #define VXB_MAX_SUMMARY 128
@@ -196,14 +198,23 @@ __device__ __forceinline__ Real logistic_step(Real x, Real a, Real c, Real inv_k
     }
 }
 
-// Runs one path; returns rho.  Summaries are handed to `emit(k, value)` as they
-// are produced, so the trajectory never leaves registers; the squared distance
-// accumulates left to right in observation order (abc.cpp:16-24).  `bad` is set
-// when an observed state is not finite.
+// Runs observations [obs_begin, obs_end) of one path: steps obs_begin * stride up to
+// obs_end * stride (up to the last step when obs_end == n_obs), from state x and partial
+// squared distance ss, both updated in place.  Summaries are handed to `emit(k, value)` as
+// they are produced, so the trajectory never leaves registers; the squared distance
+// accumulates left to right in observation order (abc.cpp:16-24).  `bad` is set when an
+// observed state is not finite.  The noise source must stand at step obs_begin * stride
+// (a multiple of its batch).
+// ss_bound (early rejection, vxb_abc_reject with VXB_OPT_EARLY_REJECT; +inf otherwise): the
+// squared distance only grows, so a row whose partial sum exceeds the bound can no longer
+// come out with rho <= epsilon; the segment stops at the first observation at which that
+// holds for every row of the warp (observations fall on the same step in every row).
 template <class Real, class A, class Noise, class Emit>
-__device__ __forceinline__ Real logistic_path(const LogisticModel& m, const double* theta,
-                                              const double* __restrict__ observed, Noise& noise,
-                                              Emit&& emit, bool& bad) {
+__device__ __forceinline__ void logistic_segment(const LogisticModel& m, const double* theta,
+                                                 const double* __restrict__ observed, Noise& noise,
+                                                 Emit&& emit, bool& bad, Real ss_bound,
+                                                 uint32_t obs_begin, uint32_t obs_end, Real& x_io,
+                                                 Real& ss_io) {
     const Real r = static_cast<Real>(theta[0]);
     const Real k = static_cast<Real>(theta[1]);
     const Real sigma = static_cast<Real>(theta[2]);
@@ -211,12 +222,15 @@ __device__ __forceinline__ Real logistic_path(const LogisticModel& m, const doub
     const Real c = Exact::mul(sigma, static_cast<Real>(m.sqdt));
     const Real inv_k = Exact::div(Real(1), k);
     const Real a1 = Real(1) + a, bk = -a * inv_k;  // throughput-mode form of the step
-    Real x = static_cast<Real>(m.x0);
-    Real ss = 0;
-    uint32_t next = 0, since = 0;
+    Real x = x_io;
+    Real ss = ss_io;
+    uint32_t next = obs_begin, since = 0;
+    bool stop = false;
+    const bool early = isfinite(ss_bound);
     bad = false;
     constexpr uint32_t kB = Noise::kBatch;
-    const uint32_t steps = m.steps, stride = m.obs_stride;
+    const uint32_t stride = m.obs_stride;
+    const uint32_t steps = obs_end >= m.n_obs ? m.steps : obs_end * stride;
     auto observe = [&] {
         since = 0;
         if (next < m.n_obs) {
@@ -225,9 +239,10 @@ __device__ __forceinline__ Real logistic_path(const LogisticModel& m, const doub
             bad = bad || !isfinite(x);
             emit(next, x);
             ++next;
+            if (early) stop = __all_sync(__activemask(), !(ss <= ss_bound)) != 0;
         }
     };
-    if (stride % kB == 0 && steps == stride * m.n_obs) {
+    if (stride % kB == 0 && m.steps == stride * m.n_obs) {
         // observation stride a multiple of the batch (e.g. the exact instance, batch 2,
         // on the BASELINE grid of 100): whole batches between observations, no per-step
         // bookkeeping.  The throughput instances on the BASELINE grid (100 = 12 x 8 + 4 =
@@ -235,7 +250,8 @@ __device__ __forceinline__ Real logistic_path(const LogisticModel& m, const doub
         // (fp64: 70.8 ms per 2e7 rows at stride 100 against 71.9-72.3 ms at strides 80 /
         // 200 / 400, which come through here; profiles/r2_stride_probe.json)
         const uint32_t per = stride / kB;
-        for (uint32_t k = 0; k < m.n_obs; ++k) {
+        const uint32_t last = obs_end < m.n_obs ? obs_end : m.n_obs;
+        for (uint32_t o = obs_begin; o < last; ++o) {
             for (uint32_t i = 0; i < per; ++i) {
                 Real z[kB];
                 noise.next(z);
@@ -243,11 +259,14 @@ __device__ __forceinline__ Real logistic_path(const LogisticModel& m, const doub
                 for (uint32_t q = 0; q < kB; ++q) x = logistic_step<Real, A>(x, a, c, inv_k, z[q], a1, bk);
             }
             observe();
+            if (stop) break;
         }
-        return Exact::sqrt(ss);
+        x_io = x;
+        ss_io = ss;
+        return;
     }
-    uint32_t j = 0;
-    for (; j + kB <= steps; j += kB) {
+    uint32_t j = obs_begin * stride;
+    for (; j + kB <= steps && !stop; j += kB) {
         Real z[kB];
         noise.next(z);
         if (since + kB < stride) {  // no observation inside this batch (warp-uniform)
@@ -262,7 +281,7 @@ __device__ __forceinline__ Real logistic_path(const LogisticModel& m, const doub
             }
         }
     }
-    if (j < steps) {  // ragged tail: fewer than kBatch steps left
+    if (j < steps && !stop) {  // ragged tail: fewer than kBatch steps left
         Real z[kB];
         noise.next(z);
         for (uint32_t q = 0; j + q < steps; ++q) {
@@ -270,6 +289,17 @@ __device__ __forceinline__ Real logistic_path(const LogisticModel& m, const doub
             if (++since == stride) observe();
         }
     }
+    x_io = x;
+    ss_io = ss;
+}
+
+// Runs one whole path; returns rho.
+template <class Real, class A, class Noise, class Emit>
+__device__ __forceinline__ Real logistic_path(const LogisticModel& m, const double* theta,
+                                              const double* __restrict__ observed, Noise& noise,
+                                              Emit&& emit, bool& bad) {
+    Real x = static_cast<Real>(m.x0), ss = 0;
+    logistic_segment<Real, A>(m, theta, observed, noise, emit, bad, static_cast<Real>(INFINITY), 0u, m.n_obs, x, ss);
     return Exact::sqrt(ss);
 }
 

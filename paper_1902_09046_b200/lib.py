@@ -384,6 +384,11 @@ class Context:
         self._check(self.lib.vxb_host_exp_variant(self.handle, C.byref(v)))
         return v.value
 
+    def set_early_reject(self, on=True):
+        """vxb_abc_reject stops rows whose partial distance already exceeds epsilon (same
+        accepted set, bit for bit); off by default."""
+        self._check(self.lib.vxb_set_option(self.handle, i32(A.VXB_OPT_EARLY_REJECT), C.c_int64(1 if on else 0)))
+
     def guard_report(self, selftest=False):
         """Guard mode (VXB_GUARD=1): (violations so far, self-test detected or None)."""
         v, d = C.c_ulonglong(), C.c_int(-1)

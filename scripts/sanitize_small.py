@@ -31,6 +31,11 @@ print("order", ctx.order_statistics(rho, f, [0, 5, n // 2])[0])
 for prec, rng in ((A.VXB_F64, A.VXB_RNG_FAST), (A.VXB_F32, A.VXB_RNG_FAST), (A.VXB_F64, A.VXB_RNG_REF)):
     mv = M.logistic_model(steps=200, obs_stride=10, precision=prec, rng=rng)
     print("reject", ctx.abc_reject(mv, M.keying(7), n, 0, n, obs, 30.0, cap=n)[0])
+ctx.set_early_reject(True)   # segment launches with survivor queues (70 001 rows: above the threshold)
+for prec, rng in ((A.VXB_F64, A.VXB_RNG_FAST), (A.VXB_F32, A.VXB_RNG_FAST), (A.VXB_F64, A.VXB_RNG_REF)):
+    mv = M.logistic_model(steps=200, obs_stride=10, precision=prec, rng=rng)
+    print("early reject", ctx.abc_reject(mv, M.keying(7), 70001, 0, 70001, obs, 30.0, cap=70001)[0])
+ctx.set_early_reject(False)
 idx, params, r, n_dev = D.sharded_reject(ctx, m, M.keying(3), n, obs, 30.0, cap_fraction=0.5)
 ctx.synchronize()
 print("sharded_reject", int(n_dev.item()))

@@ -153,6 +153,14 @@ int main(int argc, char** argv) {
         std::printf("reject %llu", static_cast<unsigned long long>(acc.total_accepted));
         for (auto r : acc.rows) std::printf(" %llu", static_cast<unsigned long long>(r));
         std::printf("\n");
+        {   // early rejection (opt-in): the same accepted set, bit for bit
+            cuda::set_early_reject(true);
+            const auto early = abc::reject_fixed_epsilon(model, 20000, 0, 20000, 1337, observed, sel.epsilon, 20000);
+            cuda::set_early_reject(false);
+            std::printf("early_reject_identical %d\n",
+                        static_cast<int>(early.total_accepted == acc.total_accepted && early.rows == acc.rows &&
+                                         early.params == acc.params && early.discrepancies == acc.discrepancies));
+        }
 
         // error behaviour mirrors the reference
         int ok = 0;

@@ -265,6 +265,50 @@ def test_fused_reject_path(ctx, oracle, golden, precision):
     assert eq(np.concatenate([i1, i2]), idx_o) and eq(np.concatenate([p1, p2]), p[idx_o])
 
 
+def test_early_rejection_returns_the_same_accepted_set(ctx, oracle, golden):
+    """VXB_OPT_EARLY_REJECT: rows stop once their partial squared distance is beyond
+    epsilon^2, survivors are re-packed between segment launches.  The accepted set --
+    count, indices, parameters, distances -- must be bit-identical to the full simulation:
+    every instance of the fused kernel, job sizes above and below the segment threshold
+    (65 536 rows), shards with an offset, epsilon = 0 (nobody), a 2 % epsilon and an epsilon
+    nobody exceeds (every row survives every segment: queues at full capacity), grids whose
+    observation stride forces aligned segment boundaries (stride 10 and 25 against noise
+    batches of 8 / 16) and trailing steps after the last observation; and the exact instance
+    against the oracle."""
+    obs = golden["logistic_observed"]
+    variants = [dict(), dict(arith=A.VXB_ARITH_FMA), dict(rng=A.VXB_RNG_FAST),
+                dict(rng=A.VXB_RNG_FAST, precision=A.VXB_F32), dict(precision=A.VXB_F32)]
+    grids = [dict(steps=2000, obs_stride=100), dict(steps=200, obs_stride=10), dict(steps=500, obs_stride=25),
+             dict(steps=2050, obs_stride=100)]
+    try:
+        for gi, grid in enumerate(grids):
+            o = obs if grid["steps"] // grid["obs_stride"] == 20 else obs[:grid["steps"] // grid["obs_stride"]]
+            for kw in variants if gi == 0 else variants[2:4] + variants[:1]:
+                m = M.logistic_model(**grid, **kw)
+                for n, first, count in ((70001, 0, 70001), (200000, 66000, 134000), (5000, 0, 5000)):
+                    ctx.set_early_reject(False)
+                    _, _, _, rho_all = ctx.abc_reject(m, M.keying(11), n, first, count, o, 1e30, cap=count)
+                    eps2 = float(np.quantile(rho_all[np.isfinite(rho_all)].astype(np.float64), 0.02))
+                    for eps in (0.0, eps2, 1e30):
+                        ctx.set_early_reject(False)
+                        full = ctx.abc_reject(m, M.keying(11), n, first, count, o, eps, cap=count)
+                        ctx.set_early_reject(True)
+                        early = ctx.abc_reject(m, M.keying(11), n, first, count, o, eps, cap=count)
+                        assert full[0] == early[0], (grid, kw, n, eps)
+                        assert all(eq(a, b) for a, b in zip(full[1:], early[1:])), (grid, kw, n, eps)
+                        assert eps != eps2 or 0.015 * count < full[0] < 0.025 * count
+        # worker keying (reference stream layout) and the oracle
+        m = M.logistic_model()
+        key = M.keying(1337, A.VXB_KEY_WORKER, 5, 4)
+        n = 70001
+        p, _, rho, f = oracle.abc_prior_predictive(m, key, n, 0, n, obs, want_summaries=False)
+        eps, idx_o = oracle.select_epsilon(rho, f, 0.01)
+        nacc, idx, params, rho_acc = ctx.abc_reject(m, key, n, 0, n, obs, eps, cap=n)
+        assert nacc == len(idx_o) and eq(idx, idx_o) and eq(params, p[idx_o]) and eq(rho_acc, rho[idx_o])
+    finally:
+        ctx.set_early_reject(False)
+
+
 def test_fast_generator_statistics(ctx, oracle, golden):
     """Mode B of north_star: the throughput generator is validated end to end --
     acceptance rate and posterior moments within Monte-Carlo error and a

@@ -53,6 +53,7 @@ def test_cpp_shim_matches_oracle(tmp_path, oracle, golden):
     p2, _, rho2, f2 = oracle.abc_prior_predictive(m, M.keying(1337), 20000, 0, 20000, obs, want_summaries=False)
     want = np.nonzero((rho2 <= eps) & (f2 == 0))[0]
     assert int(r["reject"][0]) == len(want) and [int(t) for t in r["reject"][1:]] == want.tolist()
+    assert r["early_reject_identical"] == ["1"]      # cuda::set_early_reject: same accepted set
     assert r["errors"] == ["6"]
     g = oracle.fill_gaussian(7, 1, 0, 768)
     assert float(r["ess"][0]) == oracle.ess(g[512:])          # bit-exact: host-libm exp, sequential sums
