@@ -244,6 +244,12 @@ class Multi:
         except Exception:
             pass
 
+    def set_early_reject(self, on=True):
+        """VXB_OPT_EARLY_REJECT on every device of the group (see Context.set_early_reject)."""
+        for r in range(self.size):
+            self._check(self.lib.vxb_set_option(P(self.lib.vxb_multi_ctx(self.handle, r)),
+                                                i32(A.VXB_OPT_EARLY_REJECT), C.c_int64(1 if on else 0)))
+
     def abc_prior_predictive(self, model, key, n, observed, want_summaries=True):
         dt = np.float32 if model.precision == A.VXB_F32 else np.float64
         obs = np.ascontiguousarray(observed, dtype=np.float64)

@@ -188,6 +188,12 @@ def test_multi_rank_drivers_on_one_gpu_through_the_loopback_group(ctx, oracle, g
     nacc, idx, params, rho_acc = multi.abc_reject(m, M.keying(7), 40001, obs, eps, cap=40001)
     assert nacc == len(idx_o) and np.array_equal(idx, idx_o)
     assert np.array_equal(params, p[idx_o]) and np.array_equal(rho_acc, rho[idx_o])
+    # early rejection on every rank (segment launches per shard): the same gathered set
+    multi.set_early_reject(True)
+    big = multi.abc_reject(m, M.keying(7), 300007, obs, eps, cap=300007)
+    multi.set_early_reject(False)
+    ref = multi.abc_reject(m, M.keying(7), 300007, obs, eps, cap=300007)
+    assert big[0] == ref[0] > 1000 and all(np.array_equal(a, b) for a, b in zip(big[1:], ref[1:]))
     # config 0's selection over a sharded distance vector: all-reduced digit histograms.
     # Same epsilon bits and the same indices as the oracle / one context, with failed rows
     # (flag-only, NaN-only, both), ties, fp32 keys, a capacity below the accepted count,
