@@ -24,6 +24,14 @@ def same(results):
     return True
 
 
+def early(c, call):
+    c.set_early_reject(True)
+    try:
+        return call()
+    finally:
+        c.set_early_reject(False)
+
+
 @pytest.mark.timeout(900)
 def test_kernels_with_shared_memory_or_atomics_are_repeatable(ctx, golden):
     obs = golden["logistic_observed"]
@@ -49,6 +57,8 @@ def test_kernels_with_shared_memory_or_atomics_are_repeatable(ctx, golden):
             lambda c: c.select_epsilon(rho, f, 0.013)[:2],
         "order_statistics": lambda c: (c.order_statistics(rho, f, [0, 17, n // 3, n - 200])[0],),
         "abc_reject (compaction + gather)": lambda c: c.abc_reject(m, M.keying(5), n, 0, n, o, 40.0, cap=n)[1:],
+        "abc_reject with early rejection (survivor queues filled through warp-aggregated atomics)":
+            lambda c: early(c, lambda: c.abc_reject(m, M.keying(5), 90011, 0, 90011, o, 40.0, cap=90011)[1:]),
         "resample / ess (sequential exp-sum hand-off between warps)":
             lambda c: c.resample_multinomial(lw, parts, 77, 9) + (np.array([c.ess(lw), c.logsumexp(lw)]),),
         "tauleap (shared sums, atomics)": lambda c: tuple(c.mlmc_tauleap(M.mm_tauleap_model(), mc)[k]
