@@ -78,6 +78,14 @@ def test_config1_full_size_properties(ctx, config0, variant):
     assert n1 + n2 == k
     assert np.array_equal(np.concatenate([i1, i2]).astype(np.int64), i)
     assert np.array_equal(np.concatenate([r1, r2]).astype(np.float64), r)
+    # opt-in early rejection (segment launches, survivor queues): the same set, bit for bit
+    ctx.set_early_reject(True)
+    try:
+        n3, i3, p3, r3 = ctx.abc_reject(m, M.keying(1337), n, 0, n, obs, eps, cap)
+    finally:
+        ctx.set_early_reject(False)
+    assert n3 == k and np.array_equal(i3.astype(np.int64), i)
+    assert np.array_equal(r3.astype(np.float64), r) and np.array_equal(p3.astype(np.float64), th)
 
 
 # ---------------------------------------------------------------------------
