@@ -486,7 +486,7 @@ def main():
                 except Exception as e:
                     early[name] = {"error": f"{type(e).__name__}: {e}"}
             early["note"] = ("vxb_set_option(VXB_OPT_EARLY_REJECT): a row stops when its partial squared distance "
-                             "exceeds epsilon^2; survivors are re-packed between up to five segment launches; "
+                             "exceeds epsilon^2; survivors are re-packed between up to six segment launches; "
                              "accepted indices, parameters and distances bit-identical to the full simulation")
             line["opt_in_early_reject"] = early
     if rank == 0:

@@ -514,7 +514,7 @@ static double early_reject_bound(double epsilon, bool f32) {
     return std::nextafter(b, std::numeric_limits<double>::infinity());
 }
 
-// Early rejection in up to five launches (see AbcParams): observations [0, b1) for every
+// Early rejection in up to six launches (see AbcParams): observations [0, b1) for every
 // row, [b1, b2) for the rows alive at b1, ... -- the survivors are re-packed between the
 // launches, so warps stay full although most rows die early (BASELINE config 1: 34 % alive
 // after 4 of 20 observations, 15 % after 6, 5 % after 8, 0.6 % after 12, 0.1 % at the end;
@@ -532,10 +532,11 @@ static bool early_reject_segments(vxb_ctx* ctx, const vxb_model& model, AbcParam
     }
     const uint32_t align = batch / g;  // observations per aligned boundary
     auto up = [&](uint32_t v) { return (v + align - 1) / align * align; };
-    // boundaries: VXB_EARLY_BOUNDS="b1,b2,..." (experiments) or 20 / 30 / 40 / 60 % of the
-    // observations (BASELINE config 1 at 1e8 rows, fp64 throughput instance: 104 ms with
-    // 4,6,8,12 against 117 ms with 4,8 and 351 ms without early rejection;
-    // scripts/early_reject_sweep.sh)
+    // boundaries: VXB_EARLY_BOUNDS="b1,b2,..." (experiments) or 15 / 20 / 30 / 40 / 60 % of
+    // the observations, rounded up to the alignment (BASELINE config 1 at 1e8 rows, fp64
+    // throughput instance: 104 ms with 4,6,8,12 against 117 ms with 4,8 and 351 ms without
+    // early rejection; the exact instance, whose batch of two allows it, 315 ms with
+    // 3,4,6,8,12 against 340 ms; scripts/early_reject_sweep.sh)
     uint32_t bounds[8] = {0};
     int n_seg = 1;
     if (const char* env = getenv("VXB_EARLY_BOUNDS")) {
@@ -545,8 +546,8 @@ static bool early_reject_segments(vxb_ctx* ctx, const vxb_model& model, AbcParam
             while (*c == ',') ++c;
         }
     } else {
-        for (const uint32_t tenth : {2u, 3u, 4u, 6u}) {
-            const uint32_t v = up((n_obs * tenth + 9) / 10);
+        for (const uint32_t twentieth : {3u, 4u, 6u, 8u, 12u}) {
+            const uint32_t v = up((n_obs * twentieth + 19) / 20);
             if (v > bounds[n_seg - 1] && v < n_obs) bounds[n_seg++] = v;
         }
     }
