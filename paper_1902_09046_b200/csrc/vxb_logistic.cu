@@ -117,7 +117,7 @@ logistic_abc_kernel(const __grid_constant__ AbcParams p) {
         Real x = queued ? static_cast<const Real*>(p.in_x)[item] : static_cast<Real>(p.model.x0);
         Real ss = queued ? static_cast<const Real*>(p.in_ss)[item] : Real(0);
         const uint32_t obs_begin = kSeg ? p.obs_begin : 0u, obs_end = kSeg ? p.obs_end : 0xFFFFFFFFu;
-        const uint32_t step0 = obs_begin * p.model.obs_stride;  // a multiple of the noise batch
+        const uint32_t step0 = obs_begin * p.model.obs_stride;  // the noise source starts at the batch that holds it
         if (kRng == VXB_RNG_REF) {
             RefNoise<Real> noise(key, (noise_pos >> 1) + (step0 >> 1));
             logistic_segment<Real, A>(p.model, theta, p.observed, noise, emit, bad, ss_bound, obs_begin, obs_end, x, ss);
@@ -518,36 +518,28 @@ static double early_reject_bound(double epsilon, bool f32) {
 // row, [b1, b2) for the rows alive at b1, ... -- the survivors are re-packed between the
 // launches, so warps stay full although most rows die early (BASELINE config 1: 34 % alive
 // after 4 of 20 observations, 15 % after 6, 5 % after 8, 0.6 % after 12, 0.1 % at the end;
-// scripts/survivors_probe.py).  Segment boundaries are multiples of the noise batch in steps.  Nothing returns to
-// the host: queue lengths stay on the device.  false: not applicable (plain launch).
+// scripts/survivors_probe.py).  Nothing returns to the host: queue lengths stay on the
+// device.  false: not applicable (plain launch).
 static bool early_reject_segments(vxb_ctx* ctx, const vxb_model& model, AbcParams p) {
     if (!std::isfinite(p.ss_bound) || p.count < (1u << 16) || p.count >= (1ull << 32)) return false;
-    const uint32_t n_obs = p.model.n_obs, stride = p.model.obs_stride;
-    const uint32_t batch = model.rng == VXB_RNG_FAST ? (model.precision == VXB_F32 ? 16u : 8u) : 2u;
-    uint32_t g = batch, t = stride % batch;  // gcd(stride, batch)
-    while (t) {
-        const uint32_t u = g % t;
-        g = t;
-        t = u;
-    }
-    const uint32_t align = batch / g;  // observations per aligned boundary
-    auto up = [&](uint32_t v) { return (v + align - 1) / align * align; };
+    const uint32_t n_obs = p.model.n_obs;
+    // a segment may begin inside a noise batch (logistic_segment skips the normals of the
+    // previous segment), so every observation is a possible boundary
     // boundaries: VXB_EARLY_BOUNDS="b1,b2,..." (experiments) or 15 / 20 / 30 / 40 / 60 % of
-    // the observations, rounded up to the alignment (BASELINE config 1 at 1e8 rows, fp64
-    // throughput instance: 104 ms with 4,6,8,12 against 117 ms with 4,8 and 351 ms without
-    // early rejection; the exact instance, whose batch of two allows it, 315 ms with
-    // 3,4,6,8,12 against 340 ms; scripts/early_reject_sweep.sh)
+    // the observations (BASELINE config 1 at 1e8 rows, fp64 throughput instance: 104 ms with
+    // 4,6,8,12 against 117 ms with 4,8 and 351 ms without early rejection; the exact
+    // instance 315 ms with 3,4,6,8,12 against 340 ms; scripts/early_reject_sweep.sh)
     uint32_t bounds[8] = {0};
     int n_seg = 1;
     if (const char* env = getenv("VXB_EARLY_BOUNDS")) {
         for (const char* c = env; *c && n_seg < 6;) {
-            const uint32_t v = up(static_cast<uint32_t>(strtoul(c, const_cast<char**>(&c), 10)));
+            const uint32_t v = static_cast<uint32_t>(strtoul(c, const_cast<char**>(&c), 10));
             if (v > bounds[n_seg - 1] && v < n_obs) bounds[n_seg++] = v;
             while (*c == ',') ++c;
         }
     } else {
         for (const uint32_t twentieth : {3u, 4u, 6u, 8u, 12u}) {
-            const uint32_t v = up((n_obs * twentieth + 19) / 20);
+            const uint32_t v = (n_obs * twentieth + 19) / 20;
             if (v > bounds[n_seg - 1] && v < n_obs) bounds[n_seg++] = v;
         }
     }

@@ -203,8 +203,8 @@ __device__ __forceinline__ Real logistic_step(Real x, Real a, Real c, Real inv_k
 // squared distance ss, both updated in place.  Summaries are handed to `emit(k, value)` as
 // they are produced, so the trajectory never leaves registers; the squared distance
 // accumulates left to right in observation order (abc.cpp:16-24).  `bad` is set when an
-// observed state is not finite.  The noise source must stand at step obs_begin * stride
-// (a multiple of its batch).
+// observed state is not finite.  The noise source must stand at the batch that holds step
+// obs_begin * stride.
 // ss_bound (early rejection, vxb_abc_reject with VXB_OPT_EARLY_REJECT; +inf otherwise): the
 // squared distance only grows, so a row whose partial sum exceeds the bound can no longer
 // come out with rho <= epsilon; the segment stops at the first observation at which that
@@ -266,6 +266,16 @@ __device__ __forceinline__ void logistic_segment(const LogisticModel& m, const d
         return;
     }
     uint32_t j = obs_begin * stride;
+    if (const uint32_t skip = j % kB) {
+        // a segment that begins inside a noise batch (the source stands at the batch that
+        // holds step j): the first skip normals belong to the previous segment
+        Real z[kB];
+        noise.next(z);
+        for (uint32_t q = skip; q < kB && j < steps; ++q, ++j) {
+            x = logistic_step<Real, A>(x, a, c, inv_k, z[q], a1, bk);
+            if (++since == stride) observe();
+        }
+    }
     for (; j + kB <= steps && !stop; j += kB) {
         Real z[kB];
         noise.next(z);
