@@ -305,6 +305,9 @@ def test_early_rejection_returns_the_same_accepted_set(ctx, oracle, golden):
         eps, idx_o = oracle.select_epsilon(rho, f, 0.01)
         nacc, idx, params, rho_acc = ctx.abc_reject(m, key, n, 0, n, obs, eps, cap=n)
         assert nacc == len(idx_o) and eq(idx, idx_o) and eq(params, p[idx_o]) and eq(rho_acc, rho[idx_o])
+        import ctypes as C
+        assert ctx.lib.vxb_set_option(ctx.handle, C.c_int(99), C.c_int64(1)) != 0      # unknown option
+        assert ctx.lib.vxb_last_error().decode().startswith("invalid-argument")
     finally:
         ctx.set_early_reject(False)
 
