@@ -578,7 +578,7 @@ int vxb_mlmc_tauleap(vxb_ctx* ctx, const vxb_model* model, const vxb_mlmc_cfg* c
 typedef struct vxb_comm vxb_comm;
 typedef struct vxb_multi vxb_multi;
 #define VXB_COMM_ID_BYTES 128
-enum { VXB_DT_U8 = 0, VXB_DT_I64 = 1, VXB_DT_U64 = 2, VXB_DT_F64 = 3 };
+enum { VXB_DT_U8 = 0, VXB_DT_I64 = 1, VXB_DT_U64 = 2, VXB_DT_F64 = 3, VXB_DT_U32 = 4 };
 enum { VXB_OP_SUM = 0, VXB_OP_MAX = 1 };
 
 int vxb_device_count(int* count);

@@ -78,7 +78,7 @@ class vxb_mlmc_out(C.Structure):
 
 
 VXB_COMM_ID_BYTES = 128
-VXB_DT_U8, VXB_DT_I64, VXB_DT_U64, VXB_DT_F64 = 0, 1, 2, 3
+VXB_DT_U8, VXB_DT_I64, VXB_DT_U64, VXB_DT_F64, VXB_DT_U32 = 0, 1, 2, 3, 4
 VXB_OP_SUM, VXB_OP_MAX = 0, 1
 
 

@@ -349,6 +349,7 @@ extern "C" int vxb_comm_allreduce(vxb_comm* comm, void* buf, size_t count, int d
             case VXB_DT_U8: dt = ncclUint8; break;
             case VXB_DT_I64: dt = ncclInt64; break;
             case VXB_DT_U64: dt = ncclUint64; break;
+            case VXB_DT_U32: dt = ncclUint32; break;
             case VXB_DT_F64: dt = ncclFloat64; break;
             default: raise("invalid-argument", "unknown element type");
         }
@@ -395,7 +396,7 @@ extern "C" int vxb_sharded_abc_reject(vxb_ctx* ctx, vxb_comm* comm, const vxb_mo
                            layout->cap, reinterpret_cast<uint64_t*>(base + layout->off_count),
                            reinterpret_cast<uint64_t*>(base + layout->off_idx),
                            base + layout->off_params, base + layout->off_rho));
-        if (world > 1)
+        if (comm && packed_all)  // a one-rank communicator gathers too (the NCCL path on a one-GPU box)
             comm_allgather(comm, packed_local, packed_all, layout->stride);
         else if (packed_all && packed_all != packed_local)
             VXB_CUDA(cudaMemcpyAsync(packed_all, packed_local, layout->stride,
@@ -729,7 +730,7 @@ extern "C" int vxb_sharded_ppp_pvalues(vxb_ctx* ctx, vxb_comm* comm, const vxb_m
         if (e > b)
             abi(vxb_ppp_pvalues(ctx, model, lambda, log_norm, n_lambda, m_total, b, e - b, seed, ybar_obs,
                                 local.data(), nullptr, nullptr));
-        if (world > 1) {
+        if (comm) {
             Scratch d(ctx, n_lambda * 8);
             VXB_CUDA(cudaMemcpyAsync(d.as<void>(), local.data(), n_lambda * 8, cudaMemcpyHostToDevice, ctx->stream));
             comm_allreduce_sum_i64(comm, d.as<long long>(), n_lambda);
@@ -759,7 +760,7 @@ extern "C" int vxb_sharded_mlmc_tauleap(vxb_ctx* ctx, vxb_comm* comm, const vxb_
             for (uint32_t l = 0; l < cfg->levels; ++l)
                 abi(vxb_mlmc_level(ctx, model, cfg, l, b, e - b, reinterpret_cast<int64_t*>(sums.data() + 4 * l),
                                    nullptr));
-        if (world > 1) {
+        if (comm) {
             Scratch d(ctx, sums.size() * 8);
             VXB_CUDA(cudaMemcpyAsync(d.as<void>(), sums.data(), sums.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
             comm_allreduce_sum_i64(comm, d.as<long long>(), sums.size());

@@ -480,7 +480,7 @@ void order_statistics_device(vxb_ctx* ctx, const Real* rho, const uint8_t* faile
     // picking kernel makes every rank walk the digits of the WHOLE vector's order
     // statistics -- 6 (fp64) or 3 (fp32) all-reduces of n_ranks x 2048 counters, and no
     // distance ever leaves its device.  n may be zero on a rank.
-    const bool shared = comm_size(comm) > 1;
+    const bool shared = comm != nullptr;  // a one-rank communicator runs its collectives too (tests)
     require(n_ranks >= 1 && n_ranks <= kMaxRanks, "invalid-argument", "too many ranks");
     Scratch d_state(ctx, sizeof(SelectState));
     Scratch d_hist(ctx, sizeof(unsigned int) * kMaxRanks * kBins);
@@ -549,7 +549,7 @@ uint64_t count_valid_device(vxb_ctx* ctx, const Real* rho, const uint8_t* failed
     }
     // several ranks: both counts are those of the whole vector (every rank must take the
     // same with / without flags decision, and the same ranks)
-    if (comm_size(comm) > 1) comm_allreduce_sum_i64(comm, d_cnt.as<long long>(), 2);
+    if (comm) comm_allreduce_sum_i64(comm, d_cnt.as<long long>(), 2);
     unsigned long long c[2] = {0, 0};
     VXB_CUDA(cudaMemcpyAsync(c, d_cnt.as<void>(), sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
     VXB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -801,10 +801,9 @@ extern "C" int vxb_sharded_select_epsilon(vxb_ctx* ctx, vxb_comm* comm, int prec
         require(n_local == 0 || rho_local, "invalid-argument", "null distances");
         require(accept_fraction > 0.0 && accept_fraction <= 1.0, "invalid-argument",
                 "accept fraction must lie in (0, 1]");
-        const int world = comm_size(comm);
         require(cap == 0 || (block_local && is_device_pointer(block_local)), "invalid-argument",
                 "block_local is a device buffer of VXB_INDEX_BLOCK_BYTES(cap)");
-        require(cap == 0 || world == 1 || (blocks_all && is_device_pointer(blocks_all)), "invalid-argument",
+        require(cap == 0 || !comm || (blocks_all && is_device_pointer(blocks_all)), "invalid-argument",
                 "blocks_all is a device buffer of n_ranks blocks");
         const size_t real = precision == VXB_F32 ? 4 : 8;
         Staged d_rho(ctx, rho_local, n_local * real, true, false);
@@ -819,13 +818,13 @@ extern "C" int vxb_sharded_select_epsilon(vxb_ctx* ctx, vxb_comm* comm, int prec
         compact_accepted_device(ctx, precision, d_rho.ptr(), d_failed.as<uint8_t>(), n_local, eps, first_row,
                                 cap, count_dev, cap ? reinterpret_cast<uint64_t*>(static_cast<char*>(block_local) + 16)
                                                     : nullptr);
-        if (cap && world > 1)
+        if (cap && comm)
             comm_allgather(comm, block_local, blocks_all, block);
         else if (cap && blocks_all && blocks_all != block_local)
             VXB_CUDA(cudaMemcpyAsync(blocks_all, block_local, block, cudaMemcpyDeviceToDevice, ctx->stream));
         uint64_t* total_dev = d_count.as<uint64_t>() + 1;
         VXB_CUDA(cudaMemcpyAsync(total_dev, count_dev, sizeof(uint64_t), cudaMemcpyDeviceToDevice, ctx->stream));
-        if (world > 1) comm_allreduce_sum_i64(comm, reinterpret_cast<long long*>(total_dev), 1);
+        if (comm) comm_allreduce_sum_i64(comm, reinterpret_cast<long long*>(total_dev), 1);
         uint64_t total = 0;
         VXB_CUDA(cudaMemcpyAsync(&total, total_dev, sizeof(total), cudaMemcpyDeviceToHost, ctx->stream));
         VXB_CUDA(cudaStreamSynchronize(ctx->stream));

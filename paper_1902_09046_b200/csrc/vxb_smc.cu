@@ -1226,6 +1226,9 @@ extern "C" int vxb_sharded_abcsmc_run(vxb_ctx* ctx, vxb_comm* comm, const vxb_mo
         const uint64_t round = cfg->round_size ? cfg->round_size : n;
         const uint64_t max_rounds = cfg->max_rounds ? cfg->max_rounds : 1000;
         const uint64_t world = comm_size(comm), rank = comm_rank(comm);
+        // a communicator of ONE rank still runs every collective (that is how the NCCL path
+        // is executed on a one-GPU box); without a communicator nothing is exchanged
+        const bool exchange = comm != nullptr;
         const uint64_t zero = 0;
         const uint64_t seed0 = vxb_derive_seed(cfg->seed, &zero, 1);
 
@@ -1246,14 +1249,14 @@ extern "C" int vxb_sharded_abcsmc_run(vxb_ctx* ctx, vxb_comm* comm, const vxb_mo
         Scratch theta_a(ctx, n * d * 8), theta_b(ctx, n * d * 8), rho_a(ctx, n * 8), rho_b(ctx, n * 8);
         Scratch w_a(ctx, n * 8), w_b(ctx, n * 8), cum(ctx, n * 8);
         Scratch p_theta(ctx, cap * d * 8), p_rho(ctx, cap * 8), p_flag(ctx, cap);
-        Scratch block(ctx, lay.stride), blocks(ctx, world > 1 ? world * lay.stride : 0);
+        Scratch block(ctx, lay.stride), blocks(ctx, exchange ? world * lay.stride : 0);
         Scratch state(ctx, 4 * 8), d_chol(ctx, 9 * 8), totals(ctx, nc * 8);
-        Scratch w_send(ctx, world > 1 ? w_pad * 8 : 0), w_recv(ctx, world > 1 ? world * w_pad * 8 : 0);
+        Scratch w_send(ctx, exchange ? w_pad * 8 : 0), w_recv(ctx, exchange ? world * w_pad * 8 : 0);
         VXB_CUDA(cudaMemsetAsync(block.as<void>(), 0, lay.stride, ctx->stream));
         double* th[2] = {theta_a.as<double>(), theta_b.as<double>()};
         double* rh[2] = {rho_a.as<double>(), rho_b.as<double>()};
         double* ww[2] = {w_a.as<double>(), w_b.as<double>()};
-        const void* gathered = world > 1 ? blocks.as<void>() : block.as<void>();
+        const void* gathered = exchange ? blocks.as<void>() : block.as<void>();
         auto* st = state.as<uint64_t>();
 
         double rate = 1.0;
@@ -1303,7 +1306,7 @@ extern "C" int vxb_sharded_abcsmc_run(vxb_ctx* ctx, vxb_comm* comm, const vxb_mo
                                                   g == 0 ? p_flag.as<uint8_t>() : nullptr, slice, eps, &lay,
                                                   block.as<void>(), st, n) == 0,
                             "internal", vxb_last_error());
-                    if (world > 1) comm_allgather(comm, block.as<void>(), blocks.as<void>(), lay.stride);
+                    if (exchange) comm_allgather(comm, block.as<void>(), blocks.as<void>(), lay.stride);
                     require(vxb_abcsmc_append_round(ctx, d, gathered, static_cast<uint32_t>(world), &lay,
                                                     nxt_theta, nxt_rho, n, st) == 0,
                             "internal", vxb_last_error());
@@ -1325,8 +1328,8 @@ extern "C" int vxb_sharded_abcsmc_run(vxb_ctx* ctx, vxb_comm* comm, const vxb_mo
                 check_launch("fill_kernel");
             } else {
                 const uint64_t mine = w_end - w_begin;
-                double* w_local = world > 1 ? w_send.as<double>() : nxt_w;
-                if (world > 1) VXB_CUDA(cudaMemsetAsync(w_local, 0, w_pad * 8, ctx->stream));
+                double* w_local = exchange ? w_send.as<double>() : nxt_w;
+                if (exchange) VXB_CUDA(cudaMemsetAsync(w_local, 0, w_pad * 8, ctx->stream));
                 if (mine) {
                     if (fast)
                         weights_fast_device(ctx, d, mine, nxt_theta + w_begin * d, n, cur_theta, cur_w,
@@ -1344,7 +1347,7 @@ extern "C" int vxb_sharded_abcsmc_run(vxb_ctx* ctx, vxb_comm* comm, const vxb_mo
                                                           totals.as<double>() + cb);
                     check_launch("canon_partial_kernel");
                 }
-                if (world > 1) {
+                if (exchange) {
                     comm_allgather(comm, w_send.as<void>(), w_recv.as<void>(), w_pad * 8);
                     for (uint64_t r = 0; r < world; ++r) {  // rank order = index order
                         uint64_t b2, e2;

@@ -681,6 +681,27 @@ class Context:
             _ptr(obs), C.byref(out)))
         return res
 
+    def sharded_ppp_pvalues(self, comm, model, lam, log_norm, m_total, seed, ybar_obs):
+        """SPMD config 2 (every rank calls it; comm None = one rank): counts / p-values of the whole job."""
+        lam = np.ascontiguousarray(lam, dtype=np.float64)
+        ln = np.ascontiguousarray(log_norm, dtype=np.float64)
+        counts, pv = np.zeros(lam.size, dtype=np.uint64), np.zeros(lam.size)
+        self._check(self.lib.vxb_sharded_ppp_pvalues(
+            self.handle, comm.handle if comm is not None else None, C.byref(model), _ptr(lam), _ptr(ln),
+            u32(lam.size), u64(m_total), u64(seed), f64(ybar_obs), _ptr(counts), _ptr(pv)))
+        return counts, pv
+
+    def sharded_mlmc_tauleap(self, comm, model, cfg):
+        """SPMD config 4 (every rank calls it; comm None = one rank): same dictionary as mlmc_tauleap."""
+        L = cfg.levels
+        res = dict(level_mean=np.zeros(L), level_var=np.zeros(L), level_cost=np.zeros(L))
+        out = A.vxb_mlmc_out(res["level_mean"].ctypes.data, res["level_var"].ctypes.data,
+                             res["level_cost"].ctypes.data, 0.0, 0.0)
+        self._check(self.lib.vxb_sharded_mlmc_tauleap(
+            self.handle, comm.handle if comm is not None else None, C.byref(model), C.byref(cfg), C.byref(out)))
+        res["estimate"], res["std_error"] = out.estimate, out.std_error
+        return res
+
     # ---- population statistics (canonical order) for the multi-GPU host
     def weighted_moments(self, theta, w, n=None, dim=None):
         """theta (n x dim), w (n): numpy arrays or device tensors."""

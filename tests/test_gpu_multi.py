@@ -90,6 +90,32 @@ def test_library_nccl_communicator_one_rank(ctx, oracle, golden):
         k = int(n_dev.item())
         assert k == len(idx_o) and np.array_equal(idx[:k].cpu().numpy(), idx_o.astype(np.int64))
         assert np.array_equal(r[:k].cpu().numpy(), rho[idx_o])
+    # the SPMD selection over this (real, one-rank) NCCL communicator: the all-reduces of the
+    # valid counts (int64) and of the digit histograms (uint32) and the gather of the index
+    # block run through NCCL; same epsilon bits and indices as the oracle
+    cap = 2000
+    blk = torch.zeros(16 + 8 * cap, dtype=torch.uint8, device=dev)
+    blks = torch.zeros_like(blk)
+    e, n_acc = ctx.sharded_select_epsilon(comm, rho, f, 0, 0.03, cap=cap, block_local=blk, blocks_all=blks)
+    ctx.synchronize()
+    got = blks.cpu().numpy()
+    assert e == eps and n_acc == len(idx_o) == int(got[:8].view(np.uint64)[0])
+    assert np.array_equal(got[16:16 + 8 * n_acc].view(np.uint64), idx_o.astype(np.uint64))
+    # configs 2 and 4 through the same communicator (int64 all-reduce of the counters)
+    lam = np.array(M.lambda_grid(8))
+    ln = np.array([-0.5 * math.log(2.0 * math.pi * (l * l + 0.01)) for l in lam])
+    c1, p1, _ = ctx.ppp_pvalues(M.normal_mean_model(100), lam, ln, 20001, 0, 20001, 1337, 2.9)
+    c2, p2 = ctx.sharded_ppp_pvalues(comm, M.normal_mean_model(100), lam, ln, 20001, 1337, 2.9)
+    assert np.array_equal(c1, c2) and np.array_equal(p1, p2)
+    mc = A.vxb_mlmc_cfg()
+    mc.levels, mc.refine, mc.tau0, mc.t_end, mc.paths, mc.seed = 3, 4, 1.0, 30.0, 5001, 1337
+    r1, r2 = ctx.mlmc_tauleap(M.mm_tauleap_model(), mc), ctx.sharded_mlmc_tauleap(comm, M.mm_tauleap_model(), mc)
+    assert all(np.array_equal(r1[k], r2[k]) for k in ("level_mean", "level_var")) and r1["estimate"] == r2["estimate"]
+    h = torch.arange(5000, dtype=torch.int32, device=dev)
+    with torch.cuda.stream(torch.cuda.ExternalStream(ctx.stream(), device=dev)):
+        comm.allreduce(h, h.numel(), A.VXB_DT_U32, A.VXB_OP_SUM)
+    ctx.synchronize()
+    assert torch.equal(h, torch.arange(5000, dtype=torch.int32, device=dev))
     comm.close()
 
 
