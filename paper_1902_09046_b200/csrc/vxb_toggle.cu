@@ -44,12 +44,35 @@ __device__ __forceinline__ double toggle_cell(const double* th, uint32_t steps, 
     const double alpha_u = th[3], alpha_v = th[4], beta_u = th[5], beta_v = th[6];
     double u = 10.0, v = 10.0;
     uint64_t pair = pair0;
+#ifdef VXB_TOGGLE_NO_FLOOR_SHORTCUT
+    const bool shortcut = false;
+#else
+    const bool shortcut = beta_u >= 0.0 && beta_v >= 0.0;  // beta * (+0) = +0 (uniform over the sample)
+#endif
     for (uint32_t j = 1; j < steps; ++j, ++pair) {
         double zu, zv;
         box_muller<A>(philox2x64(key, pair), zu, zv);
-        // previous-step powers (toggle_switch.cpp:50-51); the state never drops below 1
-        const double p_u = exp2_clamped<A>(A::mul(beta_u, log2_pos<A, false>(v)));
-        const double p_v = exp2_clamped<A>(A::mul(beta_v, log2_pos<A, false>(u)));
+        // previous-step powers (toggle_switch.cpp:50-51); the state never drops below 1.
+        // A species that sits ON the floor has the power 1 exactly (log2_pos(1) = +0,
+        // exp2_clamped(beta * 0) = 1 for beta >= 0), and in a settled switch one of the two
+        // species of a cell is on the floor 95 % of the time -- which one differs from cell
+        // to cell.  So every lane evaluates ONE power, of whichever species is off the floor,
+        // and the second evaluation runs only when some cell of the warp has both off it
+        // (about half of the warp-steps).  Same bits as two evaluations per step.
+        double p_u, p_v;
+        if (shortcut) {
+            const bool vf = v == 1.0, uf = u == 1.0;
+            const double p1 = exp2_clamped<A>(A::mul(vf ? beta_v : beta_u, log2_pos<A, false>(vf ? u : v)));
+            p_u = vf ? 1.0 : p1;
+            p_v = vf ? p1 : 1.0;  // v off the floor: 1 if u is on it, else the second evaluation
+            if (__any_sync(__activemask(), !vf && !uf)) {
+                const double p2 = exp2_clamped<A>(A::mul(beta_v, log2_pos<A, false>(u)));
+                if (!vf) p_v = p2;
+            }
+        } else {
+            p_u = exp2_clamped<A>(A::mul(beta_u, log2_pos<A, false>(v)));
+            p_v = exp2_clamped<A>(A::mul(beta_v, log2_pos<A, false>(u)));
+        }
         double ut = A::mul(u, 0.97);
         ut = A::add(ut, A::sub(A::div(alpha_u, A::add(1.0, p_u)), 1.0));
         double vt = A::mul(v, 0.97);
@@ -79,6 +102,8 @@ __device__ __forceinline__ double toggle_cell_fast(const double* th, uint32_t st
     FastNoise64 noise(fk, tbl, row_word, cell_word, 0u);
     const auto step = [&](double zu, double zv) {
         // (the short forms: relative error of a power ~1e-13, the model's noise is 0.5 per step)
+        // (the floor shortcut of the exact instance does not pay here: 309 against 286 ms at the
+        // paper's size -- the short power forms are cheaper than the selects and the vote)
         const double p_u = fast_exp2_short(beta_u * fast_log2_short(v, tbl), tbl);
         const double p_v = fast_exp2_short(beta_v * fast_log2_short(u, tbl), tbl);
         const double ut = fma(0.5, zu, fma(u, 0.97, fma(alpha_u, fast_rcp(1.0 + p_u), -1.0)));
