@@ -524,8 +524,8 @@ static bool early_reject_segments(vxb_ctx* ctx, const vxb_model& model, AbcParam
     if (!std::isfinite(p.ss_bound) || p.count < (1u << 16) || p.count >= (1ull << 32)) return false;
     const uint32_t n_obs = p.model.n_obs;
     // a segment may begin inside a noise batch (logistic_segment skips the normals of the
-    // previous segment), so every observation is a possible boundary
-    // boundaries: VXB_EARLY_BOUNDS="b1,b2,..." (experiments) or 15 / 20 / 30 / 40 / 60 % of
+    // previous segment), so every observation is a possible boundary.
+    // Boundaries: VXB_EARLY_BOUNDS="b1,b2,..." (experiments) or 15 / 20 / 30 / 40 / 60 % of
     // the observations (BASELINE config 1 at 1e8 rows, fp64 throughput instance: 104 ms with
     // 4,6,8,12 against 117 ms with 4,8 and 351 ms without early rejection; the exact
     // instance 315 ms with 3,4,6,8,12 against 340 ms; scripts/early_reject_sweep.sh)
@@ -546,7 +546,8 @@ static bool early_reject_segments(vxb_ctx* ctx, const vxb_model& model, AbcParam
     if (n_seg < 2) return false;
     bounds[n_seg] = n_obs;
     const size_t real = model.precision == VXB_F32 ? 4 : 8;
-    // two queues of `count` entries each: rows (u32), x, ss; two counters in front
+    // two queues of `count` entries each (x, ss, then the u32 row offsets), used alternately;
+    // in front of them one length counter per segment (64 bytes)
     const size_t per_queue = (p.count * (4 + 2 * real) + 64 + 15) & ~size_t(15);
     char* base = static_cast<char*>(arena_get(ctx, 3, 64 + 2 * per_queue));
     VXB_CUDA(cudaMemsetAsync(base, 0, 64, ctx->stream));
