@@ -229,6 +229,8 @@ def test_multi_rank_drivers_on_one_gpu_through_the_loopback_group(ctx, oracle, g
         e, idx_s, n_s = multi.select_epsilon(rho, f, q)
         e_o, i_o = oracle.select_epsilon(rho, f, q)
         assert e == e_o and n_s == len(i_o) and np.array_equal(idx_s, i_o), q
+    e0, idx0, n0 = multi.select_epsilon(rho, f, 0.02, cap=0)          # epsilon and count only
+    assert e0 == oracle.select_epsilon(rho, f, 0.02)[0] and idx0.size == 0 and n0 == len(oracle.select_epsilon(rho, f, 0.02)[1])
     r2, f2 = np.round(rs.gamma(2.0, 3.0, 30011), 1), (rs.uniform(size=30011) < 0.05).astype(np.uint8)
     r2[rs.uniform(size=30011) < 0.03] = np.nan          # NaN rows, some of them unflagged
     for arr in (r2, r2.astype(np.float32)):
