@@ -281,7 +281,9 @@ int vxb_compact_accepted(vxb_ctx* ctx, int precision, const void* rho, const uin
  * With VXB_OPT_EARLY_REJECT (vxb_set_option; off by default) a row stops as soon as its
  * partial squared distance can no longer end below epsilon^2 -- the sum of squares only
  * grows -- and the accepted set, indices, parameters and distances are bit-identical to
- * the full simulation; only the (never returned) distances of rejected rows differ. */
+ * the full simulation; only the (never returned) distances of rejected rows differ.  It
+ * pays when few rows are accepted (3.4x at 0.1 %, 1.4x at 8 %); with nothing to reject it
+ * costs 4-8 %. */
 int vxb_abc_reject(vxb_ctx* ctx, const vxb_model* model, const vxb_keying* key,
                    uint64_t n_total, uint64_t first, uint64_t count, const double* observed,
                    double epsilon, uint64_t cap, uint64_t* n_accepted, uint64_t* idx,

@@ -6,18 +6,19 @@ import numpy as np
 from paper_1902_09046_b200 import _abi as A, lib, models as M
 
 n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 20_000_000
+eps_arg = float(sys.argv[2]) if len(sys.argv) > 2 else None   # default: the 0.1 % epsilon of config 0
 ctx = lib.Context(0)
 obs = ctx.simulate_at(M.logistic_model(), [0.5, 100.0, 0.05], lib.derive_seed(1, [90]), 0, 0)
-eps = 19.47051606010851
+eps = eps_arg if eps_arg is not None else 19.47051606010851
 for name, kw in (("f64_fast", {"rng": A.VXB_RNG_FAST}), ("f32_fast", {"rng": A.VXB_RNG_FAST, "precision": A.VXB_F32}),
                  ("f64_ref", {})):
     m = M.logistic_model(**kw)
     res = []
     for early in (False, True):
         ctx.set_early_reject(early)
-        ctx.abc_reject(m, M.keying(1337), n, 0, n, obs, eps, cap=n // 100)
+        ctx.abc_reject(m, M.keying(1337), n, 0, n, obs, eps, cap=n)
         t0 = time.perf_counter()
-        out = ctx.abc_reject(m, M.keying(1337), n, 0, n, obs, eps, cap=n // 100)
+        out = ctx.abc_reject(m, M.keying(1337), n, 0, n, obs, eps, cap=n)
         res.append((time.perf_counter() - t0, out))
     (t0, a), (t1, b) = res
     same = a[0] == b[0] and all(np.array_equal(x, y) for x, y in zip(a[1:], b[1:]))
