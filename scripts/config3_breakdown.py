@@ -1,4 +1,7 @@
-import sys, time; sys.path.insert(0, "/root/repo")
+"""Config 3 (N = 1e5 x 10 generations), both generator modes: wall time against the sum of
+the kernel times, per kernel family (proposals / weights / selection / ...)."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 from paper_1902_09046_b200 import _abi as A, lib, models as M
 ctx = lib.Context(0)
